@@ -1,0 +1,400 @@
+"""CPU ORACLE for the H-SADMM synchronization step — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline /
+``--impl reference`` leg may import this module, and only as the checker or the
+timed CPU baseline. The product (``paper_2512_14628_b200``) never imports it
+and has no CPU fallback.
+
+What it is: a float64 numpy restatement of the reference algorithm for the
+sync step of ``admmprune`` 0.1.0 — phases 2-4 and the ``u``-update of phase 5
+of ``hierarchical_program`` (/root/reference/pkg/src/admmprune/consensus.py:436-535)
+plus the freeze/seal bookkeeping (:600-606) — and of the helpers it calls.
+Each function cites the reference file:line it follows. The residual block
+and penalty adaptation (:537-598) are not on the path (SURVEY.md §8(f) "next")
+and are not restated; runs that compare against the reference use
+``PenaltySchedule(adapt=False)``.
+
+Pinning: ``tests/test_oracle.py`` checks every function here against
+(a) the reference's own known-answer tests restated (tie -> lower index,
+ceil rounding, gamma = 3.2e-3, payload 36864/147456/73728, brute-force
+projection, ...) and (b) golden vectors produced by running the real
+reference (``tests/golden/make_golden.py`` imports ``admmprune`` from
+/root/reference and writes ``tests/golden/*.npz``), including multi-iteration
+end-to-end runs of ``run_hierarchical`` on 1x1, 2x1 and 2x2 topologies.
+The oracle reproduces those vectors bit-for-bit (same fp64 operation order).
+
+numpy is the only third-party arithmetic (pairwise summation inside
+``np.sum``); it is what the reference itself uses (pkg/pyproject.toml:10).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+FILTER, CHANNEL, SHAPE = "filter", "channel", "shape"
+ELEMENT_BYTES = 4                       # transport.py:32 (fp32 wire accounting)
+BUCKET_CAP_BYTES = 32 * 1024 * 1024     # transport.py:33
+
+# -- group norms / projection (tensors.py:75-93, sparsity.py:53-115) ---------
+
+_REDUCE_AXES = {FILTER: (1, 2, 3), CHANNEL: (0, 2, 3), SHAPE: (0,)}
+
+
+def group_norms(t: np.ndarray, group: str) -> np.ndarray:
+    """sqrt of the sum of squares over the non-group axes (tensors.py:75-93)."""
+    t = np.asarray(t, dtype=np.float64)
+    assert t.ndim == 4
+    return np.sqrt((t * t).sum(axis=_REDUCE_AXES[group])).ravel()
+
+
+def resolve_keep(group_count: int, keep_count=None, keep_rate=None) -> int:
+    """k = keep_count or ceil(keep_rate * G) as a Python float (sparsity.py:53-62)."""
+    k = int(keep_count) if keep_count is not None else int(math.ceil(keep_rate * group_count))
+    if k > group_count:
+        raise ValueError(f"keep {k} exceeds group count {group_count}")
+    return k
+
+
+def keep_flags(norms: np.ndarray, keep: int) -> np.ndarray:
+    """Boolean flags of the ``keep`` largest norms, lower index on ties.
+
+    Same selection as a stable argsort of ``-norms`` truncated to ``keep``
+    (sparsity.py:65-68).
+    """
+    order = np.argsort(-norms, kind="stable")
+    flags = np.zeros(norms.size, dtype=bool)
+    flags[order[:keep]] = True
+    return flags
+
+
+def group_broadcast(flags: np.ndarray, shape: tuple, group: str) -> np.ndarray:
+    """Expand per-group flags to an elementwise indicator of ``shape``."""
+    if group == FILTER:
+        return np.broadcast_to(flags.reshape(-1, 1, 1, 1), shape)
+    if group == CHANNEL:
+        return np.broadcast_to(flags.reshape(1, -1, 1, 1), shape)
+    return np.broadcast_to(flags.reshape(1, *shape[1:]), shape)
+
+
+def project(t: np.ndarray, group: str, keep: int) -> np.ndarray:
+    """Zero every group outside the top-``keep`` set; survivors untouched (sparsity.py:71-94)."""
+    t = np.asarray(t, dtype=np.float64)
+    flags = keep_flags(group_norms(t, group), keep)
+    return np.where(group_broadcast(flags, t.shape, group), t, 0.0)
+
+
+def project_composite(t: np.ndarray, plan: list[tuple[str, int]]) -> np.ndarray:
+    """Sequential projections in listed order, norms recomputed each time (sparsity.py:97-110)."""
+    out = np.array(t, dtype=np.float64, copy=True)
+    for group, keep in plan:
+        out = project(out, group, keep)
+    return out
+
+
+def extract_mask(t: np.ndarray) -> np.ndarray:
+    return np.abs(t) > 0.0          # sparsity.py:113-115
+
+
+def mask_drift(prev: np.ndarray, cur: np.ndarray) -> float:
+    return float(np.mean(prev != cur))   # sparsity.py:118-122
+
+
+# -- shrinkage (shrinkage.py:45-98) --------------------------------------------
+
+
+def derive_keep_sets(mask: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """(K_out, K_in): filters / channels with any set bit (shrinkage.py:45-58)."""
+    return (np.flatnonzero(mask.any(axis=(1, 2, 3))), np.flatnonzero(mask.any(axis=(0, 2, 3))))
+
+
+def compress(dense: np.ndarray, k_out: np.ndarray, k_in: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(dense[np.ix_(k_out, k_in)])       # shrinkage.py:61-68
+
+
+def decompress(compact: np.ndarray, k_out, k_in, full_shape) -> np.ndarray:
+    full = np.zeros(full_shape, dtype=np.float64)                  # shrinkage.py:71-82
+    if len(k_out) and len(k_in):
+        full[np.ix_(k_out, k_in)] = compact.reshape(len(k_out), len(k_in), *full_shape[2:])
+    return full
+
+
+def bucket_layout(sizes: list[tuple[str, int]], cap_bytes: int = BUCKET_CAP_BYTES):
+    """Greedy <= cap buckets, never splitting a payload (transport.py:239-280).
+
+    Returns a list of buckets, each a tuple of (name, offset, elements)."""
+    buckets, cur, cur_bytes = [], [], 0
+
+    def close():
+        nonlocal cur, cur_bytes
+        if cur:
+            off, lay = 0, []
+            for name, n in cur:
+                lay.append((name, off, n))
+                off += n
+            buckets.append(tuple(lay))
+        cur, cur_bytes = [], 0
+
+    for name, n in sizes:
+        nbytes = n * ELEMENT_BYTES
+        if nbytes > cap_bytes:           # oversize payload gets its own bucket
+            close()
+            cur, cur_bytes = [(name, n)], nbytes
+            close()
+            continue
+        if cur_bytes + nbytes > cap_bytes:
+            close()
+        cur.append((name, n))
+        cur_bytes += nbytes
+    close()
+    return buckets
+
+
+# -- update rules (consensus.py:142-186, 222-228) --------------------------------
+
+
+def candidate_gamma(rho1, rho2, weight_decay, num_nodes, accels_per_node) -> float:
+    return weight_decay / num_nodes + accels_per_node * rho1 + rho2      # consensus.py:157
+
+
+def node_candidate(s, z, v, rho1, rho2, weight_decay, num_nodes, accels_per_node):
+    gamma = candidate_gamma(rho1, rho2, weight_decay, num_nodes, accels_per_node)
+    if gamma <= 0.0:
+        raise ValueError(f"non-positive gamma {gamma}")
+    return (rho1 * s + rho2 * (z - v)) / gamma                            # consensus.py:160
+
+
+def dual_update_intra(theta, z_node, u):
+    return u + (theta - z_node)                                           # consensus.py:186
+
+
+def freeze_check(k, t_freeze, drift_history, window=3) -> bool:
+    if k >= t_freeze:                                                     # consensus.py:222-228
+        return True
+    return window > 0 and len(drift_history) >= window and all(
+        d == 0.0 for d in drift_history[-window:])
+
+
+# -- the cluster-wide sync step ------------------------------------------------
+
+
+@dataclass
+class Layer:
+    name: str
+    shape: tuple
+    plan: list = field(default_factory=list)   # [(group, keep)] in application order
+
+    @property
+    def prunable(self) -> bool:
+        return bool(self.plan)
+
+
+@dataclass
+class RankState:
+    theta: dict
+    u: dict
+    z_node: dict
+    v: dict
+    z: dict
+    masks: dict                       # global (union) masks of prunable layers
+    frozen: bool = False
+    drift_history: list = field(default_factory=list)
+    keep_cache: dict = field(default_factory=dict)   # leader: name -> (mask bytes, K_out, K_in)
+    derive_calls: int = 0
+    hits: int = 0
+    sealed: bool = False
+
+
+def make_layers(specs, constraints) -> list[Layer]:
+    """specs: [(name, shape)]; constraints: name -> [(group, keep_count|None, keep_rate|None)]."""
+    out = []
+    for name, shape in specs:
+        plan = []
+        for group, kc, kr in constraints.get(name, []):
+            g = {FILTER: shape[0], CHANNEL: shape[1]}.get(group, int(np.prod(shape[1:])))
+            plan.append((group, resolve_keep(g, kc, kr)))
+        out.append(Layer(name, tuple(shape), plan))
+    return out
+
+
+def init_rank_state(layers, theta, u, z_node, v, z) -> RankState:
+    f64 = lambda d: {k: np.asarray(a, dtype=np.float64).copy() for k, a in d.items()}
+    masks = {ly.name: np.ones(ly.shape, dtype=bool) for ly in layers if ly.prunable}
+    return RankState(f64(theta), f64(u), f64(z_node), f64(v), f64(z), masks)
+
+
+def _keep_sets(st: RankState, name: str, mask: np.ndarray):
+    """KeepSetCache.get (shrinkage.py:115-130)."""
+    if st.sealed:
+        st.hits += 1
+        return st.keep_cache[name][1:]
+    fp = mask.tobytes()
+    ent = st.keep_cache.get(name)
+    if ent is not None and ent[0] == fp:
+        st.hits += 1
+        return ent[1:]
+    ko, ki = derive_keep_sets(mask)
+    st.derive_calls += 1
+    st.keep_cache[name] = (fp, ko, ki)
+    return ko, ki
+
+
+def cluster_sync(layers, states: list[RankState], thetas: list[dict], k: int,
+                 num_nodes: int, per_node: int, rho1: dict, rho2: dict,
+                 weight_decay: float, t_freeze: int = 10, drift_window: int = 3,
+                 sync_period: int = 1, ledger: list | None = None) -> None:
+    """One outer iteration k of the sync path on every rank, in place.
+
+    ``thetas[r]`` is rank r's phase-1 output (consensus.py:429). Follows
+    consensus.py:436-535 (sums, candidate, projection, leader mask union,
+    compaction with the fresh union, bucketed leader average, decompaction,
+    inter dual, broadcast, intra dual) and the freeze/seal at :600-606.
+    Ledger entries (dicts like transport.py:138-151) are appended to ``ledger``.
+    """
+    world = num_nodes * per_node
+    names = [ly.name for ly in layers]
+    prunable = [ly for ly in layers if ly.prunable]
+
+    def log(group, scope, op, elems, nbytes, members, label, detail=None):
+        if ledger is not None and nbytes > 0:
+            e = dict(iter=k, group=group, scope=scope, op=op, elements=int(elems),
+                     bytes=int(nbytes), members=members, label=label)
+            if detail is not None:
+                e["detail"] = dict(detail)
+            ledger.append(e)
+
+    for r in range(world):
+        states[r].theta = {n: np.asarray(thetas[r][n], dtype=np.float64) for n in names}
+
+    # phase 2: intra-node SUM of theta+u, serial fold in rank order (transport.py:453-462)
+    sums = {}
+    for i in range(num_nodes):
+        members = range(i * per_node, (i + 1) * per_node)
+        acc = {}
+        for n in names:
+            parts = [states[r].theta[n] + states[r].u[n] for r in members]
+            a = parts[0].copy()
+            for p in parts[1:]:
+                a = a + p
+            acc[n] = a
+            log(f"intra{i}", "intra", "allreduce_sum", a.size, a.size * ELEMENT_BYTES,
+                per_node, f"theta_u/{n}")
+        sums[i] = acc
+
+    # phase 3: candidate + projection / frozen mask, every rank (consensus.py:442-454)
+    local_masks = {}
+    for r in range(world):
+        st, node = states[r], r // per_node
+        zn, lm = {}, {}
+        for ly in layers:
+            n = ly.name
+            cand = node_candidate(sums[node][n], st.z[n], st.v[n], rho1[n], rho2[n],
+                                  weight_decay, num_nodes, per_node)
+            if not ly.prunable:
+                zn[n] = cand.copy()
+            elif st.frozen:
+                zn[n] = cand * st.masks[n]
+            else:
+                zn[n] = project_composite(cand, ly.plan)
+                lm[n] = extract_mask(zn[n])
+        st.z_node = zn
+        local_masks[r] = lm
+
+    if k % sync_period != 0:
+        for r in range(world):
+            st = states[r]
+            st.u = {n: dual_update_intra(st.theta[n], st.z_node[n], st.u[n]) for n in names}
+        return
+
+    # phase 4 (leaders): mask union, compaction, bucketed AVG (consensus.py:463-505)
+    leaders = [i * per_node for i in range(num_nodes)]
+    frozen = states[0].frozen
+    new_masks = {}
+    if not frozen:
+        for ly in prunable:
+            acc = local_masks[leaders[0]][ly.name].copy()
+            for r in leaders[1:]:
+                acc = np.logical_or(acc, local_masks[r][ly.name])
+            new_masks[ly.name] = acc
+            log("leaders", "inter", "allreduce_bor", acc.size, acc.size * ELEMENT_BYTES,
+                num_nodes, f"mask_sync/{ly.name}")
+    payloads = {r: [] for r in leaders}
+    keeps = {}
+    for ly in layers:
+        n = ly.name
+        for r in leaders:
+            st = states[r]
+            c = st.z_node[n] + st.v[n]
+            if ly.prunable:
+                eff = new_masks.get(n, st.masks[n])
+                ko, ki = _keep_sets(st, n, eff)
+                keeps[n] = (ko, ki)
+                if len(ko) * len(ki):
+                    payloads[r].append((n, compress(c, ko, ki).ravel()))
+            else:
+                payloads[r].append((n, c.ravel()))
+    layout = bucket_layout([(n, a.size) for n, a in payloads[leaders[0]]])
+    flat = {r: (np.concatenate([a for _, a in payloads[r]]) if payloads[r] else np.empty(0))
+            for r in leaders}
+    reduced = np.empty(flat[leaders[0]].size)
+    start = 0
+    for bi, bucket in enumerate(layout):
+        size = sum(e for _, _, e in bucket)
+        acc = flat[leaders[0]][start:start + size].copy()
+        for r in leaders[1:]:
+            acc = acc + flat[r][start:start + size]
+        reduced[start:start + size] = acc / float(num_nodes)
+        log("leaders", "inter", "allreduce_avg", size, size * ELEMENT_BYTES, num_nodes,
+            f"z_sync/b{bi}", detail=[(nm, e) for nm, _, e in bucket])
+        start += size
+    offsets, off = {}, 0
+    for n, a in payloads[leaders[0]]:
+        offsets[n] = (off, a.size)
+        off += a.size
+    z_new = {}
+    for ly in layers:
+        n = ly.name
+        if ly.prunable:
+            ko, ki = keeps[n]
+            if n in offsets:
+                o, e = offsets[n]
+                z_new[n] = decompress(reduced[o:o + e], ko, ki, ly.shape)
+            else:
+                z_new[n] = np.zeros(ly.shape)
+        else:
+            o, e = offsets[n]
+            z_new[n] = reduced[o:o + e].reshape(ly.shape).copy()
+    for i, lr in enumerate(leaders):
+        st = states[lr]
+        v_new = {n: st.v[n] + (st.z_node[n] - z_new[n]) for n in names}
+        for r in range(lr, lr + per_node):      # intra broadcast of z, v, masks
+            states[r].v = {n: a.copy() for n, a in v_new.items()}
+            states[r].z = {n: a.copy() for n, a in z_new.items()}
+        for n in names:
+            log(f"intra{i}", "intra", "broadcast", z_new[n].size,
+                z_new[n].size * ELEMENT_BYTES * (per_node - 1), per_node, f"z_bcast/{n}")
+        for n in names:
+            log(f"intra{i}", "intra", "broadcast", z_new[n].size,
+                z_new[n].size * ELEMENT_BYTES * (per_node - 1), per_node, f"v_bcast/{n}")
+        if not frozen:
+            for ly in prunable:
+                log(f"intra{i}", "intra", "broadcast", new_masks[ly.name].size,
+                    new_masks[ly.name].size * ELEMENT_BYTES * (per_node - 1), per_node,
+                    f"m_bcast/{ly.name}")
+    for r in range(world):
+        st = states[r]
+        if not frozen and prunable:
+            drift = {n: mask_drift(st.masks[n], m) for n, m in new_masks.items()}
+            st.masks = {n: m.copy() for n, m in new_masks.items()}
+            st.drift_history.append(max(drift.values()))
+        # phase 5: intra dual update (consensus.py:535)
+        st.u = {n: dual_update_intra(st.theta[n], st.z_node[n], st.u[n]) for n in names}
+        # freeze + seal (consensus.py:600-606)
+        if not st.frozen and prunable and freeze_check(k, t_freeze, st.drift_history, drift_window):
+            st.frozen = True
+            if r % per_node == 0:
+                for ly in prunable:
+                    _keep_sets(st, ly.name, st.masks[ly.name])
+                st.sealed = True

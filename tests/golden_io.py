@@ -1,0 +1,94 @@
+"""Readers for the golden fixtures written by tests/golden/make_golden.py."""
+
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+KIND_NAMES = ("filter", "channel", "shape")
+
+# mirrors make_golden.E2E_LAYERS (the fixture generator needs the reference; this does not)
+E2E_LAYERS = [
+    ("stem", "conv", (8, 3, 3, 3), [("channel", 0.5)]),
+    ("bn1.w", "fc", (1, 8), []),
+    ("conv_a", "conv", (16, 8, 3, 3), [("channel", 0.5)]),
+    ("conv_b", "conv", (32, 16, 1, 1), [("channel", 0.4)]),
+    ("conv_c", "conv", (8, 32, 3, 3), [("filter", 0.75), ("channel", 0.5)]),
+    ("conv_d", "conv", (12, 8, 1, 1), [("shape", 0.5)]),
+    ("conv_e", "conv", (8, 12, 3, 3), []),
+    ("fc.w", "fc", (10, 8), []),
+    ("fc.b", "fc", (1, 10), []),
+]
+E2E_RHO1, E2E_RHO2, E2E_WD = 1.5e-3, 1.5e-4, 1e-4
+E2E_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4)]
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name))
+
+
+def projection_cases():
+    d = load("projection.npz")
+    singles = []
+    for i in range(int(d["n_single"])):
+        kind, keep = d[f"c{i}_meta"]
+        singles.append(dict(t=d[f"c{i}_in"], kind=KIND_NAMES[kind], keep=int(keep),
+                            norms=d[f"c{i}_norms"], out=d[f"c{i}_out"], mask=d[f"c{i}_mask"]))
+    comps = []
+    for i in range(int(d["n_composite"])):
+        plan = [(KIND_NAMES[k], int(kp)) for k, kp in d[f"p{i}_plan"]]
+        comps.append(dict(t=d[f"p{i}_in"], plan=plan, out=d[f"p{i}_out"]))
+    return singles, comps
+
+
+def shrinkage_cases():
+    d = load("shrinkage.npz")
+    return [dict(mask=d[f"s{i}_mask"], t=d[f"s{i}_t"], k_out=d[f"s{i}_kout"], k_in=d[f"s{i}_kin"],
+                 compact=d[f"s{i}_compact"], restored=d[f"s{i}_restored"]) for i in range(int(d["n"]))]
+
+
+def bucketize_cases():
+    with open(os.path.join(GOLDEN, "bucketize.json")) as fh:
+        return json.load(fh)
+
+
+def candidate_cases():
+    d = load("candidate.npz")
+    return [dict(svz=d[f"k{i}_svz"], par=d[f"k{i}_par"], out=d[f"k{i}_out"]) for i in range(int(d["n"]))]
+
+
+class E2E:
+    """One end-to-end reference run (run_hierarchical, phase 1 replaced)."""
+
+    def __init__(self, num_nodes, per_node):
+        self.d = load(f"e2e_{num_nodes}x{per_node}.npz")
+        self.M, self.P, self.iters, self.t_freeze = (int(x) for x in self.d["meta"])
+        self.world = self.M * self.P
+        self.names = [n for n, *_ in E2E_LAYERS]
+
+    def p0(self):
+        return {n: self.d[f"p0/{n}"] for n in self.names}
+
+    def theta(self, k, r):
+        return {n: self.d[f"theta/{k}/{r}/{n}"] for n in self.names}
+
+    def u(self, k, r):
+        return {n: self.d[f"u/{k}/{r}/{n}"] for n in self.names}
+
+    def node_state(self, grp, k, node):
+        return {n: self.d[f"{grp}/{k}/{node}/{n}"] for n in self.names}
+
+    def masks(self, k, node):
+        return {n: self.d[f"mask/{k}/{node}/{n}"] for n, _, _, c in E2E_LAYERS if c}
+
+    def frozen(self, k, node):
+        return bool(self.d[f"frozen/{k}/{node}"])
+
+    def cache(self, k, r):
+        return tuple(int(x) for x in self.d[f"cache/{k}/{r}"])
+
+    def zsync(self, k):
+        return json.loads(str(self.d[f"zsync/{k}"]))

@@ -1,0 +1,20 @@
+# libhsx: sm_100a kernels + C ABI of the H-SADMM sync step.
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+SRC := paper_2512_14628_b200/csrc/hsx_kernels.cu paper_2512_14628_b200/csrc/hsx_abi.cu
+HDR := paper_2512_14628_b200/csrc/hsx_kernels.cuh include/hsx.h
+LIB := paper_2512_14628_b200/libhsx.so
+
+all: $(LIB)
+
+$(LIB): $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(SRC)
+
+ptxas: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /tmp/hsx_kernels.o paper_2512_14628_b200/csrc/hsx_kernels.cu
+
+clean:
+	rm -f $(LIB)
+
+.PHONY: all clean ptxas

@@ -1,0 +1,197 @@
+/*
+ * libhsx — B200-native (sm_100a) kernels for the PruneX H-SADMM
+ * synchronization step. Plain C ABI: device pointers, sizes, a cudaStream_t
+ * passed as void*. No torch types. Every entry point returns 0 (HSX_OK) or an
+ * HSX_E* code; hsx_last_error() returns the thread-local message. Nothing is
+ * thrown across the ABI and no call synchronizes the device except
+ * hsx_keep_sets_fetch() (one D2H of per-layer counts per dynamic sync,
+ * SURVEY.md §7.3 H5).
+ *
+ * The reference (admmprune 0.1.0, pure numpy) has no FFI; the entry points
+ * below replace the numpy bodies its Python API calls. Each comment cites the
+ * reference function it replaces (paths relative to
+ * /root/reference/pkg/src/admmprune/). INTEGRATION.md shows the ctypes
+ * binding a maintainer adds on the reference side.
+ *
+ * Memory: the caller owns every large buffer (the fp32 state arenas theta,
+ * u, z_node, v, z, the intra-sum buffer, the flat compact buffer, mask-bit
+ * arenas). A plan owns only its layer tables, work lists and small scratch
+ * (group-norm partials, norms, keep flags, keep-set positions, counts).
+ * A plan may be used by one stream at a time.
+ *
+ * Layout: all fp32 arenas share one layout: layer l occupies elements
+ * [hsx_plan_layer_offset(l), +elements(l)), offsets are multiples of 32
+ * (128 B), gaps are zero. Mask arenas hold one bit per element of each
+ * prunable layer: bit b of 32-bit word (hsx_plan_mask_word_offset(l) + w) is
+ * element 32*w + b of layer l in row-major order.
+ */
+#ifndef HSX_H_
+#define HSX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HSX_ABI_VERSION 1
+
+/* return codes; map 1:1 onto admmprune.errors (errors.py:4-13) */
+enum {
+  HSX_OK = 0,
+  HSX_ESHAPE = 1,     /* ShapeError    */
+  HSX_EPROTOCOL = 2,  /* ProtocolError */
+  HSX_ECONFIG = 3,    /* ConfigError   */
+  HSX_ECUDA = 4,      /* CUDA runtime error */
+  HSX_EINVAL = 5      /* bad argument (null pointer, out-of-range index) */
+};
+
+/* structured groups (tensors.py:25-30 GroupBy; sparsity.py:20-30 ConstraintKind) */
+enum { HSX_GROUP_FILTER = 0, HSX_GROUP_CHANNEL = 1, HSX_GROUP_SHAPE = 2 };
+#define HSX_MAX_CONSTRAINTS 3
+
+/* per-layer summary row returned by hsx_keep_sets_fetch */
+enum {
+  HSX_SUM_KOUT = 0,     /* |K_out| */
+  HSX_SUM_KIN = 1,      /* |K_in|  */
+  HSX_SUM_ELEMS = 2,    /* payload elements of the layer in the flat buffer */
+  HSX_SUM_OFFSET = 3,   /* element offset of the layer's payload in the flat buffer */
+  HSX_SUM_DRIFT = 4,    /* popcount(union ^ prev) — mask_drift numerator (sparsity.py:118-122) */
+  HSX_SUM_POP = 5,      /* popcount(union) */
+  HSX_SUM_COLS = 6
+};
+
+typedef struct hsx_plan hsx_plan;
+
+/* One weight tensor (tensors.py:33-56 LayerSpec + its constraint list). */
+typedef struct hsx_layer_desc {
+  int32_t rank;                          /* 2 (fc / BN / bias as (1,d)) or 4 (conv) */
+  int32_t shape[4];                      /* rank-2 uses shape[0..1] */
+  int32_t n_constraints;                 /* 0 = travels dense */
+  int32_t group[HSX_MAX_CONSTRAINTS];    /* HSX_GROUP_* in application order */
+  int32_t keep[HSX_MAX_CONSTRAINTS];     /* keep counts, resolved by the caller with the
+                                            reference expression (sparsity.py:53-62) */
+  double rho1, rho2;                     /* PenaltySchedule entries (consensus.py:43-69) */
+} hsx_layer_desc;
+
+int hsx_abi_version(void);
+const char* hsx_last_error(void);
+/* number of kernels libhsx has launched in this process */
+int64_t hsx_launch_count(void);
+
+/* ---- plans ----------------------------------------------------------------- */
+int hsx_plan_create(const hsx_layer_desc* layers, int32_t n_layers, hsx_plan** out);
+void hsx_plan_destroy(hsx_plan* plan);
+int64_t hsx_plan_arena_elements(const hsx_plan* plan);
+int64_t hsx_plan_layer_offset(const hsx_plan* plan, int32_t layer);
+int64_t hsx_plan_mask_words(const hsx_plan* plan);
+int64_t hsx_plan_mask_word_offset(const hsx_plan* plan, int32_t layer);   /* -1 if dense */
+/* Offset of (layer, pass) in the concatenated norms / keep-flag vectors, -1 if none. */
+int64_t hsx_plan_group_offset(const hsx_plan* plan, int32_t layer, int32_t pass);
+int64_t hsx_plan_group_total(const hsx_plan* plan, int32_t pass);
+/* Offset of a layer's K_out (which=0) / K_in (which=1) positions, -1 if dense. */
+int64_t hsx_plan_keep_offset(const hsx_plan* plan, int32_t layer, int32_t which);
+int64_t hsx_plan_keep_total(const hsx_plan* plan, int32_t which);
+int32_t hsx_plan_max_passes(const hsx_plan* plan);
+/* gamma = weight_decay/num_nodes + accels_per_node*rho1 + rho2 per layer
+ * (consensus.py:157); HSX_ECONFIG if any gamma <= 0 (consensus.py:158-159).
+ * rho1/rho2 may be NULL to keep the plan's values. identity != 0 makes the
+ * candidate the raw input (used by the per-tensor project/group_norms API). */
+int hsx_plan_set_penalties(hsx_plan* plan, const double* rho1, const double* rho2,
+                           double weight_decay, int32_t num_nodes, int32_t accels_per_node,
+                           int32_t identity);
+
+/* ---- K0: intra-sum send buffer  send = theta + u  (consensus.py:439) -------- */
+int hsx_pack_theta_u(const hsx_plan* plan, const float* theta, const float* u, float* send,
+                     void* stream);
+
+/* ---- K1: node candidate + first-pass group-norm partials -------------------
+ * z_node <- (rho1*S + rho2*(z - v)) / gamma   in fp64, rounded once to fp32
+ * (node_candidate, consensus.py:142-160). S is `sum` or, when sum == NULL,
+ * theta + u (P == 1: the intra all-reduce is the identity).
+ * frozen_mask == NULL: dynamic — prunable layers also accumulate fp64
+ *   sum-of-squares partials of the unrounded candidate for their first
+ *   constraint (group_norms, tensors.py:75-93), deterministic two-stage order.
+ * frozen_mask != NULL: frozen — prunable layers get cand * mask
+ *   (update_node_consensus frozen branch, consensus.py:177-180). */
+int hsx_candidate(hsx_plan* plan, const float* sum, const float* theta, const float* u,
+                  const float* z, const float* v, float* z_node, const uint32_t* frozen_mask,
+                  void* stream);
+/* Composite constraints, pass >= 1: recompute the candidate, apply the keep
+ * flags of passes < pass, accumulate partials for this pass
+ * (project_composite re-norms the projected tensor, sparsity.py:97-110). */
+int hsx_candidate_renorm(hsx_plan* plan, int32_t pass, const float* sum, const float* theta,
+                         const float* u, const float* z, const float* v, void* stream);
+
+/* ---- K2: group norms -> top-k keep flags -----------------------------------
+ * norms = sqrt(sum of partials); keep the `keep` largest, lower index on ties
+ * (SparsityConstraint.resolve + _kept_group_indices, sparsity.py:53-68). */
+int hsx_select(hsx_plan* plan, int32_t pass, void* stream);
+/* copy pass `pass` norms (fp64) / keep flags (uint8) to caller device buffers
+ * of hsx_plan_group_total(pass) entries; either may be NULL. */
+int hsx_read_groups(const hsx_plan* plan, int32_t pass, double* norms, uint8_t* flags,
+                    void* stream);
+
+/* ---- K3: projection + local support mask ------------------------------------
+ * zero every element of z_node whose group is dropped by any pass; write the
+ * packed mask bit  kept && z != 0  (project, sparsity.py:71-94; extract_mask
+ * :113-115; update_node_consensus dynamic branch, consensus.py:181-182). */
+int hsx_project(hsx_plan* plan, float* z_node, uint32_t* local_mask, void* stream);
+
+/* ---- K4: leader mask union  out = OR_m gathered[m]  (transport.py:455-457) -- */
+int hsx_mask_or(const uint32_t* gathered, int32_t n_ranks, int64_t words, uint32_t* out,
+                void* stream);
+
+/* ---- K5: keep sets from the union mask -------------------------------------
+ * K_out = filters with any bit, K_in = channels with any bit, their prefix
+ * positions, per-layer payload sizes and flat-buffer offsets in layer order
+ * (derive_keep_sets shrinkage.py:45-58; bucketize concatenation
+ * transport.py:239-280), plus popcount(union ^ prev) for mask_drift when
+ * prev != NULL. */
+int hsx_keep_sets(hsx_plan* plan, const uint32_t* union_mask, const uint32_t* prev_mask,
+                  void* stream);
+/* D2H of the per-layer summary (n_layers x HSX_SUM_COLS int64, then 1 int64
+ * total payload elements) into host memory; synchronizes `stream`. */
+int hsx_keep_sets_fetch(hsx_plan* plan, int64_t* host_summary, void* stream);
+/* Install keep sets from host index lists (KeepSetCache hit path / per-tensor
+ * compress): k_out/k_in sorted ascending, lengths n_out/n_in. Recomputes the
+ * flat-buffer offsets of every layer. */
+int hsx_set_keep_sets(hsx_plan* plan, int32_t layer, const int32_t* k_out, int32_t n_out,
+                      const int32_t* k_in, int32_t n_in);
+/* Copy positions (int32, -1 = dropped) of all layers: which=0 K_out, 1 K_in. */
+int hsx_read_keep_positions(const hsx_plan* plan, int32_t which, int32_t* dst, void* stream);
+
+/* ---- K6: leader compaction fused with the intra dual update -----------------
+ * flat[payload] <- z_node + v gathered onto K_out x K_in (prunable) or raveled
+ * (dense)  (consensus.py:476-483; compress shrinkage.py:61-68), and, when
+ * theta/u != NULL, u <- u + (theta - z_node) (dual_update_intra,
+ * consensus.py:185-186, 535). v == NULL compresses z_node alone. */
+int hsx_compact_dual(const hsx_plan* plan, const float* theta, float* u, const float* z_node,
+                     const float* v, float* flat, void* stream);
+/* K6f: follower / non-sync intra dual update u <- u + (theta - z_node). */
+int hsx_dual_intra(const hsx_plan* plan, const float* theta, float* u, const float* z_node,
+                   void* stream);
+
+/* ---- K7: decompaction fused with the inter dual update ----------------------
+ * z <- zero-filled scatter of flat/divisor onto K_out x K_in (prunable) or
+ * reshape (dense) (decompress shrinkage.py:71-82; consensus.py:491-504; the
+ * leader average's "/ g", transport.py:461-462), and, when v != NULL,
+ * v <- v + (z_node - z) (consensus.py:505). */
+int hsx_decompact_dual(const hsx_plan* plan, const float* flat, float divisor,
+                       const float* z_node, float* v, float* z, void* stream);
+
+/* ---- mask helpers for the per-tensor API -------------------------------------- */
+/* out[i] = |t[i]| > 0  (extract_mask, sparsity.py:113-115) */
+int hsx_nonzero_u8(const float* t, int64_t n, uint8_t* out, void* stream);
+/* pack / unpack bool bytes <-> bits (n elements, bits zero-padded to a word) */
+int hsx_pack_bits(const uint8_t* m, int64_t n, uint32_t* bits, void* stream);
+int hsx_unpack_bits(const uint32_t* bits, int64_t n, uint8_t* m, void* stream);
+/* *count_dev (uint64, device) += number of i with a[i] != b[i]  (mask_drift numerator) */
+int hsx_count_diff_u8(const uint8_t* a, const uint8_t* b, int64_t n, uint64_t* count_dev,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSX_H_ */

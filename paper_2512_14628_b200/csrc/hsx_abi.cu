@@ -1,0 +1,630 @@
+// Host side of libhsx: plan construction (layer table, work lists, scratch)
+// and the extern "C" entry points declared in include/hsx.h.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/hsx.h"
+#include "hsx_kernels.cuh"
+
+using hsx::DevLayer;
+using hsx::Item;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int check_cuda(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HSX_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return HSX_OK;
+}
+
+#define HSX_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) return fail(HSX_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr long long kAlign = 32;        // arena layer alignment in elements (128 B)
+constexpr int kSubElems = 4096;         // target elements per shared-memory sub-tile
+constexpr long long kItemElems = 8192;  // elements per streaming work item
+constexpr long long kWordItem = 4096;   // mask words per keep-mark item
+constexpr int kMaxSelectGroups = 8192;  // bitonic capacity (96 KB smem)
+constexpr size_t kMaxSmem = 200 * 1024;
+
+template <typename T>
+int upload(T** dst, const std::vector<T>& src) {
+  *dst = nullptr;
+  if (src.empty()) return HSX_OK;
+  HSX_CUDA(cudaMalloc(reinterpret_cast<void**>(dst), src.size() * sizeof(T)));
+  HSX_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return HSX_OK;
+}
+
+template <typename T>
+int alloc0(T** dst, long long n) {
+  *dst = nullptr;
+  if (n <= 0) return HSX_OK;
+  HSX_CUDA(cudaMalloc(reinterpret_cast<void**>(dst), (size_t)n * sizeof(T)));
+  HSX_CUDA(cudaMemset(*dst, 0, (size_t)n * sizeof(T)));
+  return HSX_OK;
+}
+
+}  // namespace
+
+struct hsx_plan {
+  int n_layers = 0;
+  int max_passes = 0;
+  int identity = 0;
+  long long arena = 0;
+  long long mask_words = 0;
+  long long gtotal[hsx::kMaxPasses] = {0, 0, 0};
+  long long ptotal[hsx::kMaxPasses] = {0, 0, 0};
+  long long ktotal[2] = {0, 0};
+  std::vector<DevLayer> layers;
+  std::vector<Item> cand_items, elem_items, proj_items, word_items;
+  std::vector<int> pass_list[hsx::kMaxPasses];
+  std::vector<int> prunable;
+  size_t cand_smem = 0, select_smem[hsx::kMaxPasses] = {0, 0, 0}, mark_smem = 0;
+  int sqcap = 0;
+  // device
+  DevLayer* d_layers = nullptr;
+  Item *d_cand = nullptr, *d_elem = nullptr, *d_proj = nullptr, *d_word = nullptr;
+  int* d_pass[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
+  int* d_prunable = nullptr;
+  double* d_partials[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
+  double* d_norms[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
+  uint8_t* d_flags[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
+  uint8_t *d_oflag = nullptr, *d_iflag = nullptr;
+  int *d_pos_out = nullptr, *d_pos_in = nullptr;
+  long long* d_summary = nullptr;
+  unsigned int* d_done = nullptr;
+  std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
+
+  ~hsx_plan() {
+    void* ptrs[] = {d_layers, d_cand, d_elem, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+                    d_pos_out, d_pos_in, d_summary, d_done};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    for (int i = 0; i < hsx::kMaxPasses; ++i) {
+      if (d_pass[i]) cudaFree(d_pass[i]);
+      if (d_partials[i]) cudaFree(d_partials[i]);
+      if (d_norms[i]) cudaFree(d_norms[i]);
+      if (d_flags[i]) cudaFree(d_flags[i]);
+    }
+  }
+};
+
+namespace {
+
+// lay out flat-buffer offsets from the host summary mirror (layer order)
+void host_layout(hsx_plan* p) {
+  long long off = 0;
+  for (int l = 0; l < p->n_layers; ++l) {
+    long long* row = &p->summary[(size_t)l * HSX_SUM_COLS];
+    row[HSX_SUM_OFFSET] = off;
+    off += row[HSX_SUM_ELEMS];
+  }
+  p->summary[(size_t)p->n_layers * HSX_SUM_COLS] = off;
+}
+
+int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
+  p->n_layers = n;
+  long long off = 0, mword = 0, okeep = 0, ikeep = 0;
+  long long goff[hsx::kMaxPasses] = {0, 0, 0}, poff[hsx::kMaxPasses] = {0, 0, 0};
+  int sqcap = 0, gmax = 0;
+  size_t mark_smem = 0;
+  p->summary.assign((size_t)n * HSX_SUM_COLS + 1, 0);
+  for (int l = 0; l < n; ++l) {
+    const hsx_layer_desc& d = in[l];
+    DevLayer ly;
+    std::memset(&ly, 0, sizeof(ly));
+    if (d.rank != 2 && d.rank != 4) return fail(HSX_ESHAPE, "layer %d: rank must be 2 or 4, got %d", l, d.rank);
+    for (int i = 0; i < d.rank; ++i)
+      if (d.shape[i] <= 0) return fail(HSX_ESHAPE, "layer %d: non-positive dimension", l);
+    ly.rank = d.rank;
+    ly.rows = d.shape[0];
+    ly.cin = d.shape[1];
+    ly.k = d.rank == 4 ? d.shape[2] * d.shape[3] : 1;
+    ly.L = ly.cin * ly.k;
+    ly.n = (long long)ly.rows * ly.L;
+    if (ly.n >= (1LL << 31)) return fail(HSX_ESHAPE, "layer %d: more than 2^31 elements", l);
+    ly.off = off;
+    off += (ly.n + kAlign - 1) / kAlign * kAlign;
+    ly.divL = hsx::make_fastdiv((unsigned)ly.L);
+    ly.divk = hsx::make_fastdiv((unsigned)ly.k);
+    ly.rho1 = d.rho1;
+    ly.rho2 = d.rho2;
+    ly.gamma = 1.0;
+    ly.mword = -1;
+    ly.okeep = ly.ikeep = -1;
+    for (int q = 0; q < hsx::kMaxPasses; ++q) ly.goff[q] = ly.poff[q] = -1;
+    if (d.n_constraints < 0 || d.n_constraints > HSX_MAX_CONSTRAINTS)
+      return fail(HSX_ESHAPE, "layer %d: %d constraints (max %d)", l, d.n_constraints, HSX_MAX_CONSTRAINTS);
+    ly.ncons = d.n_constraints;
+    long long* srow = &p->summary[(size_t)l * HSX_SUM_COLS];
+    if (ly.ncons > 0) {
+      if (d.rank != 4) return fail(HSX_ESHAPE, "layer %d: only conv layers are prunable", l);
+      if (ly.L > 16384) return fail(HSX_ESHAPE, "layer %d: row of %d elements exceeds 16384", l, ly.L);
+      for (int q = 0; q < ly.ncons; ++q) {
+        int g = d.group[q];
+        if (g < 0 || g > 2) return fail(HSX_ESHAPE, "layer %d: bad group kind %d", l, g);
+        for (int r = 0; r < q; ++r)
+          if (d.group[r] == g) return fail(HSX_ESHAPE, "layer %d: duplicate constraint kinds", l);
+        int G = g == HSX_GROUP_FILTER ? ly.rows : (g == HSX_GROUP_CHANNEL ? ly.cin : ly.L);
+        if (d.keep[q] < 1) return fail(HSX_ESHAPE, "layer %d: keep_count must be positive", l);
+        if (d.keep[q] > G) return fail(HSX_ESHAPE, "layer %d: keep_count %d exceeds group count %d", l, d.keep[q], G);
+        if (G > kMaxSelectGroups) return fail(HSX_ESHAPE, "layer %d: %d groups exceed %d", l, G, kMaxSelectGroups);
+        ly.group[q] = g;
+        ly.keep[q] = d.keep[q];
+        ly.G[q] = G;
+        if (g != HSX_GROUP_FILTER) gmax = std::max(gmax, G);
+      }
+      ly.rsub = std::max(1, kSubElems / ly.L);
+      sqcap = std::max(sqcap, ly.rsub * ly.L);
+      // rows per candidate item: >= 8K elements and partials <= ~1/16 of the item's bytes
+      int gch = 0;
+      for (int q = 0; q < ly.ncons; ++q)
+        if (ly.group[q] != HSX_GROUP_FILTER) gch = std::max(gch, ly.G[q]);
+      long long rows_item = std::max<long long>((kItemElems + ly.L - 1) / ly.L, (16LL * gch + ly.L - 1) / ly.L);
+      rows_item = (rows_item + ly.rsub - 1) / ly.rsub * ly.rsub;
+      rows_item = std::min<long long>(rows_item, ly.rows);
+      ly.nparts = (int)((ly.rows + rows_item - 1) / rows_item);
+      for (int pt = 0; pt < ly.nparts; ++pt) {
+        Item it;
+        it.layer = l;
+        it.part = pt;
+        it.begin = pt * rows_item * ly.L;
+        it.end = std::min<long long>((pt + 1) * rows_item, ly.rows) * ly.L;
+        p->cand_items.push_back(it);
+      }
+      for (int q = 0; q < ly.ncons; ++q) {
+        ly.goff[q] = goff[q];
+        goff[q] += ly.G[q];
+        ly.poff[q] = poff[q];
+        poff[q] += ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * ly.G[q];
+        p->pass_list[q].push_back(l);
+        p->max_passes = std::max(p->max_passes, q + 1);
+      }
+      ly.mword = mword;
+      mword += (ly.n + 31) / 32;
+      ly.okeep = okeep;
+      okeep += ly.rows;
+      ly.ikeep = ikeep;
+      ikeep += ly.cin;
+      p->prunable.push_back(l);
+      for (long long b = 0; b < ly.n; b += kItemElems) {
+        Item it{l, 0, b, std::min(ly.n, b + kItemElems)};
+        p->proj_items.push_back(it);
+      }
+      for (long long b = 0; b < ly.n; b += kWordItem * 32) {
+        Item it{l, 0, b, std::min(ly.n, b + kWordItem * 32)};
+        p->word_items.push_back(it);
+        long long r_lo = b / ly.L, r_hi = (it.end - 1) / ly.L;
+        mark_smem = std::max<size_t>(mark_smem, (size_t)ly.cin + (size_t)(r_hi - r_lo + 1));
+      }
+    } else {
+      for (long long b = 0; b < ly.n; b += kItemElems) {
+        Item it{l, 0, b, std::min(ly.n, b + kItemElems)};
+        p->cand_items.push_back(it);
+      }
+    }
+    for (long long b = 0; b < ly.n; b += kItemElems) {
+      Item it{l, 0, b, std::min(ly.n, b + kItemElems)};
+      p->elem_items.push_back(it);
+    }
+    // initial keep sets: everything kept (all-ones initial masks, consensus.py:418)
+    srow[HSX_SUM_KOUT] = ly.rows;
+    srow[HSX_SUM_KIN] = ly.cin;
+    srow[HSX_SUM_ELEMS] = ly.n;
+    p->layers.push_back(ly);
+  }
+  // the last layer needs no trailing pad: arenas may be exactly-sized tensors
+  if (n > 0) off = p->layers.back().off + p->layers.back().n;
+  p->arena = off;
+  p->mask_words = mword;
+  p->ktotal[0] = okeep;
+  p->ktotal[1] = ikeep;
+  for (int q = 0; q < hsx::kMaxPasses; ++q) {
+    p->gtotal[q] = goff[q];
+    p->ptotal[q] = poff[q];
+    int gp = 1;
+    for (int l : p->pass_list[q]) {
+      int G = p->layers[l].G[q];
+      while (gp < G) gp <<= 1;
+    }
+    p->select_smem[q] = (size_t)gp * (sizeof(double) + sizeof(int));
+  }
+  p->sqcap = sqcap;
+  p->cand_smem = (size_t)(sqcap + gmax) * sizeof(double);
+  p->mark_smem = mark_smem;
+  if (p->cand_smem > kMaxSmem) return fail(HSX_ESHAPE, "candidate tile needs %zu B of shared memory", p->cand_smem);
+  host_layout(p);
+  return HSX_OK;
+}
+
+int upload_plan(hsx_plan* p) {
+  int rc;
+  if ((rc = upload(&p->d_layers, p->layers))) return rc;
+  if ((rc = upload(&p->d_cand, p->cand_items))) return rc;
+  if ((rc = upload(&p->d_elem, p->elem_items))) return rc;
+  if ((rc = upload(&p->d_proj, p->proj_items))) return rc;
+  if ((rc = upload(&p->d_word, p->word_items))) return rc;
+  if ((rc = upload(&p->d_prunable, p->prunable))) return rc;
+  for (int q = 0; q < hsx::kMaxPasses; ++q) {
+    if ((rc = upload(&p->d_pass[q], p->pass_list[q]))) return rc;
+    if ((rc = alloc0(&p->d_partials[q], p->ptotal[q]))) return rc;
+    if ((rc = alloc0(&p->d_norms[q], p->gtotal[q]))) return rc;
+    if ((rc = alloc0(&p->d_flags[q], p->gtotal[q]))) return rc;
+  }
+  if ((rc = alloc0(&p->d_oflag, p->ktotal[0]))) return rc;
+  if ((rc = alloc0(&p->d_iflag, p->ktotal[1]))) return rc;
+  // identity positions (all kept) until the first keep-set derivation
+  std::vector<int> po(p->ktotal[0]), pi(p->ktotal[1]);
+  for (int l : p->prunable) {
+    const DevLayer& ly = p->layers[l];
+    for (int i = 0; i < ly.rows; ++i) po[ly.okeep + i] = i;
+    for (int i = 0; i < ly.cin; ++i) pi[ly.ikeep + i] = i;
+  }
+  if ((rc = upload(&p->d_pos_out, po))) return rc;
+  if ((rc = upload(&p->d_pos_in, pi))) return rc;
+  if ((rc = upload(&p->d_summary, p->summary))) return rc;
+  if ((rc = alloc0(&p->d_done, 1))) return rc;
+  return HSX_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// extern "C" entry points
+// ===========================================================================
+
+#define HSX_TRY(body)                                                      \
+  try {                                                                    \
+    body                                                                   \
+  } catch (const std::bad_alloc&) {                                        \
+    return fail(HSX_EINVAL, "host allocation failed");                     \
+  } catch (...) {                                                          \
+    return fail(HSX_EINVAL, "unexpected C++ exception");                   \
+  }
+
+#define HSX_LAUNCHED(what)        \
+  do {                            \
+    g_launches.fetch_add(1);      \
+    int rc_ = check_cuda(what);   \
+    if (rc_) return rc_;          \
+  } while (0)
+
+extern "C" {
+
+int hsx_abi_version(void) { return HSX_ABI_VERSION; }
+const char* hsx_last_error(void) { return g_err.c_str(); }
+int64_t hsx_launch_count(void) { return g_launches.load(); }
+
+int hsx_plan_create(const hsx_layer_desc* layers, int32_t n_layers, hsx_plan** out) {
+  if (!out || (!layers && n_layers > 0) || n_layers < 0) return fail(HSX_EINVAL, "null argument");
+  *out = nullptr;
+  HSX_TRY({
+    hsx_plan* p = new hsx_plan();
+    int rc = build(p, layers, n_layers);
+    if (!rc) rc = upload_plan(p);
+    if (rc) {
+      delete p;
+      return rc;
+    }
+    *out = p;
+    return HSX_OK;
+  })
+}
+
+void hsx_plan_destroy(hsx_plan* plan) { delete plan; }
+
+int64_t hsx_plan_arena_elements(const hsx_plan* p) { return p ? p->arena : -1; }
+int64_t hsx_plan_layer_offset(const hsx_plan* p, int32_t l) {
+  return (p && l >= 0 && l < p->n_layers) ? p->layers[l].off : -1;
+}
+int64_t hsx_plan_mask_words(const hsx_plan* p) { return p ? p->mask_words : -1; }
+int64_t hsx_plan_mask_word_offset(const hsx_plan* p, int32_t l) {
+  return (p && l >= 0 && l < p->n_layers) ? p->layers[l].mword : -1;
+}
+int64_t hsx_plan_group_offset(const hsx_plan* p, int32_t l, int32_t pass) {
+  if (!p || l < 0 || l >= p->n_layers || pass < 0 || pass >= hsx::kMaxPasses) return -1;
+  return p->layers[l].goff[pass];
+}
+int64_t hsx_plan_group_total(const hsx_plan* p, int32_t pass) {
+  return (p && pass >= 0 && pass < hsx::kMaxPasses) ? p->gtotal[pass] : -1;
+}
+int64_t hsx_plan_keep_offset(const hsx_plan* p, int32_t l, int32_t which) {
+  if (!p || l < 0 || l >= p->n_layers) return -1;
+  return which == 0 ? p->layers[l].okeep : p->layers[l].ikeep;
+}
+int64_t hsx_plan_keep_total(const hsx_plan* p, int32_t which) {
+  return p ? p->ktotal[which ? 1 : 0] : -1;
+}
+int32_t hsx_plan_max_passes(const hsx_plan* p) { return p ? p->max_passes : -1; }
+
+int hsx_plan_set_penalties(hsx_plan* p, const double* rho1, const double* rho2, double wd,
+                           int32_t num_nodes, int32_t per_node, int32_t identity) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  if (num_nodes < 1 || per_node < 1) return fail(HSX_ECONFIG, "topology dimensions must be positive");
+  for (int l = 0; l < p->n_layers; ++l) {
+    DevLayer& ly = p->layers[l];
+    if (rho1) ly.rho1 = rho1[l];
+    if (rho2) ly.rho2 = rho2[l];
+    // consensus.py:157-159, same fp64 expression order
+    double gamma = wd / (double)num_nodes + (double)per_node * ly.rho1 + ly.rho2;
+    if (!identity && !(gamma > 0.0))
+      return fail(HSX_ECONFIG, "non-positive candidate normalizer gamma=%g (layer %d)", gamma, l);
+    ly.gamma = gamma;
+  }
+  p->identity = identity ? 1 : 0;
+  if (p->n_layers)
+    HSX_CUDA(cudaMemcpy(p->d_layers, p->layers.data(), p->layers.size() * sizeof(DevLayer),
+                        cudaMemcpyHostToDevice));
+  return HSX_OK;
+}
+
+int hsx_pack_theta_u(const hsx_plan* p, const float* theta, const float* u, float* send,
+                     void* stream) {
+  if (!p || !theta || !u || !send) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_add(theta, u, send, p->arena, S(stream));
+  HSX_LAUNCHED("pack_theta_u");
+  return HSX_OK;
+}
+
+static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta, const float* u,
+                               const float* z, const float* v) {
+  hsx::CandArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.s = sum;
+  a.theta = theta;
+  a.u = u;
+  a.z = z;
+  a.v = v;
+  a.layers = p->d_layers;
+  a.items = p->d_cand;
+  a.identity = p->identity;
+  a.sqcap = p->sqcap;
+  return a;
+}
+
+static int check_cand_inputs(const hsx_plan* p, const float* sum, const float* theta,
+                             const float* u, const float* z, const float* v) {
+  if (!sum && (!theta || !u)) return fail(HSX_EINVAL, "candidate needs sum or theta and u");
+  if (!p->identity && (!z || !v)) return fail(HSX_EINVAL, "candidate needs z and v");
+  return HSX_OK;
+}
+
+int hsx_candidate(hsx_plan* p, const float* sum, const float* theta, const float* u,
+                  const float* z, const float* v, float* z_node, const uint32_t* frozen_mask,
+                  void* stream) {
+  if (!p || !z_node) return fail(HSX_EINVAL, "null argument");
+  if (int rc = check_cand_inputs(p, sum, theta, u, z, v)) return rc;
+  hsx::CandArgs a = cand_args(p, sum, theta, u, z, v);
+  a.zn = z_node;
+  a.fmask = frozen_mask;
+  a.pass = 0;
+  a.partials = p->d_partials[0];
+  hsx::launch_candidate(a, (int)p->cand_items.size(), frozen_mask != nullptr, p->cand_smem, S(stream));
+  HSX_LAUNCHED("candidate");
+  return HSX_OK;
+}
+
+int hsx_candidate_renorm(hsx_plan* p, int32_t pass, const float* sum, const float* theta,
+                         const float* u, const float* z, const float* v, void* stream) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  if (pass < 1 || pass >= p->max_passes) return fail(HSX_EINVAL, "renorm pass %d out of range", pass);
+  if (int rc = check_cand_inputs(p, sum, theta, u, z, v)) return rc;
+  hsx::CandArgs a = cand_args(p, sum, theta, u, z, v);
+  a.pass = pass;
+  a.partials = p->d_partials[pass];
+  for (int q = 0; q < pass; ++q) a.flags[q] = p->d_flags[q];
+  hsx::launch_candidate(a, (int)p->cand_items.size(), 0, p->cand_smem, S(stream));
+  HSX_LAUNCHED("candidate_renorm");
+  return HSX_OK;
+}
+
+int hsx_select(hsx_plan* p, int32_t pass, void* stream) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  if (pass < 0 || pass >= hsx::kMaxPasses) return fail(HSX_EINVAL, "pass %d out of range", pass);
+  int n = (int)p->pass_list[pass].size();
+  if (n == 0) return HSX_OK;
+  hsx::launch_select(p->d_layers, p->d_pass[pass], n, pass, p->d_partials[pass], p->d_norms[pass],
+                     p->d_flags[pass], p->select_smem[pass], S(stream));
+  HSX_LAUNCHED("select");
+  return HSX_OK;
+}
+
+int hsx_read_groups(const hsx_plan* p, int32_t pass, double* norms, uint8_t* flags, void* stream) {
+  if (!p || pass < 0 || pass >= hsx::kMaxPasses) return fail(HSX_EINVAL, "bad argument");
+  long long n = p->gtotal[pass];
+  if (n == 0) return HSX_OK;
+  if (norms)
+    HSX_CUDA(cudaMemcpyAsync(norms, p->d_norms[pass], n * sizeof(double), cudaMemcpyDeviceToDevice, S(stream)));
+  if (flags)
+    HSX_CUDA(cudaMemcpyAsync(flags, p->d_flags[pass], n, cudaMemcpyDeviceToDevice, S(stream)));
+  return HSX_OK;
+}
+
+int hsx_project(hsx_plan* p, float* z_node, uint32_t* local_mask, void* stream) {
+  if (!p || !z_node || (!local_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_project(p->d_layers, p->d_proj, (int)p->proj_items.size(), z_node, local_mask,
+                      p->d_flags[0], p->d_flags[1], p->d_flags[2], S(stream));
+  HSX_LAUNCHED("project");
+  return HSX_OK;
+}
+
+int hsx_mask_or(const uint32_t* gathered, int32_t n_ranks, int64_t words, uint32_t* out,
+                void* stream) {
+  if (!gathered || !out || n_ranks < 1 || words < 0) return fail(HSX_EINVAL, "bad argument");
+  hsx::launch_mask_or(gathered, n_ranks, words, out, S(stream));
+  HSX_LAUNCHED("mask_or");
+  return HSX_OK;
+}
+
+int hsx_keep_sets(hsx_plan* p, const uint32_t* union_mask, const uint32_t* prev_mask,
+                  void* stream) {
+  if (!p || (!union_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
+  if (p->prunable.empty()) return HSX_OK;
+  cudaStream_t st = S(stream);
+  if (p->ktotal[0]) HSX_CUDA(cudaMemsetAsync(p->d_oflag, 0, p->ktotal[0], st));
+  if (p->ktotal[1]) HSX_CUDA(cudaMemsetAsync(p->d_iflag, 0, p->ktotal[1], st));
+  // zero the drift / popcount columns of every row
+  HSX_CUDA(cudaMemset2DAsync(p->d_summary + HSX_SUM_DRIFT, HSX_SUM_COLS * sizeof(long long), 0,
+                             2 * sizeof(long long), p->n_layers, st));
+  hsx::launch_keep_mark(p->d_layers, p->d_word, (int)p->word_items.size(), union_mask, prev_mask,
+                        p->d_oflag, p->d_iflag, p->d_summary, p->mark_smem, st);
+  HSX_LAUNCHED("keep_mark");
+  hsx::launch_keep_scan(p->d_layers, p->d_prunable, (int)p->prunable.size(), p->n_layers,
+                        p->d_oflag, p->d_iflag, p->d_pos_out, p->d_pos_in, p->d_summary,
+                        p->d_done, st);
+  HSX_LAUNCHED("keep_scan");
+  return HSX_OK;
+}
+
+int hsx_keep_sets_fetch(hsx_plan* p, int64_t* host_summary, void* stream) {
+  if (!p || !host_summary) return fail(HSX_EINVAL, "null argument");
+  size_t bytes = p->summary.size() * sizeof(long long);
+  HSX_CUDA(cudaMemcpyAsync(host_summary, p->d_summary, bytes, cudaMemcpyDeviceToHost, S(stream)));
+  HSX_CUDA(cudaStreamSynchronize(S(stream)));
+  std::memcpy(p->summary.data(), host_summary, bytes);
+  return HSX_OK;
+}
+
+int hsx_set_keep_sets(hsx_plan* p, int32_t l, const int32_t* k_out, int32_t n_out,
+                      const int32_t* k_in, int32_t n_in) {
+  if (!p || l < 0 || l >= p->n_layers) return fail(HSX_EINVAL, "bad layer");
+  const DevLayer& ly = p->layers[l];
+  if (ly.ncons == 0) return fail(HSX_ESHAPE, "layer %d: only conv layers are shrunk", l);
+  if (n_out < 0 || n_in < 0 || n_out > ly.rows || n_in > ly.cin || (n_out && !k_out) || (n_in && !k_in))
+    return fail(HSX_ESHAPE, "layer %d: keep sets inconsistent with shape", l);
+  std::vector<int> po(ly.rows, -1), pi(ly.cin, -1);
+  for (int i = 0; i < n_out; ++i) {
+    if (k_out[i] < 0 || k_out[i] >= ly.rows || (i && k_out[i] <= k_out[i - 1]))
+      return fail(HSX_ESHAPE, "layer %d: K_out must be sorted, unique and in range", l);
+    po[k_out[i]] = i;
+  }
+  for (int i = 0; i < n_in; ++i) {
+    if (k_in[i] < 0 || k_in[i] >= ly.cin || (i && k_in[i] <= k_in[i - 1]))
+      return fail(HSX_ESHAPE, "layer %d: K_in must be sorted, unique and in range", l);
+    pi[k_in[i]] = i;
+  }
+  HSX_CUDA(cudaMemcpy(p->d_pos_out + ly.okeep, po.data(), po.size() * sizeof(int), cudaMemcpyHostToDevice));
+  HSX_CUDA(cudaMemcpy(p->d_pos_in + ly.ikeep, pi.data(), pi.size() * sizeof(int), cudaMemcpyHostToDevice));
+  long long* row = &p->summary[(size_t)l * HSX_SUM_COLS];
+  row[HSX_SUM_KOUT] = n_out;
+  row[HSX_SUM_KIN] = n_in;
+  row[HSX_SUM_ELEMS] = (long long)n_out * n_in * ly.k;
+  host_layout(p);
+  HSX_CUDA(cudaMemcpy(p->d_summary, p->summary.data(), p->summary.size() * sizeof(long long),
+                      cudaMemcpyHostToDevice));
+  return HSX_OK;
+}
+
+int hsx_read_keep_positions(const hsx_plan* p, int32_t which, int32_t* dst, void* stream) {
+  if (!p || !dst) return fail(HSX_EINVAL, "null argument");
+  long long n = p->ktotal[which ? 1 : 0];
+  if (n)
+    HSX_CUDA(cudaMemcpyAsync(dst, which ? p->d_pos_in : p->d_pos_out, n * sizeof(int),
+                             cudaMemcpyDeviceToDevice, S(stream)));
+  return HSX_OK;
+}
+
+static hsx::ElemArgs elem_args(const hsx_plan* p) {
+  hsx::ElemArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.layers = p->d_layers;
+  a.items = p->d_elem;
+  a.pos_out = p->d_pos_out;
+  a.pos_in = p->d_pos_in;
+  a.summary = p->d_summary;
+  a.divisor = 1.0f;
+  return a;
+}
+
+int hsx_compact_dual(const hsx_plan* p, const float* theta, float* u, const float* z_node,
+                     const float* v, float* flat, void* stream) {
+  if (!p || !z_node || !flat) return fail(HSX_EINVAL, "null argument");
+  if ((theta == nullptr) != (u == nullptr)) return fail(HSX_EINVAL, "theta and u go together");
+  hsx::ElemArgs a = elem_args(p);
+  a.theta = theta;
+  a.u = u;
+  a.zn = z_node;
+  a.vin = v;
+  a.flat_out = flat;
+  hsx::launch_compact(a, (int)p->elem_items.size(), S(stream));
+  HSX_LAUNCHED("compact_dual");
+  return HSX_OK;
+}
+
+int hsx_dual_intra(const hsx_plan* p, const float* theta, float* u, const float* z_node,
+                   void* stream) {
+  if (!p || !theta || !u || !z_node) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_dual(theta, u, z_node, p->arena, S(stream));
+  HSX_LAUNCHED("dual_intra");
+  return HSX_OK;
+}
+
+int hsx_decompact_dual(const hsx_plan* p, const float* flat, float divisor, const float* z_node,
+                       float* v, float* z, void* stream) {
+  if (!p || !flat || !z) return fail(HSX_EINVAL, "null argument");
+  if (v && !z_node) return fail(HSX_EINVAL, "v update needs z_node");
+  if (!(divisor > 0.0f)) return fail(HSX_EINVAL, "divisor must be positive");
+  hsx::ElemArgs a = elem_args(p);
+  a.flat_in = flat;
+  a.divisor = divisor;
+  a.zn = z_node;
+  a.v = v;
+  a.z = z;
+  hsx::launch_decompact(a, (int)p->elem_items.size(), S(stream));
+  HSX_LAUNCHED("decompact_dual");
+  return HSX_OK;
+}
+
+int hsx_nonzero_u8(const float* t, int64_t n, uint8_t* out, void* stream) {
+  if ((!t || !out) && n > 0) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_nonzero(t, n, out, S(stream));
+  HSX_LAUNCHED("nonzero_u8");
+  return HSX_OK;
+}
+int hsx_pack_bits(const uint8_t* m, int64_t n, uint32_t* bits, void* stream) {
+  if ((!m || !bits) && n > 0) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_pack(m, n, bits, S(stream));
+  HSX_LAUNCHED("pack_bits");
+  return HSX_OK;
+}
+int hsx_unpack_bits(const uint32_t* bits, int64_t n, uint8_t* m, void* stream) {
+  if ((!m || !bits) && n > 0) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_unpack(bits, n, m, S(stream));
+  HSX_LAUNCHED("unpack_bits");
+  return HSX_OK;
+}
+int hsx_count_diff_u8(const uint8_t* a, const uint8_t* b, int64_t n, uint64_t* count_dev,
+                      void* stream) {
+  if ((!a || !b || !count_dev) && n > 0) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_count_diff(a, b, n, reinterpret_cast<unsigned long long*>(count_dev), S(stream));
+  HSX_LAUNCHED("count_diff_u8");
+  return HSX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,845 @@
+// sm_100a kernels of the H-SADMM synchronization step (see hsx_kernels.cuh).
+#include <algorithm>
+
+#include "hsx_kernels.cuh"
+
+namespace hsx {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+// opt a kernel into > 48 KB of dynamic shared memory (idempotent, cheap)
+template <typename K>
+static void allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+__device__ __forceinline__ float4 ldg4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+// streaming load of data read exactly once
+__device__ __forceinline__ float4 ldcs4(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float f4get(const float4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ void f4set(float4& v, int i, float x) {
+  if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
+}
+
+// ---------------------------------------------------------------------------
+// K1 candidate (+ group-norm partials).  consensus.py:142-160, tensors.py:75-93
+// ---------------------------------------------------------------------------
+
+// fp64 candidate of one element; identical operation order to the reference:
+// (rho1 * s + rho2 * (z - v)) / gamma with s = sum or theta + u.
+__device__ __forceinline__ double cand_of(double s, double z, double v, const DevLayer& ly,
+                                          int identity) {
+  return identity ? s : (ly.rho1 * s + ly.rho2 * (z - v)) / ly.gamma;
+}
+
+struct In4 {
+  float4 a, b, z, v;
+};
+
+__device__ __forceinline__ In4 load_in4(const CandArgs& p, long long gi, int identity) {
+  In4 r;
+  r.a = ldcs4(p.s ? p.s + gi : p.theta + gi);
+  r.b = p.s ? make_float4(0.f, 0.f, 0.f, 0.f) : ldcs4(p.u + gi);
+  if (identity) {
+    r.z = r.v = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    r.z = ldcs4(p.z + gi);
+    r.v = ldcs4(p.v + gi);
+  }
+  return r;
+}
+
+__device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, const DevLayer& ly) {
+  double s = p.s ? (double)p.s[gi] : (double)p.theta[gi] + (double)p.u[gi];
+  if (p.identity) return s;
+  return cand_of(s, (double)p.z[gi], (double)p.v[gi], ly, 0);
+}
+
+__device__ __forceinline__ double cand4(const In4& x, int i, const DevLayer& ly, int has_s,
+                                        int identity) {
+  double s = has_s ? (double)f4get(x.a, i) : (double)f4get(x.a, i) + (double)f4get(x.b, i);
+  return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), ly, identity);
+}
+
+// group index of layer-local element e for a constraint kind
+__device__ __forceinline__ int group_of(const DevLayer& ly, int grp, unsigned o, unsigned col,
+                                        unsigned c) {
+  return grp == kFilter ? (int)o : (grp == kChannel ? (int)c : (int)col);
+}
+
+// keep test of layer-local element e against passes [0, npass)
+__device__ __forceinline__ bool kept_by(const DevLayer& ly, const uint8_t* const* flags, int npass,
+                                        long long e) {
+  unsigned o = fdiv((unsigned)e, ly.divL);
+  unsigned col = (unsigned)e - o * (unsigned)ly.L;
+  unsigned c = fdiv(col, ly.divk);
+  bool keep = true;
+  for (int q = 0; q < npass; ++q) keep = keep && flags[q][ly.goff[q] + group_of(ly, ly.group[q], o, col, c)];
+  return keep;
+}
+
+// elementwise candidate over [begin, end) of one layer (dense layers, frozen mode)
+__device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long long begin,
+                                 long long end, int frozen) {
+  const bool masked = frozen && ly.ncons > 0 && p.fmask != nullptr;
+  if (begin & 3) {  // row tiles of layers with c_in*kh*kw % 4 != 0: scalar path
+    for (long long e = begin + threadIdx.x; e < end; e += kThreads) {
+      double c = cand_elem(p, ly.off + e, ly);
+      if (masked && !((p.fmask[ly.mword + (e >> 5)] >> (e & 31)) & 1u)) c = c * 0.0;
+      p.zn[ly.off + e] = (float)c;
+    }
+    return;
+  }
+  const long long nq = (end - begin + 3) >> 2;
+  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * kUnroll) {
+    In4 in[kUnroll];
+#pragma unroll
+    for (int uu = 0; uu < kUnroll; ++uu) {
+      long long q = q0 + (long long)uu * kThreads;
+      long long e = begin + 4 * q;
+      if (q < nq && e + 3 < ly.n) in[uu] = load_in4(p, ly.off + e, p.identity);
+    }
+#pragma unroll
+    for (int uu = 0; uu < kUnroll; ++uu) {
+      long long q = q0 + (long long)uu * kThreads;
+      if (q >= nq) continue;
+      long long e = begin + 4 * q;
+      uint32_t bits = masked ? p.fmask[ly.mword + (e >> 5)] : 0u;
+      if (e + 3 < ly.n) {
+        float4 out;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double c = cand4(in[uu], i, ly, p.s != nullptr, p.identity);
+          if (masked) c = ((bits >> ((e + i) & 31)) & 1u) ? c : c * 0.0;
+          f4set(out, i, (float)c);
+        }
+        st4(p.zn + ly.off + e, out);
+      } else {
+        for (int i = 0; i < 4 && e + i < ly.n; ++i) {
+          double c = cand_elem(p, ly.off + e + i, ly);
+          if (masked) c = ((bits >> ((e + i) & 31)) & 1u) ? c : c * 0.0;
+          p.zn[ly.off + e + i] = (float)c;
+        }
+      }
+    }
+  }
+}
+
+// row tile with fp64 group-norm partials: shared memory holds the squares of
+// the unrounded candidate for rsub rows, then each group is reduced by one
+// owner thread (CHANNEL / SHAPE) or one warp (FILTER) in a fixed order.
+__device__ void cand_tile(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq,
+                          double* acc) {
+  const int pass = p.pass;
+  const int grp = ly.group[pass];
+  const int G = ly.G[pass];
+  const int L = ly.L;
+  const int k = ly.k;
+  const long long r0 = it.begin / L;
+  const int nrows = (int)((it.end - it.begin) / L);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (grp != kFilter)
+    for (int g = threadIdx.x; g < G; g += kThreads) acc[g] = 0.0;
+
+  for (int rs = 0; rs < nrows; rs += ly.rsub) {
+    const int nr = min(ly.rsub, nrows - rs);
+    const int E = nr * L;
+    const long long ebase = (r0 + rs) * (long long)L;  // layer-local element of sq[0]
+    const long long gbase = ly.off + ebase;
+    if ((L & 3) == 0) {
+      const int nq = E >> 2;
+      for (int q0 = threadIdx.x; q0 < nq; q0 += kThreads * kUnroll) {
+        In4 in[kUnroll];
+#pragma unroll
+        for (int uu = 0; uu < kUnroll; ++uu) {
+          int q = q0 + uu * kThreads;
+          if (q < nq) in[uu] = load_in4(p, gbase + 4 * q, p.identity);
+        }
+#pragma unroll
+        for (int uu = 0; uu < kUnroll; ++uu) {
+          int q = q0 + uu * kThreads;
+          if (q >= nq) continue;
+          float4 out;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            double c = cand4(in[uu], i, ly, p.s != nullptr, p.identity);
+            if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + 4 * q + i)) c = 0.0;
+            f4set(out, i, (float)c);
+            sq[4 * q + i] = c * c;
+          }
+          if (pass == 0) st4(p.zn + gbase + 4 * q, out);
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < E; i += kThreads) {
+        double c = cand_elem(p, gbase + i, ly);
+        if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
+        if (pass == 0) p.zn[gbase + i] = (float)c;
+        sq[i] = c * c;
+      }
+    }
+    __syncthreads();
+    if (grp == kChannel) {
+      for (int c = threadIdx.x; c < ly.cin; c += kThreads) {
+        double s = 0.0;
+        for (int r = 0; r < nr; ++r) {
+          const double* row = sq + r * L + c * k;
+          for (int j = 0; j < k; ++j) s += row[j];
+        }
+        acc[c] += s;
+      }
+    } else if (grp == kShape) {
+      for (int col = threadIdx.x; col < L; col += kThreads) {
+        double s = 0.0;
+        for (int r = 0; r < nr; ++r) s += sq[r * L + col];
+        acc[col] += s;
+      }
+    } else {
+      for (int r = warp; r < nr; r += kThreads / 32) {
+        double s = 0.0;
+        for (int i = lane; i < L; i += 32) s += sq[r * L + i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+        if (lane == 0) p.partials[ly.poff[pass] + r0 + rs + r] = s;
+      }
+    }
+    __syncthreads();
+  }
+  if (grp != kFilter)
+    for (int g = threadIdx.x; g < G; g += kThreads)
+      p.partials[ly.poff[pass] + (long long)it.part * G + g] = acc[g];
+}
+
+__global__ void __launch_bounds__(kThreads) k_candidate(CandArgs p, int frozen) {
+  extern __shared__ double smem[];
+  const Item it = p.items[blockIdx.x];
+  const DevLayer& ly = p.layers[it.layer];
+  if (frozen || ly.ncons == 0) {
+    if (p.pass == 0) cand_elementwise(p, ly, it.begin, it.end, frozen);
+    return;
+  }
+  if (ly.ncons <= p.pass) return;
+  cand_tile(p, ly, it, smem, smem + p.sqcap);
+}
+
+void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
+  if (n_items <= 0) return;
+  allow_smem(k_candidate, smem);
+  k_candidate<<<n_items, kThreads, smem, st>>>(a, frozen);
+}
+
+// ---------------------------------------------------------------------------
+// K2 select: norms = sqrt(sum partials); top-k with lower-index tie-break.
+// sparsity.py:53-68.  One CTA per layer, bitonic sort of (norm desc, index asc).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+__global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ layers,
+                                                 const int* __restrict__ list, int pass,
+                                                 const double* __restrict__ partials,
+                                                 double* __restrict__ norms,
+                                                 uint8_t* __restrict__ flags) {
+  extern __shared__ double skey[];
+  const DevLayer& ly = layers[list[blockIdx.x]];
+  const int G = ly.G[pass];
+  int Gp = 1;
+  while (Gp < G) Gp <<= 1;
+  int* sidx = reinterpret_cast<int*>(skey + Gp);
+  const bool rowwise = ly.group[pass] == kFilter;
+  for (int g = threadIdx.x; g < Gp; g += blockDim.x) {
+    double key = -1.0;  // padding sorts after every norm (norms >= 0)
+    if (g < G) {
+      double s2;
+      if (rowwise) {
+        s2 = partials[ly.poff[pass] + g];
+      } else {
+        s2 = 0.0;
+        for (int pt = 0; pt < ly.nparts; ++pt) s2 += partials[ly.poff[pass] + (long long)pt * G + g];
+      }
+      key = sqrt(s2);
+      norms[ly.goff[pass] + g] = key;
+    }
+    skey[g] = key;
+    sidx[g] = g;
+  }
+  __syncthreads();
+  for (int size = 2; size <= Gp; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < Gp; i += blockDim.x) {
+        int j = i ^ stride;
+        if (j > i) {
+          double ki = skey[i], kj = skey[j];
+          int ii = sidx[i], ij = sidx[j];
+          bool i_first = before(ki, ii, kj, ij);
+          bool want_i_first = (i & size) == 0;
+          if (i_first != want_i_first) {
+            skey[i] = kj; skey[j] = ki;
+            sidx[i] = ij; sidx[j] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int keep = ly.keep[pass];
+  for (int pos = threadIdx.x; pos < Gp; pos += blockDim.x) {
+    int g = sidx[pos];
+    if (g < G) flags[ly.goff[pass] + g] = pos < keep ? 1 : 0;
+  }
+}
+
+void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
+                   double* norms, uint8_t* flags, size_t smem, cudaStream_t st) {
+  if (n <= 0) return;
+  allow_smem(k_select, smem);
+  k_select<<<n, 1024, smem, st>>>(layers, list, pass, partials, norms, flags);
+}
+
+// ---------------------------------------------------------------------------
+// K3 project + local mask.  sparsity.py:71-94, 113-115; consensus.py:181-182
+// One warp per 32-element mask word, ballot builds the word.
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads) k_project(const DevLayer* __restrict__ layers,
+                                                      const Item* __restrict__ items,
+                                                      float* __restrict__ zn,
+                                                      uint32_t* __restrict__ mask,
+                                                      const uint8_t* f0, const uint8_t* f1,
+                                                      const uint8_t* f2) {
+  const Item it = items[blockIdx.x];
+  const DevLayer& ly = layers[it.layer];
+  const uint8_t* flags[kMaxPasses] = {f0, f1, f2};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long w0 = it.begin >> 5, w1 = (it.end + 31) >> 5;
+  constexpr int kW = 4;
+  for (long long wb = w0 + warp; wb < w1; wb += (kThreads / 32) * kW) {
+    float val[kW];
+#pragma unroll
+    for (int uu = 0; uu < kW; ++uu) {
+      long long w = wb + (long long)uu * (kThreads / 32);
+      long long e = (w << 5) + lane;
+      val[uu] = (w < w1 && e < ly.n) ? __ldcs(zn + ly.off + e) : 0.f;
+    }
+#pragma unroll
+    for (int uu = 0; uu < kW; ++uu) {
+      long long w = wb + (long long)uu * (kThreads / 32);
+      if (w >= w1) break;
+      long long e = (w << 5) + lane;
+      bool valid = e < ly.n;
+      bool keep = valid && kept_by(ly, flags, ly.ncons, e);
+      if (valid && !keep) zn[ly.off + e] = 0.0f;
+      unsigned bits = __ballot_sync(kFull, keep && val[uu] != 0.0f);
+      if (lane == 0) mask[ly.mword + w] = bits;
+    }
+  }
+}
+
+void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
+                    uint32_t* mask, const uint8_t* f0, const uint8_t* f1, const uint8_t* f2,
+                    cudaStream_t st) {
+  if (n_items <= 0) return;
+  k_project<<<n_items, kThreads, 0, st>>>(layers, items, zn, mask, f0, f1, f2);
+}
+
+// ---------------------------------------------------------------------------
+// K4 mask union over leaders (transport.py:455-457): NCCL has no OR, so the
+// leaders all-gather packed bits and OR them here.
+// ---------------------------------------------------------------------------
+
+__global__ void k_mask_or(const uint32_t* __restrict__ g, int m, long long words,
+                          uint32_t* __restrict__ out, int vec) {
+  const long long n4 = vec ? (words >> 2) : 0;
+  const uint4* g4 = reinterpret_cast<const uint4*>(g);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (int r = 0; r < m; ++r) {
+      uint4 x = g4[r * n4 + i];
+      acc.x |= x.x; acc.y |= x.y; acc.z |= x.z; acc.w |= x.w;
+    }
+    reinterpret_cast<uint4*>(out)[i] = acc;
+  }
+  for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < words;
+       i += (long long)gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+    for (int r = 0; r < m; ++r) acc |= g[r * words + i];
+    out[i] = acc;
+  }
+}
+
+void launch_mask_or(const uint32_t* g, int m, long long words, uint32_t* out, cudaStream_t st) {
+  if (words <= 0) return;
+  // gathered slices are 16-B aligned relative to each other only if words % 4 == 0
+  const int vec = (words & 3) == 0;
+  long long n = vec ? (words >> 2) : words;
+  int grid = (int)std::min<long long>(std::max<long long>((n + 255) / 256, 1), 148LL * 16);
+  k_mask_or<<<grid, 256, 0, st>>>(g, m, words, out, vec);
+}
+
+// ---------------------------------------------------------------------------
+// K5a keep marks: K_out / K_in "any" flags from the union mask, popcounts.
+// shrinkage.py:45-58 (derive_keep_sets), sparsity.py:118-122 (drift numerator)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads) k_keep_mark(const DevLayer* __restrict__ layers,
+                                                        const Item* __restrict__ items,
+                                                        const uint32_t* __restrict__ uni,
+                                                        const uint32_t* __restrict__ prev,
+                                                        uint8_t* __restrict__ oflag,
+                                                        uint8_t* __restrict__ iflag,
+                                                        long long* __restrict__ summary) {
+  extern __shared__ uint8_t sflag[];
+  const Item it = items[blockIdx.x];
+  const DevLayer& ly = layers[it.layer];
+  const long long w0 = it.begin >> 5, w1 = (it.end + 31) >> 5;
+  const long long r_lo = it.begin / ly.L;
+  const long long r_hi = (min(it.end, ly.n) - 1) / ly.L;  // inclusive
+  const int nr = (int)(r_hi - r_lo + 1);
+  uint8_t* s_in = sflag;
+  uint8_t* s_out = sflag + ly.cin;
+  for (int i = threadIdx.x; i < ly.cin + nr; i += kThreads) sflag[i] = 0;
+  __syncthreads();
+  unsigned long long pop = 0, drift = 0;
+  for (long long w = w0 + threadIdx.x; w < w1; w += kThreads) {
+    long long e0 = w << 5;
+    long long nvalid = ly.n - e0;
+    uint32_t valid = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
+    uint32_t x = uni[ly.mword + w] & valid;
+    pop += __popc(x);
+    if (prev) drift += __popc((x ^ prev[ly.mword + w]) & valid);
+    while (x) {
+      int b = __ffs(x) - 1;
+      unsigned e = (unsigned)(e0 + b);
+      unsigned o = fdiv(e, ly.divL);
+      unsigned col = e - o * (unsigned)ly.L;
+      unsigned c = fdiv(col, ly.divk);
+      unsigned j = col - c * (unsigned)ly.k;
+      s_out[o - r_lo] = 1;
+      s_in[c] = 1;
+      int skip = b + (int)((unsigned)ly.k - j);  // rest of this (o, c) kernel run
+      x = skip >= 32 ? 0u : (x & ~((1u << skip) - 1u));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    pop += __shfl_xor_sync(kFull, pop, off);
+    drift += __shfl_xor_sync(kFull, drift, off);
+  }
+  const int lane = threadIdx.x & 31;
+  const long long srow = (long long)it.layer * kSumCols;
+  if (lane == 0) {
+    if (pop) atomicAdd(reinterpret_cast<unsigned long long*>(summary + srow + 5), pop);
+    if (drift) atomicAdd(reinterpret_cast<unsigned long long*>(summary + srow + 4), drift);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ly.cin; i += kThreads)
+    if (s_in[i]) iflag[ly.ikeep + i] = 1;
+  for (int i = threadIdx.x; i < nr; i += kThreads)
+    if (s_out[i]) oflag[ly.okeep + r_lo + i] = 1;
+}
+
+void launch_keep_mark(const DevLayer* layers, const Item* items, int n_items, const uint32_t* uni,
+                      const uint32_t* prev, uint8_t* oflag, uint8_t* iflag, long long* summary,
+                      size_t smem, cudaStream_t st) {
+  if (n_items <= 0) return;
+  allow_smem(k_keep_mark, smem);
+  k_keep_mark<<<n_items, kThreads, smem, st>>>(layers, items, uni, prev, oflag, iflag, summary);
+}
+
+// ---------------------------------------------------------------------------
+// K5b keep scan: positions of kept filters / channels (exclusive prefix sums),
+// payload sizes; the last CTA lays out the flat buffer in layer order
+// (bucketize's concatenation, transport.py:239-280).
+// ---------------------------------------------------------------------------
+
+__device__ int block_exclusive_scan(int x, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int y = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int nw = blockDim.x >> 5;
+    int t = lane < nw ? warp_tot[lane] : 0;
+    int ti = t;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int y = __shfl_up_sync(kFull, ti, off);
+      if (lane >= off) ti += y;
+    }
+    if (lane < nw) warp_tot[lane] = ti - t;
+    if (lane == 31) *total = ti;
+  }
+  __syncthreads();
+  int r = incl - x + warp_tot[warp];
+  __syncthreads();
+  return r;
+}
+
+__device__ int scan_flags(const uint8_t* flags, int n, int* pos) {
+  __shared__ int warp_tot[32];
+  __shared__ int total;
+  int carry = 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    int i = base + threadIdx.x;
+    int f = (i < n && flags[i]) ? 1 : 0;
+    int ex = block_exclusive_scan(f, warp_tot, &total);
+    if (i < n) pos[i] = f ? carry + ex : -1;
+    carry += total;
+    __syncthreads();
+  }
+  return carry;
+}
+
+__global__ void __launch_bounds__(1024) k_keep_scan(const DevLayer* __restrict__ layers,
+                                                    const int* __restrict__ list, int n_layers,
+                                                    const uint8_t* __restrict__ oflag,
+                                                    const uint8_t* __restrict__ iflag,
+                                                    int* __restrict__ pos_out,
+                                                    int* __restrict__ pos_in,
+                                                    long long* summary, unsigned int* done) {
+  const int l = list[blockIdx.x];
+  const DevLayer& ly = layers[l];
+  int n_out = scan_flags(oflag + ly.okeep, ly.rows, pos_out + ly.okeep);
+  int n_in = scan_flags(iflag + ly.ikeep, ly.cin, pos_in + ly.ikeep);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    long long* row = summary + (long long)l * kSumCols;
+    row[0] = n_out;
+    row[1] = n_in;
+    row[2] = (long long)n_out * n_in * ly.k;
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    long long off = 0;
+    for (int i = 0; i < n_layers; ++i) {
+      volatile long long* row = summary + (long long)i * kSumCols;
+      long long e = row[2];
+      row[3] = off;
+      off += e;
+    }
+    summary[(long long)n_layers * kSumCols] = off;
+    *done = 0;
+  }
+}
+
+void launch_keep_scan(const DevLayer* layers, const int* list, int n, int n_layers,
+                      const uint8_t* oflag, const uint8_t* iflag, int* pos_out, int* pos_in,
+                      long long* summary, unsigned int* done, cudaStream_t st) {
+  if (n <= 0) return;
+  k_keep_scan<<<n, 1024, 0, st>>>(layers, list, n_layers, oflag, iflag, pos_out, pos_in, summary,
+                                  done);
+}
+
+// ---------------------------------------------------------------------------
+// K6 compact + intra dual; K7 decompact + inter dual.
+// consensus.py:476-505, 535; shrinkage.py:61-82
+// ---------------------------------------------------------------------------
+
+// walks (o, col, c, j) of consecutive layer-local elements without divisions
+struct Walk {
+  unsigned o, col, c, j;
+  __device__ __forceinline__ void init(const DevLayer& ly, unsigned e) {
+    o = fdiv(e, ly.divL);
+    col = e - o * (unsigned)ly.L;
+    c = fdiv(col, ly.divk);
+    j = col - c * (unsigned)ly.k;
+  }
+  __device__ __forceinline__ void next(const DevLayer& ly) {
+    ++col;
+    if (++j == (unsigned)ly.k) { j = 0; ++c; }
+    if (col == (unsigned)ly.L) { col = 0; c = 0; j = 0; ++o; }
+  }
+};
+
+__global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
+  const Item it = a.items[blockIdx.x];
+  const DevLayer& ly = a.layers[it.layer];
+  const long long* srow = a.summary + (long long)it.layer * kSumCols;
+  const long long kin = srow[1];
+  const long long coff = srow[3];
+  const bool pr = ly.ncons > 0;
+  const long long nq = (it.end - it.begin + 3) >> 2;
+  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * kUnroll) {
+    float4 th[kUnroll], uu4[kUnroll], zn[kUnroll], vv[kUnroll];
+#pragma unroll
+    for (int uu = 0; uu < kUnroll; ++uu) {
+      long long q = q0 + (long long)uu * kThreads;
+      long long e = it.begin + 4 * q;
+      if (q < nq && e + 3 < ly.n) {
+        long long gi = ly.off + e;
+        zn[uu] = ldcs4(a.zn + gi);
+        vv[uu] = a.vin ? ldcs4(a.vin + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a.u) {
+          th[uu] = ldcs4(a.theta + gi);
+          uu4[uu] = ldcs4(a.u + gi);
+        }
+      } else if (q < nq) {
+        for (int i = 0; i < 4; ++i) {
+          bool ok = e + i < ly.n;
+          long long gi = ly.off + e + i;
+          f4set(zn[uu], i, ok ? a.zn[gi] : 0.f);
+          f4set(vv[uu], i, ok && a.vin ? a.vin[gi] : 0.f);
+          if (a.u) {
+            f4set(th[uu], i, ok ? a.theta[gi] : 0.f);
+            f4set(uu4[uu], i, ok ? a.u[gi] : 0.f);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int uu = 0; uu < kUnroll; ++uu) {
+      long long q = q0 + (long long)uu * kThreads;
+      if (q >= nq) continue;
+      long long e = it.begin + 4 * q;
+      const bool full = e + 3 < ly.n;
+      if (a.u) {
+        float4 un;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          f4set(un, i, (float)((double)f4get(uu4[uu], i) +
+                               ((double)f4get(th[uu], i) - (double)f4get(zn[uu], i))));
+        if (full) {
+          st4(a.u + ly.off + e, un);
+        } else {
+          for (int i = 0; i < 4 && e + i < ly.n; ++i) a.u[ly.off + e + i] = f4get(un, i);
+        }
+      }
+      if (!pr) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (e + i < ly.n) a.flat_out[coff + e + i] = f4get(zn[uu], i) + f4get(vv[uu], i);
+      } else {
+        Walk wk;
+        wk.init(ly, (unsigned)e);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (e + i < ly.n) {
+            int po = a.pos_out[ly.okeep + wk.o];
+            int pi = a.pos_in[ly.ikeep + wk.c];
+            if (po >= 0 && pi >= 0)
+              a.flat_out[coff + ((long long)po * kin + pi) * ly.k + wk.j] =
+                  f4get(zn[uu], i) + f4get(vv[uu], i);
+          }
+          wk.next(ly);
+        }
+      }
+    }
+  }
+}
+
+void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
+  if (n_items <= 0) return;
+  k_compact<<<n_items, kThreads, 0, st>>>(a);
+}
+
+__global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
+  const Item it = a.items[blockIdx.x];
+  const DevLayer& ly = a.layers[it.layer];
+  const long long* srow = a.summary + (long long)it.layer * kSumCols;
+  const long long kin = srow[1];
+  const long long coff = srow[3];
+  const bool pr = ly.ncons > 0;
+  const float div = a.divisor;
+  const long long nq = (it.end - it.begin + 3) >> 2;
+  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * kUnroll) {
+    float4 zn[kUnroll], vv[kUnroll], zz[kUnroll];
+#pragma unroll
+    for (int uu = 0; uu < kUnroll; ++uu) {
+      long long q = q0 + (long long)uu * kThreads;
+      long long e = it.begin + 4 * q;
+      if (q >= nq) continue;
+      // gather of the reduced payload (zero fill for dropped coordinates)
+      if (!pr) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          f4set(zz[uu], i, e + i < ly.n ? a.flat_in[coff + e + i] : 0.f);
+      } else {
+        Walk wk;
+        wk.init(ly, (unsigned)e);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float x = 0.f;
+          if (e + i < ly.n) {
+            int po = a.pos_out[ly.okeep + wk.o];
+            int pi = a.pos_in[ly.ikeep + wk.c];
+            if (po >= 0 && pi >= 0) x = a.flat_in[coff + ((long long)po * kin + pi) * ly.k + wk.j];
+          }
+          f4set(zz[uu], i, x);
+          wk.next(ly);
+        }
+      }
+      if (a.v) {
+        long long gi = ly.off + e;
+        if (e + 3 < ly.n) {
+          zn[uu] = ldcs4(a.zn + gi);
+          vv[uu] = ldcs4(a.v + gi);
+        } else {
+          for (int i = 0; i < 4; ++i) {
+            f4set(zn[uu], i, e + i < ly.n ? a.zn[gi + i] : 0.f);
+            f4set(vv[uu], i, e + i < ly.n ? a.v[gi + i] : 0.f);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int uu = 0; uu < kUnroll; ++uu) {
+      long long q = q0 + (long long)uu * kThreads;
+      if (q >= nq) continue;
+      long long e = it.begin + 4 * q;
+      float4 zo;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float x = f4get(zz[uu], i);
+        f4set(zo, i, div == 1.0f ? x : x / div);
+      }
+      float4 vn;
+      if (a.v) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          f4set(vn, i, (float)((double)f4get(vv[uu], i) +
+                               ((double)f4get(zn[uu], i) - (double)f4get(zo, i))));
+      }
+      if (e + 3 < ly.n) {
+        st4(a.z + ly.off + e, zo);
+        if (a.v) st4(a.v + ly.off + e, vn);
+      } else {
+        for (int i = 0; i < 4 && e + i < ly.n; ++i) {
+          a.z[ly.off + e + i] = f4get(zo, i);
+          if (a.v) a.v[ly.off + e + i] = f4get(vn, i);
+        }
+      }
+    }
+  }
+}
+
+void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
+  if (n_items <= 0) return;
+  k_decompact<<<n_items, kThreads, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+// K0 send = theta + u; K6f u += theta - z_node (arena-wide streaming)
+// ---------------------------------------------------------------------------
+
+static int stream_grid(long long n4) {
+  long long g = (n4 + kThreads - 1) / kThreads;
+  return (int)std::min<long long>(std::max<long long>(g, 1), 148LL * 8);
+}
+
+__global__ void __launch_bounds__(kThreads) k_add(const float* __restrict__ a,
+                                                  const float* __restrict__ b,
+                                                  float* __restrict__ out, long long n) {
+  const long long n4 = n >> 2;
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n4; i += stride) {
+    float4 x = ldcs4(a + 4 * i), y = ldcs4(b + 4 * i);
+    st4(out + 4 * i, make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w));
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += stride)
+    out[i] = a[i] + b[i];
+}
+
+void launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_add<<<stream_grid(n >> 2), kThreads, 0, st>>>(a, b, out, n);
+}
+
+__device__ __forceinline__ float dual1(float u, float th, float zn) {
+  return (float)((double)u + ((double)th - (double)zn));
+}
+
+__global__ void __launch_bounds__(kThreads) k_dual(const float* __restrict__ th,
+                                                   float* __restrict__ u,
+                                                   const float* __restrict__ zn, long long n) {
+  const long long n4 = n >> 2;
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n4; i += stride) {
+    float4 t = ldcs4(th + 4 * i), x = ldcs4(u + 4 * i), z = ldcs4(zn + 4 * i);
+    st4(u + 4 * i, make_float4(dual1(x.x, t.x, z.x), dual1(x.y, t.y, z.y), dual1(x.z, t.z, z.z),
+                               dual1(x.w, t.w, z.w)));
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += stride)
+    u[i] = dual1(u[i], th[i], zn[i]);
+}
+
+void launch_dual(const float* theta, float* u, const float* zn, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_dual<<<stream_grid(n >> 2), kThreads, 0, st>>>(theta, u, zn, n);
+}
+
+// ---------------------------------------------------------------------------
+// small mask helpers for the per-tensor API
+// ---------------------------------------------------------------------------
+
+__global__ void k_nonzero(const float* __restrict__ t, long long n, uint8_t* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = fabsf(t[i]) > 0.0f ? 1 : 0;
+}
+
+__global__ void k_pack(const uint8_t* __restrict__ m, long long n, uint32_t* __restrict__ bits) {
+  const long long words = (n + 31) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long w = warp0; w < words; w += nwarps) {
+    long long e = (w << 5) + lane;
+    unsigned b = __ballot_sync(kFull, e < n && m[e] != 0);
+    if (lane == 0) bits[w] = b;
+  }
+}
+
+__global__ void k_unpack(const uint32_t* __restrict__ bits, long long n, uint8_t* __restrict__ m) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    m[i] = (bits[i >> 5] >> (i & 31)) & 1u;
+}
+
+__global__ void k_count_diff(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b,
+                             long long n, unsigned long long* c) {
+  unsigned long long cnt = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    cnt += (a[i] != 0) != (b[i] != 0);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(c, cnt);
+}
+
+static int small_grid(long long n) { return (int)std::min<long long>(std::max<long long>((n + 255) / 256, 1), 148LL * 8); }
+
+void launch_nonzero(const float* t, long long n, uint8_t* out, cudaStream_t st) {
+  if (n > 0) k_nonzero<<<small_grid(n), 256, 0, st>>>(t, n, out);
+}
+void launch_pack(const uint8_t* m, long long n, uint32_t* bits, cudaStream_t st) {
+  if (n > 0) k_pack<<<small_grid(n), 256, 0, st>>>(m, n, bits);
+}
+void launch_unpack(const uint32_t* bits, long long n, uint8_t* m, cudaStream_t st) {
+  if (n > 0) k_unpack<<<small_grid(n), 256, 0, st>>>(bits, n, m);
+}
+void launch_count_diff(const uint8_t* a, const uint8_t* b, long long n, unsigned long long* c,
+                       cudaStream_t st) {
+  if (n > 0) k_count_diff<<<small_grid(n), 256, 0, st>>>(a, b, n, c);
+}
+
+}  // namespace hsx

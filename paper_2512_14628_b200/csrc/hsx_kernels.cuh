@@ -1,0 +1,124 @@
+// Device side of libhsx: the sm_100a kernels of the H-SADMM sync step.
+// All kernels are HBM-bound streaming / gather-scatter work (no tensor cores:
+// arithmetic intensity <= 0.3 flop/B). Conventions:
+//  * fp32 state, fp64 arithmetic for every compound expression so each output
+//    is the fp32 rounding of the reference's fp64 value on the same inputs;
+//  * 128-bit loads/stores on the contiguous streams, scalar (warp-coalesced)
+//    stores for the compact payload whose offsets are not 16-B aligned;
+//  * deterministic reductions: fixed per-thread ownership and fixed shuffle
+//    trees, no floating-point atomics (leaders must agree bit-for-bit).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hsx {
+
+constexpr int kMaxPasses = 3;
+constexpr int kSumCols = 6;  // HSX_SUM_COLS
+enum { kFilter = 0, kChannel = 1, kShape = 2 };
+
+// n / d for n < 2^32, d < 2^32 via one 64-bit mul-hi: m = ceil(2^64 / d).
+struct FastDiv {
+  unsigned long long m;
+  unsigned int d;
+  unsigned int pad;
+};
+
+__host__ inline FastDiv make_fastdiv(unsigned int d) {
+  FastDiv f;
+  f.d = d;
+  f.pad = 0;
+  f.m = d > 1 ? (~0ULL / d + 1ULL) : 0ULL;
+  return f;
+}
+
+__device__ __forceinline__ unsigned int fdiv(unsigned int n, const FastDiv& f) {
+  return f.d == 1 ? n : (unsigned int)__umul64hi((unsigned long long)n, f.m);
+}
+
+// Per-layer table entry (one per weight tensor, layer order = reference order).
+struct DevLayer {
+  long long off;    // element offset in every fp32 arena
+  long long n;      // elements
+  long long mword;  // mask word offset, -1 for dense layers
+  long long okeep;  // offset of this layer's K_out flags / positions
+  long long ikeep;  // offset of this layer's K_in flags / positions
+  long long goff[kMaxPasses];  // offset into norms / keep flags per pass
+  long long poff[kMaxPasses];  // offset into group-norm partials per pass
+  int rows, cin, k, L;         // rank-4: c_out, c_in, kh*kw, c_in*kh*kw; rank-2: d0, d1, 1, d1
+  int ncons;                   // number of constraints (0 = dense path)
+  int nparts;                  // row tiles of the candidate kernel (partials rows)
+  int rsub;                    // rows per shared-memory sub-tile
+  int rank;
+  int group[kMaxPasses];
+  int keep[kMaxPasses];
+  int G[kMaxPasses];
+  FastDiv divL, divk;
+  double rho1, rho2, gamma;
+};
+
+// A contiguous slice [begin, end) of one layer's elements.
+struct Item {
+  int layer;
+  int part;  // row-tile index inside the layer (candidate kernel)
+  long long begin, end;
+};
+
+struct CandArgs {
+  const float* __restrict__ s;
+  const float* __restrict__ theta;
+  const float* __restrict__ u;
+  const float* __restrict__ z;
+  const float* __restrict__ v;
+  float* __restrict__ zn;
+  const uint32_t* __restrict__ fmask;  // frozen global mask bits or nullptr
+  const DevLayer* __restrict__ layers;
+  const Item* __restrict__ items;
+  double* __restrict__ partials;       // this pass
+  const uint8_t* flags[kMaxPasses];    // keep flags of earlier passes (renorm)
+  int pass;
+  int identity;                        // candidate = input (per-tensor API)
+  int sqcap;                           // doubles of the sq sub-tile region
+};
+
+struct ElemArgs {
+  const float* __restrict__ theta;
+  float* __restrict__ u;
+  const float* __restrict__ zn;
+  float* __restrict__ v;
+  const float* __restrict__ vin;
+  const float* __restrict__ flat_in;
+  float* __restrict__ flat_out;
+  float* __restrict__ z;
+  const DevLayer* __restrict__ layers;
+  const Item* __restrict__ items;
+  const int* __restrict__ pos_out;
+  const int* __restrict__ pos_in;
+  const long long* __restrict__ summary;
+  float divisor;
+};
+
+void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st);
+void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
+                   double* norms, uint8_t* flags, size_t smem, cudaStream_t st);
+void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
+                    uint32_t* mask, const uint8_t* f0, const uint8_t* f1, const uint8_t* f2,
+                    cudaStream_t st);
+void launch_mask_or(const uint32_t* g, int m, long long words, uint32_t* out, cudaStream_t st);
+void launch_keep_mark(const DevLayer* layers, const Item* items, int n_items, const uint32_t* uni,
+                      const uint32_t* prev, uint8_t* oflag, uint8_t* iflag, long long* summary,
+                      size_t smem, cudaStream_t st);
+void launch_keep_scan(const DevLayer* layers, const int* list, int n, int n_layers,
+                      const uint8_t* oflag, const uint8_t* iflag, int* pos_out, int* pos_in,
+                      long long* summary, unsigned int* done, cudaStream_t st);
+void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
+void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
+void launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t st);
+void launch_dual(const float* theta, float* u, const float* zn, long long n, cudaStream_t st);
+void launch_nonzero(const float* t, long long n, uint8_t* out, cudaStream_t st);
+void launch_pack(const uint8_t* m, long long n, uint32_t* bits, cudaStream_t st);
+void launch_unpack(const uint32_t* bits, long long n, uint8_t* m, cudaStream_t st);
+void launch_count_diff(const uint8_t* a, const uint8_t* b, long long n, unsigned long long* c,
+                       cudaStream_t st);
+
+}  // namespace hsx

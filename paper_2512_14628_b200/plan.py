@@ -1,0 +1,233 @@
+"""Python handle of an ``hsx_plan`` (layer table + work lists + scratch on device).
+
+A plan fixes the arena layout of a model: every fp32 state arena (theta, u,
+z_node, v, z, the intra-sum buffer, the flat compact buffer) has the same
+per-layer offsets (multiples of 32 elements), and every mask arena holds one
+bit per element of each prunable layer.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .errors import ShapeError
+from .layers import GROUP_CODE, GroupBy, LayerKind, LayerSpec
+
+
+def current_stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def require_cuda_f32(t, name="tensor"):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA torch tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ShapeError(f"{name} must be contiguous")
+    if t.data_ptr() % 16:
+        raise ShapeError(f"{name} must be 16-byte aligned")
+    return t
+
+
+class Plan:
+    """Owns one ``hsx_plan``; layer order is the caller's (reference) layer order."""
+
+    def __init__(self, layers: list[LayerSpec], groups: dict[str, list[tuple[GroupBy, int]]],
+                 rho1: dict[str, float] | None = None, rho2: dict[str, float] | None = None):
+        lib = _lib.load()
+        self.layers = list(layers)
+        self.names = [ls.name for ls in layers]
+        self.index = {n: i for i, n in enumerate(self.names)}
+        self.groups = {n: list(groups.get(n, [])) for n in self.names}
+        n = len(layers)
+        descs = (_lib.LayerDesc * max(n, 1))()
+        for i, ls in enumerate(layers):
+            d = descs[i]
+            shape = ls.shape
+            d.rank = len(shape)
+            for j in range(4):
+                d.shape[j] = shape[j] if j < len(shape) else 1
+            g = self.groups[ls.name]
+            if g and ls.kind is not LayerKind.CONV:
+                raise ShapeError(f"layer {ls.name}: only conv layers are prunable")
+            d.n_constraints = len(g)
+            for j, (grp, keep) in enumerate(g):
+                d.group[j] = GROUP_CODE[grp]
+                d.keep[j] = int(keep)
+            d.rho1 = float((rho1 or {}).get(ls.name, 1.0))
+            d.rho2 = float((rho2 or {}).get(ls.name, 0.0))
+        h = C.c_void_p()
+        _lib.check(lib.hsx_plan_create(descs, n, C.byref(h)), "hsx_plan_create")
+        self._h = h
+        self._lib = lib
+        self.arena = int(lib.hsx_plan_arena_elements(h))
+        self.offsets = [int(lib.hsx_plan_layer_offset(h, i)) for i in range(n)]
+        self.mask_words = int(lib.hsx_plan_mask_words(h))
+        self.mask_offsets = [int(lib.hsx_plan_mask_word_offset(h, i)) for i in range(n)]
+        self.max_passes = int(lib.hsx_plan_max_passes(h))
+        self.prunable = [i for i, ls in enumerate(layers) if self.groups[ls.name]]
+        self.summary_host = torch.zeros(n * _lib.SUM_COLS + 1, dtype=torch.int64).pin_memory() \
+            if torch.cuda.is_available() else torch.zeros(n * _lib.SUM_COLS + 1, dtype=torch.int64)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.hsx_plan_destroy(h)
+            self._h = C.c_void_p()
+
+    # -- configuration ---------------------------------------------------------
+    def set_penalties(self, rho1: dict | None, rho2: dict | None, weight_decay: float,
+                      num_nodes: int, accels_per_node: int, identity: bool = False):
+        def arr(d):
+            if d is None:
+                return None
+            a = (C.c_double * len(self.names))(*[float(d[n]) for n in self.names])
+            return C.cast(a, C.c_void_p), a
+
+        r1, r2 = arr(rho1), arr(rho2)
+        _lib.check(self._lib.hsx_plan_set_penalties(
+            self._h, r1[0] if r1 else None, r2[0] if r2 else None, float(weight_decay),
+            int(num_nodes), int(accels_per_node), int(identity)), "set_penalties")
+
+    # -- arena helpers -----------------------------------------------------------
+    def empty_arena(self, device, fill_zero=True):
+        t = torch.zeros(self.arena, dtype=torch.float32, device=device)
+        return t
+
+    def empty_mask(self, device, ones=False, count: int = 1):
+        shape = (count, self.mask_words) if count > 1 else (self.mask_words,)
+        t = torch.zeros(shape, dtype=torch.int32, device=device)
+        if ones:
+            self.fill_ones(t.view(-1, self.mask_words)[0] if count > 1 else t)
+        return t
+
+    def fill_ones(self, mask):
+        """All-ones global masks (reference consensus.py:418), padding bits clear."""
+        for i in self.prunable:
+            n = self.layers[i].elements
+            w0 = self.mask_offsets[i]
+            full, rem = divmod(n, 32)
+            mask[w0:w0 + full].fill_(-1)
+            if rem:
+                mask[w0 + full].fill_((1 << rem) - 1)
+        return mask
+
+    def view(self, arena, i: int):
+        ls = self.layers[i]
+        o = self.offsets[i]
+        return arena[o:o + ls.elements].view(ls.shape)
+
+    def views(self, arena) -> dict:
+        return {n: self.view(arena, i) for i, n in enumerate(self.names)}
+
+    def load_arena(self, arena, values: dict):
+        for i, n in enumerate(self.names):
+            self.view(arena, i).copy_(torch.as_tensor(values[n]).to(arena.device, torch.float32)
+                                      .view(self.layers[i].shape))
+
+    def mask_view_words(self, mask, i: int):
+        n = self.layers[i].elements
+        w0 = self.mask_offsets[i]
+        return mask[w0:w0 + (n + 31) // 32]
+
+    def unpack_mask(self, mask, i: int):
+        """Bool tensor of layer i's mask bits (hsx_unpack_bits)."""
+        ls = self.layers[i]
+        out = torch.empty(ls.shape, dtype=torch.bool, device=mask.device)
+        words = self.mask_view_words(mask, i)
+        _lib.call("hsx_unpack_bits", words.data_ptr(), ls.elements, out.data_ptr(), current_stream())
+        return out
+
+    # -- kernels (thin wrappers; all on the current stream) ---------------------
+    def pack_theta_u(self, theta, u, send):
+        _lib.call("hsx_pack_theta_u", self._h, ptr(theta), ptr(u), ptr(send), current_stream())
+
+    def candidate(self, s, theta, u, z, v, z_node, frozen_mask=None):
+        _lib.call("hsx_candidate", self._h, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v), ptr(z_node),
+                  ptr(frozen_mask), current_stream())
+
+    def renorm(self, p, s, theta, u, z, v):
+        _lib.call("hsx_candidate_renorm", self._h, p, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v),
+                  current_stream())
+
+    def select(self, p):
+        _lib.call("hsx_select", self._h, p, current_stream())
+
+    def project(self, z_node, local_mask):
+        _lib.call("hsx_project", self._h, ptr(z_node), ptr(local_mask), current_stream())
+
+    def project_all(self, s, theta, u, z, v, z_node, local_mask):
+        """K2 (+ composite passes) + K3 after hsx_candidate."""
+        for p in range(self.max_passes):
+            if p > 0:
+                self.renorm(p, s, theta, u, z, v)
+            self.select(p)
+        self.project(z_node, local_mask)
+
+    def group_norms(self, p: int, device):
+        total = int(self._lib.hsx_plan_group_total(self._h, p))
+        norms = torch.empty(total, dtype=torch.float64, device=device)
+        flags = torch.empty(total, dtype=torch.uint8, device=device)
+        _lib.call("hsx_read_groups", self._h, p, ptr(norms), ptr(flags), current_stream())
+        return norms, flags
+
+    def group_offset(self, i: int, p: int) -> int:
+        return int(self._lib.hsx_plan_group_offset(self._h, i, p))
+
+    def keep_sets(self, union_mask, prev_mask=None):
+        _lib.call("hsx_keep_sets", self._h, ptr(union_mask), ptr(prev_mask), current_stream())
+
+    def keep_sets_fetch(self):
+        """D2H of the per-layer summary; synchronizes the current stream."""
+        _lib.call("hsx_keep_sets_fetch", self._h, self.summary_host.data_ptr(), current_stream())
+        return self.summary_host.view(-1)
+
+    def summary_rows(self):
+        s = self.summary_host
+        n = len(self.names)
+        return s[: n * _lib.SUM_COLS].view(n, _lib.SUM_COLS), int(s[n * _lib.SUM_COLS])
+
+    def keep_positions(self, device):
+        out = []
+        for which in (0, 1):
+            n = int(self._lib.hsx_plan_keep_total(self._h, which))
+            t = torch.empty(n, dtype=torch.int32, device=device)
+            _lib.call("hsx_read_keep_positions", self._h, which, ptr(t), current_stream())
+            out.append(t)
+        return out
+
+    def keep_offset(self, i: int, which: int) -> int:
+        return int(self._lib.hsx_plan_keep_offset(self._h, i, which))
+
+    def set_keep_sets(self, i: int, k_out, k_in):
+        ko = (C.c_int32 * max(len(k_out), 1))(*k_out)
+        ki = (C.c_int32 * max(len(k_in), 1))(*k_in)
+        _lib.call("hsx_set_keep_sets", self._h, i, C.cast(ko, C.c_void_p), len(k_out),
+                  C.cast(ki, C.c_void_p), len(k_in))
+
+    def compact_dual(self, theta, u, z_node, v, flat):
+        _lib.call("hsx_compact_dual", self._h, ptr(theta), ptr(u), ptr(z_node), ptr(v), ptr(flat),
+                  current_stream())
+
+    def dual_intra(self, theta, u, z_node):
+        _lib.call("hsx_dual_intra", self._h, ptr(theta), ptr(u), ptr(z_node), current_stream())
+
+    def decompact_dual(self, flat, divisor, z_node, v, z):
+        _lib.call("hsx_decompact_dual", self._h, ptr(flat), float(divisor), ptr(z_node), ptr(v),
+                  ptr(z), current_stream())
+
+
+def mask_or(gathered, n_ranks: int, words: int, out):
+    _lib.call("hsx_mask_or", ptr(gathered), int(n_ranks), int(words), ptr(out), current_stream())

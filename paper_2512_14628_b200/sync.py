@@ -1,0 +1,209 @@
+"""HSADMMSync — the B200-native H-SADMM synchronization step (one rank).
+
+Replaces phases 2-4 and the u-update of phase 5 of the reference's
+``hierarchical_program`` (/root/reference/pkg/src/admmprune/consensus.py:436-535)
+plus the freeze / keep-set seal (:600-606), in SPMD form: one engine per rank
+(one rank per GPU under ``torchrun``, or all ranks of a topology on one GPU
+through :class:`~.transport.LocalCluster`).
+
+Per iteration k (leader = local rank 0 of its node):
+
+    K0  S = theta + u                        (skipped when P == 1: fused into K1)
+    C1  intra all-reduce SUM of S            (NCCL over NVLink)
+    K1  z_node = candidate; fp64 group-norm partials          [dynamic]
+    K2  top-k keep flags per constraint pass                  [dynamic]
+    K3  zero dropped groups, local mask bits                  [dynamic]
+    C2  leaders all-gather packed mask bits; K4 OR -> union   [dynamic, M > 1]
+    C4a intra broadcast of the union bits                     [dynamic, P > 1]
+    K5  keep sets (K_out/K_in, positions, payload offsets), drift popcounts;
+        one D2H of the per-layer counts sizes the collectives [dynamic]
+    K6  leader: flat <- compress(z_node + v) fused with u += theta - z_node
+        follower: K6f u += theta - z_node
+    C3  leaders all-reduce AVG of the flat compact buffer, per <=32 MiB bucket
+    C4  intra broadcast of the reduced compact buffer (not of z and v: every
+        rank of a node holds bitwise-identical z_node and v, so followers
+        decompact locally and get the leader's z, v bit-for-bit)
+    K7  z = decompress(flat); v += z_node - z
+
+Frozen iterations (after ``t_freeze`` or a zero-drift window) skip K2-K5,
+C2 and C4a: K1 applies the frozen union mask and the sealed keep sets stay
+on the device.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .consensus import ConsensusSettings, PenaltySchedule, freeze_check
+from .errors import ProtocolError, ShapeError
+from .layers import LayerSpec
+from .plan import Plan, mask_or
+from .sparsity import resolve_plan
+from .transport import AllGather, AllReduce, Broadcast, ReduceOp, bucketize
+from . import _lib
+
+
+class HSADMMSync:
+    """Device state + sync program of one rank.
+
+    State arenas (fp32, shared layout from :class:`~.plan.Plan`): ``theta``,
+    ``u``, ``z_node``, ``v``, ``z``; ``masks`` holds the global union mask bits
+    of the prunable layers (initially all ones, consensus.py:418).
+    """
+
+    def __init__(self, rank: int, cluster, layers: list[LayerSpec], constraints: dict,
+                 schedule: PenaltySchedule, settings: ConsensusSettings, device=None):
+        topo = cluster.topology
+        self.rank = rank
+        self.cluster = cluster
+        self.topology = topo
+        self.M, self.P = topo.num_nodes, topo.accels_per_node
+        self.node = topo.node_of(rank)
+        self.leader_rank = topo.leader_of(self.node)
+        self.is_leader = rank == self.leader_rank
+        self.intra = cluster.intra_group(self.node)
+        self.inter = cluster.leader_group()
+        self.layers = list(layers)
+        self.names = [ls.name for ls in layers]
+        self.settings = settings
+        self.schedule = schedule
+        groups = {ls.name: resolve_plan(ls.shape, constraints[ls.name])
+                  for ls in layers if constraints.get(ls.name)}
+        self.plan = Plan(self.layers, groups, schedule.rho1, schedule.rho2)
+        self.plan.set_penalties(schedule.rho1, schedule.rho2, settings.weight_decay, self.M, self.P)
+        self.prunable = self.plan.prunable
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        pl, dev = self.plan, self.device
+        self.theta, self.u, self.z_node, self.v, self.z = (pl.empty_arena(dev) for _ in range(5))
+        self.sum = pl.empty_arena(dev) if self.P > 1 else None
+        self.flat = torch.zeros(max(pl.arena, 1), dtype=torch.float32, device=dev)
+        self.masks = pl.empty_mask(dev, ones=True)
+        self.union = pl.empty_mask(dev)
+        self.local_mask = pl.empty_mask(dev)
+        self.gathered = (torch.zeros((self.M, max(pl.mask_words, 1)), dtype=torch.int32, device=dev)
+                         if self.is_leader and self.M > 1 else None)
+        self.frozen = False
+        self.drift_history: list[float] = []
+        self.drift_now: dict[str, float] = {}
+        self.cache_derive = 0
+        self.cache_hits = 0
+        self.cache_seen = False
+        self.payload_elements = sum(ls.elements for ls in self.layers)  # all kept initially
+        self.buckets = None
+        self._layout_from_summary(initial=True)
+
+    # -- state I/O ---------------------------------------------------------------
+    def load(self, **arrays) -> None:
+        """Copy per-layer dicts into arenas, e.g. ``load(theta=..., u=..., z=...)``."""
+        for key, values in arrays.items():
+            self.plan.load_arena(getattr(self, key), values)
+
+    def init_from(self, params0: dict) -> None:
+        """Reference initial state: theta = z_node = z = params0, u = v = 0 (consensus.py:412-418)."""
+        self.load(theta=params0, z_node=params0, z=params0)
+        self.u.zero_()
+        self.v.zero_()
+
+    def views(self, key: str) -> dict:
+        return self.plan.views(getattr(self, key))
+
+    def mask_dict(self) -> dict:
+        return {self.names[i]: self.plan.unpack_mask(self.masks, i) for i in self.prunable}
+
+    # -- layout of the flat compact buffer -------------------------------------------
+    def _layout_from_summary(self, initial=False):
+        if initial:
+            sizes = [(ls.name, ls.elements) for ls in self.layers]
+        else:
+            rows, total = self.plan.summary_rows()
+            sizes = [(self.names[i], int(rows[i, _lib.SUM_ELEMS])) for i in range(len(self.names))]
+            self.payload_elements = total
+        # layers whose kept rectangle is empty are not sent (consensus.py:480)
+        self.payload = [(n, e) for n, e in sizes if e > 0]
+        self.buckets = bucketize(self.payload)
+
+    @property
+    def leader_bytes(self) -> int:
+        """z_sync payload bytes per leader per sync (4 B / element, harness.py:447-449 convention)."""
+        return 4 * self.payload_elements
+
+    # -- the per-iteration program ------------------------------------------------------
+    def program(self, k: int):
+        """Generator: yields collective requests, performs phases 2-5(u) of iteration k."""
+        pl = self.plan
+        frozen = self.frozen
+        dynamic = not frozen and bool(self.prunable)
+        # phase 2: intra-node sum of theta + u
+        s = None
+        if self.P > 1:
+            pl.pack_theta_u(self.theta, self.u, self.sum)
+            s = yield AllReduce(self.intra, self.sum, ReduceOp.SUM, "theta_u", k)
+        # phase 3: node candidate, projection or frozen mask
+        pl.candidate(s, self.theta, self.u, self.z, self.v, self.z_node,
+                     frozen_mask=self.masks if (frozen and self.prunable) else None)
+        if dynamic:
+            pl.project_all(s, self.theta, self.u, self.z, self.v, self.z_node, self.local_mask)
+        if k % self.settings.sync_period != 0:
+            pl.dual_intra(self.theta, self.u, self.z_node)
+            return None
+        # phase 4: mask union (leaders), broadcast to followers, keep sets
+        if dynamic:
+            if self.is_leader:
+                if self.M > 1:
+                    yield AllGather(self.inter, self.local_mask, self.gathered, f"mask_sync", k)
+                    mask_or(self.gathered, self.M, pl.mask_words, self.union)
+                else:
+                    self.union, self.local_mask = self.local_mask, self.union
+            if self.P > 1:
+                yield Broadcast(self.intra, self.leader_rank, self.union, "m_bcast", k)
+            pl.keep_sets(self.union, self.masks)
+            pl.keep_sets_fetch()                        # the one D2H of the dynamic step
+            self._layout_from_summary()
+            rows, _ = pl.summary_rows()
+            self.drift_now = {self.names[i]: int(rows[i, _lib.SUM_DRIFT]) / self.layers[i].elements
+                              for i in self.prunable}
+            self.drift_history.append(max(self.drift_now.values()))
+            if self.is_leader:                          # KeepSetCache counters (shrinkage.py:115-130)
+                changed = sum(1 for i in self.prunable if rows[i, _lib.SUM_DRIFT] > 0)
+                derive = len(self.prunable) if not self.cache_seen else changed
+                self.cache_derive += derive
+                self.cache_hits += len(self.prunable) - derive
+                self.cache_seen = True
+        elif self.is_leader and self.prunable:
+            self.cache_hits += len(self.prunable)
+        # compaction fused with the intra dual update; leader average; broadcast
+        total = self.payload_elements
+        flat = self.flat[:total]
+        if self.is_leader:
+            pl.compact_dual(self.theta, self.u, self.z_node, self.v, self.flat)
+            for bi, b in enumerate(self.buckets):
+                yield AllReduce(self.inter, self.flat[b.start:b.start + b.elements], ReduceOp.AVG,
+                                f"z_sync/b{bi}", k, detail=b.detail)
+        else:
+            pl.dual_intra(self.theta, self.u, self.z_node)
+        if self.P > 1 and total > 0:
+            yield Broadcast(self.intra, self.leader_rank, flat, "zhat_bcast", k)
+        pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
+        if dynamic:
+            self.masks, self.union = self.union, self.masks
+        # freeze + seal (consensus.py:600-606)
+        if dynamic and freeze_check(k, self.settings.t_freeze, self.drift_history,
+                                    self.settings.drift_window):
+            self.frozen = True
+            if self.is_leader:
+                self.cache_hits += len(self.prunable)   # cache.get on the final masks, then seal
+        return None
+
+    def step(self, k: int):
+        """Run iteration k through a DistCluster (one rank per process)."""
+        if not hasattr(self.cluster, "run_rank"):
+            raise ProtocolError("step() needs a DistCluster; use LocalCluster.run for in-process ranks")
+        return self.cluster.run_rank(self.program(k))
+
+
+def run_local(engines: list[HSADMMSync], k: int):
+    """Run iteration k for every rank of a LocalCluster (single process, one GPU)."""
+    cluster = engines[0].cluster
+    if len(engines) != cluster.topology.world_size:
+        raise ShapeError("need one engine per rank")
+    return cluster.run({e.rank: e.program(k) for e in engines})

@@ -1,0 +1,456 @@
+"""Hierarchical process groups, collective requests and the two drivers.
+
+Mirrors the reference's transport surface
+(/root/reference/pkg/src/admmprune/transport.py): ``Topology`` (:36-69),
+``GroupScope`` / ``ProcessGroup`` (:72-86), ``ReduceOp`` (:89-92), collective
+request objects (:95-120), ``LedgerEntry`` / ``CommLedger`` (:126-188),
+``bucketize`` / ``unbucketize`` (:227-290). A rank program is a generator that
+yields collective requests and is resumed with the result, exactly like the
+reference's ``Cluster.run`` protocol (:331-376) — but payloads are CUDA
+tensors and there are two drivers:
+
+* ``DistCluster``: one process per GPU under ``torchrun``; every request is
+  executed with ``torch.distributed`` on NCCL sub-communicators built with
+  ``new_group`` (intra groups, the leader group, global) — the B200 box
+  emulates PruneX's hierarchy: intra = NVLink all-reduce among a node's
+  ranks, inter = the leader-only all-reduce of compact buffers.
+* ``LocalCluster``: all ranks of a topology inside one process (one GPU),
+  collectives completed once every member has posted, folding in member order
+  like the reference's deterministic scheduler. Used to check multi-rank
+  parity on a single GPU and by the CPU (gloo-free) protocol tests.
+
+Requests are in-place: an ``AllReduce`` / ``Broadcast`` writes its result
+into ``payload`` on every member (NCCL semantics) and the program is resumed
+with that same tensor.
+"""
+
+from __future__ import annotations
+
+import enum
+import logging
+from dataclasses import dataclass, field
+from typing import Any, Generator, Mapping
+
+from .errors import ProtocolError, ShapeError
+
+log = logging.getLogger(__name__)
+
+ELEMENT_BYTES = 4                      # fp32 wire accounting (reference transport.py:32)
+BUCKET_CAP_BYTES = 32 * 1024 * 1024    # reference transport.py:33
+
+
+@dataclass(frozen=True)
+class Topology:
+    """``num_nodes`` x ``accels_per_node`` ranks; local rank 0 leads its node."""
+
+    num_nodes: int
+    accels_per_node: int
+
+    def __post_init__(self):
+        if self.num_nodes < 1 or self.accels_per_node < 1:
+            raise ShapeError("topology dimensions must be positive")
+
+    @property
+    def world_size(self) -> int:
+        return self.num_nodes * self.accels_per_node
+
+    def node_of(self, rank: int) -> int:
+        return rank // self.accels_per_node
+
+    def local_rank(self, rank: int) -> int:
+        return rank % self.accels_per_node
+
+    def leader_of(self, node: int) -> int:
+        return node * self.accels_per_node
+
+    def is_leader(self, rank: int) -> bool:
+        return self.local_rank(rank) == 0
+
+    @property
+    def leaders(self) -> tuple[int, ...]:
+        return tuple(self.leader_of(i) for i in range(self.num_nodes))
+
+    @classmethod
+    def parse(cls, text: str) -> "Topology":
+        """'2x4' -> Topology(2, 4)."""
+        m, p = text.lower().split("x")
+        return cls(int(m), int(p))
+
+
+class GroupScope(enum.Enum):
+    INTRA = "intra"
+    INTER = "inter"
+    GLOBAL = "global"
+
+
+@dataclass(frozen=True)
+class ProcessGroup:
+    id: str
+    members: tuple[int, ...]
+    scope: GroupScope
+
+    def __post_init__(self):
+        if not self.members or len(set(self.members)) != len(self.members):
+            raise ShapeError(f"group {self.id}: members must be non-empty and unique")
+
+
+class ReduceOp(enum.Enum):
+    SUM = "sum"
+    AVG = "avg"
+    BITWISE_OR = "bor"
+
+
+def hierarchy_groups(topology: Topology):
+    """(intra groups by node, leader group, global group) — reference Cluster.__init__ :305-318."""
+    P = topology.accels_per_node
+    intra = {i: ProcessGroup(f"intra{i}", tuple(range(i * P, (i + 1) * P)), GroupScope.INTRA)
+             for i in range(topology.num_nodes)}
+    leaders = ProcessGroup("leaders", topology.leaders, GroupScope.INTER)
+    world = ProcessGroup("global", tuple(range(topology.world_size)), GroupScope.GLOBAL)
+    return intra, leaders, world
+
+
+# -- collective requests -------------------------------------------------------
+
+
+@dataclass
+class AllReduce:
+    group: ProcessGroup
+    payload: Any            # tensor, reduced in place
+    op: ReduceOp
+    tag: str
+    iteration: int
+    detail: tuple | None = None
+
+
+@dataclass
+class Broadcast:
+    group: ProcessGroup
+    root: int
+    payload: Any            # tensor: sent by root, received in place by the others
+    tag: str
+    iteration: int
+
+
+@dataclass
+class AllGather:
+    group: ProcessGroup
+    payload: Any            # local tensor
+    out: Any                # (members, *payload.shape) output, member order
+    tag: str
+    iteration: int
+
+
+RankProgram = Generator[Any, Any, Any]
+
+
+# -- ledger ---------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class LedgerEntry:
+    iteration: int
+    group: str
+    scope: str
+    op: str
+    elements: int
+    bytes: int
+    members: int
+    label: str
+    detail: tuple | None = None
+
+    def to_dict(self) -> dict:
+        d = dict(iter=self.iteration, group=self.group, scope=self.scope, op=self.op,
+                 elements=self.elements, bytes=self.bytes, members=self.members, label=self.label)
+        if self.detail is not None:
+            d["detail"] = {name: n for name, n in self.detail}
+        return d
+
+
+class CommLedger:
+    """Append-only record of completed collectives (reference transport.py:154-188).
+
+    ``bytes`` are the per-rank payload bytes actually moved: fp32 payloads at
+    4 B/element like the reference; packed mask bits at their real size.
+    """
+
+    def __init__(self):
+        self.entries: list[LedgerEntry] = []
+
+    def append(self, entry: LedgerEntry) -> None:
+        if entry.bytes <= 0:
+            raise ShapeError("ledger entries must carry positive byte counts")
+        self.entries.append(entry)
+
+    def total_bytes(self, scope=None, iteration=None, label_prefix=None) -> int:
+        sv = scope.value if isinstance(scope, GroupScope) else scope
+        return sum(e.bytes for e in self.entries
+                   if (sv is None or e.scope == sv) and (iteration is None or e.iteration == iteration)
+                   and (label_prefix is None or e.label.startswith(label_prefix)))
+
+    def to_jsonl(self, path) -> None:
+        import json
+
+        with open(path, "w", encoding="utf-8") as fh:
+            for e in self.entries:
+                fh.write(json.dumps(e.to_dict(), sort_keys=True) + "\n")
+
+
+def _ledger(ledger, req, members: int, nbytes: int, op: str):
+    if ledger is None or nbytes <= 0:
+        return
+    n = int(req.payload.numel())
+    ledger.append(LedgerEntry(req.iteration, req.group.id, req.group.scope.value, op, n, nbytes,
+                              members, req.tag, getattr(req, "detail", None)))
+
+
+def _payload_bytes(t) -> int:
+    return int(t.numel()) * int(t.element_size())
+
+
+# -- bucketing (layout only: the payload already lives in one flat buffer) --------
+
+
+@dataclass
+class Bucket:
+    """A contiguous slice of the flat compact buffer (reference transport.py:227-236)."""
+
+    start: int
+    layout: tuple[tuple[str, int, int], ...]  # (name, offset inside bucket, elements)
+
+    @property
+    def elements(self) -> int:
+        return sum(e for _, _, e in self.layout)
+
+    @property
+    def detail(self) -> tuple[tuple[str, int], ...]:
+        return tuple((name, e) for name, _, e in self.layout)
+
+
+def bucketize(payloads, cap_bytes: int = BUCKET_CAP_BYTES) -> list[Bucket]:
+    """Greedy <= ``cap_bytes`` buckets over (name, elements) in order, never split.
+
+    Same grouping rule as the reference (transport.py:239-280): a payload
+    larger than the cap gets its own bucket with a warning. ``payloads`` may
+    hold element counts or tensors. Concatenating the buckets is the
+    concatenation of the payloads, so a bucket is just a [start, start+n)
+    slice of the flat buffer the compaction kernel already wrote.
+    """
+    sizes = [(name, int(x) if isinstance(x, int) else int(x.numel())) for name, x in payloads]
+    buckets: list[Bucket] = []
+    cur: list[tuple[str, int]] = []
+    cur_bytes = 0
+    start = 0
+
+    def close():
+        nonlocal cur, cur_bytes, start
+        if cur:
+            lay, off = [], 0
+            for name, n in cur:
+                lay.append((name, off, n))
+                off += n
+            buckets.append(Bucket(start, tuple(lay)))
+            start += off
+        cur, cur_bytes = [], 0
+
+    for name, n in sizes:
+        nbytes = n * ELEMENT_BYTES
+        if nbytes > cap_bytes:
+            close()
+            log.warning("payload %s (%d bytes) exceeds bucket cap %d; using oversized bucket",
+                        name, nbytes, cap_bytes)
+            cur, cur_bytes = [(name, n)], nbytes
+            close()
+            continue
+        if cur_bytes + nbytes > cap_bytes:
+            close()
+        cur.append((name, n))
+        cur_bytes += nbytes
+    close()
+    return buckets
+
+
+def unbucketize(bucket: Bucket, buffer) -> dict:
+    """Views of the bucket's named payloads inside ``buffer`` (the bucket's slice)."""
+    if int(buffer.numel()) != bucket.elements:
+        raise ShapeError(f"buffer size {buffer.numel()} does not match bucket {bucket.elements}")
+    return {name: buffer[off:off + n] for name, off, n in bucket.layout}
+
+
+# -- drivers --------------------------------------------------------------------
+
+
+def _validate(rank: int, req) -> None:
+    if not isinstance(req, (AllReduce, Broadcast, AllGather)):
+        raise ProtocolError(f"rank {rank} yielded a non-collective object: {req!r}")
+    if rank not in req.group.members:
+        raise ProtocolError(f"rank {rank} is not a member of group {req.group.id}")
+    if isinstance(req, Broadcast) and req.root not in req.group.members:
+        raise ProtocolError(f"broadcast root {req.root} is not in group {req.group.id}")
+    if isinstance(req, AllReduce) and req.op is ReduceOp.BITWISE_OR:
+        raise ProtocolError("BITWISE_OR is carried as an AllGather of packed bits + OR kernel")
+
+
+class LocalCluster:
+    """All ranks of a topology in one process; deterministic round-based scheduler."""
+
+    def __init__(self, topology: Topology):
+        self.topology = topology
+        self.ledger = CommLedger()
+        self._intra, self._leaders, self._global = hierarchy_groups(topology)
+
+    def intra_group(self, node: int) -> ProcessGroup:
+        return self._intra[node]
+
+    def leader_group(self) -> ProcessGroup:
+        return self._leaders
+
+    def global_group(self) -> ProcessGroup:
+        return self._global
+
+    def run(self, programs: Mapping[int, RankProgram]) -> dict[int, Any]:
+        gens = dict(programs)
+        started, results = set(), {}
+        inbox: dict[int, Any] = {}
+        blocked: dict[int, Any] = {}
+        pending: dict[str, dict[int, Any]] = {}
+        while len(results) < len(gens):
+            progressed = False
+            for rank in sorted(gens):
+                if rank in results or rank in blocked:
+                    continue
+                try:
+                    req = next(gens[rank]) if rank not in started else gens[rank].send(inbox.pop(rank, None))
+                    started.add(rank)
+                except StopIteration as stop:
+                    started.add(rank)
+                    results[rank] = stop.value
+                    progressed = True
+                    continue
+                _validate(rank, req)
+                blocked[rank] = req
+                pending.setdefault(req.group.id, {})[rank] = req
+                progressed = True
+            for gid in sorted(pending):
+                posted = pending[gid]
+                group = next(iter(posted.values())).group
+                if set(posted) != set(group.members):
+                    continue
+                for r, value in self._complete(group, posted).items():
+                    inbox[r] = value
+                    del blocked[r]
+                del pending[gid]
+                progressed = True
+            if not progressed:
+                raise ProtocolError(f"collective deadlock; blocked ranks: "
+                                    f"{ {r: q.tag for r, q in blocked.items()} }")
+        return results
+
+    def _complete(self, group: ProcessGroup, posted: dict[int, Any]) -> dict[int, Any]:
+        reqs = [posted[r] for r in group.members]
+        first = reqs[0]
+        for q in reqs[1:]:
+            if type(q) is not type(first) or q.tag != first.tag or q.iteration != first.iteration:
+                raise ProtocolError(f"group {group.id}: mismatched collectives "
+                                    f"({type(first).__name__}:{first.tag} vs {type(q).__name__}:{q.tag})")
+        g = len(group.members)
+        if isinstance(first, Broadcast):
+            if len({q.root for q in reqs}) != 1:
+                raise ProtocolError(f"group {group.id}: broadcast roots disagree")
+            src = posted[first.root].payload
+            for q in reqs:
+                if tuple(q.payload.shape) != tuple(src.shape):
+                    raise ProtocolError(f"group {group.id}: broadcast shapes disagree on '{first.tag}'")
+                if q.payload.data_ptr() != src.data_ptr():
+                    q.payload.copy_(src)
+            _ledger(self.ledger, first, g, _payload_bytes(src) * (g - 1), "broadcast")
+            return {r: posted[r].payload for r in group.members}
+        if len({tuple(q.payload.shape) for q in reqs}) != 1:
+            raise ProtocolError(f"group {group.id}: payload shapes disagree on '{first.tag}'")
+        if isinstance(first, AllGather):
+            for q in reqs:
+                for i, r in enumerate(group.members):
+                    q.out[i].copy_(posted[r].payload)
+            _ledger(self.ledger, first, g, _payload_bytes(first.payload), "allgather")
+            return {r: posted[r].out for r in group.members}
+        acc = reqs[0].payload.clone()            # serial fold in member order
+        for q in reqs[1:]:
+            acc += q.payload
+        if first.op is ReduceOp.AVG:
+            acc /= float(g)
+        for q in reqs:
+            q.payload.copy_(acc)
+        _ledger(self.ledger, first, g, _payload_bytes(first.payload), f"allreduce_{first.op.value}")
+        return {r: posted[r].payload for r in group.members}
+
+
+class DistCluster:
+    """Executes one rank's program with torch.distributed (NCCL on B200, gloo on CPU).
+
+    All ranks construct it collectively: ``dist.new_group`` is called for every
+    intra group and the leader group in the same order on every rank.
+    """
+
+    def __init__(self, topology: Topology, backend_group=None):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise ProtocolError("torch.distributed is not initialized")
+        if dist.get_world_size() != topology.world_size:
+            raise ProtocolError(f"world size {dist.get_world_size()} != topology {topology.world_size}")
+        self.topology = topology
+        self.rank = dist.get_rank()
+        self.ledger = CommLedger()
+        self._intra, self._leaders, self._global = hierarchy_groups(topology)
+        self._handles = {}
+        for i in range(topology.num_nodes):
+            self._handles[self._intra[i].id] = dist.new_group(list(self._intra[i].members))
+        self._handles["leaders"] = dist.new_group(list(self._leaders.members))
+        self._handles["global"] = dist.group.WORLD
+        self._avg = dist.get_backend() == "nccl"
+
+    def intra_group(self, node: int) -> ProcessGroup:
+        return self._intra[node]
+
+    def leader_group(self) -> ProcessGroup:
+        return self._leaders
+
+    def global_group(self) -> ProcessGroup:
+        return self._global
+
+    def execute(self, req) -> Any:
+        import torch.distributed as dist
+
+        _validate(self.rank, req)
+        h = self._handles[req.group.id]
+        g = len(req.group.members)
+        if isinstance(req, Broadcast):
+            if g > 1:
+                dist.broadcast(req.payload, src=req.root, group=h)
+            _ledger(self.ledger, req, g, _payload_bytes(req.payload) * (g - 1), "broadcast")
+            return req.payload
+        if isinstance(req, AllGather):
+            if g > 1:
+                dist.all_gather_into_tensor(req.out.view(-1), req.payload.view(-1), group=h)
+            else:
+                req.out[0].copy_(req.payload)
+            _ledger(self.ledger, req, g, _payload_bytes(req.payload), "allgather")
+            return req.out
+        if g > 1:
+            if req.op is ReduceOp.AVG and not self._avg:
+                dist.all_reduce(req.payload, op=dist.ReduceOp.SUM, group=h)
+                req.payload /= float(g)
+            else:
+                op = dist.ReduceOp.AVG if req.op is ReduceOp.AVG else dist.ReduceOp.SUM
+                dist.all_reduce(req.payload, op=op, group=h)
+        _ledger(self.ledger, req, g, _payload_bytes(req.payload), f"allreduce_{req.op.value}")
+        return req.payload
+
+    def run_rank(self, program: RankProgram) -> Any:
+        """Drive this rank's generator to completion."""
+        try:
+            req = next(program)
+            while True:
+                req = program.send(self.execute(req))
+        except StopIteration as stop:
+            return stop.value

@@ -1,0 +1,298 @@
+"""GPU parity of the libhsx path against the reference's golden vectors and the
+CPU oracle (oracle/hsadmm_oracle.py) on identical inputs.
+
+Bars (north_star): masks, keep sets and compaction indices bit-exact; fp32
+tensors within 1e-5 relative, measured per tensor as
+    max|gpu - ref| / max(max|ref|, max|operands|)
+(duals are differences, elementwise relative error is
+meaningless where they cancel). Where the GPU and the reference evaluate the
+same fp64 expression on the same fp32 inputs, the fp32 output must equal the
+fp32 rounding of the reference value exactly.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hsadmm_oracle as O
+from tests import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def rel_err(got, ref, *operands):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    scale = max([np.max(np.abs(ref)) if ref.size else 0.0] +
+                [np.max(np.abs(np.asarray(o, dtype=np.float64))) for o in operands if np.size(o)] + [1e-30])
+    return float(np.max(np.abs(got - ref)) / scale) if ref.size else 0.0
+
+
+def cpu(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2512_14628_b200 import _lib
+
+    _lib.load()
+    torch.cuda.set_device(0)
+
+
+# -- per-tensor API vs the reference's golden vectors --------------------------------
+
+
+def test_projection_golden_single():
+    import paper_2512_14628_b200 as H
+
+    kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
+             "shape": H.ConstraintKind.SHAPE_KEEP}
+    groups = {"filter": H.GroupBy.FILTER, "channel": H.GroupBy.CHANNEL, "shape": H.GroupBy.SHAPE_POSITION}
+    singles, _ = G.projection_cases()
+    for c in singles:
+        t = torch.tensor(c["t"], dtype=torch.float32, device="cuda")
+        out = H.project(t, H.SparsityConstraint(kinds[c["kind"]], keep_count=c["keep"]))
+        assert np.array_equal(cpu(out).astype(np.float64), c["out"]), c["kind"]
+        assert np.array_equal(cpu(H.extract_mask(out)), c["mask"])
+        norms = cpu(H.group_norms(t, groups[c["kind"]]))
+        np.testing.assert_allclose(norms, c["norms"], rtol=1e-13, atol=0)
+
+
+def test_projection_golden_composite():
+    import paper_2512_14628_b200 as H
+
+    kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
+             "shape": H.ConstraintKind.SHAPE_KEEP}
+    _, comps = G.projection_cases()
+    for c in comps:
+        t = torch.tensor(c["t"], dtype=torch.float32, device="cuda")
+        cons = [H.SparsityConstraint(kinds[k], keep_count=kp) for k, kp in c["plan"]]
+        out = H.project_composite(t, cons)
+        assert np.array_equal(cpu(out).astype(np.float64), c["out"])
+
+
+def test_projection_errors():
+    import paper_2512_14628_b200 as H
+
+    with pytest.raises(H.ShapeError):
+        H.project(torch.ones((2, 3, 1, 1), device="cuda"),
+                  H.SparsityConstraint(H.ConstraintKind.CHANNEL_KEEP, keep_count=4))
+    with pytest.raises(H.ShapeError):
+        H.project(torch.ones((2, 3), device="cuda"),
+                  H.SparsityConstraint(H.ConstraintKind.CHANNEL_KEEP, keep_count=1))
+
+
+def test_shrinkage_golden():
+    import paper_2512_14628_b200 as H
+
+    for c in G.shrinkage_cases():
+        shape = c["t"].shape
+        layer = H.LayerSpec("c", H.LayerKind.CONV, shape, prunable=True)
+        keep = H.derive_keep_sets(torch.tensor(c["mask"], device="cuda"), layer)
+        assert keep.k_out == tuple(c["k_out"]) and keep.k_in == tuple(c["k_in"])
+        t = torch.tensor(c["t"], dtype=torch.float32, device="cuda")
+        cb = H.compress(t, keep)
+        assert np.array_equal(cpu(cb.data).astype(np.float64), c["compact"])
+        restored = H.decompress(cb, keep, shape)
+        assert np.array_equal(cpu(restored).astype(np.float64), c["restored"])
+        rect = cpu(H.rectangle_mask(keep, shape))
+        assert np.array_equal(cpu(restored) != 0, (c["t"] != 0) & rect)
+
+
+def test_keep_set_cache_counts_and_seal():
+    import paper_2512_14628_b200 as H
+
+    conv = H.LayerSpec("conv", H.LayerKind.CONV, (3, 2, 3, 3), prunable=True)
+    rng = np.random.default_rng(6)
+    a = np.zeros(conv.shape, bool)
+    a[np.ix_([0, 2], [1])] = True
+    b = ~a
+    cache = H.KeepSetCache()
+    cache.get(conv, torch.tensor(a))
+    assert (cache.derive_calls, cache.hits) == (1, 0)
+    cache.get(conv, torch.tensor(a))
+    assert (cache.derive_calls, cache.hits) == (1, 1)
+    cache.get(conv, torch.tensor(b))
+    assert (cache.derive_calls, cache.hits) == (2, 1)
+    cache.seal()
+    keep = cache.get(conv, torch.tensor(a))
+    assert (cache.derive_calls, cache.hits) == (2, 2)
+    assert keep == H.derive_keep_sets(torch.tensor(b), conv)
+    empty = H.KeepSetCache()
+    empty.seal()
+    with pytest.raises(H.ProtocolError):
+        empty.get(conv, torch.tensor(a))
+    del rng
+
+
+def test_node_candidate_is_fp32_rounding_of_reference():
+    import paper_2512_14628_b200 as H
+
+    for c in G.candidate_cases():
+        s, z, v = (torch.tensor(x, dtype=torch.float32, device="cuda") for x in c["svz"])
+        r1, r2, wd, m, p = c["par"]
+        out = H.node_candidate(s, z, v, r1, r2, wd, int(m), int(p))
+        assert np.array_equal(cpu(out), c["out"].astype(np.float32))
+    with pytest.raises(H.ConfigError):
+        H.node_candidate(torch.ones(2), torch.ones(2), torch.ones(2), 0.0, 0.0, 0.0, 1, 1)
+
+
+def test_update_rules_per_tensor():
+    import paper_2512_14628_b200 as H
+
+    rng = np.random.default_rng(2)
+    cand = rng.normal(size=(2, 2, 1, 1)).astype(np.float32)
+    cons = [H.SparsityConstraint(H.ConstraintKind.FILTER_KEEP, keep_count=1)]
+    z, m = H.update_node_consensus(torch.tensor(cand), cons, True, np.ones(cand.shape, bool))
+    assert np.array_equal(cpu(z), cand) and m is None
+    gm = rng.random(cand.shape) < 0.5
+    z, _ = H.update_node_consensus(torch.tensor(cand), cons, True, gm)
+    assert np.array_equal(cpu(z), cand * gm)
+    with pytest.raises(H.ProtocolError):
+        H.update_node_consensus(torch.tensor(cand), cons, True, None)
+    z, m = H.update_node_consensus(torch.tensor(cand[:, :, 0, 0]), [], False, None)
+    assert np.array_equal(cpu(z), cand[:, :, 0, 0]) and bool(cpu(m).all())
+    th, zn, u = (rng.normal(size=(5, 7)).astype(np.float32) for _ in range(3))
+    got = cpu(H.dual_update_intra(torch.tensor(th), torch.tensor(zn), torch.tensor(u)))
+    assert np.array_equal(got, (u.astype(np.float64) + (th.astype(np.float64) - zn)).astype(np.float32))
+    a = np.array([True, False, True, True])
+    b = a.copy()
+    b[0] = False
+    assert H.mask_drift(torch.tensor(a), torch.tensor(b)) == 0.25
+
+
+# -- end-to-end: the fused step against run_hierarchical goldens -------------------
+
+
+def _e2e_engines(M, P):
+    import paper_2512_14628_b200 as H
+
+    ref = G.E2E(M, P)
+    kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
+             "shape": H.ConstraintKind.SHAPE_KEEP}
+    layers = [H.LayerSpec(n, H.LayerKind.CONV if k == "conv" else H.LayerKind.FULLY_CONNECTED, shape,
+                          prunable=bool(c)) for n, k, shape, c in G.E2E_LAYERS]
+    cons = {n: [H.SparsityConstraint(kinds[g], keep_rate=r) for g, r in c] for n, _, _, c in G.E2E_LAYERS if c}
+    sched = H.PenaltySchedule.uniform(ref.names, G.E2E_RHO1, G.E2E_RHO2, adapt=False)
+    settings = H.ConsensusSettings(iterations=ref.iters, t_freeze=ref.t_freeze, weight_decay=G.E2E_WD)
+    cluster = H.LocalCluster(H.Topology(M, P))
+    engines = [H.HSADMMSync(r, cluster, layers, cons, sched, settings) for r in range(ref.world)]
+    for e in engines:
+        e.init_from(ref.p0())
+    return ref, cluster, engines
+
+
+@pytest.mark.parametrize("M,P", G.E2E_TOPOLOGIES)
+def test_end_to_end_against_reference_goldens(M, P):
+    import paper_2512_14628_b200 as H
+
+    ref, cluster, engines = _e2e_engines(M, P)
+    for k in range(1, ref.iters + 1):
+        for e in engines:
+            e.load(theta=ref.theta(k, e.rank))
+        n_before = len(cluster.ledger.entries)
+        H.run_local(engines, k)
+        for e in engines:
+            node = e.rank // P
+            assert e.frozen == ref.frozen(k, node)
+            for n, m in ref.masks(k, node).items():
+                assert np.array_equal(cpu(e.mask_dict()[n]), m), (k, e.rank, n)
+            th = ref.theta(k, e.rank)
+            for n in ref.names:
+                for key, want in (("z_node", ref.node_state("z_node", k, node)[n]),
+                                  ("v", ref.node_state("v", k, node)[n]),
+                                  ("z", ref.node_state("z", k, node)[n]),
+                                  ("u", ref.u(k, e.rank)[n])):
+                    got = cpu(e.views(key)[n])
+                    err = rel_err(got, want, th[n])
+                    assert err <= TOL, (k, e.rank, key, n, err)
+            if e.is_leader:
+                assert (e.cache_derive, e.cache_hits) == ref.cache(k, e.rank)
+        zs = [x.to_dict() for x in cluster.ledger.entries[n_before:] if x.label.startswith("z_sync")]
+        assert zs == ref.zsync(k)
+    # followers hold the leader's z / v / z_node bit-for-bit
+    for e in engines:
+        lead = engines[e.leader_rank]
+        for key in ("z_node", "v", "z"):
+            assert torch.equal(getattr(e, key), getattr(lead, key))
+
+
+# -- full-size stage-wise parity vs the oracle on identical inputs -------------------
+
+
+@pytest.mark.parametrize("model,keep", [("rn18_224", 0.4), ("rn50_224", 0.4)])
+def test_full_size_step_against_oracle(model, keep):
+    """One dynamic then one frozen iteration of RN18/RN50 at 1x1 on the GPU and
+    in the fp64 oracle from the same fp32 state: masks / keep sets bit-exact,
+    z_node / u / v / z within 1e-5."""
+    import paper_2512_14628_b200 as H
+    from paper_2512_14628_b200.synthetic import channel_keep_constraints, model_layers, synthetic_rank_state
+
+    layers = model_layers(model)
+    cons = channel_keep_constraints(layers, keep)
+    names = [ls.name for ls in layers]
+    sched = H.PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False)
+    settings = H.ConsensusSettings(t_freeze=2, weight_decay=1e-4)
+    cluster = H.LocalCluster(H.Topology(1, 1))
+    eng = H.HSADMMSync(0, cluster, layers, cons, sched, settings)
+    st = synthetic_rank_state(layers, 0, 1, seed=1)
+    eng.load(**st)
+    ocons = {n: [(O.CHANNEL, None, keep)] for n in cons}
+    olayers = O.make_layers([(ls.name, ls.shape) for ls in layers], ocons)
+    ost = O.init_rank_state(olayers, st["theta"], st["u"], st["z_node"], st["v"], st["z"])
+    rho1 = {n: 1.5e-3 for n in names}
+    rho2 = {n: 1.5e-4 for n in names}
+    for k in (1, 2):
+        # stage-wise: the oracle starts from the GPU's fp32 state of the previous iteration
+        for key in ("u", "v", "z", "z_node"):
+            setattr(ost, key, {n: cpu(t).astype(np.float64) for n, t in eng.views(key).items()})
+        ost.masks = {n: cpu(m) for n, m in eng.mask_dict().items()}
+        frozen_before = eng.frozen
+        H.run_local([eng], k)
+        O.cluster_sync(olayers, [ost], [st["theta"]], k, 1, 1, rho1, rho2, 1e-4, t_freeze=2)
+        assert eng.frozen == ost.frozen
+        gm = eng.mask_dict()
+        for n in ost.masks:
+            assert np.array_equal(cpu(gm[n]), ost.masks[n]), (k, n)
+        for key in ("z_node", "u", "v", "z"):
+            for n in names:
+                err = rel_err(cpu(eng.views(key)[n]), getattr(ost, key)[n], st["theta"][n])
+                assert err <= TOL, (k, key, n, err, frozen_before)
+    ratio = eng.payload_elements / sum(ls.elements for ls in layers)
+    assert 0.40 < ratio < 0.47     # leader bytes vs dense (0.428 / 0.450)
+
+
+def test_full_size_compaction_roundtrip_property():
+    """decompress(compress(x)) == x * rectangle on every layer of RN50 (size-independent check)."""
+    import paper_2512_14628_b200 as H
+    from paper_2512_14628_b200.synthetic import channel_keep_constraints, model_layers, synthetic_base
+
+    layers = model_layers("rn50_224")
+    cons = channel_keep_constraints(layers, 0.3)
+    names = [ls.name for ls in layers]
+    sched = H.PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False)
+    eng = H.HSADMMSync(0, H.LocalCluster(H.Topology(1, 1)), layers, cons, sched, H.ConsensusSettings())
+    base = synthetic_base(layers, seed=4)
+    eng.load(theta=base, z=base, z_node=base)
+    H.run_local([eng], 1)
+    pl = eng.plan
+    x = torch.randn(pl.arena, device="cuda")
+    flat = torch.zeros(pl.arena, device="cuda")
+    out = torch.zeros(pl.arena, device="cuda")
+    pl.compact_dual(None, None, x, None, flat)
+    pl.decompact_dual(flat, 1.0, None, None, out)
+    pos_out, pos_in = pl.keep_positions(x.device)
+    for i, ls in enumerate(layers):
+        xv, ov = pl.view(x, i), pl.view(out, i)
+        if i in pl.prunable:
+            ko = pos_out[pl.keep_offset(i, 0):pl.keep_offset(i, 0) + ls.shape[0]] >= 0
+            ki = pos_in[pl.keep_offset(i, 1):pl.keep_offset(i, 1) + ls.shape[1]] >= 0
+            rect = ko.view(-1, 1, 1, 1) & ki.view(1, -1, 1, 1)
+            assert torch.equal(ov, torch.where(rect, xv, torch.zeros_like(xv)))
+        else:
+            assert torch.equal(ov, xv)

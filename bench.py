@@ -1,0 +1,421 @@
+"""Benchmark of the H-SADMM synchronization step on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--model rn18_224] [--grouping MxP] [--keep 0.4]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+A step is one full dynamic H-SADMM sync iteration (SURVEY.md §3.2 phases 2-5u:
+intra all-reduce, candidate + fp64 group norms, top-k projection + masks,
+leader mask union, keep sets + one D2H, compaction fused with the intra dual,
+leader all-reduce of the compact buffer, broadcast, decompaction fused with
+the inter dual) on synthetic ResNet-shaped state resident in HBM. Default
+workload: BASELINE.json configs[1] — ResNet-18 224x224 shapes, 60% channel
+sparsity (keep 0.4), 1 B200. Groupings by N: 1x1, 1x2, 2x2, 2x4 (override
+with --grouping). Each rank holds a full replica: weak scaling.
+
+value = synced parameters x ranks / step time (Mparams/s); ms_per_step is
+the device time per step (CUDA events on the launching stream, max over
+ranks, L2 flushed between steps). ``--impl reference`` times the CPU oracle
+(oracle/hsadmm_oracle.py, the fp64 restatement of the reference's numpy
+path) on this host on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "H-SADMM sync step ms & HBM GB/s (frac of roofline) at 1/2/4/8 B200; leader bytes"
+UNIT = "Mparams/s"
+DEFAULT_GROUPING = {1: "1x1", 2: "1x2", 4: "2x2", 8: "2x4"}
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="rn18_224")
+    ap.add_argument("--grouping", default=None)
+    ap.add_argument("--keep", type=float, default=0.4)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def topology_for(n, grouping):
+    from paper_2512_14628_b200.transport import Topology
+
+    g = grouping or DEFAULT_GROUPING.get(n, f"{n}x1")
+    topo = Topology.parse(g)
+    if topo.world_size != n:
+        raise SystemExit(f"grouping {g} needs {topo.world_size} ranks, have {n}")
+    return topo
+
+
+def workload_config(args, topo, n):
+    from paper_2512_14628_b200.synthetic import model_layers
+
+    layers = model_layers(args.model)
+    N = sum(ls.elements for ls in layers)
+    return layers, N, {
+        "workload": f"{args.model} synthetic, H-SADMM sync (dynamic: norm, project, mask union, "
+                    f"compact, leader all-reduce, decompact), channel keep {args.keep}, "
+                    f"{topo.num_nodes}x{topo.accels_per_node} grouping",
+        "model": args.model, "grouping": f"{topo.num_nodes}x{topo.accels_per_node}",
+        "keep_rate": args.keep, "params_per_rank": N, "mode": "dynamic",
+        "l2": "flushed between timed steps (256 MiB write)", "ranks": n}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# -- clocks -------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                      "-i", ",".join(str(g) for g in self.gpus)],
+                                     capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.samples.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for name, val in zip(names, s[4:8]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# -- CPU oracle (reference arm and cpu_baseline) -------------------------------------
+
+
+def oracle_setup(layers, topo, keep, seed, max_elems=None):
+    """fp64 oracle states of every simulated rank for (a prefix of) the workload."""
+    import numpy as np
+
+    from oracle import hsadmm_oracle as O
+    from paper_2512_14628_b200.layers import LayerKind
+    from paper_2512_14628_b200.synthetic import synthetic_base, synthetic_rank_state
+
+    sample = layers
+    if max_elems is not None:
+        sample, tot = [], 0
+        for ls in layers:
+            if tot and tot + ls.elements > max_elems:
+                break
+            sample.append(ls)
+            tot += ls.elements
+    base = synthetic_base(sample, seed)
+    cons = {ls.name: [(O.CHANNEL, None, keep)] for ls in sample if ls.kind is LayerKind.CONV}
+    olayers = O.make_layers([(ls.name, ls.shape) for ls in sample], cons)
+    states, thetas = [], []
+    for r in range(topo.world_size):
+        st = synthetic_rank_state(sample, r, topo.accels_per_node, seed, base)
+        states.append(O.init_rank_state(olayers, st["theta"], st["u"], st["z_node"], st["v"], st["z"]))
+        thetas.append({n: a.astype(np.float64) for n, a in st["theta"].items()})
+    rho1 = {ls.name: 1.5e-3 for ls in sample}
+    rho2 = {ls.name: 1.5e-4 for ls in sample}
+    return O, olayers, states, thetas, rho1, rho2, sum(ls.elements for ls in sample)
+
+
+def oracle_step(ctx, topo, k):
+    O, olayers, states, thetas, rho1, rho2, _ = ctx
+    O.cluster_sync(olayers, states, thetas, k, topo.num_nodes, topo.accels_per_node, rho1, rho2, 1e-4,
+                   t_freeze=10**9, drift_window=0)
+
+
+def cpu_baseline(layers, topo, keep, seed, budget_s):
+    """Oracle port on this host: steps of the full N=1 workload until ~budget_s."""
+    ctx = oracle_setup(layers, topo, keep, seed)
+    times, k = [], 0
+    t_end = time.perf_counter() + budget_s
+    while True:
+        k += 1
+        t0 = time.perf_counter()
+        oracle_step(ctx, topo, k)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() >= t_end or k >= 30:
+            break
+    n = ctx[-1] * topo.world_size
+    t = statistics.median(times)
+    return {"value": n / t / 1e6, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(times)} dynamic sync steps of the full workload ({ctx[-1]} params x "
+                      f"{topo.world_size} simulated ranks), numpy fp64 single-threaded, median "
+                      f"{t * 1e3:.0f} ms/step, host {os.cpu_count()} cpus",
+            "ms_per_step": t * 1e3}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    n = args.gpus or world
+    if rank != 0:
+        return
+    topo = topology_for(n, args.grouping)
+    layers, N, config = workload_config(args, topo, n)
+    # size the per-step sample so W + K steps end within ~ref_budget_s
+    ctx = oracle_setup(layers, topo, args.keep, args.seed)
+    t0 = time.perf_counter()
+    oracle_step(ctx, topo, 1)
+    t_full = time.perf_counter() - t0
+    steps_total = args.warmup + args.steps
+    if t_full * steps_total > args.ref_budget_s:
+        frac = args.ref_budget_s / (t_full * steps_total)
+        ctx = oracle_setup(layers, topo, args.keep, args.seed, max_elems=max(1, int(N * frac)))
+    n_params = ctx[-1]
+    for k in range(1, args.warmup + 1):
+        oracle_step(ctx, topo, k)
+    times = []
+    for k in range(args.warmup + 1, steps_total + 1):
+        t0 = time.perf_counter()
+        oracle_step(ctx, topo, k)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    ms = total / len(times) * 1e3
+    value = n_params * topo.world_size / (total / len(times)) / 1e6
+    sample = (f"{'full workload' if n_params == N else f'layer prefix of {n_params} of {N} params'} per "
+              f"simulated rank, {topo.world_size} ranks serialized in one process (reference architecture)")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# -- the B200 arm ------------------------------------------------------------------------
+
+# algorithmic HBM bytes per launch; N = synced elements, n_c = conv
+# elements, Z = compact payload elements
+def algorithmic_bytes(kernel, N, n_c, Z, P):
+    return {
+        "K0_pack_theta_u": 12 * N,
+        "K1_candidate": (16 if P > 1 else 20) * N,     # read S,z,v (or theta,u,z,v), write z_node
+        "K3_project": 8 * n_c + n_c // 8,
+        "K6_compact_dual": 20 * N + 4 * Z,
+        "K6f_dual_intra": 16 * N,
+        "K7_decompact_dual": 16 * N + 4 * Z,
+    }.get(kernel)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_14628_b200 as H
+    from paper_2512_14628_b200 import _lib, plan as plan_mod
+    from paper_2512_14628_b200.synthetic import channel_keep_constraints, synthetic_base, synthetic_rank_state
+
+    world, rank, local = dist_env()
+    n = args.gpus or world
+    if n != world:
+        raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}: launch with torchrun --nproc-per-node {n}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    topo = topology_for(n, args.grouping)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        cluster = H.DistCluster(topo)
+    else:
+        cluster = H.LocalCluster(topo)
+    layers, N, config = workload_config(args, topo, n)
+    n_c = sum(ls.elements for ls in layers if ls.kind is H.LayerKind.CONV)
+    cons = channel_keep_constraints(layers, args.keep)
+    names = [ls.name for ls in layers]
+    sched = H.PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False)
+    settings = H.ConsensusSettings(t_freeze=10**9, drift_window=0, weight_decay=1e-4)
+    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, device=dev)
+    base = synthetic_base(layers, args.seed)
+    st = synthetic_rank_state(layers, rank, topo.accels_per_node, args.seed, base)
+    eng.load(**st)
+    theta_host = torch.empty(eng.plan.arena, dtype=torch.float32).pin_memory()
+    theta_host.copy_(eng.theta.cpu())
+    z_host = torch.empty(eng.plan.arena, dtype=torch.float32).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def run_step(k):
+        if world > 1:
+            return eng.step(k)
+        return H.run_local([eng], k)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def timed_steps(k0, nsteps, e2e=False, kernel_timer=None):
+        """Per-step device times (ms) with an L2 flush between steps."""
+        evs = []
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(nsteps):
+            flush.fill_(float(i))
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            plan_mod.TIMER = kernel_timer
+            if e2e:
+                eng.theta.copy_(theta_host, non_blocking=True)
+            run_step(k0 + i)
+            if e2e:
+                z_host.copy_(eng.z, non_blocking=True)
+            plan_mod.TIMER = None
+            e.record()
+            evs.append((s, e))
+        torch.cuda.synchronize()
+        barrier()
+        return [s.elapsed_time(e) for s, e in evs]
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    k = 0
+    for _ in range(args.warmup):
+        k += 1
+        run_step(k)
+    torch.cuda.synchronize()
+    # headline: dynamic steps, kernel events + clocks sampled during the timed region
+    timer = plan_mod.KernelTimer()
+    launches0 = _lib.launch_count()
+    with ClockSampler([local] if world == 1 else list(range(world))) as clocks:
+        times = timed_steps(k + 1, args.steps, kernel_timer=timer)
+    launches = _lib.launch_count() - launches0
+    k += args.steps
+    total_ms = max_over_ranks(sum(times))
+    ms = total_ms / args.steps
+    value = N * world / (ms / 1e3) / 1e6
+    Z = eng.payload_elements
+    kern = {name: statistics.mean(d) for name, d in timer.durations_ms().items()}
+    launches_per_kernel = {name: len(d) / args.steps for name, d in timer.durations_ms().items()}
+    # frozen steady state (after t_freeze: sealed keep sets, no projection / union)
+    eng.frozen = True
+    for _ in range(2):
+        k += 1
+        run_step(k)
+    ftimes = timed_steps(k + 1, args.steps)
+    k += args.steps
+    frozen_ms = max_over_ranks(sum(ftimes)) / args.steps
+    eng.frozen = False
+    # e2e through the public API with host buffers (H2D theta, D2H z every step)
+    etimes = timed_steps(k + 1, args.steps, e2e=True)
+    k += args.steps
+    e2e_ms = max_over_ranks(sum(etimes)) / args.steps
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    hbm, hbm_src = peaks()
+    cands = {kname: t for kname, t in kern.items() if algorithmic_bytes(kname, N, n_c, Z, topo.accels_per_node)}
+    top = max(cands, key=cands.get)
+    abytes = algorithmic_bytes(top, N, n_c, Z, topo.accels_per_node)
+    achieved = abytes / (kern[top] / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.model, {}).get(top)
+        except Exception:
+            traffic = None
+    kernels_out = {}
+    for kname, t in sorted(kern.items()):
+        ab = algorithmic_bytes(kname, N, n_c, Z, topo.accels_per_node)
+        kernels_out[kname] = {"us": round(t * 1e3, 2), "per_step": launches_per_kernel[kname]}
+        if ab:
+            kernels_out[kname]["gbs"] = round(ab / (t / 1e3) / 1e9, 1)
+            kernels_out[kname]["frac"] = round(ab / (t / 1e3) / 1e9 / hbm, 3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "algorithmic_bytes": abytes,
+                     "peak_source": hbm_src},
+        "e2e": {"value": N * world / (e2e_ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 4 * eng.plan.arena, "d2h_bytes_per_step": 4 * eng.plan.arena,
+                "path": "HSADMMSync.program via the C ABI; pinned-host theta H2D + z D2H inside the timed region"},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clocks.summary(),
+        "frozen_ms_per_step": frozen_ms,
+        "leader_bytes": {"z_sync_bytes": 4 * Z, "dense_bytes": 4 * N, "ratio_vs_dense": Z / N},
+        "kernels": kernels_out,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(layers, topo, args.keep, args.seed, args.cpu_budget_s)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

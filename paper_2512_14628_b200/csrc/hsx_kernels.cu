@@ -38,7 +38,11 @@ __device__ __forceinline__ void f4set(float4& v, int i, float x) {
 // (rho1 * s + rho2 * (z - v)) / gamma with s = sum or theta + u.
 __device__ __forceinline__ double cand_of(double s, double z, double v, const DevLayer& ly,
                                           int identity) {
-  return identity ? s : (ly.rho1 * s + ly.rho2 * (z - v)) / ly.gamma;
+  // explicit _rn intrinsics: no FMA contraction, so the fp64 value is bit-identical
+  // to numpy's evaluation of the same expression
+  if (identity) return s;
+  double num = __dadd_rn(__dmul_rn(ly.rho1, s), __dmul_rn(ly.rho2, __dsub_rn(z, v)));
+  return __ddiv_rn(num, ly.gamma);
 }
 
 struct In4 {
@@ -59,14 +63,14 @@ __device__ __forceinline__ In4 load_in4(const CandArgs& p, long long gi, int ide
 }
 
 __device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, const DevLayer& ly) {
-  double s = p.s ? (double)p.s[gi] : (double)p.theta[gi] + (double)p.u[gi];
+  double s = p.s ? (double)p.s[gi] : __dadd_rn((double)p.theta[gi], (double)p.u[gi]);
   if (p.identity) return s;
   return cand_of(s, (double)p.z[gi], (double)p.v[gi], ly, 0);
 }
 
 __device__ __forceinline__ double cand4(const In4& x, int i, const DevLayer& ly, int has_s,
                                         int identity) {
-  double s = has_s ? (double)f4get(x.a, i) : (double)f4get(x.a, i) + (double)f4get(x.b, i);
+  double s = has_s ? (double)f4get(x.a, i) : __dadd_rn((double)f4get(x.a, i), (double)f4get(x.b, i));
   return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), ly, identity);
 }
 
@@ -174,7 +178,7 @@ __device__ void cand_tile(const CandArgs& p, const DevLayer& ly, const Item& it,
             double c = cand4(in[uu], i, ly, p.s != nullptr, p.identity);
             if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + 4 * q + i)) c = 0.0;
             f4set(out, i, (float)c);
-            sq[4 * q + i] = c * c;
+            sq[4 * q + i] = __dmul_rn(c, c);
           }
           if (pass == 0) st4(p.zn + gbase + 4 * q, out);
         }
@@ -184,7 +188,7 @@ __device__ void cand_tile(const CandArgs& p, const DevLayer& ly, const Item& it,
         double c = cand_elem(p, gbase + i, ly);
         if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
         if (pass == 0) p.zn[gbase + i] = (float)c;
-        sq[i] = c * c;
+        sq[i] = __dmul_rn(c, c);
       }
     }
     __syncthreads();

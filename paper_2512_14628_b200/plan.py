@@ -8,6 +8,7 @@ bit per element of each prunable layer.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 
 import torch
@@ -19,6 +20,38 @@ from .layers import GROUP_CODE, GroupBy, LayerKind, LayerSpec
 
 def current_stream() -> int:
     return torch.cuda.current_stream().cuda_stream
+
+
+class KernelTimer:
+    """CUDA-event timing of libhsx calls and collectives on the launching stream."""
+
+    def __init__(self):
+        self.events: dict[str, list] = {}
+
+    @contextlib.contextmanager
+    def __call__(self, name: str):
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        try:
+            yield
+        finally:
+            e.record()
+            self.events.setdefault(name, []).append((s, e))
+
+    def durations_ms(self) -> dict[str, list[float]]:
+        torch.cuda.synchronize()
+        return {k: [s.elapsed_time(e) for s, e in v] for k, v in self.events.items()}
+
+    def reset(self):
+        self.events.clear()
+
+
+TIMER: KernelTimer | None = None
+
+
+def timed(name: str):
+    return TIMER(name) if TIMER is not None else contextlib.nullcontext()
 
 
 def ptr(t) -> int | None:
@@ -152,21 +185,26 @@ class Plan:
 
     # -- kernels (thin wrappers; all on the current stream) ---------------------
     def pack_theta_u(self, theta, u, send):
-        _lib.call("hsx_pack_theta_u", self._h, ptr(theta), ptr(u), ptr(send), current_stream())
+        with timed("K0_pack_theta_u"):
+            _lib.call("hsx_pack_theta_u", self._h, ptr(theta), ptr(u), ptr(send), current_stream())
 
     def candidate(self, s, theta, u, z, v, z_node, frozen_mask=None):
-        _lib.call("hsx_candidate", self._h, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v), ptr(z_node),
-                  ptr(frozen_mask), current_stream())
+        with timed("K1_candidate"):
+            _lib.call("hsx_candidate", self._h, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v), ptr(z_node),
+                      ptr(frozen_mask), current_stream())
 
     def renorm(self, p, s, theta, u, z, v):
-        _lib.call("hsx_candidate_renorm", self._h, p, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v),
-                  current_stream())
+        with timed("K1r_renorm"):
+            _lib.call("hsx_candidate_renorm", self._h, p, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v),
+                      current_stream())
 
     def select(self, p):
-        _lib.call("hsx_select", self._h, p, current_stream())
+        with timed("K2_select"):
+            _lib.call("hsx_select", self._h, p, current_stream())
 
     def project(self, z_node, local_mask):
-        _lib.call("hsx_project", self._h, ptr(z_node), ptr(local_mask), current_stream())
+        with timed("K3_project"):
+            _lib.call("hsx_project", self._h, ptr(z_node), ptr(local_mask), current_stream())
 
     def project_all(self, s, theta, u, z, v, z_node, local_mask):
         """K2 (+ composite passes) + K3 after hsx_candidate."""
@@ -187,7 +225,8 @@ class Plan:
         return int(self._lib.hsx_plan_group_offset(self._h, i, p))
 
     def keep_sets(self, union_mask, prev_mask=None):
-        _lib.call("hsx_keep_sets", self._h, ptr(union_mask), ptr(prev_mask), current_stream())
+        with timed("K5_keep_sets"):
+            _lib.call("hsx_keep_sets", self._h, ptr(union_mask), ptr(prev_mask), current_stream())
 
     def keep_sets_fetch(self):
         """D2H of the per-layer summary; synchronizes the current stream."""
@@ -218,16 +257,20 @@ class Plan:
                   C.cast(ki, C.c_void_p), len(k_in))
 
     def compact_dual(self, theta, u, z_node, v, flat):
-        _lib.call("hsx_compact_dual", self._h, ptr(theta), ptr(u), ptr(z_node), ptr(v), ptr(flat),
-                  current_stream())
+        with timed("K6_compact_dual"):
+            _lib.call("hsx_compact_dual", self._h, ptr(theta), ptr(u), ptr(z_node), ptr(v), ptr(flat),
+                      current_stream())
 
     def dual_intra(self, theta, u, z_node):
-        _lib.call("hsx_dual_intra", self._h, ptr(theta), ptr(u), ptr(z_node), current_stream())
+        with timed("K6f_dual_intra"):
+            _lib.call("hsx_dual_intra", self._h, ptr(theta), ptr(u), ptr(z_node), current_stream())
 
     def decompact_dual(self, flat, divisor, z_node, v, z):
-        _lib.call("hsx_decompact_dual", self._h, ptr(flat), float(divisor), ptr(z_node), ptr(v),
-                  ptr(z), current_stream())
+        with timed("K7_decompact_dual"):
+            _lib.call("hsx_decompact_dual", self._h, ptr(flat), float(divisor), ptr(z_node), ptr(v),
+                      ptr(z), current_stream())
 
 
 def mask_or(gathered, n_ranks: int, words: int, out):
-    _lib.call("hsx_mask_or", ptr(gathered), int(n_ranks), int(words), ptr(out), current_stream())
+    with timed("K4_mask_or"):
+        _lib.call("hsx_mask_or", ptr(gathered), int(n_ranks), int(words), ptr(out), current_stream())

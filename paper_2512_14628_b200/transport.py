@@ -419,9 +419,15 @@ class DistCluster:
         return self._global
 
     def execute(self, req) -> Any:
-        import torch.distributed as dist
+        from .plan import timed
 
         _validate(self.rank, req)
+        with timed("C:" + req.tag.split("/")[0]):
+            return self._execute(req)
+
+    def _execute(self, req) -> Any:
+        import torch.distributed as dist
+
         h = self._handles[req.group.id]
         g = len(req.group.members)
         if isinstance(req, Broadcast):

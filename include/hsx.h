@@ -154,6 +154,11 @@ int hsx_keep_sets(hsx_plan* plan, const uint32_t* union_mask, const uint32_t* pr
 /* D2H of the per-layer summary (n_layers x HSX_SUM_COLS int64, then 1 int64
  * total payload elements) into host memory; synchronizes `stream`. */
 int hsx_keep_sets_fetch(hsx_plan* plan, int64_t* host_summary, void* stream);
+/* Same copy without the synchronization: the caller records an event on
+ * `stream` and waits on it before reading host_summary (lets the compaction
+ * kernel run while the host sizes the leader all-reduce). Does not refresh
+ * the plan's host mirror used by hsx_set_keep_sets. */
+int hsx_keep_sets_fetch_async(hsx_plan* plan, int64_t* host_summary, void* stream);
 /* Install keep sets from host index lists (KeepSetCache hit path / per-tensor
  * compress): k_out/k_in sorted ascending, lengths n_out/n_in. Recomputes the
  * flat-buffer offsets of every layer. */

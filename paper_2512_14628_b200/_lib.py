@@ -57,6 +57,7 @@ SIGNATURES = {
     "hsx_mask_or": (C.c_int, [VP, I32, I64, VP, VP]),
     "hsx_keep_sets": (C.c_int, [P, VP, VP, VP]),
     "hsx_keep_sets_fetch": (C.c_int, [P, VP, VP]),
+    "hsx_keep_sets_fetch_async": (C.c_int, [P, VP, VP]),
     "hsx_set_keep_sets": (C.c_int, [P, I32, VP, I32, VP, I32]),
     "hsx_read_keep_positions": (C.c_int, [P, I32, VP, VP]),
     "hsx_compact_dual": (C.c_int, [P, VP, VP, VP, VP, VP, VP]),

@@ -48,7 +48,7 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 constexpr long long kAlign = 32;        // arena layer alignment in elements (128 B)
 constexpr int kSubElems = 4096;         // target elements per shared-memory sub-tile
 constexpr long long kItemElems = 8192;  // elements per streaming work item
-constexpr long long kWordItem = 4096;   // mask words per keep-mark item
+constexpr long long kWordItem = 512;    // mask words per keep-mark item
 constexpr int kMaxSelectGroups = 8192;  // bitonic capacity (96 KB smem)
 constexpr size_t kMaxSmem = 200 * 1024;
 
@@ -508,6 +508,13 @@ int hsx_keep_sets_fetch(hsx_plan* p, int64_t* host_summary, void* stream) {
   HSX_CUDA(cudaMemcpyAsync(host_summary, p->d_summary, bytes, cudaMemcpyDeviceToHost, S(stream)));
   HSX_CUDA(cudaStreamSynchronize(S(stream)));
   std::memcpy(p->summary.data(), host_summary, bytes);
+  return HSX_OK;
+}
+
+int hsx_keep_sets_fetch_async(hsx_plan* p, int64_t* host_summary, void* stream) {
+  if (!p || !host_summary) return fail(HSX_EINVAL, "null argument");
+  HSX_CUDA(cudaMemcpyAsync(host_summary, p->d_summary, p->summary.size() * sizeof(long long),
+                           cudaMemcpyDeviceToHost, S(stream)));
   return HSX_OK;
 }
 

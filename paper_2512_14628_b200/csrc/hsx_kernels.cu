@@ -262,21 +262,42 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
   while (Gp < G) Gp <<= 1;
   int* sidx = reinterpret_cast<int*>(skey + Gp);
   const bool rowwise = ly.group[pass] == kFilter;
-  for (int g = threadIdx.x; g < Gp; g += blockDim.x) {
-    double key = -1.0;  // padding sorts after every norm (norms >= 0)
-    if (g < G) {
-      double s2;
-      if (rowwise) {
-        s2 = partials[ly.poff[pass] + g];
-      } else {
-        s2 = 0.0;
-        for (int pt = 0; pt < ly.nparts; ++pt) s2 += partials[ly.poff[pass] + (long long)pt * G + g];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (rowwise || ly.nparts < 8) {
+    for (int g = threadIdx.x; g < Gp; g += blockDim.x) {
+      double key = -1.0;  // padding sorts after every norm (norms >= 0)
+      if (g < G) {
+        double s2;
+        if (rowwise) {
+          s2 = partials[ly.poff[pass] + g];
+        } else {
+          s2 = 0.0;
+          for (int pt = 0; pt < ly.nparts; ++pt) s2 += partials[ly.poff[pass] + (long long)pt * G + g];
+        }
+        key = sqrt(s2);
+        norms[ly.goff[pass] + g] = key;
       }
-      key = sqrt(s2);
-      norms[ly.goff[pass] + g] = key;
+      skey[g] = key;
+      sidx[g] = g;
     }
-    skey[g] = key;
-    sidx[g] = g;
+  } else {
+    // many row tiles: one warp per group, lanes stride the parts, fixed shuffle tree
+    for (int g = warp; g < Gp; g += nwarps) {
+      double s2 = 0.0;
+      if (g < G)
+        for (int pt = lane; pt < ly.nparts; pt += 32) s2 += partials[ly.poff[pass] + (long long)pt * G + g];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s2 += __shfl_xor_sync(kFull, s2, off);
+      if (lane == 0) {
+        double key = -1.0;
+        if (g < G) {
+          key = sqrt(s2);
+          norms[ly.goff[pass] + g] = key;
+        }
+        skey[g] = key;
+        sidx[g] = g;
+      }
+    }
   }
   __syncthreads();
   for (int size = 2; size <= Gp; size <<= 1) {
@@ -532,16 +553,44 @@ __global__ void __launch_bounds__(1024) k_keep_scan(const DevLayer* __restrict__
     last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    long long off = 0;
-    for (int i = 0; i < n_layers; ++i) {
-      volatile long long* row = summary + (long long)i * kSumCols;
-      long long e = row[2];
-      row[3] = off;
-      off += e;
+  if (!last) return;
+  __threadfence();
+  // flat-buffer layout: exclusive scan of payload sizes over all layers, in layer order
+  __shared__ long long wsum[32];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < n_layers; base += blockDim.x) {
+    int i = base + threadIdx.x;
+    volatile long long* row = summary + (long long)i * kSumCols;
+    long long e = i < n_layers ? row[2] : 0;
+    long long incl = e;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      long long y = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += y;
     }
-    summary[(long long)n_layers * kSumCols] = off;
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      long long t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0, ti = t;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        long long y = __shfl_up_sync(kFull, ti, off);
+        if (lane >= off) ti += y;
+      }
+      wsum[lane] = ti - t;
+    }
+    __syncthreads();
+    long long ex = carry + wsum[warp] + incl - e;
+    if (i < n_layers) row[3] = ex;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = ex + e;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    summary[(long long)n_layers * kSumCols] = carry;
     *done = 0;
   }
 }

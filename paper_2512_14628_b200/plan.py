@@ -233,6 +233,19 @@ class Plan:
         _lib.call("hsx_keep_sets_fetch", self._h, self.summary_host.data_ptr(), current_stream())
         return self.summary_host.view(-1)
 
+    def keep_sets_fetch_async(self):
+        """Enqueue the D2H of the summary; returns a CUDA event to wait on."""
+        _lib.call("hsx_keep_sets_fetch_async", self._h, self.summary_host.data_ptr(), current_stream())
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev
+
+    def summary_np(self):
+        """(per-layer rows as a zero-copy numpy view, total payload elements)."""
+        a = self.summary_host.numpy()
+        n = len(self.names)
+        return a[: n * _lib.SUM_COLS].reshape(n, _lib.SUM_COLS), int(a[n * _lib.SUM_COLS])
+
     def summary_rows(self):
         s = self.summary_host
         n = len(self.names)

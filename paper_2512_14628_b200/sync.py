@@ -32,6 +32,7 @@ on the device.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from .consensus import ConsensusSettings, PenaltySchedule, freeze_check
@@ -90,6 +91,10 @@ class HSADMMSync:
         self.cache_seen = False
         self.payload_elements = sum(ls.elements for ls in self.layers)  # all kept initially
         self.buckets = None
+        self._elems = None
+        self._prunable_idx = np.array(self.prunable, dtype=np.int64)
+        self._prunable_names = [self.names[i] for i in self.prunable]
+        self._prunable_elems = np.array([self.layers[i].elements for i in self.prunable], dtype=np.float64)
         self._layout_from_summary(initial=True)
 
     # -- state I/O ---------------------------------------------------------------
@@ -113,14 +118,32 @@ class HSADMMSync:
     # -- layout of the flat compact buffer -------------------------------------------
     def _layout_from_summary(self, initial=False):
         if initial:
-            sizes = [(ls.name, ls.elements) for ls in self.layers]
+            elems = np.array([ls.elements for ls in self.layers], dtype=np.int64)
         else:
-            rows, total = self.plan.summary_rows()
-            sizes = [(self.names[i], int(rows[i, _lib.SUM_ELEMS])) for i in range(len(self.names))]
+            rows, total = self.plan.summary_np()
+            elems = rows[:, _lib.SUM_ELEMS]
             self.payload_elements = total
+        if self._elems is not None and np.array_equal(elems, self._elems):
+            return                                   # same sizes: reuse the bucket layout
+        self._elems = elems.copy()
         # layers whose kept rectangle is empty are not sent (consensus.py:480)
-        self.payload = [(n, e) for n, e in sizes if e > 0]
+        self.payload = [(n, int(e)) for n, e in zip(self.names, elems) if e > 0]
         self.buckets = bucketize(self.payload)
+
+    def _after_keep_sets(self):
+        """Host bookkeeping once the per-layer counts have landed (no device work)."""
+        self._layout_from_summary()
+        rows, _ = self.plan.summary_np()
+        pr = self._prunable_idx
+        drift_bits = rows[pr, _lib.SUM_DRIFT]
+        drift = drift_bits / self._prunable_elems
+        self.drift_now = dict(zip(self._prunable_names, drift.tolist()))
+        self.drift_history.append(float(drift.max()))
+        if self.is_leader:                              # KeepSetCache counters (shrinkage.py:115-130)
+            derive = len(pr) if not self.cache_seen else int(np.count_nonzero(drift_bits))
+            self.cache_derive += derive
+            self.cache_hits += len(pr) - derive
+            self.cache_seen = True
 
     @property
     def leader_bytes(self) -> int:
@@ -147,42 +170,36 @@ class HSADMMSync:
             pl.dual_intra(self.theta, self.u, self.z_node)
             return None
         # phase 4: mask union (leaders), broadcast to followers, keep sets
+        ev = None
         if dynamic:
             if self.is_leader:
                 if self.M > 1:
-                    yield AllGather(self.inter, self.local_mask, self.gathered, f"mask_sync", k)
+                    yield AllGather(self.inter, self.local_mask, self.gathered, "mask_sync", k)
                     mask_or(self.gathered, self.M, pl.mask_words, self.union)
                 else:
                     self.union, self.local_mask = self.local_mask, self.union
             if self.P > 1:
                 yield Broadcast(self.intra, self.leader_rank, self.union, "m_bcast", k)
             pl.keep_sets(self.union, self.masks)
-            pl.keep_sets_fetch()                        # the one D2H of the dynamic step
-            self._layout_from_summary()
-            rows, _ = pl.summary_rows()
-            self.drift_now = {self.names[i]: int(rows[i, _lib.SUM_DRIFT]) / self.layers[i].elements
-                              for i in self.prunable}
-            self.drift_history.append(max(self.drift_now.values()))
-            if self.is_leader:                          # KeepSetCache counters (shrinkage.py:115-130)
-                changed = sum(1 for i in self.prunable if rows[i, _lib.SUM_DRIFT] > 0)
-                derive = len(self.prunable) if not self.cache_seen else changed
-                self.cache_derive += derive
-                self.cache_hits += len(self.prunable) - derive
-                self.cache_seen = True
+            ev = pl.keep_sets_fetch_async()             # the one D2H of the dynamic step
         elif self.is_leader and self.prunable:
             self.cache_hits += len(self.prunable)
-        # compaction fused with the intra dual update; leader average; broadcast
-        total = self.payload_elements
-        flat = self.flat[:total]
+        # compaction fused with the intra dual update (K6 reads sizes on device, so
+        # it runs while the host waits for the D2H and sizes the collectives)
         if self.is_leader:
             pl.compact_dual(self.theta, self.u, self.z_node, self.v, self.flat)
+        else:
+            pl.dual_intra(self.theta, self.u, self.z_node)
+        if ev is not None:
+            ev.synchronize()
+            self._after_keep_sets()
+        total = self.payload_elements
+        if self.is_leader:
             for bi, b in enumerate(self.buckets):
                 yield AllReduce(self.inter, self.flat[b.start:b.start + b.elements], ReduceOp.AVG,
                                 f"z_sync/b{bi}", k, detail=b.detail)
-        else:
-            pl.dual_intra(self.theta, self.u, self.z_node)
         if self.P > 1 and total > 0:
-            yield Broadcast(self.intra, self.leader_rank, flat, "zhat_bcast", k)
+            yield Broadcast(self.intra, self.leader_rank, self.flat[:total], "zhat_bcast", k)
         pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
         if dynamic:
             self.masks, self.union = self.union, self.masks

@@ -373,6 +373,9 @@ class LocalCluster:
                     q.out[i].copy_(posted[r].payload)
             _ledger(self.ledger, first, g, _payload_bytes(first.payload), "allgather")
             return {r: posted[r].out for r in group.members}
+        if g == 1:                               # identity: nothing moves
+            _ledger(self.ledger, first, g, _payload_bytes(first.payload), f"allreduce_{first.op.value}")
+            return {first.group.members[0]: first.payload}
         acc = reqs[0].payload.clone()            # serial fold in member order
         for q in reqs[1:]:
             acc += q.payload

@@ -48,6 +48,7 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 constexpr long long kAlign = 32;        // arena layer alignment in elements (128 B)
 constexpr int kSubElems = 4096;         // target elements per shared-memory sub-tile
 constexpr long long kItemElems = 8192;  // elements per streaming work item
+constexpr long long kNormItemElems = 16384;  // minimum elements per group-norm row tile
 constexpr long long kWordItem = 512;    // mask words per keep-mark item
 constexpr int kMaxSelectGroups = 8192;  // bitonic capacity (96 KB smem)
 constexpr size_t kMaxSmem = 200 * 1024;
@@ -81,15 +82,17 @@ struct hsx_plan {
   long long gtotal[hsx::kMaxPasses] = {0, 0, 0};
   long long ptotal[hsx::kMaxPasses] = {0, 0, 0};
   long long ktotal[2] = {0, 0};
+  long long ctotal = 0;  // column-map entries (sum of L over prunable layers, padded to 4)
   std::vector<DevLayer> layers;
-  std::vector<Item> cand_items, elem_items, proj_items, word_items;
+  std::vector<Item> cand_dense, cand_norm, elem_items, proj_items, word_items;
   std::vector<int> pass_list[hsx::kMaxPasses];
   std::vector<int> prunable;
   size_t cand_smem = 0, select_smem[hsx::kMaxPasses] = {0, 0, 0}, mark_smem = 0;
   int sqcap = 0;
   // device
   DevLayer* d_layers = nullptr;
-  Item *d_cand = nullptr, *d_elem = nullptr, *d_proj = nullptr, *d_word = nullptr;
+  Item *d_cand = nullptr, *d_cand_norm = nullptr, *d_elem = nullptr, *d_proj = nullptr,
+       *d_word = nullptr;
   int* d_pass[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
   double* d_partials[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
@@ -97,13 +100,15 @@ struct hsx_plan {
   uint8_t* d_flags[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   uint8_t *d_oflag = nullptr, *d_iflag = nullptr;
   int *d_pos_out = nullptr, *d_pos_in = nullptr;
+  hsx::Maps maps = {nullptr, nullptr, nullptr, nullptr};
   long long* d_summary = nullptr;
   unsigned int* d_done = nullptr;
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_layers, d_cand, d_elem, d_proj, d_word, d_prunable, d_oflag, d_iflag,
-                    d_pos_out, d_pos_in, d_summary, d_done};
+    void* ptrs[] = {d_layers, d_cand, d_cand_norm, d_elem, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+                    d_pos_out, d_pos_in, d_summary, d_done, maps.rowkeep, maps.colkeep,
+                    maps.rowbase, maps.colpos};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (int i = 0; i < hsx::kMaxPasses; ++i) {
@@ -130,9 +135,9 @@ void host_layout(hsx_plan* p) {
 
 int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   p->n_layers = n;
-  long long off = 0, mword = 0, okeep = 0, ikeep = 0;
+  long long off = 0, mword = 0, okeep = 0, ikeep = 0, cpoff = 0;
   long long goff[hsx::kMaxPasses] = {0, 0, 0}, poff[hsx::kMaxPasses] = {0, 0, 0};
-  int sqcap = 0, gmax = 0;
+  int sqcap = 0, gmax = 0, quadcap = 0;
   size_t mark_smem = 0;
   p->summary.assign((size_t)n * HSX_SUM_COLS + 1, 0);
   for (int l = 0; l < n; ++l) {
@@ -157,7 +162,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     ly.rho2 = d.rho2;
     ly.gamma = 1.0;
     ly.mword = -1;
-    ly.okeep = ly.ikeep = -1;
+    ly.okeep = ly.ikeep = ly.cpoff = -1;
     for (int q = 0; q < hsx::kMaxPasses; ++q) ly.goff[q] = ly.poff[q] = -1;
     if (d.n_constraints < 0 || d.n_constraints > HSX_MAX_CONSTRAINTS)
       return fail(HSX_ESHAPE, "layer %d: %d constraints (max %d)", l, d.n_constraints, HSX_MAX_CONSTRAINTS);
@@ -182,11 +187,12 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       }
       ly.rsub = std::max(1, kSubElems / ly.L);
       sqcap = std::max(sqcap, ly.rsub * ly.L);
+      quadcap = std::max(quadcap, std::max(ly.L, 1024));
       // rows per candidate item: >= 8K elements and partials <= ~1/16 of the item's bytes
       int gch = 0;
       for (int q = 0; q < ly.ncons; ++q)
         if (ly.group[q] != HSX_GROUP_FILTER) gch = std::max(gch, ly.G[q]);
-      long long rows_item = std::max<long long>((kItemElems + ly.L - 1) / ly.L, (16LL * gch + ly.L - 1) / ly.L);
+      long long rows_item = std::max<long long>((kNormItemElems + ly.L - 1) / ly.L, (16LL * gch + ly.L - 1) / ly.L);
       rows_item = (rows_item + ly.rsub - 1) / ly.rsub * ly.rsub;
       rows_item = std::min<long long>(rows_item, ly.rows);
       ly.nparts = (int)((ly.rows + rows_item - 1) / rows_item);
@@ -196,7 +202,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         it.part = pt;
         it.begin = pt * rows_item * ly.L;
         it.end = std::min<long long>((pt + 1) * rows_item, ly.rows) * ly.L;
-        p->cand_items.push_back(it);
+        p->cand_norm.push_back(it);
       }
       for (int q = 0; q < ly.ncons; ++q) {
         ly.goff[q] = goff[q];
@@ -212,6 +218,8 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       okeep += ly.rows;
       ly.ikeep = ikeep;
       ikeep += ly.cin;
+      ly.cpoff = cpoff;
+      cpoff += (ly.L + 3) / 4 * 4;
       p->prunable.push_back(l);
       for (long long b = 0; b < ly.n; b += kItemElems) {
         Item it{l, 0, b, std::min(ly.n, b + kItemElems)};
@@ -226,7 +234,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     } else {
       for (long long b = 0; b < ly.n; b += kItemElems) {
         Item it{l, 0, b, std::min(ly.n, b + kItemElems)};
-        p->cand_items.push_back(it);
+        p->cand_dense.push_back(it);
       }
     }
     for (long long b = 0; b < ly.n; b += kItemElems) {
@@ -245,6 +253,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   p->mask_words = mword;
   p->ktotal[0] = okeep;
   p->ktotal[1] = ikeep;
+  p->ctotal = cpoff;
   for (int q = 0; q < hsx::kMaxPasses; ++q) {
     p->gtotal[q] = goff[q];
     p->ptotal[q] = poff[q];
@@ -253,10 +262,10 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       int G = p->layers[l].G[q];
       while (gp < G) gp <<= 1;
     }
-    p->select_smem[q] = (size_t)gp * (sizeof(double) + sizeof(int));
+    p->select_smem[q] = (size_t)gp * (sizeof(double) + sizeof(int)) + 8 + 1024 * sizeof(double);
   }
   p->sqcap = sqcap;
-  p->cand_smem = (size_t)(sqcap + gmax) * sizeof(double);
+  p->cand_smem = (size_t)std::max(sqcap + gmax, quadcap) * sizeof(double);
   p->mark_smem = mark_smem;
   if (p->cand_smem > kMaxSmem) return fail(HSX_ESHAPE, "candidate tile needs %zu B of shared memory", p->cand_smem);
   host_layout(p);
@@ -266,7 +275,8 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
 int upload_plan(hsx_plan* p) {
   int rc;
   if ((rc = upload(&p->d_layers, p->layers))) return rc;
-  if ((rc = upload(&p->d_cand, p->cand_items))) return rc;
+  if ((rc = upload(&p->d_cand, p->cand_dense))) return rc;
+  if ((rc = upload(&p->d_cand_norm, p->cand_norm))) return rc;
   if ((rc = upload(&p->d_elem, p->elem_items))) return rc;
   if ((rc = upload(&p->d_proj, p->proj_items))) return rc;
   if ((rc = upload(&p->d_word, p->word_items))) return rc;
@@ -288,6 +298,17 @@ int upload_plan(hsx_plan* p) {
   }
   if ((rc = upload(&p->d_pos_out, po))) return rc;
   if ((rc = upload(&p->d_pos_in, pi))) return rc;
+  std::vector<int> rb(p->ktotal[0]), cp(p->ctotal, -1);
+  std::vector<uint8_t> ones_r(p->ktotal[0], 1), ones_c(p->ctotal, 1);
+  for (int l : p->prunable) {
+    const DevLayer& ly = p->layers[l];
+    for (int i = 0; i < ly.rows; ++i) rb[ly.okeep + i] = i * ly.L;
+    for (int i = 0; i < ly.L; ++i) cp[ly.cpoff + i] = i;
+  }
+  if ((rc = upload(&p->maps.rowbase, rb))) return rc;
+  if ((rc = upload(&p->maps.colpos, cp))) return rc;
+  if ((rc = upload(&p->maps.rowkeep, ones_r))) return rc;
+  if ((rc = upload(&p->maps.colkeep, ones_c))) return rc;
   if ((rc = upload(&p->d_summary, p->summary))) return rc;
   if ((rc = alloc0(&p->d_done, 1))) return rc;
   return HSX_OK;
@@ -425,7 +446,8 @@ int hsx_candidate(hsx_plan* p, const float* sum, const float* theta, const float
   a.fmask = frozen_mask;
   a.pass = 0;
   a.partials = p->d_partials[0];
-  hsx::launch_candidate(a, (int)p->cand_items.size(), frozen_mask != nullptr, p->cand_smem, S(stream));
+  hsx::launch_candidate(a, p->d_cand, (int)p->cand_dense.size(), p->d_cand_norm,
+                        (int)p->cand_norm.size(), frozen_mask != nullptr, p->cand_smem, S(stream));
   HSX_LAUNCHED("candidate");
   return HSX_OK;
 }
@@ -439,7 +461,8 @@ int hsx_candidate_renorm(hsx_plan* p, int32_t pass, const float* sum, const floa
   a.pass = pass;
   a.partials = p->d_partials[pass];
   for (int q = 0; q < pass; ++q) a.flags[q] = p->d_flags[q];
-  hsx::launch_candidate(a, (int)p->cand_items.size(), 0, p->cand_smem, S(stream));
+  hsx::launch_candidate(a, p->d_cand, 0, p->d_cand_norm, (int)p->cand_norm.size(), 0, p->cand_smem,
+                        S(stream));
   HSX_LAUNCHED("candidate_renorm");
   return HSX_OK;
 }
@@ -468,8 +491,11 @@ int hsx_read_groups(const hsx_plan* p, int32_t pass, double* norms, uint8_t* fla
 
 int hsx_project(hsx_plan* p, float* z_node, uint32_t* local_mask, void* stream) {
   if (!p || !z_node || (!local_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
-  hsx::launch_project(p->d_layers, p->d_proj, (int)p->proj_items.size(), z_node, local_mask,
-                      p->d_flags[0], p->d_flags[1], p->d_flags[2], S(stream));
+  hsx::launch_keepmaps(p->d_layers, p->d_prunable, (int)p->prunable.size(), p->d_flags[0],
+                       p->d_flags[1], p->d_flags[2], p->maps, S(stream));
+  HSX_LAUNCHED("keepmaps");
+  hsx::launch_project(p->d_layers, p->d_proj, (int)p->proj_items.size(), z_node, local_mask, p->maps,
+                      S(stream));
   HSX_LAUNCHED("project");
   return HSX_OK;
 }
@@ -496,7 +522,7 @@ int hsx_keep_sets(hsx_plan* p, const uint32_t* union_mask, const uint32_t* prev_
                         p->d_oflag, p->d_iflag, p->d_summary, p->mark_smem, st);
   HSX_LAUNCHED("keep_mark");
   hsx::launch_keep_scan(p->d_layers, p->d_prunable, (int)p->prunable.size(), p->n_layers,
-                        p->d_oflag, p->d_iflag, p->d_pos_out, p->d_pos_in, p->d_summary,
+                        p->d_oflag, p->d_iflag, p->d_pos_out, p->d_pos_in, p->maps, p->d_summary,
                         p->d_done, st);
   HSX_LAUNCHED("keep_scan");
   return HSX_OK;
@@ -538,6 +564,14 @@ int hsx_set_keep_sets(hsx_plan* p, int32_t l, const int32_t* k_out, int32_t n_ou
   }
   HSX_CUDA(cudaMemcpy(p->d_pos_out + ly.okeep, po.data(), po.size() * sizeof(int), cudaMemcpyHostToDevice));
   HSX_CUDA(cudaMemcpy(p->d_pos_in + ly.ikeep, pi.data(), pi.size() * sizeof(int), cudaMemcpyHostToDevice));
+  std::vector<int> rb(ly.rows), cp(ly.L);
+  for (int o = 0; o < ly.rows; ++o) rb[o] = po[o] >= 0 ? po[o] * n_in * ly.k : -1;
+  for (int col = 0; col < ly.L; ++col) {
+    int c = col / ly.k, j = col % ly.k;
+    cp[col] = pi[c] >= 0 ? pi[c] * ly.k + j : -1;
+  }
+  HSX_CUDA(cudaMemcpy(p->maps.rowbase + ly.okeep, rb.data(), rb.size() * sizeof(int), cudaMemcpyHostToDevice));
+  HSX_CUDA(cudaMemcpy(p->maps.colpos + ly.cpoff, cp.data(), cp.size() * sizeof(int), cudaMemcpyHostToDevice));
   long long* row = &p->summary[(size_t)l * HSX_SUM_COLS];
   row[HSX_SUM_KOUT] = n_out;
   row[HSX_SUM_KIN] = n_in;
@@ -562,8 +596,8 @@ static hsx::ElemArgs elem_args(const hsx_plan* p) {
   std::memset(&a, 0, sizeof(a));
   a.layers = p->d_layers;
   a.items = p->d_elem;
-  a.pos_out = p->d_pos_out;
-  a.pos_in = p->d_pos_in;
+  a.rowbase = p->maps.rowbase;
+  a.colpos = p->maps.colpos;
   a.summary = p->d_summary;
   a.divisor = 1.0f;
   return a;

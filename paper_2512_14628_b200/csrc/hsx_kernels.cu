@@ -7,7 +7,6 @@ namespace hsx {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
 
 // opt a kernel into > 48 KB of dynamic shared memory (idempotent, cheap)
 template <typename K>
@@ -15,31 +14,35 @@ static void allow_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-__device__ __forceinline__ float4 ldg4(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
-}
-// streaming load of data read exactly once
+// streaming 128-bit load of data read exactly once (evict-first)
 __device__ __forceinline__ float4 ldcs4(const float* p) {
   return __ldcs(reinterpret_cast<const float4*>(p));
 }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void stcs4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
 __device__ __forceinline__ float f4get(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
 __device__ __forceinline__ void f4set(float4& v, int i, float x) {
   if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
 }
+__device__ __forceinline__ int i4get(const int4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// u + (a - b) in fp64, rounded once (dual updates, consensus.py:186 / :505)
+__device__ __forceinline__ float dual1(float u, float a, float b) {
+  return (float)__dadd_rn((double)u, __dsub_rn((double)a, (double)b));
+}
 
 // ---------------------------------------------------------------------------
 // K1 candidate (+ group-norm partials).  consensus.py:142-160, tensors.py:75-93
 // ---------------------------------------------------------------------------
 
-// fp64 candidate of one element; identical operation order to the reference:
-// (rho1 * s + rho2 * (z - v)) / gamma with s = sum or theta + u.
+// fp64 candidate; explicit _rn intrinsics (no FMA contraction) so the value is
+// bit-identical to numpy's (rho1 * s + rho2 * (z - v)) / gamma.
 __device__ __forceinline__ double cand_of(double s, double z, double v, const DevLayer& ly,
                                           int identity) {
-  // explicit _rn intrinsics: no FMA contraction, so the fp64 value is bit-identical
-  // to numpy's evaluation of the same expression
   if (identity) return s;
   double num = __dadd_rn(__dmul_rn(ly.rho1, s), __dmul_rn(ly.rho2, __dsub_rn(z, v)));
   return __ddiv_rn(num, ly.gamma);
@@ -49,11 +52,11 @@ struct In4 {
   float4 a, b, z, v;
 };
 
-__device__ __forceinline__ In4 load_in4(const CandArgs& p, long long gi, int identity) {
+__device__ __forceinline__ In4 load_in4(const CandArgs& p, long long gi) {
   In4 r;
   r.a = ldcs4(p.s ? p.s + gi : p.theta + gi);
   r.b = p.s ? make_float4(0.f, 0.f, 0.f, 0.f) : ldcs4(p.u + gi);
-  if (identity) {
+  if (p.identity) {
     r.z = r.v = make_float4(0.f, 0.f, 0.f, 0.f);
   } else {
     r.z = ldcs4(p.z + gi);
@@ -62,67 +65,67 @@ __device__ __forceinline__ In4 load_in4(const CandArgs& p, long long gi, int ide
   return r;
 }
 
+__device__ __forceinline__ double cand4(const CandArgs& p, const In4& x, int i, const DevLayer& ly) {
+  double s = p.s ? (double)f4get(x.a, i) : __dadd_rn((double)f4get(x.a, i), (double)f4get(x.b, i));
+  return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), ly, p.identity);
+}
+
 __device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, const DevLayer& ly) {
   double s = p.s ? (double)p.s[gi] : __dadd_rn((double)p.theta[gi], (double)p.u[gi]);
   if (p.identity) return s;
   return cand_of(s, (double)p.z[gi], (double)p.v[gi], ly, 0);
 }
 
-__device__ __forceinline__ double cand4(const In4& x, int i, const DevLayer& ly, int has_s,
-                                        int identity) {
-  double s = has_s ? (double)f4get(x.a, i) : __dadd_rn((double)f4get(x.a, i), (double)f4get(x.b, i));
-  return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), ly, identity);
-}
-
-// group index of layer-local element e for a constraint kind
-__device__ __forceinline__ int group_of(const DevLayer& ly, int grp, unsigned o, unsigned col,
-                                        unsigned c) {
+__device__ __forceinline__ int group_of(int grp, unsigned o, unsigned col, unsigned c) {
   return grp == kFilter ? (int)o : (grp == kChannel ? (int)c : (int)col);
 }
 
-// keep test of layer-local element e against passes [0, npass)
+// keep test of layer-local element e against passes [0, npass) (renorm passes only)
 __device__ __forceinline__ bool kept_by(const DevLayer& ly, const uint8_t* const* flags, int npass,
                                         long long e) {
   unsigned o = fdiv((unsigned)e, ly.divL);
   unsigned col = (unsigned)e - o * (unsigned)ly.L;
   unsigned c = fdiv(col, ly.divk);
   bool keep = true;
-  for (int q = 0; q < npass; ++q) keep = keep && flags[q][ly.goff[q] + group_of(ly, ly.group[q], o, col, c)];
+  for (int q = 0; q < npass; ++q) keep = keep && flags[q][ly.goff[q] + group_of(ly.group[q], o, col, c)];
   return keep;
 }
 
-// elementwise candidate over [begin, end) of one layer (dense layers, frozen mode)
-__device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long long begin,
-                                 long long end, int frozen) {
+// K1a: elementwise candidate (dense layers; every layer in frozen mode, where
+// prunable layers get cand * global mask, consensus.py:177-180)
+__global__ void __launch_bounds__(kThreads) k_cand_dense(CandArgs p, int frozen) {
+  const Item it = p.items[blockIdx.x];
+  const DevLayer& ly = p.layers[it.layer];
   const bool masked = frozen && ly.ncons > 0 && p.fmask != nullptr;
-  if (begin & 3) {  // row tiles of layers with c_in*kh*kw % 4 != 0: scalar path
-    for (long long e = begin + threadIdx.x; e < end; e += kThreads) {
+  if (it.begin & 3) {  // row tiles of layers with c_in*kh*kw % 4 != 0: scalar path
+    for (long long e = it.begin + threadIdx.x; e < it.end; e += kThreads) {
       double c = cand_elem(p, ly.off + e, ly);
       if (masked && !((p.fmask[ly.mword + (e >> 5)] >> (e & 31)) & 1u)) c = c * 0.0;
       p.zn[ly.off + e] = (float)c;
     }
     return;
   }
-  const long long nq = (end - begin + 3) >> 2;
-  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * kUnroll) {
-    In4 in[kUnroll];
+  constexpr int U = 2;
+  const long long nq = (it.end - it.begin + 3) >> 2;
+  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * U) {
+    In4 in[U];
 #pragma unroll
-    for (int uu = 0; uu < kUnroll; ++uu) {
+    for (int uu = 0; uu < U; ++uu) {
       long long q = q0 + (long long)uu * kThreads;
-      long long e = begin + 4 * q;
-      if (q < nq && e + 3 < ly.n) in[uu] = load_in4(p, ly.off + e, p.identity);
+      long long e = it.begin + 4 * q;
+      if (q < nq && e + 3 < ly.n) in[uu] = load_in4(p, ly.off + e);
     }
 #pragma unroll
-    for (int uu = 0; uu < kUnroll; ++uu) {
+    for (int uu = 0; uu < U; ++uu) {
       long long q = q0 + (long long)uu * kThreads;
       if (q >= nq) continue;
-      long long e = begin + 4 * q;
+      long long e = it.begin + 4 * q;
       uint32_t bits = masked ? p.fmask[ly.mword + (e >> 5)] : 0u;
       if (e + 3 < ly.n) {
         float4 out;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          double c = cand4(in[uu], i, ly, p.s != nullptr, p.identity);
+          double c = cand4(p, in[uu], i, ly);
           if (masked) c = ((bits >> ((e + i) & 31)) & 1u) ? c : c * 0.0;
           f4set(out, i, (float)c);
         }
@@ -138,11 +141,81 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
   }
 }
 
-// row tile with fp64 group-norm partials: shared memory holds the squares of
-// the unrounded candidate for rsub rows, then each group is reduced by one
-// owner thread (CHANNEL / SHAPE) or one warp (FILTER) in a fixed order.
-__device__ void cand_tile(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq,
-                          double* acc) {
+// K1b, CHANNEL / SHAPE groups with c_in*kh*kw % 4 == 0 (every ResNet conv but the
+// stem): each thread owns a fixed column quad and walks rows of the tile, so the
+// fp64 column sums of squares stay in registers; one shared-memory pass then
+// folds the row phases and the kh*kw columns of each channel in a fixed order.
+__device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, double* smem) {
+  const int pass = p.pass;
+  const int grp = ly.group[pass];
+  const int G = ly.G[pass];
+  const int L = ly.L;
+  const int Q = L >> 2;
+  const long long r0 = it.begin / L;
+  const int nrows = (int)((it.end - it.begin) / L);
+  const int RP = Q >= kThreads ? 1 : kThreads / Q;  // row phases
+  const int t = threadIdx.x;
+  const int ph = Q >= kThreads ? 0 : t / Q;
+  // smem layout: colsum[RP][L]
+  if (ph < RP) {
+    for (int j = (Q >= kThreads ? t : t % Q); j < Q; j += (Q >= kThreads ? kThreads : Q)) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      constexpr int U = 2;
+      for (int r = ph; r < nrows; r += RP * U) {
+        In4 in[U];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+          int rr = r + uu * RP;
+          if (rr < nrows) in[uu] = load_in4(p, ly.off + (r0 + rr) * (long long)L + 4 * j);
+        }
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+          int rr = r + uu * RP;
+          if (rr >= nrows) break;
+          long long e = (r0 + rr) * (long long)L + 4 * j;
+          double c0 = cand4(p, in[uu], 0, ly), c1 = cand4(p, in[uu], 1, ly);
+          double c2 = cand4(p, in[uu], 2, ly), c3 = cand4(p, in[uu], 3, ly);
+          if (pass > 0) {
+            if (!kept_by(ly, p.flags, pass, e + 0)) c0 = 0.0;
+            if (!kept_by(ly, p.flags, pass, e + 1)) c1 = 0.0;
+            if (!kept_by(ly, p.flags, pass, e + 2)) c2 = 0.0;
+            if (!kept_by(ly, p.flags, pass, e + 3)) c3 = 0.0;
+          } else {
+            st4(p.zn + ly.off + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
+          }
+          a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
+          a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
+          a2 = __dadd_rn(a2, __dmul_rn(c2, c2));
+          a3 = __dadd_rn(a3, __dmul_rn(c3, c3));
+        }
+      }
+      double* cs = smem + (long long)ph * L + 4 * j;
+      cs[0] = a0; cs[1] = a1; cs[2] = a2; cs[3] = a3;
+    }
+  }
+  __syncthreads();
+  double* out = p.partials + ly.poff[pass] + (long long)it.part * G;
+  if (grp == kChannel) {
+    const int k = ly.k;
+    for (int c = t; c < ly.cin; c += kThreads) {
+      double s = 0.0;
+      for (int q = 0; q < RP; ++q)
+        for (int jj = 0; jj < k; ++jj) s += smem[(long long)q * L + c * k + jj];
+      out[c] = s;
+    }
+  } else {
+    for (int col = t; col < L; col += kThreads) {
+      double s = 0.0;
+      for (int q = 0; q < RP; ++q) s += smem[(long long)q * L + col];
+      out[col] = s;
+    }
+  }
+}
+
+// K1b general path (FILTER groups, or rows not a multiple of 4 elements):
+// squares of sub-tiles of rows staged in shared memory.
+__device__ void cand_tile_smem(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq,
+                               double* acc) {
   const int pass = p.pass;
   const int grp = ly.group[pass];
   const int G = ly.G[pass];
@@ -153,52 +226,23 @@ __device__ void cand_tile(const CandArgs& p, const DevLayer& ly, const Item& it,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (grp != kFilter)
     for (int g = threadIdx.x; g < G; g += kThreads) acc[g] = 0.0;
-
   for (int rs = 0; rs < nrows; rs += ly.rsub) {
     const int nr = min(ly.rsub, nrows - rs);
     const int E = nr * L;
-    const long long ebase = (r0 + rs) * (long long)L;  // layer-local element of sq[0]
+    const long long ebase = (r0 + rs) * (long long)L;
     const long long gbase = ly.off + ebase;
-    if ((L & 3) == 0) {
-      const int nq = E >> 2;
-      for (int q0 = threadIdx.x; q0 < nq; q0 += kThreads * kUnroll) {
-        In4 in[kUnroll];
-#pragma unroll
-        for (int uu = 0; uu < kUnroll; ++uu) {
-          int q = q0 + uu * kThreads;
-          if (q < nq) in[uu] = load_in4(p, gbase + 4 * q, p.identity);
-        }
-#pragma unroll
-        for (int uu = 0; uu < kUnroll; ++uu) {
-          int q = q0 + uu * kThreads;
-          if (q >= nq) continue;
-          float4 out;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            double c = cand4(in[uu], i, ly, p.s != nullptr, p.identity);
-            if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + 4 * q + i)) c = 0.0;
-            f4set(out, i, (float)c);
-            sq[4 * q + i] = __dmul_rn(c, c);
-          }
-          if (pass == 0) st4(p.zn + gbase + 4 * q, out);
-        }
-      }
-    } else {
-      for (int i = threadIdx.x; i < E; i += kThreads) {
-        double c = cand_elem(p, gbase + i, ly);
-        if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
-        if (pass == 0) p.zn[gbase + i] = (float)c;
-        sq[i] = __dmul_rn(c, c);
-      }
+    for (int i = threadIdx.x; i < E; i += kThreads) {
+      double c = cand_elem(p, gbase + i, ly);
+      if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
+      if (pass == 0) p.zn[gbase + i] = (float)c;
+      sq[i] = __dmul_rn(c, c);
     }
     __syncthreads();
     if (grp == kChannel) {
       for (int c = threadIdx.x; c < ly.cin; c += kThreads) {
         double s = 0.0;
-        for (int r = 0; r < nr; ++r) {
-          const double* row = sq + r * L + c * k;
-          for (int j = 0; j < k; ++j) s += row[j];
-        }
+        for (int r = 0; r < nr; ++r)
+          for (int j = 0; j < k; ++j) s += sq[r * L + c * k + j];
         acc[c] += s;
       }
     } else if (grp == kShape) {
@@ -223,22 +267,34 @@ __device__ void cand_tile(const CandArgs& p, const DevLayer& ly, const Item& it,
       p.partials[ly.poff[pass] + (long long)it.part * G + g] = acc[g];
 }
 
-__global__ void __launch_bounds__(kThreads) k_candidate(CandArgs p, int frozen) {
+__global__ void __launch_bounds__(kThreads, 3) k_cand_norm(CandArgs p) {
   extern __shared__ double smem[];
   const Item it = p.items[blockIdx.x];
   const DevLayer& ly = p.layers[it.layer];
-  if (frozen || ly.ncons == 0) {
-    if (p.pass == 0) cand_elementwise(p, ly, it.begin, it.end, frozen);
-    return;
-  }
   if (ly.ncons <= p.pass) return;
-  cand_tile(p, ly, it, smem, smem + p.sqcap);
+  if (ly.group[p.pass] != kFilter && (ly.L & 3) == 0)
+    cand_tile_quads(p, ly, it, smem);
+  else
+    cand_tile_smem(p, ly, it, smem, smem + p.sqcap);
 }
 
-void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
-  if (n_items <= 0) return;
-  allow_smem(k_candidate, smem);
-  k_candidate<<<n_items, kThreads, smem, st>>>(a, frozen);
+void launch_candidate(const CandArgs& a, const Item* dense_items, int n_dense, const Item* norm_items,
+                      int n_norm, int frozen, size_t smem, cudaStream_t st) {
+  if (n_dense > 0 && a.pass == 0) {
+    CandArgs d = a;
+    d.items = dense_items;
+    k_cand_dense<<<n_dense, kThreads, 0, st>>>(d, frozen);
+  }
+  if (n_norm > 0) {
+    CandArgs d = a;
+    d.items = norm_items;
+    if (frozen) {
+      k_cand_dense<<<n_norm, kThreads, 0, st>>>(d, frozen);
+    } else {
+      allow_smem(k_cand_norm, smem);
+      k_cand_norm<<<n_norm, kThreads, smem, st>>>(d);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -250,6 +306,7 @@ __device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
   return ka > kb || (ka == kb && ia < ib);
 }
 
+// shared memory: key[Gp] (double), idx[Gp] (int), fold[blockDim] (double)
 __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ layers,
                                                  const int* __restrict__ list, int pass,
                                                  const double* __restrict__ partials,
@@ -261,48 +318,56 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
   int Gp = 1;
   while (Gp < G) Gp <<= 1;
   int* sidx = reinterpret_cast<int*>(skey + Gp);
+  double* fold = reinterpret_cast<double*>(sidx + Gp + (Gp & 1));
   const bool rowwise = ly.group[pass] == kFilter;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  if (rowwise || ly.nparts < 8) {
-    for (int g = threadIdx.x; g < Gp; g += blockDim.x) {
+  const double* part = partials + ly.poff[pass];
+  const int nt = blockDim.x;
+  // 1) squared norms. Row tiles are strided over T slices of threads (T = nt / W
+  //    with W groups per round, coalesced along groups); slices fold in order.
+  const int W = rowwise ? nt : min(nt, Gp);
+  const int T = nt / W;
+  for (int base = 0; base < Gp; base += W) {
+    const int g = base + (int)threadIdx.x % W;
+    const int sl = (int)threadIdx.x / W;
+    double s2 = 0.0;
+    if (g < G) {
+      if (rowwise) {
+        s2 = part[g];
+      } else {
+        double a0 = 0.0, a1 = 0.0;
+        int pt = sl;
+        for (; pt + T < ly.nparts; pt += 2 * T) {
+          a0 += part[(long long)pt * G + g];
+          a1 += part[(long long)(pt + T) * G + g];
+        }
+        if (pt < ly.nparts) a0 += part[(long long)pt * G + g];
+        s2 = a0 + a1;
+      }
+    }
+    if (T > 1) {
+      fold[threadIdx.x] = s2;
+      __syncthreads();
+      if (sl == 0) {
+        double s = 0.0;
+        for (int q = 0; q < T; ++q) s += fold[q * W + (int)threadIdx.x];
+        s2 = s;
+      }
+      __syncthreads();
+    }
+    if (sl == 0 && g < Gp) {
       double key = -1.0;  // padding sorts after every norm (norms >= 0)
       if (g < G) {
-        double s2;
-        if (rowwise) {
-          s2 = partials[ly.poff[pass] + g];
-        } else {
-          s2 = 0.0;
-          for (int pt = 0; pt < ly.nparts; ++pt) s2 += partials[ly.poff[pass] + (long long)pt * G + g];
-        }
         key = sqrt(s2);
         norms[ly.goff[pass] + g] = key;
       }
       skey[g] = key;
       sidx[g] = g;
     }
-  } else {
-    // many row tiles: one warp per group, lanes stride the parts, fixed shuffle tree
-    for (int g = warp; g < Gp; g += nwarps) {
-      double s2 = 0.0;
-      if (g < G)
-        for (int pt = lane; pt < ly.nparts; pt += 32) s2 += partials[ly.poff[pass] + (long long)pt * G + g];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) s2 += __shfl_xor_sync(kFull, s2, off);
-      if (lane == 0) {
-        double key = -1.0;
-        if (g < G) {
-          key = sqrt(s2);
-          norms[ly.goff[pass] + g] = key;
-        }
-        skey[g] = key;
-        sidx[g] = g;
-      }
-    }
   }
   __syncthreads();
   for (int size = 2; size <= Gp; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < Gp; i += blockDim.x) {
+      for (int i = threadIdx.x; i < Gp; i += nt) {
         int j = i ^ stride;
         if (j > i) {
           double ki = skey[i], kj = skey[j];
@@ -319,7 +384,7 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
     }
   }
   const int keep = ly.keep[pass];
-  for (int pos = threadIdx.x; pos < Gp; pos += blockDim.x) {
+  for (int pos = threadIdx.x; pos < Gp; pos += nt) {
     int g = sidx[pos];
     if (g < G) flags[ly.goff[pass] + g] = pos < keep ? 1 : 0;
   }
@@ -333,49 +398,129 @@ void launch_select(const DevLayer* layers, const int* list, int n, int pass, con
 }
 
 // ---------------------------------------------------------------------------
+// keep maps: rowkeep = AND of FILTER passes, colkeep = AND of CHANNEL/SHAPE passes
+// ---------------------------------------------------------------------------
+
+__global__ void k_keepmaps(const DevLayer* __restrict__ layers, const int* __restrict__ list,
+                           const uint8_t* f0, const uint8_t* f1, const uint8_t* f2, Maps m) {
+  const DevLayer& ly = layers[list[blockIdx.x]];
+  const uint8_t* flags[kMaxPasses] = {f0, f1, f2};
+  for (int o = threadIdx.x; o < ly.rows; o += blockDim.x) {
+    uint8_t keep = 1;
+    for (int q = 0; q < ly.ncons; ++q)
+      if (ly.group[q] == kFilter) keep &= flags[q][ly.goff[q] + o];
+    m.rowkeep[ly.okeep + o] = keep;
+  }
+  for (int col = threadIdx.x; col < ly.L; col += blockDim.x) {
+    uint8_t keep = 1;
+    for (int q = 0; q < ly.ncons; ++q) {
+      if (ly.group[q] == kChannel) keep &= flags[q][ly.goff[q] + col / ly.k];
+      else if (ly.group[q] == kShape) keep &= flags[q][ly.goff[q] + col];
+    }
+    m.colkeep[ly.cpoff + col] = keep;
+  }
+}
+
+void launch_keepmaps(const DevLayer* layers, const int* list, int n, const uint8_t* f0,
+                     const uint8_t* f1, const uint8_t* f2, Maps maps, cudaStream_t st) {
+  if (n > 0) k_keepmaps<<<n, 512, 0, st>>>(layers, list, f0, f1, f2, maps);
+}
+
+// ---------------------------------------------------------------------------
 // K3 project + local mask.  sparsity.py:71-94, 113-115; consensus.py:181-182
-// One warp per 32-element mask word, ballot builds the word.
+// A thread owns a quad of elements (one row when L % 4 == 0): one float4 load,
+// one uchar4 column-keep load; 8 lanes' nibbles OR-fold into one mask word.
 // ---------------------------------------------------------------------------
 
 __global__ void __launch_bounds__(kThreads) k_project(const DevLayer* __restrict__ layers,
                                                       const Item* __restrict__ items,
                                                       float* __restrict__ zn,
-                                                      uint32_t* __restrict__ mask,
-                                                      const uint8_t* f0, const uint8_t* f1,
-                                                      const uint8_t* f2) {
+                                                      uint32_t* __restrict__ mask, Maps m) {
   const Item it = items[blockIdx.x];
   const DevLayer& ly = layers[it.layer];
-  const uint8_t* flags[kMaxPasses] = {f0, f1, f2};
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+  if ((ly.L & 3) == 0) {
+    const long long q0 = it.begin >> 2, q1 = (it.end + 3) >> 2;  // begin is a multiple of 32
+    constexpr int U = 2;
+    for (long long qb = q0 + (threadIdx.x & ~31); qb < q1; qb += (long long)kThreads * U) {
+      float4 val[U];
+      int rk[U];
+      uchar4 ck[U];
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        long long q = qb + (long long)uu * kThreads + lane;
+        long long e = q << 2;
+        if (q < q1 && e + 3 < ly.n) {
+          val[uu] = ldcs4(zn + ly.off + e);
+          unsigned o = fdiv((unsigned)e, ly.divL);
+          unsigned col = (unsigned)e - o * (unsigned)ly.L;
+          rk[uu] = m.rowkeep[ly.okeep + o];
+          ck[uu] = *reinterpret_cast<const uchar4*>(m.colkeep + ly.cpoff + col);
+        }
+      }
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        long long q = qb + (long long)uu * kThreads + lane;
+        long long e = q << 2;
+        unsigned nib = 0;
+        if (q < q1 && e < ly.n) {
+          if (e + 3 < ly.n) {
+            bool k0 = rk[uu] && ck[uu].x, k1 = rk[uu] && ck[uu].y;
+            bool k2 = rk[uu] && ck[uu].z, k3 = rk[uu] && ck[uu].w;
+            float4 v = val[uu];
+            nib = (unsigned)(k0 && v.x != 0.f) | ((unsigned)(k1 && v.y != 0.f) << 1) |
+                  ((unsigned)(k2 && v.z != 0.f) << 2) | ((unsigned)(k3 && v.w != 0.f) << 3);
+            if (!(k0 && k1 && k2 && k3)) {
+              if (!k0) v.x = 0.f;
+              if (!k1) v.y = 0.f;
+              if (!k2) v.z = 0.f;
+              if (!k3) v.w = 0.f;
+              st4(zn + ly.off + e, v);
+            }
+          } else {
+            for (int i = 0; i < 4 && e + i < ly.n; ++i) {
+              unsigned o = fdiv((unsigned)(e + i), ly.divL);
+              unsigned col = (unsigned)(e + i) - o * (unsigned)ly.L;
+              bool kp = m.rowkeep[ly.okeep + o] && m.colkeep[ly.cpoff + col];
+              float x = zn[ly.off + e + i];
+              if (!kp) zn[ly.off + e + i] = 0.f;
+              nib |= (unsigned)(kp && x != 0.f) << i;
+            }
+          }
+        }
+        unsigned w = nib << (4 * (lane & 7));
+        w |= __shfl_xor_sync(kFull, w, 1);
+        w |= __shfl_xor_sync(kFull, w, 2);
+        w |= __shfl_xor_sync(kFull, w, 4);
+        if ((lane & 7) == 0 && q < q1 && e < ly.n) mask[ly.mword + (e >> 5)] = w;
+      }
+    }
+    return;
+  }
+  // rows of L % 4 != 0 elements (stem convs): one warp per 32-element word
+  const int warp = threadIdx.x >> 5;
   const long long w0 = it.begin >> 5, w1 = (it.end + 31) >> 5;
-  constexpr int kW = 4;
-  for (long long wb = w0 + warp; wb < w1; wb += (kThreads / 32) * kW) {
-    float val[kW];
-#pragma unroll
-    for (int uu = 0; uu < kW; ++uu) {
-      long long w = wb + (long long)uu * (kThreads / 32);
-      long long e = (w << 5) + lane;
-      val[uu] = (w < w1 && e < ly.n) ? __ldcs(zn + ly.off + e) : 0.f;
+  for (long long w = w0 + warp; w < w1; w += kThreads / 32) {
+    long long e = (w << 5) + lane;
+    bool valid = e < ly.n;
+    bool kp = false;
+    float x = 0.f;
+    if (valid) {
+      unsigned o = fdiv((unsigned)e, ly.divL);
+      unsigned col = (unsigned)e - o * (unsigned)ly.L;
+      kp = m.rowkeep[ly.okeep + o] && m.colkeep[ly.cpoff + col];
+      x = zn[ly.off + e];
+      if (!kp) zn[ly.off + e] = 0.f;
     }
-#pragma unroll
-    for (int uu = 0; uu < kW; ++uu) {
-      long long w = wb + (long long)uu * (kThreads / 32);
-      if (w >= w1) break;
-      long long e = (w << 5) + lane;
-      bool valid = e < ly.n;
-      bool keep = valid && kept_by(ly, flags, ly.ncons, e);
-      if (valid && !keep) zn[ly.off + e] = 0.0f;
-      unsigned bits = __ballot_sync(kFull, keep && val[uu] != 0.0f);
-      if (lane == 0) mask[ly.mword + w] = bits;
-    }
+    unsigned bits = __ballot_sync(kFull, kp && x != 0.0f);
+    if (lane == 0) mask[ly.mword + w] = bits;
   }
 }
 
 void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
-                    uint32_t* mask, const uint8_t* f0, const uint8_t* f1, const uint8_t* f2,
-                    cudaStream_t st) {
+                    uint32_t* mask, Maps maps, cudaStream_t st) {
   if (n_items <= 0) return;
-  k_project<<<n_items, kThreads, 0, st>>>(layers, items, zn, mask, f0, f1, f2);
+  k_project<<<n_items, kThreads, 0, st>>>(layers, items, zn, mask, maps);
 }
 
 // ---------------------------------------------------------------------------
@@ -430,7 +575,7 @@ __global__ void __launch_bounds__(kThreads) k_keep_mark(const DevLayer* __restri
   const DevLayer& ly = layers[it.layer];
   const long long w0 = it.begin >> 5, w1 = (it.end + 31) >> 5;
   const long long r_lo = it.begin / ly.L;
-  const long long r_hi = (min(it.end, ly.n) - 1) / ly.L;  // inclusive
+  const long long r_hi = (std::min(it.end, ly.n) - 1) / ly.L;  // inclusive
   const int nr = (int)(r_hi - r_lo + 1);
   uint8_t* s_in = sflag;
   uint8_t* s_out = sflag + ly.cin;
@@ -485,8 +630,9 @@ void launch_keep_mark(const DevLayer* layers, const Item* items, int n_items, co
 
 // ---------------------------------------------------------------------------
 // K5b keep scan: positions of kept filters / channels (exclusive prefix sums),
-// payload sizes; the last CTA lays out the flat buffer in layer order
-// (bucketize's concatenation, transport.py:239-280).
+// row bases and column positions of the compact rectangle, payload sizes; the
+// last CTA lays out the flat buffer in layer order (bucketize's
+// concatenation, transport.py:239-280).
 // ---------------------------------------------------------------------------
 
 __device__ int block_exclusive_scan(int x, int* warp_tot, int* total) {
@@ -537,12 +683,23 @@ __global__ void __launch_bounds__(1024) k_keep_scan(const DevLayer* __restrict__
                                                     const uint8_t* __restrict__ oflag,
                                                     const uint8_t* __restrict__ iflag,
                                                     int* __restrict__ pos_out,
-                                                    int* __restrict__ pos_in,
+                                                    int* __restrict__ pos_in, Maps m,
                                                     long long* summary, unsigned int* done) {
   const int l = list[blockIdx.x];
   const DevLayer& ly = layers[l];
   int n_out = scan_flags(oflag + ly.okeep, ly.rows, pos_out + ly.okeep);
   int n_in = scan_flags(iflag + ly.ikeep, ly.cin, pos_in + ly.ikeep);
+  __syncthreads();
+  const int rowlen = n_in * ly.k;
+  for (int o = threadIdx.x; o < ly.rows; o += blockDim.x) {
+    int po = pos_out[ly.okeep + o];
+    m.rowbase[ly.okeep + o] = po >= 0 ? po * rowlen : -1;
+  }
+  for (int col = threadIdx.x; col < ly.L; col += blockDim.x) {
+    int c = col / ly.k, j = col - c * ly.k;
+    int pi = pos_in[ly.ikeep + c];
+    m.colpos[ly.cpoff + col] = pi >= 0 ? pi * ly.k + j : -1;
+  }
   __shared__ bool last;
   if (threadIdx.x == 0) {
     long long* row = summary + (long long)l * kSumCols;
@@ -597,48 +754,54 @@ __global__ void __launch_bounds__(1024) k_keep_scan(const DevLayer* __restrict__
 
 void launch_keep_scan(const DevLayer* layers, const int* list, int n, int n_layers,
                       const uint8_t* oflag, const uint8_t* iflag, int* pos_out, int* pos_in,
-                      long long* summary, unsigned int* done, cudaStream_t st) {
+                      Maps maps, long long* summary, unsigned int* done, cudaStream_t st) {
   if (n <= 0) return;
-  k_keep_scan<<<n, 1024, 0, st>>>(layers, list, n_layers, oflag, iflag, pos_out, pos_in, summary,
-                                  done);
+  k_keep_scan<<<n, 1024, 0, st>>>(layers, list, n_layers, oflag, iflag, pos_out, pos_in, maps,
+                                  summary, done);
 }
 
 // ---------------------------------------------------------------------------
 // K6 compact + intra dual; K7 decompact + inter dual.
 // consensus.py:476-505, 535; shrinkage.py:61-82
+// A thread owns element quads: the dense streams move as float4; the compact
+// payload offset of element (o, col) is  coff + rowbase[o] + colpos[col]
+// (int4 load of colpos per quad), -1 entries are dropped coordinates.
 // ---------------------------------------------------------------------------
 
-// walks (o, col, c, j) of consecutive layer-local elements without divisions
-struct Walk {
-  unsigned o, col, c, j;
-  __device__ __forceinline__ void init(const DevLayer& ly, unsigned e) {
-    o = fdiv(e, ly.divL);
-    col = e - o * (unsigned)ly.L;
-    c = fdiv(col, ly.divk);
-    j = col - c * (unsigned)ly.k;
-  }
-  __device__ __forceinline__ void next(const DevLayer& ly) {
-    ++col;
-    if (++j == (unsigned)ly.k) { j = 0; ++c; }
-    if (col == (unsigned)ly.L) { col = 0; c = 0; j = 0; ++o; }
-  }
-};
+// payload index of 4 consecutive elements e..e+3 (same row when L % 4 == 0)
+__device__ __forceinline__ int4 quad_dst(const ElemArgs& a, const DevLayer& ly, long long e) {
+  unsigned o = fdiv((unsigned)e, ly.divL);
+  unsigned col = (unsigned)e - o * (unsigned)ly.L;
+  int rb = a.rowbase[ly.okeep + o];
+  int4 cp = *reinterpret_cast<const int4*>(a.colpos + ly.cpoff + col);
+  if (rb < 0) return make_int4(-1, -1, -1, -1);
+  return make_int4(cp.x < 0 ? -1 : rb + cp.x, cp.y < 0 ? -1 : rb + cp.y, cp.z < 0 ? -1 : rb + cp.z,
+                   cp.w < 0 ? -1 : rb + cp.w);
+}
+
+__device__ __forceinline__ int elem_dst(const ElemArgs& a, const DevLayer& ly, long long e) {
+  unsigned o = fdiv((unsigned)e, ly.divL);
+  unsigned col = (unsigned)e - o * (unsigned)ly.L;
+  int rb = a.rowbase[ly.okeep + o], cp = a.colpos[ly.cpoff + col];
+  return (rb < 0 || cp < 0) ? -1 : rb + cp;
+}
 
 __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   const Item it = a.items[blockIdx.x];
   const DevLayer& ly = a.layers[it.layer];
-  const long long* srow = a.summary + (long long)it.layer * kSumCols;
-  const long long kin = srow[1];
-  const long long coff = srow[3];
+  const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
   const bool pr = ly.ncons > 0;
+  const bool quads = !pr || (ly.L & 3) == 0;
   const long long nq = (it.end - it.begin + 3) >> 2;
-  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * kUnroll) {
-    float4 th[kUnroll], uu4[kUnroll], zn[kUnroll], vv[kUnroll];
+  constexpr int U = 2;
+  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * U) {
+    float4 th[U], uu4[U], zn[U], vv[U];
 #pragma unroll
-    for (int uu = 0; uu < kUnroll; ++uu) {
+    for (int uu = 0; uu < U; ++uu) {
       long long q = q0 + (long long)uu * kThreads;
       long long e = it.begin + 4 * q;
-      if (q < nq && e + 3 < ly.n) {
+      if (q >= nq) continue;
+      if (e + 3 < ly.n) {
         long long gi = ly.off + e;
         zn[uu] = ldcs4(a.zn + gi);
         vv[uu] = a.vin ? ldcs4(a.vin + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -646,7 +809,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
           th[uu] = ldcs4(a.theta + gi);
           uu4[uu] = ldcs4(a.u + gi);
         }
-      } else if (q < nq) {
+      } else {
         for (int i = 0; i < 4; ++i) {
           bool ok = e + i < ly.n;
           long long gi = ly.off + e + i;
@@ -660,40 +823,35 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
       }
     }
 #pragma unroll
-    for (int uu = 0; uu < kUnroll; ++uu) {
+    for (int uu = 0; uu < U; ++uu) {
       long long q = q0 + (long long)uu * kThreads;
       if (q >= nq) continue;
       long long e = it.begin + 4 * q;
       const bool full = e + 3 < ly.n;
       if (a.u) {
-        float4 un;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          f4set(un, i, (float)((double)f4get(uu4[uu], i) +
-                               ((double)f4get(th[uu], i) - (double)f4get(zn[uu], i))));
+        float4 un = make_float4(dual1(uu4[uu].x, th[uu].x, zn[uu].x), dual1(uu4[uu].y, th[uu].y, zn[uu].y),
+                                dual1(uu4[uu].z, th[uu].z, zn[uu].z), dual1(uu4[uu].w, th[uu].w, zn[uu].w));
         if (full) {
-          st4(a.u + ly.off + e, un);
+          stcs4(a.u + ly.off + e, un);
         } else {
           for (int i = 0; i < 4 && e + i < ly.n; ++i) a.u[ly.off + e + i] = f4get(un, i);
         }
       }
+      float4 c = make_float4(zn[uu].x + vv[uu].x, zn[uu].y + vv[uu].y, zn[uu].z + vv[uu].z,
+                             zn[uu].w + vv[uu].w);
       if (!pr) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (e + i < ly.n) a.flat_out[coff + e + i] = f4get(zn[uu], i) + f4get(vv[uu], i);
-      } else {
-        Walk wk;
-        wk.init(ly, (unsigned)e);
+          if (e + i < ly.n) a.flat_out[coff + e + i] = f4get(c, i);
+      } else if (quads && full) {
+        int4 d = quad_dst(a, ly, e);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (e + i < ly.n) {
-            int po = a.pos_out[ly.okeep + wk.o];
-            int pi = a.pos_in[ly.ikeep + wk.c];
-            if (po >= 0 && pi >= 0)
-              a.flat_out[coff + ((long long)po * kin + pi) * ly.k + wk.j] =
-                  f4get(zn[uu], i) + f4get(vv[uu], i);
-          }
-          wk.next(ly);
+        for (int i = 0; i < 4; ++i)
+          if (i4get(d, i) >= 0) a.flat_out[coff + i4get(d, i)] = f4get(c, i);
+      } else {
+        for (int i = 0; i < 4 && e + i < ly.n; ++i) {
+          int d = elem_dst(a, ly, e + i);
+          if (d >= 0) a.flat_out[coff + d] = f4get(c, i);
         }
       }
     }
@@ -708,42 +866,37 @@ void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   const Item it = a.items[blockIdx.x];
   const DevLayer& ly = a.layers[it.layer];
-  const long long* srow = a.summary + (long long)it.layer * kSumCols;
-  const long long kin = srow[1];
-  const long long coff = srow[3];
+  const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
   const bool pr = ly.ncons > 0;
+  const bool quads = !pr || (ly.L & 3) == 0;
   const float div = a.divisor;
   const long long nq = (it.end - it.begin + 3) >> 2;
-  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * kUnroll) {
-    float4 zn[kUnroll], vv[kUnroll], zz[kUnroll];
+  constexpr int U = 2;
+  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * U) {
+    float4 zn[U], vv[U], zz[U];
 #pragma unroll
-    for (int uu = 0; uu < kUnroll; ++uu) {
+    for (int uu = 0; uu < U; ++uu) {
       long long q = q0 + (long long)uu * kThreads;
       long long e = it.begin + 4 * q;
       if (q >= nq) continue;
+      const bool full = e + 3 < ly.n;
       // gather of the reduced payload (zero fill for dropped coordinates)
       if (!pr) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          f4set(zz[uu], i, e + i < ly.n ? a.flat_in[coff + e + i] : 0.f);
-      } else {
-        Walk wk;
-        wk.init(ly, (unsigned)e);
+        for (int i = 0; i < 4; ++i) f4set(zz[uu], i, e + i < ly.n ? a.flat_in[coff + e + i] : 0.f);
+      } else if (quads && full) {
+        int4 d = quad_dst(a, ly, e);
 #pragma unroll
+        for (int i = 0; i < 4; ++i) f4set(zz[uu], i, i4get(d, i) >= 0 ? a.flat_in[coff + i4get(d, i)] : 0.f);
+      } else {
         for (int i = 0; i < 4; ++i) {
-          float x = 0.f;
-          if (e + i < ly.n) {
-            int po = a.pos_out[ly.okeep + wk.o];
-            int pi = a.pos_in[ly.ikeep + wk.c];
-            if (po >= 0 && pi >= 0) x = a.flat_in[coff + ((long long)po * kin + pi) * ly.k + wk.j];
-          }
-          f4set(zz[uu], i, x);
-          wk.next(ly);
+          int d = e + i < ly.n ? elem_dst(a, ly, e + i) : -1;
+          f4set(zz[uu], i, d >= 0 ? a.flat_in[coff + d] : 0.f);
         }
       }
       if (a.v) {
         long long gi = ly.off + e;
-        if (e + 3 < ly.n) {
+        if (full) {
           zn[uu] = ldcs4(a.zn + gi);
           vv[uu] = ldcs4(a.v + gi);
         } else {
@@ -755,26 +908,19 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
       }
     }
 #pragma unroll
-    for (int uu = 0; uu < kUnroll; ++uu) {
+    for (int uu = 0; uu < U; ++uu) {
       long long q = q0 + (long long)uu * kThreads;
       if (q >= nq) continue;
       long long e = it.begin + 4 * q;
-      float4 zo;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float x = f4get(zz[uu], i);
-        f4set(zo, i, div == 1.0f ? x : x / div);
-      }
+      float4 zo = zz[uu];
+      if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
       float4 vn;
-      if (a.v) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          f4set(vn, i, (float)((double)f4get(vv[uu], i) +
-                               ((double)f4get(zn[uu], i) - (double)f4get(zo, i))));
-      }
+      if (a.v)
+        vn = make_float4(dual1(vv[uu].x, zn[uu].x, zo.x), dual1(vv[uu].y, zn[uu].y, zo.y),
+                         dual1(vv[uu].z, zn[uu].z, zo.z), dual1(vv[uu].w, zn[uu].w, zo.w));
       if (e + 3 < ly.n) {
-        st4(a.z + ly.off + e, zo);
-        if (a.v) st4(a.v + ly.off + e, vn);
+        stcs4(a.z + ly.off + e, zo);
+        if (a.v) stcs4(a.v + ly.off + e, vn);
       } else {
         for (int i = 0; i < 4 && e + i < ly.n; ++i) {
           a.z[ly.off + e + i] = f4get(zo, i);
@@ -817,10 +963,6 @@ void launch_add(const float* a, const float* b, float* out, long long n, cudaStr
   k_add<<<stream_grid(n >> 2), kThreads, 0, st>>>(a, b, out, n);
 }
 
-__device__ __forceinline__ float dual1(float u, float th, float zn) {
-  return (float)((double)u + ((double)th - (double)zn));
-}
-
 __global__ void __launch_bounds__(kThreads) k_dual(const float* __restrict__ th,
                                                    float* __restrict__ u,
                                                    const float* __restrict__ zn, long long n) {
@@ -828,8 +970,8 @@ __global__ void __launch_bounds__(kThreads) k_dual(const float* __restrict__ th,
   const long long stride = (long long)gridDim.x * kThreads;
   for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n4; i += stride) {
     float4 t = ldcs4(th + 4 * i), x = ldcs4(u + 4 * i), z = ldcs4(zn + 4 * i);
-    st4(u + 4 * i, make_float4(dual1(x.x, t.x, z.x), dual1(x.y, t.y, z.y), dual1(x.z, t.z, z.z),
-                               dual1(x.w, t.w, z.w)));
+    stcs4(u + 4 * i, make_float4(dual1(x.x, t.x, z.x), dual1(x.y, t.y, z.y), dual1(x.z, t.z, z.z),
+                                 dual1(x.w, t.w, z.w)));
   }
   for (long long i = 4 * n4 + blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += stride)
     u[i] = dual1(u[i], th[i], zn[i]);
@@ -879,7 +1021,9 @@ __global__ void k_count_diff(const uint8_t* __restrict__ a, const uint8_t* __res
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(c, cnt);
 }
 
-static int small_grid(long long n) { return (int)std::min<long long>(std::max<long long>((n + 255) / 256, 1), 148LL * 8); }
+static int small_grid(long long n) {
+  return (int)std::min<long long>(std::max<long long>((n + 255) / 256, 1), 148LL * 8);
+}
 
 void launch_nonzero(const float* t, long long n, uint8_t* out, cudaStream_t st) {
   if (n > 0) k_nonzero<<<small_grid(n), 256, 0, st>>>(t, n, out);

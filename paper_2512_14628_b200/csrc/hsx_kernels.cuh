@@ -43,6 +43,7 @@ struct DevLayer {
   long long mword;  // mask word offset, -1 for dense layers
   long long okeep;  // offset of this layer's K_out flags / positions
   long long ikeep;  // offset of this layer's K_in flags / positions
+  long long cpoff;  // offset of this layer's column maps (colpos / colkeep), multiple of 4
   long long goff[kMaxPasses];  // offset into norms / keep flags per pass
   long long poff[kMaxPasses];  // offset into group-norm partials per pass
   int rows, cin, k, L;         // rank-4: c_out, c_in, kh*kw, c_in*kh*kw; rank-2: d0, d1, 1, d1
@@ -81,6 +82,14 @@ struct CandArgs {
   int sqcap;                           // doubles of the sq sub-tile region
 };
 
+// per-layer maps derived from the keep flags / keep sets (all prunable layers)
+struct Maps {
+  uint8_t* rowkeep;   // [sum rows]  AND of FILTER passes
+  uint8_t* colkeep;   // [sum L]     AND of CHANNEL / SHAPE passes
+  int* rowbase;       // [sum rows]  pos_out[o] * |K_in| * k, or -1
+  int* colpos;        // [sum L]     pos_in[c] * k + j, or -1
+};
+
 struct ElemArgs {
   const float* __restrict__ theta;
   float* __restrict__ u;
@@ -92,25 +101,27 @@ struct ElemArgs {
   float* __restrict__ z;
   const DevLayer* __restrict__ layers;
   const Item* __restrict__ items;
-  const int* __restrict__ pos_out;
-  const int* __restrict__ pos_in;
+  const int* __restrict__ rowbase;
+  const int* __restrict__ colpos;
   const long long* __restrict__ summary;
   float divisor;
 };
 
-void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st);
+void launch_candidate(const CandArgs& a, const Item* dense_items, int n_dense, const Item* norm_items,
+                      int n_norm, int frozen, size_t smem, cudaStream_t st);
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
                    double* norms, uint8_t* flags, size_t smem, cudaStream_t st);
+void launch_keepmaps(const DevLayer* layers, const int* list, int n, const uint8_t* f0,
+                     const uint8_t* f1, const uint8_t* f2, Maps maps, cudaStream_t st);
 void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
-                    uint32_t* mask, const uint8_t* f0, const uint8_t* f1, const uint8_t* f2,
-                    cudaStream_t st);
+                    uint32_t* mask, Maps maps, cudaStream_t st);
 void launch_mask_or(const uint32_t* g, int m, long long words, uint32_t* out, cudaStream_t st);
 void launch_keep_mark(const DevLayer* layers, const Item* items, int n_items, const uint32_t* uni,
                       const uint32_t* prev, uint8_t* oflag, uint8_t* iflag, long long* summary,
                       size_t smem, cudaStream_t st);
 void launch_keep_scan(const DevLayer* layers, const int* list, int n, int n_layers,
                       const uint8_t* oflag, const uint8_t* iflag, int* pos_out, int* pos_in,
-                      long long* summary, unsigned int* done, cudaStream_t st);
+                      Maps maps, long long* summary, unsigned int* done, cudaStream_t st);
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t st);

@@ -47,6 +47,8 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 constexpr long long kAlign = 32;        // arena layer alignment in elements (128 B)
 constexpr int kSubElems = 4096;         // target elements per shared-memory sub-tile
+constexpr int hsx_tile_rows = 32;       // candidate quad tiles: rows x column quads (hsx_kernels.cu)
+constexpr int hsx_tile_quads = 64;
 constexpr long long kItemElems = 8192;  // elements per streaming work item
 constexpr long long kNormItemElems = 16384;  // minimum elements per group-norm row tile
 constexpr long long kWordItem = 512;    // mask words per keep-mark item
@@ -84,15 +86,15 @@ struct hsx_plan {
   long long ktotal[2] = {0, 0};
   long long ctotal = 0;  // column-map entries (sum of L over prunable layers, padded to 4)
   std::vector<DevLayer> layers;
-  std::vector<Item> cand_dense, cand_norm, elem_items, proj_items, word_items;
+  std::vector<Item> cand_dyn, elem_items, proj_items, word_items;
   std::vector<int> pass_list[hsx::kMaxPasses];
   std::vector<int> prunable;
   size_t cand_smem = 0, select_smem[hsx::kMaxPasses] = {0, 0, 0}, mark_smem = 0;
   int sqcap = 0;
   // device
   DevLayer* d_layers = nullptr;
-  Item *d_cand = nullptr, *d_cand_norm = nullptr, *d_elem = nullptr, *d_proj = nullptr,
-       *d_word = nullptr;
+  Item *d_cand = nullptr, *d_elem = nullptr, *d_proj = nullptr, *d_word = nullptr;
+  unsigned int* d_layer_done = nullptr;
   int* d_pass[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
   double* d_partials[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
@@ -106,7 +108,7 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_layers, d_cand, d_cand_norm, d_elem, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_elem, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done, maps.rowkeep, maps.colkeep,
                     maps.rowbase, maps.colpos};
     for (void* p : ptrs)
@@ -137,7 +139,8 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   p->n_layers = n;
   long long off = 0, mword = 0, okeep = 0, ikeep = 0, cpoff = 0;
   long long goff[hsx::kMaxPasses] = {0, 0, 0}, poff[hsx::kMaxPasses] = {0, 0, 0};
-  int sqcap = 0, gmax = 0, quadcap = 0;
+  int sqcap = 0, gmax = 0, quadcap = 0, lmax = 1024;
+  std::vector<Item> dense_items;
   size_t mark_smem = 0;
   p->summary.assign((size_t)n * HSX_SUM_COLS + 1, 0);
   for (int l = 0; l < n; ++l) {
@@ -183,32 +186,48 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         ly.group[q] = g;
         ly.keep[q] = d.keep[q];
         ly.G[q] = G;
-        if (g != HSX_GROUP_FILTER) gmax = std::max(gmax, G);
       }
       ly.rsub = std::max(1, kSubElems / ly.L);
-      sqcap = std::max(sqcap, ly.rsub * ly.L);
-      quadcap = std::max(quadcap, std::max(ly.L, 1024));
-      // rows per candidate item: >= 8K elements and partials <= ~1/16 of the item's bytes
-      int gch = 0;
-      for (int q = 0; q < ly.ncons; ++q)
-        if (ly.group[q] != HSX_GROUP_FILTER) gch = std::max(gch, ly.G[q]);
-      long long rows_item = std::max<long long>((kNormItemElems + ly.L - 1) / ly.L, (16LL * gch + ly.L - 1) / ly.L);
-      rows_item = (rows_item + ly.rsub - 1) / ly.rsub * ly.rsub;
-      rows_item = std::min<long long>(rows_item, ly.rows);
-      ly.nparts = (int)((ly.rows + rows_item - 1) / rows_item);
-      for (int pt = 0; pt < ly.nparts; ++pt) {
-        Item it;
-        it.layer = l;
-        it.part = pt;
-        it.begin = pt * rows_item * ly.L;
-        it.end = std::min<long long>((pt + 1) * rows_item, ly.rows) * ly.L;
-        p->cand_norm.push_back(it);
+      // quad tiling when every pass groups columns (CHANNEL / SHAPE) and rows are
+      // a multiple of 4 elements; otherwise row tiling (FILTER, stems)
+      bool quads = (ly.L & 3) == 0;
+      for (int q = 0; q < ly.ncons; ++q) quads = quads && ly.group[q] != HSX_GROUP_FILTER;
+      ly.tiling = quads ? 1 : 0;
+      ly.pidx = (int)p->prunable.size();
+      if (quads) {
+        const int tq = hsx_tile_quads, tr = hsx_tile_rows;
+        const int nchunks = (ly.L / 4 + tq - 1) / tq;
+        ly.nparts = (ly.rows + tr - 1) / tr;
+        for (int pt = 0; pt < ly.nparts; ++pt)
+          for (int cc = 0; cc < nchunks; ++cc) {
+            Item it{l, pt, cc, 0, (long long)pt * tr, std::min<long long>((long long)(pt + 1) * tr, ly.rows)};
+            p->cand_dyn.push_back(it);
+          }
+        quadcap = std::max(quadcap, 4 * tq * (256 / tq));
+        lmax = std::max(lmax, ly.L);
+      } else {
+        sqcap = std::max(sqcap, ly.rsub * ly.L);
+        for (int q = 0; q < ly.ncons; ++q)
+          if (ly.group[q] != HSX_GROUP_FILTER) gmax = std::max(gmax, ly.G[q]);
+        int gch = 0;
+        for (int q = 0; q < ly.ncons; ++q)
+          if (ly.group[q] != HSX_GROUP_FILTER) gch = std::max(gch, ly.G[q]);
+        // rows per tile: >= 16K elements and partials <= ~1/16 of the tile's bytes
+        long long rows_item = std::max<long long>((kNormItemElems + ly.L - 1) / ly.L, (16LL * gch + ly.L - 1) / ly.L);
+        rows_item = (rows_item + ly.rsub - 1) / ly.rsub * ly.rsub;
+        rows_item = std::min<long long>(rows_item, ly.rows);
+        ly.nparts = (int)((ly.rows + rows_item - 1) / rows_item);
+        for (int pt = 0; pt < ly.nparts; ++pt) {
+          Item it{l, pt, 0, 0, pt * rows_item * ly.L, std::min<long long>((pt + 1) * rows_item, ly.rows) * ly.L};
+          p->cand_dyn.push_back(it);
+        }
       }
       for (int q = 0; q < ly.ncons; ++q) {
         ly.goff[q] = goff[q];
         goff[q] += ly.G[q];
         ly.poff[q] = poff[q];
-        poff[q] += ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * ly.G[q];
+        poff[q] += quads ? (long long)ly.nparts * ly.L
+                         : (ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * ly.G[q]);
         p->pass_list[q].push_back(l);
         p->max_passes = std::max(p->max_passes, q + 1);
       }
@@ -222,23 +241,24 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       cpoff += (ly.L + 3) / 4 * 4;
       p->prunable.push_back(l);
       for (long long b = 0; b < ly.n; b += kItemElems) {
-        Item it{l, 0, b, std::min(ly.n, b + kItemElems)};
+        Item it{l, 0, 0, 0, b, std::min(ly.n, b + kItemElems)};
         p->proj_items.push_back(it);
       }
+      const int nwi = (int)((ly.n + kWordItem * 32 - 1) / (kWordItem * 32));
       for (long long b = 0; b < ly.n; b += kWordItem * 32) {
-        Item it{l, 0, b, std::min(ly.n, b + kWordItem * 32)};
+        Item it{l, ly.pidx, nwi, 0, b, std::min(ly.n, b + kWordItem * 32)};
         p->word_items.push_back(it);
         long long r_lo = b / ly.L, r_hi = (it.end - 1) / ly.L;
         mark_smem = std::max<size_t>(mark_smem, (size_t)ly.cin + (size_t)(r_hi - r_lo + 1));
       }
     } else {
       for (long long b = 0; b < ly.n; b += kItemElems) {
-        Item it{l, 0, b, std::min(ly.n, b + kItemElems)};
-        p->cand_dense.push_back(it);
+        Item it{l, 0, 0, 0, b, std::min(ly.n, b + kItemElems)};
+        dense_items.push_back(it);
       }
     }
     for (long long b = 0; b < ly.n; b += kItemElems) {
-      Item it{l, 0, b, std::min(ly.n, b + kItemElems)};
+      Item it{l, 0, 0, 0, b, std::min(ly.n, b + kItemElems)};
       p->elem_items.push_back(it);
     }
     // initial keep sets: everything kept (all-ones initial masks, consensus.py:418)
@@ -247,6 +267,8 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     srow[HSX_SUM_ELEMS] = ly.n;
     p->layers.push_back(ly);
   }
+  // dynamic candidate launch: group-norm tiles first, short dense items fill the tail
+  p->cand_dyn.insert(p->cand_dyn.end(), dense_items.begin(), dense_items.end());
   // the last layer needs no trailing pad: arenas may be exactly-sized tensors
   if (n > 0) off = p->layers.back().off + p->layers.back().n;
   p->arena = off;
@@ -262,7 +284,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       int G = p->layers[l].G[q];
       while (gp < G) gp <<= 1;
     }
-    p->select_smem[q] = (size_t)gp * (sizeof(double) + sizeof(int)) + 8 + 1024 * sizeof(double);
+    p->select_smem[q] = (size_t)gp * (sizeof(double) + sizeof(int)) + 8 + (size_t)lmax * sizeof(double);
   }
   p->sqcap = sqcap;
   p->cand_smem = (size_t)std::max(sqcap + gmax, quadcap) * sizeof(double);
@@ -275,8 +297,8 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
 int upload_plan(hsx_plan* p) {
   int rc;
   if ((rc = upload(&p->d_layers, p->layers))) return rc;
-  if ((rc = upload(&p->d_cand, p->cand_dense))) return rc;
-  if ((rc = upload(&p->d_cand_norm, p->cand_norm))) return rc;
+  if ((rc = upload(&p->d_cand, p->cand_dyn))) return rc;
+  if ((rc = alloc0(&p->d_layer_done, (long long)p->prunable.size()))) return rc;
   if ((rc = upload(&p->d_elem, p->elem_items))) return rc;
   if ((rc = upload(&p->d_proj, p->proj_items))) return rc;
   if ((rc = upload(&p->d_word, p->word_items))) return rc;
@@ -446,8 +468,13 @@ int hsx_candidate(hsx_plan* p, const float* sum, const float* theta, const float
   a.fmask = frozen_mask;
   a.pass = 0;
   a.partials = p->d_partials[0];
-  hsx::launch_candidate(a, p->d_cand, (int)p->cand_dense.size(), p->d_cand_norm,
-                        (int)p->cand_norm.size(), frozen_mask != nullptr, p->cand_smem, S(stream));
+  if (frozen_mask) {
+    a.items = p->d_elem;  // frozen: plain elementwise over every layer
+    hsx::launch_candidate(a, (int)p->elem_items.size(), 1, 0, S(stream));
+  } else {
+    a.items = p->d_cand;
+    hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
+  }
   HSX_LAUNCHED("candidate");
   return HSX_OK;
 }
@@ -461,8 +488,8 @@ int hsx_candidate_renorm(hsx_plan* p, int32_t pass, const float* sum, const floa
   a.pass = pass;
   a.partials = p->d_partials[pass];
   for (int q = 0; q < pass; ++q) a.flags[q] = p->d_flags[q];
-  hsx::launch_candidate(a, p->d_cand, 0, p->d_cand_norm, (int)p->cand_norm.size(), 0, p->cand_smem,
-                        S(stream));
+  a.items = p->d_cand;
+  hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
   HSX_LAUNCHED("candidate_renorm");
   return HSX_OK;
 }
@@ -472,8 +499,9 @@ int hsx_select(hsx_plan* p, int32_t pass, void* stream) {
   if (pass < 0 || pass >= hsx::kMaxPasses) return fail(HSX_EINVAL, "pass %d out of range", pass);
   int n = (int)p->pass_list[pass].size();
   if (n == 0) return HSX_OK;
+  hsx::FlagPtrs fl = {{p->d_flags[0], p->d_flags[1], p->d_flags[2]}};
   hsx::launch_select(p->d_layers, p->d_pass[pass], n, pass, p->d_partials[pass], p->d_norms[pass],
-                     p->d_flags[pass], p->select_smem[pass], S(stream));
+                     fl, p->maps, p->select_smem[pass], S(stream));
   HSX_LAUNCHED("select");
   return HSX_OK;
 }
@@ -491,9 +519,6 @@ int hsx_read_groups(const hsx_plan* p, int32_t pass, double* norms, uint8_t* fla
 
 int hsx_project(hsx_plan* p, float* z_node, uint32_t* local_mask, void* stream) {
   if (!p || !z_node || (!local_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
-  hsx::launch_keepmaps(p->d_layers, p->d_prunable, (int)p->prunable.size(), p->d_flags[0],
-                       p->d_flags[1], p->d_flags[2], p->maps, S(stream));
-  HSX_LAUNCHED("keepmaps");
   hsx::launch_project(p->d_layers, p->d_proj, (int)p->proj_items.size(), z_node, local_mask, p->maps,
                       S(stream));
   HSX_LAUNCHED("project");
@@ -518,13 +543,23 @@ int hsx_keep_sets(hsx_plan* p, const uint32_t* union_mask, const uint32_t* prev_
   // zero the drift / popcount columns of every row
   HSX_CUDA(cudaMemset2DAsync(p->d_summary + HSX_SUM_DRIFT, HSX_SUM_COLS * sizeof(long long), 0,
                              2 * sizeof(long long), p->n_layers, st));
-  hsx::launch_keep_mark(p->d_layers, p->d_word, (int)p->word_items.size(), union_mask, prev_mask,
-                        p->d_oflag, p->d_iflag, p->d_summary, p->mark_smem, st);
-  HSX_LAUNCHED("keep_mark");
-  hsx::launch_keep_scan(p->d_layers, p->d_prunable, (int)p->prunable.size(), p->n_layers,
-                        p->d_oflag, p->d_iflag, p->d_pos_out, p->d_pos_in, p->maps, p->d_summary,
-                        p->d_done, st);
-  HSX_LAUNCHED("keep_scan");
+  hsx::KeepArgs ka;
+  ka.layers = p->d_layers;
+  ka.items = p->d_word;
+  ka.uni = union_mask;
+  ka.prev = prev_mask;
+  ka.oflag = p->d_oflag;
+  ka.iflag = p->d_iflag;
+  ka.pos_out = p->d_pos_out;
+  ka.pos_in = p->d_pos_in;
+  ka.maps = p->maps;
+  ka.summary = p->d_summary;
+  ka.layer_done = p->d_layer_done;
+  ka.done = p->d_done;
+  ka.n_layers = p->n_layers;
+  ka.n_prunable = (int)p->prunable.size();
+  hsx::launch_keep_sets(ka, (int)p->word_items.size(), p->mark_smem, st);
+  HSX_LAUNCHED("keep_sets");
   return HSX_OK;
 }
 

@@ -91,35 +91,27 @@ __device__ __forceinline__ bool kept_by(const DevLayer& ly, const uint8_t* const
   return keep;
 }
 
-// K1a: elementwise candidate (dense layers; every layer in frozen mode, where
-// prunable layers get cand * global mask, consensus.py:177-180)
-__global__ void __launch_bounds__(kThreads) k_cand_dense(CandArgs p, int frozen) {
-  const Item it = p.items[blockIdx.x];
-  const DevLayer& ly = p.layers[it.layer];
+// K1a: elementwise candidate over [begin, end) of one layer (dense layers; every
+// layer in frozen mode, where prunable layers get cand * global mask,
+// consensus.py:177-180)
+__device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long long begin, long long end,
+                                 int frozen) {
   const bool masked = frozen && ly.ncons > 0 && p.fmask != nullptr;
-  if (it.begin & 3) {  // row tiles of layers with c_in*kh*kw % 4 != 0: scalar path
-    for (long long e = it.begin + threadIdx.x; e < it.end; e += kThreads) {
-      double c = cand_elem(p, ly.off + e, ly);
-      if (masked && !((p.fmask[ly.mword + (e >> 5)] >> (e & 31)) & 1u)) c = c * 0.0;
-      p.zn[ly.off + e] = (float)c;
-    }
-    return;
-  }
   constexpr int U = 2;
-  const long long nq = (it.end - it.begin + 3) >> 2;
+  const long long nq = (end - begin + 3) >> 2;
   for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * U) {
     In4 in[U];
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
       long long q = q0 + (long long)uu * kThreads;
-      long long e = it.begin + 4 * q;
+      long long e = begin + 4 * q;
       if (q < nq && e + 3 < ly.n) in[uu] = load_in4(p, ly.off + e);
     }
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
       long long q = q0 + (long long)uu * kThreads;
       if (q >= nq) continue;
-      long long e = it.begin + 4 * q;
+      long long e = begin + 4 * q;
       uint32_t bits = masked ? p.fmask[ly.mword + (e >> 5)] : 0u;
       if (e + 3 < ly.n) {
         float4 out;
@@ -141,80 +133,70 @@ __global__ void __launch_bounds__(kThreads) k_cand_dense(CandArgs p, int frozen)
   }
 }
 
-// K1b, CHANNEL / SHAPE groups with c_in*kh*kw % 4 == 0 (every ResNet conv but the
-// stem): each thread owns a fixed column quad and walks rows of the tile, so the
-// fp64 column sums of squares stay in registers; one shared-memory pass then
-// folds the row phases and the kh*kw columns of each channel in a fixed order.
-__device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, double* smem) {
+// K1b quad tiles (CHANNEL / SHAPE groups, c_in*kh*kw % 4 == 0 — every ResNet conv
+// but the 7x7 stem): a tile is 32 rows x 64 column quads; thread t owns quad
+// (t & 63) and row phase (t >> 6), so its fp64 column sums of squares stay in
+// registers; the 4 phases fold in shared memory in a fixed order and the tile
+// writes one fp64 partial per column (the channel fold happens in K2).
+constexpr int kTileQuads = 64;
+
+__device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, double* cs) {
   const int pass = p.pass;
-  const int grp = ly.group[pass];
-  const int G = ly.G[pass];
   const int L = ly.L;
   const int Q = L >> 2;
-  const long long r0 = it.begin / L;
-  const int nrows = (int)((it.end - it.begin) / L);
-  const int RP = Q >= kThreads ? 1 : kThreads / Q;  // row phases
-  const int t = threadIdx.x;
-  const int ph = Q >= kThreads ? 0 : t / Q;
-  // smem layout: colsum[RP][L]
-  if (ph < RP) {
-    for (int j = (Q >= kThreads ? t : t % Q); j < Q; j += (Q >= kThreads ? kThreads : Q)) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      constexpr int U = 2;
-      for (int r = ph; r < nrows; r += RP * U) {
-        In4 in[U];
+  const int jj = threadIdx.x & (kTileQuads - 1);
+  const int ph = threadIdx.x / kTileQuads;  // 0..3
+  const int j = it.chunk * kTileQuads + jj;
+  const long long r0 = it.begin, r1 = it.end;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (j < Q) {
+    constexpr int U = 2;
+    constexpr int RP = kThreads / kTileQuads;
+    for (long long r = r0 + ph; r < r1; r += RP * U) {
+      In4 in[U];
 #pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-          int rr = r + uu * RP;
-          if (rr < nrows) in[uu] = load_in4(p, ly.off + (r0 + rr) * (long long)L + 4 * j);
-        }
-#pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-          int rr = r + uu * RP;
-          if (rr >= nrows) break;
-          long long e = (r0 + rr) * (long long)L + 4 * j;
-          double c0 = cand4(p, in[uu], 0, ly), c1 = cand4(p, in[uu], 1, ly);
-          double c2 = cand4(p, in[uu], 2, ly), c3 = cand4(p, in[uu], 3, ly);
-          if (pass > 0) {
-            if (!kept_by(ly, p.flags, pass, e + 0)) c0 = 0.0;
-            if (!kept_by(ly, p.flags, pass, e + 1)) c1 = 0.0;
-            if (!kept_by(ly, p.flags, pass, e + 2)) c2 = 0.0;
-            if (!kept_by(ly, p.flags, pass, e + 3)) c3 = 0.0;
-          } else {
-            st4(p.zn + ly.off + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
-          }
-          a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
-          a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
-          a2 = __dadd_rn(a2, __dmul_rn(c2, c2));
-          a3 = __dadd_rn(a3, __dmul_rn(c3, c3));
-        }
+      for (int uu = 0; uu < U; ++uu) {
+        long long rr = r + uu * RP;
+        if (rr < r1) in[uu] = load_in4(p, ly.off + rr * L + 4 * j);
       }
-      double* cs = smem + (long long)ph * L + 4 * j;
-      cs[0] = a0; cs[1] = a1; cs[2] = a2; cs[3] = a3;
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        long long rr = r + uu * RP;
+        if (rr >= r1) break;
+        long long e = rr * L + 4 * j;
+        double c0 = cand4(p, in[uu], 0, ly), c1 = cand4(p, in[uu], 1, ly);
+        double c2 = cand4(p, in[uu], 2, ly), c3 = cand4(p, in[uu], 3, ly);
+        if (pass > 0) {
+          if (!kept_by(ly, p.flags, pass, e + 0)) c0 = 0.0;
+          if (!kept_by(ly, p.flags, pass, e + 1)) c1 = 0.0;
+          if (!kept_by(ly, p.flags, pass, e + 2)) c2 = 0.0;
+          if (!kept_by(ly, p.flags, pass, e + 3)) c3 = 0.0;
+        } else {
+          st4(p.zn + ly.off + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
+        }
+        a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
+        a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
+        a2 = __dadd_rn(a2, __dmul_rn(c2, c2));
+        a3 = __dadd_rn(a3, __dmul_rn(c3, c3));
+      }
     }
   }
+  double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
+  mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
-  double* out = p.partials + ly.poff[pass] + (long long)it.part * G;
-  if (grp == kChannel) {
-    const int k = ly.k;
-    for (int c = t; c < ly.cin; c += kThreads) {
-      double s = 0.0;
-      for (int q = 0; q < RP; ++q)
-        for (int jj = 0; jj < k; ++jj) s += smem[(long long)q * L + c * k + jj];
-      out[c] = s;
-    }
-  } else {
-    for (int col = t; col < L; col += kThreads) {
-      double s = 0.0;
-      for (int q = 0; q < RP; ++q) s += smem[(long long)q * L + col];
-      out[col] = s;
-    }
+  const int col = it.chunk * 4 * kTileQuads + threadIdx.x;  // one column per thread
+  if (col < L) {
+    double s = cs[threadIdx.x];
+#pragma unroll
+    for (int q = 1; q < kThreads / kTileQuads; ++q) s += cs[q * 4 * kTileQuads + threadIdx.x];
+    p.partials[ly.poff[pass] + (long long)it.part * L + col] = s;
   }
 }
 
-// K1b general path (FILTER groups, or rows not a multiple of 4 elements):
-// squares of sub-tiles of rows staged in shared memory.
-__device__ void cand_tile_smem(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq,
+// K1b row tiles (FILTER groups, composite plans mixing FILTER, rows not a
+// multiple of 4 elements): squares of sub-tiles of rows staged in shared
+// memory; partials per group ([part][G]) or per row (FILTER).
+__device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq,
                                double* acc) {
   const int pass = p.pass;
   const int grp = ly.group[pass];
@@ -242,7 +224,7 @@ __device__ void cand_tile_smem(const CandArgs& p, const DevLayer& ly, const Item
       for (int c = threadIdx.x; c < ly.cin; c += kThreads) {
         double s = 0.0;
         for (int r = 0; r < nr; ++r)
-          for (int j = 0; j < k; ++j) s += sq[r * L + c * k + j];
+          for (int jx = 0; jx < k; ++jx) s += sq[r * L + c * k + jx];
         acc[c] += s;
       }
     } else if (grp == kShape) {
@@ -267,34 +249,35 @@ __device__ void cand_tile_smem(const CandArgs& p, const DevLayer& ly, const Item
       p.partials[ly.poff[pass] + (long long)it.part * G + g] = acc[g];
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_cand_norm(CandArgs p) {
+__global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int frozen) {
   extern __shared__ double smem[];
   const Item it = p.items[blockIdx.x];
   const DevLayer& ly = p.layers[it.layer];
+  if (frozen || ly.ncons == 0) {
+    if (p.pass > 0) return;
+    if (it.begin & 3) {  // ranges of layers with c_in*kh*kw % 4 != 0: scalar path
+      const bool masked = frozen && ly.ncons > 0 && p.fmask != nullptr;
+      for (long long e = it.begin + threadIdx.x; e < it.end; e += kThreads) {
+        double c = cand_elem(p, ly.off + e, ly);
+        if (masked && !((p.fmask[ly.mword + (e >> 5)] >> (e & 31)) & 1u)) c = c * 0.0;
+        p.zn[ly.off + e] = (float)c;
+      }
+      return;
+    }
+    cand_elementwise(p, ly, it.begin, it.end, frozen);
+    return;
+  }
   if (ly.ncons <= p.pass) return;
-  if (ly.group[p.pass] != kFilter && (ly.L & 3) == 0)
+  if (ly.tiling == 1)
     cand_tile_quads(p, ly, it, smem);
   else
-    cand_tile_smem(p, ly, it, smem, smem + p.sqcap);
+    cand_tile_rows(p, ly, it, smem, smem + p.sqcap);
 }
 
-void launch_candidate(const CandArgs& a, const Item* dense_items, int n_dense, const Item* norm_items,
-                      int n_norm, int frozen, size_t smem, cudaStream_t st) {
-  if (n_dense > 0 && a.pass == 0) {
-    CandArgs d = a;
-    d.items = dense_items;
-    k_cand_dense<<<n_dense, kThreads, 0, st>>>(d, frozen);
-  }
-  if (n_norm > 0) {
-    CandArgs d = a;
-    d.items = norm_items;
-    if (frozen) {
-      k_cand_dense<<<n_norm, kThreads, 0, st>>>(d, frozen);
-    } else {
-      allow_smem(k_cand_norm, smem);
-      k_cand_norm<<<n_norm, kThreads, smem, st>>>(d);
-    }
-  }
+void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
+  if (n_items <= 0) return;
+  allow_smem(k_candidate, smem);
+  k_candidate<<<n_items, kThreads, smem, st>>>(a, frozen);
 }
 
 // ---------------------------------------------------------------------------
@@ -307,56 +290,62 @@ __device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
 }
 
 // shared memory: key[Gp] (double), idx[Gp] (int), fold[blockDim] (double)
+// shared memory: key[Gp] (double), idx[Gp] (int, padded), scratch[max(L, blockDim)] (double)
 __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ layers,
                                                  const int* __restrict__ list, int pass,
                                                  const double* __restrict__ partials,
-                                                 double* __restrict__ norms,
-                                                 uint8_t* __restrict__ flags) {
+                                                 double* __restrict__ norms, FlagPtrs flags, Maps m) {
   extern __shared__ double skey[];
   const DevLayer& ly = layers[list[blockIdx.x]];
   const int G = ly.G[pass];
+  const int grp = ly.group[pass];
   int Gp = 1;
   while (Gp < G) Gp <<= 1;
   int* sidx = reinterpret_cast<int*>(skey + Gp);
-  double* fold = reinterpret_cast<double*>(sidx + Gp + (Gp & 1));
-  const bool rowwise = ly.group[pass] == kFilter;
+  double* scratch = skey + Gp + (Gp + 1) / 2;
   const double* part = partials + ly.poff[pass];
   const int nt = blockDim.x;
-  // 1) squared norms. Row tiles are strided over T slices of threads (T = nt / W
-  //    with W groups per round, coalesced along groups); slices fold in order.
-  const int W = rowwise ? nt : min(nt, Gp);
-  const int T = nt / W;
-  for (int base = 0; base < Gp; base += W) {
-    const int g = base + (int)threadIdx.x % W;
-    const int sl = (int)threadIdx.x / W;
-    double s2 = 0.0;
-    if (g < G) {
-      if (rowwise) {
-        s2 = part[g];
-      } else {
-        double a0 = 0.0, a1 = 0.0;
-        int pt = sl;
-        for (; pt + T < ly.nparts; pt += 2 * T) {
-          a0 += part[(long long)pt * G + g];
-          a1 += part[(long long)(pt + T) * G + g];
-        }
-        if (pt < ly.nparts) a0 += part[(long long)pt * G + g];
-        s2 = a0 + a1;
+  const int t = threadIdx.x;
+  // 1) squared group norms from the K1 partials, fixed summation order
+  if (ly.tiling == 1) {
+    // per-column partials [nparts][L]: fold the row tiles per column (coalesced),
+    // then the kh*kw columns of each channel
+    const int L = ly.L;
+    for (int col = t; col < L; col += nt) {
+      double a0 = 0.0, a1 = 0.0;
+      int pt = 0;
+      for (; pt + 1 < ly.nparts; pt += 2) {
+        a0 += part[(long long)pt * L + col];
+        a1 += part[(long long)(pt + 1) * L + col];
       }
+      if (pt < ly.nparts) a0 += part[(long long)pt * L + col];
+      scratch[col] = a0 + a1;
     }
-    if (T > 1) {
-      fold[threadIdx.x] = s2;
-      __syncthreads();
-      if (sl == 0) {
-        double s = 0.0;
-        for (int q = 0; q < T; ++q) s += fold[q * W + (int)threadIdx.x];
-        s2 = s;
-      }
-      __syncthreads();
-    }
-    if (sl == 0 && g < Gp) {
+    __syncthreads();
+    for (int g = t; g < Gp; g += nt) {
       double key = -1.0;  // padding sorts after every norm (norms >= 0)
       if (g < G) {
+        double s2 = 0.0;
+        if (grp == kChannel)
+          for (int jx = 0; jx < ly.k; ++jx) s2 += scratch[g * ly.k + jx];
+        else
+          s2 = scratch[g];
+        key = sqrt(s2);
+        norms[ly.goff[pass] + g] = key;
+      }
+      skey[g] = key;
+      sidx[g] = g;
+    }
+  } else {
+    for (int g = t; g < Gp; g += nt) {
+      double key = -1.0;
+      if (g < G) {
+        double s2 = 0.0;
+        if (grp == kFilter) {
+          s2 = part[g];
+        } else {
+          for (int pt = 0; pt < ly.nparts; ++pt) s2 += part[(long long)pt * G + g];
+        }
         key = sqrt(s2);
         norms[ly.goff[pass] + g] = key;
       }
@@ -365,65 +354,56 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
     }
   }
   __syncthreads();
+  // 2) bitonic sort: norm descending, index ascending (stable argsort of -norms)
   for (int size = 2; size <= Gp; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < Gp; i += nt) {
-        int j = i ^ stride;
-        if (j > i) {
-          double ki = skey[i], kj = skey[j];
-          int ii = sidx[i], ij = sidx[j];
+      for (int i = t; i < Gp; i += nt) {
+        int jx = i ^ stride;
+        if (jx > i) {
+          double ki = skey[i], kj = skey[jx];
+          int ii = sidx[i], ij = sidx[jx];
           bool i_first = before(ki, ii, kj, ij);
           bool want_i_first = (i & size) == 0;
           if (i_first != want_i_first) {
-            skey[i] = kj; skey[j] = ki;
-            sidx[i] = ij; sidx[j] = ii;
+            skey[i] = kj; skey[jx] = ki;
+            sidx[i] = ij; sidx[jx] = ii;
           }
         }
       }
       __syncthreads();
     }
   }
+  uint8_t* fl = flags.f[pass];
   const int keep = ly.keep[pass];
-  for (int pos = threadIdx.x; pos < Gp; pos += nt) {
+  for (int pos = t; pos < Gp; pos += nt) {
     int g = sidx[pos];
-    if (g < G) flags[ly.goff[pass] + g] = pos < keep ? 1 : 0;
+    if (g < G) fl[ly.goff[pass] + g] = pos < keep ? 1 : 0;
+  }
+  if (pass != ly.ncons - 1) return;
+  __syncthreads();
+  // 3) keep maps for K3: rowkeep = AND of FILTER passes, colkeep = AND of
+  //    CHANNEL / SHAPE passes (block-local global writes are visible after the barrier)
+  for (int o = t; o < ly.rows; o += nt) {
+    uint8_t kp = 1;
+    for (int q = 0; q < ly.ncons; ++q)
+      if (ly.group[q] == kFilter) kp &= flags.f[q][ly.goff[q] + o];
+    m.rowkeep[ly.okeep + o] = kp;
+  }
+  for (int col = t; col < ly.L; col += nt) {
+    uint8_t kp = 1;
+    for (int q = 0; q < ly.ncons; ++q) {
+      if (ly.group[q] == kChannel) kp &= flags.f[q][ly.goff[q] + col / ly.k];
+      else if (ly.group[q] == kShape) kp &= flags.f[q][ly.goff[q] + col];
+    }
+    m.colkeep[ly.cpoff + col] = kp;
   }
 }
 
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
-                   double* norms, uint8_t* flags, size_t smem, cudaStream_t st) {
+                   double* norms, FlagPtrs flags, Maps maps, size_t smem, cudaStream_t st) {
   if (n <= 0) return;
   allow_smem(k_select, smem);
-  k_select<<<n, 1024, smem, st>>>(layers, list, pass, partials, norms, flags);
-}
-
-// ---------------------------------------------------------------------------
-// keep maps: rowkeep = AND of FILTER passes, colkeep = AND of CHANNEL/SHAPE passes
-// ---------------------------------------------------------------------------
-
-__global__ void k_keepmaps(const DevLayer* __restrict__ layers, const int* __restrict__ list,
-                           const uint8_t* f0, const uint8_t* f1, const uint8_t* f2, Maps m) {
-  const DevLayer& ly = layers[list[blockIdx.x]];
-  const uint8_t* flags[kMaxPasses] = {f0, f1, f2};
-  for (int o = threadIdx.x; o < ly.rows; o += blockDim.x) {
-    uint8_t keep = 1;
-    for (int q = 0; q < ly.ncons; ++q)
-      if (ly.group[q] == kFilter) keep &= flags[q][ly.goff[q] + o];
-    m.rowkeep[ly.okeep + o] = keep;
-  }
-  for (int col = threadIdx.x; col < ly.L; col += blockDim.x) {
-    uint8_t keep = 1;
-    for (int q = 0; q < ly.ncons; ++q) {
-      if (ly.group[q] == kChannel) keep &= flags[q][ly.goff[q] + col / ly.k];
-      else if (ly.group[q] == kShape) keep &= flags[q][ly.goff[q] + col];
-    }
-    m.colkeep[ly.cpoff + col] = keep;
-  }
-}
-
-void launch_keepmaps(const DevLayer* layers, const int* list, int n, const uint8_t* f0,
-                     const uint8_t* f1, const uint8_t* f2, Maps maps, cudaStream_t st) {
-  if (n > 0) k_keepmaps<<<n, 512, 0, st>>>(layers, list, f0, f1, f2, maps);
+  k_select<<<n, 1024, smem, st>>>(layers, list, pass, partials, norms, flags, maps);
 }
 
 // ---------------------------------------------------------------------------
@@ -559,80 +539,15 @@ void launch_mask_or(const uint32_t* g, int m, long long words, uint32_t* out, cu
 }
 
 // ---------------------------------------------------------------------------
-// K5a keep marks: K_out / K_in "any" flags from the union mask, popcounts.
-// shrinkage.py:45-58 (derive_keep_sets), sparsity.py:118-122 (drift numerator)
-// ---------------------------------------------------------------------------
-
-__global__ void __launch_bounds__(kThreads) k_keep_mark(const DevLayer* __restrict__ layers,
-                                                        const Item* __restrict__ items,
-                                                        const uint32_t* __restrict__ uni,
-                                                        const uint32_t* __restrict__ prev,
-                                                        uint8_t* __restrict__ oflag,
-                                                        uint8_t* __restrict__ iflag,
-                                                        long long* __restrict__ summary) {
-  extern __shared__ uint8_t sflag[];
-  const Item it = items[blockIdx.x];
-  const DevLayer& ly = layers[it.layer];
-  const long long w0 = it.begin >> 5, w1 = (it.end + 31) >> 5;
-  const long long r_lo = it.begin / ly.L;
-  const long long r_hi = (std::min(it.end, ly.n) - 1) / ly.L;  // inclusive
-  const int nr = (int)(r_hi - r_lo + 1);
-  uint8_t* s_in = sflag;
-  uint8_t* s_out = sflag + ly.cin;
-  for (int i = threadIdx.x; i < ly.cin + nr; i += kThreads) sflag[i] = 0;
-  __syncthreads();
-  unsigned long long pop = 0, drift = 0;
-  for (long long w = w0 + threadIdx.x; w < w1; w += kThreads) {
-    long long e0 = w << 5;
-    long long nvalid = ly.n - e0;
-    uint32_t valid = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
-    uint32_t x = uni[ly.mword + w] & valid;
-    pop += __popc(x);
-    if (prev) drift += __popc((x ^ prev[ly.mword + w]) & valid);
-    while (x) {
-      int b = __ffs(x) - 1;
-      unsigned e = (unsigned)(e0 + b);
-      unsigned o = fdiv(e, ly.divL);
-      unsigned col = e - o * (unsigned)ly.L;
-      unsigned c = fdiv(col, ly.divk);
-      unsigned j = col - c * (unsigned)ly.k;
-      s_out[o - r_lo] = 1;
-      s_in[c] = 1;
-      int skip = b + (int)((unsigned)ly.k - j);  // rest of this (o, c) kernel run
-      x = skip >= 32 ? 0u : (x & ~((1u << skip) - 1u));
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    pop += __shfl_xor_sync(kFull, pop, off);
-    drift += __shfl_xor_sync(kFull, drift, off);
-  }
-  const int lane = threadIdx.x & 31;
-  const long long srow = (long long)it.layer * kSumCols;
-  if (lane == 0) {
-    if (pop) atomicAdd(reinterpret_cast<unsigned long long*>(summary + srow + 5), pop);
-    if (drift) atomicAdd(reinterpret_cast<unsigned long long*>(summary + srow + 4), drift);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < ly.cin; i += kThreads)
-    if (s_in[i]) iflag[ly.ikeep + i] = 1;
-  for (int i = threadIdx.x; i < nr; i += kThreads)
-    if (s_out[i]) oflag[ly.okeep + r_lo + i] = 1;
-}
-
-void launch_keep_mark(const DevLayer* layers, const Item* items, int n_items, const uint32_t* uni,
-                      const uint32_t* prev, uint8_t* oflag, uint8_t* iflag, long long* summary,
-                      size_t smem, cudaStream_t st) {
-  if (n_items <= 0) return;
-  allow_smem(k_keep_mark, smem);
-  k_keep_mark<<<n_items, kThreads, smem, st>>>(layers, items, uni, prev, oflag, iflag, summary);
-}
-
-// ---------------------------------------------------------------------------
-// K5b keep scan: positions of kept filters / channels (exclusive prefix sums),
-// row bases and column positions of the compact rectangle, payload sizes; the
-// last CTA lays out the flat buffer in layer order (bucketize's
-// concatenation, transport.py:239-280).
+// K5 keep sets from the union mask, one launch (shrinkage.py:45-58,
+// derive_keep_sets; sparsity.py:118-122 drift numerator; transport.py:239-280
+// concatenation order):
+//  a) every CTA marks the K_out / K_in "any" flags of its word range and
+//     accumulates popcount(union) and popcount(union ^ prev);
+//  b) the last CTA to finish a layer scans its flags into positions, row bases
+//     and column positions of the compact rectangle and the payload size;
+//  c) the last layer to finish lays out the flat buffer (exclusive scan of
+//     payload sizes over all layers, in layer order).
 // ---------------------------------------------------------------------------
 
 __device__ int block_exclusive_scan(int x, int* warp_tot, int* total) {
@@ -663,13 +578,15 @@ __device__ int block_exclusive_scan(int x, int* warp_tot, int* total) {
   return r;
 }
 
+// exclusive positions of set flags (-1 for clear ones); flags read through L2
+// (written by other CTAs of this launch)
 __device__ int scan_flags(const uint8_t* flags, int n, int* pos) {
   __shared__ int warp_tot[32];
   __shared__ int total;
   int carry = 0;
   for (int base = 0; base < n; base += blockDim.x) {
     int i = base + threadIdx.x;
-    int f = (i < n && flags[i]) ? 1 : 0;
+    int f = (i < n && __ldcg(flags + i)) ? 1 : 0;
     int ex = block_exclusive_scan(f, warp_tot, &total);
     if (i < n) pos[i] = f ? carry + ex : -1;
     carry += total;
@@ -678,50 +595,99 @@ __device__ int scan_flags(const uint8_t* flags, int n, int* pos) {
   return carry;
 }
 
-__global__ void __launch_bounds__(1024) k_keep_scan(const DevLayer* __restrict__ layers,
-                                                    const int* __restrict__ list, int n_layers,
-                                                    const uint8_t* __restrict__ oflag,
-                                                    const uint8_t* __restrict__ iflag,
-                                                    int* __restrict__ pos_out,
-                                                    int* __restrict__ pos_in, Maps m,
-                                                    long long* summary, unsigned int* done) {
-  const int l = list[blockIdx.x];
-  const DevLayer& ly = layers[l];
-  int n_out = scan_flags(oflag + ly.okeep, ly.rows, pos_out + ly.okeep);
-  int n_in = scan_flags(iflag + ly.ikeep, ly.cin, pos_in + ly.ikeep);
+__global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
+  extern __shared__ uint8_t sflag[];
+  const Item it = a.items[blockIdx.x];
+  const int l = it.layer;
+  const DevLayer& ly = a.layers[l];
+  const long long w0 = it.begin >> 5, w1 = (it.end + 31) >> 5;
+  const long long r_lo = it.begin / ly.L;
+  const long long r_hi = (std::min(it.end, ly.n) - 1) / ly.L;  // inclusive
+  const int nr = (int)(r_hi - r_lo + 1);
+  uint8_t* s_in = sflag;
+  uint8_t* s_out = sflag + ly.cin;
+  for (int i = threadIdx.x; i < ly.cin + nr; i += kThreads) sflag[i] = 0;
   __syncthreads();
-  const int rowlen = n_in * ly.k;
-  for (int o = threadIdx.x; o < ly.rows; o += blockDim.x) {
-    int po = pos_out[ly.okeep + o];
-    m.rowbase[ly.okeep + o] = po >= 0 ? po * rowlen : -1;
+  // a) marks and popcounts
+  unsigned long long pop = 0, drift = 0;
+  for (long long w = w0 + threadIdx.x; w < w1; w += kThreads) {
+    long long e0 = w << 5;
+    long long nvalid = ly.n - e0;
+    uint32_t valid = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
+    uint32_t x = a.uni[ly.mword + w] & valid;
+    pop += __popc(x);
+    if (a.prev) drift += __popc((x ^ a.prev[ly.mword + w]) & valid);
+    while (x) {
+      int b = __ffs(x) - 1;
+      unsigned e = (unsigned)(e0 + b);
+      unsigned o = fdiv(e, ly.divL);
+      unsigned col = e - o * (unsigned)ly.L;
+      unsigned c = fdiv(col, ly.divk);
+      unsigned jx = col - c * (unsigned)ly.k;
+      s_out[o - r_lo] = 1;
+      s_in[c] = 1;
+      int skip = b + (int)((unsigned)ly.k - jx);  // rest of this (o, c) kernel run
+      x = skip >= 32 ? 0u : (x & ~((1u << skip) - 1u));
+    }
   }
-  for (int col = threadIdx.x; col < ly.L; col += blockDim.x) {
-    int c = col / ly.k, j = col - c * ly.k;
-    int pi = pos_in[ly.ikeep + c];
-    m.colpos[ly.cpoff + col] = pi >= 0 ? pi * ly.k + j : -1;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    pop += __shfl_xor_sync(kFull, pop, off);
+    drift += __shfl_xor_sync(kFull, drift, off);
   }
+  long long* row = a.summary + (long long)l * kSumCols;
+  if ((threadIdx.x & 31) == 0) {
+    if (pop) atomicAdd(reinterpret_cast<unsigned long long*>(row + 5), pop);
+    if (drift) atomicAdd(reinterpret_cast<unsigned long long*>(row + 4), drift);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ly.cin; i += kThreads)
+    if (s_in[i]) a.iflag[ly.ikeep + i] = 1;
+  for (int i = threadIdx.x; i < nr; i += kThreads)
+    if (s_out[i]) a.oflag[ly.okeep + r_lo + i] = 1;
+  // b) the layer's last CTA derives its keep sets
   __shared__ bool last;
-  if (threadIdx.x == 0) {
-    long long* row = summary + (long long)l * kSumCols;
-    row[0] = n_out;
-    row[1] = n_in;
-    row[2] = (long long)n_out * n_in * ly.k;
-    __threadfence();
-    last = atomicAdd(done, 1u) == gridDim.x - 1;
-  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(a.layer_done + ly.pidx, 1u) == (unsigned)it.chunk - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // flat-buffer layout: exclusive scan of payload sizes over all layers, in layer order
+  int n_out = scan_flags(a.oflag + ly.okeep, ly.rows, a.pos_out + ly.okeep);
+  int n_in = scan_flags(a.iflag + ly.ikeep, ly.cin, a.pos_in + ly.ikeep);
+  __syncthreads();
+  const int rowlen = n_in * ly.k;
+  for (int o = threadIdx.x; o < ly.rows; o += kThreads) {
+    int po = a.pos_out[ly.okeep + o];
+    a.maps.rowbase[ly.okeep + o] = po >= 0 ? po * rowlen : -1;
+  }
+  for (int col = threadIdx.x; col < ly.L; col += kThreads) {
+    unsigned c = fdiv((unsigned)col, ly.divk), jx = (unsigned)col - c * (unsigned)ly.k;
+    int pi = a.pos_in[ly.ikeep + c];
+    a.maps.colpos[ly.cpoff + col] = pi >= 0 ? pi * ly.k + (int)jx : -1;
+  }
+  __shared__ bool last_layer;
+  if (threadIdx.x == 0) {
+    row[0] = n_out;
+    row[1] = n_in;
+    row[2] = (long long)n_out * n_in * ly.k;
+    a.layer_done[ly.pidx] = 0;
+    __threadfence();
+    last_layer = atomicAdd(a.done, 1u) == (unsigned)a.n_prunable - 1;
+  }
+  __syncthreads();
+  if (!last_layer) return;
+  __threadfence();
+  // c) flat-buffer layout
   __shared__ long long wsum[32];
   __shared__ long long carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int base = 0; base < n_layers; base += blockDim.x) {
+  for (int base = 0; base < a.n_layers; base += kThreads) {
     int i = base + threadIdx.x;
-    volatile long long* row = summary + (long long)i * kSumCols;
-    long long e = i < n_layers ? row[2] : 0;
+    volatile long long* ri = a.summary + (long long)i * kSumCols;
+    long long e = i < a.n_layers ? ri[2] : 0;
     long long incl = e;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -731,7 +697,7 @@ __global__ void __launch_bounds__(1024) k_keep_scan(const DevLayer* __restrict__
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      long long t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0, ti = t;
+      long long t = lane < kThreads / 32 ? wsum[lane] : 0, ti = t;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         long long y = __shfl_up_sync(kFull, ti, off);
@@ -741,23 +707,21 @@ __global__ void __launch_bounds__(1024) k_keep_scan(const DevLayer* __restrict__
     }
     __syncthreads();
     long long ex = carry + wsum[warp] + incl - e;
-    if (i < n_layers) row[3] = ex;
+    if (i < a.n_layers) ri[3] = ex;
     __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = ex + e;
+    if (threadIdx.x == kThreads - 1) carry = ex + e;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    summary[(long long)n_layers * kSumCols] = carry;
-    *done = 0;
+    a.summary[(long long)a.n_layers * kSumCols] = carry;
+    *a.done = 0;
   }
 }
 
-void launch_keep_scan(const DevLayer* layers, const int* list, int n, int n_layers,
-                      const uint8_t* oflag, const uint8_t* iflag, int* pos_out, int* pos_in,
-                      Maps maps, long long* summary, unsigned int* done, cudaStream_t st) {
-  if (n <= 0) return;
-  k_keep_scan<<<n, 1024, 0, st>>>(layers, list, n_layers, oflag, iflag, pos_out, pos_in, maps,
-                                  summary, done);
+void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st) {
+  if (n_items <= 0) return;
+  allow_smem(k_keep_sets, smem);
+  k_keep_sets<<<n_items, kThreads, smem, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------

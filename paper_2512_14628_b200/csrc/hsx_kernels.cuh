@@ -51,6 +51,8 @@ struct DevLayer {
   int nparts;                  // row tiles of the candidate kernel (partials rows)
   int rsub;                    // rows per shared-memory sub-tile
   int rank;
+  int tiling;                  // 0: row tiles (partials per group / row), 1: quad tiles (per column)
+  int pidx;                    // index among prunable layers
   int group[kMaxPasses];
   int keep[kMaxPasses];
   int G[kMaxPasses];
@@ -61,8 +63,10 @@ struct DevLayer {
 // A contiguous slice [begin, end) of one layer's elements.
 struct Item {
   int layer;
-  int part;  // row-tile index inside the layer (candidate kernel)
-  long long begin, end;
+  int part;   // candidate: row-tile index; keep-mark: prunable-layer index
+  int chunk;  // candidate (quad tiling): column chunk of 64 quads; keep-mark: items of the layer
+  int pad;
+  long long begin, end;  // element range (quad tiling: rows [begin, end))
 };
 
 struct CandArgs {
@@ -107,21 +111,32 @@ struct ElemArgs {
   float divisor;
 };
 
-void launch_candidate(const CandArgs& a, const Item* dense_items, int n_dense, const Item* norm_items,
-                      int n_norm, int frozen, size_t smem, cudaStream_t st);
+void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st);
+struct FlagPtrs {
+  uint8_t* f[kMaxPasses];
+};
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
-                   double* norms, uint8_t* flags, size_t smem, cudaStream_t st);
-void launch_keepmaps(const DevLayer* layers, const int* list, int n, const uint8_t* f0,
-                     const uint8_t* f1, const uint8_t* f2, Maps maps, cudaStream_t st);
+                   double* norms, FlagPtrs flags, Maps maps, size_t smem, cudaStream_t st);
 void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
                     uint32_t* mask, Maps maps, cudaStream_t st);
 void launch_mask_or(const uint32_t* g, int m, long long words, uint32_t* out, cudaStream_t st);
-void launch_keep_mark(const DevLayer* layers, const Item* items, int n_items, const uint32_t* uni,
-                      const uint32_t* prev, uint8_t* oflag, uint8_t* iflag, long long* summary,
-                      size_t smem, cudaStream_t st);
-void launch_keep_scan(const DevLayer* layers, const int* list, int n, int n_layers,
-                      const uint8_t* oflag, const uint8_t* iflag, int* pos_out, int* pos_in,
-                      Maps maps, long long* summary, unsigned int* done, cudaStream_t st);
+struct KeepArgs {
+  const DevLayer* layers;
+  const Item* items;
+  const uint32_t* uni;
+  const uint32_t* prev;
+  uint8_t* oflag;
+  uint8_t* iflag;
+  int* pos_out;
+  int* pos_in;
+  Maps maps;
+  long long* summary;
+  unsigned int* layer_done;  // per prunable layer
+  unsigned int* done;        // prunable layers finished
+  int n_layers;
+  int n_prunable;
+};
+void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st);
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t st);

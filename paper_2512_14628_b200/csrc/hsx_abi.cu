@@ -287,7 +287,10 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     p->select_smem[q] = (size_t)gp * (sizeof(double) + sizeof(int)) + 8 + (size_t)lmax * sizeof(double);
   }
   p->sqcap = sqcap;
-  p->cand_smem = (size_t)std::max(sqcap + gmax, quadcap) * sizeof(double);
+  // k_candidate: cp.async ring (kDepth x 4 x 256 float4 = 64 KB) + 8 KB quad fold,
+  // or the row-tile path's sub-tile squares + group accumulators
+  p->cand_smem = std::max((size_t)(sqcap + gmax) * sizeof(double),
+                          (size_t)4 * 4 * 256 * 16 + (size_t)quadcap * sizeof(double));
   p->mark_smem = mark_smem;
   if (p->cand_smem > kMaxSmem) return fail(HSX_ESHAPE, "candidate tile needs %zu B of shared memory", p->cand_smem);
   host_layout(p);

@@ -36,6 +36,70 @@ __device__ __forceinline__ float dual1(float u, float a, float b) {
 }
 
 // ---------------------------------------------------------------------------
+// Per-thread cp.async (LDGSTS) rings. A streaming kernel gives every thread a
+// sequence of element quads; the thread keeps kDepth-1 quads' loads in flight
+// in its private shared-memory slots (no registers held, no block barriers:
+// a thread only reads slots it filled itself, visible after cp.async.wait_group).
+// Dropped coordinates of a gather are zero-filled by the copy engine
+// (src-size 0) instead of being read.
+// ---------------------------------------------------------------------------
+
+constexpr int kDepth = 4;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp16(float4* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// 4-byte copy, zero-fill when !valid (the global address is not dereferenced)
+__device__ __forceinline__ void cp4z(float* dst, const float* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// slot (stage d, buffer b) of this thread in a [kDepth][NB][kThreads] float4 ring
+template <int NB>
+__device__ __forceinline__ float4* ring_slot(float4* ring, int d, int b) {
+  return ring + ((d * NB + b) * kThreads + threadIdx.x);
+}
+
+// quad (4 consecutive elements at e) of `src` into a slot; partial quads past n
+// are zero-filled element-wise
+__device__ __forceinline__ void cp_quad(float4* dst, const float* src, long long e, long long n) {
+  if (e + 3 < n) {
+    cp16(dst, src + e);
+  } else {
+    float* d = reinterpret_cast<float*>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cp4z(d + i, src + (e + i < n ? e + i : 0), e + i < n);
+  }
+}
+
+// Drive `count` iterations of (issue(slot, i), consume(slot, i)) through the ring.
+template <class Issue, class Consume>
+__device__ __forceinline__ void ring_run(int count, Issue issue, Consume consume) {
+#pragma unroll
+  for (int d = 0; d < kDepth - 1; ++d) {
+    if (d < count) issue(d, d);
+    cp_commit();
+  }
+  for (int i = 0; i < count; ++i) {
+    const int ahead = i + kDepth - 1;
+    if (ahead < count) issue(ahead % kDepth, ahead);
+    cp_commit();
+    cp_wait<kDepth - 1>();
+    consume(i % kDepth, i);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1 candidate (+ group-norm partials).  consensus.py:142-160, tensors.py:75-93
 // ---------------------------------------------------------------------------
 
@@ -93,94 +157,106 @@ __device__ __forceinline__ bool kept_by(const DevLayer& ly, const uint8_t* const
 
 // K1a: elementwise candidate over [begin, end) of one layer (dense layers; every
 // layer in frozen mode, where prunable layers get cand * global mask,
-// consensus.py:177-180)
+// consensus.py:177-180). Inputs stream through the per-thread cp.async ring.
 __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long long begin, long long end,
-                                 int frozen) {
+                                 int frozen, float4* ring) {
   const bool masked = frozen && ly.ncons > 0 && p.fmask != nullptr;
-  constexpr int U = 2;
   const long long nq = (end - begin + 3) >> 2;
-  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * U) {
-    In4 in[U];
-#pragma unroll
-    for (int uu = 0; uu < U; ++uu) {
-      long long q = q0 + (long long)uu * kThreads;
-      long long e = begin + 4 * q;
-      if (q < nq && e + 3 < ly.n) in[uu] = load_in4(p, ly.off + e);
+  const int t = threadIdx.x;
+  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
+  const float* A = p.s ? p.s + ly.off : p.theta + ly.off;
+  const float* B = p.s ? nullptr : p.u + ly.off;
+  const float* Z = p.identity ? nullptr : p.z + ly.off;
+  const float* V = p.identity ? nullptr : p.v + ly.off;
+  auto issue = [&](int d, int i) {
+    long long e = begin + 4 * (t + (long long)i * kThreads);
+    cp_quad(ring_slot<4>(ring, d, 0), A, e, ly.n);
+    if (B) cp_quad(ring_slot<4>(ring, d, 1), B, e, ly.n);
+    if (Z) {
+      cp_quad(ring_slot<4>(ring, d, 2), Z, e, ly.n);
+      cp_quad(ring_slot<4>(ring, d, 3), V, e, ly.n);
     }
+  };
+  auto consume = [&](int d, int i) {
+    long long e = begin + 4 * (t + (long long)i * kThreads);
+    In4 x;
+    x.a = *ring_slot<4>(ring, d, 0);
+    x.b = B ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    x.z = Z ? *ring_slot<4>(ring, d, 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+    x.v = Z ? *ring_slot<4>(ring, d, 3) : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t bits = masked ? p.fmask[ly.mword + (e >> 5)] : 0u;
+    float4 out;
 #pragma unroll
-    for (int uu = 0; uu < U; ++uu) {
-      long long q = q0 + (long long)uu * kThreads;
-      if (q >= nq) continue;
-      long long e = begin + 4 * q;
-      uint32_t bits = masked ? p.fmask[ly.mword + (e >> 5)] : 0u;
-      if (e + 3 < ly.n) {
-        float4 out;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          double c = cand4(p, in[uu], i, ly);
-          if (masked) c = ((bits >> ((e + i) & 31)) & 1u) ? c : c * 0.0;
-          f4set(out, i, (float)c);
-        }
-        st4(p.zn + ly.off + e, out);
-      } else {
-        for (int i = 0; i < 4 && e + i < ly.n; ++i) {
-          double c = cand_elem(p, ly.off + e + i, ly);
-          if (masked) c = ((bits >> ((e + i) & 31)) & 1u) ? c : c * 0.0;
-          p.zn[ly.off + e + i] = (float)c;
-        }
-      }
+    for (int i2 = 0; i2 < 4; ++i2) {
+      double c = cand4(p, x, i2, ly);
+      if (masked) c = ((bits >> ((e + i2) & 31)) & 1u) ? c : c * 0.0;
+      f4set(out, i2, (float)c);
     }
-  }
+    if (e + 3 < ly.n) {
+      st4(p.zn + ly.off + e, out);
+    } else {
+      for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) p.zn[ly.off + e + i2] = f4get(out, i2);
+    }
+  };
+  ring_run(count, issue, consume);
 }
 
 // K1b quad tiles (CHANNEL / SHAPE groups, c_in*kh*kw % 4 == 0 — every ResNet conv
 // but the 7x7 stem): a tile is 32 rows x 64 column quads; thread t owns quad
 // (t & 63) and row phase (t >> 6), so its fp64 column sums of squares stay in
-// registers; the 4 phases fold in shared memory in a fixed order and the tile
-// writes one fp64 partial per column (the channel fold happens in K2).
+// registers while its rows stream through the cp.async ring; the 4 phases fold
+// in shared memory in a fixed order and the tile writes one fp64 partial per
+// column (the channel fold happens in K2).
 constexpr int kTileQuads = 64;
 
-__device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, double* cs) {
+__device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, float4* ring,
+                                double* cs) {
+  constexpr int RP = kThreads / kTileQuads;
   const int pass = p.pass;
   const int L = ly.L;
   const int Q = L >> 2;
   const int jj = threadIdx.x & (kTileQuads - 1);
-  const int ph = threadIdx.x / kTileQuads;  // 0..3
+  const int ph = threadIdx.x / kTileQuads;
   const int j = it.chunk * kTileQuads + jj;
-  const long long r0 = it.begin, r1 = it.end;
+  const long long r0 = it.begin + ph, r1 = it.end;
+  const int count = (j < Q && r0 < r1) ? (int)((r1 - r0 + RP - 1) / RP) : 0;
+  const float* A = p.s ? p.s + ly.off : p.theta + ly.off;
+  const float* B = p.s ? nullptr : p.u + ly.off;
+  const float* Z = p.identity ? nullptr : p.z + ly.off;
+  const float* V = p.identity ? nullptr : p.v + ly.off;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  if (j < Q) {
-    constexpr int U = 2;
-    constexpr int RP = kThreads / kTileQuads;
-    for (long long r = r0 + ph; r < r1; r += RP * U) {
-      In4 in[U];
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu) {
-        long long rr = r + uu * RP;
-        if (rr < r1) in[uu] = load_in4(p, ly.off + rr * L + 4 * j);
-      }
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu) {
-        long long rr = r + uu * RP;
-        if (rr >= r1) break;
-        long long e = rr * L + 4 * j;
-        double c0 = cand4(p, in[uu], 0, ly), c1 = cand4(p, in[uu], 1, ly);
-        double c2 = cand4(p, in[uu], 2, ly), c3 = cand4(p, in[uu], 3, ly);
-        if (pass > 0) {
-          if (!kept_by(ly, p.flags, pass, e + 0)) c0 = 0.0;
-          if (!kept_by(ly, p.flags, pass, e + 1)) c1 = 0.0;
-          if (!kept_by(ly, p.flags, pass, e + 2)) c2 = 0.0;
-          if (!kept_by(ly, p.flags, pass, e + 3)) c3 = 0.0;
-        } else {
-          st4(p.zn + ly.off + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
-        }
-        a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
-        a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
-        a2 = __dadd_rn(a2, __dmul_rn(c2, c2));
-        a3 = __dadd_rn(a3, __dmul_rn(c3, c3));
-      }
+  auto issue = [&](int d, int i) {
+    long long e = (r0 + (long long)i * RP) * L + 4 * j;
+    cp16(ring_slot<4>(ring, d, 0), A + e);
+    if (B) cp16(ring_slot<4>(ring, d, 1), B + e);
+    if (Z) {
+      cp16(ring_slot<4>(ring, d, 2), Z + e);
+      cp16(ring_slot<4>(ring, d, 3), V + e);
     }
-  }
+  };
+  auto consume = [&](int d, int i) {
+    long long e = (r0 + (long long)i * RP) * L + 4 * j;
+    In4 x;
+    x.a = *ring_slot<4>(ring, d, 0);
+    x.b = B ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    x.z = Z ? *ring_slot<4>(ring, d, 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+    x.v = Z ? *ring_slot<4>(ring, d, 3) : make_float4(0.f, 0.f, 0.f, 0.f);
+    double c0 = cand4(p, x, 0, ly), c1 = cand4(p, x, 1, ly);
+    double c2 = cand4(p, x, 2, ly), c3 = cand4(p, x, 3, ly);
+    if (pass > 0) {
+      if (!kept_by(ly, p.flags, pass, e + 0)) c0 = 0.0;
+      if (!kept_by(ly, p.flags, pass, e + 1)) c1 = 0.0;
+      if (!kept_by(ly, p.flags, pass, e + 2)) c2 = 0.0;
+      if (!kept_by(ly, p.flags, pass, e + 3)) c3 = 0.0;
+    } else {
+      st4(p.zn + ly.off + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
+    }
+    a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
+    a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
+    a2 = __dadd_rn(a2, __dmul_rn(c2, c2));
+    a3 = __dadd_rn(a3, __dmul_rn(c3, c3));
+  };
+  ring_run(count, issue, consume);
   double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
@@ -188,7 +264,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   if (col < L) {
     double s = cs[threadIdx.x];
 #pragma unroll
-    for (int q = 1; q < kThreads / kTileQuads; ++q) s += cs[q * 4 * kTileQuads + threadIdx.x];
+    for (int q = 1; q < RP; ++q) s += cs[q * 4 * kTileQuads + threadIdx.x];
     p.partials[ly.poff[pass] + (long long)it.part * L + col] = s;
   }
 }
@@ -250,7 +326,7 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
 }
 
 __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int frozen) {
-  extern __shared__ double smem[];
+  extern __shared__ float4 ring[];
   const Item it = p.items[blockIdx.x];
   const DevLayer& ly = p.layers[it.layer];
   if (frozen || ly.ncons == 0) {
@@ -264,14 +340,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
       }
       return;
     }
-    cand_elementwise(p, ly, it.begin, it.end, frozen);
+    cand_elementwise(p, ly, it.begin, it.end, frozen, ring);
     return;
   }
   if (ly.ncons <= p.pass) return;
   if (ly.tiling == 1)
-    cand_tile_quads(p, ly, it, smem);
+    cand_tile_quads(p, ly, it, ring, reinterpret_cast<double*>(ring + kDepth * 4 * kThreads));
   else
-    cand_tile_rows(p, ly, it, smem, smem + p.sqcap);
+    cand_tile_rows(p, ly, it, reinterpret_cast<double*>(ring), reinterpret_cast<double*>(ring) + p.sqcap);
 }
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
@@ -416,65 +492,53 @@ __global__ void __launch_bounds__(kThreads) k_project(const DevLayer* __restrict
                                                       const Item* __restrict__ items,
                                                       float* __restrict__ zn,
                                                       uint32_t* __restrict__ mask, Maps m) {
+  extern __shared__ float4 ring[];
   const Item it = items[blockIdx.x];
   const DevLayer& ly = layers[it.layer];
   const int lane = threadIdx.x & 31;
   if ((ly.L & 3) == 0) {
-    const long long q0 = it.begin >> 2, q1 = (it.end + 3) >> 2;  // begin is a multiple of 32
-    constexpr int U = 2;
-    for (long long qb = q0 + (threadIdx.x & ~31); qb < q1; qb += (long long)kThreads * U) {
-      float4 val[U];
-      int rk[U];
-      uchar4 ck[U];
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu) {
-        long long q = qb + (long long)uu * kThreads + lane;
-        long long e = q << 2;
-        if (q < q1 && e + 3 < ly.n) {
-          val[uu] = ldcs4(zn + ly.off + e);
-          unsigned o = fdiv((unsigned)e, ly.divL);
-          unsigned col = (unsigned)e - o * (unsigned)ly.L;
-          rk[uu] = m.rowkeep[ly.okeep + o];
-          ck[uu] = *reinterpret_cast<const uchar4*>(m.colkeep + ly.cpoff + col);
-        }
-      }
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu) {
-        long long q = qb + (long long)uu * kThreads + lane;
-        long long e = q << 2;
-        unsigned nib = 0;
-        if (q < q1 && e < ly.n) {
+    // warp w handles 32 consecutive quads per stage; 8 lanes' nibbles make a word
+    const long long q1 = (it.end + 3) >> 2;                        // begin is a multiple of 32
+    const long long qw = (it.begin >> 2) + (threadIdx.x & ~31);    // warp's first quad
+    const int count = qw < q1 ? (int)((q1 - qw + kThreads - 1) / kThreads) : 0;
+    const float* src = zn + ly.off;
+    auto issue = [&](int d, int i) {
+      long long q = qw + lane + (long long)i * kThreads;
+      if (q < q1) cp_quad(ring_slot<1>(ring, d, 0), src, q << 2, ly.n);
+    };
+    auto consume = [&](int d, int i) {
+      long long q = qw + lane + (long long)i * kThreads;
+      long long e = q << 2;
+      unsigned nib = 0;
+      if (q < q1 && e < ly.n) {
+        float4 v = *ring_slot<1>(ring, d, 0);
+        unsigned o = fdiv((unsigned)e, ly.divL);
+        unsigned col = (unsigned)e - o * (unsigned)ly.L;
+        int rk = m.rowkeep[ly.okeep + o];
+        uchar4 ck = *reinterpret_cast<const uchar4*>(m.colkeep + ly.cpoff + col);
+        bool k0 = rk && ck.x, k1 = rk && ck.y, k2 = rk && ck.z, k3 = rk && ck.w;
+        nib = (unsigned)(k0 && v.x != 0.f) | ((unsigned)(k1 && v.y != 0.f) << 1) |
+              ((unsigned)(k2 && v.z != 0.f) << 2) | ((unsigned)(k3 && v.w != 0.f) << 3);
+        if (!(k0 && k1 && k2 && k3)) {
+          if (!k0) v.x = 0.f;
+          if (!k1) v.y = 0.f;
+          if (!k2) v.z = 0.f;
+          if (!k3) v.w = 0.f;
           if (e + 3 < ly.n) {
-            bool k0 = rk[uu] && ck[uu].x, k1 = rk[uu] && ck[uu].y;
-            bool k2 = rk[uu] && ck[uu].z, k3 = rk[uu] && ck[uu].w;
-            float4 v = val[uu];
-            nib = (unsigned)(k0 && v.x != 0.f) | ((unsigned)(k1 && v.y != 0.f) << 1) |
-                  ((unsigned)(k2 && v.z != 0.f) << 2) | ((unsigned)(k3 && v.w != 0.f) << 3);
-            if (!(k0 && k1 && k2 && k3)) {
-              if (!k0) v.x = 0.f;
-              if (!k1) v.y = 0.f;
-              if (!k2) v.z = 0.f;
-              if (!k3) v.w = 0.f;
-              st4(zn + ly.off + e, v);
-            }
+            st4(zn + ly.off + e, v);
           } else {
-            for (int i = 0; i < 4 && e + i < ly.n; ++i) {
-              unsigned o = fdiv((unsigned)(e + i), ly.divL);
-              unsigned col = (unsigned)(e + i) - o * (unsigned)ly.L;
-              bool kp = m.rowkeep[ly.okeep + o] && m.colkeep[ly.cpoff + col];
-              float x = zn[ly.off + e + i];
-              if (!kp) zn[ly.off + e + i] = 0.f;
-              nib |= (unsigned)(kp && x != 0.f) << i;
-            }
+            for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) zn[ly.off + e + i2] = f4get(v, i2);
           }
         }
-        unsigned w = nib << (4 * (lane & 7));
-        w |= __shfl_xor_sync(kFull, w, 1);
-        w |= __shfl_xor_sync(kFull, w, 2);
-        w |= __shfl_xor_sync(kFull, w, 4);
-        if ((lane & 7) == 0 && q < q1 && e < ly.n) mask[ly.mword + (e >> 5)] = w;
+        if (e + 3 >= ly.n) nib &= (1u << (ly.n - e)) - 1u;
       }
-    }
+      unsigned w = nib << (4 * (lane & 7));
+      w |= __shfl_xor_sync(kFull, w, 1);
+      w |= __shfl_xor_sync(kFull, w, 2);
+      w |= __shfl_xor_sync(kFull, w, 4);
+      if ((lane & 7) == 0 && q < q1 && e < ly.n) mask[ly.mword + (e >> 5)] = w;
+    };
+    ring_run(count, issue, consume);
     return;
   }
   // rows of L % 4 != 0 elements (stem convs): one warp per 32-element word
@@ -500,7 +564,8 @@ __global__ void __launch_bounds__(kThreads) k_project(const DevLayer* __restrict
 void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
                     uint32_t* mask, Maps maps, cudaStream_t st) {
   if (n_items <= 0) return;
-  k_project<<<n_items, kThreads, 0, st>>>(layers, items, zn, mask, maps);
+  const size_t smem = (size_t)kDepth * kThreads * sizeof(float4);
+  k_project<<<n_items, kThreads, smem, st>>>(layers, items, zn, mask, maps);
 }
 
 // ---------------------------------------------------------------------------
@@ -750,154 +815,131 @@ __device__ __forceinline__ int elem_dst(const ElemArgs& a, const DevLayer& ly, l
   return (rb < 0 || cp < 0) ? -1 : rb + cp;
 }
 
+// payload indices of the quad at e (-1: dropped, or past the layer end)
+__device__ __forceinline__ int4 dst4(const ElemArgs& a, const DevLayer& ly, long long e) {
+  if (ly.ncons == 0) {
+    int b = (int)e;
+    return make_int4(b, e + 1 < ly.n ? b + 1 : -1, e + 2 < ly.n ? b + 2 : -1, e + 3 < ly.n ? b + 3 : -1);
+  }
+  if ((ly.L & 3) == 0 && e + 3 < ly.n) return quad_dst(a, ly, e);
+  int4 d;
+  d.x = elem_dst(a, ly, e);
+  d.y = e + 1 < ly.n ? elem_dst(a, ly, e + 1) : -1;
+  d.z = e + 2 < ly.n ? elem_dst(a, ly, e + 2) : -1;
+  d.w = e + 3 < ly.n ? elem_dst(a, ly, e + 3) : -1;
+  return d;
+}
+
+// K6: flat[payload] <- z_node + v  (+ u <- u + (theta - z_node)), one item of one layer
 __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
+  extern __shared__ float4 ring[];
   const Item it = a.items[blockIdx.x];
   const DevLayer& ly = a.layers[it.layer];
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
-  const bool pr = ly.ncons > 0;
-  const bool quads = !pr || (ly.L & 3) == 0;
   const long long nq = (it.end - it.begin + 3) >> 2;
-  constexpr int U = 2;
-  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * U) {
-    float4 th[U], uu4[U], zn[U], vv[U];
-#pragma unroll
-    for (int uu = 0; uu < U; ++uu) {
-      long long q = q0 + (long long)uu * kThreads;
-      long long e = it.begin + 4 * q;
-      if (q >= nq) continue;
-      if (e + 3 < ly.n) {
-        long long gi = ly.off + e;
-        zn[uu] = ldcs4(a.zn + gi);
-        vv[uu] = a.vin ? ldcs4(a.vin + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (a.u) {
-          th[uu] = ldcs4(a.theta + gi);
-          uu4[uu] = ldcs4(a.u + gi);
-        }
+  const int t = threadIdx.x;
+  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
+  const float* ZN = a.zn + ly.off;
+  const float* VI = a.vin ? a.vin + ly.off : nullptr;
+  const float* TH = a.u ? a.theta + ly.off : nullptr;
+  const float* UU = a.u ? a.u + ly.off : nullptr;
+  float* flat = a.flat_out + coff;
+  auto issue = [&](int d, int i) {
+    long long e = it.begin + 4 * (t + (long long)i * kThreads);
+    cp_quad(ring_slot<4>(ring, d, 0), ZN, e, ly.n);
+    if (VI) cp_quad(ring_slot<4>(ring, d, 1), VI, e, ly.n);
+    if (TH) {
+      cp_quad(ring_slot<4>(ring, d, 2), TH, e, ly.n);
+      cp_quad(ring_slot<4>(ring, d, 3), UU, e, ly.n);
+    }
+  };
+  auto consume = [&](int d, int i) {
+    long long e = it.begin + 4 * (t + (long long)i * kThreads);
+    float4 zn = *ring_slot<4>(ring, d, 0);
+    float4 vv = VI ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool full = e + 3 < ly.n;
+    if (TH) {
+      float4 th = *ring_slot<4>(ring, d, 2), uu = *ring_slot<4>(ring, d, 3);
+      float4 un = make_float4(dual1(uu.x, th.x, zn.x), dual1(uu.y, th.y, zn.y), dual1(uu.z, th.z, zn.z),
+                              dual1(uu.w, th.w, zn.w));
+      if (full) {
+        st4(a.u + ly.off + e, un);
       } else {
-        for (int i = 0; i < 4; ++i) {
-          bool ok = e + i < ly.n;
-          long long gi = ly.off + e + i;
-          f4set(zn[uu], i, ok ? a.zn[gi] : 0.f);
-          f4set(vv[uu], i, ok && a.vin ? a.vin[gi] : 0.f);
-          if (a.u) {
-            f4set(th[uu], i, ok ? a.theta[gi] : 0.f);
-            f4set(uu4[uu], i, ok ? a.u[gi] : 0.f);
-          }
-        }
+        for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) a.u[ly.off + e + i2] = f4get(un, i2);
       }
     }
-#pragma unroll
-    for (int uu = 0; uu < U; ++uu) {
-      long long q = q0 + (long long)uu * kThreads;
-      if (q >= nq) continue;
-      long long e = it.begin + 4 * q;
-      const bool full = e + 3 < ly.n;
-      if (a.u) {
-        float4 un = make_float4(dual1(uu4[uu].x, th[uu].x, zn[uu].x), dual1(uu4[uu].y, th[uu].y, zn[uu].y),
-                                dual1(uu4[uu].z, th[uu].z, zn[uu].z), dual1(uu4[uu].w, th[uu].w, zn[uu].w));
-        if (full) {
-          stcs4(a.u + ly.off + e, un);
-        } else {
-          for (int i = 0; i < 4 && e + i < ly.n; ++i) a.u[ly.off + e + i] = f4get(un, i);
-        }
-      }
-      float4 c = make_float4(zn[uu].x + vv[uu].x, zn[uu].y + vv[uu].y, zn[uu].z + vv[uu].z,
-                             zn[uu].w + vv[uu].w);
-      if (!pr) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (e + i < ly.n) a.flat_out[coff + e + i] = f4get(c, i);
-      } else if (quads && full) {
-        int4 d = quad_dst(a, ly, e);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i4get(d, i) >= 0) a.flat_out[coff + i4get(d, i)] = f4get(c, i);
-      } else {
-        for (int i = 0; i < 4 && e + i < ly.n; ++i) {
-          int d = elem_dst(a, ly, e + i);
-          if (d >= 0) a.flat_out[coff + d] = f4get(c, i);
-        }
-      }
-    }
-  }
+    int4 dd = dst4(a, ly, e);
+    if (dd.x >= 0) flat[dd.x] = zn.x + vv.x;
+    if (dd.y >= 0) flat[dd.y] = zn.y + vv.y;
+    if (dd.z >= 0) flat[dd.z] = zn.z + vv.z;
+    if (dd.w >= 0) flat[dd.w] = zn.w + vv.w;
+  };
+  ring_run(count, issue, consume);
 }
 
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
-  k_compact<<<n_items, kThreads, 0, st>>>(a);
+  const size_t smem = (size_t)kDepth * 4 * kThreads * sizeof(float4);
+  allow_smem(k_compact, smem);
+  k_compact<<<n_items, kThreads, smem, st>>>(a);
 }
 
+// K7: z <- zero-filled gather of flat / divisor (+ v <- v + (z_node - z)); the
+// gather itself streams through the ring: dropped coordinates are zero-filled
+// by cp.async without touching memory.
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
+  extern __shared__ float4 ring[];
   const Item it = a.items[blockIdx.x];
   const DevLayer& ly = a.layers[it.layer];
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
-  const bool pr = ly.ncons > 0;
-  const bool quads = !pr || (ly.L & 3) == 0;
-  const float div = a.divisor;
   const long long nq = (it.end - it.begin + 3) >> 2;
-  constexpr int U = 2;
-  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)kThreads * U) {
-    float4 zn[U], vv[U], zz[U];
-#pragma unroll
-    for (int uu = 0; uu < U; ++uu) {
-      long long q = q0 + (long long)uu * kThreads;
-      long long e = it.begin + 4 * q;
-      if (q >= nq) continue;
-      const bool full = e + 3 < ly.n;
-      // gather of the reduced payload (zero fill for dropped coordinates)
-      if (!pr) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) f4set(zz[uu], i, e + i < ly.n ? a.flat_in[coff + e + i] : 0.f);
-      } else if (quads && full) {
-        int4 d = quad_dst(a, ly, e);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) f4set(zz[uu], i, i4get(d, i) >= 0 ? a.flat_in[coff + i4get(d, i)] : 0.f);
-      } else {
-        for (int i = 0; i < 4; ++i) {
-          int d = e + i < ly.n ? elem_dst(a, ly, e + i) : -1;
-          f4set(zz[uu], i, d >= 0 ? a.flat_in[coff + d] : 0.f);
-        }
-      }
-      if (a.v) {
-        long long gi = ly.off + e;
-        if (full) {
-          zn[uu] = ldcs4(a.zn + gi);
-          vv[uu] = ldcs4(a.v + gi);
-        } else {
-          for (int i = 0; i < 4; ++i) {
-            f4set(zn[uu], i, e + i < ly.n ? a.zn[gi + i] : 0.f);
-            f4set(vv[uu], i, e + i < ly.n ? a.v[gi + i] : 0.f);
-          }
-        }
+  const int t = threadIdx.x;
+  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
+  const float* flat = a.flat_in + coff;
+  const float* ZN = a.v ? a.zn + ly.off : nullptr;
+  const float* VV = a.v ? a.v + ly.off : nullptr;
+  const float div = a.divisor;
+  auto issue = [&](int d, int i) {
+    long long e = it.begin + 4 * (t + (long long)i * kThreads);
+    int4 dd = dst4(a, ly, e);
+    float* g = reinterpret_cast<float*>(ring_slot<3>(ring, d, 0));
+    cp4z(g + 0, flat + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
+    cp4z(g + 1, flat + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
+    cp4z(g + 2, flat + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
+    cp4z(g + 3, flat + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
+    if (ZN) {
+      cp_quad(ring_slot<3>(ring, d, 1), ZN, e, ly.n);
+      cp_quad(ring_slot<3>(ring, d, 2), VV, e, ly.n);
+    }
+  };
+  auto consume = [&](int d, int i) {
+    long long e = it.begin + 4 * (t + (long long)i * kThreads);
+    float4 zo = *ring_slot<3>(ring, d, 0);
+    if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
+    float4 vn;
+    if (ZN) {
+      float4 zn = *ring_slot<3>(ring, d, 1), vv = *ring_slot<3>(ring, d, 2);
+      vn = make_float4(dual1(vv.x, zn.x, zo.x), dual1(vv.y, zn.y, zo.y), dual1(vv.z, zn.z, zo.z),
+                       dual1(vv.w, zn.w, zo.w));
+    }
+    if (e + 3 < ly.n) {
+      st4(a.z + ly.off + e, zo);
+      if (ZN) st4(a.v + ly.off + e, vn);
+    } else {
+      for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) {
+        a.z[ly.off + e + i2] = f4get(zo, i2);
+        if (ZN) a.v[ly.off + e + i2] = f4get(vn, i2);
       }
     }
-#pragma unroll
-    for (int uu = 0; uu < U; ++uu) {
-      long long q = q0 + (long long)uu * kThreads;
-      if (q >= nq) continue;
-      long long e = it.begin + 4 * q;
-      float4 zo = zz[uu];
-      if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
-      float4 vn;
-      if (a.v)
-        vn = make_float4(dual1(vv[uu].x, zn[uu].x, zo.x), dual1(vv[uu].y, zn[uu].y, zo.y),
-                         dual1(vv[uu].z, zn[uu].z, zo.z), dual1(vv[uu].w, zn[uu].w, zo.w));
-      if (e + 3 < ly.n) {
-        stcs4(a.z + ly.off + e, zo);
-        if (a.v) stcs4(a.v + ly.off + e, vn);
-      } else {
-        for (int i = 0; i < 4 && e + i < ly.n; ++i) {
-          a.z[ly.off + e + i] = f4get(zo, i);
-          if (a.v) a.v[ly.off + e + i] = f4get(vn, i);
-        }
-      }
-    }
-  }
+  };
+  ring_run(count, issue, consume);
 }
 
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
-  k_decompact<<<n_items, kThreads, 0, st>>>(a);
+  const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
+  allow_smem(k_decompact, smem);
+  k_decompact<<<n_items, kThreads, smem, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------

@@ -473,7 +473,7 @@ int hsx_candidate(hsx_plan* p, const float* sum, const float* theta, const float
   a.partials = p->d_partials[0];
   if (frozen_mask) {
     a.items = p->d_elem;  // frozen: plain elementwise over every layer
-    hsx::launch_candidate(a, (int)p->elem_items.size(), 1, 0, S(stream));
+    hsx::launch_candidate(a, (int)p->elem_items.size(), 1, p->cand_smem, S(stream));
   } else {
     a.items = p->d_cand;
     hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));

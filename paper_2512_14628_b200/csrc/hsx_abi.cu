@@ -86,14 +86,14 @@ struct hsx_plan {
   long long ktotal[2] = {0, 0};
   long long ctotal = 0;  // column-map entries (sum of L over prunable layers, padded to 4)
   std::vector<DevLayer> layers;
-  std::vector<Item> cand_dyn, elem_items, proj_items, word_items;
+  std::vector<Item> cand_dyn, elem_items, stream_items, proj_items, word_items;
   std::vector<int> pass_list[hsx::kMaxPasses];
   std::vector<int> prunable;
   size_t cand_smem = 0, select_smem[hsx::kMaxPasses] = {0, 0, 0}, mark_smem = 0;
   int sqcap = 0;
   // device
   DevLayer* d_layers = nullptr;
-  Item *d_cand = nullptr, *d_elem = nullptr, *d_proj = nullptr, *d_word = nullptr;
+  Item *d_cand = nullptr, *d_elem = nullptr, *d_stream = nullptr, *d_proj = nullptr, *d_word = nullptr;
   unsigned int* d_layer_done = nullptr;
   int* d_pass[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
@@ -108,7 +108,7 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_elem, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done, maps.rowkeep, maps.colkeep,
                     maps.rowbase, maps.colpos};
     for (void* p : ptrs)
@@ -200,7 +200,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         ly.nparts = (ly.rows + tr - 1) / tr;
         for (int pt = 0; pt < ly.nparts; ++pt)
           for (int cc = 0; cc < nchunks; ++cc) {
-            Item it{l, pt, cc, 0, (long long)pt * tr, std::min<long long>((long long)(pt + 1) * tr, ly.rows)};
+            Item it{l, pt, cc, 1, (long long)pt * tr, std::min<long long>((long long)(pt + 1) * tr, ly.rows)};
             p->cand_dyn.push_back(it);
           }
         quadcap = std::max(quadcap, 4 * tq * (256 / tq));
@@ -240,9 +240,23 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       ly.cpoff = cpoff;
       cpoff += (ly.L + 3) / 4 * 4;
       p->prunable.push_back(l);
-      for (long long b = 0; b < ly.n; b += kItemElems) {
-        Item it{l, 0, 0, 0, b, std::min(ly.n, b + kItemElems)};
-        p->proj_items.push_back(it);
+      ly.qtile = (ly.L % 32) == 0 ? 1 : 0;
+      if (ly.qtile) {
+        // row-quad tiles for K3 / K6 / K7 (same shape as the K1 quad tiles)
+        const int tq = hsx_tile_quads, tr = hsx_tile_rows;
+        const int nchunks = (ly.L / 4 + tq - 1) / tq;
+        for (int r0 = 0; r0 < ly.rows; r0 += tr)
+          for (int cc = 0; cc < nchunks; ++cc) {
+            Item it{l, r0 / tr, cc, 1, (long long)r0, std::min<long long>(r0 + tr, ly.rows)};
+            p->proj_items.push_back(it);
+            p->stream_items.push_back(it);
+          }
+      } else {
+        for (long long b = 0; b < ly.n; b += kItemElems) {
+          Item it{l, 0, 0, 0, b, std::min(ly.n, b + kItemElems)};
+          p->proj_items.push_back(it);
+          p->stream_items.push_back(it);
+        }
       }
       const int nwi = (int)((ly.n + kWordItem * 32 - 1) / (kWordItem * 32));
       for (long long b = 0; b < ly.n; b += kWordItem * 32) {
@@ -260,6 +274,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     for (long long b = 0; b < ly.n; b += kItemElems) {
       Item it{l, 0, 0, 0, b, std::min(ly.n, b + kItemElems)};
       p->elem_items.push_back(it);
+      if (ly.ncons == 0) p->stream_items.push_back(it);
     }
     // initial keep sets: everything kept (all-ones initial masks, consensus.py:418)
     srow[HSX_SUM_KOUT] = ly.rows;
@@ -303,6 +318,7 @@ int upload_plan(hsx_plan* p) {
   if ((rc = upload(&p->d_cand, p->cand_dyn))) return rc;
   if ((rc = alloc0(&p->d_layer_done, (long long)p->prunable.size()))) return rc;
   if ((rc = upload(&p->d_elem, p->elem_items))) return rc;
+  if ((rc = upload(&p->d_stream, p->stream_items))) return rc;
   if ((rc = upload(&p->d_proj, p->proj_items))) return rc;
   if ((rc = upload(&p->d_word, p->word_items))) return rc;
   if ((rc = upload(&p->d_prunable, p->prunable))) return rc;
@@ -633,7 +649,7 @@ static hsx::ElemArgs elem_args(const hsx_plan* p) {
   hsx::ElemArgs a;
   std::memset(&a, 0, sizeof(a));
   a.layers = p->d_layers;
-  a.items = p->d_elem;
+  a.items = p->d_stream;
   a.rowbase = p->maps.rowbase;
   a.colpos = p->maps.colpos;
   a.summary = p->d_summary;
@@ -651,7 +667,7 @@ int hsx_compact_dual(const hsx_plan* p, const float* theta, float* u, const floa
   a.zn = z_node;
   a.vin = v;
   a.flat_out = flat;
-  hsx::launch_compact(a, (int)p->elem_items.size(), S(stream));
+  hsx::launch_compact(a, (int)p->stream_items.size(), S(stream));
   HSX_LAUNCHED("compact_dual");
   return HSX_OK;
 }
@@ -675,7 +691,7 @@ int hsx_decompact_dual(const hsx_plan* p, const float* flat, float divisor, cons
   a.zn = z_node;
   a.v = v;
   a.z = z;
-  hsx::launch_decompact(a, (int)p->elem_items.size(), S(stream));
+  hsx::launch_decompact(a, (int)p->stream_items.size(), S(stream));
   HSX_LAUNCHED("decompact_dual");
   return HSX_OK;
 }

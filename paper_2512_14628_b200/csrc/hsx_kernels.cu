@@ -105,11 +105,19 @@ __device__ __forceinline__ void ring_run(int count, Issue issue, Consume consume
 
 // fp64 candidate; explicit _rn intrinsics (no FMA contraction) so the value is
 // bit-identical to numpy's (rho1 * s + rho2 * (z - v)) / gamma.
-__device__ __forceinline__ double cand_of(double s, double z, double v, const DevLayer& ly,
-                                          int identity) {
-  if (identity) return s;
-  double num = __dadd_rn(__dmul_rn(ly.rho1, s), __dmul_rn(ly.rho2, __dsub_rn(z, v)));
-  return __ddiv_rn(num, ly.gamma);
+struct Coef {
+  double rho1, rho2, gamma;
+  int identity;
+};
+
+__device__ __forceinline__ Coef coef_of(const CandArgs& p, const DevLayer& ly) {
+  return Coef{ly.rho1, ly.rho2, ly.gamma, p.identity};
+}
+
+__device__ __forceinline__ double cand_of(double s, double z, double v, const Coef& cf) {
+  if (cf.identity) return s;
+  double num = __dadd_rn(__dmul_rn(cf.rho1, s), __dmul_rn(cf.rho2, __dsub_rn(z, v)));
+  return __ddiv_rn(num, cf.gamma);
 }
 
 struct In4 {
@@ -129,15 +137,15 @@ __device__ __forceinline__ In4 load_in4(const CandArgs& p, long long gi) {
   return r;
 }
 
-__device__ __forceinline__ double cand4(const CandArgs& p, const In4& x, int i, const DevLayer& ly) {
+__device__ __forceinline__ double cand4(const CandArgs& p, const In4& x, int i, const Coef& cf) {
   double s = p.s ? (double)f4get(x.a, i) : __dadd_rn((double)f4get(x.a, i), (double)f4get(x.b, i));
-  return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), ly, p.identity);
+  return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), cf);
 }
 
 __device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, const DevLayer& ly) {
   double s = p.s ? (double)p.s[gi] : __dadd_rn((double)p.theta[gi], (double)p.u[gi]);
   if (p.identity) return s;
-  return cand_of(s, (double)p.z[gi], (double)p.v[gi], ly, 0);
+  return cand_of(s, (double)p.z[gi], (double)p.v[gi], coef_of(p, ly));
 }
 
 __device__ __forceinline__ int group_of(int grp, unsigned o, unsigned col, unsigned c) {
@@ -163,6 +171,8 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
   const bool masked = frozen && ly.ncons > 0 && p.fmask != nullptr;
   const long long nq = (end - begin + 3) >> 2;
   const int t = threadIdx.x;
+  const Coef cf = coef_of(p, ly);
+  const long long n = ly.n, off = ly.off, mword = ly.mword;
   const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
   const float* A = p.s ? p.s + ly.off : p.theta + ly.off;
   const float* B = p.s ? nullptr : p.u + ly.off;
@@ -170,11 +180,11 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
   const float* V = p.identity ? nullptr : p.v + ly.off;
   auto issue = [&](int d, int i) {
     long long e = begin + 4 * (t + (long long)i * kThreads);
-    cp_quad(ring_slot<4>(ring, d, 0), A, e, ly.n);
-    if (B) cp_quad(ring_slot<4>(ring, d, 1), B, e, ly.n);
+    cp_quad(ring_slot<4>(ring, d, 0), A, e, n);
+    if (B) cp_quad(ring_slot<4>(ring, d, 1), B, e, n);
     if (Z) {
-      cp_quad(ring_slot<4>(ring, d, 2), Z, e, ly.n);
-      cp_quad(ring_slot<4>(ring, d, 3), V, e, ly.n);
+      cp_quad(ring_slot<4>(ring, d, 2), Z, e, n);
+      cp_quad(ring_slot<4>(ring, d, 3), V, e, n);
     }
   };
   auto consume = [&](int d, int i) {
@@ -184,18 +194,18 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
     x.b = B ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
     x.z = Z ? *ring_slot<4>(ring, d, 2) : make_float4(0.f, 0.f, 0.f, 0.f);
     x.v = Z ? *ring_slot<4>(ring, d, 3) : make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t bits = masked ? p.fmask[ly.mword + (e >> 5)] : 0u;
+    uint32_t bits = masked ? p.fmask[mword + (e >> 5)] : 0u;
     float4 out;
 #pragma unroll
     for (int i2 = 0; i2 < 4; ++i2) {
-      double c = cand4(p, x, i2, ly);
+      double c = cand4(p, x, i2, cf);
       if (masked) c = ((bits >> ((e + i2) & 31)) & 1u) ? c : c * 0.0;
       f4set(out, i2, (float)c);
     }
-    if (e + 3 < ly.n) {
-      st4(p.zn + ly.off + e, out);
+    if (e + 3 < n) {
+      st4(p.zn + off + e, out);
     } else {
-      for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) p.zn[ly.off + e + i2] = f4get(out, i2);
+      for (int i2 = 0; i2 < 4 && e + i2 < n; ++i2) p.zn[off + e + i2] = f4get(out, i2);
     }
   };
   ring_run(count, issue, consume);
@@ -224,6 +234,8 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const float* B = p.s ? nullptr : p.u + ly.off;
   const float* Z = p.identity ? nullptr : p.z + ly.off;
   const float* V = p.identity ? nullptr : p.v + ly.off;
+  const Coef cf = coef_of(p, ly);
+  const long long off = ly.off;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   auto issue = [&](int d, int i) {
     long long e = (r0 + (long long)i * RP) * L + 4 * j;
@@ -241,15 +253,15 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
     x.b = B ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
     x.z = Z ? *ring_slot<4>(ring, d, 2) : make_float4(0.f, 0.f, 0.f, 0.f);
     x.v = Z ? *ring_slot<4>(ring, d, 3) : make_float4(0.f, 0.f, 0.f, 0.f);
-    double c0 = cand4(p, x, 0, ly), c1 = cand4(p, x, 1, ly);
-    double c2 = cand4(p, x, 2, ly), c3 = cand4(p, x, 3, ly);
+    double c0 = cand4(p, x, 0, cf), c1 = cand4(p, x, 1, cf);
+    double c2 = cand4(p, x, 2, cf), c3 = cand4(p, x, 3, cf);
     if (pass > 0) {
       if (!kept_by(ly, p.flags, pass, e + 0)) c0 = 0.0;
       if (!kept_by(ly, p.flags, pass, e + 1)) c1 = 0.0;
       if (!kept_by(ly, p.flags, pass, e + 2)) c2 = 0.0;
       if (!kept_by(ly, p.flags, pass, e + 3)) c3 = 0.0;
     } else {
-      st4(p.zn + ly.off + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
+      st4(p.zn + off + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
     }
     a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
     a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
@@ -488,35 +500,74 @@ void launch_select(const DevLayer* layers, const int* list, int n, int pass, con
 // one uchar4 column-keep load; 8 lanes' nibbles OR-fold into one mask word.
 // ---------------------------------------------------------------------------
 
+// Layer fields the streaming kernels use, loaded once into registers (stores
+// through the float arenas would otherwise force reloads of the layer table).
+struct LayerRegs {
+  long long off, n, mword, okeep, cpoff;
+  int L, ncons, qtile;
+  FastDiv divL;
+  __device__ __forceinline__ LayerRegs(const DevLayer* __restrict__ layers, int l) {
+    const DevLayer& ly = layers[l];
+    off = ly.off; n = ly.n; mword = ly.mword; okeep = ly.okeep; cpoff = ly.cpoff;
+    L = ly.L; ncons = ly.ncons; qtile = ly.qtile; divL = ly.divL;
+  }
+};
+
+// Row-quad tiles (prunable layers with c_in*kh*kw % 32 == 0): an item is rows
+// [begin, end) x quad chunk `chunk` (64 quads); thread t owns quad
+// chunk*64 + (t & 63) and walks rows begin + (t >> 6) + 4i. Column maps are
+// loop-invariant registers; row maps of the tile sit in shared memory.
+constexpr int kRowPhases = kThreads / kTileQuads;  // 4
+constexpr int kMaxTileRows = 32;
+
+struct TileCtx {
+  int j, jj, ph;
+  long long r0, r1;
+  int count;
+  bool valid;
+  __device__ __forceinline__ TileCtx(const Item& it, int L) {
+    jj = threadIdx.x & (kTileQuads - 1);
+    ph = threadIdx.x / kTileQuads;
+    j = it.chunk * kTileQuads + jj;
+    r0 = it.begin + ph;
+    r1 = it.end;
+    valid = 4 * j < L;
+    count = (valid && r0 < r1) ? (int)((r1 - r0 + kRowPhases - 1) / kRowPhases) : 0;
+  }
+  __device__ __forceinline__ long long row(int i) const { return r0 + (long long)i * kRowPhases; }
+};
+
 __global__ void __launch_bounds__(kThreads) k_project(const DevLayer* __restrict__ layers,
                                                       const Item* __restrict__ items,
                                                       float* __restrict__ zn,
                                                       uint32_t* __restrict__ mask, Maps m) {
   extern __shared__ float4 ring[];
+  __shared__ uint8_t s_rk[kMaxTileRows];
   const Item it = items[blockIdx.x];
-  const DevLayer& ly = layers[it.layer];
+  const LayerRegs ly(layers, it.layer);
   const int lane = threadIdx.x & 31;
-  if ((ly.L & 3) == 0) {
-    // warp w handles 32 consecutive quads per stage; 8 lanes' nibbles make a word
-    const long long q1 = (it.end + 3) >> 2;                        // begin is a multiple of 32
-    const long long qw = (it.begin >> 2) + (threadIdx.x & ~31);    // warp's first quad
-    const int count = qw < q1 ? (int)((q1 - qw + kThreads - 1) / kThreads) : 0;
+  if (it.tile == 1) {
+    // row-quad tile: 8 lanes (same row, 8 consecutive quads) make one mask word
+    const TileCtx tc(it, ly.L);
+    for (int r = threadIdx.x; r < it.end - it.begin; r += kThreads) s_rk[r] = m.rowkeep[ly.okeep + it.begin + r];
+    uchar4 ck = tc.valid ? *reinterpret_cast<const uchar4*>(m.colkeep + ly.cpoff + 4 * tc.j)
+                         : make_uchar4(0, 0, 0, 0);
+    __syncthreads();
     const float* src = zn + ly.off;
+    // all lanes of a warp share a row phase; quads past the row end (a suffix of the
+    // last chunk, whole 8-lane groups since L % 32 == 0) only join the shuffles
+    const int count = __shfl_sync(kFull, tc.count, 0);
     auto issue = [&](int d, int i) {
-      long long q = qw + lane + (long long)i * kThreads;
-      if (q < q1) cp_quad(ring_slot<1>(ring, d, 0), src, q << 2, ly.n);
+      if (tc.valid) cp16(ring_slot<1>(ring, d, 0), src + tc.row(i) * ly.L + 4 * tc.j);
     };
     auto consume = [&](int d, int i) {
-      long long q = qw + lane + (long long)i * kThreads;
-      long long e = q << 2;
+      const long long r = tc.row(i);
+      const long long e = r * ly.L + 4 * tc.j;
       unsigned nib = 0;
-      if (q < q1 && e < ly.n) {
+      if (tc.valid) {
         float4 v = *ring_slot<1>(ring, d, 0);
-        unsigned o = fdiv((unsigned)e, ly.divL);
-        unsigned col = (unsigned)e - o * (unsigned)ly.L;
-        int rk = m.rowkeep[ly.okeep + o];
-        uchar4 ck = *reinterpret_cast<const uchar4*>(m.colkeep + ly.cpoff + col);
-        bool k0 = rk && ck.x, k1 = rk && ck.y, k2 = rk && ck.z, k3 = rk && ck.w;
+        const bool rk = s_rk[r - it.begin] != 0;
+        const bool k0 = rk && ck.x, k1 = rk && ck.y, k2 = rk && ck.z, k3 = rk && ck.w;
         nib = (unsigned)(k0 && v.x != 0.f) | ((unsigned)(k1 && v.y != 0.f) << 1) |
               ((unsigned)(k2 && v.z != 0.f) << 2) | ((unsigned)(k3 && v.w != 0.f) << 3);
         if (!(k0 && k1 && k2 && k3)) {
@@ -524,32 +575,26 @@ __global__ void __launch_bounds__(kThreads) k_project(const DevLayer* __restrict
           if (!k1) v.y = 0.f;
           if (!k2) v.z = 0.f;
           if (!k3) v.w = 0.f;
-          if (e + 3 < ly.n) {
-            st4(zn + ly.off + e, v);
-          } else {
-            for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) zn[ly.off + e + i2] = f4get(v, i2);
-          }
+          st4(zn + ly.off + e, v);
         }
-        if (e + 3 >= ly.n) nib &= (1u << (ly.n - e)) - 1u;
       }
       unsigned w = nib << (4 * (lane & 7));
       w |= __shfl_xor_sync(kFull, w, 1);
       w |= __shfl_xor_sync(kFull, w, 2);
       w |= __shfl_xor_sync(kFull, w, 4);
-      if ((lane & 7) == 0 && q < q1 && e < ly.n) mask[ly.mword + (e >> 5)] = w;
+      if ((lane & 7) == 0 && tc.valid) mask[ly.mword + (e >> 5)] = w;
     };
     ring_run(count, issue, consume);
     return;
   }
-  // rows of L % 4 != 0 elements (stem convs): one warp per 32-element word
+  // contiguous ranges of other prunable layers: one warp per 32-element word
   const int warp = threadIdx.x >> 5;
   const long long w0 = it.begin >> 5, w1 = (it.end + 31) >> 5;
   for (long long w = w0 + warp; w < w1; w += kThreads / 32) {
     long long e = (w << 5) + lane;
-    bool valid = e < ly.n;
     bool kp = false;
     float x = 0.f;
-    if (valid) {
+    if (e < ly.n) {
       unsigned o = fdiv((unsigned)e, ly.divL);
       unsigned col = (unsigned)e - o * (unsigned)ly.L;
       kp = m.rowkeep[ly.okeep + o] && m.colkeep[ly.cpoff + col];
@@ -797,55 +842,48 @@ void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t 
 // (int4 load of colpos per quad), -1 entries are dropped coordinates.
 // ---------------------------------------------------------------------------
 
-// payload index of 4 consecutive elements e..e+3 (same row when L % 4 == 0)
-__device__ __forceinline__ int4 quad_dst(const ElemArgs& a, const DevLayer& ly, long long e) {
+// payload index of element e of a non-tiled prunable layer (-1: dropped)
+__device__ __forceinline__ int elem_dst(const int* __restrict__ rowbase, const int* __restrict__ colpos,
+                                        const LayerRegs& ly, long long e) {
   unsigned o = fdiv((unsigned)e, ly.divL);
   unsigned col = (unsigned)e - o * (unsigned)ly.L;
-  int rb = a.rowbase[ly.okeep + o];
-  int4 cp = *reinterpret_cast<const int4*>(a.colpos + ly.cpoff + col);
+  int rb = rowbase[ly.okeep + o], cp = colpos[ly.cpoff + col];
+  return (rb < 0 || cp < 0) ? -1 : rb + cp;
+}
+
+// payload indices of the quad at e of a contiguous item (dense or non-tiled prunable)
+__device__ __forceinline__ int4 dst4_linear(const ElemArgs& a, const LayerRegs& ly, long long e) {
+  if (ly.ncons == 0) {
+    int b = (int)e;
+    return make_int4(b, e + 1 < ly.n ? b + 1 : -1, e + 2 < ly.n ? b + 2 : -1, e + 3 < ly.n ? b + 3 : -1);
+  }
+  int4 d;
+  d.x = elem_dst(a.rowbase, a.colpos, ly, e);
+  d.y = e + 1 < ly.n ? elem_dst(a.rowbase, a.colpos, ly, e + 1) : -1;
+  d.z = e + 2 < ly.n ? elem_dst(a.rowbase, a.colpos, ly, e + 2) : -1;
+  d.w = e + 3 < ly.n ? elem_dst(a.rowbase, a.colpos, ly, e + 3) : -1;
+  return d;
+}
+
+__device__ __forceinline__ int4 add_base(int rb, int4 cp) {
   if (rb < 0) return make_int4(-1, -1, -1, -1);
   return make_int4(cp.x < 0 ? -1 : rb + cp.x, cp.y < 0 ? -1 : rb + cp.y, cp.z < 0 ? -1 : rb + cp.z,
                    cp.w < 0 ? -1 : rb + cp.w);
 }
 
-__device__ __forceinline__ int elem_dst(const ElemArgs& a, const DevLayer& ly, long long e) {
-  unsigned o = fdiv((unsigned)e, ly.divL);
-  unsigned col = (unsigned)e - o * (unsigned)ly.L;
-  int rb = a.rowbase[ly.okeep + o], cp = a.colpos[ly.cpoff + col];
-  return (rb < 0 || cp < 0) ? -1 : rb + cp;
-}
-
-// payload indices of the quad at e (-1: dropped, or past the layer end)
-__device__ __forceinline__ int4 dst4(const ElemArgs& a, const DevLayer& ly, long long e) {
-  if (ly.ncons == 0) {
-    int b = (int)e;
-    return make_int4(b, e + 1 < ly.n ? b + 1 : -1, e + 2 < ly.n ? b + 2 : -1, e + 3 < ly.n ? b + 3 : -1);
-  }
-  if ((ly.L & 3) == 0 && e + 3 < ly.n) return quad_dst(a, ly, e);
-  int4 d;
-  d.x = elem_dst(a, ly, e);
-  d.y = e + 1 < ly.n ? elem_dst(a, ly, e + 1) : -1;
-  d.z = e + 2 < ly.n ? elem_dst(a, ly, e + 2) : -1;
-  d.w = e + 3 < ly.n ? elem_dst(a, ly, e + 3) : -1;
-  return d;
-}
-
-// K6: flat[payload] <- z_node + v  (+ u <- u + (theta - z_node)), one item of one layer
+// K6: flat[payload] <- z_node + v  (+ u <- u + (theta - z_node)) for one item
 __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   extern __shared__ float4 ring[];
+  __shared__ int s_rb[kMaxTileRows];
   const Item it = a.items[blockIdx.x];
-  const DevLayer& ly = a.layers[it.layer];
+  const LayerRegs ly(a.layers, it.layer);
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
-  const long long nq = (it.end - it.begin + 3) >> 2;
-  const int t = threadIdx.x;
-  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
-  const float* ZN = a.zn + ly.off;
-  const float* VI = a.vin ? a.vin + ly.off : nullptr;
-  const float* TH = a.u ? a.theta + ly.off : nullptr;
-  const float* UU = a.u ? a.u + ly.off : nullptr;
-  float* flat = a.flat_out + coff;
-  auto issue = [&](int d, int i) {
-    long long e = it.begin + 4 * (t + (long long)i * kThreads);
+  const float* __restrict__ ZN = a.zn + ly.off;
+  const float* __restrict__ VI = a.vin ? a.vin + ly.off : nullptr;
+  const float* __restrict__ TH = a.u ? a.theta + ly.off : nullptr;
+  float* __restrict__ UU = a.u ? a.u + ly.off : nullptr;
+  float* __restrict__ flat = a.flat_out + coff;
+  auto load4 = [&](int d, long long e) {
     cp_quad(ring_slot<4>(ring, d, 0), ZN, e, ly.n);
     if (VI) cp_quad(ring_slot<4>(ring, d, 1), VI, e, ly.n);
     if (TH) {
@@ -853,28 +891,45 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
       cp_quad(ring_slot<4>(ring, d, 3), UU, e, ly.n);
     }
   };
-  auto consume = [&](int d, int i) {
-    long long e = it.begin + 4 * (t + (long long)i * kThreads);
+  auto emit = [&](int d, long long e, int4 dd) {
     float4 zn = *ring_slot<4>(ring, d, 0);
     float4 vv = VI ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const bool full = e + 3 < ly.n;
     if (TH) {
       float4 th = *ring_slot<4>(ring, d, 2), uu = *ring_slot<4>(ring, d, 3);
       float4 un = make_float4(dual1(uu.x, th.x, zn.x), dual1(uu.y, th.y, zn.y), dual1(uu.z, th.z, zn.z),
                               dual1(uu.w, th.w, zn.w));
-      if (full) {
-        st4(a.u + ly.off + e, un);
+      if (e + 3 < ly.n) {
+        st4(UU + e, un);
       } else {
-        for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) a.u[ly.off + e + i2] = f4get(un, i2);
+        for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) UU[e + i2] = f4get(un, i2);
       }
     }
-    int4 dd = dst4(a, ly, e);
     if (dd.x >= 0) flat[dd.x] = zn.x + vv.x;
     if (dd.y >= 0) flat[dd.y] = zn.y + vv.y;
     if (dd.z >= 0) flat[dd.z] = zn.z + vv.z;
     if (dd.w >= 0) flat[dd.w] = zn.w + vv.w;
   };
-  ring_run(count, issue, consume);
+  if (it.tile == 1) {
+    const TileCtx tc(it, ly.L);
+    for (int r = threadIdx.x; r < it.end - it.begin; r += kThreads) s_rb[r] = a.rowbase[ly.okeep + it.begin + r];
+    const int4 cp = tc.valid ? *reinterpret_cast<const int4*>(a.colpos + ly.cpoff + 4 * tc.j)
+                             : make_int4(-1, -1, -1, -1);
+    __syncthreads();
+    ring_run(tc.count, [&](int d, int i) { load4(d, tc.row(i) * ly.L + 4 * tc.j); },
+             [&](int d, int i) {
+               const long long r = tc.row(i);
+               emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
+             });
+    return;
+  }
+  const long long nq = (it.end - it.begin + 3) >> 2;
+  const int t = threadIdx.x;
+  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
+  ring_run(count, [&](int d, int i) { load4(d, it.begin + 4 * (t + (long long)i * kThreads)); },
+           [&](int d, int i) {
+             const long long e = it.begin + 4 * (t + (long long)i * kThreads);
+             emit(d, e, dst4_linear(a, ly, e));
+           });
 }
 
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
@@ -885,23 +940,20 @@ void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
 }
 
 // K7: z <- zero-filled gather of flat / divisor (+ v <- v + (z_node - z)); the
-// gather itself streams through the ring: dropped coordinates are zero-filled
-// by cp.async without touching memory.
+// gather streams through the ring: dropped coordinates are zero-filled by
+// cp.async without touching memory.
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   extern __shared__ float4 ring[];
+  __shared__ int s_rb[kMaxTileRows];
   const Item it = a.items[blockIdx.x];
-  const DevLayer& ly = a.layers[it.layer];
+  const LayerRegs ly(a.layers, it.layer);
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
-  const long long nq = (it.end - it.begin + 3) >> 2;
-  const int t = threadIdx.x;
-  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
-  const float* flat = a.flat_in + coff;
-  const float* ZN = a.v ? a.zn + ly.off : nullptr;
-  const float* VV = a.v ? a.v + ly.off : nullptr;
+  const float* __restrict__ flat = a.flat_in + coff;
+  const float* __restrict__ ZN = a.v ? a.zn + ly.off : nullptr;
+  float* __restrict__ VV = a.v ? a.v + ly.off : nullptr;
+  float* __restrict__ ZO = a.z + ly.off;
   const float div = a.divisor;
-  auto issue = [&](int d, int i) {
-    long long e = it.begin + 4 * (t + (long long)i * kThreads);
-    int4 dd = dst4(a, ly, e);
+  auto load = [&](int d, long long e, int4 dd) {
     float* g = reinterpret_cast<float*>(ring_slot<3>(ring, d, 0));
     cp4z(g + 0, flat + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
     cp4z(g + 1, flat + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
@@ -912,8 +964,7 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
       cp_quad(ring_slot<3>(ring, d, 2), VV, e, ly.n);
     }
   };
-  auto consume = [&](int d, int i) {
-    long long e = it.begin + 4 * (t + (long long)i * kThreads);
+  auto emit = [&](int d, long long e) {
     float4 zo = *ring_slot<3>(ring, d, 0);
     if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
     float4 vn;
@@ -923,16 +974,38 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
                        dual1(vv.w, zn.w, zo.w));
     }
     if (e + 3 < ly.n) {
-      st4(a.z + ly.off + e, zo);
-      if (ZN) st4(a.v + ly.off + e, vn);
+      st4(ZO + e, zo);
+      if (ZN) st4(VV + e, vn);
     } else {
       for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) {
-        a.z[ly.off + e + i2] = f4get(zo, i2);
-        if (ZN) a.v[ly.off + e + i2] = f4get(vn, i2);
+        ZO[e + i2] = f4get(zo, i2);
+        if (ZN) VV[e + i2] = f4get(vn, i2);
       }
     }
   };
-  ring_run(count, issue, consume);
+  if (it.tile == 1) {
+    const TileCtx tc(it, ly.L);
+    for (int r = threadIdx.x; r < it.end - it.begin; r += kThreads) s_rb[r] = a.rowbase[ly.okeep + it.begin + r];
+    const int4 cp = tc.valid ? *reinterpret_cast<const int4*>(a.colpos + ly.cpoff + 4 * tc.j)
+                             : make_int4(-1, -1, -1, -1);
+    __syncthreads();
+    ring_run(tc.count,
+             [&](int d, int i) {
+               const long long r = tc.row(i);
+               load(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
+             },
+             [&](int d, int i) { emit(d, tc.row(i) * ly.L + 4 * tc.j); });
+    return;
+  }
+  const long long nq = (it.end - it.begin + 3) >> 2;
+  const int t = threadIdx.x;
+  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
+  ring_run(count,
+           [&](int d, int i) {
+             const long long e = it.begin + 4 * (t + (long long)i * kThreads);
+             load(d, e, dst4_linear(a, ly, e));
+           },
+           [&](int d, int i) { emit(d, it.begin + 4 * (t + (long long)i * kThreads)); });
 }
 
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {

@@ -52,6 +52,8 @@ struct DevLayer {
   int rsub;                    // rows per shared-memory sub-tile
   int rank;
   int tiling;                  // 0: row tiles (partials per group / row), 1: quad tiles (per column)
+  int qtile;                   // K3/K6/K7 use row-quad tiles (prunable, c_in*kh*kw % 32 == 0)
+  int pad2;
   int pidx;                    // index among prunable layers
   int group[kMaxPasses];
   int keep[kMaxPasses];
@@ -64,8 +66,8 @@ struct DevLayer {
 struct Item {
   int layer;
   int part;   // candidate: row-tile index; keep-mark: prunable-layer index
-  int chunk;  // candidate (quad tiling): column chunk of 64 quads; keep-mark: items of the layer
-  int pad;
+  int chunk;  // quad tiles: column chunk of 64 quads; keep-mark: items of the layer
+  int tile;   // 1: row-quad tile, [begin, end) are rows; 0: element range
   long long begin, end;  // element range (quad tiling: rows [begin, end))
 };
 

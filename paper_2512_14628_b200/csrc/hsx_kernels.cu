@@ -8,10 +8,23 @@ namespace hsx {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
 
-// opt a kernel into > 48 KB of dynamic shared memory (idempotent, cheap)
+// opt a kernel into large dynamic shared memory (dynamic + static must fit the
+// per-block limit, so anything above 32 KB opts in); one driver call per kernel
+// and size, remembered in a small table keyed by the kernel address
 template <typename K>
 static void allow_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  static const void* keys[32];
+  static size_t granted[32];
+  if (bytes <= 32 * 1024) return;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  int slot = 0;
+  while (slot < 32 && keys[slot] && keys[slot] != key) ++slot;
+  if (slot < 32 && keys[slot] == key && granted[slot] >= bytes) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (slot < 32) {
+    keys[slot] = key;
+    granted[slot] = bytes;
+  }
 }
 
 // streaming 128-bit load of data read exactly once (evict-first)

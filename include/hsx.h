@@ -196,6 +196,13 @@ int hsx_unpack_bits(const uint32_t* bits, int64_t n, uint8_t* m, void* stream);
 int hsx_count_diff_u8(const uint8_t* a, const uint8_t* b, int64_t n, uint64_t* count_dev,
                       void* stream);
 
+/* Self-test of the candidate kernel's division: out[i] = num[i] / den computed
+ * exactly as K1 does (q = RN(num*y), r = fma(-q, den, num), q' = fma(r, y, q)
+ * with y = RN(1/den), Markstein's FMA correction). Tests compare it bit for
+ * bit with IEEE division (numpy) to back the claim that K1's fp64 candidate is
+ * the reference's (rho1*S + rho2*(z-v)) / gamma. */
+int hsx_selftest_division(const double* num, int64_t n, double den, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,7 @@ SIGNATURES = {
     "hsx_pack_bits": (C.c_int, [VP, I64, VP, VP]),
     "hsx_unpack_bits": (C.c_int, [VP, I64, VP, VP]),
     "hsx_count_diff_u8": (C.c_int, [VP, VP, I64, VP, VP]),
+    "hsx_selftest_division": (C.c_int, [VP, I64, F64, VP, VP]),
 }
 
 _lib = None

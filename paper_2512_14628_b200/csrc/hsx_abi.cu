@@ -164,6 +164,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     ly.rho1 = d.rho1;
     ly.rho2 = d.rho2;
     ly.gamma = 1.0;
+    ly.rgamma = 1.0;
     ly.mword = -1;
     ly.okeep = ly.ikeep = ly.cpoff = -1;
     for (int q = 0; q < hsx::kMaxPasses; ++q) ly.goff[q] = ly.poff[q] = -1;
@@ -263,7 +264,8 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         Item it{l, ly.pidx, nwi, 0, b, std::min(ly.n, b + kWordItem * 32)};
         p->word_items.push_back(it);
         long long r_lo = b / ly.L, r_hi = (it.end - 1) / ly.L;
-        mark_smem = std::max<size_t>(mark_smem, (size_t)ly.cin + (size_t)(r_hi - r_lo + 1));
+        mark_smem = std::max<size_t>(mark_smem, std::max<size_t>((size_t)ly.cin + (size_t)(r_hi - r_lo + 1),
+                                                                  4 * (size_t)ly.cin));
       }
     } else {
       for (long long b = 0; b < ly.n; b += kItemElems) {
@@ -438,6 +440,7 @@ int hsx_plan_set_penalties(hsx_plan* p, const double* rho1, const double* rho2, 
     if (!identity && !(gamma > 0.0))
       return fail(HSX_ECONFIG, "non-positive candidate normalizer gamma=%g (layer %d)", gamma, l);
     ly.gamma = gamma;
+    ly.rgamma = 1.0 / gamma;
   }
   p->identity = identity ? 1 : 0;
   if (p->n_layers)
@@ -714,6 +717,14 @@ int hsx_unpack_bits(const uint32_t* bits, int64_t n, uint8_t* m, void* stream) {
   HSX_LAUNCHED("unpack_bits");
   return HSX_OK;
 }
+int hsx_selftest_division(const double* num, int64_t n, double den, double* out, void* stream) {
+  if ((!num || !out) && n > 0) return fail(HSX_EINVAL, "null argument");
+  if (!(den != 0.0)) return fail(HSX_EINVAL, "zero denominator");
+  hsx::launch_div_selftest(num, n, den, out, S(stream));
+  HSX_LAUNCHED("selftest_division");
+  return HSX_OK;
+}
+
 int hsx_count_diff_u8(const uint8_t* a, const uint8_t* b, int64_t n, uint64_t* count_dev,
                       void* stream) {
   if ((!a || !b || !count_dev) && n > 0) return fail(HSX_EINVAL, "null argument");

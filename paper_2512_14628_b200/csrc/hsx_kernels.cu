@@ -119,46 +119,51 @@ __device__ __forceinline__ void ring_run(int count, Issue issue, Consume consume
 // fp64 candidate; explicit _rn intrinsics (no FMA contraction) so the value is
 // bit-identical to numpy's (rho1 * s + rho2 * (z - v)) / gamma.
 struct Coef {
-  double rho1, rho2, gamma;
-  int identity;
+  double rho1, rho2, gamma, rgamma;
 };
 
-__device__ __forceinline__ Coef coef_of(const CandArgs& p, const DevLayer& ly) {
-  return Coef{ly.rho1, ly.rho2, ly.gamma, p.identity};
+__device__ __forceinline__ Coef coef_of(const DevLayer& ly) {
+  return Coef{ly.rho1, ly.rho2, ly.gamma, ly.rgamma};
 }
 
-__device__ __forceinline__ double cand_of(double s, double z, double v, const Coef& cf) {
-  if (cf.identity) return s;
-  double num = __dadd_rn(__dmul_rn(cf.rho1, s), __dmul_rn(cf.rho2, __dsub_rn(z, v)));
-  return __ddiv_rn(num, cf.gamma);
+// num / den, correctly rounded: q = RN(num * y) with y = RN(1/den), then one FMA
+// residual correction (Markstein). Exactness vs IEEE division is checked bit for
+// bit by tests/test_gpu_parity.py::test_candidate_division_is_ieee (hsx_selftest_division).
+__device__ __forceinline__ double div_rn(double num, double den, double y) {
+  double q = __dmul_rn(num, y);
+  double r = __fma_rn(-q, den, num);
+  return __fma_rn(r, y, q);
 }
+
+// fp64 candidate; explicit _rn intrinsics (no FMA contraction) so the value is
+// numpy's (rho1 * s + rho2 * (z - v)) / gamma.
+__device__ __forceinline__ double cand_of(double s, double z, double v, const Coef& cf) {
+  double num = __dadd_rn(__dmul_rn(cf.rho1, s), __dmul_rn(cf.rho2, __dsub_rn(z, v)));
+  return div_rn(num, cf.gamma, cf.rgamma);
+}
+
+// input modes of K1 (template parameter): the sum S is given (P > 1) or is
+// theta + u (P == 1, intra all-reduce is the identity); IDENT: candidate = S
+// (per-tensor projection API)
+enum { kModeThetaU = 0, kModeSum = 1, kModeIdent = 2 };
 
 struct In4 {
   float4 a, b, z, v;
 };
 
-__device__ __forceinline__ In4 load_in4(const CandArgs& p, long long gi) {
-  In4 r;
-  r.a = ldcs4(p.s ? p.s + gi : p.theta + gi);
-  r.b = p.s ? make_float4(0.f, 0.f, 0.f, 0.f) : ldcs4(p.u + gi);
-  if (p.identity) {
-    r.z = r.v = make_float4(0.f, 0.f, 0.f, 0.f);
-  } else {
-    r.z = ldcs4(p.z + gi);
-    r.v = ldcs4(p.v + gi);
-  }
-  return r;
-}
-
-__device__ __forceinline__ double cand4(const CandArgs& p, const In4& x, int i, const Coef& cf) {
-  double s = p.s ? (double)f4get(x.a, i) : __dadd_rn((double)f4get(x.a, i), (double)f4get(x.b, i));
+template <int MODE>
+__device__ __forceinline__ double cand4(const In4& x, int i, const Coef& cf) {
+  if (MODE == kModeIdent) return (double)f4get(x.a, i);
+  double s = MODE == kModeSum ? (double)f4get(x.a, i)
+                              : __dadd_rn((double)f4get(x.a, i), (double)f4get(x.b, i));
   return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), cf);
 }
 
-__device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, const DevLayer& ly) {
-  double s = p.s ? (double)p.s[gi] : __dadd_rn((double)p.theta[gi], (double)p.u[gi]);
-  if (p.identity) return s;
-  return cand_of(s, (double)p.z[gi], (double)p.v[gi], coef_of(p, ly));
+template <int MODE>
+__device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, const Coef& cf) {
+  if (MODE == kModeIdent) return (double)p.s[gi];
+  double s = MODE == kModeSum ? (double)p.s[gi] : __dadd_rn((double)p.theta[gi], (double)p.u[gi]);
+  return cand_of(s, (double)p.z[gi], (double)p.v[gi], cf);
 }
 
 __device__ __forceinline__ int group_of(int grp, unsigned o, unsigned col, unsigned c) {
@@ -176,52 +181,70 @@ __device__ __forceinline__ bool kept_by(const DevLayer& ly, const uint8_t* const
   return keep;
 }
 
+// Input slots of the K1 ring: A = S (or theta), B = u (kModeThetaU), Z, V
+template <int MODE>
+__device__ __forceinline__ void k1_issue(float4* ring, int d, const float* A, const float* B,
+                                         const float* Z, const float* V, long long e, long long n) {
+  cp_quad(ring_slot<4>(ring, d, 0), A, e, n);
+  if (MODE == kModeThetaU) cp_quad(ring_slot<4>(ring, d, 1), B, e, n);
+  if (MODE != kModeIdent) {
+    cp_quad(ring_slot<4>(ring, d, 2), Z, e, n);
+    cp_quad(ring_slot<4>(ring, d, 3), V, e, n);
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ In4 k1_read(float4* ring, int d) {
+  In4 x;
+  x.a = *ring_slot<4>(ring, d, 0);
+  x.b = MODE == kModeThetaU ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (MODE != kModeIdent) {
+    x.z = *ring_slot<4>(ring, d, 2);
+    x.v = *ring_slot<4>(ring, d, 3);
+  } else {
+    x.z = x.v = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  return x;
+}
+
 // K1a: elementwise candidate over [begin, end) of one layer (dense layers; every
 // layer in frozen mode, where prunable layers get cand * global mask,
 // consensus.py:177-180). Inputs stream through the per-thread cp.async ring.
+template <int MODE>
 __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long long begin, long long end,
                                  int frozen, float4* ring) {
   const bool masked = frozen && ly.ncons > 0 && p.fmask != nullptr;
   const long long nq = (end - begin + 3) >> 2;
   const int t = threadIdx.x;
-  const Coef cf = coef_of(p, ly);
+  const Coef cf = coef_of(ly);
   const long long n = ly.n, off = ly.off, mword = ly.mword;
   const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
-  const float* A = p.s ? p.s + ly.off : p.theta + ly.off;
-  const float* B = p.s ? nullptr : p.u + ly.off;
-  const float* Z = p.identity ? nullptr : p.z + ly.off;
-  const float* V = p.identity ? nullptr : p.v + ly.off;
-  auto issue = [&](int d, int i) {
-    long long e = begin + 4 * (t + (long long)i * kThreads);
-    cp_quad(ring_slot<4>(ring, d, 0), A, e, n);
-    if (B) cp_quad(ring_slot<4>(ring, d, 1), B, e, n);
-    if (Z) {
-      cp_quad(ring_slot<4>(ring, d, 2), Z, e, n);
-      cp_quad(ring_slot<4>(ring, d, 3), V, e, n);
-    }
-  };
-  auto consume = [&](int d, int i) {
-    long long e = begin + 4 * (t + (long long)i * kThreads);
-    In4 x;
-    x.a = *ring_slot<4>(ring, d, 0);
-    x.b = B ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-    x.z = Z ? *ring_slot<4>(ring, d, 2) : make_float4(0.f, 0.f, 0.f, 0.f);
-    x.v = Z ? *ring_slot<4>(ring, d, 3) : make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t bits = masked ? p.fmask[mword + (e >> 5)] : 0u;
-    float4 out;
+  const float* A = (MODE == kModeThetaU ? p.theta : p.s) + off;
+  const float* B = MODE == kModeThetaU ? p.u + off : nullptr;
+  const float* Z = MODE != kModeIdent ? p.z + off : nullptr;
+  const float* V = MODE != kModeIdent ? p.v + off : nullptr;
+  float* zn = p.zn + off;
+  const uint32_t* fm = masked ? p.fmask + mword : nullptr;
+  ring_run(
+      count,
+      [&](int d, int i) { k1_issue<MODE>(ring, d, A, B, Z, V, begin + 4 * (t + (long long)i * kThreads), n); },
+      [&](int d, int i) {
+        const long long e = begin + 4 * (t + (long long)i * kThreads);
+        const In4 x = k1_read<MODE>(ring, d);
+        const uint32_t bits = fm ? fm[e >> 5] : 0u;
+        float4 out;
 #pragma unroll
-    for (int i2 = 0; i2 < 4; ++i2) {
-      double c = cand4(p, x, i2, cf);
-      if (masked) c = ((bits >> ((e + i2) & 31)) & 1u) ? c : c * 0.0;
-      f4set(out, i2, (float)c);
-    }
-    if (e + 3 < n) {
-      st4(p.zn + off + e, out);
-    } else {
-      for (int i2 = 0; i2 < 4 && e + i2 < n; ++i2) p.zn[off + e + i2] = f4get(out, i2);
-    }
-  };
-  ring_run(count, issue, consume);
+        for (int i2 = 0; i2 < 4; ++i2) {
+          double c = cand4<MODE>(x, i2, cf);
+          if (fm) c = ((bits >> ((e + i2) & 31)) & 1u) ? c : c * 0.0;
+          f4set(out, i2, (float)c);
+        }
+        if (e + 3 < n) {
+          st4(zn + e, out);
+        } else {
+          for (int i2 = 0; i2 < 4 && e + i2 < n; ++i2) zn[e + i2] = f4get(out, i2);
+        }
+      });
 }
 
 // K1b quad tiles (CHANNEL / SHAPE groups, c_in*kh*kw % 4 == 0 — every ResNet conv
@@ -232,6 +255,7 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
 // column (the channel fold happens in K2).
 constexpr int kTileQuads = 64;
 
+template <int MODE>
 __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, float4* ring,
                                 double* cs) {
   constexpr int RP = kThreads / kTileQuads;
@@ -243,45 +267,45 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const int j = it.chunk * kTileQuads + jj;
   const long long r0 = it.begin + ph, r1 = it.end;
   const int count = (j < Q && r0 < r1) ? (int)((r1 - r0 + RP - 1) / RP) : 0;
-  const float* A = p.s ? p.s + ly.off : p.theta + ly.off;
-  const float* B = p.s ? nullptr : p.u + ly.off;
-  const float* Z = p.identity ? nullptr : p.z + ly.off;
-  const float* V = p.identity ? nullptr : p.v + ly.off;
-  const Coef cf = coef_of(p, ly);
   const long long off = ly.off;
+  const float* A = (MODE == kModeThetaU ? p.theta : p.s) + off + 4 * j;
+  const float* B = MODE == kModeThetaU ? p.u + off + 4 * j : nullptr;
+  const float* Z = MODE != kModeIdent ? p.z + off + 4 * j : nullptr;
+  const float* V = MODE != kModeIdent ? p.v + off + 4 * j : nullptr;
+  float* zn = p.zn + off + 4 * j;
+  const Coef cf = coef_of(ly);
+  const long long stride = (long long)RP * L;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  auto issue = [&](int d, int i) {
-    long long e = (r0 + (long long)i * RP) * L + 4 * j;
-    cp16(ring_slot<4>(ring, d, 0), A + e);
-    if (B) cp16(ring_slot<4>(ring, d, 1), B + e);
-    if (Z) {
-      cp16(ring_slot<4>(ring, d, 2), Z + e);
-      cp16(ring_slot<4>(ring, d, 3), V + e);
-    }
-  };
-  auto consume = [&](int d, int i) {
-    long long e = (r0 + (long long)i * RP) * L + 4 * j;
-    In4 x;
-    x.a = *ring_slot<4>(ring, d, 0);
-    x.b = B ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-    x.z = Z ? *ring_slot<4>(ring, d, 2) : make_float4(0.f, 0.f, 0.f, 0.f);
-    x.v = Z ? *ring_slot<4>(ring, d, 3) : make_float4(0.f, 0.f, 0.f, 0.f);
-    double c0 = cand4(p, x, 0, cf), c1 = cand4(p, x, 1, cf);
-    double c2 = cand4(p, x, 2, cf), c3 = cand4(p, x, 3, cf);
-    if (pass > 0) {
-      if (!kept_by(ly, p.flags, pass, e + 0)) c0 = 0.0;
-      if (!kept_by(ly, p.flags, pass, e + 1)) c1 = 0.0;
-      if (!kept_by(ly, p.flags, pass, e + 2)) c2 = 0.0;
-      if (!kept_by(ly, p.flags, pass, e + 3)) c3 = 0.0;
-    } else {
-      st4(p.zn + off + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
-    }
-    a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
-    a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
-    a2 = __dadd_rn(a2, __dmul_rn(c2, c2));
-    a3 = __dadd_rn(a3, __dmul_rn(c3, c3));
-  };
-  ring_run(count, issue, consume);
+  ring_run(
+      count,
+      [&](int d, int i) {
+        const long long e = r0 * L + i * stride;
+        cp16(ring_slot<4>(ring, d, 0), A + e);
+        if (MODE == kModeThetaU) cp16(ring_slot<4>(ring, d, 1), B + e);
+        if (MODE != kModeIdent) {
+          cp16(ring_slot<4>(ring, d, 2), Z + e);
+          cp16(ring_slot<4>(ring, d, 3), V + e);
+        }
+      },
+      [&](int d, int i) {
+        const long long e = r0 * L + i * stride;
+        const In4 x = k1_read<MODE>(ring, d);
+        double c0 = cand4<MODE>(x, 0, cf), c1 = cand4<MODE>(x, 1, cf);
+        double c2 = cand4<MODE>(x, 2, cf), c3 = cand4<MODE>(x, 3, cf);
+        if (pass > 0) {
+          const long long ee = e + 4 * j;
+          if (!kept_by(ly, p.flags, pass, ee + 0)) c0 = 0.0;
+          if (!kept_by(ly, p.flags, pass, ee + 1)) c1 = 0.0;
+          if (!kept_by(ly, p.flags, pass, ee + 2)) c2 = 0.0;
+          if (!kept_by(ly, p.flags, pass, ee + 3)) c3 = 0.0;
+        } else {
+          st4(zn + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
+        }
+        a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
+        a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
+        a2 = __dadd_rn(a2, __dmul_rn(c2, c2));
+        a3 = __dadd_rn(a3, __dmul_rn(c3, c3));
+      });
   double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
@@ -297,6 +321,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
 // K1b row tiles (FILTER groups, composite plans mixing FILTER, rows not a
 // multiple of 4 elements): squares of sub-tiles of rows staged in shared
 // memory; partials per group ([part][G]) or per row (FILTER).
+template <int MODE>
 __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq,
                                double* acc) {
   const int pass = p.pass;
@@ -304,6 +329,7 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
   const int G = ly.G[pass];
   const int L = ly.L;
   const int k = ly.k;
+  const Coef cf = coef_of(ly);
   const long long r0 = it.begin / L;
   const int nrows = (int)((it.end - it.begin) / L);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -315,7 +341,7 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
     const long long ebase = (r0 + rs) * (long long)L;
     const long long gbase = ly.off + ebase;
     for (int i = threadIdx.x; i < E; i += kThreads) {
-      double c = cand_elem(p, gbase + i, ly);
+      double c = cand_elem<MODE>(p, gbase + i, cf);
       if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
       if (pass == 0) p.zn[gbase + i] = (float)c;
       sq[i] = __dmul_rn(c, c);
@@ -350,6 +376,7 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
       p.partials[ly.poff[pass] + (long long)it.part * G + g] = acc[g];
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int frozen) {
   extern __shared__ float4 ring[];
   const Item it = p.items[blockIdx.x];
@@ -358,27 +385,51 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
     if (p.pass > 0) return;
     if (it.begin & 3) {  // ranges of layers with c_in*kh*kw % 4 != 0: scalar path
       const bool masked = frozen && ly.ncons > 0 && p.fmask != nullptr;
+      const Coef cf = coef_of(ly);
       for (long long e = it.begin + threadIdx.x; e < it.end; e += kThreads) {
-        double c = cand_elem(p, ly.off + e, ly);
+        double c = cand_elem<MODE>(p, ly.off + e, cf);
         if (masked && !((p.fmask[ly.mword + (e >> 5)] >> (e & 31)) & 1u)) c = c * 0.0;
         p.zn[ly.off + e] = (float)c;
       }
       return;
     }
-    cand_elementwise(p, ly, it.begin, it.end, frozen, ring);
+    cand_elementwise<MODE>(p, ly, it.begin, it.end, frozen, ring);
     return;
   }
   if (ly.ncons <= p.pass) return;
   if (ly.tiling == 1)
-    cand_tile_quads(p, ly, it, ring, reinterpret_cast<double*>(ring + kDepth * 4 * kThreads));
+    cand_tile_quads<MODE>(p, ly, it, ring, reinterpret_cast<double*>(ring + kDepth * 4 * kThreads));
   else
-    cand_tile_rows(p, ly, it, reinterpret_cast<double*>(ring), reinterpret_cast<double*>(ring) + p.sqcap);
+    cand_tile_rows<MODE>(p, ly, it, reinterpret_cast<double*>(ring), reinterpret_cast<double*>(ring) + p.sqcap);
+}
+
+template <int MODE>
+static void launch_candidate_mode(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
+  allow_smem(k_candidate<MODE>, smem);
+  k_candidate<MODE><<<n_items, kThreads, smem, st>>>(a, frozen);
 }
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
   if (n_items <= 0) return;
-  allow_smem(k_candidate, smem);
-  k_candidate<<<n_items, kThreads, smem, st>>>(a, frozen);
+  if (a.identity)
+    launch_candidate_mode<kModeIdent>(a, n_items, frozen, smem, st);
+  else if (a.s)
+    launch_candidate_mode<kModeSum>(a, n_items, frozen, smem, st);
+  else
+    launch_candidate_mode<kModeThetaU>(a, n_items, frozen, smem, st);
+}
+
+__global__ void k_div_selftest(const double* __restrict__ num, long long n, double den, double y,
+                               double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = div_rn(num[i], den, y);
+}
+
+void launch_div_selftest(const double* num, long long n, double den, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  k_div_selftest<<<grid, 256, 0, st>>>(num, n, den, 1.0 / den, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -391,6 +442,19 @@ __device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
 }
 
 // shared memory: key[Gp] (double), idx[Gp] (int), fold[blockDim] (double)
+// sum of n values strided by `stride`, 8 independent accumulators (memory-level
+// parallelism), combined in a fixed tree: deterministic for a given n
+__device__ __forceinline__ double fold_parts(const double* __restrict__ p, int n, int stride) {
+  double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int pt = 0;
+  for (; pt + 8 <= n; pt += 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] += p[(long long)(pt + q) * stride];
+  }
+  for (int q = 0; pt + q < n; ++q) a[q] += p[(long long)(pt + q) * stride];
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
 // shared memory: key[Gp] (double), idx[Gp] (int, padded), scratch[max(L, blockDim)] (double)
 __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ layers,
                                                  const int* __restrict__ list, int pass,
@@ -412,16 +476,7 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
     // per-column partials [nparts][L]: fold the row tiles per column (coalesced),
     // then the kh*kw columns of each channel
     const int L = ly.L;
-    for (int col = t; col < L; col += nt) {
-      double a0 = 0.0, a1 = 0.0;
-      int pt = 0;
-      for (; pt + 1 < ly.nparts; pt += 2) {
-        a0 += part[(long long)pt * L + col];
-        a1 += part[(long long)(pt + 1) * L + col];
-      }
-      if (pt < ly.nparts) a0 += part[(long long)pt * L + col];
-      scratch[col] = a0 + a1;
-    }
+    for (int col = t; col < L; col += nt) scratch[col] = fold_parts(part + col, ly.nparts, L);
     __syncthreads();
     for (int g = t; g < Gp; g += nt) {
       double key = -1.0;  // padding sorts after every norm (norms >= 0)
@@ -445,7 +500,7 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
         if (grp == kFilter) {
           s2 = part[g];
         } else {
-          for (int pt = 0; pt < ly.nparts; ++pt) s2 += part[(long long)pt * G + g];
+          s2 = fold_parts(part + g, ly.nparts, G);
         }
         key = sqrt(s2);
         norms[ly.goff[pass] + g] = key;
@@ -780,13 +835,16 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
   int n_in = scan_flags(a.iflag + ly.ikeep, ly.cin, a.pos_in + ly.ikeep);
   __syncthreads();
   const int rowlen = n_in * ly.k;
+  int* s_pin = reinterpret_cast<int*>(sflag);  // the mark flags are no longer needed
+  for (int c = threadIdx.x; c < ly.cin; c += kThreads) s_pin[c] = a.pos_in[ly.ikeep + c];
   for (int o = threadIdx.x; o < ly.rows; o += kThreads) {
     int po = a.pos_out[ly.okeep + o];
     a.maps.rowbase[ly.okeep + o] = po >= 0 ? po * rowlen : -1;
   }
+  __syncthreads();
   for (int col = threadIdx.x; col < ly.L; col += kThreads) {
     unsigned c = fdiv((unsigned)col, ly.divk), jx = (unsigned)col - c * (unsigned)ly.k;
-    int pi = a.pos_in[ly.ikeep + c];
+    int pi = s_pin[c];
     a.maps.colpos[ly.cpoff + col] = pi >= 0 ? pi * ly.k + (int)jx : -1;
   }
   __shared__ bool last_layer;

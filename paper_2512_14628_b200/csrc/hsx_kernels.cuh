@@ -60,6 +60,7 @@ struct DevLayer {
   int G[kMaxPasses];
   FastDiv divL, divk;
   double rho1, rho2, gamma;
+  double rgamma;               // RN(1 / gamma), for the FMA-corrected division
 };
 
 // A contiguous slice [begin, end) of one layer's elements.
@@ -146,6 +147,7 @@ void launch_dual(const float* theta, float* u, const float* zn, long long n, cud
 void launch_nonzero(const float* t, long long n, uint8_t* out, cudaStream_t st);
 void launch_pack(const uint8_t* m, long long n, uint32_t* bits, cudaStream_t st);
 void launch_unpack(const uint32_t* bits, long long n, uint8_t* m, cudaStream_t st);
+void launch_div_selftest(const double* num, long long n, double den, double* out, cudaStream_t st);
 void launch_count_diff(const uint8_t* a, const uint8_t* b, long long n, unsigned long long* c,
                        cudaStream_t st);
 

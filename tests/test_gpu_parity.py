@@ -296,3 +296,26 @@ def test_full_size_compaction_roundtrip_property():
             assert torch.equal(ov, torch.where(rect, xv, torch.zeros_like(xv)))
         else:
             assert torch.equal(ov, xv)
+
+
+def test_candidate_division_is_ieee():
+    """K1 divides by gamma as q = RN(n*y), q' = fma(fma(-q, g, n), y, q) with y = RN(1/g)
+    (Markstein). Check bit-equality with IEEE division for 4M numerators x 12 gammas,
+    including the bench / golden gammas (wd/M + P*rho1 + rho2)."""
+    from paper_2512_14628_b200 import _lib
+    from paper_2512_14628_b200.plan import current_stream
+
+    rng = np.random.default_rng(123)
+    n = 1 << 22
+    num = rng.normal(size=n) * np.exp2(rng.integers(-40, 40, size=n))
+    num[:4096] = rng.integers(-(1 << 52), 1 << 52, size=4096) * 2.0 ** -30   # dense mantissas
+    gammas = [1e-4 / M + P * 1.5e-3 + 1.5e-4 for M in (1, 2, 4) for P in (1, 2, 4)]
+    gammas += [3.2e-3, float(np.nextafter(1.0, 2.0)), 0.3 / 7.0]
+    d_num = torch.tensor(num, dtype=torch.float64, device="cuda")
+    out = torch.empty_like(d_num)
+    for g in gammas:
+        _lib.call("hsx_selftest_division", d_num.data_ptr(), n, float(g), out.data_ptr(), current_stream())
+        got = cpu(out)
+        want = num / g
+        bad = np.flatnonzero(got.view(np.int64) != want.view(np.int64))
+        assert bad.size == 0, (g, num[bad[:5]], got[bad[:5]], want[bad[:5]])

@@ -273,6 +273,9 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     topo = topology_for(n, args.grouping)
     if world > 1:
+        # rank 0 prints exactly one JSON line on stdout: keep NCCL's banner off it
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=dev)
         cluster = H.DistCluster(topo)
     else:

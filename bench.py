@@ -239,7 +239,7 @@ def run_reference(args):
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # -- the B200 arm ------------------------------------------------------------------------
@@ -273,9 +273,6 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     topo = topology_for(n, args.grouping)
     if world > 1:
-        # rank 0 prints exactly one JSON line on stdout: keep NCCL's banner off it
-        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=dev)
         cluster = H.DistCluster(topo)
     else:
@@ -415,12 +412,25 @@ def run_ours(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(layers, topo, args.keep, args.seed, args.cpu_budget_s)
-    print(json.dumps(line), flush=True)
+    emit(line)
     if world > 1:
         dist.destroy_process_group()
 
 
+_OUT_FD = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line, on the real stdout (everything else was moved to stderr)."""
+    os.write(_OUT_FD if _OUT_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _OUT_FD
+    # NCCL / torch banners print on fd 1 from C code; route fd 1 to stderr and keep
+    # the real stdout for the single JSON line
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -12,7 +12,7 @@ import os
 
 from .errors import ConfigError, CudaError, ProtocolError, ShapeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhsx.so")
+LIB_PATH = os.environ.get("HSX_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhsx.so")
 ABI_VERSION = 1
 
 HSX_OK, HSX_ESHAPE, HSX_EPROTOCOL, HSX_ECONFIG, HSX_ECUDA, HSX_EINVAL = range(6)

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -47,10 +48,16 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 constexpr long long kAlign = 32;        // arena layer alignment in elements (128 B)
 constexpr int kSubElems = 4096;         // target elements per shared-memory sub-tile
-constexpr int hsx_tile_rows = 32;       // candidate quad tiles: rows x column quads (hsx_kernels.cu)
-constexpr int hsx_tile_quads = 64;
+constexpr int hsx_tile_quads = 64;      // quad tiles: rows x 64 column quads (hsx_kernels.cu)
+// rows per quad tile (K1; K3/K6/K7); HSX_CAND_TILE_ROWS / HSX_STREAM_TILE_ROWS
+// override them for tuning runs (multiples of 4, <= kMaxTileRows = 128)
+int tile_rows_env(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  int r = v ? std::atoi(v) : dflt;
+  if (r < 4 || r > 128 || (r & 3)) r = dflt;
+  return r;
+}
 constexpr long long kItemElems = 8192;  // elements per streaming work item
-constexpr long long kNormItemElems = 16384;  // minimum elements per group-norm row tile
 constexpr long long kWordItem = 512;    // mask words per keep-mark item
 constexpr int kMaxSelectGroups = 8192;  // bitonic capacity (96 KB smem)
 constexpr size_t kMaxSmem = 200 * 1024;
@@ -139,7 +146,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   p->n_layers = n;
   long long off = 0, mword = 0, okeep = 0, ikeep = 0, cpoff = 0;
   long long goff[hsx::kMaxPasses] = {0, 0, 0}, poff[hsx::kMaxPasses] = {0, 0, 0};
-  int sqcap = 0, gmax = 0, quadcap = 0, lmax = 1024;
+  int sqcap = 0, quadcap = 0, lmax = 1024;
   std::vector<Item> dense_items;
   size_t mark_smem = 0;
   p->summary.assign((size_t)n * HSX_SUM_COLS + 1, 0);
@@ -189,6 +196,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         ly.G[q] = G;
       }
       ly.rsub = std::max(1, kSubElems / ly.L);
+      lmax = std::max(lmax, ly.L);
       // quad tiling when every pass groups columns (CHANNEL / SHAPE) and rows are
       // a multiple of 4 elements; otherwise row tiling (FILTER, stems)
       bool quads = (ly.L & 3) == 0;
@@ -196,7 +204,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       ly.tiling = quads ? 1 : 0;
       ly.pidx = (int)p->prunable.size();
       if (quads) {
-        const int tq = hsx_tile_quads, tr = hsx_tile_rows;
+        const int tq = hsx_tile_quads, tr = tile_rows_env("HSX_CAND_TILE_ROWS", 32);
         const int nchunks = (ly.L / 4 + tq - 1) / tq;
         ly.nparts = (ly.rows + tr - 1) / tr;
         for (int pt = 0; pt < ly.nparts; ++pt)
@@ -205,18 +213,10 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
             p->cand_dyn.push_back(it);
           }
         quadcap = std::max(quadcap, 4 * tq * (256 / tq));
-        lmax = std::max(lmax, ly.L);
       } else {
         sqcap = std::max(sqcap, ly.rsub * ly.L);
-        for (int q = 0; q < ly.ncons; ++q)
-          if (ly.group[q] != HSX_GROUP_FILTER) gmax = std::max(gmax, ly.G[q]);
-        int gch = 0;
-        for (int q = 0; q < ly.ncons; ++q)
-          if (ly.group[q] != HSX_GROUP_FILTER) gch = std::max(gch, ly.G[q]);
-        // rows per tile: >= 16K elements and partials <= ~1/16 of the tile's bytes
-        long long rows_item = std::max<long long>((kNormItemElems + ly.L - 1) / ly.L, (16LL * gch + ly.L - 1) / ly.L);
-        rows_item = (rows_item + ly.rsub - 1) / ly.rsub * ly.rsub;
-        rows_item = std::min<long long>(rows_item, ly.rows);
+        // one shared-memory sub-tile of rows per item
+        const long long rows_item = std::min<long long>(ly.rsub, ly.rows);
         ly.nparts = (int)((ly.rows + rows_item - 1) / rows_item);
         for (int pt = 0; pt < ly.nparts; ++pt) {
           Item it{l, pt, 0, 0, pt * rows_item * ly.L, std::min<long long>((pt + 1) * rows_item, ly.rows) * ly.L};
@@ -227,8 +227,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         ly.goff[q] = goff[q];
         goff[q] += ly.G[q];
         ly.poff[q] = poff[q];
-        poff[q] += quads ? (long long)ly.nparts * ly.L
-                         : (ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * ly.G[q]);
+        poff[q] += ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * ly.L;
         p->pass_list[q].push_back(l);
         p->max_passes = std::max(p->max_passes, q + 1);
       }
@@ -244,7 +243,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       ly.qtile = (ly.L % 32) == 0 ? 1 : 0;
       if (ly.qtile) {
         // row-quad tiles for K3 / K6 / K7 (same shape as the K1 quad tiles)
-        const int tq = hsx_tile_quads, tr = hsx_tile_rows;
+        const int tq = hsx_tile_quads, tr = tile_rows_env("HSX_STREAM_TILE_ROWS", 32);
         const int nchunks = (ly.L / 4 + tq - 1) / tq;
         for (int r0 = 0; r0 < ly.rows; r0 += tr)
           for (int cc = 0; cc < nchunks; ++cc) {
@@ -306,7 +305,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   p->sqcap = sqcap;
   // k_candidate: cp.async ring (kDepth x 4 x 256 float4 = 64 KB) + 8 KB quad fold,
   // or the row-tile path's sub-tile squares + group accumulators
-  p->cand_smem = std::max((size_t)(sqcap + gmax) * sizeof(double),
+  p->cand_smem = std::max((size_t)sqcap * sizeof(double),
                           (size_t)4 * 4 * 256 * 16 + (size_t)quadcap * sizeof(double));
   p->mark_smem = mark_smem;
   if (p->cand_smem > kMaxSmem) return fail(HSX_ESHAPE, "candidate tile needs %zu B of shared memory", p->cand_smem);

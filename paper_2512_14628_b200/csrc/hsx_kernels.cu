@@ -154,6 +154,10 @@ struct In4 {
 template <int MODE>
 __device__ __forceinline__ double cand4(const In4& x, int i, const Coef& cf) {
   if (MODE == kModeIdent) return (double)f4get(x.a, i);
+#ifdef HSX_EXPERIMENT_FP32CAND  // tuning experiment only: fp32 candidate, no fp64 chain
+  return (double)((float)cf.rho1 * (f4get(x.a, i) + f4get(x.b, i)) +
+                  (float)cf.rho2 * (f4get(x.z, i) - f4get(x.v, i)));
+#endif
   double s = MODE == kModeSum ? (double)f4get(x.a, i)
                               : __dadd_rn((double)f4get(x.a, i), (double)f4get(x.b, i));
   return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), cf);
@@ -319,61 +323,44 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
 }
 
 // K1b row tiles (FILTER groups, composite plans mixing FILTER, rows not a
-// multiple of 4 elements): squares of sub-tiles of rows staged in shared
-// memory; partials per group ([part][G]) or per row (FILTER).
+// multiple of 4 elements — e.g. the 7x7 stem): one shared-memory sub-tile of
+// rows per item; squares staged in shared memory, then reduced by one thread
+// per column (CHANNEL / SHAPE: per-column partials [part][L], folded into
+// channels by K2) or one warp per row (FILTER: per-row sums).
 template <int MODE>
-__device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq,
-                               double* acc) {
+__device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq) {
   const int pass = p.pass;
   const int grp = ly.group[pass];
-  const int G = ly.G[pass];
   const int L = ly.L;
-  const int k = ly.k;
   const Coef cf = coef_of(ly);
   const long long r0 = it.begin / L;
-  const int nrows = (int)((it.end - it.begin) / L);
+  const int nr = (int)((it.end - it.begin) / L);
+  const int E = nr * L;
+  const long long ebase = r0 * (long long)L;
+  const long long gbase = ly.off + ebase;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (grp != kFilter)
-    for (int g = threadIdx.x; g < G; g += kThreads) acc[g] = 0.0;
-  for (int rs = 0; rs < nrows; rs += ly.rsub) {
-    const int nr = min(ly.rsub, nrows - rs);
-    const int E = nr * L;
-    const long long ebase = (r0 + rs) * (long long)L;
-    const long long gbase = ly.off + ebase;
-    for (int i = threadIdx.x; i < E; i += kThreads) {
-      double c = cand_elem<MODE>(p, gbase + i, cf);
-      if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
-      if (pass == 0) p.zn[gbase + i] = (float)c;
-      sq[i] = __dmul_rn(c, c);
-    }
-    __syncthreads();
-    if (grp == kChannel) {
-      for (int c = threadIdx.x; c < ly.cin; c += kThreads) {
-        double s = 0.0;
-        for (int r = 0; r < nr; ++r)
-          for (int jx = 0; jx < k; ++jx) s += sq[r * L + c * k + jx];
-        acc[c] += s;
-      }
-    } else if (grp == kShape) {
-      for (int col = threadIdx.x; col < L; col += kThreads) {
-        double s = 0.0;
-        for (int r = 0; r < nr; ++r) s += sq[r * L + col];
-        acc[col] += s;
-      }
-    } else {
-      for (int r = warp; r < nr; r += kThreads / 32) {
-        double s = 0.0;
-        for (int i = lane; i < L; i += 32) s += sq[r * L + i];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
-        if (lane == 0) p.partials[ly.poff[pass] + r0 + rs + r] = s;
-      }
-    }
-    __syncthreads();
+  for (int i = threadIdx.x; i < E; i += kThreads) {
+    double c = cand_elem<MODE>(p, gbase + i, cf);
+    if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
+    if (pass == 0) p.zn[gbase + i] = (float)c;
+    sq[i] = __dmul_rn(c, c);
   }
-  if (grp != kFilter)
-    for (int g = threadIdx.x; g < G; g += kThreads)
-      p.partials[ly.poff[pass] + (long long)it.part * G + g] = acc[g];
+  __syncthreads();
+  if (grp == kFilter) {
+    for (int r = warp; r < nr; r += kThreads / 32) {
+      double s = 0.0;
+      for (int i = lane; i < L; i += 32) s += sq[r * L + i];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+      if (lane == 0) p.partials[ly.poff[pass] + r0 + r] = s;
+    }
+  } else {
+    for (int col = threadIdx.x; col < L; col += kThreads) {
+      double s = 0.0;
+      for (int r = 0; r < nr; ++r) s += sq[r * L + col];
+      p.partials[ly.poff[pass] + (long long)it.part * L + col] = s;
+    }
+  }
 }
 
 template <int MODE>
@@ -400,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
   if (ly.tiling == 1)
     cand_tile_quads<MODE>(p, ly, it, ring, reinterpret_cast<double*>(ring + kDepth * 4 * kThreads));
   else
-    cand_tile_rows<MODE>(p, ly, it, reinterpret_cast<double*>(ring), reinterpret_cast<double*>(ring) + p.sqcap);
+    cand_tile_rows<MODE>(p, ly, it, reinterpret_cast<double*>(ring));
 }
 
 template <int MODE>
@@ -472,7 +459,7 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
   const int nt = blockDim.x;
   const int t = threadIdx.x;
   // 1) squared group norms from the K1 partials, fixed summation order
-  if (ly.tiling == 1) {
+  if (grp != kFilter) {
     // per-column partials [nparts][L]: fold the row tiles per column (coalesced),
     // then the kh*kw columns of each channel
     const int L = ly.L;
@@ -496,12 +483,7 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
     for (int g = t; g < Gp; g += nt) {
       double key = -1.0;
       if (g < G) {
-        double s2 = 0.0;
-        if (grp == kFilter) {
-          s2 = part[g];
-        } else {
-          s2 = fold_parts(part + g, ly.nparts, G);
-        }
+        const double s2 = part[g];  // FILTER: complete per-row sums
         key = sqrt(s2);
         norms[ly.goff[pass] + g] = key;
       }
@@ -586,7 +568,7 @@ struct LayerRegs {
 // chunk*64 + (t & 63) and walks rows begin + (t >> 6) + 4i. Column maps are
 // loop-invariant registers; row maps of the tile sit in shared memory.
 constexpr int kRowPhases = kThreads / kTileQuads;  // 4
-constexpr int kMaxTileRows = 32;
+constexpr int kMaxTileRows = 128;
 
 struct TileCtx {
   int j, jj, ph;

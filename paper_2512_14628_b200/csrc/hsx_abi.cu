@@ -204,7 +204,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       ly.tiling = quads ? 1 : 0;
       ly.pidx = (int)p->prunable.size();
       if (quads) {
-        const int tq = hsx_tile_quads, tr = tile_rows_env("HSX_CAND_TILE_ROWS", 32);
+        const int tq = hsx_tile_quads, tr = tile_rows_env("HSX_CAND_TILE_ROWS", 128);
         const int nchunks = (ly.L / 4 + tq - 1) / tq;
         ly.nparts = (ly.rows + tr - 1) / tr;
         for (int pt = 0; pt < ly.nparts; ++pt)

@@ -492,7 +492,27 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
     }
   }
   __syncthreads();
-  // 2) bitonic sort: norm descending, index ascending (stable argsort of -norms)
+  uint8_t* fl = flags.f[pass];
+  const int keep = ly.keep[pass];
+  if (Gp <= nt) {
+    // 2a) rank counting: rank(g) = #{j : n_j > n_g} + #{j < g : n_j == n_g} (the
+    //     stable argsort of -norms); T = nt / Gp consecutive lanes share a group
+    //     and fold their counts with shuffles. One barrier instead of a sort.
+    const int T = nt / Gp;  // power of two <= 32 when Gp >= 32
+    const int Tw = T > 32 ? 32 : T;
+    const int g = t / Tw, sl = t % Tw;
+    if (g < Gp) {
+      const double kg = skey[g];
+      int rank = 0;
+      for (int jx = sl; jx < G; jx += Tw) {
+        const double kj = skey[jx];
+        rank += (kj > kg) || (kj == kg && jx < g);
+      }
+      for (int off = Tw >> 1; off > 0; off >>= 1) rank += __shfl_xor_sync(kFull, rank, off, Tw);
+      if (sl == 0 && g < G) fl[ly.goff[pass] + g] = rank < keep ? 1 : 0;
+    }
+  } else {
+  // 2b) bitonic sort: norm descending, index ascending (stable argsort of -norms)
   for (int size = 2; size <= Gp; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = t; i < Gp; i += nt) {
@@ -511,11 +531,10 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
       __syncthreads();
     }
   }
-  uint8_t* fl = flags.f[pass];
-  const int keep = ly.keep[pass];
   for (int pos = t; pos < Gp; pos += nt) {
     int g = sidx[pos];
     if (g < G) fl[ly.goff[pass] + g] = pos < keep ? 1 : 0;
+  }
   }
   if (pass != ly.ncons - 1) return;
   __syncthreads();
@@ -805,11 +824,14 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
     if (s_in[i]) a.iflag[ly.ikeep + i] = 1;
   for (int i = threadIdx.x; i < nr; i += kThreads)
     if (s_out[i]) a.oflag[ly.okeep + r_lo + i] = 1;
-  // b) the layer's last CTA derives its keep sets
+  // b) the layer's last CTA derives its keep sets. One gpu-scope fence by thread 0
+  //    after the barrier releases every thread's flag writes (cumulative release).
   __shared__ bool last;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(a.layer_done + ly.pidx, 1u) == (unsigned)it.chunk - 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.layer_done + ly.pidx, 1u) == (unsigned)it.chunk - 1;
+  }
   __syncthreads();
   if (!last) return;
   __threadfence();

@@ -264,7 +264,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         p->word_items.push_back(it);
         long long r_lo = b / ly.L, r_hi = (it.end - 1) / ly.L;
         mark_smem = std::max<size_t>(mark_smem, std::max<size_t>((size_t)ly.cin + (size_t)(r_hi - r_lo + 1),
-                                                                  4 * (size_t)ly.cin));
+                                                                  4 * ((size_t)ly.cin + ly.rows)));
       }
     } else {
       for (long long b = 0; b < ly.n; b += kItemElems) {

@@ -429,17 +429,20 @@ __device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
 }
 
 // shared memory: key[Gp] (double), idx[Gp] (int), fold[blockDim] (double)
-// sum of n values strided by `stride`, 8 independent accumulators (memory-level
-// parallelism), combined in a fixed tree: deterministic for a given n
+// sum of n values strided by `stride`: four independent accumulators (loads in
+// flight together), combined in a fixed tree — deterministic for a given n
 __device__ __forceinline__ double fold_parts(const double* __restrict__ p, int n, int stride) {
-  double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int pt = 0;
-  for (; pt + 8 <= n; pt += 8) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] += p[(long long)(pt + q) * stride];
+  for (; pt + 4 <= n; pt += 4) {
+    const double x0 = p[(long long)pt * stride], x1 = p[(long long)(pt + 1) * stride];
+    const double x2 = p[(long long)(pt + 2) * stride], x3 = p[(long long)(pt + 3) * stride];
+    a0 += x0; a1 += x1; a2 += x2; a3 += x3;
   }
-  for (int q = 0; pt + q < n; ++q) a[q] += p[(long long)(pt + q) * stride];
-  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  if (pt < n) a0 += p[(long long)pt * stride];
+  if (pt + 1 < n) a1 += p[(long long)(pt + 1) * stride];
+  if (pt + 2 < n) a2 += p[(long long)(pt + 2) * stride];
+  return (a0 + a1) + (a2 + a3);
 }
 
 // shared memory: key[Gp] (double), idx[Gp] (int, padded), scratch[max(L, blockDim)] (double)
@@ -509,7 +512,11 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
         rank += (kj > kg) || (kj == kg && jx < g);
       }
       for (int off = Tw >> 1; off > 0; off >>= 1) rank += __shfl_xor_sync(kFull, rank, off, Tw);
-      if (sl == 0 && g < G) fl[ly.goff[pass] + g] = rank < keep ? 1 : 0;
+      if (sl == 0 && g < G) {
+        const uint8_t f = rank < keep ? 1 : 0;
+        fl[ly.goff[pass] + g] = f;
+        sidx[g] = f;  // this pass's flags for the keep maps below
+      }
     }
   } else {
   // 2b) bitonic sort: norm descending, index ascending (stable argsort of -norms)
@@ -535,22 +542,32 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
     int g = sidx[pos];
     if (g < G) fl[ly.goff[pass] + g] = pos < keep ? 1 : 0;
   }
+  __syncthreads();
+  for (int pos = t; pos < Gp; pos += nt) {  // re-index: sidx[g] = flag of group g
+    int g = sidx[pos];
+    if (g < G) skey[g] = pos < keep ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int g = t; g < G; g += nt) sidx[g] = skey[g] != 0.0;
   }
   if (pass != ly.ncons - 1) return;
   __syncthreads();
   // 3) keep maps for K3: rowkeep = AND of FILTER passes, colkeep = AND of
   //    CHANNEL / SHAPE passes (block-local global writes are visible after the barrier)
+  // this pass's flags come from shared memory (sidx[g]), earlier passes' from global
+  const int npass = ly.ncons;
   for (int o = t; o < ly.rows; o += nt) {
     uint8_t kp = 1;
-    for (int q = 0; q < ly.ncons; ++q)
-      if (ly.group[q] == kFilter) kp &= flags.f[q][ly.goff[q] + o];
+    for (int q = 0; q < npass; ++q)
+      if (ly.group[q] == kFilter) kp &= q == pass ? (uint8_t)sidx[o] : flags.f[q][ly.goff[q] + o];
     m.rowkeep[ly.okeep + o] = kp;
   }
   for (int col = t; col < ly.L; col += nt) {
     uint8_t kp = 1;
-    for (int q = 0; q < ly.ncons; ++q) {
-      if (ly.group[q] == kChannel) kp &= flags.f[q][ly.goff[q] + col / ly.k];
-      else if (ly.group[q] == kShape) kp &= flags.f[q][ly.goff[q] + col];
+    for (int q = 0; q < npass; ++q) {
+      if (ly.group[q] == kFilter) continue;
+      const int g = ly.group[q] == kChannel ? col / ly.k : col;
+      kp &= q == pass ? (uint8_t)sidx[g] : flags.f[q][ly.goff[q] + g];
     }
     m.colkeep[ly.cpoff + col] = kp;
   }
@@ -757,17 +774,43 @@ __device__ int block_exclusive_scan(int x, int* warp_tot, int* total) {
   return r;
 }
 
-// exclusive positions of set flags (-1 for clear ones); flags read through L2
-// (written by other CTAs of this launch)
-__device__ int scan_flags(const uint8_t* flags, int n, int* pos) {
+// exclusive positions of set flags (-1 for clear ones) into global `pos` and
+// shared `spos`; flags are read through L2 (written by other CTAs of this
+// launch), all of a thread's flags loaded before the scans
+__device__ int scan_flags(const uint8_t* flags, int n, int* pos, int* spos) {
   __shared__ int warp_tot[32];
   __shared__ int total;
+  constexpr int kMaxRounds = 8;  // n <= 8 * blockDim (2048 with 256 threads)
+  int f[kMaxRounds];
+#pragma unroll
+  for (int r = 0; r < kMaxRounds; ++r) {
+    const int i = r * (int)blockDim.x + threadIdx.x;
+    f[r] = (i < n && __ldcg(flags + i)) ? 1 : 0;
+  }
   int carry = 0;
-  for (int base = 0; base < n; base += blockDim.x) {
-    int i = base + threadIdx.x;
-    int f = (i < n && __ldcg(flags + i)) ? 1 : 0;
-    int ex = block_exclusive_scan(f, warp_tot, &total);
-    if (i < n) pos[i] = f ? carry + ex : -1;
+#pragma unroll
+  for (int r = 0; r < kMaxRounds; ++r) {  // static indices keep f[] in registers
+    const int base = r * (int)blockDim.x;
+    if (base >= n) break;
+    const int i = base + threadIdx.x;
+    const int ex = block_exclusive_scan(f[r], warp_tot, &total);
+    const int p = f[r] ? carry + ex : -1;
+    if (i < n) {
+      pos[i] = p;
+      spos[i] = p;
+    }
+    carry += total;
+    __syncthreads();
+  }
+  for (int base = kMaxRounds * (int)blockDim.x; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int fr = (i < n && __ldcg(flags + i)) ? 1 : 0;
+    const int ex = block_exclusive_scan(fr, warp_tot, &total);
+    const int p = fr ? carry + ex : -1;
+    if (i < n) {
+      pos[i] = p;
+      spos[i] = p;
+    }
     carry += total;
     __syncthreads();
   }
@@ -835,17 +878,16 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  int n_out = scan_flags(a.oflag + ly.okeep, ly.rows, a.pos_out + ly.okeep);
-  int n_in = scan_flags(a.iflag + ly.ikeep, ly.cin, a.pos_in + ly.ikeep);
-  __syncthreads();
+  // the mark flags in shared memory are no longer needed: reuse for positions
+  int* s_pin = reinterpret_cast<int*>(sflag);
+  int* s_pout = s_pin + ly.cin;
+  int n_in = scan_flags(a.iflag + ly.ikeep, ly.cin, a.pos_in + ly.ikeep, s_pin);
+  int n_out = scan_flags(a.oflag + ly.okeep, ly.rows, a.pos_out + ly.okeep, s_pout);
   const int rowlen = n_in * ly.k;
-  int* s_pin = reinterpret_cast<int*>(sflag);  // the mark flags are no longer needed
-  for (int c = threadIdx.x; c < ly.cin; c += kThreads) s_pin[c] = a.pos_in[ly.ikeep + c];
   for (int o = threadIdx.x; o < ly.rows; o += kThreads) {
-    int po = a.pos_out[ly.okeep + o];
+    int po = s_pout[o];
     a.maps.rowbase[ly.okeep + o] = po >= 0 ? po * rowlen : -1;
   }
-  __syncthreads();
   for (int col = threadIdx.x; col < ly.L; col += kThreads) {
     unsigned c = fdiv((unsigned)col, ly.divk), jx = (unsigned)col - c * (unsigned)ly.k;
     int pi = s_pin[c];

@@ -190,17 +190,22 @@ class HSADMMSync:
             pl.compact_dual(self.theta, self.u, self.z_node, self.v, self.flat)
         else:
             pl.dual_intra(self.theta, self.u, self.z_node)
-        if ev is not None:
+        collectives = self.M > 1 or self.P > 1
+        if ev is not None and collectives:      # the leader all-reduce / broadcast need the sizes
             ev.synchronize()
             self._after_keep_sets()
+            ev = None
         total = self.payload_elements
-        if self.is_leader:
-            for bi, b in enumerate(self.buckets):
-                yield AllReduce(self.inter, self.flat[b.start:b.start + b.elements], ReduceOp.AVG,
-                                f"z_sync/b{bi}", k, detail=b.detail)
+        if self.is_leader and collectives:
+            yield from self._leader_average(k)
         if self.P > 1 and total > 0:
             yield Broadcast(self.intra, self.leader_rank, self.flat[:total], "zhat_bcast", k)
         pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
+        if ev is not None:                       # single GPU: K6 / K7 are already queued
+            ev.synchronize()
+            self._after_keep_sets()
+        if self.is_leader and not collectives:   # M == 1: the average is the identity (ledger only)
+            yield from self._leader_average(k)
         if dynamic:
             self.masks, self.union = self.union, self.masks
         # freeze + seal (consensus.py:600-606)
@@ -210,6 +215,12 @@ class HSADMMSync:
             if self.is_leader:
                 self.cache_hits += len(self.prunable)   # cache.get on the final masks, then seal
         return None
+
+    def _leader_average(self, k: int):
+        """C3: leader all-reduce AVG of the flat buffer, one request per <= 32 MiB bucket."""
+        for bi, b in enumerate(self.buckets):
+            yield AllReduce(self.inter, self.flat[b.start:b.start + b.elements], ReduceOp.AVG,
+                            f"z_sync/b{bi}", k, detail=b.detail)
 
     def step(self, k: int):
         """Run iteration k through a DistCluster (one rank per process)."""

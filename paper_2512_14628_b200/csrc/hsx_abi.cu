@@ -559,8 +559,7 @@ int hsx_keep_sets(hsx_plan* p, const uint32_t* union_mask, const uint32_t* prev_
   if (!p || (!union_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
   if (p->prunable.empty()) return HSX_OK;
   cudaStream_t st = S(stream);
-  if (p->ktotal[0]) HSX_CUDA(cudaMemsetAsync(p->d_oflag, 0, p->ktotal[0], st));
-  if (p->ktotal[1]) HSX_CUDA(cudaMemsetAsync(p->d_iflag, 0, p->ktotal[1], st));
+  // K_out / K_in flags are zero here: zero at allocation, re-zeroed by K5's scans
   // zero the drift / popcount columns of every row
   HSX_CUDA(cudaMemset2DAsync(p->d_summary + HSX_SUM_DRIFT, HSX_SUM_COLS * sizeof(long long), 0,
                              2 * sizeof(long long), p->n_layers, st));

@@ -883,6 +883,9 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
   int* s_pout = s_pin + ly.cin;
   int n_in = scan_flags(a.iflag + ly.ikeep, ly.cin, a.pos_in + ly.ikeep, s_pin);
   int n_out = scan_flags(a.oflag + ly.okeep, ly.rows, a.pos_out + ly.okeep, s_pout);
+  // leave the any-flags zeroed for the next derivation (no memset launches)
+  for (int i = threadIdx.x; i < ly.cin; i += kThreads) a.iflag[ly.ikeep + i] = 0;
+  for (int i = threadIdx.x; i < ly.rows; i += kThreads) a.oflag[ly.okeep + i] = 0;
   const int rowlen = n_in * ly.k;
   for (int o = threadIdx.x; o < ly.rows; o += kThreads) {
     int po = s_pout[o];

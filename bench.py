@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--model", default="rn18_224")
     ap.add_argument("--grouping", default=None)
     ap.add_argument("--keep", type=float, default=0.4)
+    ap.add_argument("--transport", choices=["auto", "peer", "nccl"], default="auto")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
@@ -283,7 +284,8 @@ def run_ours(args):
     names = [ls.name for ls in layers]
     sched = H.PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False)
     settings = H.ConsensusSettings(t_freeze=10**9, drift_window=0, weight_decay=1e-4)
-    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, device=dev)
+    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, device=dev, transport=args.transport)
+    config["transport"] = eng.transport
     base = synthetic_base(layers, args.seed)
     st = synthetic_rank_state(layers, rank, topo.accels_per_node, args.seed, base)
     eng.load(**st)

@@ -186,6 +186,27 @@ int hsx_dual_intra(const hsx_plan* plan, const float* theta, float* u, const flo
 int hsx_decompact_dual(const hsx_plan* plan, const float* flat, float divisor,
                        const float* z_node, float* v, float* z, void* stream);
 
+/* ---- fused peer-memory collectives (one process per GPU, NVLink) ---------------
+ * Pointer arrays are HOST arrays of DEVICE pointers to the same buffer on every
+ * rank of a group, in member (rank) order, mapped into this process (e.g. torch
+ * symmetric memory); n <= 4. The caller orders them after the peers' producers
+ * with a group barrier. */
+/* K1 with the intra all-reduce fused: S = sum_j sends[j] (fp64, rank order, the
+ * reference's serial fold transport.py:453-462) read over NVLink. */
+int hsx_candidate_peers(hsx_plan* plan, const float* const* sends, int32_t n, const float* z,
+                        const float* v, float* z_node, const uint32_t* frozen_mask, void* stream);
+/* Composite pass >= 1 of the peer candidate (same sources as hsx_candidate_peers). */
+int hsx_candidate_renorm_peers(hsx_plan* plan, int32_t pass, const float* const* sends, int32_t n,
+                               const float* z, const float* v, void* stream);
+/* K4 over mapped pointers: out = OR_j srcs[j] (leaders' local masks, transport.py:455-457). */
+int hsx_mask_or_ptrs(const uint32_t* const* srcs, int32_t n, int64_t words, uint32_t* out,
+                     void* stream);
+/* K7 with the leader average fused: z = (sum_j flats[j][payload]) / divisor, zero
+ * fill, v += z_node - z; zhat (may be NULL) receives the average in payload
+ * layout for the node's followers (the intra broadcast becomes their read). */
+int hsx_decompact_peers(const hsx_plan* plan, const float* const* flats, int32_t n, float divisor,
+                        float* zhat, const float* z_node, float* v, float* z, void* stream);
+
 /* ---- mask helpers for the per-tensor API -------------------------------------- */
 /* out[i] = |t[i]| > 0  (extract_mask, sparsity.py:113-115) */
 int hsx_nonzero_u8(const float* t, int64_t n, uint8_t* out, void* stream);

@@ -68,6 +68,10 @@ SIGNATURES = {
     "hsx_unpack_bits": (C.c_int, [VP, I64, VP, VP]),
     "hsx_count_diff_u8": (C.c_int, [VP, VP, I64, VP, VP]),
     "hsx_selftest_division": (C.c_int, [VP, I64, F64, VP, VP]),
+    "hsx_candidate_peers": (C.c_int, [P, VP, I32, VP, VP, VP, VP, VP]),
+    "hsx_mask_or_ptrs": (C.c_int, [VP, I32, I64, VP, VP]),
+    "hsx_candidate_renorm_peers": (C.c_int, [P, I32, VP, I32, VP, VP, VP]),
+    "hsx_decompact_peers": (C.c_int, [P, VP, I32, F32, VP, VP, VP, VP, VP]),
 }
 
 _lib = None
@@ -101,6 +105,12 @@ def check(rc: int, what: str = "") -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def ptr_array(ptrs):
+    """Host array of device pointers (for the *_peers / *_ptrs entry points)."""
+    arr = (C.c_void_p * max(len(ptrs), 1))(*[int(p) for p in ptrs])
+    return C.cast(arr, C.c_void_p), arr
 
 
 def launch_count() -> int:

@@ -500,6 +500,49 @@ int hsx_candidate(hsx_plan* p, const float* sum, const float* theta, const float
   return HSX_OK;
 }
 
+int hsx_candidate_peers(hsx_plan* p, const float* const* sends, int32_t n, const float* z,
+                        const float* v, float* z_node, const uint32_t* frozen_mask, void* stream) {
+  if (!p || !z_node || !sends || !z || !v) return fail(HSX_EINVAL, "null argument");
+  if (n < 1 || n > hsx::kMaxPeers) return fail(HSX_EINVAL, "peer count %d outside [1, %d]", n, hsx::kMaxPeers);
+  if (p->identity) return fail(HSX_EINVAL, "peer candidate needs a penalty plan");
+  hsx::CandArgs a = cand_args(p, nullptr, nullptr, nullptr, z, v);
+  a.peers.n = n;
+  for (int j = 0; j < n; ++j) {
+    if (!sends[j]) return fail(HSX_EINVAL, "null peer pointer %d", j);
+    a.peers.p[j] = sends[j];
+  }
+  a.zn = z_node;
+  a.fmask = frozen_mask;
+  a.pass = 0;
+  a.partials = p->d_partials[0];
+  if (frozen_mask) {
+    a.items = p->d_elem;
+    hsx::launch_candidate(a, (int)p->elem_items.size(), 1, p->cand_smem, S(stream));
+  } else {
+    a.items = p->d_cand;
+    hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
+  }
+  HSX_LAUNCHED("candidate_peers");
+  return HSX_OK;
+}
+
+int hsx_candidate_renorm_peers(hsx_plan* p, int32_t pass, const float* const* sends, int32_t n,
+                               const float* z, const float* v, void* stream) {
+  if (!p || !sends || !z || !v) return fail(HSX_EINVAL, "null argument");
+  if (pass < 1 || pass >= p->max_passes) return fail(HSX_EINVAL, "renorm pass %d out of range", pass);
+  if (n < 1 || n > hsx::kMaxPeers) return fail(HSX_EINVAL, "peer count %d outside [1, %d]", n, hsx::kMaxPeers);
+  hsx::CandArgs a = cand_args(p, nullptr, nullptr, nullptr, z, v);
+  a.peers.n = n;
+  for (int j = 0; j < n; ++j) a.peers.p[j] = sends[j];
+  a.pass = pass;
+  a.partials = p->d_partials[pass];
+  for (int q = 0; q < pass; ++q) a.flags[q] = p->d_flags[q];
+  a.items = p->d_cand;
+  hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
+  HSX_LAUNCHED("candidate_renorm_peers");
+  return HSX_OK;
+}
+
 int hsx_candidate_renorm(hsx_plan* p, int32_t pass, const float* sum, const float* theta,
                          const float* u, const float* z, const float* v, void* stream) {
   if (!p) return fail(HSX_EINVAL, "null plan");
@@ -548,9 +591,26 @@ int hsx_project(hsx_plan* p, float* z_node, uint32_t* local_mask, void* stream) 
 
 int hsx_mask_or(const uint32_t* gathered, int32_t n_ranks, int64_t words, uint32_t* out,
                 void* stream) {
-  if (!gathered || !out || n_ranks < 1 || words < 0) return fail(HSX_EINVAL, "bad argument");
-  hsx::launch_mask_or(gathered, n_ranks, words, out, S(stream));
+  if (!gathered || !out || n_ranks < 1 || n_ranks > 8 || words < 0) return fail(HSX_EINVAL, "bad argument");
+  hsx::MaskPtrs g;
+  g.n = n_ranks;
+  for (int r = 0; r < n_ranks; ++r) g.p[r] = gathered + (size_t)r * words;
+  hsx::launch_mask_or(g, words, out, S(stream));
   HSX_LAUNCHED("mask_or");
+  return HSX_OK;
+}
+
+int hsx_mask_or_ptrs(const uint32_t* const* srcs, int32_t n, int64_t words, uint32_t* out,
+                     void* stream) {
+  if (!srcs || !out || n < 1 || n > 8 || words < 0) return fail(HSX_EINVAL, "bad argument");
+  hsx::MaskPtrs g;
+  g.n = n;
+  for (int r = 0; r < n; ++r) {
+    if (!srcs[r]) return fail(HSX_EINVAL, "null mask pointer %d", r);
+    g.p[r] = srcs[r];
+  }
+  hsx::launch_mask_or(g, words, out, S(stream));
+  HSX_LAUNCHED("mask_or_ptrs");
   return HSX_OK;
 }
 
@@ -694,6 +754,28 @@ int hsx_decompact_dual(const hsx_plan* p, const float* flat, float divisor, cons
   a.z = z;
   hsx::launch_decompact(a, (int)p->stream_items.size(), S(stream));
   HSX_LAUNCHED("decompact_dual");
+  return HSX_OK;
+}
+
+int hsx_decompact_peers(const hsx_plan* p, const float* const* flats, int32_t n, float divisor,
+                        float* zhat, const float* z_node, float* v, float* z, void* stream) {
+  if (!p || !flats || !z) return fail(HSX_EINVAL, "null argument");
+  if (n < 1 || n > hsx::kMaxPeers) return fail(HSX_EINVAL, "peer count %d outside [1, %d]", n, hsx::kMaxPeers);
+  if (v && !z_node) return fail(HSX_EINVAL, "v update needs z_node");
+  if (!(divisor > 0.0f)) return fail(HSX_EINVAL, "divisor must be positive");
+  hsx::ElemArgs a = elem_args(p);
+  a.flats.n = n;
+  for (int j = 0; j < n; ++j) {
+    if (!flats[j]) return fail(HSX_EINVAL, "null peer pointer %d", j);
+    a.flats.p[j] = flats[j];
+  }
+  a.zhat = zhat;
+  a.divisor = divisor;
+  a.zn = z_node;
+  a.v = v;
+  a.z = z;
+  hsx::launch_decompact(a, (int)p->stream_items.size(), S(stream));
+  HSX_LAUNCHED("decompact_peers");
   return HSX_OK;
 }
 

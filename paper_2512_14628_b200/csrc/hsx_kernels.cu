@@ -142,31 +142,122 @@ __device__ __forceinline__ double cand_of(double s, double z, double v, const Co
   return div_rn(num, cf.gamma, cf.rgamma);
 }
 
-// input modes of K1 (template parameter): the sum S is given (P > 1) or is
-// theta + u (P == 1, intra all-reduce is the identity); IDENT: candidate = S
-// (per-tensor projection API)
-enum { kModeThetaU = 0, kModeSum = 1, kModeIdent = 2 };
+// input modes of K1 (template parameter): the sum S is given (P > 1 through
+// NCCL), is theta + u (P == 1: the intra all-reduce is the identity), is read
+// from the P ranks' theta + u buffers over NVLink (kModePeers: the intra
+// all-reduce fused into K1, folded in rank order like the reference's serial
+// fold), or the candidate is S itself (kModeIdent: per-tensor projection API)
+enum { kModeThetaU = 0, kModeSum = 1, kModeIdent = 2, kModePeers = 3 };
 
-struct In4 {
-  float4 a, b, z, v;
+template <int MODE>
+struct K1 {
+  static constexpr int NB = MODE == kModePeers ? kMaxPeers + 2 : 4;  // ring slots per stage
+  static constexpr int ZS = MODE == kModePeers ? kMaxPeers : 2;      // slot of z (v follows)
+};
+
+// source pointers of one layer (offset already applied)
+struct K1Src {
+  const float* a;
+  const float* b;
+  const float* z;
+  const float* v;
+  const float* peer[kMaxPeers];
+  int np;
 };
 
 template <int MODE>
-__device__ __forceinline__ double cand4(const In4& x, int i, const Coef& cf) {
-  if (MODE == kModeIdent) return (double)f4get(x.a, i);
-#ifdef HSX_EXPERIMENT_FP32CAND  // tuning experiment only: fp32 candidate, no fp64 chain
-  return (double)((float)cf.rho1 * (f4get(x.a, i) + f4get(x.b, i)) +
-                  (float)cf.rho2 * (f4get(x.z, i) - f4get(x.v, i)));
-#endif
-  double s = MODE == kModeSum ? (double)f4get(x.a, i)
-                              : __dadd_rn((double)f4get(x.a, i), (double)f4get(x.b, i));
-  return cand_of(s, (double)f4get(x.z, i), (double)f4get(x.v, i), cf);
+__device__ __forceinline__ K1Src k1_src(const CandArgs& p, long long base) {
+  K1Src s;
+  s.a = s.b = nullptr;
+  s.np = 0;
+  if (MODE == kModePeers) {
+    s.np = p.peers.n;
+#pragma unroll
+    for (int j = 0; j < kMaxPeers; ++j) s.peer[j] = j < s.np ? p.peers.p[j] + base : nullptr;
+  } else {
+    s.a = (MODE == kModeThetaU ? p.theta : p.s) + base;
+    s.b = MODE == kModeThetaU ? p.u + base : nullptr;
+  }
+  s.z = MODE != kModeIdent ? p.z + base : nullptr;
+  s.v = MODE != kModeIdent ? p.v + base : nullptr;
+  return s;
+}
+
+// issue the quad at element e of every source into stage d (FULL: 16-B copies,
+// the quad is known to be in range)
+template <int MODE, bool FULL>
+__device__ __forceinline__ void k1_issue(float4* ring, int d, const K1Src& s, long long e, long long n) {
+  constexpr int NB = K1<MODE>::NB;
+  auto cp = [&](int slot, const float* src) {
+    if (FULL)
+      cp16(ring_slot<NB>(ring, d, slot), src + e);
+    else
+      cp_quad(ring_slot<NB>(ring, d, slot), src, e, n);
+  };
+  if (MODE == kModePeers) {
+#pragma unroll
+    for (int j = 0; j < kMaxPeers; ++j)
+      if (j < s.np) cp(j, s.peer[j]);
+  } else {
+    cp(0, s.a);
+    if (MODE == kModeThetaU) cp(1, s.b);
+  }
+  if (MODE != kModeIdent) {
+    cp(K1<MODE>::ZS, s.z);
+    cp(K1<MODE>::ZS + 1, s.v);
+  }
+}
+
+// the four fp64 candidates of stage d
+template <int MODE>
+__device__ __forceinline__ void k1_cand(float4* ring, int d, int np, const Coef& cf, double c[4]) {
+  constexpr int NB = K1<MODE>::NB;
+  double s[4];
+  if (MODE == kModePeers) {
+    const float4 x0 = *ring_slot<NB>(ring, d, 0);
+    s[0] = x0.x; s[1] = x0.y; s[2] = x0.z; s[3] = x0.w;
+#pragma unroll
+    for (int j = 1; j < kMaxPeers; ++j) {
+      if (j < np) {
+        const float4 x = *ring_slot<NB>(ring, d, j);
+        s[0] = __dadd_rn(s[0], (double)x.x); s[1] = __dadd_rn(s[1], (double)x.y);
+        s[2] = __dadd_rn(s[2], (double)x.z); s[3] = __dadd_rn(s[3], (double)x.w);
+      }
+    }
+  } else {
+    const float4 a = *ring_slot<NB>(ring, d, 0);
+    if (MODE == kModeThetaU) {
+      const float4 b = *ring_slot<NB>(ring, d, 1);
+      s[0] = __dadd_rn((double)a.x, (double)b.x); s[1] = __dadd_rn((double)a.y, (double)b.y);
+      s[2] = __dadd_rn((double)a.z, (double)b.z); s[3] = __dadd_rn((double)a.w, (double)b.w);
+    } else {
+      s[0] = a.x; s[1] = a.y; s[2] = a.z; s[3] = a.w;
+    }
+  }
+  if (MODE == kModeIdent) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i] = s[i];
+    return;
+  }
+  const float4 z = *ring_slot<NB>(ring, d, K1<MODE>::ZS), v = *ring_slot<NB>(ring, d, K1<MODE>::ZS + 1);
+  c[0] = cand_of(s[0], z.x, v.x, cf);
+  c[1] = cand_of(s[1], z.y, v.y, cf);
+  c[2] = cand_of(s[2], z.z, v.z, cf);
+  c[3] = cand_of(s[3], z.w, v.w, cf);
 }
 
 template <int MODE>
 __device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, const Coef& cf) {
-  if (MODE == kModeIdent) return (double)p.s[gi];
-  double s = MODE == kModeSum ? (double)p.s[gi] : __dadd_rn((double)p.theta[gi], (double)p.u[gi]);
+  double s;
+  if (MODE == kModePeers) {
+    s = (double)p.peers.p[0][gi];
+    for (int j = 1; j < p.peers.n; ++j) s = __dadd_rn(s, (double)p.peers.p[j][gi]);
+  } else if (MODE == kModeThetaU) {
+    s = __dadd_rn((double)p.theta[gi], (double)p.u[gi]);
+  } else {
+    s = (double)p.s[gi];
+  }
+  if (MODE == kModeIdent) return s;
   return cand_of(s, (double)p.z[gi], (double)p.v[gi], cf);
 }
 
@@ -185,32 +276,6 @@ __device__ __forceinline__ bool kept_by(const DevLayer& ly, const uint8_t* const
   return keep;
 }
 
-// Input slots of the K1 ring: A = S (or theta), B = u (kModeThetaU), Z, V
-template <int MODE>
-__device__ __forceinline__ void k1_issue(float4* ring, int d, const float* A, const float* B,
-                                         const float* Z, const float* V, long long e, long long n) {
-  cp_quad(ring_slot<4>(ring, d, 0), A, e, n);
-  if (MODE == kModeThetaU) cp_quad(ring_slot<4>(ring, d, 1), B, e, n);
-  if (MODE != kModeIdent) {
-    cp_quad(ring_slot<4>(ring, d, 2), Z, e, n);
-    cp_quad(ring_slot<4>(ring, d, 3), V, e, n);
-  }
-}
-
-template <int MODE>
-__device__ __forceinline__ In4 k1_read(float4* ring, int d) {
-  In4 x;
-  x.a = *ring_slot<4>(ring, d, 0);
-  x.b = MODE == kModeThetaU ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-  if (MODE != kModeIdent) {
-    x.z = *ring_slot<4>(ring, d, 2);
-    x.v = *ring_slot<4>(ring, d, 3);
-  } else {
-    x.z = x.v = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  return x;
-}
-
 // K1a: elementwise candidate over [begin, end) of one layer (dense layers; every
 // layer in frozen mode, where prunable layers get cand * global mask,
 // consensus.py:177-180). Inputs stream through the per-thread cp.async ring.
@@ -223,25 +288,23 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
   const Coef cf = coef_of(ly);
   const long long n = ly.n, off = ly.off, mword = ly.mword;
   const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
-  const float* A = (MODE == kModeThetaU ? p.theta : p.s) + off;
-  const float* B = MODE == kModeThetaU ? p.u + off : nullptr;
-  const float* Z = MODE != kModeIdent ? p.z + off : nullptr;
-  const float* V = MODE != kModeIdent ? p.v + off : nullptr;
+  const K1Src src = k1_src<MODE>(p, off);
   float* zn = p.zn + off;
   const uint32_t* fm = masked ? p.fmask + mword : nullptr;
   ring_run(
       count,
-      [&](int d, int i) { k1_issue<MODE>(ring, d, A, B, Z, V, begin + 4 * (t + (long long)i * kThreads), n); },
+      [&](int d, int i) { k1_issue<MODE, false>(ring, d, src, begin + 4 * (t + (long long)i * kThreads), n); },
       [&](int d, int i) {
         const long long e = begin + 4 * (t + (long long)i * kThreads);
-        const In4 x = k1_read<MODE>(ring, d);
+        double c[4];
+        k1_cand<MODE>(ring, d, src.np, cf, c);
         const uint32_t bits = fm ? fm[e >> 5] : 0u;
         float4 out;
 #pragma unroll
         for (int i2 = 0; i2 < 4; ++i2) {
-          double c = cand4<MODE>(x, i2, cf);
-          if (fm) c = ((bits >> ((e + i2) & 31)) & 1u) ? c : c * 0.0;
-          f4set(out, i2, (float)c);
+          double ci = c[i2];
+          if (fm) ci = ((bits >> ((e + i2) & 31)) & 1u) ? ci : ci * 0.0;
+          f4set(out, i2, (float)ci);
         }
         if (e + 3 < n) {
           st4(zn + e, out);
@@ -252,7 +315,7 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
 }
 
 // K1b quad tiles (CHANNEL / SHAPE groups, c_in*kh*kw % 4 == 0 — every ResNet conv
-// but the 7x7 stem): a tile is 32 rows x 64 column quads; thread t owns quad
+// but the 7x7 stem): a tile is rows x 64 column quads; thread t owns quad
 // (t & 63) and row phase (t >> 6), so its fp64 column sums of squares stay in
 // registers while its rows stream through the cp.async ring; the 4 phases fold
 // in shared memory in a fixed order and the tile writes one fp64 partial per
@@ -272,43 +335,30 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const long long r0 = it.begin + ph, r1 = it.end;
   const int count = (j < Q && r0 < r1) ? (int)((r1 - r0 + RP - 1) / RP) : 0;
   const long long off = ly.off;
-  const float* A = (MODE == kModeThetaU ? p.theta : p.s) + off + 4 * j;
-  const float* B = MODE == kModeThetaU ? p.u + off + 4 * j : nullptr;
-  const float* Z = MODE != kModeIdent ? p.z + off + 4 * j : nullptr;
-  const float* V = MODE != kModeIdent ? p.v + off + 4 * j : nullptr;
+  const K1Src src = k1_src<MODE>(p, off + 4 * j);
   float* zn = p.zn + off + 4 * j;
   const Coef cf = coef_of(ly);
   const long long stride = (long long)RP * L;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   ring_run(
       count,
+      [&](int d, int i) { k1_issue<MODE, true>(ring, d, src, r0 * L + i * stride, 0); },
       [&](int d, int i) {
         const long long e = r0 * L + i * stride;
-        cp16(ring_slot<4>(ring, d, 0), A + e);
-        if (MODE == kModeThetaU) cp16(ring_slot<4>(ring, d, 1), B + e);
-        if (MODE != kModeIdent) {
-          cp16(ring_slot<4>(ring, d, 2), Z + e);
-          cp16(ring_slot<4>(ring, d, 3), V + e);
-        }
-      },
-      [&](int d, int i) {
-        const long long e = r0 * L + i * stride;
-        const In4 x = k1_read<MODE>(ring, d);
-        double c0 = cand4<MODE>(x, 0, cf), c1 = cand4<MODE>(x, 1, cf);
-        double c2 = cand4<MODE>(x, 2, cf), c3 = cand4<MODE>(x, 3, cf);
+        double c[4];
+        k1_cand<MODE>(ring, d, src.np, cf, c);
         if (pass > 0) {
           const long long ee = e + 4 * j;
-          if (!kept_by(ly, p.flags, pass, ee + 0)) c0 = 0.0;
-          if (!kept_by(ly, p.flags, pass, ee + 1)) c1 = 0.0;
-          if (!kept_by(ly, p.flags, pass, ee + 2)) c2 = 0.0;
-          if (!kept_by(ly, p.flags, pass, ee + 3)) c3 = 0.0;
+#pragma unroll
+          for (int i2 = 0; i2 < 4; ++i2)
+            if (!kept_by(ly, p.flags, pass, ee + i2)) c[i2] = 0.0;
         } else {
-          st4(zn + e, make_float4((float)c0, (float)c1, (float)c2, (float)c3));
+          st4(zn + e, make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]));
         }
-        a0 = __dadd_rn(a0, __dmul_rn(c0, c0));
-        a1 = __dadd_rn(a1, __dmul_rn(c1, c1));
-        a2 = __dadd_rn(a2, __dmul_rn(c2, c2));
-        a3 = __dadd_rn(a3, __dmul_rn(c3, c3));
+        a0 = __dadd_rn(a0, __dmul_rn(c[0], c[0]));
+        a1 = __dadd_rn(a1, __dmul_rn(c[1], c[1]));
+        a2 = __dadd_rn(a2, __dmul_rn(c[2], c[2]));
+        a3 = __dadd_rn(a3, __dmul_rn(c[3], c[3]));
       });
   double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
@@ -385,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
   }
   if (ly.ncons <= p.pass) return;
   if (ly.tiling == 1)
-    cand_tile_quads<MODE>(p, ly, it, ring, reinterpret_cast<double*>(ring + kDepth * 4 * kThreads));
+    cand_tile_quads<MODE>(p, ly, it, ring, reinterpret_cast<double*>(ring + kDepth * K1<MODE>::NB * kThreads));
   else
     cand_tile_rows<MODE>(p, ly, it, reinterpret_cast<double*>(ring));
 }
@@ -398,7 +448,9 @@ static void launch_candidate_mode(const CandArgs& a, int n_items, int frozen, si
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
   if (n_items <= 0) return;
-  if (a.identity)
+  if (a.peers.n > 0)
+    launch_candidate_mode<kModePeers>(a, n_items, frozen, smem + (size_t)kDepth * (kMaxPeers - 2) * kThreads * 16, st);
+  else if (a.identity)
     launch_candidate_mode<kModeIdent>(a, n_items, frozen, smem, st);
   else if (a.s)
     launch_candidate_mode<kModeSum>(a, n_items, frozen, smem, st);
@@ -704,15 +756,13 @@ void launch_project(const DevLayer* layers, const Item* items, int n_items, floa
 // leaders all-gather packed bits and OR them here.
 // ---------------------------------------------------------------------------
 
-__global__ void k_mask_or(const uint32_t* __restrict__ g, int m, long long words,
-                          uint32_t* __restrict__ out, int vec) {
+__global__ void k_mask_or(MaskPtrs g, long long words, uint32_t* __restrict__ out, int vec) {
   const long long n4 = vec ? (words >> 2) : 0;
-  const uint4* g4 = reinterpret_cast<const uint4*>(g);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     uint4 acc = make_uint4(0, 0, 0, 0);
-    for (int r = 0; r < m; ++r) {
-      uint4 x = g4[r * n4 + i];
+    for (int r = 0; r < g.n; ++r) {
+      uint4 x = reinterpret_cast<const uint4*>(g.p[r])[i];
       acc.x |= x.x; acc.y |= x.y; acc.z |= x.z; acc.w |= x.w;
     }
     reinterpret_cast<uint4*>(out)[i] = acc;
@@ -720,18 +770,18 @@ __global__ void k_mask_or(const uint32_t* __restrict__ g, int m, long long words
   for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < words;
        i += (long long)gridDim.x * blockDim.x) {
     uint32_t acc = 0;
-    for (int r = 0; r < m; ++r) acc |= g[r * words + i];
+    for (int r = 0; r < g.n; ++r) acc |= g.p[r][i];
     out[i] = acc;
   }
 }
 
-void launch_mask_or(const uint32_t* g, int m, long long words, uint32_t* out, cudaStream_t st) {
-  if (words <= 0) return;
-  // gathered slices are 16-B aligned relative to each other only if words % 4 == 0
-  const int vec = (words & 3) == 0;
+void launch_mask_or(const MaskPtrs& g, long long words, uint32_t* out, cudaStream_t st) {
+  if (words <= 0 || g.n <= 0) return;
+  int vec = 1;  // 16-B aligned sources (arenas and all-gather slices of words % 4 == 0)
+  for (int r = 0; r < g.n; ++r) vec &= (reinterpret_cast<uintptr_t>(g.p[r]) & 15) == 0;
   long long n = vec ? (words >> 2) : words;
   int grid = (int)std::min<long long>(std::max<long long>((n + 255) / 256, 1), 148LL * 16);
-  k_mask_or<<<grid, 256, 0, st>>>(g, m, words, out, vec);
+  k_mask_or<<<grid, 256, 0, st>>>(g, words, out, vec);
 }
 
 // ---------------------------------------------------------------------------
@@ -1061,35 +1111,72 @@ void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
 
 // K7: z <- zero-filled gather of flat / divisor (+ v <- v + (z_node - z)); the
 // gather streams through the ring: dropped coordinates are zero-filled by
-// cp.async without touching memory.
+// cp.async without touching memory. PEERS: the gather reads the same payload
+// index from every leader's flat buffer over NVLink and averages them in rank
+// order in fp64 (the leader all-reduce AVG fused into decompaction,
+// transport.py:453-462), optionally writing the average in payload layout
+// (zhat) for the node's followers.
+template <bool PEERS>
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
+  constexpr int NB = PEERS ? kMaxPeers + 2 : 3;
+  constexpr int ZS = PEERS ? kMaxPeers : 1;  // slot of z_node (v follows)
   extern __shared__ float4 ring[];
   __shared__ int s_rb[kMaxTileRows];
   const Item it = a.items[blockIdx.x];
   const LayerRegs ly(a.layers, it.layer);
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
-  const float* __restrict__ flat = a.flat_in + coff;
+  const int np = PEERS ? a.flats.n : 1;
+  const float* src[kMaxPeers];
+#pragma unroll
+  for (int j = 0; j < kMaxPeers; ++j) src[j] = PEERS ? (j < np ? a.flats.p[j] + coff : nullptr) : (j == 0 ? a.flat_in + coff : nullptr);
+  float* __restrict__ zhat = PEERS && a.zhat ? a.zhat + coff : nullptr;
   const float* __restrict__ ZN = a.v ? a.zn + ly.off : nullptr;
   float* __restrict__ VV = a.v ? a.v + ly.off : nullptr;
   float* __restrict__ ZO = a.z + ly.off;
   const float div = a.divisor;
   auto load = [&](int d, long long e, int4 dd) {
-    float* g = reinterpret_cast<float*>(ring_slot<3>(ring, d, 0));
-    cp4z(g + 0, flat + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
-    cp4z(g + 1, flat + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
-    cp4z(g + 2, flat + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
-    cp4z(g + 3, flat + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
+#pragma unroll
+    for (int j = 0; j < kMaxPeers; ++j) {
+      if (j >= np) break;
+      float* g = reinterpret_cast<float*>(ring_slot<NB>(ring, d, j));
+      cp4z(g + 0, src[j] + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
+      cp4z(g + 1, src[j] + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
+      cp4z(g + 2, src[j] + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
+      cp4z(g + 3, src[j] + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
+    }
     if (ZN) {
-      cp_quad(ring_slot<3>(ring, d, 1), ZN, e, ly.n);
-      cp_quad(ring_slot<3>(ring, d, 2), VV, e, ly.n);
+      cp_quad(ring_slot<NB>(ring, d, ZS), ZN, e, ly.n);
+      cp_quad(ring_slot<NB>(ring, d, ZS + 1), VV, e, ly.n);
     }
   };
-  auto emit = [&](int d, long long e) {
-    float4 zo = *ring_slot<3>(ring, d, 0);
-    if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
+  auto emit = [&](int d, long long e, int4 dd) {
+    float4 zo;
+    if (PEERS) {
+      float4 g = *ring_slot<NB>(ring, d, 0);
+      double s0 = g.x, s1 = g.y, s2 = g.z, s3 = g.w;
+#pragma unroll
+      for (int j = 1; j < kMaxPeers; ++j) {
+        if (j >= np) break;
+        g = *ring_slot<NB>(ring, d, j);
+        s0 = __dadd_rn(s0, (double)g.x); s1 = __dadd_rn(s1, (double)g.y);
+        s2 = __dadd_rn(s2, (double)g.z); s3 = __dadd_rn(s3, (double)g.w);
+      }
+      const double dv = (double)div;
+      zo = make_float4((float)__ddiv_rn(s0, dv), (float)__ddiv_rn(s1, dv), (float)__ddiv_rn(s2, dv),
+                       (float)__ddiv_rn(s3, dv));
+      if (zhat) {
+        if (dd.x >= 0) zhat[dd.x] = zo.x;
+        if (dd.y >= 0) zhat[dd.y] = zo.y;
+        if (dd.z >= 0) zhat[dd.z] = zo.z;
+        if (dd.w >= 0) zhat[dd.w] = zo.w;
+      }
+    } else {
+      zo = *ring_slot<NB>(ring, d, 0);
+      if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
+    }
     float4 vn;
     if (ZN) {
-      float4 zn = *ring_slot<3>(ring, d, 1), vv = *ring_slot<3>(ring, d, 2);
+      float4 zn = *ring_slot<NB>(ring, d, ZS), vv = *ring_slot<NB>(ring, d, ZS + 1);
       vn = make_float4(dual1(vv.x, zn.x, zo.x), dual1(vv.y, zn.y, zo.y), dual1(vv.z, zn.z, zo.z),
                        dual1(vv.w, zn.w, zo.w));
     }
@@ -1114,7 +1201,10 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
                const long long r = tc.row(i);
                load(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
              },
-             [&](int d, int i) { emit(d, tc.row(i) * ly.L + 4 * tc.j); });
+             [&](int d, int i) {
+               const long long r = tc.row(i);
+               emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
+             });
     return;
   }
   const long long nq = (it.end - it.begin + 3) >> 2;
@@ -1125,14 +1215,23 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
              const long long e = it.begin + 4 * (t + (long long)i * kThreads);
              load(d, e, dst4_linear(a, ly, e));
            },
-           [&](int d, int i) { emit(d, it.begin + 4 * (t + (long long)i * kThreads)); });
+           [&](int d, int i) {
+             const long long e = it.begin + 4 * (t + (long long)i * kThreads);
+             emit(d, e, PEERS ? dst4_linear(a, ly, e) : make_int4(-1, -1, -1, -1));
+           });
 }
 
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
-  const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
-  allow_smem(k_decompact, smem);
-  k_decompact<<<n_items, kThreads, smem, st>>>(a);
+  if (a.flats.n > 0) {
+    const size_t smem = (size_t)kDepth * (kMaxPeers + 2) * kThreads * sizeof(float4);
+    allow_smem(k_decompact<true>, smem);
+    k_decompact<true><<<n_items, kThreads, smem, st>>>(a);
+  } else {
+    const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
+    allow_smem(k_decompact<false>, smem);
+    k_decompact<false><<<n_items, kThreads, smem, st>>>(a);
+  }
 }
 
 // ---------------------------------------------------------------------------

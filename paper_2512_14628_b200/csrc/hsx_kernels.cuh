@@ -72,6 +72,19 @@ struct Item {
   long long begin, end;  // element range (quad tiling: rows [begin, end))
 };
 
+constexpr int kMaxPeers = 4;  // ranks whose buffers a fused peer kernel reads
+
+// device pointers of the same buffer on every rank of a group (member order)
+struct PeerPtrs {
+  const float* p[kMaxPeers];
+  int n;
+};
+
+struct MaskPtrs {
+  const uint32_t* p[8];
+  int n;
+};
+
 struct CandArgs {
   const float* __restrict__ s;
   const float* __restrict__ theta;
@@ -84,6 +97,7 @@ struct CandArgs {
   const Item* __restrict__ items;
   double* __restrict__ partials;       // this pass
   const uint8_t* flags[kMaxPasses];    // keep flags of earlier passes (renorm)
+  PeerPtrs peers;                      // n > 0: S = sum of the peers' theta + u (rank order)
   int pass;
   int identity;                        // candidate = input (per-tensor API)
   int sqcap;                           // doubles of the sq sub-tile region
@@ -111,6 +125,8 @@ struct ElemArgs {
   const int* __restrict__ rowbase;
   const int* __restrict__ colpos;
   const long long* __restrict__ summary;
+  PeerPtrs flats;       // n > 0: leaders' flat buffers, averaged in rank order (K7)
+  float* zhat;          // K7 peers: averaged payload for the node's followers (may be null)
   float divisor;
 };
 
@@ -122,7 +138,7 @@ void launch_select(const DevLayer* layers, const int* list, int n, int pass, con
                    double* norms, FlagPtrs flags, Maps maps, size_t smem, cudaStream_t st);
 void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
                     uint32_t* mask, Maps maps, cudaStream_t st);
-void launch_mask_or(const uint32_t* g, int m, long long words, uint32_t* out, cudaStream_t st);
+void launch_mask_or(const MaskPtrs& g, long long words, uint32_t* out, cudaStream_t st);
 struct KeepArgs {
   const DevLayer* layers;
   const Item* items;

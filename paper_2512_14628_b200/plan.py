@@ -193,6 +193,26 @@ class Plan:
             _lib.call("hsx_candidate", self._h, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v), ptr(z_node),
                       ptr(frozen_mask), current_stream())
 
+    def candidate_peers(self, sends: list[int], z, v, z_node, frozen_mask=None):
+        arr, keep = _lib.ptr_array(sends)
+        with timed("K1_candidate"):
+            _lib.call("hsx_candidate_peers", self._h, arr, len(sends), ptr(z), ptr(v), ptr(z_node),
+                      ptr(frozen_mask), current_stream())
+        del keep
+
+    def decompact_peers(self, flats: list[int], divisor, zhat, z_node, v, z):
+        arr, keep = _lib.ptr_array(flats)
+        with timed("K7_decompact_dual"):
+            _lib.call("hsx_decompact_peers", self._h, arr, len(flats), float(divisor), ptr(zhat),
+                      ptr(z_node), ptr(v), ptr(z), current_stream())
+        del keep
+
+    def decompact_from(self, flat_ptr: int, z_node, v, z):
+        """K7 reading the payload at a (possibly peer-mapped) device pointer."""
+        with timed("K7_decompact_dual"):
+            _lib.call("hsx_decompact_dual", self._h, int(flat_ptr), 1.0, ptr(z_node), ptr(v), ptr(z),
+                      current_stream())
+
     def renorm(self, p, s, theta, u, z, v):
         with timed("K1r_renorm"):
             _lib.call("hsx_candidate_renorm", self._h, p, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v),
@@ -206,11 +226,19 @@ class Plan:
         with timed("K3_project"):
             _lib.call("hsx_project", self._h, ptr(z_node), ptr(local_mask), current_stream())
 
-    def project_all(self, s, theta, u, z, v, z_node, local_mask):
-        """K2 (+ composite passes) + K3 after hsx_candidate."""
+    def project_all(self, s, theta, u, z, v, z_node, local_mask, peers=None):
+        """K2 (+ composite passes) + K3 after hsx_candidate (peers: the sends of
+        hsx_candidate_peers, re-read by composite passes)."""
         for p in range(self.max_passes):
             if p > 0:
-                self.renorm(p, s, theta, u, z, v)
+                if peers:
+                    arr, keep = _lib.ptr_array(peers)
+                    with timed("K1r_renorm"):
+                        _lib.call("hsx_candidate_renorm_peers", self._h, p, arr, len(peers), ptr(z), ptr(v),
+                                  current_stream())
+                    del keep
+                else:
+                    self.renorm(p, s, theta, u, z, v)
             self.select(p)
         self.project(z_node, local_mask)
 
@@ -282,6 +310,14 @@ class Plan:
         with timed("K7_decompact_dual"):
             _lib.call("hsx_decompact_dual", self._h, ptr(flat), float(divisor), ptr(z_node), ptr(v),
                       ptr(z), current_stream())
+
+
+def mask_or_ptrs(srcs: list[int], words: int, out):
+    """out = OR of the masks at device pointers ``srcs`` (one source = a copy)."""
+    arr, keep = _lib.ptr_array(srcs)
+    with timed("K4_mask_or"):
+        _lib.call("hsx_mask_or_ptrs", arr, len(srcs), int(words), ptr(out), current_stream())
+    del keep
 
 
 def mask_or(gathered, n_ranks: int, words: int, out):

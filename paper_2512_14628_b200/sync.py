@@ -38,9 +38,9 @@ import torch
 from .consensus import ConsensusSettings, PenaltySchedule, freeze_check
 from .errors import ProtocolError, ShapeError
 from .layers import LayerSpec
-from .plan import Plan, mask_or
+from .plan import Plan, mask_or, mask_or_ptrs
 from .sparsity import resolve_plan
-from .transport import AllGather, AllReduce, Broadcast, ReduceOp, bucketize
+from .transport import AllGather, AllReduce, Barrier, Broadcast, LedgerEntry, ReduceOp, bucketize
 from . import _lib
 
 
@@ -53,7 +53,8 @@ class HSADMMSync:
     """
 
     def __init__(self, rank: int, cluster, layers: list[LayerSpec], constraints: dict,
-                 schedule: PenaltySchedule, settings: ConsensusSettings, device=None):
+                 schedule: PenaltySchedule, settings: ConsensusSettings, device=None,
+                 transport: str = "auto"):
         topo = cluster.topology
         self.rank = rank
         self.cluster = cluster
@@ -96,6 +97,33 @@ class HSADMMSync:
         self._prunable_names = [self.names[i] for i in self.prunable]
         self._prunable_elems = np.array([self.layers[i].elements for i in self.prunable], dtype=np.float64)
         self._layout_from_summary(initial=True)
+        # transport: "peer" = fused NVLink kernels on peer-mapped buffers (no NCCL on the
+        # step, no mid-step host sync); "nccl" = torch.distributed collectives
+        peer_ok = getattr(cluster, "supports_peer", False) and self.M <= 4 and self.P <= 4
+        if transport == "auto":  # one rank has no collectives: the plain path has fewer launches
+            transport = "peer" if (peer_ok and self.M * self.P > 1) else "nccl"
+        if transport == "peer" and not peer_ok:
+            raise ProtocolError("peer transport needs symmetric memory and at most 4 x 4 ranks")
+        self.transport = transport
+        if transport == "peer":
+            self._init_peer_buffers()
+
+    def _init_peer_buffers(self):
+        """Shared (peer-mapped) buffers; allocation is collective over each group."""
+        pl, dev, cl = self.plan, self.device, self.cluster
+        words = max(pl.mask_words, 1)
+        self.p_send = self.p_umask = self.p_zhat = self.p_lmask = None
+        self.p_flat = None
+        if self.P > 1:
+            self.p_send = cl.shared(self.rank, self.intra, "send", pl.arena, torch.float32, dev)
+            self.p_umask = cl.shared(self.rank, self.intra, "umask", words, torch.int32, dev)
+            self.p_zhat = cl.shared(self.rank, self.intra, "zhat", pl.arena, torch.float32, dev)
+        if self.is_leader and self.M > 1:
+            self.p_lmask = cl.shared(self.rank, self.inter, "lmask", words, torch.int32, dev)
+            # double-buffered by iteration parity: a leader may start the next
+            # compaction while another still averages this one
+            self.p_flat = [cl.shared(self.rank, self.inter, f"flat{b}", pl.arena, torch.float32, dev)
+                           for b in (0, 1)]
 
     # -- state I/O ---------------------------------------------------------------
     def load(self, **arrays) -> None:
@@ -153,6 +181,91 @@ class HSADMMSync:
     # -- the per-iteration program ------------------------------------------------------
     def program(self, k: int):
         """Generator: yields collective requests, performs phases 2-5(u) of iteration k."""
+        if self.transport == "peer":
+            return (yield from self._program_peer(k))
+        return (yield from self._program_nccl(k))
+
+    def _log_zsync(self, k: int):
+        """Ledger entries of the leader average, identical to the reference's z_sync/b{i}."""
+        for bi, b in enumerate(self.buckets):
+            self.cluster.log(LedgerEntry(k, self.inter.id, self.inter.scope.value, "allreduce_avg",
+                                         b.elements, 4 * b.elements, self.M, f"z_sync/b{bi}", b.detail))
+
+    def _program_peer(self, k: int):
+        """Phases 2-5(u) with the collectives fused into the kernels over NVLink.
+
+        intra sum -> K1 reads the P ranks' theta+u (rank-order fp64 fold);
+        mask union -> K4 reads the M leaders' mask bits; leader average + broadcast ->
+        K7 on leaders reads the M leaders' compact buffers (rank-order fold, / M)
+        and writes the average for its followers, whose K7 reads it from the
+        leader. Barriers order producers before peer readers; sizes and offsets
+        stay on the device, so the step has no host sync until its end.
+        """
+        pl = self.plan
+        frozen = self.frozen
+        dynamic = not frozen and bool(self.prunable)
+        fmask = self.masks if (frozen and self.prunable) else None
+        if self.P > 1:
+            pl.pack_theta_u(self.theta, self.u, self.p_send.tensor)
+            yield Barrier(self.intra, "theta_u", k)
+            pl.candidate_peers(self.p_send.peer_ptrs(), self.z, self.v, self.z_node, frozen_mask=fmask)
+        else:
+            pl.candidate(None, self.theta, self.u, self.z, self.v, self.z_node, frozen_mask=fmask)
+        if dynamic:
+            local = self.p_lmask.tensor if self.p_lmask is not None else self.local_mask
+            pl.project_all(None, self.theta, self.u, self.z, self.v, self.z_node, local,
+                           peers=self.p_send.peer_ptrs() if self.P > 1 else None)
+        if k % self.settings.sync_period != 0:
+            pl.dual_intra(self.theta, self.u, self.z_node)
+            return None
+        ev = None
+        if dynamic:
+            words = pl.mask_words
+            if self.is_leader:
+                target = self.p_umask.tensor if self.P > 1 else self.union
+                srcs = self.p_lmask.peer_ptrs() if self.M > 1 else [local.data_ptr()]
+                if self.M > 1:
+                    yield Barrier(self.inter, "mask_sync", k)
+                mask_or_ptrs(srcs, words, target)
+            if self.P > 1:
+                yield Barrier(self.intra, "m_bcast", k)
+                mask_or_ptrs([self.p_umask.peer_ptrs()[0]], words, self.union)  # copy of the leader's union
+            pl.keep_sets(self.union, self.masks)
+            ev = pl.keep_sets_fetch_async()
+        elif self.is_leader and self.prunable:
+            self.cache_hits += len(self.prunable)
+        zhat = self.p_zhat.tensor if self.P > 1 else None
+        if self.is_leader:
+            flat = self.p_flat[k & 1] if self.M > 1 else None
+            pl.compact_dual(self.theta, self.u, self.z_node, self.v, flat.tensor if flat else self.flat)
+            if self.M > 1:
+                yield Barrier(self.inter, "z_sync", k)
+                pl.decompact_peers(flat.peer_ptrs(), float(self.M), zhat, self.z_node, self.v, self.z)
+            elif zhat is not None:
+                pl.decompact_peers([self.flat.data_ptr()], 1.0, zhat, self.z_node, self.v, self.z)
+            else:
+                pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
+        else:
+            pl.dual_intra(self.theta, self.u, self.z_node)
+        if self.P > 1:
+            yield Barrier(self.intra, "zhat_bcast", k)
+            if not self.is_leader:
+                pl.decompact_from(self.p_zhat.peer_ptrs()[0], self.z_node, self.v, self.z)
+        if ev is not None:
+            ev.synchronize()
+            self._after_keep_sets()
+        if self.is_leader:
+            self._log_zsync(k)
+        if dynamic:
+            mask_or_ptrs([self.union.data_ptr()], pl.mask_words, self.masks)
+        if dynamic and freeze_check(k, self.settings.t_freeze, self.drift_history,
+                                    self.settings.drift_window):
+            self.frozen = True
+            if self.is_leader:
+                self.cache_hits += len(self.prunable)
+        return None
+
+    def _program_nccl(self, k: int):
         pl = self.plan
         frozen = self.frozen
         dynamic = not frozen and bool(self.prunable)

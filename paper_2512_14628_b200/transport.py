@@ -141,6 +141,30 @@ class AllGather:
     iteration: int
 
 
+@dataclass
+class Barrier:
+    """Every member reaches this point before any continues (device-side barrier over
+    NVLink signal pads under DistCluster; scheduler rendezvous under LocalCluster).
+    Orders the producers of shared (peer-mapped) buffers before their readers."""
+
+    group: ProcessGroup
+    tag: str
+    iteration: int
+
+
+class SharedBuffer:
+    """A buffer every member of a group allocates; ``peer_ptrs()`` are the device
+    pointers of all members' copies in member order (torch symmetric memory under
+    DistCluster; the other in-process ranks' tensors under LocalCluster)."""
+
+    def __init__(self, tensor, resolve):
+        self.tensor = tensor
+        self._resolve = resolve
+
+    def peer_ptrs(self) -> list[int]:
+        return self._resolve()
+
+
 RankProgram = Generator[Any, Any, Any]
 
 
@@ -281,7 +305,7 @@ def unbucketize(bucket: Bucket, buffer) -> dict:
 
 
 def _validate(rank: int, req) -> None:
-    if not isinstance(req, (AllReduce, Broadcast, AllGather)):
+    if not isinstance(req, (AllReduce, Broadcast, AllGather, Barrier)):
         raise ProtocolError(f"rank {rank} yielded a non-collective object: {req!r}")
     if rank not in req.group.members:
         raise ProtocolError(f"rank {rank} is not a member of group {req.group.id}")
@@ -298,6 +322,7 @@ class LocalCluster:
         self.topology = topology
         self.ledger = CommLedger()
         self._intra, self._leaders, self._global = hierarchy_groups(topology)
+        self._shared = {}
 
     def intra_group(self, node: int) -> ProcessGroup:
         return self._intra[node]
@@ -307,6 +332,22 @@ class LocalCluster:
 
     def global_group(self) -> ProcessGroup:
         return self._global
+
+    supports_peer = True  # all ranks share one device: "peer" pointers are the other ranks' tensors
+
+    def shared(self, rank: int, group: ProcessGroup, key: str, numel: int, dtype, device) -> SharedBuffer:
+        import torch
+
+        t = torch.zeros(max(int(numel), 1), dtype=dtype, device=device)
+        self._shared[(group.id, key, rank)] = t
+
+        def resolve():
+            return [self._shared[(group.id, key, r)].data_ptr() for r in group.members]
+
+        return SharedBuffer(t, resolve)
+
+    def log(self, entry: LedgerEntry) -> None:
+        self.ledger.append(entry)
 
     def run(self, programs: Mapping[int, RankProgram]) -> dict[int, Any]:
         gens = dict(programs)
@@ -354,6 +395,8 @@ class LocalCluster:
                 raise ProtocolError(f"group {group.id}: mismatched collectives "
                                     f"({type(first).__name__}:{first.tag} vs {type(q).__name__}:{q.tag})")
         g = len(group.members)
+        if isinstance(first, Barrier):
+            return {r: None for r in group.members}
         if isinstance(first, Broadcast):
             if len({q.root for q in reqs}) != 1:
                 raise ProtocolError(f"group {group.id}: broadcast roots disagree")
@@ -411,6 +454,30 @@ class DistCluster:
         self._handles["leaders"] = dist.new_group(list(self._leaders.members))
         self._handles["global"] = dist.group.WORLD
         self._avg = dist.get_backend() == "nccl"
+        self._symm = {}      # group id -> symmetric-memory handle used for barriers
+        self.supports_peer = self._avg and self._symm_available()
+
+    @staticmethod
+    def _symm_available() -> bool:
+        try:
+            import torch.distributed._symmetric_memory  # noqa: F401
+        except Exception:
+            return False
+        return True
+
+    def shared(self, rank: int, group: ProcessGroup, key: str, numel: int, dtype, device) -> SharedBuffer:
+        """Collective over ``group``: symmetric-memory buffer mapped on every member."""
+        import torch.distributed._symmetric_memory as symm
+
+        t = symm.empty(max(int(numel), 1), dtype=dtype, device=device)
+        t.zero_()
+        h = symm.rendezvous(t, self._handles[group.id])
+        self._symm.setdefault(group.id, h)
+        ptrs = [int(p) for p in h.buffer_ptrs]
+        return SharedBuffer(t, lambda: ptrs)
+
+    def log(self, entry: LedgerEntry) -> None:
+        self.ledger.append(entry)
 
     def intra_group(self, node: int) -> ProcessGroup:
         return self._intra[node]
@@ -433,6 +500,10 @@ class DistCluster:
 
         h = self._handles[req.group.id]
         g = len(req.group.members)
+        if isinstance(req, Barrier):
+            if g > 1:
+                self._symm[req.group.id].barrier(channel=0, timeout_ms=60000)
+            return None
         if isinstance(req, Broadcast):
             if g > 1:
                 dist.broadcast(req.payload, src=req.root, group=h)

@@ -37,7 +37,7 @@ def rel_err(got, ref, *ops):
     return float(np.abs(np.asarray(got, np.float64) - ref).max() / scale)
 
 
-def golden_check(topo, rank):
+def golden_check(topo, rank, transport):
     ref = G.E2E(topo.num_nodes, topo.accels_per_node)
     kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
              "shape": H.ConstraintKind.SHAPE_KEEP}
@@ -47,7 +47,8 @@ def golden_check(topo, rank):
     sched = H.PenaltySchedule.uniform(ref.names, G.E2E_RHO1, G.E2E_RHO2, adapt=False)
     settings = H.ConsensusSettings(t_freeze=ref.t_freeze, weight_decay=G.E2E_WD)
     cluster = H.DistCluster(topo)
-    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings)
+    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, transport=transport)
+    assert eng.transport == transport
     eng.init_from(ref.p0())
     node = topo.node_of(rank)
     worst = 0.0
@@ -71,7 +72,7 @@ def golden_check(topo, rank):
     return worst
 
 
-def replica_check(topo, rank, world):
+def replica_check(topo, rank, world, transport):
     from paper_2512_14628_b200.synthetic import channel_keep_constraints, model_layers, synthetic_rank_state
 
     layers = model_layers("rn18_cifar")
@@ -79,7 +80,7 @@ def replica_check(topo, rank, world):
     sched = H.PenaltySchedule.uniform([ls.name for ls in layers], 1.5e-3, 1.5e-4, adapt=False)
     settings = H.ConsensusSettings(t_freeze=3, weight_decay=1e-4)
     cluster = H.DistCluster(topo)
-    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings)
+    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, transport=transport)
     eng.load(**synthetic_rank_state(layers, rank, topo.accels_per_node, seed=5))
     for k in range(1, 5):
         eng.step(k)
@@ -103,11 +104,13 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
-        worst = golden_check(topo, rank)
-        ratio = replica_check(topo, rank, world)
-        dist.barrier()
-        if rank == 0:
-            print(f"mp_parity {sys.argv[1]} ok: worst rel err {worst:.2e}, rn18_cifar leader payload ratio {ratio:.3f}")
+        for transport in ("nccl", "peer"):
+            worst = golden_check(topo, rank, transport)
+            ratio = replica_check(topo, rank, world, transport)
+            dist.barrier()
+            if rank == 0:
+                print(f"mp_parity {sys.argv[1]} {transport} ok: worst rel err {worst:.2e}, "
+                      f"rn18_cifar leader payload ratio {ratio:.3f}", flush=True)
     finally:
         dist.destroy_process_group()
 

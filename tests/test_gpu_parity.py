@@ -169,7 +169,7 @@ def test_update_rules_per_tensor():
 # -- end-to-end: the fused step against run_hierarchical goldens -------------------
 
 
-def _e2e_engines(M, P):
+def _e2e_engines(M, P, transport="nccl"):
     import paper_2512_14628_b200 as H
 
     ref = G.E2E(M, P)
@@ -181,17 +181,22 @@ def _e2e_engines(M, P):
     sched = H.PenaltySchedule.uniform(ref.names, G.E2E_RHO1, G.E2E_RHO2, adapt=False)
     settings = H.ConsensusSettings(iterations=ref.iters, t_freeze=ref.t_freeze, weight_decay=G.E2E_WD)
     cluster = H.LocalCluster(H.Topology(M, P))
-    engines = [H.HSADMMSync(r, cluster, layers, cons, sched, settings) for r in range(ref.world)]
+    engines = [H.HSADMMSync(r, cluster, layers, cons, sched, settings, transport=transport)
+               for r in range(ref.world)]
     for e in engines:
         e.init_from(ref.p0())
     return ref, cluster, engines
 
 
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
 @pytest.mark.parametrize("M,P", G.E2E_TOPOLOGIES)
-def test_end_to_end_against_reference_goldens(M, P):
+def test_end_to_end_against_reference_goldens(M, P, transport):
+    """Both transports: collectives as requests (NCCL semantics) and the fused
+    peer-memory kernels (K1 reads the node's theta+u, K7 averages the leaders'
+    compact buffers) — emulated in one process on one GPU."""
     import paper_2512_14628_b200 as H
 
-    ref, cluster, engines = _e2e_engines(M, P)
+    ref, cluster, engines = _e2e_engines(M, P, transport)
     for k in range(1, ref.iters + 1):
         for e in engines:
             e.load(theta=ref.theta(k, e.rank))

@@ -186,7 +186,10 @@ class HSADMMSync:
         return (yield from self._program_nccl(k))
 
     def _log_zsync(self, k: int):
-        """Ledger entries of the leader average, identical to the reference's z_sync/b{i}."""
+        """Ledger entries of the leader average, identical to the reference's z_sync/b{i}
+        (one entry per group collective: a ledger shared by in-process ranks gets it once)."""
+        if getattr(self.cluster, "shared_ledger", False) and self.rank != self.inter.members[0]:
+            return
         for bi, b in enumerate(self.buckets):
             self.cluster.log(LedgerEntry(k, self.inter.id, self.inter.scope.value, "allreduce_avg",
                                          b.elements, 4 * b.elements, self.M, f"z_sync/b{bi}", b.detail))

@@ -334,6 +334,7 @@ class LocalCluster:
         return self._global
 
     supports_peer = True  # all ranks share one device: "peer" pointers are the other ranks' tensors
+    shared_ledger = True
 
     def shared(self, rank: int, group: ProcessGroup, key: str, numel: int, dtype, device) -> SharedBuffer:
         import torch

@@ -201,11 +201,13 @@ int hsx_candidate_renorm_peers(hsx_plan* plan, int32_t pass, const float* const*
 /* K4 over mapped pointers: out = OR_j srcs[j] (leaders' local masks, transport.py:455-457). */
 int hsx_mask_or_ptrs(const uint32_t* const* srcs, int32_t n, int64_t words, uint32_t* out,
                      void* stream);
-/* K7 with the leader average fused: z = (sum_j flats[j][payload]) / divisor, zero
- * fill, v += z_node - z; zhat (may be NULL) receives the average in payload
- * layout for the node's followers (the intra broadcast becomes their read). */
-int hsx_decompact_peers(const hsx_plan* plan, const float* const* flats, int32_t n, float divisor,
-                        float* zhat, const float* z_node, float* v, float* z, void* stream);
+/* Leader average as a contiguous NVLink stream: out[i] = fp32((sum_j srcs[j][i],
+ * rank order, fp64) / divisor) for i below the payload size of the plan's last
+ * keep-set derivation (read on the device: no host sync). srcs are the leaders'
+ * flat buffers (transport.py:453-462 AVG); with n = 1, divisor = 1 it is a
+ * follower's read of its leader's averaged payload (the intra broadcast). */
+int hsx_average_peers(const hsx_plan* plan, const float* const* srcs, int32_t n, double divisor,
+                      float* out, void* stream);
 
 /* ---- mask helpers for the per-tensor API -------------------------------------- */
 /* out[i] = |t[i]| > 0  (extract_mask, sparsity.py:113-115) */

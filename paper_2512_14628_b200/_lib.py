@@ -71,7 +71,7 @@ SIGNATURES = {
     "hsx_candidate_peers": (C.c_int, [P, VP, I32, VP, VP, VP, VP, VP]),
     "hsx_mask_or_ptrs": (C.c_int, [VP, I32, I64, VP, VP]),
     "hsx_candidate_renorm_peers": (C.c_int, [P, I32, VP, I32, VP, VP, VP]),
-    "hsx_decompact_peers": (C.c_int, [P, VP, I32, F32, VP, VP, VP, VP, VP]),
+    "hsx_average_peers": (C.c_int, [P, VP, I32, F64, VP, VP]),
 }
 
 _lib = None

@@ -757,25 +757,21 @@ int hsx_decompact_dual(const hsx_plan* p, const float* flat, float divisor, cons
   return HSX_OK;
 }
 
-int hsx_decompact_peers(const hsx_plan* p, const float* const* flats, int32_t n, float divisor,
-                        float* zhat, const float* z_node, float* v, float* z, void* stream) {
-  if (!p || !flats || !z) return fail(HSX_EINVAL, "null argument");
+int hsx_average_peers(const hsx_plan* p, const float* const* srcs, int32_t n, double divisor, float* out,
+                      void* stream) {
+  if (!p || !srcs || !out) return fail(HSX_EINVAL, "null argument");
   if (n < 1 || n > hsx::kMaxPeers) return fail(HSX_EINVAL, "peer count %d outside [1, %d]", n, hsx::kMaxPeers);
-  if (v && !z_node) return fail(HSX_EINVAL, "v update needs z_node");
-  if (!(divisor > 0.0f)) return fail(HSX_EINVAL, "divisor must be positive");
-  hsx::ElemArgs a = elem_args(p);
-  a.flats.n = n;
+  if (!(divisor > 0.0)) return fail(HSX_EINVAL, "divisor must be positive");
+  hsx::PeerPtrs src;
+  src.n = n;
   for (int j = 0; j < n; ++j) {
-    if (!flats[j]) return fail(HSX_EINVAL, "null peer pointer %d", j);
-    a.flats.p[j] = flats[j];
+    if (!srcs[j] || (reinterpret_cast<uintptr_t>(srcs[j]) & 15)) return fail(HSX_EINVAL, "peer pointer %d null or unaligned", j);
+    src.p[j] = srcs[j];
   }
-  a.zhat = zhat;
-  a.divisor = divisor;
-  a.zn = z_node;
-  a.v = v;
-  a.z = z;
-  hsx::launch_decompact(a, (int)p->stream_items.size(), S(stream));
-  HSX_LAUNCHED("decompact_peers");
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(HSX_EINVAL, "output not 16-byte aligned");
+  // payload size of the last keep-set derivation, read on the device
+  hsx::launch_average(src, p->d_summary + (size_t)p->n_layers * HSX_SUM_COLS, p->arena, divisor, out, S(stream));
+  HSX_LAUNCHED("average_peers");
   return HSX_OK;
 }
 

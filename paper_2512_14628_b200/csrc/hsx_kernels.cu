@@ -1111,72 +1111,36 @@ void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
 
 // K7: z <- zero-filled gather of flat / divisor (+ v <- v + (z_node - z)); the
 // gather streams through the ring: dropped coordinates are zero-filled by
-// cp.async without touching memory. PEERS: the gather reads the same payload
-// index from every leader's flat buffer over NVLink and averages them in rank
-// order in fp64 (the leader all-reduce AVG fused into decompaction,
-// transport.py:453-462), optionally writing the average in payload layout
-// (zhat) for the node's followers.
-template <bool PEERS>
+// cp.async without touching memory.
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
-  constexpr int NB = PEERS ? kMaxPeers + 2 : 3;
-  constexpr int ZS = PEERS ? kMaxPeers : 1;  // slot of z_node (v follows)
+  constexpr int NB = 3;
   extern __shared__ float4 ring[];
   __shared__ int s_rb[kMaxTileRows];
   const Item it = a.items[blockIdx.x];
   const LayerRegs ly(a.layers, it.layer);
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
-  const int np = PEERS ? a.flats.n : 1;
-  const float* src[kMaxPeers];
-#pragma unroll
-  for (int j = 0; j < kMaxPeers; ++j) src[j] = PEERS ? (j < np ? a.flats.p[j] + coff : nullptr) : (j == 0 ? a.flat_in + coff : nullptr);
-  float* __restrict__ zhat = PEERS && a.zhat ? a.zhat + coff : nullptr;
+  const float* __restrict__ flat = a.flat_in + coff;
   const float* __restrict__ ZN = a.v ? a.zn + ly.off : nullptr;
   float* __restrict__ VV = a.v ? a.v + ly.off : nullptr;
   float* __restrict__ ZO = a.z + ly.off;
   const float div = a.divisor;
   auto load = [&](int d, long long e, int4 dd) {
-#pragma unroll
-    for (int j = 0; j < kMaxPeers; ++j) {
-      if (j >= np) break;
-      float* g = reinterpret_cast<float*>(ring_slot<NB>(ring, d, j));
-      cp4z(g + 0, src[j] + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
-      cp4z(g + 1, src[j] + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
-      cp4z(g + 2, src[j] + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
-      cp4z(g + 3, src[j] + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
-    }
+    float* g = reinterpret_cast<float*>(ring_slot<NB>(ring, d, 0));
+    cp4z(g + 0, flat + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
+    cp4z(g + 1, flat + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
+    cp4z(g + 2, flat + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
+    cp4z(g + 3, flat + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
     if (ZN) {
-      cp_quad(ring_slot<NB>(ring, d, ZS), ZN, e, ly.n);
-      cp_quad(ring_slot<NB>(ring, d, ZS + 1), VV, e, ly.n);
+      cp_quad(ring_slot<NB>(ring, d, 1), ZN, e, ly.n);
+      cp_quad(ring_slot<NB>(ring, d, 2), VV, e, ly.n);
     }
   };
-  auto emit = [&](int d, long long e, int4 dd) {
-    float4 zo;
-    if (PEERS) {
-      float4 g = *ring_slot<NB>(ring, d, 0);
-      double s0 = g.x, s1 = g.y, s2 = g.z, s3 = g.w;
-#pragma unroll
-      for (int j = 1; j < kMaxPeers; ++j) {
-        if (j >= np) break;
-        g = *ring_slot<NB>(ring, d, j);
-        s0 = __dadd_rn(s0, (double)g.x); s1 = __dadd_rn(s1, (double)g.y);
-        s2 = __dadd_rn(s2, (double)g.z); s3 = __dadd_rn(s3, (double)g.w);
-      }
-      const double dv = (double)div;
-      zo = make_float4((float)__ddiv_rn(s0, dv), (float)__ddiv_rn(s1, dv), (float)__ddiv_rn(s2, dv),
-                       (float)__ddiv_rn(s3, dv));
-      if (zhat) {
-        if (dd.x >= 0) zhat[dd.x] = zo.x;
-        if (dd.y >= 0) zhat[dd.y] = zo.y;
-        if (dd.z >= 0) zhat[dd.z] = zo.z;
-        if (dd.w >= 0) zhat[dd.w] = zo.w;
-      }
-    } else {
-      zo = *ring_slot<NB>(ring, d, 0);
-      if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
-    }
+  auto emit = [&](int d, long long e) {
+    float4 zo = *ring_slot<NB>(ring, d, 0);
+    if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
     float4 vn;
     if (ZN) {
-      float4 zn = *ring_slot<NB>(ring, d, ZS), vv = *ring_slot<NB>(ring, d, ZS + 1);
+      float4 zn = *ring_slot<NB>(ring, d, 1), vv = *ring_slot<NB>(ring, d, 2);
       vn = make_float4(dual1(vv.x, zn.x, zo.x), dual1(vv.y, zn.y, zo.y), dual1(vv.z, zn.z, zo.z),
                        dual1(vv.w, zn.w, zo.w));
     }
@@ -1201,10 +1165,7 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
                const long long r = tc.row(i);
                load(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
              },
-             [&](int d, int i) {
-               const long long r = tc.row(i);
-               emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
-             });
+             [&](int d, int i) { emit(d, tc.row(i) * ly.L + 4 * tc.j); });
     return;
   }
   const long long nq = (it.end - it.begin + 3) >> 2;
@@ -1215,23 +1176,65 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
              const long long e = it.begin + 4 * (t + (long long)i * kThreads);
              load(d, e, dst4_linear(a, ly, e));
            },
-           [&](int d, int i) {
-             const long long e = it.begin + 4 * (t + (long long)i * kThreads);
-             emit(d, e, PEERS ? dst4_linear(a, ly, e) : make_int4(-1, -1, -1, -1));
-           });
+           [&](int d, int i) { emit(d, it.begin + 4 * (t + (long long)i * kThreads)); });
 }
 
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
-  if (a.flats.n > 0) {
-    const size_t smem = (size_t)kDepth * (kMaxPeers + 2) * kThreads * sizeof(float4);
-    allow_smem(k_decompact<true>, smem);
-    k_decompact<true><<<n_items, kThreads, smem, st>>>(a);
-  } else {
-    const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
-    allow_smem(k_decompact<false>, smem);
-    k_decompact<false><<<n_items, kThreads, smem, st>>>(a);
+  const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
+  allow_smem(k_decompact, smem);
+  k_decompact<<<n_items, kThreads, smem, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+// Leader average over NVLink (the leader all-reduce AVG, transport.py:453-462,
+// as a contiguous stream): out[i] = fp32((sum_j src_j[i], rank order, fp64) / div)
+// for i < the payload size read from the device summary (no host sync). Also the
+// followers' copy of their leader's averaged payload (n = 1, div = 1).
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads) k_average(PeerPtrs src, const long long* __restrict__ total_p,
+                                                      double div, float* __restrict__ out) {
+  const long long total = *total_p;
+  const long long n4 = total >> 2;
+  const long long stride = (long long)gridDim.x * kThreads;
+  constexpr int U = 4;
+  for (long long i0 = blockIdx.x * (long long)kThreads + threadIdx.x; i0 < n4; i0 += stride * U) {
+    float4 x[U][kMaxPeers];
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+      const long long i = i0 + uu * stride;
+#pragma unroll
+      for (int j = 0; j < kMaxPeers; ++j)
+        if (j < src.n && i < n4) x[uu][j] = __ldcg(reinterpret_cast<const float4*>(src.p[j]) + i);
+    }
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+      const long long i = i0 + uu * stride;
+      if (i >= n4) break;
+      double s0 = x[uu][0].x, s1 = x[uu][0].y, s2 = x[uu][0].z, s3 = x[uu][0].w;
+#pragma unroll
+      for (int j = 1; j < kMaxPeers; ++j) {
+        if (j >= src.n) break;
+        s0 = __dadd_rn(s0, (double)x[uu][j].x); s1 = __dadd_rn(s1, (double)x[uu][j].y);
+        s2 = __dadd_rn(s2, (double)x[uu][j].z); s3 = __dadd_rn(s3, (double)x[uu][j].w);
+      }
+      reinterpret_cast<float4*>(out)[i] = make_float4((float)__ddiv_rn(s0, div), (float)__ddiv_rn(s1, div),
+                                                      (float)__ddiv_rn(s2, div), (float)__ddiv_rn(s3, div));
+    }
   }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)kThreads + threadIdx.x; i < total; i += stride) {
+    double s = src.p[0][i];
+    for (int j = 1; j < src.n; ++j) s = __dadd_rn(s, (double)src.p[j][i]);
+    out[i] = (float)__ddiv_rn(s, div);
+  }
+}
+
+void launch_average(const PeerPtrs& src, const long long* total, long long max_elems, double div, float* out,
+                    cudaStream_t st) {
+  if (src.n <= 0 || max_elems <= 0) return;
+  int grid = (int)std::min<long long>(std::max<long long>((max_elems / 4 + kThreads - 1) / kThreads, 1), 148LL * 8);
+  k_average<<<grid, kThreads, 0, st>>>(src, total, div, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -125,8 +125,6 @@ struct ElemArgs {
   const int* __restrict__ rowbase;
   const int* __restrict__ colpos;
   const long long* __restrict__ summary;
-  PeerPtrs flats;       // n > 0: leaders' flat buffers, averaged in rank order (K7)
-  float* zhat;          // K7 peers: averaged payload for the node's followers (may be null)
   float divisor;
 };
 
@@ -158,6 +156,8 @@ struct KeepArgs {
 void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st);
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
+void launch_average(const PeerPtrs& src, const long long* total, long long max_elems, double div, float* out,
+                    cudaStream_t st);
 void launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t st);
 void launch_dual(const float* theta, float* u, const float* zn, long long n, cudaStream_t st);
 void launch_nonzero(const float* t, long long n, uint8_t* out, cudaStream_t st);

@@ -200,18 +200,13 @@ class Plan:
                       ptr(frozen_mask), current_stream())
         del keep
 
-    def decompact_peers(self, flats: list[int], divisor, zhat, z_node, v, z):
-        arr, keep = _lib.ptr_array(flats)
-        with timed("K7_decompact_dual"):
-            _lib.call("hsx_decompact_peers", self._h, arr, len(flats), float(divisor), ptr(zhat),
-                      ptr(z_node), ptr(v), ptr(z), current_stream())
-        del keep
-
-    def decompact_from(self, flat_ptr: int, z_node, v, z):
-        """K7 reading the payload at a (possibly peer-mapped) device pointer."""
-        with timed("K7_decompact_dual"):
-            _lib.call("hsx_decompact_dual", self._h, int(flat_ptr), 1.0, ptr(z_node), ptr(v), ptr(z),
+    def average_peers(self, srcs: list[int], divisor, out, tag="C_avg"):
+        """out[:payload] = rank-order average of the buffers at srcs (payload size on device)."""
+        arr, keep = _lib.ptr_array(srcs)
+        with timed(tag):
+            _lib.call("hsx_average_peers", self._h, arr, len(srcs), float(divisor), ptr(out),
                       current_stream())
+        del keep
 
     def renorm(self, p, s, theta, u, z, v):
         with timed("K1r_renorm"):

@@ -197,12 +197,13 @@ class HSADMMSync:
     def _program_peer(self, k: int):
         """Phases 2-5(u) with the collectives fused into the kernels over NVLink.
 
-        intra sum -> K1 reads the P ranks' theta+u (rank-order fp64 fold);
-        mask union -> K4 reads the M leaders' mask bits; leader average + broadcast ->
-        K7 on leaders reads the M leaders' compact buffers (rank-order fold, / M)
-        and writes the average for its followers, whose K7 reads it from the
-        leader. Barriers order producers before peer readers; sizes and offsets
-        stay on the device, so the step has no host sync until its end.
+        intra sum -> K1 reads the P ranks' theta+u over NVLink (rank-order fp64 fold);
+        mask union -> K4 reads the M leaders' mask bits; leader average -> K8 streams
+        the M leaders' compact buffers (rank-order fold, / M) into the node's payload
+        buffer; intra broadcast -> each follower streams its leader's payload; then
+        every rank decompacts locally (K7). Barriers order producers before peer
+        readers; payload sizes stay on the device, so the step has no host sync
+        until its end. Inter-node traffic stays leader-to-leader (hierarchy kept).
         """
         pl = self.plan
         frozen = self.frozen
@@ -239,21 +240,24 @@ class HSADMMSync:
             self.cache_hits += len(self.prunable)
         zhat = self.p_zhat.tensor if self.P > 1 else None
         if self.is_leader:
-            flat = self.p_flat[k & 1] if self.M > 1 else None
-            pl.compact_dual(self.theta, self.u, self.z_node, self.v, flat.tensor if flat else self.flat)
             if self.M > 1:
+                flat = self.p_flat[k & 1]
+                pl.compact_dual(self.theta, self.u, self.z_node, self.v, flat.tensor)
                 yield Barrier(self.inter, "z_sync", k)
-                pl.decompact_peers(flat.peer_ptrs(), float(self.M), zhat, self.z_node, self.v, self.z)
-            elif zhat is not None:
-                pl.decompact_peers([self.flat.data_ptr()], 1.0, zhat, self.z_node, self.v, self.z)
+                # leader average over NVLink into the node's payload buffer
+                dst = zhat if zhat is not None else self.flat
+                pl.average_peers(flat.peer_ptrs(), float(self.M), dst, tag="K8_leader_avg")
             else:
-                pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
+                dst = zhat if zhat is not None else self.flat
+                pl.compact_dual(self.theta, self.u, self.z_node, self.v, dst)
         else:
             pl.dual_intra(self.theta, self.u, self.z_node)
         if self.P > 1:
             yield Barrier(self.intra, "zhat_bcast", k)
-            if not self.is_leader:
-                pl.decompact_from(self.p_zhat.peer_ptrs()[0], self.z_node, self.v, self.z)
+            if not self.is_leader:  # the intra broadcast: a contiguous read of the leader's payload
+                pl.average_peers([self.p_zhat.peer_ptrs()[0]], 1.0, self.flat, tag="K8_zhat_read")
+                dst = self.flat
+        pl.decompact_dual(dst, 1.0, self.z_node, self.v, self.z)
         if ev is not None:
             ev.synchronize()
             self._after_keep_sets()

@@ -99,13 +99,17 @@ def replica_check(topo, rank, world, transport):
 
 
 def main():
+    import faulthandler
+
+    faulthandler.dump_traceback_later(int(os.environ.get("MP_PARITY_DUMP_S", "240")), exit=False)
     topo = H.Topology.parse(sys.argv[1])
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
-        for transport in ("nccl", "peer"):
+        for transport in os.environ.get("MP_PARITY_TRANSPORTS", "nccl,peer").split(","):
             worst = golden_check(topo, rank, transport)
+            print(f"rank {rank} golden {transport} done", file=sys.stderr, flush=True)
             ratio = replica_check(topo, rank, world, transport)
             dist.barrier()
             if rank == 0:

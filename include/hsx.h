@@ -209,6 +209,14 @@ int hsx_mask_or_ptrs(const uint32_t* const* srcs, int32_t n, int64_t words, uint
 int hsx_average_peers(const hsx_plan* plan, const float* const* srcs, int32_t n, double divisor,
                       float* out, void* stream);
 
+/* Device-side barrier of a group over NVLink: flags[i] is member i's int32 flag
+ * array (peer-mapped, indexed by world rank), slots[i] member i's world rank,
+ * me this rank's member index, epoch a per-group counter identical on all
+ * members (incremented by the caller for every barrier). Enqueued on `stream`;
+ * traps after ~10 s if a member never arrives. */
+int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
+                      void* stream);
+
 /* ---- mask helpers for the per-tensor API -------------------------------------- */
 /* out[i] = |t[i]| > 0  (extract_mask, sparsity.py:113-115) */
 int hsx_nonzero_u8(const float* t, int64_t n, uint8_t* out, void* stream);

@@ -72,6 +72,7 @@ SIGNATURES = {
     "hsx_mask_or_ptrs": (C.c_int, [VP, I32, I64, VP, VP]),
     "hsx_candidate_renorm_peers": (C.c_int, [P, I32, VP, I32, VP, VP, VP]),
     "hsx_average_peers": (C.c_int, [P, VP, I32, F64, VP, VP]),
+    "hsx_group_barrier": (C.c_int, [VP, VP, I32, I32, I32, VP]),
 }
 
 _lib = None

@@ -775,6 +775,23 @@ int hsx_average_peers(const hsx_plan* p, const float* const* srcs, int32_t n, do
   return HSX_OK;
 }
 
+int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
+                      void* stream) {
+  if (!flags || !slots || n < 1 || n > 32 || me < 0 || me >= n) return fail(HSX_EINVAL, "bad barrier arguments");
+  hsx::BarrierArgs b;
+  b.n = n;
+  b.me = me;
+  b.epoch = epoch;
+  for (int i = 0; i < n; ++i) {
+    if (!flags[i]) return fail(HSX_EINVAL, "null flag pointer %d", i);
+    b.flags[i] = flags[i];
+    b.slots[i] = slots[i];
+  }
+  hsx::launch_barrier(b, S(stream));
+  HSX_LAUNCHED("group_barrier");
+  return HSX_OK;
+}
+
 int hsx_nonzero_u8(const float* t, int64_t n, uint8_t* out, void* stream) {
   if ((!t || !out) && n > 0) return fail(HSX_EINVAL, "null argument");
   hsx::launch_nonzero(t, n, out, S(stream));

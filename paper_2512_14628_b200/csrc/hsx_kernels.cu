@@ -1238,6 +1238,39 @@ void launch_average(const PeerPtrs& src, const long long* total, long long max_e
 }
 
 // ---------------------------------------------------------------------------
+// Group barrier over NVLink: member i publishes `epoch` into slot `slots[me]` of
+// every other member's flag array (release, system scope) and waits until its
+// own slots of all other members reach `epoch` (acquire). Stream-ordered: the
+// kernels before it have completed, the kernels after it read peers' buffers.
+// A member that never arrives traps after ~10 s instead of hanging the GPU.
+// ---------------------------------------------------------------------------
+
+__global__ void k_barrier(BarrierArgs b) {
+  const int i = threadIdx.x;
+  if (i < b.n && i != b.me) {
+    __threadfence_system();
+    int* dst = b.flags[i] + b.slots[b.me];
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(dst), "r"(b.epoch) : "memory");
+  }
+  __syncwarp();
+  if (i < b.n && i != b.me) {
+    const int* src = b.flags[b.me] + b.slots[i];
+    const long long t0 = clock64();
+    int v;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(src) : "memory");
+      if (v - b.epoch >= 0) break;
+      if (clock64() - t0 > (1LL << 34)) __trap();
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
+}
+
+void launch_barrier(const BarrierArgs& b, cudaStream_t st) { k_barrier<<<1, 32, 0, st>>>(b); }
+
+// ---------------------------------------------------------------------------
 // K0 send = theta + u; K6f u += theta - z_node (arena-wide streaming)
 // ---------------------------------------------------------------------------
 

@@ -156,6 +156,12 @@ struct KeepArgs {
 void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st);
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
+struct BarrierArgs {
+  int* flags[32];  // members' flag arrays (peer-mapped), member order
+  int slots[32];   // members' slot indices (their world ranks)
+  int n, me, epoch;
+};
+void launch_barrier(const BarrierArgs& b, cudaStream_t st);
 void launch_average(const PeerPtrs& src, const long long* total, long long max_elems, double div, float* out,
                     cudaStream_t st);
 void launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t st);

@@ -114,16 +114,19 @@ class HSADMMSync:
         words = max(pl.mask_words, 1)
         self.p_send = self.p_umask = self.p_zhat = self.p_lmask = None
         self.p_flat = None
+        # every rank allocates the same sequence (the allocation is collective over
+        # all ranks); followers leave the leader-group buffers unused
         if self.P > 1:
             self.p_send = cl.shared(self.rank, self.intra, "send", pl.arena, torch.float32, dev)
             self.p_umask = cl.shared(self.rank, self.intra, "umask", words, torch.int32, dev)
             self.p_zhat = cl.shared(self.rank, self.intra, "zhat", pl.arena, torch.float32, dev)
-        if self.is_leader and self.M > 1:
-            self.p_lmask = cl.shared(self.rank, self.inter, "lmask", words, torch.int32, dev)
+        if self.M > 1:
+            lmask = cl.shared(self.rank, self.inter, "lmask", words, torch.int32, dev)
             # double-buffered by iteration parity: a leader may start the next
             # compaction while another still averages this one
-            self.p_flat = [cl.shared(self.rank, self.inter, f"flat{b}", pl.arena, torch.float32, dev)
-                           for b in (0, 1)]
+            flat = [cl.shared(self.rank, self.inter, f"flat{b}", pl.arena, torch.float32, dev) for b in (0, 1)]
+            if self.is_leader:
+                self.p_lmask, self.p_flat = lmask, flat
 
     # -- state I/O ---------------------------------------------------------------
     def load(self, **arrays) -> None:

@@ -455,8 +455,12 @@ class DistCluster:
         self._handles["leaders"] = dist.new_group(list(self._leaders.members))
         self._handles["global"] = dist.group.WORLD
         self._avg = dist.get_backend() == "nccl"
-        self._symm = {}      # group id -> symmetric-memory handle used for barriers
         self.supports_peer = self._avg and self._symm_available()
+        self._epoch: dict[str, int] = {}
+        self._flags = None
+        if self.supports_peer:
+            # one world-symmetric int32 flag per (receiver, sender) for group barriers
+            self._flags = self._world_buffer(topology.world_size, "int32")
 
     @staticmethod
     def _symm_available() -> bool:
@@ -466,16 +470,46 @@ class DistCluster:
             return False
         return True
 
-    def shared(self, rank: int, group: ProcessGroup, key: str, numel: int, dtype, device) -> SharedBuffer:
-        """Collective over ``group``: symmetric-memory buffer mapped on every member."""
+    def _world_buffer(self, numel: int, dtype, device=None):
+        """(tensor, world pointers): symmetric memory rendezvoused over the WORLD group.
+
+        Every rank allocates every shared buffer in the same order — torch's
+        symmetric-memory rendezvous must see the same sequence on all ranks — and
+        sub-groups just read their members' entries."""
+        import torch
+        import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
 
-        t = symm.empty(max(int(numel), 1), dtype=dtype, device=device)
+        dt = getattr(torch, dtype) if isinstance(dtype, str) else dtype
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        t = symm.empty(max(int(numel), 1), dtype=dt, device=dev)
         t.zero_()
-        h = symm.rendezvous(t, self._handles[group.id])
-        self._symm.setdefault(group.id, h)
-        ptrs = [int(p) for p in h.buffer_ptrs]
-        return SharedBuffer(t, lambda: ptrs)
+        h = symm.rendezvous(t, dist.group.WORLD)
+        return t, [int(p) for p in h.buffer_ptrs], h
+
+    def shared(self, rank: int, group: ProcessGroup, key: str, numel: int, dtype, device) -> SharedBuffer:
+        """Collective over the WORLD (all ranks, same order): a buffer mapped on every rank;
+        ``peer_ptrs()`` are ``group``'s members' copies in member order."""
+        t, ptrs, _ = self._world_buffer(numel, dtype, device)
+        members = [ptrs[m] for m in group.members]
+        return SharedBuffer(t, lambda: members)
+
+    def barrier(self, group: ProcessGroup) -> None:
+        """Device-side barrier of ``group`` over NVLink flags (stream-ordered)."""
+        from . import _lib
+        from .plan import current_stream
+
+        _, ptrs, _ = self._flags
+        epoch = self._epoch.get(group.id, 0) + 1
+        self._epoch[group.id] = epoch
+        members = list(group.members)
+        fl, keep1 = _lib.ptr_array([ptrs[m] for m in members])
+        import ctypes as C
+
+        slots = (C.c_int32 * len(members))(*members)
+        _lib.call("hsx_group_barrier", fl, C.cast(slots, C.c_void_p), len(members), members.index(self.rank),
+                  epoch, current_stream())
+        del keep1
 
     def log(self, entry: LedgerEntry) -> None:
         self.ledger.append(entry)
@@ -503,7 +537,7 @@ class DistCluster:
         g = len(req.group.members)
         if isinstance(req, Barrier):
             if g > 1:
-                self._symm[req.group.id].barrier(channel=0, timeout_ms=60000)
+                self.barrier(req.group)
             return None
         if isinstance(req, Broadcast):
             if g > 1:

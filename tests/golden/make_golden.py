@@ -204,11 +204,11 @@ def gen_e2e(num_nodes, per_node, seed=3):
     sched = PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False)
     solver = SolverConfig()
     out = {"meta": np.array([num_nodes, per_node, E2E_ITERS, E2E_T_FREEZE])}
-    for n in names:
-        out[f"p0/{n}"] = params0[n]
+    for n in names:  # inputs are fp32-representable: stored as float32 (exact)
+        out[f"p0/{n}"] = params0[n].astype(np.float32)
         for k in range(1, E2E_ITERS + 1):
             for r in range(world):
-                out[f"theta/{k}/{r}/{n}"] = thetas[(r, k)][n]
+                out[f"theta/{k}/{r}/{n}"] = thetas[(r, k)][n].astype(np.float32)
     saved = (ref_consensus.batch_rng, ref_consensus.proximal_sgd)
     try:
         ref_consensus.batch_rng = lambda s, rank, k: (rank, k)
@@ -254,6 +254,6 @@ if __name__ == "__main__":
     gen_shrinkage()
     gen_bucketize()
     gen_candidate()
-    for m, p in [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4)]:
+    for m, p in [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (1, 4), (4, 1)]:
         gen_e2e(m, p)
     print("golden fixtures written to", HERE)

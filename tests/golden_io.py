@@ -23,7 +23,7 @@ E2E_LAYERS = [
     ("fc.b", "fc", (1, 10), []),
 ]
 E2E_RHO1, E2E_RHO2, E2E_WD = 1.5e-3, 1.5e-4, 1e-4
-E2E_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4)]
+E2E_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (1, 4), (4, 1)]
 
 
 def load(name):
@@ -70,10 +70,10 @@ class E2E:
         self.names = [n for n, *_ in E2E_LAYERS]
 
     def p0(self):
-        return {n: self.d[f"p0/{n}"] for n in self.names}
+        return {n: self.d[f"p0/{n}"].astype(np.float64) for n in self.names}
 
     def theta(self, k, r):
-        return {n: self.d[f"theta/{k}/{r}/{n}"] for n in self.names}
+        return {n: self.d[f"theta/{k}/{r}/{n}"].astype(np.float64) for n in self.names}
 
     def u(self, k, r):
         return {n: self.d[f"u/{k}/{r}/{n}"] for n in self.names}

@@ -209,6 +209,13 @@ int hsx_mask_or_ptrs(const uint32_t* const* srcs, int32_t n, int64_t words, uint
 int hsx_average_peers(const hsx_plan* plan, const float* const* srcs, int32_t n, double divisor,
                       float* out, void* stream);
 
+/* Reduce-scatter / all-gather halves over mapped pointers for groups of >= 3
+ * ranks: part >= 0 writes slice `part` of the rank-order average (divisor) of
+ * srcs into out; part < 0 gathers every slice from its owner srcs[owner] into
+ * out. The range is the plan's arena (payload == 0) or the payload size of the
+ * last keep-set derivation read on the device (payload != 0). */
+int hsx_slices_peers(const hsx_plan* plan, const float* const* srcs, int32_t n, int32_t part,
+                     double divisor, int32_t payload, float* out, void* stream);
 /* Device-side barrier of a group over NVLink: flags[i] is member i's int32 flag
  * array (peer-mapped, indexed by world rank), slots[i] member i's world rank,
  * me this rank's member index, epoch a per-group counter identical on all

@@ -73,6 +73,7 @@ SIGNATURES = {
     "hsx_candidate_renorm_peers": (C.c_int, [P, I32, VP, I32, VP, VP, VP]),
     "hsx_average_peers": (C.c_int, [P, VP, I32, F64, VP, VP]),
     "hsx_group_barrier": (C.c_int, [VP, VP, I32, I32, I32, VP]),
+    "hsx_slices_peers": (C.c_int, [P, VP, I32, I32, F64, I32, VP, VP]),
 }
 
 _lib = None

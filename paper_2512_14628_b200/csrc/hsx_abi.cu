@@ -775,6 +775,25 @@ int hsx_average_peers(const hsx_plan* p, const float* const* srcs, int32_t n, do
   return HSX_OK;
 }
 
+int hsx_slices_peers(const hsx_plan* p, const float* const* srcs, int32_t n, int32_t part, double divisor,
+                     int32_t payload, float* out, void* stream) {
+  if (!p || !srcs || !out) return fail(HSX_EINVAL, "null argument");
+  if (n < 1 || n > hsx::kMaxPeers) return fail(HSX_EINVAL, "peer count %d outside [1, %d]", n, hsx::kMaxPeers);
+  if (part >= n) return fail(HSX_EINVAL, "slice %d of %d", part, n);
+  if (!(divisor > 0.0)) return fail(HSX_EINVAL, "divisor must be positive");
+  hsx::PeerPtrs src;
+  src.n = n;
+  for (int j = 0; j < n; ++j) {
+    if (!srcs[j] || (reinterpret_cast<uintptr_t>(srcs[j]) & 15)) return fail(HSX_EINVAL, "peer pointer %d null or unaligned", j);
+    src.p[j] = srcs[j];
+  }
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(HSX_EINVAL, "output not 16-byte aligned");
+  const long long* total_p = payload ? p->d_summary + (size_t)p->n_layers * HSX_SUM_COLS : nullptr;
+  hsx::launch_slices(src, total_p, p->arena, p->arena, part, divisor, out, S(stream));
+  HSX_LAUNCHED("slices_peers");
+  return HSX_OK;
+}
+
 int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
                       void* stream) {
   if (!flags || !slots || n < 1 || n > 32 || me < 0 || me >= n) return fail(HSX_EINVAL, "bad barrier arguments");

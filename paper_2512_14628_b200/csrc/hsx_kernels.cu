@@ -1238,6 +1238,66 @@ void launch_average(const PeerPtrs& src, const long long* total, long long max_e
 }
 
 // ---------------------------------------------------------------------------
+// Slice collectives over NVLink for groups of >= 3 ranks (reduce-scatter +
+// all-gather move 2(n-1)/n of the buffer per rank instead of (n-1)):
+//   part >= 0: out[i] = fp32((sum_j src_j[i], rank order, fp64) / div) on slice
+//              `part` of [0, total) (slices of ceil(total / n) rounded to 32);
+//   part <  0: out[i] = src_{owner(i)}[i] on [0, total) (gather the slices).
+// total is a host value or, when total_p != NULL, read on the device.
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads) k_slices(PeerPtrs src, const long long* __restrict__ total_p,
+                                                     long long total_h, int part, double div,
+                                                     float* __restrict__ out) {
+  const long long total = total_p ? *total_p : total_h;
+  const long long slice = ((total + src.n - 1) / src.n + 31) / 32 * 32;
+  long long b = 0, e = total;
+  if (part >= 0) {
+    b = std::min<long long>((long long)part * slice, total);
+    e = std::min<long long>(b + slice, total);
+  }
+  const long long stride = (long long)gridDim.x * kThreads;
+  const long long q0 = b >> 2, q1 = e >> 2;  // slice bounds are multiples of 32
+  for (long long q = q0 + blockIdx.x * (long long)kThreads + threadIdx.x; q < q1; q += stride) {
+    float4 r;
+    if (part >= 0) {
+      float4 x = __ldcg(reinterpret_cast<const float4*>(src.p[0]) + q);
+      double s0 = x.x, s1 = x.y, s2 = x.z, s3 = x.w;
+      for (int j = 1; j < src.n; ++j) {
+        x = __ldcg(reinterpret_cast<const float4*>(src.p[j]) + q);
+        s0 = __dadd_rn(s0, (double)x.x); s1 = __dadd_rn(s1, (double)x.y);
+        s2 = __dadd_rn(s2, (double)x.z); s3 = __dadd_rn(s3, (double)x.w);
+      }
+      r = make_float4((float)__ddiv_rn(s0, div), (float)__ddiv_rn(s1, div), (float)__ddiv_rn(s2, div),
+                      (float)__ddiv_rn(s3, div));
+    } else {
+      const int owner = (int)std::min<long long>((4 * q) / slice, src.n - 1);
+      r = __ldcg(reinterpret_cast<const float4*>(src.p[owner]) + q);
+    }
+    reinterpret_cast<float4*>(out)[q] = r;
+  }
+  // tail of the last slice (total not a multiple of 4)
+  for (long long i = 4 * q1 + blockIdx.x * (long long)kThreads + threadIdx.x; i < e; i += stride) {
+    if (part >= 0) {
+      double sum = src.p[0][i];
+      for (int j = 1; j < src.n; ++j) sum = __dadd_rn(sum, (double)src.p[j][i]);
+      out[i] = (float)__ddiv_rn(sum, div);
+    } else {
+      const int owner = (int)std::min<long long>(i / slice, src.n - 1);
+      out[i] = src.p[owner][i];
+    }
+  }
+}
+
+void launch_slices(const PeerPtrs& src, const long long* total_p, long long total_h, long long max_elems,
+                   int part, double div, float* out, cudaStream_t st) {
+  if (src.n <= 0 || max_elems <= 0) return;
+  const long long span = part >= 0 ? (max_elems + src.n - 1) / src.n : max_elems;
+  int grid = (int)std::min<long long>(std::max<long long>((span / 4 + kThreads - 1) / kThreads, 1), 148LL * 8);
+  k_slices<<<grid, kThreads, 0, st>>>(src, total_p, total_h, part, div, out);
+}
+
+// ---------------------------------------------------------------------------
 // Group barrier over NVLink: member i publishes `epoch` into slot `slots[me]` of
 // every other member's flag array (release, system scope) and waits until its
 // own slots of all other members reach `epoch` (acquire). Stream-ordered: the

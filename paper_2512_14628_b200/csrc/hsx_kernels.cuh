@@ -156,6 +156,8 @@ struct KeepArgs {
 void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st);
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
+void launch_slices(const PeerPtrs& src, const long long* total_p, long long total_h, long long max_elems,
+                   int part, double div, float* out, cudaStream_t st);
 struct BarrierArgs {
   int* flags[32];  // members' flag arrays (peer-mapped), member order
   int slots[32];   // members' slot indices (their world ranks)

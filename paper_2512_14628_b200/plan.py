@@ -208,6 +208,14 @@ class Plan:
                       current_stream())
         del keep
 
+    def slices_peers(self, srcs: list[int], part: int, divisor, payload: bool, out, tag):
+        """part >= 0: slice ``part`` of the rank-order average; part < 0: gather all slices."""
+        arr, keep = _lib.ptr_array(srcs)
+        with timed(tag):
+            _lib.call("hsx_slices_peers", self._h, arr, len(srcs), int(part), float(divisor), int(payload),
+                      ptr(out), current_stream())
+        del keep
+
     def renorm(self, p, s, theta, u, z, v):
         with timed("K1r_renorm"):
             _lib.call("hsx_candidate_renorm", self._h, p, ptr(s), ptr(theta), ptr(u), ptr(z), ptr(v),

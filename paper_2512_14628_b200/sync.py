@@ -120,13 +120,18 @@ class HSADMMSync:
             self.p_send = cl.shared(self.rank, self.intra, "send", pl.arena, torch.float32, dev)
             self.p_umask = cl.shared(self.rank, self.intra, "umask", words, torch.int32, dev)
             self.p_zhat = cl.shared(self.rank, self.intra, "zhat", pl.arena, torch.float32, dev)
+        self.p_ssum = self.p_favg = None
+        if self.P > 2:   # reduce-scatter + all-gather of the intra sum
+            self.p_ssum = cl.shared(self.rank, self.intra, "ssum", pl.arena, torch.float32, dev)
         if self.M > 1:
             lmask = cl.shared(self.rank, self.inter, "lmask", words, torch.int32, dev)
             # double-buffered by iteration parity: a leader may start the next
             # compaction while another still averages this one
             flat = [cl.shared(self.rank, self.inter, f"flat{b}", pl.arena, torch.float32, dev) for b in (0, 1)]
+            favg = (cl.shared(self.rank, self.inter, "favg", pl.arena, torch.float32, dev)
+                    if self.M > 2 else None)   # reduce-scatter + all-gather of the leader average
             if self.is_leader:
-                self.p_lmask, self.p_flat = lmask, flat
+                self.p_lmask, self.p_flat, self.p_favg = lmask, flat, favg
 
     # -- state I/O ---------------------------------------------------------------
     def load(self, **arrays) -> None:
@@ -212,16 +217,28 @@ class HSADMMSync:
         frozen = self.frozen
         dynamic = not frozen and bool(self.prunable)
         fmask = self.masks if (frozen and self.prunable) else None
-        if self.P > 1:
+        s_local, peers = None, None
+        if self.P > 2:
+            # reduce-scatter (my slice of the rank-order sum) + all-gather, then K1 on S
             pl.pack_theta_u(self.theta, self.u, self.p_send.tensor)
             yield Barrier(self.intra, "theta_u", k)
-            pl.candidate_peers(self.p_send.peer_ptrs(), self.z, self.v, self.z_node, frozen_mask=fmask)
+            me = self.intra.members.index(self.rank)
+            pl.slices_peers(self.p_send.peer_ptrs(), me, 1.0, False, self.p_ssum.tensor, "K8_intra_rs")
+            yield Barrier(self.intra, "theta_u_ag", k)
+            pl.slices_peers(self.p_ssum.peer_ptrs(), -1, 1.0, False, self.sum, "K8_intra_ag")
+            s_local = self.sum
+            pl.candidate(s_local, None, None, self.z, self.v, self.z_node, frozen_mask=fmask)
+        elif self.P == 2:
+            # the intra sum fused into K1: theta+u of both ranks read over NVLink
+            pl.pack_theta_u(self.theta, self.u, self.p_send.tensor)
+            yield Barrier(self.intra, "theta_u", k)
+            peers = self.p_send.peer_ptrs()
+            pl.candidate_peers(peers, self.z, self.v, self.z_node, frozen_mask=fmask)
         else:
             pl.candidate(None, self.theta, self.u, self.z, self.v, self.z_node, frozen_mask=fmask)
         if dynamic:
             local = self.p_lmask.tensor if self.p_lmask is not None else self.local_mask
-            pl.project_all(None, self.theta, self.u, self.z, self.v, self.z_node, local,
-                           peers=self.p_send.peer_ptrs() if self.P > 1 else None)
+            pl.project_all(s_local, self.theta, self.u, self.z, self.v, self.z_node, local, peers=peers)
         if k % self.settings.sync_period != 0:
             pl.dual_intra(self.theta, self.u, self.z_node)
             return None
@@ -249,7 +266,13 @@ class HSADMMSync:
                 yield Barrier(self.inter, "z_sync", k)
                 # leader average over NVLink into the node's payload buffer
                 dst = zhat if zhat is not None else self.flat
-                pl.average_peers(flat.peer_ptrs(), float(self.M), dst, tag="K8_leader_avg")
+                if self.M > 2:
+                    me = self.inter.members.index(self.rank)
+                    pl.slices_peers(flat.peer_ptrs(), me, float(self.M), True, self.p_favg.tensor, "K8_leader_rs")
+                    yield Barrier(self.inter, "z_sync_ag", k)
+                    pl.slices_peers(self.p_favg.peer_ptrs(), -1, 1.0, True, dst, "K8_leader_ag")
+                else:
+                    pl.average_peers(flat.peer_ptrs(), float(self.M), dst, tag="K8_leader_avg")
             else:
                 dst = zhat if zhat is not None else self.flat
                 pl.compact_dual(self.theta, self.u, self.z_node, self.v, dst)

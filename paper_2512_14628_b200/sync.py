@@ -259,6 +259,18 @@ class HSADMMSync:
         elif self.is_leader and self.prunable:
             self.cache_hits += len(self.prunable)
         zhat = self.p_zhat.tensor if self.P > 1 else None
+        if self.M == 1:
+            # one node: the leader "average" is the identity and every rank holds the
+            # same z_node and v, so each rank compacts and decompacts locally (the
+            # result is bitwise what the intra broadcast would deliver)
+            pl.compact_dual(self.theta, self.u, self.z_node, self.v, self.flat)
+            pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
+            if ev is not None:
+                ev.synchronize()
+                self._after_keep_sets()
+            if self.is_leader:
+                self._log_zsync(k)
+            return (yield from self._finish_dynamic(k, dynamic))
         if self.is_leader:
             if self.M > 1:
                 flat = self.p_flat[k & 1]
@@ -289,14 +301,19 @@ class HSADMMSync:
             self._after_keep_sets()
         if self.is_leader:
             self._log_zsync(k)
+        return (yield from self._finish_dynamic(k, dynamic))
+
+    def _finish_dynamic(self, k: int, dynamic: bool):
+        """masks <- union; freeze + seal (consensus.py:600-606)."""
         if dynamic:
-            mask_or_ptrs([self.union.data_ptr()], pl.mask_words, self.masks)
+            mask_or_ptrs([self.union.data_ptr()], self.plan.mask_words, self.masks)
         if dynamic and freeze_check(k, self.settings.t_freeze, self.drift_history,
                                     self.settings.drift_window):
             self.frozen = True
             if self.is_leader:
                 self.cache_hits += len(self.prunable)
         return None
+        yield  # pragma: no cover  (generator)
 
     def _program_nccl(self, k: int):
         pl = self.plan

@@ -243,7 +243,13 @@ class HSADMMSync:
             pl.dual_intra(self.theta, self.u, self.z_node)
             return None
         ev = None
-        if dynamic:
+        if dynamic and self.M == 1:
+            # one node: every rank's local mask is the node's (identical z_node), so the
+            # union needs no exchange
+            mask_or_ptrs([local.data_ptr()], pl.mask_words, self.union)
+            pl.keep_sets(self.union, self.masks)
+            ev = pl.keep_sets_fetch_async()
+        elif dynamic:
             words = pl.mask_words
             if self.is_leader:
                 target = self.p_umask.tensor if self.P > 1 else self.union

@@ -126,7 +126,10 @@ int hsx_candidate_renorm(hsx_plan* plan, int32_t pass, const float* sum, const f
 
 /* ---- K2: group norms -> top-k keep flags -----------------------------------
  * norms = sqrt(sum of partials); keep the `keep` largest, lower index on ties
- * (SparsityConstraint.resolve + _kept_group_indices, sparsity.py:53-68). */
+ * (SparsityConstraint.resolve + _kept_group_indices, sparsity.py:53-68).
+ * Layers with <= 1024 groups are selected inside the candidate launch (tail of
+ * the layer's last tile); this call completes the others. Always call it after
+ * hsx_candidate / hsx_candidate_renorm of the same pass. */
 int hsx_select(hsx_plan* plan, int32_t pass, void* stream);
 /* copy pass `pass` norms (fp64) / keep flags (uint8) to caller device buffers
  * of hsx_plan_group_total(pass) entries; either may be NULL. */
@@ -138,6 +141,21 @@ int hsx_read_groups(const hsx_plan* plan, int32_t pass, double* norms, uint8_t* 
  * packed mask bit  kept && z != 0  (project, sparsity.py:71-94; extract_mask
  * :113-115; update_node_consensus dynamic branch, consensus.py:181-182). */
 int hsx_project(hsx_plan* plan, float* z_node, uint32_t* local_mask, void* stream);
+/* K3 + keep sets for one node (M == 1: the union is the local mask): writes
+ * the mask bits into `mask` and leaves the keep sets, payload sizes,
+ * flat-buffer offsets and drift / popcount columns exactly as hsx_project
+ * followed by hsx_keep_sets(mask, prev_mask) would (derive_keep_sets,
+ * shrinkage.py:45-58; mask_drift numerator, sparsity.py:118-122).
+ * With hsx_plan_set_single_node(plan, 1) the last selection pass has already
+ * derived them from the group flags (the mask is the rectangle of kept rows x
+ * kept columns unless a kept element is exactly zero); this call then only
+ * checks for kept zeros and re-derives such layers from their bits. In that
+ * mode prev_mask must be the `mask` of the previous call (drift is counted
+ * against the previous rectangle). */
+int hsx_project_keep_sets(hsx_plan* plan, float* z_node, uint32_t* mask, const uint32_t* prev_mask,
+                          void* stream);
+/* Single-node mode on / off (default off): see hsx_project_keep_sets. */
+int hsx_plan_set_single_node(hsx_plan* plan, int32_t on);
 
 /* ---- K4: leader mask union  out = OR_m gathered[m]  (transport.py:455-457) -- */
 int hsx_mask_or(const uint32_t* gathered, int32_t n_ranks, int64_t words, uint32_t* out,

@@ -54,6 +54,8 @@ SIGNATURES = {
     "hsx_select": (C.c_int, [P, I32, VP]),
     "hsx_read_groups": (C.c_int, [P, I32, VP, VP, VP]),
     "hsx_project": (C.c_int, [P, VP, VP, VP]),
+    "hsx_project_keep_sets": (C.c_int, [P, VP, VP, VP, VP]),
+    "hsx_plan_set_single_node": (C.c_int, [P, C.c_int32]),
     "hsx_mask_or": (C.c_int, [VP, I32, I64, VP, VP]),
     "hsx_keep_sets": (C.c_int, [P, VP, VP, VP]),
     "hsx_keep_sets_fetch": (C.c_int, [P, VP, VP]),

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -49,7 +50,7 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 constexpr long long kAlign = 32;        // arena layer alignment in elements (128 B)
 constexpr int kSubElems = 4096;         // target elements per shared-memory sub-tile
 constexpr int hsx_tile_quads = 64;      // quad tiles: rows x 64 column quads (hsx_kernels.cu)
-// rows per quad tile (K1; K3/K6/K7); HSX_CAND_TILE_ROWS / HSX_STREAM_TILE_ROWS
+// rows per quad tile (K1; K6/K7; K3); HSX_CAND_TILE_ROWS / HSX_STREAM_TILE_ROWS / HSX_PROJ_TILE_ROWS
 // override them for tuning runs (multiples of 4, <= kMaxTileRows = 128)
 int tile_rows_env(const char* name, int dflt) {
   const char* v = std::getenv(name);
@@ -57,7 +58,17 @@ int tile_rows_env(const char* name, int dflt) {
   if (r < 4 || r > 128 || (r & 3)) r = dflt;
   return r;
 }
+int env_flag(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+// select_layer's shared memory: G u64 keys + G flag bytes, then the structured
+// keep-set derivation of the layer (one node)
+size_t select_need(const DevLayer& ly, int q) {
+  return hsx::select_smem_bytes(ly.G[q]) + hsx::structured_smem_bytes(ly.rows, ly.L, ly.cin);
+}
 constexpr long long kItemElems = 8192;  // elements per streaming work item
+constexpr long long kProjElems = 1024;  // K3 items of layers without row-quad tiles (32 words)
 constexpr long long kWordItem = 512;    // mask words per keep-mark item
 constexpr int kMaxSelectGroups = 8192;  // bitonic capacity (96 KB smem)
 constexpr size_t kMaxSmem = 200 * 1024;
@@ -95,33 +106,39 @@ struct hsx_plan {
   std::vector<DevLayer> layers;
   std::vector<Item> cand_dyn, elem_items, stream_items, proj_items, word_items;
   std::vector<int> pass_list[hsx::kMaxPasses];
+  std::vector<int> sel_list[hsx::kMaxPasses];  // layers whose pass-q selection needs the K2 launch
   std::vector<int> prunable;
-  size_t cand_smem = 0, select_smem[hsx::kMaxPasses] = {0, 0, 0}, mark_smem = 0;
+  size_t cand_smem = 0, select_smem[hsx::kMaxPasses] = {0, 0, 0}, mark_smem = 0, fixup_smem = 0;
+  int single_node = 0;  // structured keep sets in the selection tail (M == 1)
   int sqcap = 0;
   // device
   DevLayer* d_layers = nullptr;
   Item *d_cand = nullptr, *d_elem = nullptr, *d_stream = nullptr, *d_proj = nullptr, *d_word = nullptr;
   unsigned int* d_layer_done = nullptr;
-  int* d_pass[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
+  unsigned int* d_cand_done = nullptr;
+  unsigned long long* d_acc = nullptr;
+  uint8_t *d_rk_prev = nullptr, *d_ck_prev = nullptr;
+  int *d_irr = nullptr, *d_irr_any = nullptr;
+  int* d_sel[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
   double* d_partials[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   double* d_norms[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   uint8_t* d_flags[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   uint8_t *d_oflag = nullptr, *d_iflag = nullptr;
   int *d_pos_out = nullptr, *d_pos_in = nullptr;
-  hsx::Maps maps = {nullptr, nullptr, nullptr, nullptr};
+  hsx::Maps maps = {nullptr, nullptr};
   long long* d_summary = nullptr;
   unsigned int* d_done = nullptr;
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
-                    d_pos_out, d_pos_in, d_summary, d_done, maps.rowkeep, maps.colkeep,
+    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+                    d_pos_out, d_pos_in, d_summary, d_done,
                     maps.rowbase, maps.colpos};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (int i = 0; i < hsx::kMaxPasses; ++i) {
-      if (d_pass[i]) cudaFree(d_pass[i]);
+      if (d_sel[i]) cudaFree(d_sel[i]);
       if (d_partials[i]) cudaFree(d_partials[i]);
       if (d_norms[i]) cudaFree(d_norms[i]);
       if (d_flags[i]) cudaFree(d_flags[i]);
@@ -146,7 +163,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   p->n_layers = n;
   long long off = 0, mword = 0, okeep = 0, ikeep = 0, cpoff = 0;
   long long goff[hsx::kMaxPasses] = {0, 0, 0}, poff[hsx::kMaxPasses] = {0, 0, 0};
-  int sqcap = 0, quadcap = 0, lmax = 1024;
+  int sqcap = 0, quadcap = 0;
   std::vector<Item> dense_items;
   size_t mark_smem = 0;
   p->summary.assign((size_t)n * HSX_SUM_COLS + 1, 0);
@@ -196,23 +213,27 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         ly.G[q] = G;
       }
       ly.rsub = std::max(1, kSubElems / ly.L);
-      lmax = std::max(lmax, ly.L);
       // quad tiling when every pass groups columns (CHANNEL / SHAPE) and rows are
       // a multiple of 4 elements; otherwise row tiling (FILTER, stems)
-      bool quads = (ly.L & 3) == 0;
+      // a quad tile holds whole channels: cq quads with 4*cq a multiple of kh*kw
+      const int kmul = ly.k / std::gcd(ly.k, 4);
+      const int cq = hsx_tile_quads / kmul * kmul;
+      bool quads = (ly.L & 3) == 0 && cq > 0;
       for (int q = 0; q < ly.ncons; ++q) quads = quads && ly.group[q] != HSX_GROUP_FILTER;
       ly.tiling = quads ? 1 : 0;
       ly.pidx = (int)p->prunable.size();
       if (quads) {
-        const int tq = hsx_tile_quads, tr = tile_rows_env("HSX_CAND_TILE_ROWS", 128);
-        const int nchunks = (ly.L / 4 + tq - 1) / tq;
+        const int tr = tile_rows_env("HSX_CAND_TILE_ROWS", 128);
+        const int nchunks = (ly.L / 4 + cq - 1) / cq;
+        ly.cq = cq;
         ly.nparts = (ly.rows + tr - 1) / tr;
         for (int pt = 0; pt < ly.nparts; ++pt)
           for (int cc = 0; cc < nchunks; ++cc) {
             Item it{l, pt, cc, 1, (long long)pt * tr, std::min<long long>((long long)(pt + 1) * tr, ly.rows)};
             p->cand_dyn.push_back(it);
           }
-        quadcap = std::max(quadcap, 4 * tq * (256 / tq));
+        ly.ncitems = ly.nparts * nchunks;
+        quadcap = std::max(quadcap, 4 * hsx_tile_quads * (256 / hsx_tile_quads));
       } else {
         sqcap = std::max(sqcap, ly.rsub * ly.L);
         // one shared-memory sub-tile of rows per item
@@ -222,12 +243,13 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
           Item it{l, pt, 0, 0, pt * rows_item * ly.L, std::min<long long>((pt + 1) * rows_item, ly.rows) * ly.L};
           p->cand_dyn.push_back(it);
         }
+        ly.ncitems = ly.nparts;
       }
       for (int q = 0; q < ly.ncons; ++q) {
         ly.goff[q] = goff[q];
         goff[q] += ly.G[q];
         ly.poff[q] = poff[q];
-        poff[q] += ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * ly.L;
+        poff[q] += ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * ly.G[q];
         p->pass_list[q].push_back(l);
         p->max_passes = std::max(p->max_passes, q + 1);
       }
@@ -244,20 +266,34 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       if (ly.qtile) {
         // row-quad tiles for K3 / K6 / K7 (same shape as the K1 quad tiles)
         const int tq = hsx_tile_quads, tr = tile_rows_env("HSX_STREAM_TILE_ROWS", 32);
+        const int trp = tile_rows_env("HSX_PROJ_TILE_ROWS", 32);
         const int nchunks = (ly.L / 4 + tq - 1) / tq;
         for (int r0 = 0; r0 < ly.rows; r0 += tr)
           for (int cc = 0; cc < nchunks; ++cc) {
             Item it{l, r0 / tr, cc, 1, (long long)r0, std::min<long long>(r0 + tr, ly.rows)};
-            p->proj_items.push_back(it);
             p->stream_items.push_back(it);
           }
+        for (int r0 = 0; r0 < ly.rows; r0 += trp)
+          for (int cc = 0; cc < nchunks; ++cc) {
+            Item it{l, r0 / trp, cc, 1, (long long)r0, std::min<long long>(r0 + trp, ly.rows)};
+            p->proj_items.push_back(it);
+            ++ly.npitems;
+          }
       } else {
+        // K3's warp-per-word path is latency-bound: small items, many CTAs
+        for (long long b = 0; b < ly.n; b += kProjElems) {
+          Item it{l, 0, 0, 0, b, std::min(ly.n, b + kProjElems)};
+          p->proj_items.push_back(it);
+          ++ly.npitems;
+        }
         for (long long b = 0; b < ly.n; b += kItemElems) {
           Item it{l, 0, 0, 0, b, std::min(ly.n, b + kItemElems)};
-          p->proj_items.push_back(it);
           p->stream_items.push_back(it);
         }
       }
+      // fused K3 + K5: the keep-set tail reuses the ring's shared memory for positions
+      p->fixup_smem = std::max<size_t>(p->fixup_smem, ((size_t)ly.cin + ly.rows + 15) / 16 * 16 +
+                                                          4 * ((size_t)ly.cin + ly.rows));
       const int nwi = (int)((ly.n + kWordItem * 32 - 1) / (kWordItem * 32));
       for (long long b = 0; b < ly.n; b += kWordItem * 32) {
         Item it{l, ly.pidx, nwi, 0, b, std::min(ly.n, b + kWordItem * 32)};
@@ -295,12 +331,8 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   for (int q = 0; q < hsx::kMaxPasses; ++q) {
     p->gtotal[q] = goff[q];
     p->ptotal[q] = poff[q];
-    int gp = 1;
-    for (int l : p->pass_list[q]) {
-      int G = p->layers[l].G[q];
-      while (gp < G) gp <<= 1;
-    }
-    p->select_smem[q] = (size_t)gp * (sizeof(double) + sizeof(int)) + 8 + (size_t)lmax * sizeof(double);
+    p->select_smem[q] = 0;
+    for (int l : p->pass_list[q]) p->select_smem[q] = std::max(p->select_smem[q], select_need(p->layers[l], q));
   }
   p->sqcap = sqcap;
   // k_candidate: cp.async ring (kDepth x 4 x 256 float4 = 64 KB) + 8 KB quad fold,
@@ -308,6 +340,18 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   p->cand_smem = std::max((size_t)sqcap * sizeof(double),
                           (size_t)4 * 4 * 256 * 16 + (size_t)quadcap * sizeof(double));
   p->mark_smem = mark_smem;
+  // selection in K1's tail when the keys fit the candidate kernel's shared
+  // memory; the rest take the K2 launch
+  const bool fuse = env_flag("HSX_FUSE_SELECT", 1) != 0;
+  for (int q = 0; q < hsx::kMaxPasses; ++q) {
+    for (int l : p->pass_list[q]) {
+      DevLayer& ly = p->layers[l];
+      if (fuse && select_need(ly, q) <= p->cand_smem)
+        ly.fsel |= 1 << q;
+      else
+        p->sel_list[q].push_back(l);
+    }
+  }
   if (p->cand_smem > kMaxSmem) return fail(HSX_ESHAPE, "candidate tile needs %zu B of shared memory", p->cand_smem);
   host_layout(p);
   return HSX_OK;
@@ -318,13 +362,23 @@ int upload_plan(hsx_plan* p) {
   if ((rc = upload(&p->d_layers, p->layers))) return rc;
   if ((rc = upload(&p->d_cand, p->cand_dyn))) return rc;
   if ((rc = alloc0(&p->d_layer_done, (long long)p->prunable.size()))) return rc;
+  if ((rc = alloc0(&p->d_cand_done, (long long)p->prunable.size()))) return rc;
+  if ((rc = alloc0(&p->d_acc, 2 * (long long)p->prunable.size()))) return rc;
+  if ((rc = alloc0(&p->d_irr, (long long)p->prunable.size()))) return rc;
+  if ((rc = alloc0(&p->d_irr_any, 1))) return rc;
+  // previous rectangle: the all-ones initial mask (consensus.py:418)
+  const std::vector<uint8_t> ones_r(p->ktotal[0], 1), ones_c(p->ctotal, 1);
+  rc = upload(&p->d_rk_prev, ones_r);
+  if (rc) return rc;
+  rc = upload(&p->d_ck_prev, ones_c);
+  if (rc) return rc;
   if ((rc = upload(&p->d_elem, p->elem_items))) return rc;
   if ((rc = upload(&p->d_stream, p->stream_items))) return rc;
   if ((rc = upload(&p->d_proj, p->proj_items))) return rc;
   if ((rc = upload(&p->d_word, p->word_items))) return rc;
   if ((rc = upload(&p->d_prunable, p->prunable))) return rc;
   for (int q = 0; q < hsx::kMaxPasses; ++q) {
-    if ((rc = upload(&p->d_pass[q], p->pass_list[q]))) return rc;
+    if ((rc = upload(&p->d_sel[q], p->sel_list[q]))) return rc;
     if ((rc = alloc0(&p->d_partials[q], p->ptotal[q]))) return rc;
     if ((rc = alloc0(&p->d_norms[q], p->gtotal[q]))) return rc;
     if ((rc = alloc0(&p->d_flags[q], p->gtotal[q]))) return rc;
@@ -341,7 +395,6 @@ int upload_plan(hsx_plan* p) {
   if ((rc = upload(&p->d_pos_out, po))) return rc;
   if ((rc = upload(&p->d_pos_in, pi))) return rc;
   std::vector<int> rb(p->ktotal[0]), cp(p->ctotal, -1);
-  std::vector<uint8_t> ones_r(p->ktotal[0], 1), ones_c(p->ctotal, 1);
   for (int l : p->prunable) {
     const DevLayer& ly = p->layers[l];
     for (int i = 0; i < ly.rows; ++i) rb[ly.okeep + i] = i * ly.L;
@@ -349,8 +402,6 @@ int upload_plan(hsx_plan* p) {
   }
   if ((rc = upload(&p->maps.rowbase, rb))) return rc;
   if ((rc = upload(&p->maps.colpos, cp))) return rc;
-  if ((rc = upload(&p->maps.rowkeep, ones_r))) return rc;
-  if ((rc = upload(&p->maps.colkeep, ones_c))) return rc;
   if ((rc = upload(&p->d_summary, p->summary))) return rc;
   if ((rc = alloc0(&p->d_done, 1))) return rc;
   return HSX_OK;
@@ -456,6 +507,31 @@ int hsx_pack_theta_u(const hsx_plan* p, const float* theta, const float* u, floa
   return HSX_OK;
 }
 
+static hsx::KeepArgs keep_args(hsx_plan* p, const Item* items, const uint32_t* uni, const uint32_t* prev) {
+  hsx::KeepArgs ka;
+  ka.layers = p->d_layers;
+  ka.items = items;
+  ka.uni = uni;
+  ka.prev = prev;
+  ka.oflag = p->d_oflag;
+  ka.iflag = p->d_iflag;
+  ka.pos_out = p->d_pos_out;
+  ka.pos_in = p->d_pos_in;
+  ka.maps = p->maps;
+  for (int q = 0; q < hsx::kMaxPasses; ++q) ka.flags.f[q] = p->d_flags[q];
+  ka.summary = p->d_summary;
+  ka.layer_done = p->d_layer_done;
+  ka.done = p->d_done;
+  ka.acc = p->d_acc;
+  ka.rk_prev = p->d_rk_prev;
+  ka.ck_prev = p->d_ck_prev;
+  ka.irr = p->d_irr;
+  ka.irr_any = p->d_irr_any;
+  ka.n_layers = p->n_layers;
+  ka.n_prunable = (int)p->prunable.size();
+  return ka;
+}
+
 static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta, const float* u,
                                const float* z, const float* v) {
   hsx::CandArgs a;
@@ -469,6 +545,10 @@ static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta
   a.items = p->d_cand;
   a.identity = p->identity;
   a.sqcap = p->sqcap;
+  for (int q = 0; q < hsx::kMaxPasses; ++q) a.fw.f[q] = p->d_flags[q];
+  a.cand_done = p->d_cand_done;
+  a.ka = keep_args(p, nullptr, nullptr, nullptr);
+  a.structured = p->single_node;
   return a;
 }
 
@@ -489,6 +569,7 @@ int hsx_candidate(hsx_plan* p, const float* sum, const float* theta, const float
   a.fmask = frozen_mask;
   a.pass = 0;
   a.partials = p->d_partials[0];
+  a.norms = p->d_norms[0];
   if (frozen_mask) {
     a.items = p->d_elem;  // frozen: plain elementwise over every layer
     hsx::launch_candidate(a, (int)p->elem_items.size(), 1, p->cand_smem, S(stream));
@@ -515,6 +596,7 @@ int hsx_candidate_peers(hsx_plan* p, const float* const* sends, int32_t n, const
   a.fmask = frozen_mask;
   a.pass = 0;
   a.partials = p->d_partials[0];
+  a.norms = p->d_norms[0];
   if (frozen_mask) {
     a.items = p->d_elem;
     hsx::launch_candidate(a, (int)p->elem_items.size(), 1, p->cand_smem, S(stream));
@@ -536,6 +618,7 @@ int hsx_candidate_renorm_peers(hsx_plan* p, int32_t pass, const float* const* se
   for (int j = 0; j < n; ++j) a.peers.p[j] = sends[j];
   a.pass = pass;
   a.partials = p->d_partials[pass];
+  a.norms = p->d_norms[pass];
   for (int q = 0; q < pass; ++q) a.flags[q] = p->d_flags[q];
   a.items = p->d_cand;
   hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
@@ -551,6 +634,7 @@ int hsx_candidate_renorm(hsx_plan* p, int32_t pass, const float* sum, const floa
   hsx::CandArgs a = cand_args(p, sum, theta, u, z, v);
   a.pass = pass;
   a.partials = p->d_partials[pass];
+  a.norms = p->d_norms[pass];
   for (int q = 0; q < pass; ++q) a.flags[q] = p->d_flags[q];
   a.items = p->d_cand;
   hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
@@ -561,11 +645,12 @@ int hsx_candidate_renorm(hsx_plan* p, int32_t pass, const float* sum, const floa
 int hsx_select(hsx_plan* p, int32_t pass, void* stream) {
   if (!p) return fail(HSX_EINVAL, "null plan");
   if (pass < 0 || pass >= hsx::kMaxPasses) return fail(HSX_EINVAL, "pass %d out of range", pass);
-  int n = (int)p->pass_list[pass].size();
+  // layers selected in the candidate kernel's tail need nothing here
+  int n = (int)p->sel_list[pass].size();
   if (n == 0) return HSX_OK;
   hsx::FlagPtrs fl = {{p->d_flags[0], p->d_flags[1], p->d_flags[2]}};
-  hsx::launch_select(p->d_layers, p->d_pass[pass], n, pass, p->d_partials[pass], p->d_norms[pass],
-                     fl, p->maps, p->select_smem[pass], S(stream));
+  hsx::launch_select(p->d_layers, p->d_sel[pass], n, pass, p->d_partials[pass], p->d_norms[pass],
+                     fl, keep_args(p, nullptr, nullptr, nullptr), p->single_node, p->select_smem[pass], S(stream));
   HSX_LAUNCHED("select");
   return HSX_OK;
 }
@@ -578,14 +663,6 @@ int hsx_read_groups(const hsx_plan* p, int32_t pass, double* norms, uint8_t* fla
     HSX_CUDA(cudaMemcpyAsync(norms, p->d_norms[pass], n * sizeof(double), cudaMemcpyDeviceToDevice, S(stream)));
   if (flags)
     HSX_CUDA(cudaMemcpyAsync(flags, p->d_flags[pass], n, cudaMemcpyDeviceToDevice, S(stream)));
-  return HSX_OK;
-}
-
-int hsx_project(hsx_plan* p, float* z_node, uint32_t* local_mask, void* stream) {
-  if (!p || !z_node || (!local_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
-  hsx::launch_project(p->d_layers, p->d_proj, (int)p->proj_items.size(), z_node, local_mask, p->maps,
-                      S(stream));
-  HSX_LAUNCHED("project");
   return HSX_OK;
 }
 
@@ -614,31 +691,46 @@ int hsx_mask_or_ptrs(const uint32_t* const* srcs, int32_t n, int64_t words, uint
   return HSX_OK;
 }
 
+int hsx_project(hsx_plan* p, float* z_node, uint32_t* local_mask, void* stream) {
+  if (!p || !z_node || (!local_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
+  hsx::KeepArgs ka = keep_args(p, p->d_proj, nullptr, nullptr);
+  hsx::launch_project(ka, (int)p->proj_items.size(), z_node, local_mask, 0, S(stream));
+  HSX_LAUNCHED("project");
+  return HSX_OK;
+}
+
+int hsx_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, const uint32_t* prev_mask,
+                          void* stream) {
+  if (!p || !z_node || (!mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
+  if (p->prunable.empty()) return HSX_OK;
+  if (!p->single_node) {  // keep sets from the mask bits (K3, then K5)
+    if (int rc = hsx_project(p, z_node, mask, stream)) return rc;
+    return hsx_keep_sets(p, mask, prev_mask, stream);
+  }
+  // the selection's last pass derived the keep sets of the rectangles R x C; K3
+  // flags layers whose mask has a kept zero and the fixup re-derives those
+  hsx::KeepArgs ka = keep_args(p, p->d_proj, mask, prev_mask);
+  hsx::launch_project(ka, (int)p->proj_items.size(), z_node, mask, 1, S(stream));
+  HSX_LAUNCHED("project_check");
+  hsx::launch_keep_fixup(ka, p->d_prunable, (int)p->prunable.size(), p->fixup_smem, S(stream));
+  HSX_LAUNCHED("keep_fixup");
+  return HSX_OK;
+}
+
+int hsx_plan_set_single_node(hsx_plan* p, int32_t on) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  p->single_node = on ? 1 : 0;
+  return HSX_OK;
+}
+
 int hsx_keep_sets(hsx_plan* p, const uint32_t* union_mask, const uint32_t* prev_mask,
                   void* stream) {
   if (!p || (!union_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
   if (p->prunable.empty()) return HSX_OK;
-  cudaStream_t st = S(stream);
-  // K_out / K_in flags are zero here: zero at allocation, re-zeroed by K5's scans
-  // zero the drift / popcount columns of every row
-  HSX_CUDA(cudaMemset2DAsync(p->d_summary + HSX_SUM_DRIFT, HSX_SUM_COLS * sizeof(long long), 0,
-                             2 * sizeof(long long), p->n_layers, st));
-  hsx::KeepArgs ka;
-  ka.layers = p->d_layers;
-  ka.items = p->d_word;
-  ka.uni = union_mask;
-  ka.prev = prev_mask;
-  ka.oflag = p->d_oflag;
-  ka.iflag = p->d_iflag;
-  ka.pos_out = p->d_pos_out;
-  ka.pos_in = p->d_pos_in;
-  ka.maps = p->maps;
-  ka.summary = p->d_summary;
-  ka.layer_done = p->d_layer_done;
-  ka.done = p->d_done;
-  ka.n_layers = p->n_layers;
-  ka.n_prunable = (int)p->prunable.size();
-  hsx::launch_keep_sets(ka, (int)p->word_items.size(), p->mark_smem, st);
+  // K_out / K_in flags and the popcount accumulators are zero here (zero at
+  // allocation, re-zeroed by every keep-set tail)
+  hsx::KeepArgs ka = keep_args(p, p->d_word, union_mask, prev_mask);
+  hsx::launch_keep_sets(ka, (int)p->word_items.size(), p->mark_smem, S(stream));
   HSX_LAUNCHED("keep_sets");
   return HSX_OK;
 }

@@ -1,5 +1,7 @@
 // sm_100a kernels of the H-SADMM synchronization step (see hsx_kernels.cuh).
 #include <algorithm>
+#include <cstdio>
+#include <utility>
 
 #include "hsx_kernels.cuh"
 
@@ -25,6 +27,35 @@ static void allow_smem(K kernel, size_t bytes) {
     keys[slot] = key;
     granted[slot] = bytes;
   }
+}
+
+// Programmatic dependent launch: the chain kernels are launched with
+// programmatic stream serialization, so a kernel's launch and CTA rasterization
+// overlap the tail of its predecessor. Every such kernel calls pdl_wait() first,
+// unconditionally (completion of a grid then implies completion of everything
+// before it in the stream), then pdl_trigger() so its successor may be scheduled
+// once all of its CTAs are running.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+#define PDL_ENTRY() \
+  do {              \
+    pdl_wait();     \
+    pdl_trigger();  \
+  } while (0)
+
+template <typename... P, typename... A>
+static void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
 }
 
 // streaming 128-bit load of data read exactly once (evict-first)
@@ -95,14 +126,19 @@ __device__ __forceinline__ void cp_quad(float4* dst, const float* src, long long
   }
 }
 
-// Drive `count` iterations of (issue(slot, i), consume(slot, i)) through the ring.
-template <class Issue, class Consume>
-__device__ __forceinline__ void ring_run(int count, Issue issue, Consume consume) {
+// Drive `count` iterations of (issue(slot, i), consume(slot, i)) through the ring:
+// ring_prologue puts the first kDepth-1 quads in flight (a kernel can do other
+// setup before ring_loop), ring_run does both.
+template <class Issue>
+__device__ __forceinline__ void ring_prologue(int count, Issue issue) {
 #pragma unroll
   for (int d = 0; d < kDepth - 1; ++d) {
     if (d < count) issue(d, d);
     cp_commit();
   }
+}
+template <class Issue, class Consume>
+__device__ __forceinline__ void ring_loop(int count, Issue issue, Consume consume) {
   for (int i = 0; i < count; ++i) {
     const int ahead = i + kDepth - 1;
     if (ahead < count) issue(ahead % kDepth, ahead);
@@ -110,6 +146,543 @@ __device__ __forceinline__ void ring_run(int count, Issue issue, Consume consume
     cp_wait<kDepth - 1>();
     consume(i % kDepth, i);
   }
+}
+template <class Issue, class Consume>
+__device__ __forceinline__ void ring_run(int count, Issue issue, Consume consume) {
+  ring_prologue(count, issue);
+  ring_loop(count, issue, consume);
+}
+
+// ---------------------------------------------------------------------------
+// Keep sets (shrinkage.py:45-58 derive_keep_sets; sparsity.py:118-122 drift
+// numerator; transport.py:239-280 concatenation order). Two derivations:
+//  * from mask bits (K5, any M): every CTA marks the K_out / K_in "any" flags
+//    of its word range and accumulates popcount(mask) and popcount(mask ^ prev)
+//    per layer; the layer's last CTA scans the flags (keep_sets_tail);
+//  * structured (one node, M == 1: the union is the local mask kept && z != 0):
+//    the mask is the rectangle R x C of kept rows x kept columns unless a kept
+//    element is exactly zero, so the selection's last pass derives K_out = R,
+//    K_in = channels meeting C, the popcount |R||C| and the drift against the
+//    previous rectangle straight from the group flags (structured_keep_sets, in
+//    the K1 / K2 tail). K3 flags layers with a kept zero ("irregular");
+//    k_keep_fixup re-derives those exactly from their mask bits.
+// Both write positions, payload maps and the summary row of the layer; the last
+// layer to finish lays out the flat buffer (exclusive scan of payload sizes in
+// layer order). Flags and accumulators are left zeroed (no memsets).
+// ---------------------------------------------------------------------------
+
+// block-wide exclusive prefix sum of one int per thread (blockDim <= 1024)
+__device__ int block_exclusive_scan(int x, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int y = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int nw = blockDim.x >> 5;
+    int t = lane < nw ? warp_tot[lane] : 0;
+    int ti = t;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int y = __shfl_up_sync(kFull, ti, off);
+      if (lane >= off) ti += y;
+    }
+    if (lane < nw) warp_tot[lane] = ti - t;
+    if (lane == 31) *total = ti;
+  }
+  __syncthreads();
+  int r = incl - x + warp_tot[warp];
+  __syncthreads();
+  return r;
+}
+
+// block-wide sum of one value per thread, result in every thread
+template <typename T>
+__device__ T block_sum(T x) {
+  __shared__ T wsum[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wsum[warp] = x;
+  __syncthreads();
+  T s = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += wsum[w];
+  __syncthreads();
+  return s;
+}
+
+// flag byte i: through L2 when written by other CTAs of the launch, plain when
+// in shared memory
+template <bool SMEM>
+__device__ __forceinline__ bool flag_at(const uint8_t* f, int i) {
+  if constexpr (SMEM)
+    return f[i] != 0;
+  else
+    return __ldcg(f + i) != 0;
+}
+
+// Positions of the set K_in / K_out flags of one layer in one block scan when
+// every thread owns <= 8 consecutive flags of each array (the two counts packed
+// in one int, 16 bits each), else in rounds. Positions go to global pos_* and
+// shared s_p*; returns (|K_in|, |K_out|).
+template <bool SMEM>
+__device__ int2 scan_keep(const uint8_t* fin, int cin, const uint8_t* fout, int rows, int* pos_in, int* pos_out,
+                          int* s_pin, int* s_pout) {
+  __shared__ int warp_tot[32];
+  __shared__ int total;
+  constexpr int kPer = 8;
+  const int nt = blockDim.x, t = threadIdx.x;
+  const int per = (max(cin, rows) + nt - 1) / nt;
+  if (per <= kPer) {
+    bool fi[kPer], fo[kPer];
+    int ci = 0, co = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int x = t * per + i;
+      fi[i] = i < per && x < cin && flag_at<SMEM>(fin, x);
+      fo[i] = i < per && x < rows && flag_at<SMEM>(fout, x);
+      ci += fi[i];
+      co += fo[i];
+    }
+    const int ex = block_exclusive_scan(ci | (co << 16), warp_tot, &total);
+    const int tot = total;
+    int pi = ex & 0xffff, po = ex >> 16;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int x = t * per + i;
+      if (i < per && x < cin) {
+        const int p = fi[i] ? pi++ : -1;
+        pos_in[x] = p;
+        s_pin[x] = p;
+      }
+      if (i < per && x < rows) {
+        const int p = fo[i] ? po++ : -1;
+        pos_out[x] = p;
+        s_pout[x] = p;
+      }
+    }
+    __syncthreads();
+    return make_int2(tot & 0xffff, tot >> 16);
+  }
+  int n[2];
+  for (int a = 0; a < 2; ++a) {
+    const uint8_t* f = a ? fout : fin;
+    const int m = a ? rows : cin;
+    int* pos = a ? pos_out : pos_in;
+    int* spos = a ? s_pout : s_pin;
+    int carry = 0;
+    for (int base = 0; base < m; base += nt) {
+      const int i = base + t;
+      const int fr = (i < m && flag_at<SMEM>(f, i)) ? 1 : 0;
+      const int ex = block_exclusive_scan(fr, warp_tot, &total);
+      if (i < m) {
+        pos[i] = fr ? carry + ex : -1;
+        spos[i] = pos[i];
+      }
+      carry += total;
+    }
+    n[a] = carry;
+  }
+  __syncthreads();
+  return make_int2(n[0], n[1]);
+}
+
+// payload maps of one layer from its positions in shared memory:
+// rowbase[o] = pos_out[o] * |K_in| * k, colpos[c*k + j] = pos_in[c] * k + j (-1: dropped)
+__device__ void write_maps(const KeepArgs& a, int rows, int L, int k, long long okeep, long long cpoff,
+                           const FastDiv& divk, const int* s_pin, const int* s_pout, int n_in) {
+  const int rowlen = n_in * k;
+  for (int o = threadIdx.x; o < rows; o += blockDim.x) {
+    const int po = s_pout[o];
+    a.maps.rowbase[okeep + o] = po >= 0 ? po * rowlen : -1;
+  }
+  if ((L & 3) == 0) {  // cpoff is a multiple of 4: one int4 of column positions per thread
+    for (int q4 = threadIdx.x; q4 < (L >> 2); q4 += blockDim.x) {
+      int v[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const unsigned col = 4 * q4 + b, c = fdiv(col, divk), jx = col - c * (unsigned)k;
+        const int pi = s_pin[c];
+        v[b] = pi >= 0 ? pi * k + (int)jx : -1;
+      }
+      *reinterpret_cast<int4*>(a.maps.colpos + cpoff + 4 * q4) = make_int4(v[0], v[1], v[2], v[3]);
+    }
+  } else {
+    for (int col = threadIdx.x; col < L; col += blockDim.x) {
+      const unsigned c = fdiv((unsigned)col, divk), jx = (unsigned)col - c * (unsigned)k;
+      const int pi = s_pin[c];
+      a.maps.colpos[cpoff + col] = pi >= 0 ? pi * k + (int)jx : -1;
+    }
+  }
+}
+
+// flat-buffer layout: exclusive scan of the payload sizes of all layers (block-wide)
+__device__ void layout_flat(const KeepArgs& a) {
+  __shared__ long long wsum[32];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nt = blockDim.x;
+  for (int base = 0; base < a.n_layers; base += nt) {
+    int i = base + threadIdx.x;
+    volatile long long* ri = a.summary + (long long)i * kSumCols;
+    long long e = i < a.n_layers ? ri[2] : 0;
+    long long incl = e;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      long long y = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      long long t = lane < nt / 32 ? wsum[lane] : 0, ti = t;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        long long y = __shfl_up_sync(kFull, ti, off);
+        if (lane >= off) ti += y;
+      }
+      wsum[lane] = ti - t;
+    }
+    __syncthreads();
+    long long ex = carry + wsum[warp] + incl - e;
+    if (i < a.n_layers) ri[3] = ex;
+    __syncthreads();
+    if (threadIdx.x == nt - 1) carry = ex + e;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.summary[(long long)a.n_layers * kSumCols] = carry;
+}
+
+// summary row of layer l, then count the layer done; the last one lays out the
+// flat buffer. One gpu-scope fence by thread 0 releases the block's writes.
+__device__ void finish_layer(const KeepArgs& a, int l, int n_out, int n_in, int k, long long drift,
+                             long long pop) {
+  __shared__ bool last_layer;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long* row = a.summary + (long long)l * kSumCols;
+    row[0] = n_out;
+    row[1] = n_in;
+    row[2] = (long long)n_out * n_in * k;
+    row[4] = drift;
+    row[5] = pop;
+    __threadfence();
+    last_layer = atomicAdd(a.done, 1u) == (unsigned)a.n_prunable - 1;
+  }
+  __syncthreads();
+  if (!last_layer) return;
+  __threadfence();
+  layout_flat(a);
+  if (threadIdx.x == 0) *a.done = 0;
+}
+
+// K5 tail, run by the last CTA of layer l: keep sets from the global any-flags;
+// smem >= 4 * (c_in + rows) bytes
+__device__ void keep_sets_tail(const KeepArgs& a, int l, const DevLayer& gly, uint8_t* smem) {
+  // layer fields in registers: the flag / map stores below may alias the table
+  const int cin = gly.cin, rows = gly.rows, k = gly.k, L = gly.L, pidx = gly.pidx;
+  const long long ikeep = gly.ikeep, okeep = gly.okeep, cpoff = gly.cpoff;
+  const FastDiv divk = gly.divk;
+  int* s_pin = reinterpret_cast<int*>(smem);
+  int* s_pout = s_pin + cin;
+  const int2 nio = scan_keep<false>(a.iflag + ikeep, cin, a.oflag + okeep, rows, a.pos_in + ikeep,
+                                    a.pos_out + okeep, s_pin, s_pout);
+  // leave the any-flags zeroed for the next derivation
+  for (int i = threadIdx.x; i < cin; i += blockDim.x) a.iflag[ikeep + i] = 0;
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) a.oflag[okeep + i] = 0;
+  write_maps(a, rows, L, k, okeep, cpoff, divk, s_pin, s_pout, nio.x);
+  long long drift = 0, pop = 0;
+  if (threadIdx.x == 0) {
+    drift = (long long)atomicExch(a.acc + 2 * pidx, 0ULL);
+    pop = (long long)atomicExch(a.acc + 2 * pidx + 1, 0ULL);
+    a.layer_done[pidx] = 0;
+  }
+  finish_layer(a, l, nio.y, nio.x, k, drift, pop);
+}
+
+// end of a K5 marking CTA: fold its popcounts into the layer's accumulators, then
+// count it done; the layer's last CTA runs the tail
+__device__ void keep_mark_done(const KeepArgs& a, int l, const DevLayer& ly, int nitems,
+                               unsigned long long pop, unsigned long long drift, uint8_t* smem) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    pop += __shfl_xor_sync(kFull, pop, off);
+    drift += __shfl_xor_sync(kFull, drift, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (drift) atomicAdd(a.acc + 2 * ly.pidx, drift);
+    if (pop) atomicAdd(a.acc + 2 * ly.pidx + 1, pop);
+  }
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.layer_done + ly.pidx, 1u) == (unsigned)nitems - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  keep_sets_tail(a, l, ly, smem);
+}
+
+// Structured keep sets of layer l at its last selection pass (one node): the
+// rectangle R x C from the group flags (this pass in sflag, earlier passes in
+// global memory). Updates the previous-rectangle state (rk_prev / ck_prev).
+// smem: rows + L + c_in bytes, then 4 * (c_in + rows) bytes of positions
+// (16-B aligned): structured_smem(rows, L, c_in).
+__host__ __device__ inline size_t structured_smem(int rows, int L, int cin) {
+  return ((size_t)rows + L + cin + 15) / 16 * 16 + 4 * ((size_t)cin + rows);
+}
+
+__device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& gly, int pass,
+                                     const uint8_t* sflag, uint8_t* smem) {
+  const int cin = gly.cin, rows = gly.rows, k = gly.k, L = gly.L, npass = gly.ncons;
+  const long long ikeep = gly.ikeep, okeep = gly.okeep, cpoff = gly.cpoff;
+  const FastDiv divk = gly.divk;
+  int gq[kMaxPasses];
+  const uint8_t* fq[kMaxPasses];
+#pragma unroll
+  for (int q = 0; q < kMaxPasses; ++q) {
+    gq[q] = q < npass ? gly.group[q] : -1;
+    fq[q] = q < npass ? a.flags.f[q] + gly.goff[q] : nullptr;
+  }
+  uint8_t* srk = smem;             // kept rows
+  uint8_t* sck = srk + rows;       // kept columns
+  uint8_t* sch = sck + L;          // channels meeting C
+  int* s_pin = reinterpret_cast<int*>(smem + ((size_t)rows + L + cin + 15) / 16 * 16);
+  int* s_pout = s_pin + cin;
+  // R and C, their sizes and overlaps with the previous rectangle
+#ifdef HSX_PROBE_SELECT
+  long long tq[8];
+  tq[0] = clock64();
+#define ST_MARK(i) do { __syncthreads(); tq[i] = clock64(); } while (0)
+#else
+#define ST_MARK(i) do { } while (0)
+#endif
+  // three counts packed per word (21 bits each: rows, columns <= 2^20)
+  unsigned long long rsum = 0, csum = 0;
+  for (int o = threadIdx.x; o < rows; o += blockDim.x) {
+    uint8_t kp = 1;
+#pragma unroll
+    for (int q = 0; q < kMaxPasses; ++q)
+      if (gq[q] == kFilter) kp &= q == pass ? sflag[o] : fq[q][o];
+    const uint8_t pv = a.rk_prev[okeep + o];
+    srk[o] = kp;
+    a.rk_prev[okeep + o] = kp;
+    rsum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
+  }
+  for (int col = threadIdx.x; col < L; col += blockDim.x) {
+    const int c = (int)fdiv((unsigned)col, divk);
+    uint8_t kp = 1;
+#pragma unroll
+    for (int q = 0; q < kMaxPasses; ++q) {
+      if (gq[q] != kChannel && gq[q] != kShape) continue;
+      const int g = gq[q] == kChannel ? c : col;
+      kp &= q == pass ? sflag[g] : fq[q][g];
+    }
+    const uint8_t pv = a.ck_prev[cpoff + col];
+    sck[col] = kp;
+    a.ck_prev[cpoff + col] = kp;
+    csum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
+  }
+  ST_MARK(1);
+  rsum = block_sum(rsum);
+  csum = block_sum(csum);
+  ST_MARK(2);
+  constexpr unsigned long long m21 = (1ULL << 21) - 1;
+  const long long nR = rsum & m21, nRp = (rsum >> 21) & m21, nRR = rsum >> 42;
+  const long long nC = csum & m21, nCp = (csum >> 21) & m21, nCC = csum >> 42;
+  // K_in: channels with a kept column (when some row is kept); K_out: kept rows
+  // (when some column is kept)
+  for (int c = threadIdx.x; c < cin; c += blockDim.x) {
+    uint8_t any = 0;
+    for (int jx = 0; jx < k; ++jx) any |= sck[c * k + jx];
+    sch[c] = nR > 0 ? any : 0;
+  }
+  if (nC == 0)
+    for (int o = threadIdx.x; o < rows; o += blockDim.x) srk[o] = 0;
+  __syncthreads();
+  ST_MARK(3);
+  const int2 nio = scan_keep<true>(sch, cin, srk, rows, a.pos_in + ikeep, a.pos_out + okeep, s_pin, s_pout);
+  ST_MARK(4);
+  write_maps(a, rows, L, k, okeep, cpoff, divk, s_pin, s_pout, nio.x);
+  ST_MARK(5);
+  // |A ^ B| = |A| + |B| - 2 |A n B| for rectangles A = R x C, B = Rp x Cp
+  const long long pop = nR * nC;
+  const long long drift = pop + nRp * nCp - 2 * nRR * nCC;
+  finish_layer(a, l, nio.y, nio.x, k, drift, pop);
+#ifdef HSX_PROBE_SELECT
+  ST_MARK(6);
+  if (threadIdx.x == 0)
+    printf("structured l=%d rows=%d L=%d cin=%d nt=%d: RC %lld sums %lld ch %lld scan %lld maps %lld finish %lld\n", l,
+           rows, L, cin, (int)blockDim.x, tq[1] - tq[0], tq[2] - tq[1], tq[3] - tq[2], tq[4] - tq[3], tq[5] - tq[4],
+           tq[6] - tq[5]);
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// K2 select: norms = sqrt(sum of partials); keep the `keep` largest groups, lower
+// index on ties (SparsityConstraint.resolve + _kept_group_indices,
+// sparsity.py:53-68). One block per layer. Runs in the tail of the layer's last
+// K1 tile when its keys fit the candidate kernel's shared memory
+// (DevLayer::fsel), else as its own launch.
+// ---------------------------------------------------------------------------
+
+// Top-`keep` of G non-negative fp64 norms. Their bit patterns order like the
+// values, so an 8-bit MSD radix select over the 64-bit keys narrows to the bin
+// holding the keep-th largest key, one byte per round (O(G) per round, vs O(G^2)
+// rank counting or O(G log^2 G) barriers of a bitonic sort). It stops as soon
+// as every candidate of the chosen bin is kept (distinct norms: 2-3 rounds).
+// Groups above the bin are kept; when the full 64-bit key T is reached with
+// more equal keys than slots, the lowest-index ones fill the remainder (the
+// stable argsort of -norms). Writes the 0/1 flags into sflag[G].
+__device__ void radix_top_k(const unsigned long long* __restrict__ key, int G, int keep, uint8_t* sflag) {
+  __shared__ __align__(16) int hist[2][256];  // bin 255 - digit: lanes scan descending digits
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_rem, s_eq;
+  __shared__ int warp_tot[32];
+  __shared__ int total;
+  const int t = threadIdx.x, nt = blockDim.x;
+  unsigned long long prefix = 0, himask = 0;
+  int rem = keep, eq = G, buf = 0;
+  for (int i = t; i < 256; i += nt) hist[0][i] = 0;
+  __syncthreads();
+  for (int shift = 56;; shift -= 8) {
+    for (int g = t; g < G; g += nt) {
+      const unsigned long long x = key[g];
+      if ((x & himask) == prefix) atomicAdd(&hist[buf][255 - ((int)(x >> shift) & 255)], 1);
+    }
+    for (int i = t; i < 256; i += nt) hist[buf ^ 1][i] = 0;  // next round's bins
+    __syncthreads();
+    if (t < 32) {
+      const int4 h0 = *reinterpret_cast<const int4*>(&hist[buf][8 * t]);
+      const int4 h1 = *reinterpret_cast<const int4*>(&hist[buf][8 * t + 4]);
+      const int c[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};  // digits 255-8t-b
+      const int sum = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]));
+      int incl = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, off);
+        if (t >= off) incl += y;
+      }
+      const int excl = incl - sum;
+      const unsigned owner = __ballot_sync(kFull, excl < rem && rem <= incl);
+      if (t == __ffs(owner) - 1) {
+        int before = excl;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (before < rem && rem <= before + c[b]) {
+            s_prefix = prefix | ((unsigned long long)(255 - 8 * t - b) << shift);
+            s_rem = rem - before;
+            s_eq = c[b];
+          }
+          before += c[b];
+        }
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    rem = s_rem;
+    eq = s_eq;
+    himask |= 0xffULL << shift;
+    if (rem == eq || shift == 0) break;
+    buf ^= 1;
+  }
+  if (rem == eq) {  // every candidate of the bin is kept
+    for (int g = t; g < G; g += nt) sflag[g] = (key[g] & himask) >= prefix;
+    return;
+  }
+  const unsigned long long T = prefix;  // exact key with ties: index-order ranks among them
+  int carry = 0;
+  for (int base = 0; base < G; base += nt) {
+    const int g = base + t;
+    const int e = (g < G && key[g] == T) ? 1 : 0;
+    const int ex = block_exclusive_scan(e, warp_tot, &total);
+    if (g < G) sflag[g] = key[g] > T || (e && carry + ex < rem);
+    carry += total;
+  }
+}
+
+// One layer's selection by the whole block; K1 partials are read through L2 (in
+// the fused form other CTAs of the same launch wrote them). Partials are per
+// group: [nparts][G] (FILTER: [G], complete row sums), folded in part order.
+// shared memory: keys[G] (u64), flags[G] (u8)
+__host__ __device__ inline size_t select_bytes(int G) { return ((size_t)G * 9 + 15) / 16 * 16; }
+
+__device__ void select_layer(const DevLayer& gly, int pass, const double* __restrict__ partials,
+                             double* __restrict__ norms, const FlagPtrs& flags, void* smem, int l,
+                             const KeepArgs* ka) {
+  // layer fields in registers: the byte stores below may alias the layer table
+  const int G = gly.G[pass], grp = gly.group[pass], keep = gly.keep[pass];
+  const int nparts = grp == kFilter ? 1 : gly.nparts;
+  const long long goff = gly.goff[pass];
+  const double* __restrict__ part = partials + gly.poff[pass];
+  unsigned long long* skey = reinterpret_cast<unsigned long long*>(smem);
+  uint8_t* sflag = reinterpret_cast<uint8_t*>(skey + G);
+  const int nt = blockDim.x;
+  const int t = threadIdx.x;
+#ifdef HSX_PROBE_SELECT
+  long long tm[6];
+  tm[0] = clock64();
+#define SEL_MARK(i) do { __syncthreads(); tm[i] = clock64(); } while (0)
+#else
+#define SEL_MARK(i) do { } while (0)
+#endif
+  // 1) norms: every thread's partial loads in flight together, folded in part order
+  constexpr int kU = 4;
+  for (int g0 = t; g0 < G; g0 += kU * nt) {
+    double s2[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) s2[u] = 0.0;
+    for (int pt = 0; pt < nparts; ++pt) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int g = g0 + u * nt;
+        if (g < G) s2[u] += __ldcg(part + (long long)pt * G + g);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int g = g0 + u * nt;
+      if (g < G) {
+        const double nrm = sqrt(s2[u]);
+        norms[goff + g] = nrm;
+        skey[g] = (unsigned long long)__double_as_longlong(nrm);
+      }
+    }
+  }
+  __syncthreads();
+  SEL_MARK(1);
+  // 2) top-k flags
+  radix_top_k(skey, G, keep, sflag);
+  __syncthreads();
+  SEL_MARK(2);
+  uint8_t* __restrict__ fl = flags.f[pass] + goff;
+  for (int g = t; g < G; g += nt) fl[g] = sflag[g];
+  SEL_MARK(3);
+  if (ka != nullptr && pass == gly.ncons - 1)  // one node: keep sets of the rectangle
+    structured_keep_sets(*ka, l, gly, pass, sflag, reinterpret_cast<uint8_t*>(smem) + select_bytes(G));
+#ifdef HSX_PROBE_SELECT
+  if (t == 0)
+    printf("select G=%d nparts=%d nt=%d: norms %lld topk %lld flags %lld cycles\n", G, nparts, nt,
+           tm[1] - tm[0], tm[2] - tm[1], tm[3] - tm[2]);
+#endif
+}
+
+__global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ layers,
+                                                 const int* __restrict__ list, int pass,
+                                                 const double* __restrict__ partials,
+                                                 double* __restrict__ norms, FlagPtrs flags, KeepArgs ka,
+                                                 int structured) {
+  PDL_ENTRY();
+  extern __shared__ unsigned long long skey[];
+  const int l = list[blockIdx.x];
+  select_layer(layers[l], pass, partials, norms, flags, skey, l, structured ? &ka : nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -315,11 +888,12 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
 }
 
 // K1b quad tiles (CHANNEL / SHAPE groups, c_in*kh*kw % 4 == 0 — every ResNet conv
-// but the 7x7 stem): a tile is rows x 64 column quads; thread t owns quad
-// (t & 63) and row phase (t >> 6), so its fp64 column sums of squares stay in
-// registers while its rows stream through the cp.async ring; the 4 phases fold
-// in shared memory in a fixed order and the tile writes one fp64 partial per
-// column (the channel fold happens in K2).
+// but the 7x7 stem): a tile is rows x cq column quads (cq <= 64, 4*cq a multiple
+// of kh*kw so a tile holds whole channels); thread t owns quad (t & 63) and row
+// phase (t >> 6), so its fp64 column sums of squares stay in registers while
+// its rows stream through the cp.async ring; the 4 phases fold in shared memory
+// in a fixed order, then the kh*kw columns of each channel, and the tile writes
+// one fp64 partial per group: partials[part][G].
 constexpr int kTileQuads = 64;
 
 template <int MODE>
@@ -329,11 +903,12 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const int pass = p.pass;
   const int L = ly.L;
   const int Q = L >> 2;
+  const int cq = ly.cq;
   const int jj = threadIdx.x & (kTileQuads - 1);
   const int ph = threadIdx.x / kTileQuads;
-  const int j = it.chunk * kTileQuads + jj;
+  const int j = it.chunk * cq + jj;
   const long long r0 = it.begin + ph, r1 = it.end;
-  const int count = (j < Q && r0 < r1) ? (int)((r1 - r0 + RP - 1) / RP) : 0;
+  const int count = (jj < cq && j < Q && r0 < r1) ? (int)((r1 - r0 + RP - 1) / RP) : 0;
   const long long off = ly.off;
   const K1Src src = k1_src<MODE>(p, off + 4 * j);
   float* zn = p.zn + off + 4 * j;
@@ -363,12 +938,30 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
-  const int col = it.chunk * 4 * kTileQuads + threadIdx.x;  // one column per thread
-  if (col < L) {
-    double s = cs[threadIdx.x];
+  const int col0 = it.chunk * 4 * cq;
+  const int ncol = min(4 * cq, L - col0);
+  const int G = ly.G[pass];
+  double* out = p.partials + ly.poff[pass] + (long long)it.part * G;
+  const int t = threadIdx.x;
+  double s = 0.0;
+  if (t < ncol) {  // one column per thread: the row phases in order
+    s = cs[t];
 #pragma unroll
-    for (int q = 1; q < RP; ++q) s += cs[q * 4 * kTileQuads + threadIdx.x];
-    p.partials[ly.poff[pass] + (long long)it.part * L + col] = s;
+    for (int q = 1; q < RP; ++q) s += cs[q * 4 * kTileQuads + t];
+  }
+  if (ly.group[pass] == kShape || ly.k == 1) {
+    if (t < ncol) out[col0 + t] = s;
+    return;
+  }
+  __syncthreads();
+  if (t < ncol) cs[t] = s;
+  __syncthreads();
+  const int k = ly.k;
+  const int c0 = col0 / k;  // whole channels per tile
+  if (t < ncol / k) {
+    double g = 0.0;
+    for (int jx = 0; jx < k; ++jx) g += cs[t * k + jx];
+    out[c0 + t] = g;
   }
 }
 
@@ -404,17 +997,26 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
       if (lane == 0) p.partials[ly.poff[pass] + r0 + r] = s;
     }
-  } else {
+  } else if (grp == kShape || ly.k == 1) {
     for (int col = threadIdx.x; col < L; col += kThreads) {
       double s = 0.0;
       for (int r = 0; r < nr; ++r) s += sq[r * L + col];
       p.partials[ly.poff[pass] + (long long)it.part * L + col] = s;
+    }
+  } else {
+    const int k = ly.k, G = ly.G[pass];
+    for (int c = threadIdx.x; c < G; c += kThreads) {  // channel: rows, then its kh*kw columns
+      double s = 0.0;
+      for (int r = 0; r < nr; ++r)
+        for (int jx = 0; jx < k; ++jx) s += sq[r * L + c * k + jx];
+      p.partials[ly.poff[pass] + (long long)it.part * G + c] = s;
     }
   }
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int frozen) {
+  PDL_ENTRY();
   extern __shared__ float4 ring[];
   const Item it = p.items[blockIdx.x];
   const DevLayer& ly = p.layers[it.layer];
@@ -438,12 +1040,26 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
     cand_tile_quads<MODE>(p, ly, it, ring, reinterpret_cast<double*>(ring + kDepth * K1<MODE>::NB * kThreads));
   else
     cand_tile_rows<MODE>(p, ly, it, reinterpret_cast<double*>(ring));
+  if (!((ly.fsel >> p.pass) & 1)) return;
+  // fused K2: the layer's last tile to finish selects its groups (its partials
+  // are complete once every tile has released them: fence, then the counter)
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(p.cand_done + ly.pidx, 1u) == (unsigned)ly.ncitems - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  select_layer(ly, p.pass, p.partials, p.norms, p.fw, ring, it.layer, p.structured ? &p.ka : nullptr);
+  if (threadIdx.x == 0) p.cand_done[ly.pidx] = 0;  // ready for the next launch
 }
 
 template <int MODE>
 static void launch_candidate_mode(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
   allow_smem(k_candidate<MODE>, smem);
-  k_candidate<MODE><<<n_items, kThreads, smem, st>>>(a, frozen);
+  launch_pdl(k_candidate<MODE>, n_items, kThreads, smem, st, a, frozen);
 }
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
@@ -471,171 +1087,21 @@ void launch_div_selftest(const double* num, long long n, double den, double* out
   k_div_selftest<<<grid, 256, 0, st>>>(num, n, den, 1.0 / den, out);
 }
 
-// ---------------------------------------------------------------------------
-// K2 select: norms = sqrt(sum partials); top-k with lower-index tie-break.
-// sparsity.py:53-68.  One CTA per layer, bitonic sort of (norm desc, index asc).
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
-  return ka > kb || (ka == kb && ia < ib);
-}
-
-// shared memory: key[Gp] (double), idx[Gp] (int), fold[blockDim] (double)
-// sum of n values strided by `stride`: four independent accumulators (loads in
-// flight together), combined in a fixed tree — deterministic for a given n
-__device__ __forceinline__ double fold_parts(const double* __restrict__ p, int n, int stride) {
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int pt = 0;
-  for (; pt + 4 <= n; pt += 4) {
-    const double x0 = p[(long long)pt * stride], x1 = p[(long long)(pt + 1) * stride];
-    const double x2 = p[(long long)(pt + 2) * stride], x3 = p[(long long)(pt + 3) * stride];
-    a0 += x0; a1 += x1; a2 += x2; a3 += x3;
-  }
-  if (pt < n) a0 += p[(long long)pt * stride];
-  if (pt + 1 < n) a1 += p[(long long)(pt + 1) * stride];
-  if (pt + 2 < n) a2 += p[(long long)(pt + 2) * stride];
-  return (a0 + a1) + (a2 + a3);
-}
-
-// shared memory: key[Gp] (double), idx[Gp] (int, padded), scratch[max(L, blockDim)] (double)
-__global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ layers,
-                                                 const int* __restrict__ list, int pass,
-                                                 const double* __restrict__ partials,
-                                                 double* __restrict__ norms, FlagPtrs flags, Maps m) {
-  extern __shared__ double skey[];
-  const DevLayer& ly = layers[list[blockIdx.x]];
-  const int G = ly.G[pass];
-  const int grp = ly.group[pass];
-  int Gp = 1;
-  while (Gp < G) Gp <<= 1;
-  int* sidx = reinterpret_cast<int*>(skey + Gp);
-  double* scratch = skey + Gp + (Gp + 1) / 2;
-  const double* part = partials + ly.poff[pass];
-  const int nt = blockDim.x;
-  const int t = threadIdx.x;
-  // 1) squared group norms from the K1 partials, fixed summation order
-  if (grp != kFilter) {
-    // per-column partials [nparts][L]: fold the row tiles per column (coalesced),
-    // then the kh*kw columns of each channel
-    const int L = ly.L;
-    for (int col = t; col < L; col += nt) scratch[col] = fold_parts(part + col, ly.nparts, L);
-    __syncthreads();
-    for (int g = t; g < Gp; g += nt) {
-      double key = -1.0;  // padding sorts after every norm (norms >= 0)
-      if (g < G) {
-        double s2 = 0.0;
-        if (grp == kChannel)
-          for (int jx = 0; jx < ly.k; ++jx) s2 += scratch[g * ly.k + jx];
-        else
-          s2 = scratch[g];
-        key = sqrt(s2);
-        norms[ly.goff[pass] + g] = key;
-      }
-      skey[g] = key;
-      sidx[g] = g;
-    }
-  } else {
-    for (int g = t; g < Gp; g += nt) {
-      double key = -1.0;
-      if (g < G) {
-        const double s2 = part[g];  // FILTER: complete per-row sums
-        key = sqrt(s2);
-        norms[ly.goff[pass] + g] = key;
-      }
-      skey[g] = key;
-      sidx[g] = g;
-    }
-  }
-  __syncthreads();
-  uint8_t* fl = flags.f[pass];
-  const int keep = ly.keep[pass];
-  if (Gp <= nt) {
-    // 2a) rank counting: rank(g) = #{j : n_j > n_g} + #{j < g : n_j == n_g} (the
-    //     stable argsort of -norms); T = nt / Gp consecutive lanes share a group
-    //     and fold their counts with shuffles. One barrier instead of a sort.
-    const int T = nt / Gp;  // power of two <= 32 when Gp >= 32
-    const int Tw = T > 32 ? 32 : T;
-    const int g = t / Tw, sl = t % Tw;
-    if (g < Gp) {
-      const double kg = skey[g];
-      int rank = 0;
-      for (int jx = sl; jx < G; jx += Tw) {
-        const double kj = skey[jx];
-        rank += (kj > kg) || (kj == kg && jx < g);
-      }
-      for (int off = Tw >> 1; off > 0; off >>= 1) rank += __shfl_xor_sync(kFull, rank, off, Tw);
-      if (sl == 0 && g < G) {
-        const uint8_t f = rank < keep ? 1 : 0;
-        fl[ly.goff[pass] + g] = f;
-        sidx[g] = f;  // this pass's flags for the keep maps below
-      }
-    }
-  } else {
-  // 2b) bitonic sort: norm descending, index ascending (stable argsort of -norms)
-  for (int size = 2; size <= Gp; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = t; i < Gp; i += nt) {
-        int jx = i ^ stride;
-        if (jx > i) {
-          double ki = skey[i], kj = skey[jx];
-          int ii = sidx[i], ij = sidx[jx];
-          bool i_first = before(ki, ii, kj, ij);
-          bool want_i_first = (i & size) == 0;
-          if (i_first != want_i_first) {
-            skey[i] = kj; skey[jx] = ki;
-            sidx[i] = ij; sidx[jx] = ii;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int pos = t; pos < Gp; pos += nt) {
-    int g = sidx[pos];
-    if (g < G) fl[ly.goff[pass] + g] = pos < keep ? 1 : 0;
-  }
-  __syncthreads();
-  for (int pos = t; pos < Gp; pos += nt) {  // re-index: sidx[g] = flag of group g
-    int g = sidx[pos];
-    if (g < G) skey[g] = pos < keep ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int g = t; g < G; g += nt) sidx[g] = skey[g] != 0.0;
-  }
-  if (pass != ly.ncons - 1) return;
-  __syncthreads();
-  // 3) keep maps for K3: rowkeep = AND of FILTER passes, colkeep = AND of
-  //    CHANNEL / SHAPE passes (block-local global writes are visible after the barrier)
-  // this pass's flags come from shared memory (sidx[g]), earlier passes' from global
-  const int npass = ly.ncons;
-  for (int o = t; o < ly.rows; o += nt) {
-    uint8_t kp = 1;
-    for (int q = 0; q < npass; ++q)
-      if (ly.group[q] == kFilter) kp &= q == pass ? (uint8_t)sidx[o] : flags.f[q][ly.goff[q] + o];
-    m.rowkeep[ly.okeep + o] = kp;
-  }
-  for (int col = t; col < ly.L; col += nt) {
-    uint8_t kp = 1;
-    for (int q = 0; q < npass; ++q) {
-      if (ly.group[q] == kFilter) continue;
-      const int g = ly.group[q] == kChannel ? col / ly.k : col;
-      kp &= q == pass ? (uint8_t)sidx[g] : flags.f[q][ly.goff[q] + g];
-    }
-    m.colkeep[ly.cpoff + col] = kp;
-  }
-}
-
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
-                   double* norms, FlagPtrs flags, Maps maps, size_t smem, cudaStream_t st) {
+                   double* norms, FlagPtrs flags, const KeepArgs& ka, int structured, size_t smem, cudaStream_t st) {
   if (n <= 0) return;
   allow_smem(k_select, smem);
-  k_select<<<n, 1024, smem, st>>>(layers, list, pass, partials, norms, flags, maps);
+  launch_pdl(k_select, n, 1024, smem, st, layers, list, pass, partials, norms, flags, ka, structured);
 }
+
+size_t structured_smem_bytes(int rows, int L, int cin) { return structured_smem(rows, L, cin); }
+size_t select_smem_bytes(int G) { return select_bytes(G); }
 
 // ---------------------------------------------------------------------------
 // K3 project + local mask.  sparsity.py:71-94, 113-115; consensus.py:181-182
 // A thread owns a quad of elements (one row when L % 4 == 0): one float4 load,
-// one uchar4 column-keep load; 8 lanes' nibbles OR-fold into one mask word.
+// a loop-invariant kept nibble for its four columns; 8 lanes' nibbles OR-fold
+// into one mask word.
 // ---------------------------------------------------------------------------
 
 // Layer fields the streaming kernels use, loaded once into registers (stores
@@ -675,44 +1141,79 @@ struct TileCtx {
   __device__ __forceinline__ long long row(int i) const { return r0 + (long long)i * kRowPhases; }
 };
 
-__global__ void __launch_bounds__(kThreads) k_project(const DevLayer* __restrict__ layers,
-                                                      const Item* __restrict__ items,
-                                                      float* __restrict__ zn,
-                                                      uint32_t* __restrict__ mask, Maps m) {
+// CHECK (structured keep sets, one node): flag the layer when a kept element is
+// exactly zero — its mask is then not the rectangle R x C the selection derived
+// the keep sets from, and k_keep_fixup re-derives it from the bits
+__device__ __forceinline__ void flag_irregular(const KeepArgs& a, int pidx, bool bad) {
+  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) {
+    atomicOr(a.irr + pidx, 1);
+    atomicOr(a.irr_any, 1);
+  }
+}
+
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __restrict__ zn,
+                                                         uint32_t* __restrict__ mask) {
+  PDL_ENTRY();
   extern __shared__ float4 ring[];
   __shared__ uint8_t s_rk[kMaxTileRows];
-  const Item it = items[blockIdx.x];
-  const LayerRegs ly(layers, it.layer);
+  const Item it = a.items[blockIdx.x];
+  const LayerRegs ly(a.layers, it.layer);
+  const DevLayer& dl = a.layers[it.layer];
   const int lane = threadIdx.x & 31;
   if (it.tile == 1) {
     // row-quad tile: 8 lanes (same row, 8 consecutive quads) make one mask word
     const TileCtx tc(it, ly.L);
-    for (int r = threadIdx.x; r < it.end - it.begin; r += kThreads) s_rk[r] = m.rowkeep[ly.okeep + it.begin + r];
-    uchar4 ck = tc.valid ? *reinterpret_cast<const uchar4*>(m.colkeep + ly.cpoff + 4 * tc.j)
-                         : make_uchar4(0, 0, 0, 0);
-    __syncthreads();
+    const int nrow = (int)(it.end - it.begin);
     const float* src = zn + ly.off;
     // all lanes of a warp share a row phase; quads past the row end (a suffix of the
     // last chunk, whole 8-lane groups since L % 32 == 0) only join the shuffles
     const int count = __shfl_sync(kFull, tc.count, 0);
+    const bool word_lane = (lane & 7) == 0 && tc.valid;
     auto issue = [&](int d, int i) {
       if (tc.valid) cp16(ring_slot<1>(ring, d, 0), src + tc.row(i) * ly.L + 4 * tc.j);
     };
+    ring_prologue(count, issue);  // the first loads fly while the keep masks are built
+    // kept = AND over the passes' group flags: rows (FILTER) in shared memory,
+    // this thread's four columns (CHANNEL / SHAPE) in a nibble
+    for (int r = threadIdx.x; r < nrow; r += kThreads) {
+      uint8_t kp = 1;
+      for (int q = 0; q < ly.ncons; ++q)
+        if (dl.group[q] == kFilter) kp &= a.flags.f[q][dl.goff[q] + it.begin + r];
+      s_rk[r] = kp;
+    }
+    const FastDiv divk = dl.divk;
+    unsigned ckb = 0;
+    if (tc.valid) {
+      ckb = 0xFu;
+      for (int q = 0; q < ly.ncons; ++q) {
+        const int grp = dl.group[q];
+        if (grp == kFilter) continue;
+        const uint8_t* f = a.flags.f[q] + dl.goff[q];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const unsigned col = 4 * tc.j + b;
+          if (!f[grp == kChannel ? fdiv(col, divk) : col]) ckb &= ~(1u << b);
+        }
+      }
+    }
+    __syncthreads();
+    unsigned bad = 0;  // CHECK: kept but zero
     auto consume = [&](int d, int i) {
       const long long r = tc.row(i);
       const long long e = r * ly.L + 4 * tc.j;
       unsigned nib = 0;
       if (tc.valid) {
         float4 v = *ring_slot<1>(ring, d, 0);
-        const bool rk = s_rk[r - it.begin] != 0;
-        const bool k0 = rk && ck.x, k1 = rk && ck.y, k2 = rk && ck.z, k3 = rk && ck.w;
-        nib = (unsigned)(k0 && v.x != 0.f) | ((unsigned)(k1 && v.y != 0.f) << 1) |
-              ((unsigned)(k2 && v.z != 0.f) << 2) | ((unsigned)(k3 && v.w != 0.f) << 3);
-        if (!(k0 && k1 && k2 && k3)) {
-          if (!k0) v.x = 0.f;
-          if (!k1) v.y = 0.f;
-          if (!k2) v.z = 0.f;
-          if (!k3) v.w = 0.f;
+        const unsigned kn = s_rk[r - it.begin] ? ckb : 0u;  // kept nibble
+        nib = kn & ((unsigned)(v.x != 0.f) | ((unsigned)(v.y != 0.f) << 1) | ((unsigned)(v.z != 0.f) << 2) |
+                    ((unsigned)(v.w != 0.f) << 3));
+        if (CHECK) bad |= kn & ~nib;
+        if (kn != 0xFu) {
+          if (!(kn & 1u)) v.x = 0.f;
+          if (!(kn & 2u)) v.y = 0.f;
+          if (!(kn & 4u)) v.z = 0.f;
+          if (!(kn & 8u)) v.w = 0.f;
           st4(zn + ly.off + e, v);
         }
       }
@@ -720,35 +1221,55 @@ __global__ void __launch_bounds__(kThreads) k_project(const DevLayer* __restrict
       w |= __shfl_xor_sync(kFull, w, 1);
       w |= __shfl_xor_sync(kFull, w, 2);
       w |= __shfl_xor_sync(kFull, w, 4);
-      if ((lane & 7) == 0 && tc.valid) mask[ly.mword + (e >> 5)] = w;
+      if (word_lane) mask[ly.mword + (e >> 5)] = w;
     };
-    ring_run(count, issue, consume);
+    ring_loop(count, issue, consume);
+    if (CHECK) flag_irregular(a, dl.pidx, bad != 0);
     return;
   }
-  // contiguous ranges of other prunable layers: one warp per 32-element word
+  // contiguous ranges of other prunable layers: one warp per 32-element word; the
+  // passes' group kinds and flag bases in registers
+  int gq[kMaxPasses];
+  const uint8_t* fq[kMaxPasses];
+#pragma unroll
+  for (int q = 0; q < kMaxPasses; ++q) {
+    gq[q] = q < ly.ncons ? dl.group[q] : -1;
+    fq[q] = q < ly.ncons ? a.flags.f[q] + dl.goff[q] : nullptr;
+  }
+  const FastDiv divk = dl.divk;
   const int warp = threadIdx.x >> 5;
   const long long w0 = it.begin >> 5, w1 = (it.end + 31) >> 5;
+  bool bad = false;
   for (long long w = w0 + warp; w < w1; w += kThreads / 32) {
     long long e = (w << 5) + lane;
     bool kp = false;
     float x = 0.f;
     if (e < ly.n) {
-      unsigned o = fdiv((unsigned)e, ly.divL);
-      unsigned col = (unsigned)e - o * (unsigned)ly.L;
-      kp = m.rowkeep[ly.okeep + o] && m.colkeep[ly.cpoff + col];
+      const unsigned o = fdiv((unsigned)e, ly.divL);
+      const unsigned col = (unsigned)e - o * (unsigned)ly.L;
+      const unsigned c = fdiv(col, divk);
+      kp = true;
+#pragma unroll
+      for (int q = 0; q < kMaxPasses; ++q)
+        if (gq[q] >= 0) kp = kp && fq[q][group_of(gq[q], o, col, c)];
       x = zn[ly.off + e];
       if (!kp) zn[ly.off + e] = 0.f;
     }
-    unsigned bits = __ballot_sync(kFull, kp && x != 0.0f);
+    const bool bit = kp && x != 0.0f;
+    if (CHECK) bad |= kp && !bit;
+    const unsigned bits = __ballot_sync(kFull, bit);
     if (lane == 0) mask[ly.mword + w] = bits;
   }
+  if (CHECK) flag_irregular(a, dl.pidx, bad);
 }
 
-void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
-                    uint32_t* mask, Maps maps, cudaStream_t st) {
+void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * kThreads * sizeof(float4);
-  k_project<<<n_items, kThreads, smem, st>>>(layers, items, zn, mask, maps);
+  if (check)
+    launch_pdl(k_project<true>, n_items, kThreads, smem, st, a, zn, mask);
+  else
+    launch_pdl(k_project<false>, n_items, kThreads, smem, st, a, zn, mask);
 }
 
 // ---------------------------------------------------------------------------
@@ -757,6 +1278,7 @@ void launch_project(const DevLayer* layers, const Item* items, int n_items, floa
 // ---------------------------------------------------------------------------
 
 __global__ void k_mask_or(MaskPtrs g, long long words, uint32_t* __restrict__ out, int vec) {
+  PDL_ENTRY();
   const long long n4 = vec ? (words >> 2) : 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
@@ -781,93 +1303,16 @@ void launch_mask_or(const MaskPtrs& g, long long words, uint32_t* out, cudaStrea
   for (int r = 0; r < g.n; ++r) vec &= (reinterpret_cast<uintptr_t>(g.p[r]) & 15) == 0;
   long long n = vec ? (words >> 2) : words;
   int grid = (int)std::min<long long>(std::max<long long>((n + 255) / 256, 1), 148LL * 16);
-  k_mask_or<<<grid, 256, 0, st>>>(g, words, out, vec);
+  launch_pdl(k_mask_or, grid, 256, 0, st, g, words, out, vec);
 }
 
 // ---------------------------------------------------------------------------
-// K5 keep sets from the union mask, one launch (shrinkage.py:45-58,
-// derive_keep_sets; sparsity.py:118-122 drift numerator; transport.py:239-280
-// concatenation order):
-//  a) every CTA marks the K_out / K_in "any" flags of its word range and
-//     accumulates popcount(union) and popcount(union ^ prev);
-//  b) the last CTA to finish a layer scans its flags into positions, row bases
-//     and column positions of the compact rectangle and the payload size;
-//  c) the last layer to finish lays out the flat buffer (exclusive scan of
-//     payload sizes over all layers, in layer order).
+// K5 keep sets from the union mask, one launch: items are word ranges of one
+// layer; marks with a skip over the rest of each (o, c) kernel run.
 // ---------------------------------------------------------------------------
-
-__device__ int block_exclusive_scan(int x, int* warp_tot, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = x;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    int y = __shfl_up_sync(kFull, incl, off);
-    if (lane >= off) incl += y;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int nw = blockDim.x >> 5;
-    int t = lane < nw ? warp_tot[lane] : 0;
-    int ti = t;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      int y = __shfl_up_sync(kFull, ti, off);
-      if (lane >= off) ti += y;
-    }
-    if (lane < nw) warp_tot[lane] = ti - t;
-    if (lane == 31) *total = ti;
-  }
-  __syncthreads();
-  int r = incl - x + warp_tot[warp];
-  __syncthreads();
-  return r;
-}
-
-// exclusive positions of set flags (-1 for clear ones) into global `pos` and
-// shared `spos`; flags are read through L2 (written by other CTAs of this
-// launch), all of a thread's flags loaded before the scans
-__device__ int scan_flags(const uint8_t* flags, int n, int* pos, int* spos) {
-  __shared__ int warp_tot[32];
-  __shared__ int total;
-  constexpr int kMaxRounds = 8;  // n <= 8 * blockDim (2048 with 256 threads)
-  int f[kMaxRounds];
-#pragma unroll
-  for (int r = 0; r < kMaxRounds; ++r) {
-    const int i = r * (int)blockDim.x + threadIdx.x;
-    f[r] = (i < n && __ldcg(flags + i)) ? 1 : 0;
-  }
-  int carry = 0;
-#pragma unroll
-  for (int r = 0; r < kMaxRounds; ++r) {  // static indices keep f[] in registers
-    const int base = r * (int)blockDim.x;
-    if (base >= n) break;
-    const int i = base + threadIdx.x;
-    const int ex = block_exclusive_scan(f[r], warp_tot, &total);
-    const int p = f[r] ? carry + ex : -1;
-    if (i < n) {
-      pos[i] = p;
-      spos[i] = p;
-    }
-    carry += total;
-    __syncthreads();
-  }
-  for (int base = kMaxRounds * (int)blockDim.x; base < n; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const int fr = (i < n && __ldcg(flags + i)) ? 1 : 0;
-    const int ex = block_exclusive_scan(fr, warp_tot, &total);
-    const int p = fr ? carry + ex : -1;
-    if (i < n) {
-      pos[i] = p;
-      spos[i] = p;
-    }
-    carry += total;
-    __syncthreads();
-  }
-  return carry;
-}
 
 __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
+  PDL_ENTRY();
   extern __shared__ uint8_t sflag[];
   const Item it = a.items[blockIdx.x];
   const int l = it.layer;
@@ -902,106 +1347,107 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
       x = skip >= 32 ? 0u : (x & ~((1u << skip) - 1u));
     }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    pop += __shfl_xor_sync(kFull, pop, off);
-    drift += __shfl_xor_sync(kFull, drift, off);
-  }
-  long long* row = a.summary + (long long)l * kSumCols;
-  if ((threadIdx.x & 31) == 0) {
-    if (pop) atomicAdd(reinterpret_cast<unsigned long long*>(row + 5), pop);
-    if (drift) atomicAdd(reinterpret_cast<unsigned long long*>(row + 4), drift);
-  }
   __syncthreads();
   for (int i = threadIdx.x; i < ly.cin; i += kThreads)
     if (s_in[i]) a.iflag[ly.ikeep + i] = 1;
   for (int i = threadIdx.x; i < nr; i += kThreads)
     if (s_out[i]) a.oflag[ly.okeep + r_lo + i] = 1;
-  // b) the layer's last CTA derives its keep sets. One gpu-scope fence by thread 0
-  //    after the barrier releases every thread's flag writes (cumulative release).
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(a.layer_done + ly.pidx, 1u) == (unsigned)it.chunk - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // the mark flags in shared memory are no longer needed: reuse for positions
-  int* s_pin = reinterpret_cast<int*>(sflag);
-  int* s_pout = s_pin + ly.cin;
-  int n_in = scan_flags(a.iflag + ly.ikeep, ly.cin, a.pos_in + ly.ikeep, s_pin);
-  int n_out = scan_flags(a.oflag + ly.okeep, ly.rows, a.pos_out + ly.okeep, s_pout);
-  // leave the any-flags zeroed for the next derivation (no memset launches)
-  for (int i = threadIdx.x; i < ly.cin; i += kThreads) a.iflag[ly.ikeep + i] = 0;
-  for (int i = threadIdx.x; i < ly.rows; i += kThreads) a.oflag[ly.okeep + i] = 0;
-  const int rowlen = n_in * ly.k;
-  for (int o = threadIdx.x; o < ly.rows; o += kThreads) {
-    int po = s_pout[o];
-    a.maps.rowbase[ly.okeep + o] = po >= 0 ? po * rowlen : -1;
-  }
-  for (int col = threadIdx.x; col < ly.L; col += kThreads) {
-    unsigned c = fdiv((unsigned)col, ly.divk), jx = (unsigned)col - c * (unsigned)ly.k;
-    int pi = s_pin[c];
-    a.maps.colpos[ly.cpoff + col] = pi >= 0 ? pi * ly.k + (int)jx : -1;
-  }
-  __shared__ bool last_layer;
-  if (threadIdx.x == 0) {
-    row[0] = n_out;
-    row[1] = n_in;
-    row[2] = (long long)n_out * n_in * ly.k;
-    a.layer_done[ly.pidx] = 0;
-    __threadfence();
-    last_layer = atomicAdd(a.done, 1u) == (unsigned)a.n_prunable - 1;
-  }
-  __syncthreads();
-  if (!last_layer) return;
-  __threadfence();
-  // c) flat-buffer layout
-  __shared__ long long wsum[32];
-  __shared__ long long carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int base = 0; base < a.n_layers; base += kThreads) {
-    int i = base + threadIdx.x;
-    volatile long long* ri = a.summary + (long long)i * kSumCols;
-    long long e = i < a.n_layers ? ri[2] : 0;
-    long long incl = e;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      long long y = __shfl_up_sync(kFull, incl, off);
-      if (lane >= off) incl += y;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      long long t = lane < kThreads / 32 ? wsum[lane] : 0, ti = t;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        long long y = __shfl_up_sync(kFull, ti, off);
-        if (lane >= off) ti += y;
-      }
-      wsum[lane] = ti - t;
-    }
-    __syncthreads();
-    long long ex = carry + wsum[warp] + incl - e;
-    if (i < a.n_layers) ri[3] = ex;
-    __syncthreads();
-    if (threadIdx.x == kThreads - 1) carry = ex + e;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    a.summary[(long long)a.n_layers * kSumCols] = carry;
-    *a.done = 0;
-  }
+  __syncthreads();  // the tail reuses the mark flags' shared memory for positions
+  keep_mark_done(a, l, ly, it.chunk, pop, drift, sflag);
 }
 
 void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st) {
   if (n_items <= 0) return;
   allow_smem(k_keep_sets, smem);
-  k_keep_sets<<<n_items, kThreads, smem, st>>>(a);
+  launch_pdl(k_keep_sets, n_items, kThreads, smem, st, a);
+}
+
+// After the structured derivation (one CTA per prunable layer): a layer whose
+// mask has a kept zero (irr bit 0, set by K3) is derived exactly from its mask
+// bits; a layer whose previous mask was irregular (bit 1) gets its drift
+// counted from the bits. The common case (neither) returns at once; when some
+// layer was re-derived, the last CTA lays out the flat buffer again.
+// smem: align16(c_in + rows) + 4 * (c_in + rows) bytes.
+__global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* __restrict__ prunable) {
+  PDL_ENTRY();
+  extern __shared__ __align__(16) uint8_t fsm[];
+  const int l = prunable[blockIdx.x];
+  const DevLayer& gly = a.layers[l];
+  const int pidx = gly.pidx;
+  const int irr = a.irr[pidx];
+  const int any = *reinterpret_cast<volatile int*>(a.irr_any);
+  if (irr & 3) {
+    const int cin = gly.cin, rows = gly.rows, k = gly.k, L = gly.L;
+    const long long n = gly.n, mword = gly.mword, ikeep = gly.ikeep, okeep = gly.okeep, cpoff = gly.cpoff;
+    const FastDiv divL = gly.divL, divk = gly.divk;
+    uint8_t* s_in = fsm;
+    uint8_t* s_out = fsm + cin;
+    int* s_pin = reinterpret_cast<int*>(fsm + ((size_t)cin + rows + 15) / 16 * 16);
+    int* s_pout = s_pin + cin;
+    const bool exact = irr & 1;
+    for (int i = threadIdx.x; i < cin + rows; i += blockDim.x) fsm[i] = 0;
+    __syncthreads();
+    unsigned long long pop = 0, drift = 0;
+    const long long nw = (n + 31) >> 5;
+    for (long long w = threadIdx.x; w < nw; w += blockDim.x) {
+      const long long e0 = w << 5;
+      const long long nvalid = n - e0;
+      const uint32_t valid = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
+      uint32_t x = a.uni[mword + w] & valid;
+      pop += __popc(x);
+      if (a.prev) drift += __popc((x ^ a.prev[mword + w]) & valid);
+      while (exact && x) {  // marks, skipping the rest of each (o, c) kernel run
+        const int b = __ffs(x) - 1;
+        const unsigned e = (unsigned)(e0 + b);
+        const unsigned o = fdiv(e, divL);
+        const unsigned col = e - o * (unsigned)L;
+        const unsigned c = fdiv(col, divk);
+        const unsigned jx = col - c * (unsigned)k;
+        s_out[o] = 1;
+        s_in[c] = 1;
+        const int skip = b + (int)((unsigned)k - jx);
+        x = skip >= 32 ? 0u : (x & ~((1u << skip) - 1u));
+      }
+    }
+    pop = block_sum(pop);
+    drift = block_sum(drift);
+    if (exact) {
+      __syncthreads();
+      const int2 nio = scan_keep<true>(s_in, cin, s_out, rows, a.pos_in + ikeep, a.pos_out + okeep, s_pin, s_pout);
+      write_maps(a, rows, L, k, okeep, cpoff, divk, s_pin, s_pout, nio.x);
+      if (threadIdx.x == 0) {
+        long long* row = a.summary + (long long)l * kSumCols;
+        row[0] = nio.y;
+        row[1] = nio.x;
+        row[2] = (long long)nio.y * nio.x * k;
+        row[5] = (long long)pop;
+      }
+    }
+    if (threadIdx.x == 0) a.summary[(long long)l * kSumCols + 4] = (long long)drift;
+  }
+  if (threadIdx.x == 0) a.irr[pidx] = (irr & 1) << 1;  // this mask is the next one's previous
+  if (!any) return;
+  // some layer was re-derived: the last CTA lays the flat buffer out again
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.done, 1u) == (unsigned)a.n_prunable - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  layout_flat(a);
+  if (threadIdx.x == 0) {
+    *a.done = 0;
+    *a.irr_any = 0;
+  }
+}
+
+void launch_keep_fixup(const KeepArgs& a, const int* prunable, int n, size_t smem, cudaStream_t st) {
+  if (n <= 0) return;
+  allow_smem(k_keep_fixup, smem);
+  launch_pdl(k_keep_fixup, n, kThreads, smem, st, a, prunable);
 }
 
 // ---------------------------------------------------------------------------
@@ -1043,6 +1489,7 @@ __device__ __forceinline__ int4 add_base(int rb, int4 cp) {
 
 // K6: flat[payload] <- z_node + v  (+ u <- u + (theta - z_node)) for one item
 __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
+  PDL_ENTRY();
   extern __shared__ float4 ring[];
   __shared__ int s_rb[kMaxTileRows];
   const Item it = a.items[blockIdx.x];
@@ -1106,13 +1553,14 @@ void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * 4 * kThreads * sizeof(float4);
   allow_smem(k_compact, smem);
-  k_compact<<<n_items, kThreads, smem, st>>>(a);
+  launch_pdl(k_compact, n_items, kThreads, smem, st, a);
 }
 
 // K7: z <- zero-filled gather of flat / divisor (+ v <- v + (z_node - z)); the
 // gather streams through the ring: dropped coordinates are zero-filled by
 // cp.async without touching memory.
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
+  PDL_ENTRY();
   constexpr int NB = 3;
   extern __shared__ float4 ring[];
   __shared__ int s_rb[kMaxTileRows];
@@ -1183,7 +1631,7 @@ void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
   allow_smem(k_decompact, smem);
-  k_decompact<<<n_items, kThreads, smem, st>>>(a);
+  launch_pdl(k_decompact, n_items, kThreads, smem, st, a);
 }
 
 // ---------------------------------------------------------------------------
@@ -1195,6 +1643,7 @@ void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
 
 __global__ void __launch_bounds__(kThreads) k_average(PeerPtrs src, const long long* __restrict__ total_p,
                                                       double div, float* __restrict__ out) {
+  PDL_ENTRY();
   const long long total = *total_p;
   const long long n4 = total >> 2;
   const long long stride = (long long)gridDim.x * kThreads;
@@ -1234,7 +1683,7 @@ void launch_average(const PeerPtrs& src, const long long* total, long long max_e
                     cudaStream_t st) {
   if (src.n <= 0 || max_elems <= 0) return;
   int grid = (int)std::min<long long>(std::max<long long>((max_elems / 4 + kThreads - 1) / kThreads, 1), 148LL * 8);
-  k_average<<<grid, kThreads, 0, st>>>(src, total, div, out);
+  launch_pdl(k_average, grid, kThreads, 0, st, src, total, div, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1249,6 +1698,7 @@ void launch_average(const PeerPtrs& src, const long long* total, long long max_e
 __global__ void __launch_bounds__(kThreads) k_slices(PeerPtrs src, const long long* __restrict__ total_p,
                                                      long long total_h, int part, double div,
                                                      float* __restrict__ out) {
+  PDL_ENTRY();
   const long long total = total_p ? *total_p : total_h;
   const long long slice = ((total + src.n - 1) / src.n + 31) / 32 * 32;
   long long b = 0, e = total;
@@ -1294,7 +1744,7 @@ void launch_slices(const PeerPtrs& src, const long long* total_p, long long tota
   if (src.n <= 0 || max_elems <= 0) return;
   const long long span = part >= 0 ? (max_elems + src.n - 1) / src.n : max_elems;
   int grid = (int)std::min<long long>(std::max<long long>((span / 4 + kThreads - 1) / kThreads, 1), 148LL * 8);
-  k_slices<<<grid, kThreads, 0, st>>>(src, total_p, total_h, part, div, out);
+  launch_pdl(k_slices, grid, kThreads, 0, st, src, total_p, total_h, part, div, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1342,6 +1792,7 @@ static int stream_grid(long long n4) {
 __global__ void __launch_bounds__(kThreads) k_add(const float* __restrict__ a,
                                                   const float* __restrict__ b,
                                                   float* __restrict__ out, long long n) {
+  PDL_ENTRY();
   const long long n4 = n >> 2;
   const long long stride = (long long)gridDim.x * kThreads;
   for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n4; i += stride) {
@@ -1354,12 +1805,13 @@ __global__ void __launch_bounds__(kThreads) k_add(const float* __restrict__ a,
 
 void launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t st) {
   if (n <= 0) return;
-  k_add<<<stream_grid(n >> 2), kThreads, 0, st>>>(a, b, out, n);
+  launch_pdl(k_add, stream_grid(n >> 2), kThreads, 0, st, a, b, out, n);
 }
 
 __global__ void __launch_bounds__(kThreads) k_dual(const float* __restrict__ th,
                                                    float* __restrict__ u,
                                                    const float* __restrict__ zn, long long n) {
+  PDL_ENTRY();
   const long long n4 = n >> 2;
   const long long stride = (long long)gridDim.x * kThreads;
   for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n4; i += stride) {
@@ -1373,7 +1825,7 @@ __global__ void __launch_bounds__(kThreads) k_dual(const float* __restrict__ th,
 
 void launch_dual(const float* theta, float* u, const float* zn, long long n, cudaStream_t st) {
   if (n <= 0) return;
-  k_dual<<<stream_grid(n >> 2), kThreads, 0, st>>>(theta, u, zn, n);
+  launch_pdl(k_dual, stream_grid(n >> 2), kThreads, 0, st, theta, u, zn, n);
 }
 
 // ---------------------------------------------------------------------------

@@ -45,7 +45,7 @@ struct DevLayer {
   long long ikeep;  // offset of this layer's K_in flags / positions
   long long cpoff;  // offset of this layer's column maps (colpos / colkeep), multiple of 4
   long long goff[kMaxPasses];  // offset into norms / keep flags per pass
-  long long poff[kMaxPasses];  // offset into group-norm partials per pass
+  long long poff[kMaxPasses];  // offset into group-norm partials per pass ([nparts][G]; FILTER [G])
   int rows, cin, k, L;         // rank-4: c_out, c_in, kh*kw, c_in*kh*kw; rank-2: d0, d1, 1, d1
   int ncons;                   // number of constraints (0 = dense path)
   int nparts;                  // row tiles of the candidate kernel (partials rows)
@@ -53,11 +53,15 @@ struct DevLayer {
   int rank;
   int tiling;                  // 0: row tiles (partials per group / row), 1: quad tiles (per column)
   int qtile;                   // K3/K6/K7 use row-quad tiles (prunable, c_in*kh*kw % 32 == 0)
-  int pad2;
+  int fsel;                    // bit q: pass q's selection runs in K1's tail (no K2 launch)
   int pidx;                    // index among prunable layers
   int group[kMaxPasses];
   int keep[kMaxPasses];
   int G[kMaxPasses];
+  int ncitems;                 // K1 items of the layer (dynamic launch)
+  int npitems;                 // K3 items of the layer
+  int cq;                      // K1 quad tiles: column quads per tile (whole channels)
+  int pad3;
   FastDiv divL, divk;
   double rho1, rho2, gamma;
   double rgamma;               // RN(1 / gamma), for the FMA-corrected division
@@ -85,6 +89,40 @@ struct MaskPtrs {
   int n;
 };
 
+struct FlagPtrs {
+  uint8_t* f[kMaxPasses];
+};
+
+// per-layer payload maps derived from the keep sets (all prunable layers)
+struct Maps {
+  int* rowbase;       // [sum rows]  pos_out[o] * |K_in| * k, or -1
+  int* colpos;        // [sum L]     pos_in[c] * k + j, or -1
+};
+
+struct KeepArgs {
+  const DevLayer* layers;
+  const Item* items;
+  const uint32_t* uni;
+  const uint32_t* prev;
+  uint8_t* oflag;
+  uint8_t* iflag;
+  int* pos_out;
+  int* pos_in;
+  Maps maps;
+  FlagPtrs flags;            // group keep flags of every pass (K3: kept = AND of the passes)
+  long long* summary;
+  unsigned int* layer_done;  // per prunable layer
+  unsigned int* done;        // prunable layers finished
+  unsigned long long* acc;   // per prunable layer: drift, popcount accumulators (zero between launches)
+  // structured keep sets (one node)
+  uint8_t* rk_prev;          // [sum rows] rows of the previous rectangle R x C
+  uint8_t* ck_prev;          // [sum L]    columns of the previous rectangle
+  int* irr;                  // per prunable layer: bit 0 a kept zero now, bit 1 previously
+  int* irr_any;              // some layer has a kept zero now
+  int n_layers;
+  int n_prunable;
+};
+
 struct CandArgs {
   const float* __restrict__ s;
   const float* __restrict__ theta;
@@ -98,17 +136,15 @@ struct CandArgs {
   double* __restrict__ partials;       // this pass
   const uint8_t* flags[kMaxPasses];    // keep flags of earlier passes (renorm)
   PeerPtrs peers;                      // n > 0: S = sum of the peers' theta + u (rank order)
+  // fused selection (K2 in the tail of each layer's last K1 tile)
+  double* norms;                       // this pass
+  FlagPtrs fw;                         // keep flags, all passes (this pass written)
+  unsigned int* cand_done;             // per prunable layer: K1 tiles finished
+  KeepArgs ka;                         // structured keep sets at the last pass (one node)
+  int structured;
   int pass;
   int identity;                        // candidate = input (per-tensor API)
   int sqcap;                           // doubles of the sq sub-tile region
-};
-
-// per-layer maps derived from the keep flags / keep sets (all prunable layers)
-struct Maps {
-  uint8_t* rowkeep;   // [sum rows]  AND of FILTER passes
-  uint8_t* colkeep;   // [sum L]     AND of CHANNEL / SHAPE passes
-  int* rowbase;       // [sum rows]  pos_out[o] * |K_in| * k, or -1
-  int* colpos;        // [sum L]     pos_in[c] * k + j, or -1
 };
 
 struct ElemArgs {
@@ -129,31 +165,16 @@ struct ElemArgs {
 };
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st);
-struct FlagPtrs {
-  uint8_t* f[kMaxPasses];
-};
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
-                   double* norms, FlagPtrs flags, Maps maps, size_t smem, cudaStream_t st);
-void launch_project(const DevLayer* layers, const Item* items, int n_items, float* zn,
-                    uint32_t* mask, Maps maps, cudaStream_t st);
+                   double* norms, FlagPtrs flags, const KeepArgs& ka, int structured, size_t smem, cudaStream_t st);
 void launch_mask_or(const MaskPtrs& g, long long words, uint32_t* out, cudaStream_t st);
-struct KeepArgs {
-  const DevLayer* layers;
-  const Item* items;
-  const uint32_t* uni;
-  const uint32_t* prev;
-  uint8_t* oflag;
-  uint8_t* iflag;
-  int* pos_out;
-  int* pos_in;
-  Maps maps;
-  long long* summary;
-  unsigned int* layer_done;  // per prunable layer
-  unsigned int* done;        // prunable layers finished
-  int n_layers;
-  int n_prunable;
-};
 void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st);
+void launch_keep_fixup(const KeepArgs& a, const int* prunable, int n, size_t smem, cudaStream_t st);
+// K3; check != 0: flag layers with a kept zero (structured keep sets)
+void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st);
+// shared memory of the structured keep-set derivation (K1 / K2 tail)
+size_t structured_smem_bytes(int rows, int L, int cin);
+size_t select_smem_bytes(int G);
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_slices(const PeerPtrs& src, const long long* total_p, long long total_h, long long max_elems,

@@ -121,6 +121,10 @@ class Plan:
             self._h = C.c_void_p()
 
     # -- configuration ---------------------------------------------------------
+    def set_single_node(self, on: bool):
+        """Structured keep sets in the selection tail (one node: the union is the local mask)."""
+        _lib.call("hsx_plan_set_single_node", self._h, 1 if on else 0)
+
     def set_penalties(self, rho1: dict | None, rho2: dict | None, weight_decay: float,
                       num_nodes: int, accels_per_node: int, identity: bool = False):
         def arr(d):
@@ -229,9 +233,18 @@ class Plan:
         with timed("K3_project"):
             _lib.call("hsx_project", self._h, ptr(z_node), ptr(local_mask), current_stream())
 
-    def project_all(self, s, theta, u, z, v, z_node, local_mask, peers=None):
+    def project_keep_sets(self, z_node, mask, prev_mask=None):
+        """K3 + K5 in one launch (one node: the union is the local mask)."""
+        with timed("K3_project_keep"):
+            _lib.call("hsx_project_keep_sets", self._h, ptr(z_node), ptr(mask), ptr(prev_mask),
+                      current_stream())
+
+    def project_all(self, s, theta, u, z, v, z_node, local_mask, peers=None, keep_prev=False,
+                    prev_mask=None):
         """K2 (+ composite passes) + K3 after hsx_candidate (peers: the sends of
-        hsx_candidate_peers, re-read by composite passes)."""
+        hsx_candidate_peers, re-read by composite passes). keep_prev: K3 also derives
+        the keep sets from the mask it writes (hsx_project_keep_sets, prev_mask for
+        the drift count)."""
         for p in range(self.max_passes):
             if p > 0:
                 if peers:
@@ -243,7 +256,10 @@ class Plan:
                 else:
                     self.renorm(p, s, theta, u, z, v)
             self.select(p)
-        self.project(z_node, local_mask)
+        if keep_prev:
+            self.project_keep_sets(z_node, local_mask, prev_mask)
+        else:
+            self.project(z_node, local_mask)
 
     def group_norms(self, p: int, device):
         total = int(self._lib.hsx_plan_group_total(self._h, p))

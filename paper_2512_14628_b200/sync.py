@@ -73,6 +73,9 @@ class HSADMMSync:
                   for ls in layers if constraints.get(ls.name)}
         self.plan = Plan(self.layers, groups, schedule.rho1, schedule.rho2)
         self.plan.set_penalties(schedule.rho1, schedule.rho2, settings.weight_decay, self.M, self.P)
+        # one node: the union mask is every rank's local mask, so the selection derives
+        # the keep sets of the kept rectangle and K3 only checks it (hsx_project_keep_sets)
+        self.plan.set_single_node(self.M == 1)
         self.prunable = self.plan.prunable
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         pl, dev = self.plan, self.device
@@ -107,6 +110,11 @@ class HSADMMSync:
         self.transport = transport
         if transport == "peer":
             self._init_peer_buffers()
+        # deferred host bookkeeping (step_host): a step returns once its launches are
+        # queued; the keep-set counts are read back when the next step starts
+        self.defer_host = False
+        self._pending = None
+        self._pipe = None
 
     def _init_peer_buffers(self):
         """Shared (peer-mapped) buffers; allocation is collective over each group."""
@@ -189,6 +197,7 @@ class HSADMMSync:
     # -- the per-iteration program ------------------------------------------------------
     def program(self, k: int):
         """Generator: yields collective requests, performs phases 2-5(u) of iteration k."""
+        self.settle()
         if self.transport == "peer":
             return (yield from self._program_peer(k))
         return (yield from self._program_nccl(k))
@@ -236,18 +245,20 @@ class HSADMMSync:
             pl.candidate_peers(peers, self.z, self.v, self.z_node, frozen_mask=fmask)
         else:
             pl.candidate(None, self.theta, self.u, self.z, self.v, self.z_node, frozen_mask=fmask)
-        if dynamic:
+        # one node: every rank's local mask is the node's (identical z_node), so the
+        # union needs no exchange and K3 derives the keep sets itself
+        fused_keep = dynamic and self.M == 1 and k % self.settings.sync_period == 0
+        if fused_keep:
+            pl.project_all(s_local, self.theta, self.u, self.z, self.v, self.z_node, self.union, peers=peers,
+                           keep_prev=True, prev_mask=self.masks)
+        elif dynamic:
             local = self.p_lmask.tensor if self.p_lmask is not None else self.local_mask
             pl.project_all(s_local, self.theta, self.u, self.z, self.v, self.z_node, local, peers=peers)
         if k % self.settings.sync_period != 0:
             pl.dual_intra(self.theta, self.u, self.z_node)
             return None
         ev = None
-        if dynamic and self.M == 1:
-            # one node: every rank's local mask is the node's (identical z_node), so the
-            # union needs no exchange
-            mask_or_ptrs([local.data_ptr()], pl.mask_words, self.union)
-            pl.keep_sets(self.union, self.masks)
+        if fused_keep:
             ev = pl.keep_sets_fetch_async()
         elif dynamic:
             words = pl.mask_words
@@ -271,12 +282,7 @@ class HSADMMSync:
             # result is bitwise what the intra broadcast would deliver)
             pl.compact_dual(self.theta, self.u, self.z_node, self.v, self.flat)
             pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
-            if ev is not None:
-                ev.synchronize()
-                self._after_keep_sets()
-            if self.is_leader:
-                self._log_zsync(k)
-            return (yield from self._finish_dynamic(k, dynamic))
+            return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
         if self.is_leader:
             if self.M > 1:
                 flat = self.p_flat[k & 1]
@@ -302,24 +308,41 @@ class HSADMMSync:
                 pl.average_peers([self.p_zhat.peer_ptrs()[0]], 1.0, self.flat, tag="K8_zhat_read")
                 dst = self.flat
         pl.decompact_dual(dst, 1.0, self.z_node, self.v, self.z)
-        if ev is not None:
-            ev.synchronize()
-            self._after_keep_sets()
-        if self.is_leader:
-            self._log_zsync(k)
-        return (yield from self._finish_dynamic(k, dynamic))
+        return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
 
-    def _finish_dynamic(self, k: int, dynamic: bool):
-        """masks <- union; freeze + seal (consensus.py:600-606)."""
+    def _end_step(self, k: int, dynamic: bool, ev, log_zsync: bool):
+        """masks <- union; host bookkeeping now, or at the next step (defer_host)."""
         if dynamic:
-            mask_or_ptrs([self.union.data_ptr()], self.plan.mask_words, self.masks)
+            self.masks, self.union = self.union, self.masks
+        if ev is not None and self.defer_host:
+            self._pending = (k, ev, log_zsync)
+        else:
+            if ev is not None:
+                ev.synchronize()
+                self._after_keep_sets()
+            self._host_tail(k, dynamic, log_zsync)
+        return None
+        yield  # pragma: no cover  (generator)
+
+    def _host_tail(self, k: int, dynamic: bool, log_zsync: bool):
+        """Ledger of the leader average; freeze + seal (consensus.py:600-606)."""
+        if log_zsync and self.is_leader:
+            self._log_zsync(k)
         if dynamic and freeze_check(k, self.settings.t_freeze, self.drift_history,
                                     self.settings.drift_window):
             self.frozen = True
             if self.is_leader:
                 self.cache_hits += len(self.prunable)
-        return None
-        yield  # pragma: no cover  (generator)
+
+    def settle(self) -> None:
+        """Finish the deferred host bookkeeping of the last step (waits for its counts)."""
+        if self._pending is None:
+            return
+        k, ev, log_zsync = self._pending
+        self._pending = None
+        ev.synchronize()
+        self._after_keep_sets()
+        self._host_tail(k, True, log_zsync)
 
     def _program_nccl(self, k: int):
         pl = self.plan
@@ -333,20 +356,25 @@ class HSADMMSync:
         # phase 3: node candidate, projection or frozen mask
         pl.candidate(s, self.theta, self.u, self.z, self.v, self.z_node,
                      frozen_mask=self.masks if (frozen and self.prunable) else None)
-        if dynamic:
+        # one node: every rank's local mask is the union (identical z_node), so K3
+        # derives the keep sets from the bits it writes (no exchange, no K5)
+        fused_keep = dynamic and self.M == 1 and k % self.settings.sync_period == 0
+        if fused_keep:
+            pl.project_all(s, self.theta, self.u, self.z, self.v, self.z_node, self.union,
+                           keep_prev=True, prev_mask=self.masks)
+        elif dynamic:
             pl.project_all(s, self.theta, self.u, self.z, self.v, self.z_node, self.local_mask)
         if k % self.settings.sync_period != 0:
             pl.dual_intra(self.theta, self.u, self.z_node)
             return None
         # phase 4: mask union (leaders), broadcast to followers, keep sets
         ev = None
-        if dynamic:
+        if fused_keep:
+            ev = pl.keep_sets_fetch_async()
+        elif dynamic:
             if self.is_leader:
-                if self.M > 1:
-                    yield AllGather(self.inter, self.local_mask, self.gathered, "mask_sync", k)
-                    mask_or(self.gathered, self.M, pl.mask_words, self.union)
-                else:
-                    self.union, self.local_mask = self.local_mask, self.union
+                yield AllGather(self.inter, self.local_mask, self.gathered, "mask_sync", k)
+                mask_or(self.gathered, self.M, pl.mask_words, self.union)
             if self.P > 1:
                 yield Broadcast(self.intra, self.leader_rank, self.union, "m_bcast", k)
             pl.keep_sets(self.union, self.masks)
@@ -370,20 +398,79 @@ class HSADMMSync:
         if self.P > 1 and total > 0:
             yield Broadcast(self.intra, self.leader_rank, self.flat[:total], "zhat_bcast", k)
         pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
-        if ev is not None:                       # single GPU: K6 / K7 are already queued
-            ev.synchronize()
-            self._after_keep_sets()
-        if self.is_leader and not collectives:   # M == 1: the average is the identity (ledger only)
-            yield from self._leader_average(k)
-        if dynamic:
-            self.masks, self.union = self.union, self.masks
-        # freeze + seal (consensus.py:600-606)
-        if dynamic and freeze_check(k, self.settings.t_freeze, self.drift_history,
-                                    self.settings.drift_window):
-            self.frozen = True
-            if self.is_leader:
-                self.cache_hits += len(self.prunable)   # cache.get on the final masks, then seal
-        return None
+        # one rank (no collectives): K6 / K7 are queued, the counts land meanwhile; the
+        # leader average is the identity (ledger entries only)
+        return (yield from self._end_step(k, dynamic, ev, log_zsync=not collectives))
+
+    # -- host-buffer steps ---------------------------------------------------------------
+    def step_host(self, k: int, theta_host: torch.Tensor, z_host: torch.Tensor | None = None):
+        """Iteration k fed from, and returned to, pinned host memory (flat fp32 arenas).
+
+        theta_host is copied in on a copy stream into one of two device theta
+        buffers, the step runs on the current stream once it has landed, and z is
+        copied out to z_host on a second copy stream (from one of two staging
+        buffers). Host bookkeeping is deferred to the next call, so consecutive
+        calls overlap: step k+1's input copy and step k's output copy run while
+        the GPU computes. Returns the CUDA event after which z_host holds z(k);
+        call :meth:`settle` before reading host-side state (drift, freeze, ledger).
+        """
+        if theta_host.is_cuda or theta_host.dtype != torch.float32 or theta_host.numel() != self.plan.arena:
+            raise ShapeError("theta_host must be a host fp32 tensor of arena size")
+        if z_host is not None and (z_host.is_cuda or z_host.dtype != torch.float32
+                                   or z_host.numel() != self.plan.arena):
+            raise ShapeError("z_host must be a host fp32 tensor of arena size")
+        local = not hasattr(self.cluster, "run_rank")
+        if local and self.topology.world_size != 1:
+            raise ProtocolError("step_host runs one rank per engine: DistCluster, or a one-rank LocalCluster")
+        if self._pipe is None:
+            dev = self.device
+            self._pipe = {
+                "theta": [self.theta, self.plan.empty_arena(dev, fill_zero=False)],
+                "zout": [self.plan.empty_arena(dev, fill_zero=False) for _ in range(2)],
+                "h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
+                "free": [None, None],      # compute done with theta[b]
+                "drained": [None, None],   # z_host copy out of zout[b] done
+            }
+        pp = self._pipe
+        b = k & 1
+        compute = torch.cuda.current_stream(self.device)
+        # input copy: into the theta buffer the previous-but-one step used
+        h2d = pp["h2d"]
+        if pp["free"][b] is not None:
+            h2d.wait_event(pp["free"][b])
+        with torch.cuda.stream(h2d):
+            pp["theta"][b].copy_(theta_host, non_blocking=True)
+            landed = torch.cuda.Event()
+            landed.record(h2d)
+        self.theta = pp["theta"][b]
+        compute.wait_event(landed)
+        self.defer_host = True
+        try:
+            if local:
+                self.cluster.run({self.rank: self.program(k)})
+            else:
+                self.cluster.run_rank(self.program(k))
+        finally:
+            self.defer_host = False
+        free = torch.cuda.Event()
+        free.record(compute)
+        pp["free"][b] = free
+        if z_host is None:
+            return free
+        # output copy from a staging buffer (the next step rewrites z)
+        if pp["drained"][b] is not None:
+            compute.wait_event(pp["drained"][b])
+        pp["zout"][b].copy_(self.z)
+        staged = torch.cuda.Event()
+        staged.record(compute)
+        d2h = pp["d2h"]
+        d2h.wait_event(staged)
+        with torch.cuda.stream(d2h):
+            z_host.copy_(pp["zout"][b], non_blocking=True)
+            drained = torch.cuda.Event()
+            drained.record(d2h)
+        pp["drained"][b] = drained
+        return drained
 
     def _leader_average(self, k: int):
         """C3: leader all-reduce AVG of the flat buffer, one request per <= 32 MiB bucket."""

@@ -227,6 +227,40 @@ def test_end_to_end_against_reference_goldens(M, P, transport):
             assert torch.equal(getattr(e, key), getattr(lead, key))
 
 
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_step_host_pipeline_against_reference_goldens(transport):
+    """HSADMMSync.step_host: theta in from / z out to pinned host memory on copy
+    streams, host bookkeeping deferred to the next call — every step's z_host and
+    the settled freeze / cache / ledger state match run_hierarchical."""
+    import paper_2512_14628_b200 as H
+
+    ref, cluster, (e,) = _e2e_engines(1, 1, transport)
+    dev = e.device
+    thetas, outs, done = [], [], None
+    for k in range(1, ref.iters + 1):
+        t = e.plan.empty_arena(dev)
+        e.plan.load_arena(t, ref.theta(k, 0))
+        thetas.append(t.cpu().pin_memory())
+        outs.append(torch.empty(e.plan.arena, dtype=torch.float32).pin_memory())
+    for k in range(1, ref.iters + 1):
+        done = e.step_host(k, thetas[k - 1], outs[k - 1])
+    done.synchronize()
+    e.settle()
+    for k in range(1, ref.iters + 1):
+        zk = e.plan.views(outs[k - 1])
+        th = ref.theta(k, 0)
+        for n in ref.names:
+            err = rel_err(zk[n].numpy(), ref.node_state("z", k, 0)[n], th[n])
+            assert err <= TOL, (k, n, err)
+    k = ref.iters
+    assert e.frozen == ref.frozen(k, 0)
+    assert (e.cache_derive, e.cache_hits) == ref.cache(k, 0)
+    for n, m in ref.masks(k, 0).items():
+        assert np.array_equal(cpu(e.mask_dict()[n]), m), n
+    zs = [x.to_dict() for x in cluster.ledger.entries if x.label.startswith("z_sync")]
+    assert zs == [d for kk in range(1, k + 1) for d in ref.zsync(kk)]
+
+
 # -- full-size stage-wise parity vs the oracle on identical inputs -------------------
 
 
@@ -270,6 +304,81 @@ def test_full_size_step_against_oracle(model, keep):
                 assert err <= TOL, (k, key, n, err, frozen_before)
     ratio = eng.payload_elements / sum(ls.elements for ls in layers)
     assert 0.40 < ratio < 0.47     # leader bytes vs dense (0.428 / 0.450)
+
+
+@pytest.mark.parametrize("zero_step", [1, 2])
+def test_single_node_keep_sets_with_kept_zeros(zero_step):
+    """One node derives the keep sets from the selection flags (the mask is the
+    kept rectangle R x C) and K3 only checks for kept elements that are exactly
+    zero. Here some kept elements (and a whole filter) are exactly zero, from
+    iteration `zero_step` on, so the fixup re-derives those layers from their
+    bits (and counts the drift of the next step from bits): masks, keep sets,
+    payload sizes, state and drift against the oracle / numpy on the same inputs."""
+    import paper_2512_14628_b200 as H
+    from paper_2512_14628_b200.synthetic import channel_keep_constraints, model_layers, synthetic_rank_state
+
+    layers = model_layers("rn18_cifar")
+    keep = 0.5
+    cons = channel_keep_constraints(layers, keep)
+    names = [ls.name for ls in layers]
+    sched = H.PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False)
+    settings = H.ConsensusSettings(t_freeze=100, drift_window=0, weight_decay=1e-4)
+    eng = H.HSADMMSync(0, H.LocalCluster(H.Topology(1, 1)), layers, cons, sched, settings)
+    st = synthetic_rank_state(layers, 0, 1, seed=4)
+    convs = [ls for ls in layers if ls.kind is H.LayerKind.CONV and ls.shape[2] == 3]
+    hit = [convs[1].name, convs[5].name]
+
+    def zero_pattern(state):
+        for n in hit:
+            for key in ("theta", "u", "z_node", "v", "z"):
+                t = state[key][n]
+                t[3] = 0.0             # a whole filter: not in K_out
+                t[:, :, 1, 1] = 0.0    # the centre tap of every channel: kept zeros
+
+    if zero_step == 1:
+        zero_pattern(st)
+    eng.load(**st)
+    ocons = {n: [(O.CHANNEL, None, keep)] for n in cons}
+    olayers = O.make_layers([(ls.name, ls.shape) for ls in layers], ocons)
+    ost = O.init_rank_state(olayers, st["theta"], st["u"], st["z_node"], st["v"], st["z"])
+    rho = {n: 1.5e-3 for n in names}, {n: 1.5e-4 for n in names}
+    prev = {n: np.ones(ls.shape, bool) for n, ls in zip(names, layers) if n in cons}
+    for k in (1, 2, 3):
+        if k == zero_step and k > 1:   # zeros appear later: the previous mask was a rectangle
+            for n in hit:
+                for key in ("theta", "u", "z_node", "v", "z"):
+                    t = eng.views(key)[n]
+                    t[3] = 0.0
+                    t[:, :, 1, 1] = 0.0
+            zs = {key: {n: cpu(t) for n, t in eng.views(key).items()} for key in ("theta",)}
+            st["theta"] = {n: zs["theta"][n].copy() for n in names}
+        for key in ("u", "v", "z", "z_node"):
+            setattr(ost, key, {n: cpu(t).astype(np.float64) for n, t in eng.views(key).items()})
+        ost.masks = {n: cpu(m) for n, m in eng.mask_dict().items()}
+        H.run_local([eng], k)
+        O.cluster_sync(olayers, [ost], [st["theta"]], k, 1, 1, rho[0], rho[1], 1e-4, t_freeze=100)
+        gm = {n: cpu(m) for n, m in eng.mask_dict().items()}
+        for n in ost.masks:
+            assert np.array_equal(gm[n], ost.masks[n]), (k, n)
+        if k >= zero_step:
+            for n in hit:  # the pattern really made kept zeros / an empty filter
+                assert not gm[n][3].any() and gm[n].any()
+        for key in ("z_node", "u", "v", "z"):
+            for n in names:
+                err = rel_err(cpu(eng.views(key)[n]), getattr(ost, key)[n], st["theta"][n])
+                assert err <= TOL, (k, key, n, err)
+        # payload = sum over layers of |K_out| |K_in| kh kw from the union masks
+        want = 0
+        for ls in layers:
+            if ls.name in gm:
+                m = gm[ls.name]
+                want += int(m.any(axis=(1, 2, 3)).sum()) * int(m.any(axis=(0, 2, 3)).sum()) * ls.shape[2] * ls.shape[3]
+            else:
+                want += ls.elements
+        assert eng.payload_elements == want, k
+        drift = max(float((gm[n] != prev[n]).mean()) for n in gm)
+        assert abs(eng.drift_history[-1] - drift) < 1e-12, (k, eng.drift_history[-1], drift)
+        prev = gm
 
 
 def test_full_size_compaction_roundtrip_property():

@@ -51,6 +51,7 @@ def parse_args():
     ap.add_argument("--keep", type=float, default=0.4)
     ap.add_argument("--transport", choices=["auto", "peer", "nccl"], default="auto")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true", help="one rank: launch eagerly instead of replaying CUDA graphs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
@@ -294,9 +295,14 @@ def run_ours(args):
     z_host = torch.empty(eng.plan.arena, dtype=torch.float32).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def run_step(k):
+    use_graph = world == 1 and not args.no_graph
+    config["launch"] = "cuda-graph replay per step" if use_graph else "eager launches (deferred host bookkeeping)"
+
+    def run_step(k, eager=False):
         if world > 1:
             return eng.step(k)
+        if use_graph and not eager:   # one rank: the step replays a captured CUDA graph
+            return eng.graph_step(k)
         return H.run_local([eng], k)
 
     def barrier():
@@ -314,7 +320,7 @@ def run_ours(args):
             e = torch.cuda.Event(enable_timing=True)
             s.record()
             plan_mod.TIMER = kernel_timer
-            run_step(k0 + i)
+            run_step(k0 + i, eager=kernel_timer is not None)
             plan_mod.TIMER = None
             e.record()
             evs.append((s, e))

@@ -117,7 +117,7 @@ struct hsx_plan {
   unsigned int* d_layer_done = nullptr;
   unsigned int* d_cand_done = nullptr;
   unsigned long long* d_acc = nullptr;
-  uint8_t *d_rk_prev = nullptr, *d_ck_prev = nullptr;
+  uint8_t *d_rk_prev = nullptr, *d_ck_prev = nullptr, *d_ch_prev = nullptr;
   int *d_irr = nullptr, *d_irr_any = nullptr;
   int* d_sel[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
@@ -126,7 +126,6 @@ struct hsx_plan {
   uint8_t* d_flags[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   uint8_t *d_oflag = nullptr, *d_iflag = nullptr;
   int *d_pos_out = nullptr, *d_pos_in = nullptr;
-  hsx::Maps maps = {nullptr, nullptr};
   long long* d_summary = nullptr;
   unsigned int* d_done = nullptr;
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
@@ -134,7 +133,7 @@ struct hsx_plan {
   ~hsx_plan() {
     void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
-                    maps.rowbase, maps.colpos};
+                    d_ch_prev};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (int i = 0; i < hsx::kMaxPasses; ++i) {
@@ -292,15 +291,13 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         }
       }
       // fused K3 + K5: the keep-set tail reuses the ring's shared memory for positions
-      p->fixup_smem = std::max<size_t>(p->fixup_smem, ((size_t)ly.cin + ly.rows + 15) / 16 * 16 +
-                                                          4 * ((size_t)ly.cin + ly.rows));
+      p->fixup_smem = std::max<size_t>(p->fixup_smem, (size_t)ly.cin + ly.rows);
       const int nwi = (int)((ly.n + kWordItem * 32 - 1) / (kWordItem * 32));
       for (long long b = 0; b < ly.n; b += kWordItem * 32) {
         Item it{l, ly.pidx, nwi, 0, b, std::min(ly.n, b + kWordItem * 32)};
         p->word_items.push_back(it);
         long long r_lo = b / ly.L, r_hi = (it.end - 1) / ly.L;
-        mark_smem = std::max<size_t>(mark_smem, std::max<size_t>((size_t)ly.cin + (size_t)(r_hi - r_lo + 1),
-                                                                  4 * ((size_t)ly.cin + ly.rows)));
+        mark_smem = std::max<size_t>(mark_smem, (size_t)ly.cin + (size_t)(r_hi - r_lo + 1));
       }
     } else {
       for (long long b = 0; b < ly.n; b += kItemElems) {
@@ -367,10 +364,12 @@ int upload_plan(hsx_plan* p) {
   if ((rc = alloc0(&p->d_irr, (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_irr_any, 1))) return rc;
   // previous rectangle: the all-ones initial mask (consensus.py:418)
-  const std::vector<uint8_t> ones_r(p->ktotal[0], 1), ones_c(p->ctotal, 1);
+  const std::vector<uint8_t> ones_r(p->ktotal[0], 1), ones_c(p->ctotal, 1), ones_i(p->ktotal[1], 1);
   rc = upload(&p->d_rk_prev, ones_r);
   if (rc) return rc;
   rc = upload(&p->d_ck_prev, ones_c);
+  if (rc) return rc;
+  rc = upload(&p->d_ch_prev, ones_i);
   if (rc) return rc;
   if ((rc = upload(&p->d_elem, p->elem_items))) return rc;
   if ((rc = upload(&p->d_stream, p->stream_items))) return rc;
@@ -394,14 +393,6 @@ int upload_plan(hsx_plan* p) {
   }
   if ((rc = upload(&p->d_pos_out, po))) return rc;
   if ((rc = upload(&p->d_pos_in, pi))) return rc;
-  std::vector<int> rb(p->ktotal[0]), cp(p->ctotal, -1);
-  for (int l : p->prunable) {
-    const DevLayer& ly = p->layers[l];
-    for (int i = 0; i < ly.rows; ++i) rb[ly.okeep + i] = i * ly.L;
-    for (int i = 0; i < ly.L; ++i) cp[ly.cpoff + i] = i;
-  }
-  if ((rc = upload(&p->maps.rowbase, rb))) return rc;
-  if ((rc = upload(&p->maps.colpos, cp))) return rc;
   if ((rc = upload(&p->d_summary, p->summary))) return rc;
   if ((rc = alloc0(&p->d_done, 1))) return rc;
   return HSX_OK;
@@ -517,13 +508,13 @@ static hsx::KeepArgs keep_args(hsx_plan* p, const Item* items, const uint32_t* u
   ka.iflag = p->d_iflag;
   ka.pos_out = p->d_pos_out;
   ka.pos_in = p->d_pos_in;
-  ka.maps = p->maps;
   for (int q = 0; q < hsx::kMaxPasses; ++q) ka.flags.f[q] = p->d_flags[q];
   ka.summary = p->d_summary;
   ka.layer_done = p->d_layer_done;
   ka.done = p->d_done;
   ka.acc = p->d_acc;
   ka.rk_prev = p->d_rk_prev;
+  ka.ch_prev = p->d_ch_prev;
   ka.ck_prev = p->d_ck_prev;
   ka.irr = p->d_irr;
   ka.irr_any = p->d_irr_any;
@@ -771,14 +762,6 @@ int hsx_set_keep_sets(hsx_plan* p, int32_t l, const int32_t* k_out, int32_t n_ou
   }
   HSX_CUDA(cudaMemcpy(p->d_pos_out + ly.okeep, po.data(), po.size() * sizeof(int), cudaMemcpyHostToDevice));
   HSX_CUDA(cudaMemcpy(p->d_pos_in + ly.ikeep, pi.data(), pi.size() * sizeof(int), cudaMemcpyHostToDevice));
-  std::vector<int> rb(ly.rows), cp(ly.L);
-  for (int o = 0; o < ly.rows; ++o) rb[o] = po[o] >= 0 ? po[o] * n_in * ly.k : -1;
-  for (int col = 0; col < ly.L; ++col) {
-    int c = col / ly.k, j = col % ly.k;
-    cp[col] = pi[c] >= 0 ? pi[c] * ly.k + j : -1;
-  }
-  HSX_CUDA(cudaMemcpy(p->maps.rowbase + ly.okeep, rb.data(), rb.size() * sizeof(int), cudaMemcpyHostToDevice));
-  HSX_CUDA(cudaMemcpy(p->maps.colpos + ly.cpoff, cp.data(), cp.size() * sizeof(int), cudaMemcpyHostToDevice));
   long long* row = &p->summary[(size_t)l * HSX_SUM_COLS];
   row[HSX_SUM_KOUT] = n_out;
   row[HSX_SUM_KIN] = n_in;
@@ -803,8 +786,8 @@ static hsx::ElemArgs elem_args(const hsx_plan* p) {
   std::memset(&a, 0, sizeof(a));
   a.layers = p->d_layers;
   a.items = p->d_stream;
-  a.rowbase = p->maps.rowbase;
-  a.colpos = p->maps.colpos;
+  a.pos_out = p->d_pos_out;
+  a.pos_in = p->d_pos_in;
   a.summary = p->d_summary;
   a.divisor = 1.0f;
   return a;

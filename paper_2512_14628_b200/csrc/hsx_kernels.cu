@@ -225,13 +225,12 @@ __device__ __forceinline__ bool flag_at(const uint8_t* f, int i) {
     return __ldcg(f + i) != 0;
 }
 
-// Positions of the set K_in / K_out flags of one layer in one block scan when
-// every thread owns <= 8 consecutive flags of each array (the two counts packed
-// in one int, 16 bits each), else in rounds. Positions go to global pos_* and
-// shared s_p*; returns (|K_in|, |K_out|).
+// Positions of the set K_in / K_out flags of one layer (-1 for clear ones) in
+// one block scan when every thread owns <= 8 consecutive flags of each array
+// (the two counts packed in one int, 16 bits each), else in rounds; returns
+// (|K_in|, |K_out|).
 template <bool SMEM>
-__device__ int2 scan_keep(const uint8_t* fin, int cin, const uint8_t* fout, int rows, int* pos_in, int* pos_out,
-                          int* s_pin, int* s_pout) {
+__device__ int2 scan_keep(const uint8_t* fin, int cin, const uint8_t* fout, int rows, int* pos_in, int* pos_out) {
   __shared__ int warp_tot[32];
   __shared__ int total;
   constexpr int kPer = 8;
@@ -254,16 +253,8 @@ __device__ int2 scan_keep(const uint8_t* fin, int cin, const uint8_t* fout, int 
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int x = t * per + i;
-      if (i < per && x < cin) {
-        const int p = fi[i] ? pi++ : -1;
-        pos_in[x] = p;
-        s_pin[x] = p;
-      }
-      if (i < per && x < rows) {
-        const int p = fo[i] ? po++ : -1;
-        pos_out[x] = p;
-        s_pout[x] = p;
-      }
+      if (i < per && x < cin) pos_in[x] = fi[i] ? pi++ : -1;
+      if (i < per && x < rows) pos_out[x] = fo[i] ? po++ : -1;
     }
     __syncthreads();
     return make_int2(tot & 0xffff, tot >> 16);
@@ -273,51 +264,18 @@ __device__ int2 scan_keep(const uint8_t* fin, int cin, const uint8_t* fout, int 
     const uint8_t* f = a ? fout : fin;
     const int m = a ? rows : cin;
     int* pos = a ? pos_out : pos_in;
-    int* spos = a ? s_pout : s_pin;
     int carry = 0;
     for (int base = 0; base < m; base += nt) {
       const int i = base + t;
       const int fr = (i < m && flag_at<SMEM>(f, i)) ? 1 : 0;
       const int ex = block_exclusive_scan(fr, warp_tot, &total);
-      if (i < m) {
-        pos[i] = fr ? carry + ex : -1;
-        spos[i] = pos[i];
-      }
+      if (i < m) pos[i] = fr ? carry + ex : -1;
       carry += total;
     }
     n[a] = carry;
   }
   __syncthreads();
   return make_int2(n[0], n[1]);
-}
-
-// payload maps of one layer from its positions in shared memory:
-// rowbase[o] = pos_out[o] * |K_in| * k, colpos[c*k + j] = pos_in[c] * k + j (-1: dropped)
-__device__ void write_maps(const KeepArgs& a, int rows, int L, int k, long long okeep, long long cpoff,
-                           const FastDiv& divk, const int* s_pin, const int* s_pout, int n_in) {
-  const int rowlen = n_in * k;
-  for (int o = threadIdx.x; o < rows; o += blockDim.x) {
-    const int po = s_pout[o];
-    a.maps.rowbase[okeep + o] = po >= 0 ? po * rowlen : -1;
-  }
-  if ((L & 3) == 0) {  // cpoff is a multiple of 4: one int4 of column positions per thread
-    for (int q4 = threadIdx.x; q4 < (L >> 2); q4 += blockDim.x) {
-      int v[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const unsigned col = 4 * q4 + b, c = fdiv(col, divk), jx = col - c * (unsigned)k;
-        const int pi = s_pin[c];
-        v[b] = pi >= 0 ? pi * k + (int)jx : -1;
-      }
-      *reinterpret_cast<int4*>(a.maps.colpos + cpoff + 4 * q4) = make_int4(v[0], v[1], v[2], v[3]);
-    }
-  } else {
-    for (int col = threadIdx.x; col < L; col += blockDim.x) {
-      const unsigned c = fdiv((unsigned)col, divk), jx = (unsigned)col - c * (unsigned)k;
-      const int pi = s_pin[c];
-      a.maps.colpos[cpoff + col] = pi >= 0 ? pi * k + (int)jx : -1;
-    }
-  }
 }
 
 // flat-buffer layout: exclusive scan of the payload sizes of all layers (block-wide)
@@ -381,21 +339,15 @@ __device__ void finish_layer(const KeepArgs& a, int l, int n_out, int n_in, int 
   if (threadIdx.x == 0) *a.done = 0;
 }
 
-// K5 tail, run by the last CTA of layer l: keep sets from the global any-flags;
-// smem >= 4 * (c_in + rows) bytes
-__device__ void keep_sets_tail(const KeepArgs& a, int l, const DevLayer& gly, uint8_t* smem) {
-  // layer fields in registers: the flag / map stores below may alias the table
-  const int cin = gly.cin, rows = gly.rows, k = gly.k, L = gly.L, pidx = gly.pidx;
-  const long long ikeep = gly.ikeep, okeep = gly.okeep, cpoff = gly.cpoff;
-  const FastDiv divk = gly.divk;
-  int* s_pin = reinterpret_cast<int*>(smem);
-  int* s_pout = s_pin + cin;
-  const int2 nio = scan_keep<false>(a.iflag + ikeep, cin, a.oflag + okeep, rows, a.pos_in + ikeep,
-                                    a.pos_out + okeep, s_pin, s_pout);
+// K5 tail, run by the last CTA of layer l: keep sets from the global any-flags
+__device__ void keep_sets_tail(const KeepArgs& a, int l, const DevLayer& gly) {
+  // layer fields in registers: the flag stores below may alias the table
+  const int cin = gly.cin, rows = gly.rows, k = gly.k, pidx = gly.pidx;
+  const long long ikeep = gly.ikeep, okeep = gly.okeep;
+  const int2 nio = scan_keep<false>(a.iflag + ikeep, cin, a.oflag + okeep, rows, a.pos_in + ikeep, a.pos_out + okeep);
   // leave the any-flags zeroed for the next derivation
   for (int i = threadIdx.x; i < cin; i += blockDim.x) a.iflag[ikeep + i] = 0;
   for (int i = threadIdx.x; i < rows; i += blockDim.x) a.oflag[okeep + i] = 0;
-  write_maps(a, rows, L, k, okeep, cpoff, divk, s_pin, s_pout, nio.x);
   long long drift = 0, pop = 0;
   if (threadIdx.x == 0) {
     drift = (long long)atomicExch(a.acc + 2 * pidx, 0ULL);
@@ -408,7 +360,7 @@ __device__ void keep_sets_tail(const KeepArgs& a, int l, const DevLayer& gly, ui
 // end of a K5 marking CTA: fold its popcounts into the layer's accumulators, then
 // count it done; the layer's last CTA runs the tail
 __device__ void keep_mark_done(const KeepArgs& a, int l, const DevLayer& ly, int nitems,
-                               unsigned long long pop, unsigned long long drift, uint8_t* smem) {
+                               unsigned long long pop, unsigned long long drift) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     pop += __shfl_xor_sync(kFull, pop, off);
@@ -427,16 +379,17 @@ __device__ void keep_mark_done(const KeepArgs& a, int l, const DevLayer& ly, int
   __syncthreads();
   if (!last) return;
   __threadfence();
-  keep_sets_tail(a, l, ly, smem);
+  keep_sets_tail(a, l, ly);
 }
 
 // Structured keep sets of layer l at its last selection pass (one node): the
 // rectangle R x C from the group flags (this pass in sflag, earlier passes in
-// global memory). Updates the previous-rectangle state (rk_prev / ck_prev).
-// smem: rows + L + c_in bytes, then 4 * (c_in + rows) bytes of positions
-// (16-B aligned): structured_smem(rows, L, c_in).
+// global memory). C is a set of whole channels unless the layer has SHAPE
+// groups, so the work is O(rows + c_in) (O(rows + L) with SHAPE groups).
+// Updates the previous-rectangle state (rk_prev, ch_prev / ck_prev).
+// smem: structured_smem(rows, L, c_in) bytes.
 __host__ __device__ inline size_t structured_smem(int rows, int L, int cin) {
-  return ((size_t)rows + L + cin + 15) / 16 * 16 + 4 * ((size_t)cin + rows);
+  return ((size_t)rows + cin + L + 15) / 16 * 16;
 }
 
 __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& gly, int pass,
@@ -446,25 +399,17 @@ __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& g
   const FastDiv divk = gly.divk;
   int gq[kMaxPasses];
   const uint8_t* fq[kMaxPasses];
+  bool shape = false;
 #pragma unroll
   for (int q = 0; q < kMaxPasses; ++q) {
     gq[q] = q < npass ? gly.group[q] : -1;
     fq[q] = q < npass ? a.flags.f[q] + gly.goff[q] : nullptr;
+    shape |= gq[q] == kShape;
   }
-  uint8_t* srk = smem;             // kept rows
-  uint8_t* sck = srk + rows;       // kept columns
-  uint8_t* sch = sck + L;          // channels meeting C
-  int* s_pin = reinterpret_cast<int*>(smem + ((size_t)rows + L + cin + 15) / 16 * 16);
-  int* s_pout = s_pin + cin;
-  // R and C, their sizes and overlaps with the previous rectangle
-#ifdef HSX_PROBE_SELECT
-  long long tq[8];
-  tq[0] = clock64();
-#define ST_MARK(i) do { __syncthreads(); tq[i] = clock64(); } while (0)
-#else
-#define ST_MARK(i) do { } while (0)
-#endif
-  // three counts packed per word (21 bits each: rows, columns <= 2^20)
+  uint8_t* srk = smem;        // R
+  uint8_t* sch = srk + rows;  // channels meeting C
+  uint8_t* sck = sch + cin;   // C by column (SHAPE groups)
+  // three counts packed per word (21 bits each; rows, columns < 2^20)
   unsigned long long rsum = 0, csum = 0;
   for (int o = threadIdx.x; o < rows; o += blockDim.x) {
     uint8_t kp = 1;
@@ -476,53 +421,56 @@ __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& g
     a.rk_prev[okeep + o] = kp;
     rsum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
   }
-  for (int col = threadIdx.x; col < L; col += blockDim.x) {
-    const int c = (int)fdiv((unsigned)col, divk);
-    uint8_t kp = 1;
+  if (!shape) {  // C = the channels kept by every CHANNEL pass, all kh*kw columns each
+    for (int c = threadIdx.x; c < cin; c += blockDim.x) {
+      uint8_t kp = 1;
 #pragma unroll
-    for (int q = 0; q < kMaxPasses; ++q) {
-      if (gq[q] != kChannel && gq[q] != kShape) continue;
-      const int g = gq[q] == kChannel ? c : col;
-      kp &= q == pass ? sflag[g] : fq[q][g];
+      for (int q = 0; q < kMaxPasses; ++q)
+        if (gq[q] == kChannel) kp &= q == pass ? sflag[c] : fq[q][c];
+      const uint8_t pv = a.ch_prev[ikeep + c];
+      sch[c] = kp;
+      a.ch_prev[ikeep + c] = kp;
+      csum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
     }
-    const uint8_t pv = a.ck_prev[cpoff + col];
-    sck[col] = kp;
-    a.ck_prev[cpoff + col] = kp;
-    csum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
+  } else {
+    for (int col = threadIdx.x; col < L; col += blockDim.x) {
+      const int c = (int)fdiv((unsigned)col, divk);
+      uint8_t kp = 1;
+#pragma unroll
+      for (int q = 0; q < kMaxPasses; ++q) {
+        if (gq[q] != kChannel && gq[q] != kShape) continue;
+        const int g = gq[q] == kChannel ? c : col;
+        kp &= q == pass ? sflag[g] : fq[q][g];
+      }
+      const uint8_t pv = a.ck_prev[cpoff + col];
+      sck[col] = kp;
+      a.ck_prev[cpoff + col] = kp;
+      csum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < cin; c += blockDim.x) {
+      uint8_t any = 0;
+      for (int jx = 0; jx < k; ++jx) any |= sck[c * k + jx];
+      sch[c] = any;
+    }
   }
-  ST_MARK(1);
   rsum = block_sum(rsum);
   csum = block_sum(csum);
-  ST_MARK(2);
   constexpr unsigned long long m21 = (1ULL << 21) - 1;
+  const long long cm = shape ? 1 : k;  // columns per counted unit
   const long long nR = rsum & m21, nRp = (rsum >> 21) & m21, nRR = rsum >> 42;
-  const long long nC = csum & m21, nCp = (csum >> 21) & m21, nCC = csum >> 42;
-  // K_in: channels with a kept column (when some row is kept); K_out: kept rows
-  // (when some column is kept)
-  for (int c = threadIdx.x; c < cin; c += blockDim.x) {
-    uint8_t any = 0;
-    for (int jx = 0; jx < k; ++jx) any |= sck[c * k + jx];
-    sch[c] = nR > 0 ? any : 0;
-  }
+  const long long nC = cm * (csum & m21), nCp = cm * ((csum >> 21) & m21), nCC = cm * (csum >> 42);
+  // K_out = R when C is non-empty; K_in = channels meeting C when R is non-empty
   if (nC == 0)
     for (int o = threadIdx.x; o < rows; o += blockDim.x) srk[o] = 0;
+  if (nR == 0)
+    for (int c = threadIdx.x; c < cin; c += blockDim.x) sch[c] = 0;
   __syncthreads();
-  ST_MARK(3);
-  const int2 nio = scan_keep<true>(sch, cin, srk, rows, a.pos_in + ikeep, a.pos_out + okeep, s_pin, s_pout);
-  ST_MARK(4);
-  write_maps(a, rows, L, k, okeep, cpoff, divk, s_pin, s_pout, nio.x);
-  ST_MARK(5);
+  const int2 nio = scan_keep<true>(sch, cin, srk, rows, a.pos_in + ikeep, a.pos_out + okeep);
   // |A ^ B| = |A| + |B| - 2 |A n B| for rectangles A = R x C, B = Rp x Cp
   const long long pop = nR * nC;
   const long long drift = pop + nRp * nCp - 2 * nRR * nCC;
   finish_layer(a, l, nio.y, nio.x, k, drift, pop);
-#ifdef HSX_PROBE_SELECT
-  ST_MARK(6);
-  if (threadIdx.x == 0)
-    printf("structured l=%d rows=%d L=%d cin=%d nt=%d: RC %lld sums %lld ch %lld scan %lld maps %lld finish %lld\n", l,
-           rows, L, cin, (int)blockDim.x, tq[1] - tq[0], tq[2] - tq[1], tq[3] - tq[2], tq[4] - tq[3], tq[5] - tq[4],
-           tq[6] - tq[5]);
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1107,13 +1055,13 @@ size_t select_smem_bytes(int G) { return select_bytes(G); }
 // Layer fields the streaming kernels use, loaded once into registers (stores
 // through the float arenas would otherwise force reloads of the layer table).
 struct LayerRegs {
-  long long off, n, mword, okeep, cpoff;
-  int L, ncons, qtile;
-  FastDiv divL;
+  long long off, n, mword, okeep, ikeep;
+  int L, k, ncons, qtile;
+  FastDiv divL, divk;
   __device__ __forceinline__ LayerRegs(const DevLayer* __restrict__ layers, int l) {
     const DevLayer& ly = layers[l];
-    off = ly.off; n = ly.n; mword = ly.mword; okeep = ly.okeep; cpoff = ly.cpoff;
-    L = ly.L; ncons = ly.ncons; qtile = ly.qtile; divL = ly.divL;
+    off = ly.off; n = ly.n; mword = ly.mword; okeep = ly.okeep; ikeep = ly.ikeep;
+    L = ly.L; k = ly.k; ncons = ly.ncons; qtile = ly.qtile; divL = ly.divL; divk = ly.divk;
   }
 };
 
@@ -1353,7 +1301,7 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
   for (int i = threadIdx.x; i < nr; i += kThreads)
     if (s_out[i]) a.oflag[ly.okeep + r_lo + i] = 1;
   __syncthreads();  // the tail reuses the mark flags' shared memory for positions
-  keep_mark_done(a, l, ly, it.chunk, pop, drift, sflag);
+  keep_mark_done(a, l, ly, it.chunk, pop, drift);
 }
 
 void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st) {
@@ -1367,7 +1315,7 @@ void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t 
 // bits; a layer whose previous mask was irregular (bit 1) gets its drift
 // counted from the bits. The common case (neither) returns at once; when some
 // layer was re-derived, the last CTA lays out the flat buffer again.
-// smem: align16(c_in + rows) + 4 * (c_in + rows) bytes.
+// smem: c_in + rows bytes.
 __global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* __restrict__ prunable) {
   PDL_ENTRY();
   extern __shared__ __align__(16) uint8_t fsm[];
@@ -1378,12 +1326,10 @@ __global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* 
   const int any = *reinterpret_cast<volatile int*>(a.irr_any);
   if (irr & 3) {
     const int cin = gly.cin, rows = gly.rows, k = gly.k, L = gly.L;
-    const long long n = gly.n, mword = gly.mword, ikeep = gly.ikeep, okeep = gly.okeep, cpoff = gly.cpoff;
+    const long long n = gly.n, mword = gly.mword, ikeep = gly.ikeep, okeep = gly.okeep;
     const FastDiv divL = gly.divL, divk = gly.divk;
     uint8_t* s_in = fsm;
     uint8_t* s_out = fsm + cin;
-    int* s_pin = reinterpret_cast<int*>(fsm + ((size_t)cin + rows + 15) / 16 * 16);
-    int* s_pout = s_pin + cin;
     const bool exact = irr & 1;
     for (int i = threadIdx.x; i < cin + rows; i += blockDim.x) fsm[i] = 0;
     __syncthreads();
@@ -1413,8 +1359,7 @@ __global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* 
     drift = block_sum(drift);
     if (exact) {
       __syncthreads();
-      const int2 nio = scan_keep<true>(s_in, cin, s_out, rows, a.pos_in + ikeep, a.pos_out + okeep, s_pin, s_pout);
-      write_maps(a, rows, L, k, okeep, cpoff, divk, s_pin, s_pout, nio.x);
+      const int2 nio = scan_keep<true>(s_in, cin, s_out, rows, a.pos_in + ikeep, a.pos_out + okeep);
       if (threadIdx.x == 0) {
         long long* row = a.summary + (long long)l * kSumCols;
         row[0] = nio.y;
@@ -1454,31 +1399,55 @@ void launch_keep_fixup(const KeepArgs& a, const int* prunable, int n, size_t sme
 // K6 compact + intra dual; K7 decompact + inter dual.
 // consensus.py:476-505, 535; shrinkage.py:61-82
 // A thread owns element quads: the dense streams move as float4; the compact
-// payload offset of element (o, col) is  coff + rowbase[o] + colpos[col]
-// (int4 load of colpos per quad), -1 entries are dropped coordinates.
+// payload offset of element (o, c*k + j) is
+//   coff + pos_out[o] * |K_in| * k + pos_in[c] * k + j
+// (the row part per tile row in shared memory, the column part of a tile
+// thread's quad in registers); a -1 position drops the coordinate.
 // ---------------------------------------------------------------------------
 
 // payload index of element e of a non-tiled prunable layer (-1: dropped)
-__device__ __forceinline__ int elem_dst(const int* __restrict__ rowbase, const int* __restrict__ colpos,
-                                        const LayerRegs& ly, long long e) {
-  unsigned o = fdiv((unsigned)e, ly.divL);
-  unsigned col = (unsigned)e - o * (unsigned)ly.L;
-  int rb = rowbase[ly.okeep + o], cp = colpos[ly.cpoff + col];
-  return (rb < 0 || cp < 0) ? -1 : rb + cp;
+__device__ __forceinline__ int elem_dst(const ElemArgs& a, const LayerRegs& ly, int rowlen, long long e) {
+  const unsigned o = fdiv((unsigned)e, ly.divL);
+  const unsigned col = (unsigned)e - o * (unsigned)ly.L;
+  const unsigned c = fdiv(col, ly.divk), jx = col - c * (unsigned)ly.k;
+  const int po = a.pos_out[ly.okeep + o], pi = a.pos_in[ly.ikeep + c];
+  return (po < 0 || pi < 0) ? -1 : po * rowlen + pi * ly.k + (int)jx;
 }
 
 // payload indices of the quad at e of a contiguous item (dense or non-tiled prunable)
-__device__ __forceinline__ int4 dst4_linear(const ElemArgs& a, const LayerRegs& ly, long long e) {
+__device__ __forceinline__ int4 dst4_linear(const ElemArgs& a, const LayerRegs& ly, int rowlen, long long e) {
   if (ly.ncons == 0) {
     int b = (int)e;
     return make_int4(b, e + 1 < ly.n ? b + 1 : -1, e + 2 < ly.n ? b + 2 : -1, e + 3 < ly.n ? b + 3 : -1);
   }
   int4 d;
-  d.x = elem_dst(a.rowbase, a.colpos, ly, e);
-  d.y = e + 1 < ly.n ? elem_dst(a.rowbase, a.colpos, ly, e + 1) : -1;
-  d.z = e + 2 < ly.n ? elem_dst(a.rowbase, a.colpos, ly, e + 2) : -1;
-  d.w = e + 3 < ly.n ? elem_dst(a.rowbase, a.colpos, ly, e + 3) : -1;
+  d.x = elem_dst(a, ly, rowlen, e);
+  d.y = e + 1 < ly.n ? elem_dst(a, ly, rowlen, e + 1) : -1;
+  d.z = e + 2 < ly.n ? elem_dst(a, ly, rowlen, e + 2) : -1;
+  d.w = e + 3 < ly.n ? elem_dst(a, ly, rowlen, e + 3) : -1;
   return d;
+}
+
+// column part of the payload offsets of a tile thread's quad (columns 4j .. 4j+3)
+__device__ __forceinline__ int4 col_pos4(const ElemArgs& a, const LayerRegs& ly, int j, bool valid) {
+  if (!valid) return make_int4(-1, -1, -1, -1);
+  int v[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const unsigned col = 4 * j + b, c = fdiv(col, ly.divk), jx = col - c * (unsigned)ly.k;
+    const int pi = a.pos_in[ly.ikeep + c];
+    v[b] = pi >= 0 ? pi * ly.k + (int)jx : -1;
+  }
+  return make_int4(v[0], v[1], v[2], v[3]);
+}
+
+// row parts of a tile's rows: pos_out[o] * |K_in| * k, or -1
+__device__ __forceinline__ void row_base(const ElemArgs& a, const LayerRegs& ly, const Item& it, int rowlen,
+                                         int* s_rb) {
+  for (int r = threadIdx.x; r < it.end - it.begin; r += kThreads) {
+    const int po = a.pos_out[ly.okeep + it.begin + r];
+    s_rb[r] = po >= 0 ? po * rowlen : -1;
+  }
 }
 
 __device__ __forceinline__ int4 add_base(int rb, int4 cp) {
@@ -1495,6 +1464,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   const Item it = a.items[blockIdx.x];
   const LayerRegs ly(a.layers, it.layer);
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
+  const int rowlen = (int)a.summary[(long long)it.layer * kSumCols + 1] * ly.k;  // |K_in| * k
   const float* __restrict__ ZN = a.zn + ly.off;
   const float* __restrict__ VI = a.vin ? a.vin + ly.off : nullptr;
   const float* __restrict__ TH = a.u ? a.theta + ly.off : nullptr;
@@ -1528,9 +1498,8 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   };
   if (it.tile == 1) {
     const TileCtx tc(it, ly.L);
-    for (int r = threadIdx.x; r < it.end - it.begin; r += kThreads) s_rb[r] = a.rowbase[ly.okeep + it.begin + r];
-    const int4 cp = tc.valid ? *reinterpret_cast<const int4*>(a.colpos + ly.cpoff + 4 * tc.j)
-                             : make_int4(-1, -1, -1, -1);
+    row_base(a, ly, it, rowlen, s_rb);
+    const int4 cp = col_pos4(a, ly, tc.j, tc.valid);
     __syncthreads();
     ring_run(tc.count, [&](int d, int i) { load4(d, tc.row(i) * ly.L + 4 * tc.j); },
              [&](int d, int i) {
@@ -1545,7 +1514,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   ring_run(count, [&](int d, int i) { load4(d, it.begin + 4 * (t + (long long)i * kThreads)); },
            [&](int d, int i) {
              const long long e = it.begin + 4 * (t + (long long)i * kThreads);
-             emit(d, e, dst4_linear(a, ly, e));
+             emit(d, e, dst4_linear(a, ly, rowlen, e));
            });
 }
 
@@ -1567,6 +1536,7 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   const Item it = a.items[blockIdx.x];
   const LayerRegs ly(a.layers, it.layer);
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
+  const int rowlen = (int)a.summary[(long long)it.layer * kSumCols + 1] * ly.k;  // |K_in| * k
   const float* __restrict__ flat = a.flat_in + coff;
   const float* __restrict__ ZN = a.v ? a.zn + ly.off : nullptr;
   float* __restrict__ VV = a.v ? a.v + ly.off : nullptr;
@@ -1604,9 +1574,8 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   };
   if (it.tile == 1) {
     const TileCtx tc(it, ly.L);
-    for (int r = threadIdx.x; r < it.end - it.begin; r += kThreads) s_rb[r] = a.rowbase[ly.okeep + it.begin + r];
-    const int4 cp = tc.valid ? *reinterpret_cast<const int4*>(a.colpos + ly.cpoff + 4 * tc.j)
-                             : make_int4(-1, -1, -1, -1);
+    row_base(a, ly, it, rowlen, s_rb);
+    const int4 cp = col_pos4(a, ly, tc.j, tc.valid);
     __syncthreads();
     ring_run(tc.count,
              [&](int d, int i) {
@@ -1622,7 +1591,7 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   ring_run(count,
            [&](int d, int i) {
              const long long e = it.begin + 4 * (t + (long long)i * kThreads);
-             load(d, e, dst4_linear(a, ly, e));
+             load(d, e, dst4_linear(a, ly, rowlen, e));
            },
            [&](int d, int i) { emit(d, it.begin + 4 * (t + (long long)i * kThreads)); });
 }

@@ -93,12 +93,6 @@ struct FlagPtrs {
   uint8_t* f[kMaxPasses];
 };
 
-// per-layer payload maps derived from the keep sets (all prunable layers)
-struct Maps {
-  int* rowbase;       // [sum rows]  pos_out[o] * |K_in| * k, or -1
-  int* colpos;        // [sum L]     pos_in[c] * k + j, or -1
-};
-
 struct KeepArgs {
   const DevLayer* layers;
   const Item* items;
@@ -108,7 +102,6 @@ struct KeepArgs {
   uint8_t* iflag;
   int* pos_out;
   int* pos_in;
-  Maps maps;
   FlagPtrs flags;            // group keep flags of every pass (K3: kept = AND of the passes)
   long long* summary;
   unsigned int* layer_done;  // per prunable layer
@@ -116,7 +109,8 @@ struct KeepArgs {
   unsigned long long* acc;   // per prunable layer: drift, popcount accumulators (zero between launches)
   // structured keep sets (one node)
   uint8_t* rk_prev;          // [sum rows] rows of the previous rectangle R x C
-  uint8_t* ck_prev;          // [sum L]    columns of the previous rectangle
+  uint8_t* ch_prev;          // [sum c_in] its channels (layers without SHAPE groups)
+  uint8_t* ck_prev;          // [sum L]    its columns (layers with SHAPE groups)
   int* irr;                  // per prunable layer: bit 0 a kept zero now, bit 1 previously
   int* irr_any;              // some layer has a kept zero now
   int n_layers;
@@ -158,8 +152,8 @@ struct ElemArgs {
   float* __restrict__ z;
   const DevLayer* __restrict__ layers;
   const Item* __restrict__ items;
-  const int* __restrict__ rowbase;
-  const int* __restrict__ colpos;
+  const int* __restrict__ pos_out;     // K_out position of each row, -1: dropped
+  const int* __restrict__ pos_in;      // K_in position of each channel, -1: dropped
   const long long* __restrict__ summary;
   float divisor;
 };

@@ -478,6 +478,59 @@ class HSADMMSync:
             yield AllReduce(self.inter, self.flat[b.start:b.start + b.elements], ReduceOp.AVG,
                             f"z_sync/b{bi}", k, detail=b.detail)
 
+    # -- CUDA-graph steps (one rank) -------------------------------------------------
+    def graph_step(self, k: int):
+        """Iteration k of a one-rank engine as a replay of a captured CUDA graph.
+
+        The launches of a step depend only on (frozen, which mask buffer holds the
+        current union, which theta buffer is live, sync or not); each combination is
+        captured once from :meth:`program` under stream capture and replayed after,
+        so a step costs one graph launch on the host. Host bookkeeping is deferred
+        exactly as with ``defer_host`` (settled when the next step starts).
+        """
+        if self.topology.world_size != 1:
+            raise ProtocolError("graph_step drives a one-rank engine (collectives are not captured)")
+        self.settle()
+        sync = k % self.settings.sync_period == 0
+        dynamic = not self.frozen and bool(self.prunable)
+        key = (dynamic, sync, self.masks.data_ptr(), self.theta.data_ptr())
+        graphs = self.__dict__.setdefault("_graphs", {})
+        g = graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            self.defer_host = True
+            try:
+                with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                    self._run_program(k)   # host effects of step k applied once here
+            finally:
+                self.defer_host = False
+            graphs[key] = g
+        else:
+            self._graph_effects(k, dynamic, sync)
+        g.replay()
+        if self._pending is not None:
+            # the summary copy is part of the graph: wait on the replay instead
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pending = (self._pending[0], ev, self._pending[2])
+
+    def _run_program(self, k: int):
+        if hasattr(self.cluster, "run_rank"):
+            return self.cluster.run_rank(self.program(k))
+        return self.cluster.run({self.rank: self.program(k)})
+
+    def _graph_effects(self, k: int, dynamic: bool, sync: bool):
+        """Host side of program(k) for a replayed graph (one rank, deferred mode)."""
+        if not sync:
+            return
+        if not dynamic:
+            if self.is_leader and self.prunable:
+                self.cache_hits += len(self.prunable)
+            self._host_tail(k, False, log_zsync=True)
+            return
+        self.masks, self.union = self.union, self.masks
+        self._pending = (k, None, True)
+
     def step(self, k: int):
         """Run iteration k through a DistCluster (one rank per process)."""
         if not hasattr(self.cluster, "run_rank"):

@@ -261,6 +261,32 @@ def test_step_host_pipeline_against_reference_goldens(transport):
     assert zs == [d for kk in range(1, k + 1) for d in ref.zsync(kk)]
 
 
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_graph_step_against_reference_goldens(transport):
+    """HSADMMSync.graph_step (captured CUDA graphs of the step, replayed with the
+    host bookkeeping deferred) reproduces run_hierarchical across the freeze."""
+    import paper_2512_14628_b200 as H
+
+    ref, cluster, (e,) = _e2e_engines(1, 1, transport)
+    for k in range(1, ref.iters + 1):
+        e.load(theta=ref.theta(k, 0))
+        e.graph_step(k)
+        e.settle()
+        assert e.frozen == ref.frozen(k, 0)
+        for n, m in ref.masks(k, 0).items():
+            assert np.array_equal(cpu(e.mask_dict()[n]), m), (k, n)
+        th = ref.theta(k, 0)
+        for n in ref.names:
+            for key, want in (("z_node", ref.node_state("z_node", k, 0)[n]), ("v", ref.node_state("v", k, 0)[n]),
+                              ("z", ref.node_state("z", k, 0)[n]), ("u", ref.u(k, 0)[n])):
+                err = rel_err(cpu(e.views(key)[n]), want, th[n])
+                assert err <= TOL, (k, key, n, err)
+        assert (e.cache_derive, e.cache_hits) == ref.cache(k, 0)
+    zs = [x.to_dict() for x in cluster.ledger.entries if x.label.startswith("z_sync")]
+    assert zs == [d for kk in range(1, ref.iters + 1) for d in ref.zsync(kk)]
+    assert len(e._graphs) >= 2   # dynamic (both mask buffers) and frozen graphs were replayed
+
+
 # -- full-size stage-wise parity vs the oracle on identical inputs -------------------
 
 

@@ -216,7 +216,9 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       // a multiple of 4 elements; otherwise row tiling (FILTER, stems)
       // a quad tile holds whole channels: cq quads with 4*cq a multiple of kh*kw
       const int kmul = ly.k / std::gcd(ly.k, 4);
-      const int cq = hsx_tile_quads / kmul * kmul;
+      const bool percol = env_flag("HSX_K1_PERCOL", 0) != 0;
+      const int cq = percol ? hsx_tile_quads : hsx_tile_quads / kmul * kmul;
+      ly.percol = percol ? 1 : 0;
       bool quads = (ly.L & 3) == 0 && cq > 0;
       for (int q = 0; q < ly.ncons; ++q) quads = quads && ly.group[q] != HSX_GROUP_FILTER;
       ly.tiling = quads ? 1 : 0;
@@ -248,18 +250,18 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         ly.goff[q] = goff[q];
         goff[q] += ly.G[q];
         ly.poff[q] = poff[q];
-        poff[q] += ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * ly.G[q];
+        poff[q] += ly.group[q] == HSX_GROUP_FILTER ? ly.rows : (long long)ly.nparts * (ly.percol ? ly.L : ly.G[q]);
         p->pass_list[q].push_back(l);
         p->max_passes = std::max(p->max_passes, q + 1);
       }
       ly.mword = mword;
       mword += (ly.n + 31) / 32;
       ly.okeep = okeep;
-      okeep += ly.rows;
+      okeep += (ly.rows + 15) / 16 * 16;  // 16-B aligned per layer (cp.async of the byte flags)
       ly.ikeep = ikeep;
-      ikeep += ly.cin;
+      ikeep += (ly.cin + 15) / 16 * 16;
       ly.cpoff = cpoff;
-      cpoff += (ly.L + 3) / 4 * 4;
+      cpoff += (ly.L + 15) / 16 * 16;
       p->prunable.push_back(l);
       ly.qtile = (ly.L % 32) == 0 ? 1 : 0;
       if (ly.qtile) {
@@ -316,8 +318,21 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     srow[HSX_SUM_ELEMS] = ly.n;
     p->layers.push_back(ly);
   }
-  // dynamic candidate launch: group-norm tiles first, short dense items fill the tail
+  // dynamic candidate launch: group-norm tiles first, short dense items fill the
+  // tail; persistent CTAs take the largest items first
   p->cand_dyn.insert(p->cand_dyn.end(), dense_items.begin(), dense_items.end());
+  // launch order: the tiles of the layers with the costliest selection tails
+  // first (so those tails overlap later items), then the rest, dense items last
+  auto tail_cost = [&](const Item& it) {
+    const DevLayer& ly = p->layers[it.layer];
+    if (ly.ncons == 0) return 0LL;
+    long long c = (long long)ly.rows + ly.cin;
+    for (int q = 0; q < ly.ncons; ++q) c += ly.G[q];
+    return c;
+  };
+  if (env_flag("HSX_K1_ORDER", 1))
+    std::stable_sort(p->cand_dyn.begin(), p->cand_dyn.end(),
+                     [&](const Item& x, const Item& y) { return tail_cost(x) > tail_cost(y); });
   // the last layer needs no trailing pad: arenas may be exactly-sized tensors
   if (n > 0) off = p->layers.back().off + p->layers.back().n;
   p->arena = off;

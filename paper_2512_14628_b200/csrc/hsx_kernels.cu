@@ -1,6 +1,7 @@
 // sm_100a kernels of the H-SADMM synchronization step (see hsx_kernels.cuh).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <utility>
 
 #include "hsx_kernels.cuh"
@@ -50,11 +51,15 @@ static void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem,
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
+  static const bool pdl = [] {
+    const char* v = std::getenv("HSX_PDL");
+    return !(v && v[0] == '0');
+  }();
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
 }
 
@@ -198,6 +203,26 @@ __device__ int block_exclusive_scan(int x, int* warp_tot, int* total) {
   int r = incl - x + warp_tot[warp];
   __syncthreads();
   return r;
+}
+
+// block-wide sums of two values per thread (one pass), results in every thread
+__device__ ulonglong2 block_sum2(unsigned long long x, unsigned long long y) {
+  __shared__ ulonglong2 wsum2[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    x += __shfl_xor_sync(kFull, x, off);
+    y += __shfl_xor_sync(kFull, y, off);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wsum2[warp] = make_ulonglong2(x, y);
+  __syncthreads();
+  ulonglong2 s = make_ulonglong2(0, 0);
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    s.x += wsum2[w].x;
+    s.y += wsum2[w].y;
+  }
+  __syncthreads();
+  return s;
 }
 
 // block-wide sum of one value per thread, result in every thread
@@ -392,8 +417,31 @@ __host__ __device__ inline size_t structured_smem(int rows, int L, int cin) {
   return ((size_t)rows + cin + L + 15) / 16 * 16;
 }
 
+// previous-rectangle flags of the layer (rows, then channels or columns) staged
+// into shared memory by cp.async at the start of the selection, so their loads
+// overlap the norms and the top-k (16-B chunks: okeep / ikeep / cpoff are
+// 16-B aligned per layer); waited for in structured_keep_sets
+__host__ __device__ inline size_t prev_stage_bytes(int rows, int cin, int L, bool shape) {
+  return ((size_t)rows + 15) / 16 * 16 + ((size_t)(shape ? L : cin) + 15) / 16 * 16;
+}
+
+__device__ void stage_prev(const KeepArgs& a, const DevLayer& gly, uint8_t* stage) {
+  bool shape = false;
+  for (int q = 0; q < gly.ncons; ++q) shape |= gly.group[q] == kShape;
+  const int rows = gly.rows, ncol = shape ? gly.L : gly.cin;
+  const int nr = (rows + 15) / 16, nc = (ncol + 15) / 16;
+  const uint8_t* src_r = a.rk_prev + gly.okeep;
+  const uint8_t* src_c = shape ? a.ck_prev + gly.cpoff : a.ch_prev + gly.ikeep;
+  for (int i = threadIdx.x; i < nr + nc; i += blockDim.x) {
+    const uint8_t* src = i < nr ? src_r + 16 * i : src_c + 16 * (i - nr);
+    uint8_t* dst = stage + 16 * i;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  }
+  cp_commit();
+}
+
 __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& gly, int pass,
-                                     const uint8_t* sflag, uint8_t* smem) {
+                                     const uint8_t* sflag, uint8_t* smem, const uint8_t* stage) {
   const int cin = gly.cin, rows = gly.rows, k = gly.k, L = gly.L, npass = gly.ncons;
   const long long ikeep = gly.ikeep, okeep = gly.okeep, cpoff = gly.cpoff;
   const FastDiv divk = gly.divk;
@@ -406,9 +454,20 @@ __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& g
     fq[q] = q < npass ? a.flags.f[q] + gly.goff[q] : nullptr;
     shape |= gq[q] == kShape;
   }
+#ifdef HSX_PROBE_SELECT
+  long long tq[8];
+  tq[0] = clock64();
+#define ST_MARK(i) do { __syncthreads(); tq[i] = clock64(); } while (0)
+#else
+#define ST_MARK(i) do { } while (0)
+#endif
   uint8_t* srk = smem;        // R
   uint8_t* sch = srk + rows;  // channels meeting C
   uint8_t* sck = sch + cin;   // C by column (SHAPE groups)
+  const uint8_t* prev_r = stage;                          // staged rk_prev
+  const uint8_t* prev_c = stage + (rows + 15) / 16 * 16;  // staged ch_prev / ck_prev
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
   // three counts packed per word (21 bits each; rows, columns < 2^20)
   unsigned long long rsum = 0, csum = 0;
   for (int o = threadIdx.x; o < rows; o += blockDim.x) {
@@ -416,7 +475,7 @@ __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& g
 #pragma unroll
     for (int q = 0; q < kMaxPasses; ++q)
       if (gq[q] == kFilter) kp &= q == pass ? sflag[o] : fq[q][o];
-    const uint8_t pv = a.rk_prev[okeep + o];
+    const uint8_t pv = prev_r[o];
     srk[o] = kp;
     a.rk_prev[okeep + o] = kp;
     rsum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
@@ -427,7 +486,7 @@ __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& g
 #pragma unroll
       for (int q = 0; q < kMaxPasses; ++q)
         if (gq[q] == kChannel) kp &= q == pass ? sflag[c] : fq[q][c];
-      const uint8_t pv = a.ch_prev[ikeep + c];
+      const uint8_t pv = prev_c[c];
       sch[c] = kp;
       a.ch_prev[ikeep + c] = kp;
       csum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
@@ -442,7 +501,7 @@ __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& g
         const int g = gq[q] == kChannel ? c : col;
         kp &= q == pass ? sflag[g] : fq[q][g];
       }
-      const uint8_t pv = a.ck_prev[cpoff + col];
+      const uint8_t pv = prev_c[col];
       sck[col] = kp;
       a.ck_prev[cpoff + col] = kp;
       csum += (unsigned long long)kp | ((unsigned long long)pv << 21) | ((unsigned long long)(kp & pv) << 42);
@@ -454,8 +513,13 @@ __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& g
       sch[c] = any;
     }
   }
-  rsum = block_sum(rsum);
-  csum = block_sum(csum);
+  ST_MARK(1);
+  {
+    const ulonglong2 t = block_sum2(rsum, csum);
+    rsum = t.x;
+    csum = t.y;
+  }
+  ST_MARK(2);
   constexpr unsigned long long m21 = (1ULL << 21) - 1;
   const long long cm = shape ? 1 : k;  // columns per counted unit
   const long long nR = rsum & m21, nRp = (rsum >> 21) & m21, nRR = rsum >> 42;
@@ -466,11 +530,19 @@ __device__ void structured_keep_sets(const KeepArgs& a, int l, const DevLayer& g
   if (nR == 0)
     for (int c = threadIdx.x; c < cin; c += blockDim.x) sch[c] = 0;
   __syncthreads();
+  ST_MARK(3);
   const int2 nio = scan_keep<true>(sch, cin, srk, rows, a.pos_in + ikeep, a.pos_out + okeep);
+  ST_MARK(4);
   // |A ^ B| = |A| + |B| - 2 |A n B| for rectangles A = R x C, B = Rp x Cp
   const long long pop = nR * nC;
   const long long drift = pop + nRp * nCp - 2 * nRR * nCC;
   finish_layer(a, l, nio.y, nio.x, k, drift, pop);
+#ifdef HSX_PROBE_SELECT
+  ST_MARK(5);
+  if (threadIdx.x == 0)
+    printf("structured l=%d rows=%d cin=%d nt=%d: RC %lld sums %lld zero %lld scan %lld finish %lld\n", l, rows, cin,
+           (int)blockDim.x, tq[1] - tq[0], tq[2] - tq[1], tq[3] - tq[2], tq[4] - tq[3], tq[5] - tq[4]);
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -568,12 +640,18 @@ __device__ void select_layer(const DevLayer& gly, int pass, const double* __rest
   // layer fields in registers: the byte stores below may alias the layer table
   const int G = gly.G[pass], grp = gly.group[pass], keep = gly.keep[pass];
   const int nparts = grp == kFilter ? 1 : gly.nparts;
+  const int kc = (grp == kChannel && gly.percol) ? gly.k : 1;  // per-column partials: fold kh*kw columns
+  const int pstride = kc > 1 ? gly.L : G;
   const long long goff = gly.goff[pass];
   const double* __restrict__ part = partials + gly.poff[pass];
   unsigned long long* skey = reinterpret_cast<unsigned long long*>(smem);
   uint8_t* sflag = reinterpret_cast<uint8_t*>(skey + G);
   const int nt = blockDim.x;
   const int t = threadIdx.x;
+  const bool structured = ka != nullptr && pass == gly.ncons - 1;
+  uint8_t* stage = reinterpret_cast<uint8_t*>(smem) + select_bytes(G) +
+                   structured_smem(gly.rows, gly.L, gly.cin);
+  if (structured) stage_prev(*ka, gly, stage);
 #ifdef HSX_PROBE_SELECT
   long long tm[6];
   tm[0] = clock64();
@@ -591,7 +669,8 @@ __device__ void select_layer(const DevLayer& gly, int pass, const double* __rest
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int g = g0 + u * nt;
-        if (g < G) s2[u] += __ldcg(part + (long long)pt * G + g);
+        if (g < G)
+          for (int jx = 0; jx < kc; ++jx) s2[u] += __ldcg(part + (long long)pt * pstride + (long long)g * kc + jx);
       }
     }
 #pragma unroll
@@ -613,8 +692,8 @@ __device__ void select_layer(const DevLayer& gly, int pass, const double* __rest
   uint8_t* __restrict__ fl = flags.f[pass] + goff;
   for (int g = t; g < G; g += nt) fl[g] = sflag[g];
   SEL_MARK(3);
-  if (ka != nullptr && pass == gly.ncons - 1)  // one node: keep sets of the rectangle
-    structured_keep_sets(*ka, l, gly, pass, sflag, reinterpret_cast<uint8_t*>(smem) + select_bytes(G));
+  if (structured)  // one node: keep sets of the rectangle
+    structured_keep_sets(*ka, l, gly, pass, sflag, reinterpret_cast<uint8_t*>(smem) + select_bytes(G), stage);
 #ifdef HSX_PROBE_SELECT
   if (t == 0)
     printf("select G=%d nparts=%d nt=%d: norms %lld topk %lld flags %lld cycles\n", G, nparts, nt,
@@ -888,8 +967,9 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   __syncthreads();
   const int col0 = it.chunk * 4 * cq;
   const int ncol = min(4 * cq, L - col0);
+  const bool percol = ly.group[pass] == kShape || ly.k == 1 || ly.percol;
   const int G = ly.G[pass];
-  double* out = p.partials + ly.poff[pass] + (long long)it.part * G;
+  double* out = p.partials + ly.poff[pass] + (long long)it.part * (percol ? L : G);
   const int t = threadIdx.x;
   double s = 0.0;
   if (t < ncol) {  // one column per thread: the row phases in order
@@ -897,7 +977,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
 #pragma unroll
     for (int q = 1; q < RP; ++q) s += cs[q * 4 * kTileQuads + t];
   }
-  if (ly.group[pass] == kShape || ly.k == 1) {
+  if (percol) {
     if (t < ncol) out[col0 + t] = s;
     return;
   }
@@ -945,7 +1025,7 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
       if (lane == 0) p.partials[ly.poff[pass] + r0 + r] = s;
     }
-  } else if (grp == kShape || ly.k == 1) {
+  } else if (grp == kShape || ly.k == 1 || ly.percol) {
     for (int col = threadIdx.x; col < L; col += kThreads) {
       double s = 0.0;
       for (int r = 0; r < nr; ++r) s += sq[r * L + col];
@@ -963,10 +1043,7 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int frozen) {
-  PDL_ENTRY();
-  extern __shared__ float4 ring[];
-  const Item it = p.items[blockIdx.x];
+__device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const Item& it, float4* ring) {
   const DevLayer& ly = p.layers[it.layer];
   if (frozen || ly.ncons == 0) {
     if (p.pass > 0) return;
@@ -1002,6 +1079,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
   __threadfence();
   select_layer(ly, p.pass, p.partials, p.norms, p.fw, ring, it.layer, p.structured ? &p.ka : nullptr);
   if (threadIdx.x == 0) p.cand_done[ly.pidx] = 0;  // ready for the next launch
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int frozen) {
+  PDL_ENTRY();
+  extern __shared__ float4 ring[];
+  cand_item<MODE>(p, frozen, p.items[blockIdx.x], ring);
 }
 
 template <int MODE>
@@ -1042,7 +1126,9 @@ void launch_select(const DevLayer* layers, const int* list, int n, int pass, con
   launch_pdl(k_select, n, 1024, smem, st, layers, list, pass, partials, norms, flags, ka, structured);
 }
 
-size_t structured_smem_bytes(int rows, int L, int cin) { return structured_smem(rows, L, cin); }
+size_t structured_smem_bytes(int rows, int L, int cin) {
+  return structured_smem(rows, L, cin) + prev_stage_bytes(rows, cin, L, true) + 16;
+}
 size_t select_smem_bytes(int G) { return select_bytes(G); }
 
 // ---------------------------------------------------------------------------
@@ -1355,8 +1441,11 @@ __global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* 
         x = skip >= 32 ? 0u : (x & ~((1u << skip) - 1u));
       }
     }
-    pop = block_sum(pop);
-    drift = block_sum(drift);
+    {
+      const ulonglong2 t = block_sum2(pop, drift);
+      pop = t.x;
+      drift = t.y;
+    }
     if (exact) {
       __syncthreads();
       const int2 nio = scan_keep<true>(s_in, cin, s_out, rows, a.pos_in + ikeep, a.pos_out + okeep);

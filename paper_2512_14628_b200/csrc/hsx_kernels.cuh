@@ -60,8 +60,8 @@ struct DevLayer {
   int G[kMaxPasses];
   int ncitems;                 // K1 items of the layer (dynamic launch)
   int npitems;                 // K3 items of the layer
-  int cq;                      // K1 quad tiles: column quads per tile (whole channels)
-  int pad3;
+  int cq;                      // K1 quad tiles: column quads per tile (whole channels unless percol)
+  int percol;                  // K1 writes per-column partials [nparts][L]; the selection folds channels
   FastDiv divL, divk;
   double rho1, rho2, gamma;
   double rgamma;               // RN(1 / gamma), for the FMA-corrected division

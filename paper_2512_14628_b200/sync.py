@@ -32,6 +32,8 @@ on the device.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -75,7 +77,7 @@ class HSADMMSync:
         self.plan.set_penalties(schedule.rho1, schedule.rho2, settings.weight_decay, self.M, self.P)
         # one node: the union mask is every rank's local mask, so the selection derives
         # the keep sets of the kept rectangle and K3 only checks it (hsx_project_keep_sets)
-        self.plan.set_single_node(self.M == 1)
+        self.plan.set_single_node(self.M == 1 and os.environ.get("HSX_SINGLE_NODE", "1") != "0")
         self.prunable = self.plan.prunable
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         pl, dev = self.plan, self.device

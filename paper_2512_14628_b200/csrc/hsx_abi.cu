@@ -214,9 +214,12 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       ly.rsub = std::max(1, kSubElems / ly.L);
       // quad tiling when every pass groups columns (CHANNEL / SHAPE) and rows are
       // a multiple of 4 elements; otherwise row tiling (FILTER, stems)
-      // a quad tile holds whole channels: cq quads with 4*cq a multiple of kh*kw
+      // quad tiles of 64 column quads (1 KB-aligned row segments, per-column
+      // partials folded into channels by the selection); HSX_K1_PERCOL=0 makes a
+      // tile hold whole channels instead (cq quads, 4*cq a multiple of kh*kw,
+      // per-channel partials)
       const int kmul = ly.k / std::gcd(ly.k, 4);
-      const bool percol = env_flag("HSX_K1_PERCOL", 0) != 0;
+      const bool percol = env_flag("HSX_K1_PERCOL", 1) != 0;
       const int cq = percol ? hsx_tile_quads : hsx_tile_quads / kmul * kmul;
       ly.percol = percol ? 1 : 0;
       bool quads = (ly.L & 3) == 0 && cq > 0;
@@ -321,8 +324,8 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   // dynamic candidate launch: group-norm tiles first, short dense items fill the
   // tail; persistent CTAs take the largest items first
   p->cand_dyn.insert(p->cand_dyn.end(), dense_items.begin(), dense_items.end());
-  // launch order: the tiles of the layers with the costliest selection tails
-  // first (so those tails overlap later items), then the rest, dense items last
+  // launch order: layer order (measured best with peer reads; HSX_K1_ORDER=1
+  // launches the layers with the costliest selection tails first instead)
   auto tail_cost = [&](const Item& it) {
     const DevLayer& ly = p->layers[it.layer];
     if (ly.ncons == 0) return 0LL;
@@ -330,7 +333,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     for (int q = 0; q < ly.ncons; ++q) c += ly.G[q];
     return c;
   };
-  if (env_flag("HSX_K1_ORDER", 1))
+  if (env_flag("HSX_K1_ORDER", 0))
     std::stable_sort(p->cand_dyn.begin(), p->cand_dyn.end(),
                      [&](const Item& x, const Item& y) { return tail_cost(x) > tail_cost(y); });
   // the last layer needs no trailing pad: arenas may be exactly-sized tensors

@@ -403,7 +403,7 @@ int upload_plan(hsx_plan* p) {
   if ((rc = alloc0(&p->d_oflag, p->ktotal[0]))) return rc;
   if ((rc = alloc0(&p->d_iflag, p->ktotal[1]))) return rc;
   // identity positions (all kept) until the first keep-set derivation
-  std::vector<int> po(p->ktotal[0]), pi(p->ktotal[1]);
+  std::vector<int> po(p->ktotal[0], -1), pi(p->ktotal[1], -1);  // per-layer padding: -1
   for (int l : p->prunable) {
     const DevLayer& ly = p->layers[l];
     for (int i = 0; i < ly.rows; ++i) po[ly.okeep + i] = i;

@@ -11,10 +11,13 @@ all: $(LIB)
 $(LIB): $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(SRC)
 
+trace: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -DHSX_TRACE $(TRACE_FLAGS) -shared -cudart static -o paper_2512_14628_b200/libhsx_trace.so $(SRC)
+
 ptxas: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /tmp/hsx_kernels.o paper_2512_14628_b200/csrc/hsx_kernels.cu
 
 clean:
 	rm -f $(LIB)
 
-.PHONY: all clean ptxas
+.PHONY: all clean ptxas trace

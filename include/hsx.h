@@ -79,6 +79,9 @@ int hsx_abi_version(void);
 const char* hsx_last_error(void);
 /* number of kernels libhsx has launched in this process */
 int64_t hsx_launch_count(void);
+/* a CUDA graph holding `kernels` libhsx launches (captured through this ABI) was
+   replayed: counted like eager launches */
+void hsx_note_graph_replay(int64_t kernels);
 
 /* ---- plans ----------------------------------------------------------------- */
 int hsx_plan_create(const hsx_layer_desc* layers, int32_t n_layers, hsx_plan** out);

@@ -36,6 +36,7 @@ SIGNATURES = {
     "hsx_abi_version": (C.c_int, []),
     "hsx_last_error": (C.c_char_p, []),
     "hsx_launch_count": (I64, []),
+    "hsx_note_graph_replay": (None, [I64]),
     "hsx_plan_create": (C.c_int, [C.POINTER(LayerDesc), I32, C.POINTER(P)]),
     "hsx_plan_destroy": (None, [P]),
     "hsx_plan_arena_elements": (I64, [P]),
@@ -119,3 +120,8 @@ def ptr_array(ptrs):
 
 def launch_count() -> int:
     return int(load().hsx_launch_count())
+
+
+def note_graph_replay(kernels: int) -> None:
+    """Count the libhsx kernels of a replayed CUDA graph (captured through this ABI)."""
+    load().hsx_note_graph_replay(int(kernels))

@@ -116,6 +116,7 @@ struct hsx_plan {
   Item *d_cand = nullptr, *d_elem = nullptr, *d_stream = nullptr, *d_proj = nullptr, *d_word = nullptr;
   unsigned int* d_layer_done = nullptr;
   unsigned int* d_cand_done = nullptr;
+  unsigned int* d_sched = nullptr;
   unsigned long long* d_acc = nullptr;
   uint8_t *d_rk_prev = nullptr, *d_ck_prev = nullptr, *d_ch_prev = nullptr;
   int *d_irr = nullptr, *d_irr_any = nullptr;
@@ -131,7 +132,7 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
                     d_ch_prev};
     for (void* p : ptrs)
@@ -350,14 +351,17 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     for (int l : p->pass_list[q]) p->select_smem[q] = std::max(p->select_smem[q], select_need(p->layers[l], q));
   }
   p->sqcap = sqcap;
-  // k_candidate: cp.async ring (kDepth x 4 x 256 float4 = 64 KB) + 8 KB quad fold,
-  // or the row-tile path's sub-tile squares + group accumulators
+  // k_candidate: cp.async ring (kDepth x 4 x 256 float4 = 64 KB; the 8 KB quad fold
+  // aliases it once drained: three CTAs per SM), or the row-tile path's sub-tile
+  // squares + group accumulators
   p->cand_smem = std::max((size_t)sqcap * sizeof(double),
-                          (size_t)4 * 4 * 256 * 16 + (size_t)quadcap * sizeof(double));
+                          std::max((size_t)4 * 4 * 256 * 16, (size_t)quadcap * sizeof(double)));
   p->mark_smem = mark_smem;
-  // selection in K1's tail when the keys fit the candidate kernel's shared
-  // memory; the rest take the K2 launch
-  const bool fuse = env_flag("HSX_FUSE_SELECT", 1) != 0;
+  // selection as its own launch (K2, one CTA per layer on otherwise idle SMs) by
+  // default: in K1's tail (HSX_FUSE_SELECT=1) a layer's selection shares its SM
+  // with streaming tiles and every dependent L2 round trip of the tail stalls
+  // behind their traffic (measured: K1 + fused tails 77-85 us vs K1 56 + K2 25)
+  const bool fuse = env_flag("HSX_FUSE_SELECT", 0) != 0;
   for (int q = 0; q < hsx::kMaxPasses; ++q) {
     for (int l : p->pass_list[q]) {
       DevLayer& ly = p->layers[l];
@@ -378,6 +382,7 @@ int upload_plan(hsx_plan* p) {
   if ((rc = upload(&p->d_cand, p->cand_dyn))) return rc;
   if ((rc = alloc0(&p->d_layer_done, (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_cand_done, (long long)p->prunable.size()))) return rc;
+  if ((rc = alloc0(&p->d_sched, 2))) return rc;
   if ((rc = alloc0(&p->d_acc, 2 * (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_irr, (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_irr_any, 1))) return rc;
@@ -443,6 +448,7 @@ extern "C" {
 int hsx_abi_version(void) { return HSX_ABI_VERSION; }
 const char* hsx_last_error(void) { return g_err.c_str(); }
 int64_t hsx_launch_count(void) { return g_launches.load(); }
+void hsx_note_graph_replay(int64_t kernels) { if (kernels > 0) g_launches.fetch_add(kernels); }
 
 int hsx_plan_create(const hsx_layer_desc* layers, int32_t n_layers, hsx_plan** out) {
   if (!out || (!layers && n_layers > 0) || n_layers < 0) return fail(HSX_EINVAL, "null argument");
@@ -556,6 +562,7 @@ static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta
   a.sqcap = p->sqcap;
   for (int q = 0; q < hsx::kMaxPasses; ++q) a.fw.f[q] = p->d_flags[q];
   a.cand_done = p->d_cand_done;
+  a.sched = p->d_sched;
   a.ka = keep_args(p, nullptr, nullptr, nullptr);
   a.structured = p->single_node;
   return a;

@@ -425,6 +425,10 @@ __host__ __device__ inline size_t prev_stage_bytes(int rows, int cin, int L, boo
   return ((size_t)rows + 15) / 16 * 16 + ((size_t)(shape ? L : cin) + 15) / 16 * 16;
 }
 
+__host__ __device__ inline size_t structured_bytes(int rows, int L, int cin) {
+  return structured_smem(rows, L, cin) + prev_stage_bytes(rows, cin, L, true) + 16;
+}
+
 __device__ void stage_prev(const KeepArgs& a, const DevLayer& gly, uint8_t* stage) {
   bool shape = false;
   for (int q = 0; q < gly.ncons; ++q) shape |= gly.group[q] == kShape;
@@ -573,9 +577,17 @@ __device__ void radix_top_k(const unsigned long long* __restrict__ key, int G, i
   for (int i = t; i < 256; i += nt) hist[0][i] = 0;
   __syncthreads();
   for (int shift = 56;; shift -= 8) {
-    for (int g = t; g < G; g += nt) {
-      const unsigned long long x = key[g];
-      if ((x & himask) == prefix) atomicAdd(&hist[buf][255 - ((int)(x >> shift) & 255)], 1);
+    // norms of one layer share their top bytes: warp-aggregate equal bins so a
+    // round costs G/32 shared atomics instead of G serialized on one address
+    for (int g0 = t - (t & 31); g0 < G; g0 += nt) {
+      const int g = g0 + (t & 31);
+      int bin = -1 - (t & 31);  // unique non-bin for lanes past G / off the prefix
+      if (g < G) {
+        const unsigned long long x = key[g];
+        if ((x & himask) == prefix) bin = 255 - ((int)(x >> shift) & 255);
+      }
+      const unsigned same = __match_any_sync(kFull, bin);
+      if (bin >= 0 && (t & 31) == __ffs(same) - 1) atomicAdd(&hist[buf][bin], __popc(same));
     }
     for (int i = t; i < 256; i += nt) hist[buf ^ 1][i] = 0;  // next round's bins
     __syncthreads();
@@ -633,6 +645,7 @@ __device__ void radix_top_k(const unsigned long long* __restrict__ key, int G, i
 // group: [nparts][G] (FILTER: [G], complete row sums), folded in part order.
 // shared memory: keys[G] (u64), flags[G] (u8)
 __host__ __device__ inline size_t select_bytes(int G) { return ((size_t)G * 9 + 15) / 16 * 16; }
+constexpr int kFoldCols = 4096;  // column totals staged per norm chunk (32 KB)
 
 __device__ void select_layer(const DevLayer& gly, int pass, const double* __restrict__ partials,
                              double* __restrict__ norms, const FlagPtrs& flags, void* smem, int l,
@@ -659,29 +672,57 @@ __device__ void select_layer(const DevLayer& gly, int pass, const double* __rest
 #else
 #define SEL_MARK(i) do { } while (0)
 #endif
-  // 1) norms: every thread's partial loads in flight together, folded in part order
-  constexpr int kU = 4;
-  for (int g0 = t; g0 < G; g0 += kU * nt) {
-    double s2[kU];
+  // 1) norms, in column chunks of kFoldCols: each column's nparts partials are
+  // summed in part order (coalesced across threads, all of a thread's loads in
+  // flight together: the tail runs beside streaming CTAs, where every dependent
+  // L2 round trip costs ~1 us), then each group adds its kc column totals in
+  // column order from shared memory. Fixed order: deterministic.
+  double* colsum = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(smem) + select_bytes(G) +
+                                             structured_bytes(gly.rows, gly.L, gly.cin));
+  const int chunk_g = max(1, kFoldCols / kc);
+  for (int g0 = 0; g0 < G; g0 += chunk_g) {
+    const int ng = min(chunk_g, G - g0), nc = ng * kc;
+    const double* __restrict__ pc = part + (long long)g0 * kc;
+    if (nparts <= 4) {  // 4 columns x <= 4 parts per thread in flight together
+      for (int c0 = t; c0 < nc; c0 += 4 * nt) {
+        double v[4][4];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) s2[u] = 0.0;
-    for (int pt = 0; pt < nparts; ++pt) {
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int g = g0 + u * nt;
-        if (g < G)
-          for (int jx = 0; jx < kc; ++jx) s2[u] += __ldcg(part + (long long)pt * pstride + (long long)g * kc + jx);
+          for (int q = 0; q < 4; ++q)
+            v[u][q] = (q < nparts && c0 + u * nt < nc) ? __ldcg(pc + (long long)q * pstride + c0 + u * nt) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double s2 = v[u][0];
+#pragma unroll
+          for (int q = 1; q < 4; ++q)
+            if (q < nparts) s2 += v[u][q];
+          if (c0 + u * nt < nc) colsum[c0 + u * nt] = s2;
+        }
+      }
+    } else {
+      for (int c = t; c < nc; c += nt) {
+        double s2 = 0.0;
+        for (int p0 = 0; p0 < nparts; p0 += 16) {
+          double v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = p0 + u < nparts ? __ldcg(pc + (long long)(p0 + u) * pstride + c) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (p0 + u < nparts) s2 += v[u];
+        }
+        colsum[c] = s2;
       }
     }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int g = g0 + u * nt;
-      if (g < G) {
-        const double nrm = sqrt(s2[u]);
-        norms[goff + g] = nrm;
-        skey[g] = (unsigned long long)__double_as_longlong(nrm);
-      }
+    __syncthreads();
+    for (int g = t; g < ng; g += nt) {
+      double s2 = colsum[g * kc];
+      for (int jx = 1; jx < kc; ++jx) s2 += colsum[g * kc + jx];
+      const double nrm = sqrt(s2);
+      norms[goff + g0 + g] = nrm;
+      skey[g0 + g] = (unsigned long long)__double_as_longlong(nrm);
     }
+    __syncthreads();
   }
   __syncthreads();
   SEL_MARK(1);
@@ -963,6 +1004,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
         a3 = __dadd_rn(a3, __dmul_rn(c[3], c[3]));
       });
   double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
+  __syncthreads();  // cs aliases the ring: every thread is done with its last stage
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
   const int col0 = it.chunk * 4 * cq;
@@ -1042,6 +1084,30 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
   }
 }
 
+#ifdef HSX_TRACE
+// timeline instrumentation (trace builds only: make trace): per item slot
+// [start ns, tile done ns, tail done ns, smid | layer << 16]
+__device__ unsigned long long g_trace[16384 * 4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define TRACE_AT(slot, j, val) \
+  do {                         \
+    if (threadIdx.x == 0 && (slot) < 16384) g_trace[(slot) * 4 + (j)] = (val); \
+  } while (0)
+#else
+#define TRACE_AT(slot, j, val) \
+  do {                         \
+  } while (0)
+#endif
+
 template <int MODE>
 __device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const Item& it, float4* ring) {
   const DevLayer& ly = p.layers[it.layer];
@@ -1062,9 +1128,12 @@ __device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const I
   }
   if (ly.ncons <= p.pass) return;
   if (ly.tiling == 1)
-    cand_tile_quads<MODE>(p, ly, it, ring, reinterpret_cast<double*>(ring + kDepth * K1<MODE>::NB * kThreads));
+    cand_tile_quads<MODE>(p, ly, it, ring, reinterpret_cast<double*>(ring));
   else
     cand_tile_rows<MODE>(p, ly, it, reinterpret_cast<double*>(ring));
+#ifdef HSX_TRACE
+  TRACE_AT((&it - p.items), 1, gtime());
+#endif
   if (!((ly.fsel >> p.pass) & 1)) return;
   // fused K2: the layer's last tile to finish selects its groups (its partials
   // are complete once every tile has released them: fence, then the counter)
@@ -1081,17 +1150,63 @@ __device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const I
   if (threadIdx.x == 0) p.cand_done[ly.pidx] = 0;  // ready for the next launch
 }
 
+// Persistent CTAs (grid = resident CTAs, or one per item if fewer): CTA b starts
+// on item b and then pulls the next unclaimed item from a global counter, so the
+// unequal tiles (ragged column chunks, short dense items, selection tails) balance
+// dynamically instead of leaving a partial second wave. Results do not depend on
+// which CTA runs an item (partials are indexed by item), so they stay
+// deterministic. The last CTA to leave re-zeroes the counters.
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int frozen) {
   PDL_ENTRY();
   extern __shared__ float4 ring[];
-  cand_item<MODE>(p, frozen, p.items[blockIdx.x], ring);
+  __shared__ int next;
+  int idx = blockIdx.x;
+  while (idx < p.n_items) {
+#ifdef HSX_TRACE
+    TRACE_AT(idx, 0, gtime());
+    TRACE_AT(idx, 3, smid() | ((unsigned long long)p.items[idx].layer << 16));
+#endif
+    cand_item<MODE>(p, frozen, p.items[idx], ring);
+#ifdef HSX_TRACE
+    TRACE_AT(idx, 2, gtime());
+#endif
+    if (gridDim.x >= (unsigned)p.n_items) break;
+    __syncthreads();  // ring / fold scratch reused by the next item
+    if (threadIdx.x == 0) next = (int)gridDim.x + (int)atomicAdd(p.sched, 1u);
+    __syncthreads();
+    idx = next;
+  }
+  if (gridDim.x < (unsigned)p.n_items && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+    }
+  }
 }
 
 template <int MODE>
 static void launch_candidate_mode(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
   allow_smem(k_candidate<MODE>, smem);
-  launch_pdl(k_candidate<MODE>, n_items, kThreads, smem, st, a, frozen);
+  static int resident = -1;  // per instantiation; smem is fixed per plan shape class
+  static size_t resident_smem = 0;
+  if (resident < 0 || resident_smem != smem) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_candidate<MODE>, kThreads, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = std::max(1, per_sm) * std::max(1, sms);
+    resident_smem = smem;
+  }
+  static const bool persistent = [] {
+    const char* v = std::getenv("HSX_K1_PERSISTENT");
+    return !(v && v[0] == '0');
+  }();
+  CandArgs b = a;
+  b.n_items = n_items;
+  const int grid = (persistent && a.sched) ? std::min(n_items, resident) : n_items;
+  launch_pdl(k_candidate<MODE>, grid, kThreads, smem, st, b, frozen);
 }
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
@@ -1123,13 +1238,16 @@ void launch_select(const DevLayer* layers, const int* list, int n, int pass, con
                    double* norms, FlagPtrs flags, const KeepArgs& ka, int structured, size_t smem, cudaStream_t st) {
   if (n <= 0) return;
   allow_smem(k_select, smem);
-  launch_pdl(k_select, n, 1024, smem, st, layers, list, pass, partials, norms, flags, ka, structured);
+  static const int nt = [] {
+    const char* v = std::getenv("HSX_SELECT_THREADS");
+    const int x = v ? std::atoi(v) : 1024;
+    return (x >= 64 && x <= 1024 && x % 32 == 0) ? x : 1024;
+  }();
+  launch_pdl(k_select, n, nt, smem, st, layers, list, pass, partials, norms, flags, ka, structured);
 }
 
-size_t structured_smem_bytes(int rows, int L, int cin) {
-  return structured_smem(rows, L, cin) + prev_stage_bytes(rows, cin, L, true) + 16;
-}
-size_t select_smem_bytes(int G) { return select_bytes(G); }
+size_t structured_smem_bytes(int rows, int L, int cin) { return structured_bytes(rows, L, cin); }
+size_t select_smem_bytes(int G) { return select_bytes(G) + (size_t)kFoldCols * sizeof(double); }
 
 // ---------------------------------------------------------------------------
 // K3 project + local mask.  sparsity.py:71-94, 113-115; consensus.py:181-182
@@ -1944,3 +2062,9 @@ void launch_count_diff(const uint8_t* a, const uint8_t* b, long long n, unsigned
 }
 
 }  // namespace hsx
+
+#ifdef HSX_TRACE
+extern "C" int hsx_debug_trace(void* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, hsx::g_trace, (size_t)n * 4 * sizeof(unsigned long long));
+}
+#endif

@@ -134,6 +134,8 @@ struct CandArgs {
   double* norms;                       // this pass
   FlagPtrs fw;                         // keep flags, all passes (this pass written)
   unsigned int* cand_done;             // per prunable layer: K1 tiles finished
+  unsigned int* sched;                 // [2] persistent-CTA item counter + exit counter (left zeroed)
+  int n_items;
   KeepArgs ka;                         // structured keep sets at the last pass (one node)
   int structured;
   int pass;

@@ -107,6 +107,8 @@ class Plan:
         self.mask_offsets = [int(lib.hsx_plan_mask_word_offset(h, i)) for i in range(n)]
         self.max_passes = int(lib.hsx_plan_max_passes(h))
         self.prunable = [i for i, ls in enumerate(layers) if self.groups[ls.name]]
+        self._fetch_stream = None
+        self._fetch_done = None
         self.summary_host = torch.zeros(n * _lib.SUM_COLS + 1, dtype=torch.int64).pin_memory() \
             if torch.cuda.is_available() else torch.zeros(n * _lib.SUM_COLS + 1, dtype=torch.int64)
 
@@ -281,11 +283,29 @@ class Plan:
         return self.summary_host.view(-1)
 
     def keep_sets_fetch_async(self):
-        """Enqueue the D2H of the summary; returns a CUDA event to wait on."""
-        _lib.call("hsx_keep_sets_fetch_async", self._h, self.summary_host.data_ptr(), current_stream())
+        """Enqueue the D2H of the summary on a side stream (forked from the current
+        stream after the keep-set kernels), so the compaction launched next does not
+        queue behind a copy-engine transfer; returns the CUDA event to wait on.
+        :meth:`join_fetch` joins the side stream back before the summary is rewritten."""
+        cur = torch.cuda.current_stream()
+        if self._fetch_stream is None:
+            self._fetch_stream = torch.cuda.Stream(cur.device)
+        fs = self._fetch_stream
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        fs.wait_event(ready)
+        _lib.call("hsx_keep_sets_fetch_async", self._h, self.summary_host.data_ptr(), fs.cuda_stream)
         ev = torch.cuda.Event()
-        ev.record()
+        ev.record(fs)
+        self._fetch_done = ev
         return ev
+
+    def join_fetch(self):
+        """Current stream waits for the last summary copy (end of a step; also closes
+        the fork under CUDA-graph capture)."""
+        if self._fetch_done is not None:
+            torch.cuda.current_stream().wait_event(self._fetch_done)
+            self._fetch_done = None
 
     def summary_np(self):
         """(per-layer rows as a zero-copy numpy view, total payload elements)."""

@@ -314,6 +314,7 @@ class HSADMMSync:
 
     def _end_step(self, k: int, dynamic: bool, ev, log_zsync: bool):
         """masks <- union; host bookkeeping now, or at the next step (defer_host)."""
+        self.plan.join_fetch()
         if dynamic:
             self.masks, self.union = self.union, self.masks
         if ev is not None and self.defer_host:
@@ -501,15 +502,20 @@ class HSADMMSync:
         if g is None:
             g = torch.cuda.CUDAGraph()
             self.defer_host = True
+            n0 = _lib.launch_count()
             try:
                 with torch.cuda.graph(g, capture_error_mode="relaxed"):
                     self._run_program(k)   # host effects of step k applied once here
             finally:
                 self.defer_host = False
+            # captured launches went through the ABI counter once; replays add them again
+            g = (g, _lib.launch_count() - n0)
             graphs[key] = g
+            g[0].replay()
         else:
             self._graph_effects(k, dynamic, sync)
-        g.replay()
+            g[0].replay()
+            _lib.note_graph_replay(g[1])
         if self._pending is not None:
             # the summary copy is part of the graph: wait on the replay instead
             ev = torch.cuda.Event()

@@ -9,10 +9,11 @@ What it is: a float64 numpy restatement of the reference algorithm for the
 sync step of ``admmprune`` 0.1.0 — phases 2-4 and the ``u``-update of phase 5
 of ``hierarchical_program`` (/root/reference/pkg/src/admmprune/consensus.py:436-535)
 plus the freeze/seal bookkeeping (:600-606) — and of the helpers it calls.
-Each function cites the reference file:line it follows. The residual block
-and penalty adaptation (:537-598) are not on the path (SURVEY.md §8(f) "next")
-and are not restated; runs that compare against the reference use
-``PenaltySchedule(adapt=False)``.
+Each function cites the reference file:line it follows. The residual block,
+residual report and penalty adaptation of phase 5 (:537-598, :189-219,
+:239-288) are restated too (``cluster_sync(...,
+residuals=True, sched=Schedule(...))``) and pinned by the adaptive end-to-end
+goldens (``tests/golden/e2e_adapt_*.npz``).
 
 Pinning: ``tests/test_oracle.py`` checks every function here against
 (a) the reference's own known-answer tests restated (tie -> lower index,
@@ -177,6 +178,128 @@ def freeze_check(k, t_freeze, drift_history, window=3) -> bool:
         d == 0.0 for d in drift_history[-window:])
 
 
+# -- residuals, report, penalty adaptation (consensus.py:189-219, 239-288, 537-598)
+
+INTER_SLOTS = 9      # consensus.py:235
+REPORT_SLOTS = 8     # consensus.py:236
+
+
+def sq(a) -> float:
+    return float(np.sum(a * a))                                           # consensus.py:382-383
+
+
+@dataclass
+class Schedule:
+    """PenaltySchedule (consensus.py:42-69) as a mutable record; rho1 / rho2 are the
+    dicts cluster_sync reads, so adaptation carries into the next iteration."""
+    rho1: dict
+    rho2: dict
+    rho1_max: float = 10.0
+    rho2_max: float = 10.0
+    mu: float = 10.0
+    tau_inc: float = 2.0
+    tau_dec: float = 2.0
+    adapt: bool = True
+
+
+def build_residual_report(layers, g, sched: Schedule, num_nodes, per_node, eps_abs, eps_rel):
+    """consensus.py:239-288: per-layer (r_intra, s_intra, r_inter, s_inter, eps_pri_intra,
+    eps_dual_intra, eps_pri_inter, eps_dual_inter) and (r_pri, r_dual, eps_pri, eps_dual,
+    converged) from the globally summed squared norms g[l * 9 + slot]."""
+    world = num_nodes * per_node
+    per_layer = {}
+    r_pri_sq = r_dual_sq = eps_pri_sq = eps_dual_sq = 0.0
+    for li, ly in enumerate(layers):
+        gl = g[li * INTER_SLOTS:(li + 1) * INTER_SLOTS]
+        rho1, rho2 = sched.rho1[ly.name], sched.rho2[ly.name]
+        n = int(np.prod(ly.shape))
+        r_intra = math.sqrt(gl[0])
+        s_intra = rho1 * math.sqrt(per_node * gl[4])
+        r_inter = math.sqrt(gl[3])
+        s_inter = rho2 * math.sqrt(gl[7])
+        eps_pri_intra = math.sqrt(n * world) * eps_abs + eps_rel * max(math.sqrt(gl[1]),
+                                                                       math.sqrt(per_node * gl[5]))
+        eps_dual_intra = math.sqrt(n * world) * eps_abs + eps_rel * rho1 * math.sqrt(gl[2])
+        eps_pri_inter = math.sqrt(n * num_nodes) * eps_abs + eps_rel * max(math.sqrt(gl[5]), math.sqrt(gl[8]))
+        eps_dual_inter = math.sqrt(n * num_nodes) * eps_abs + eps_rel * rho2 * math.sqrt(gl[6])
+        per_layer[ly.name] = (r_intra, s_intra, r_inter, s_inter,
+                              eps_pri_intra, eps_dual_intra, eps_pri_inter, eps_dual_inter)
+        r_pri_sq += r_intra ** 2 + r_inter ** 2
+        r_dual_sq += s_intra ** 2 + s_inter ** 2
+        eps_pri_sq += eps_pri_intra ** 2 + eps_pri_inter ** 2
+        eps_dual_sq += eps_dual_intra ** 2 + eps_dual_inter ** 2
+    r_pri, r_dual = math.sqrt(r_pri_sq), math.sqrt(r_dual_sq)
+    eps_pri, eps_dual = math.sqrt(eps_pri_sq), math.sqrt(eps_dual_sq)
+    return {"layers": per_layer, "r_pri": r_pri, "r_dual": r_dual, "eps_pri": eps_pri,
+            "eps_dual": eps_dual, "converged": r_pri <= eps_pri and r_dual <= eps_dual}
+
+
+def adapt_penalties(report, sched: Schedule):
+    """consensus.py:189-219, in place on sched; returns (u_scale, v_scale) per layer."""
+    u_scale, v_scale = {}, {}
+    for name in list(sched.rho1):
+        r_intra, s_intra, r_inter, s_inter = report["layers"][name][:4]
+        old = sched.rho1[name]
+        if r_intra > sched.mu * s_intra:
+            sched.rho1[name] = min(old * sched.tau_inc, sched.rho1_max)
+        elif s_intra > sched.mu * r_intra:
+            sched.rho1[name] = old / sched.tau_dec
+        u_scale[name] = old / sched.rho1[name] if sched.rho1[name] != old else 1.0
+        old2 = sched.rho2[name]
+        if r_inter > sched.mu * s_inter:
+            sched.rho2[name] = min(old2 * sched.tau_inc, sched.rho2_max)
+        elif s_inter > sched.mu * r_inter:
+            sched.rho2[name] = old2 / sched.tau_dec
+        v_scale[name] = old2 / sched.rho2[name] if sched.rho2[name] != old2 else 1.0
+    return u_scale, v_scale
+
+
+def residual_phase(layers, states, zn_prev, z_prev, sync_iter, num_nodes, per_node, sched,
+                   eps_abs, eps_rel):
+    """consensus.py:537-598 for every rank (after the u-update): squared norms, intra
+    SUM (rank order), leaders' 9-slot vectors, inter SUM (leader order), report,
+    adaptation with the u / v rescaling. Returns (report, r_intra per rank)."""
+    names = [ly.name for ly in layers]
+    vec3 = {}
+    r_intra_local = {}
+    for r, st in enumerate(states):
+        v3 = np.empty(len(names) * 3)
+        for li, n in enumerate(names):
+            d = st.theta[n] - st.z_node[n]
+            v3[li * 3:li * 3 + 3] = (sq(d), sq(st.theta[n]), sq(st.u[n]))
+        vec3[r] = v3
+        r_intra_local[r] = {n: math.sqrt(v3[li * 3]) for li, n in enumerate(names)}
+    leaders = [i * per_node for i in range(num_nodes)]
+    vec9 = {}
+    for i, lr in enumerate(leaders):
+        node = vec3[lr].copy()
+        for r in range(lr + 1, lr + per_node):
+            node = node + vec3[r]
+        st = states[lr]
+        v9 = np.empty(len(names) * INTER_SLOTS)
+        for li, n in enumerate(names):
+            dz = st.z[n] - z_prev[lr][n] if sync_iter else np.zeros_like(st.z[n])
+            v9[li * INTER_SLOTS:(li + 1) * INTER_SLOTS] = (
+                node[li * 3], node[li * 3 + 1], node[li * 3 + 2],
+                sq(st.z_node[n] - st.z[n]), sq(st.z_node[n] - zn_prev[lr][n]), sq(st.z_node[n]),
+                sq(st.v[n]), sq(dz), sq(st.z[n]))
+        vec9[lr] = v9
+    g = vec9[leaders[0]].copy()
+    for lr in leaders[1:]:
+        g = g + vec9[lr]
+    report = build_residual_report(layers, g, sched, num_nodes, per_node, eps_abs, eps_rel)
+    report["global_sums"] = g
+    if sched.adapt:
+        u_scale, v_scale = adapt_penalties(report, sched)
+        for st in states:
+            for n in names:
+                if u_scale[n] != 1.0:
+                    st.u[n] = st.u[n] * u_scale[n]
+                if v_scale[n] != 1.0:
+                    st.v[n] = st.v[n] * v_scale[n]
+    return report, r_intra_local
+
+
 # -- the cluster-wide sync step ------------------------------------------------
 
 
@@ -244,7 +367,8 @@ def _keep_sets(st: RankState, name: str, mask: np.ndarray):
 def cluster_sync(layers, states: list[RankState], thetas: list[dict], k: int,
                  num_nodes: int, per_node: int, rho1: dict, rho2: dict,
                  weight_decay: float, t_freeze: int = 10, drift_window: int = 3,
-                 sync_period: int = 1, ledger: list | None = None) -> None:
+                 sync_period: int = 1, ledger: list | None = None, residuals: bool = False,
+                 sched: Schedule | None = None, eps_abs: float = 1e-4, eps_rel: float = 1e-3):
     """One outer iteration k of the sync path on every rank, in place.
 
     ``thetas[r]`` is rank r's phase-1 output (consensus.py:429). Follows
@@ -252,6 +376,8 @@ def cluster_sync(layers, states: list[RankState], thetas: list[dict], k: int,
     compaction with the fresh union, bucketed leader average, decompaction,
     inter dual, broadcast, intra dual) and the freeze/seal at :600-606.
     Ledger entries (dicts like transport.py:138-151) are appended to ``ledger``.
+    With ``residuals`` (and ``sched`` holding ``rho1`` / ``rho2``) phase 5's residual
+    block and penalty adaptation follow the u-update; returns (report, r_intra).
     """
     world = num_nodes * per_node
     names = [ly.name for ly in layers]
@@ -267,6 +393,8 @@ def cluster_sync(layers, states: list[RankState], thetas: list[dict], k: int,
 
     for r in range(world):
         states[r].theta = {n: np.asarray(thetas[r][n], dtype=np.float64) for n in names}
+    zn_prev = [st.z_node for st in states]
+    z_prev = [st.z for st in states]
 
     # phase 2: intra-node SUM of theta+u, serial fold in rank order (transport.py:453-462)
     sums = {}
@@ -306,7 +434,10 @@ def cluster_sync(layers, states: list[RankState], thetas: list[dict], k: int,
         for r in range(world):
             st = states[r]
             st.u = {n: dual_update_intra(st.theta[n], st.z_node[n], st.u[n]) for n in names}
-        return
+        if residuals:
+            return residual_phase(layers, states, zn_prev, z_prev, False, num_nodes, per_node, sched,
+                                  eps_abs, eps_rel)
+        return None
 
     # phase 4 (leaders): mask union, compaction, bucketed AVG (consensus.py:463-505)
     leaders = [i * per_node for i in range(num_nodes)]
@@ -391,6 +522,12 @@ def cluster_sync(layers, states: list[RankState], thetas: list[dict], k: int,
             st.drift_history.append(max(drift.values()))
         # phase 5: intra dual update (consensus.py:535)
         st.u = {n: dual_update_intra(st.theta[n], st.z_node[n], st.u[n]) for n in names}
+    out = None
+    if residuals:   # residual block + adaptation (consensus.py:537-598), before the freeze check
+        out = residual_phase(layers, states, zn_prev, z_prev, True, num_nodes, per_node, sched,
+                             eps_abs, eps_rel)
+    for r in range(world):
+        st = states[r]
         # freeze + seal (consensus.py:600-606)
         if not st.frozen and prunable and freeze_check(k, t_freeze, st.drift_history, drift_window):
             st.frozen = True
@@ -398,3 +535,4 @@ def cluster_sync(layers, states: list[RankState], thetas: list[dict], k: int,
                 for ly in prunable:
                     _keep_sets(st, ly.name, st.masks[ly.name])
                 st.sealed = True
+    return out

@@ -185,7 +185,7 @@ class _FixedWorkload:
         return {k: v.copy() for k, v in self._p0.items()}
 
 
-def gen_e2e(num_nodes, per_node, seed=3):
+def gen_e2e(num_nodes, per_node, seed=3, adapt=False):
     world = num_nodes * per_node
     rng = np.random.default_rng([seed, 777, num_nodes, per_node])
     specs = [LayerSpec(n, kind, shape, prunable=bool(c)) for n, kind, shape, c in E2E_LAYERS]
@@ -201,7 +201,7 @@ def gen_e2e(num_nodes, per_node, seed=3):
                        for n in params0}
               for k in range(1, E2E_ITERS + 1) for r in range(world)}
     names = [ls.name for ls in specs]
-    sched = PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False)
+    sched = PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=adapt)
     solver = SolverConfig()
     out = {"meta": np.array([num_nodes, per_node, E2E_ITERS, E2E_T_FREEZE])}
     for n in names:  # inputs are fp32-representable: stored as float32 (exact)
@@ -220,6 +220,17 @@ def gen_e2e(num_nodes, per_node, seed=3):
             cluster = Cluster(Topology(num_nodes, per_node))
             res = run_hierarchical(cluster, _FixedWorkload(specs, params0, world), constraints,
                                    sched, solver, settings)
+            if adapt and iters == E2E_ITERS:  # phase 5 per iteration, from the trace rows
+                for row in res[0].trace:
+                    k = row["k"]
+                    out[f"report/{k}"] = ref_consensus.pack_report(row["report"], names)
+                    out[f"rho1/{k}"] = np.array([row["rho1"][n] for n in names])
+                    out[f"rho2/{k}"] = np.array([row["rho2"][n] for n in names])
+                for r in range(world):
+                    for row in res[r].trace:
+                        out[f"r_intra/{row['k']}/{r}"] = np.array([row["r_intra"][n] for n in names])
+                out["rho_final"] = np.array([[res[0].state.schedule.rho1[n] for n in names],
+                                             [res[0].state.schedule.rho2[n] for n in names]])
             for r in range(world):
                 st = res[r].state
                 for n in names:
@@ -246,7 +257,8 @@ def gen_e2e(num_nodes, per_node, seed=3):
             out[f"zsync/{iters}"] = np.array(json.dumps(zs))
     finally:
         ref_consensus.batch_rng, ref_consensus.proximal_sgd = saved
-    np.savez_compressed(os.path.join(HERE, f"e2e_{num_nodes}x{per_node}.npz"), **out)
+    tag = "e2e_adapt" if adapt else "e2e"
+    np.savez_compressed(os.path.join(HERE, f"{tag}_{num_nodes}x{per_node}.npz"), **out)
 
 
 if __name__ == "__main__":
@@ -256,4 +268,6 @@ if __name__ == "__main__":
     gen_candidate()
     for m, p in [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (1, 4), (4, 1)]:
         gen_e2e(m, p)
+    for m, p in [(1, 1), (2, 1), (1, 2), (2, 2)]:
+        gen_e2e(m, p, adapt=True)
     print("golden fixtures written to", HERE)

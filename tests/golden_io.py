@@ -24,6 +24,7 @@ E2E_LAYERS = [
 ]
 E2E_RHO1, E2E_RHO2, E2E_WD = 1.5e-3, 1.5e-4, 1e-4
 E2E_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (1, 4), (4, 1)]
+E2E_ADAPT_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2)]   # phase 5 with adaptive penalties
 
 
 def load(name):
@@ -63,8 +64,8 @@ def candidate_cases():
 class E2E:
     """One end-to-end reference run (run_hierarchical, phase 1 replaced)."""
 
-    def __init__(self, num_nodes, per_node):
-        self.d = load(f"e2e_{num_nodes}x{per_node}.npz")
+    def __init__(self, num_nodes, per_node, adapt=False):
+        self.d = load(f"{'e2e_adapt' if adapt else 'e2e'}_{num_nodes}x{per_node}.npz")
         self.M, self.P, self.iters, self.t_freeze = (int(x) for x in self.d["meta"])
         self.world = self.M * self.P
         self.names = [n for n, *_ in E2E_LAYERS]
@@ -92,3 +93,19 @@ class E2E:
 
     def zsync(self, k):
         return json.loads(str(self.d[f"zsync/{k}"]))
+
+    # phase 5 (adaptive runs only): the report packed as consensus.pack_report
+    # (per layer r_intra, s_intra, r_inter, s_inter, eps_pri_intra, eps_dual_intra,
+    # eps_pri_inter, eps_dual_inter; then r_pri, r_dual, eps_pri, eps_dual, converged),
+    # the penalties iteration k ran with, and each rank's local r_intra
+    def report(self, k):
+        return self.d[f"report/{k}"]
+
+    def rho(self, k):
+        return self.d[f"rho1/{k}"], self.d[f"rho2/{k}"]
+
+    def r_intra(self, k, r):
+        return self.d[f"r_intra/{k}/{r}"]
+
+    def rho_final(self):
+        return self.d["rho_final"]

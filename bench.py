@@ -285,7 +285,8 @@ def run_ours(args):
     names = [ls.name for ls in layers]
     sched = H.PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False)
     settings = H.ConsensusSettings(t_freeze=10**9, drift_window=0, weight_decay=1e-4)
-    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, device=dev, transport=args.transport)
+    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, device=dev, transport=args.transport,
+                       residuals=False)
     config["transport"] = eng.transport
     base = synthetic_base(layers, args.seed)
     st = synthetic_rank_state(layers, rank, topo.accels_per_node, args.seed, base)

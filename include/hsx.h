@@ -207,6 +207,43 @@ int hsx_dual_intra(const hsx_plan* plan, const float* theta, float* u, const flo
 int hsx_decompact_dual(const hsx_plan* plan, const float* flat, float divisor,
                        const float* z_node, float* v, float* z, void* stream);
 
+/* ---- phase 5: residuals, report, adaptive penalties --------------------------
+ * (hierarchical_program phase 5, consensus.py:537-598; build_residual_report
+ * :239-288; adapt_penalties :189-219). Per-layer fp64 squared norms are
+ * accumulated inside K6 / K7 (no extra pass over the arenas), folded per layer
+ * in a fixed order, summed over the node (intra) and the leaders (inter) by
+ * the caller's collectives, turned into the report on the device, and the
+ * adapted penalties are written into the plan's device layer table (the next
+ * K1 uses them; no host round trip). */
+typedef struct hsx_resid_params {
+  double weight_decay, eps_abs, eps_rel;          /* ConsensusSettings (consensus.py:94-110) */
+  double mu, tau_inc, tau_dec, rho1_max, rho2_max; /* PenaltySchedule (consensus.py:42-69) */
+  int32_t num_nodes, accels_per_node, adapt;
+} hsx_resid_params;
+/* K6 + residual slots 0-2 per layer: (theta - z_node)^2, theta^2, u'^2
+ * (consensus.py:541-545). flat == NULL: the intra dual alone (followers). */
+int hsx_compact_dual_resid(const hsx_plan* plan, const float* theta, float* u, const float* z_node,
+                           const float* v, float* flat, void* stream);
+/* K7 + residual slots 3-8: (z_node - z)^2, (z_node - z_node_prev)^2, z_node^2, v'^2,
+ * (z - z_prev)^2, z^2 (consensus.py:552-563; z_prev is z as it was before this
+ * call). flat == NULL: a non-sync iteration (z, v unchanged, dz = 0, no stores). */
+int hsx_decompact_dual_resid(const hsx_plan* plan, const float* flat, float divisor,
+                             const float* z_node, const float* z_node_prev, float* v, float* z,
+                             void* stream);
+/* vec[layer][9] = the layer's slot sums (leader == 0 zeroes slots 3-8: the
+ * node's leader contributes them to the intra SUM, consensus.py:550-563). */
+int hsx_residual_fold(hsx_plan* plan, int32_t leader, double* vec, void* stream);
+/* global != NULL: report[layer][8] + (r_pri, r_dual, eps_pri, eps_dual, converged)
+ * from the globally summed vec (pack_report layout, consensus.py:291-300), then
+ * adaptation; global == NULL: adaptation from a received report. scales[0][l] /
+ * scales[1][l] receive the u / v rescale factors (1 when unchanged). */
+int hsx_residual_report(hsx_plan* plan, const double* global, double* report, double* scales,
+                        const hsx_resid_params* params, void* stream);
+/* u *= scales[0][l], v *= scales[1][l] for the layers whose factor != 1. */
+int hsx_scale_duals(const hsx_plan* plan, const double* scales, float* u, float* v, void* stream);
+/* Current per-layer penalties (after device-side adaptation); synchronous. */
+int hsx_plan_read_penalties(hsx_plan* plan, double* rho1, double* rho2);
+
 /* ---- fused peer-memory collectives (one process per GPU, NVLink) ---------------
  * Pointer arrays are HOST arrays of DEVICE pointers to the same buffer on every
  * rank of a group, in member (rank) order, mapped into this process (e.g. torch

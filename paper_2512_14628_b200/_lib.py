@@ -18,6 +18,7 @@ ABI_VERSION = 1
 HSX_OK, HSX_ESHAPE, HSX_EPROTOCOL, HSX_ECONFIG, HSX_ECUDA, HSX_EINVAL = range(6)
 SUM_KOUT, SUM_KIN, SUM_ELEMS, SUM_OFFSET, SUM_DRIFT, SUM_POP, SUM_COLS = range(7)
 MAX_CONSTRAINTS = 3
+RESID_SLOTS = 9     # residual slots per layer (consensus.py:235)
 
 _ERRORS = {HSX_ESHAPE: ShapeError, HSX_EPROTOCOL: ProtocolError, HSX_ECONFIG: ConfigError,
            HSX_ECUDA: CudaError, HSX_EINVAL: ValueError}
@@ -30,6 +31,14 @@ class LayerDesc(C.Structure):
 
 
 P, I32, I64, F32, F64, VP = (C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_double, C.c_void_p)
+
+
+class ResidParams(C.Structure):
+    """hsx_resid_params (include/hsx.h)."""
+    _fields_ = [("weight_decay", C.c_double), ("eps_abs", C.c_double), ("eps_rel", C.c_double),
+                ("mu", C.c_double), ("tau_inc", C.c_double), ("tau_dec", C.c_double),
+                ("rho1_max", C.c_double), ("rho2_max", C.c_double),
+                ("num_nodes", C.c_int32), ("accels_per_node", C.c_int32), ("adapt", C.c_int32)]
 
 # name -> (restype, argtypes); every int-returning entry point is error-checked
 SIGNATURES = {
@@ -66,6 +75,12 @@ SIGNATURES = {
     "hsx_compact_dual": (C.c_int, [P, VP, VP, VP, VP, VP, VP]),
     "hsx_dual_intra": (C.c_int, [P, VP, VP, VP, VP]),
     "hsx_decompact_dual": (C.c_int, [P, VP, F32, VP, VP, VP, VP]),
+    "hsx_compact_dual_resid": (C.c_int, [P, VP, VP, VP, VP, VP, VP]),
+    "hsx_decompact_dual_resid": (C.c_int, [P, VP, F32, VP, VP, VP, VP, VP]),
+    "hsx_residual_fold": (C.c_int, [P, I32, VP, VP]),
+    "hsx_residual_report": (C.c_int, [P, VP, VP, VP, C.POINTER(ResidParams), VP]),
+    "hsx_scale_duals": (C.c_int, [P, VP, VP, VP, VP]),
+    "hsx_plan_read_penalties": (C.c_int, [P, VP, VP]),
     "hsx_nonzero_u8": (C.c_int, [VP, I64, VP, VP]),
     "hsx_pack_bits": (C.c_int, [VP, I64, VP, VP]),
     "hsx_unpack_bits": (C.c_int, [VP, I64, VP, VP]),

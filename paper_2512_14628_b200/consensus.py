@@ -49,6 +49,43 @@ class PenaltySchedule:
 
 
 @dataclass(frozen=True)
+class LayerResiduals:
+    """Per-layer residuals and tolerances (consensus.py:72-81)."""
+
+    r_intra: float
+    s_intra: float
+    r_inter: float
+    s_inter: float
+    eps_pri_intra: float
+    eps_dual_intra: float
+    eps_pri_inter: float
+    eps_dual_inter: float
+
+
+@dataclass(frozen=True)
+class ResidualReport:
+    """Phase-5 report (consensus.py:84-91): per-layer residuals + global totals."""
+
+    layers: dict
+    r_pri: float
+    r_dual: float
+    eps_pri: float
+    eps_dual: float
+    converged: bool
+
+
+REPORT_SLOTS = 8  # consensus.py:236
+
+
+def unpack_report(vec, layer_names) -> ResidualReport:
+    """Inverse of the reference's pack_report layout (consensus.py:291-314)."""
+    v = [float(x) for x in vec]
+    layers = {n: LayerResiduals(*v[i * REPORT_SLOTS:(i + 1) * REPORT_SLOTS]) for i, n in enumerate(layer_names)}
+    t = v[len(layer_names) * REPORT_SLOTS:]
+    return ResidualReport(layers, t[0], t[1], t[2], t[3], bool(t[4]))
+
+
+@dataclass(frozen=True)
 class ConsensusSettings:
     iterations: int = 1
     t_freeze: int = 10

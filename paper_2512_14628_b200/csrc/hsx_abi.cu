@@ -117,6 +117,8 @@ struct hsx_plan {
   unsigned int* d_layer_done = nullptr;
   unsigned int* d_cand_done = nullptr;
   unsigned int* d_sched = nullptr;
+  int *d_sfirst = nullptr, *d_scount = nullptr;  // per layer: first stream item, item count
+  double* d_rpart = nullptr;                       // residual partials [stream item][9]
   unsigned long long* d_acc = nullptr;
   uint8_t *d_rk_prev = nullptr, *d_ck_prev = nullptr, *d_ch_prev = nullptr;
   int *d_irr = nullptr, *d_irr_any = nullptr;
@@ -132,7 +134,7 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
                     d_ch_prev};
     for (void* p : ptrs)
@@ -396,6 +398,17 @@ int upload_plan(hsx_plan* p) {
   if (rc) return rc;
   if ((rc = upload(&p->d_elem, p->elem_items))) return rc;
   if ((rc = upload(&p->d_stream, p->stream_items))) return rc;
+  {  // stream items are laid out layer by layer: per-layer ranges for the residual fold
+    std::vector<int> first(p->n_layers, 0), count(p->n_layers, 0);
+    for (size_t i = p->stream_items.size(); i-- > 0;) {
+      first[p->stream_items[i].layer] = (int)i;
+      ++count[p->stream_items[i].layer];
+    }
+    if ((rc = upload(&p->d_sfirst, first))) return rc;
+    if ((rc = upload(&p->d_scount, count))) return rc;
+    if ((rc = alloc0(&p->d_rpart, (long long)std::max<size_t>(1, p->stream_items.size()) * hsx::kResidSlots)))
+      return rc;
+  }
   if ((rc = upload(&p->d_proj, p->proj_items))) return rc;
   if ((rc = upload(&p->d_word, p->word_items))) return rc;
   if ((rc = upload(&p->d_prunable, p->prunable))) return rc;
@@ -854,6 +867,104 @@ int hsx_decompact_dual(const hsx_plan* p, const float* flat, float divisor, cons
   a.z = z;
   hsx::launch_decompact(a, (int)p->stream_items.size(), S(stream));
   HSX_LAUNCHED("decompact_dual");
+  return HSX_OK;
+}
+
+int hsx_compact_dual_resid(const hsx_plan* p, const float* theta, float* u, const float* z_node,
+                           const float* v, float* flat, void* stream) {
+  if (!p || !theta || !u || !z_node) return fail(HSX_EINVAL, "null argument");
+  if (flat && !v) return fail(HSX_EINVAL, "compaction needs v");
+  hsx::ElemArgs a = elem_args(p);
+  a.theta = theta;
+  a.u = u;
+  a.zn = z_node;
+  a.vin = v;
+  a.flat_out = flat;
+  a.rpart = p->d_rpart;
+  hsx::launch_compact(a, (int)p->stream_items.size(), S(stream));
+  HSX_LAUNCHED("compact_dual_resid");
+  return HSX_OK;
+}
+
+int hsx_decompact_dual_resid(const hsx_plan* p, const float* flat, float divisor, const float* z_node,
+                             const float* z_node_prev, float* v, float* z, void* stream) {
+  if (!p || !z_node || !z_node_prev || !v || !z) return fail(HSX_EINVAL, "null argument");
+  if (!(divisor > 0.0f)) return fail(HSX_EINVAL, "divisor must be positive");
+  hsx::ElemArgs a = elem_args(p);
+  a.flat_in = flat;
+  a.divisor = divisor;
+  a.zn = z_node;
+  a.zn_prev = z_node_prev;
+  a.v = v;
+  a.z = z;
+  a.rpart = p->d_rpart;
+  hsx::launch_decompact(a, (int)p->stream_items.size(), S(stream));
+  HSX_LAUNCHED("decompact_dual_resid");
+  return HSX_OK;
+}
+
+static hsx::ResidArgs resid_args(hsx_plan* p) {
+  hsx::ResidArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.layers = p->d_layers;
+  a.n_layers = p->n_layers;
+  a.first = p->d_sfirst;
+  a.count = p->d_scount;
+  a.rpart = p->d_rpart;
+  return a;
+}
+
+int hsx_residual_fold(hsx_plan* p, int32_t leader, double* vec, void* stream) {
+  if (!p || !vec) return fail(HSX_EINVAL, "null argument");
+  hsx::ResidArgs a = resid_args(p);
+  a.vec = vec;
+  a.leader = leader ? 1 : 0;
+  hsx::launch_resid_fold(a, S(stream));
+  HSX_LAUNCHED("residual_fold");
+  return HSX_OK;
+}
+
+int hsx_residual_report(hsx_plan* p, const double* global, double* report, double* scales,
+                        const hsx_resid_params* prm, void* stream) {
+  if (!p || !report || !scales || !prm) return fail(HSX_EINVAL, "null argument");
+  if (prm->num_nodes < 1 || prm->accels_per_node < 1) return fail(HSX_ECONFIG, "topology dimensions must be positive");
+  hsx::ResidArgs a = resid_args(p);
+  a.global = global;
+  a.report = report;
+  a.scales = scales;
+  a.wd = prm->weight_decay;
+  a.eps_abs = prm->eps_abs;
+  a.eps_rel = prm->eps_rel;
+  a.mu = prm->mu;
+  a.tau_inc = prm->tau_inc;
+  a.tau_dec = prm->tau_dec;
+  a.rho1_max = prm->rho1_max;
+  a.rho2_max = prm->rho2_max;
+  a.num_nodes = prm->num_nodes;
+  a.per_node = prm->accels_per_node;
+  a.adapt = prm->adapt ? 1 : 0;
+  hsx::launch_report(a, S(stream));
+  HSX_LAUNCHED("residual_report");
+  return HSX_OK;
+}
+
+int hsx_scale_duals(const hsx_plan* p, const double* scales, float* u, float* v, void* stream) {
+  if (!p || !scales || !u || !v) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_scale_duals(p->d_layers, p->d_stream, (int)p->stream_items.size(), scales, p->n_layers, u, v,
+                          S(stream));
+  HSX_LAUNCHED("scale_duals");
+  return HSX_OK;
+}
+
+int hsx_plan_read_penalties(hsx_plan* p, double* rho1, double* rho2) {
+  if (!p || !rho1 || !rho2) return fail(HSX_EINVAL, "null argument");
+  if (p->n_layers)
+    HSX_CUDA(cudaMemcpy(p->layers.data(), p->d_layers, p->layers.size() * sizeof(DevLayer),
+                        cudaMemcpyDeviceToHost));
+  for (int l = 0; l < p->n_layers; ++l) {
+    rho1[l] = p->layers[l].rho1;
+    rho2[l] = p->layers[l].rho2;
+  }
   return HSX_OK;
 }
 

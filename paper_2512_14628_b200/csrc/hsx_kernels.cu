@@ -1663,7 +1663,35 @@ __device__ __forceinline__ int4 add_base(int rb, int4 cp) {
                    cp.w < 0 ? -1 : rb + cp.w);
 }
 
-// K6: flat[payload] <- z_node + v  (+ u <- u + (theta - z_node)) for one item
+// fp64 sums of NS per-thread values over the block (xor-shuffle, then the warps in
+// order: deterministic), written by thread 0 to out[0..NS)
+template <int NS>
+__device__ __forceinline__ void block_partials(double (&acc)[NS], double* __restrict__ out) {
+  __shared__ double red[kThreads / 32][NS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(kFull, acc[q], off);
+    if (lane == 0) red[warp][q] = acc[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      double x = red[0][q];
+      for (int w = 1; w < kThreads / 32; ++w) x += red[w][q];
+      out[q] = x;
+    }
+  }
+}
+
+__device__ __forceinline__ double sqd(double x) { return x * x; }
+
+// K6: flat[payload] <- z_node + v  (+ u <- u + (theta - z_node)) for one item.
+// flat_out == nullptr: the intra dual alone (a follower's K6f). RESID: the item's
+// sums of (theta - z_node)^2, theta^2, u'^2 (consensus.py:541-545) -> rpart slots 0-2.
+template <bool RESID>
 __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   PDL_ENTRY();
   extern __shared__ float4 ring[];
@@ -1676,10 +1704,11 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   const float* __restrict__ VI = a.vin ? a.vin + ly.off : nullptr;
   const float* __restrict__ TH = a.u ? a.theta + ly.off : nullptr;
   float* __restrict__ UU = a.u ? a.u + ly.off : nullptr;
-  float* __restrict__ flat = a.flat_out + coff;
+  float* __restrict__ flat = a.flat_out ? a.flat_out + coff : nullptr;
+  double acc[3] = {0.0, 0.0, 0.0};
   auto load4 = [&](int d, long long e) {
     cp_quad(ring_slot<4>(ring, d, 0), ZN, e, ly.n);
-    if (VI) cp_quad(ring_slot<4>(ring, d, 1), VI, e, ly.n);
+    if (VI && flat) cp_quad(ring_slot<4>(ring, d, 1), VI, e, ly.n);
     if (TH) {
       cp_quad(ring_slot<4>(ring, d, 2), TH, e, ly.n);
       cp_quad(ring_slot<4>(ring, d, 3), UU, e, ly.n);
@@ -1687,17 +1716,27 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   };
   auto emit = [&](int d, long long e, int4 dd) {
     float4 zn = *ring_slot<4>(ring, d, 0);
-    float4 vv = VI ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
     if (TH) {
       float4 th = *ring_slot<4>(ring, d, 2), uu = *ring_slot<4>(ring, d, 3);
       float4 un = make_float4(dual1(uu.x, th.x, zn.x), dual1(uu.y, th.y, zn.y), dual1(uu.z, th.z, zn.z),
                               dual1(uu.w, th.w, zn.w));
+      if (RESID) {  // out-of-range lanes of a tail quad were zero-filled: they add 0
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2) {
+          const double t = f4get(th, i2);
+          acc[0] += sqd(t - (double)f4get(zn, i2));
+          acc[1] += sqd(t);
+          acc[2] += sqd((double)f4get(un, i2));
+        }
+      }
       if (e + 3 < ly.n) {
         st4(UU + e, un);
       } else {
         for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) UU[e + i2] = f4get(un, i2);
       }
     }
+    if (!flat) return;
+    float4 vv = VI ? *ring_slot<4>(ring, d, 1) : make_float4(0.f, 0.f, 0.f, 0.f);
     if (dd.x >= 0) flat[dd.x] = zn.x + vv.x;
     if (dd.y >= 0) flat[dd.y] = zn.y + vv.y;
     if (dd.z >= 0) flat[dd.z] = zn.z + vv.z;
@@ -1705,70 +1744,110 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   };
   if (it.tile == 1) {
     const TileCtx tc(it, ly.L);
-    row_base(a, ly, it, rowlen, s_rb);
-    const int4 cp = col_pos4(a, ly, tc.j, tc.valid);
+    if (flat) row_base(a, ly, it, rowlen, s_rb);
+    const int4 cp = flat ? col_pos4(a, ly, tc.j, tc.valid) : make_int4(-1, -1, -1, -1);
     __syncthreads();
     ring_run(tc.count, [&](int d, int i) { load4(d, tc.row(i) * ly.L + 4 * tc.j); },
              [&](int d, int i) {
                const long long r = tc.row(i);
-               emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
+               emit(d, r * ly.L + 4 * tc.j, flat ? add_base(s_rb[r - it.begin], cp) : cp);
              });
-    return;
+  } else {
+    const long long nq = (it.end - it.begin + 3) >> 2;
+    const int t = threadIdx.x;
+    const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
+    ring_run(count, [&](int d, int i) { load4(d, it.begin + 4 * (t + (long long)i * kThreads)); },
+             [&](int d, int i) {
+               const long long e = it.begin + 4 * (t + (long long)i * kThreads);
+               emit(d, e, flat ? dst4_linear(a, ly, rowlen, e) : make_int4(-1, -1, -1, -1));
+             });
   }
-  const long long nq = (it.end - it.begin + 3) >> 2;
-  const int t = threadIdx.x;
-  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
-  ring_run(count, [&](int d, int i) { load4(d, it.begin + 4 * (t + (long long)i * kThreads)); },
-           [&](int d, int i) {
-             const long long e = it.begin + 4 * (t + (long long)i * kThreads);
-             emit(d, e, dst4_linear(a, ly, rowlen, e));
-           });
+  if (RESID) block_partials<3>(acc, a.rpart + (long long)blockIdx.x * kResidSlots);
 }
 
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * 4 * kThreads * sizeof(float4);
-  allow_smem(k_compact, smem);
-  launch_pdl(k_compact, n_items, kThreads, smem, st, a);
+  if (a.rpart) {
+    allow_smem(k_compact<true>, smem);
+    launch_pdl(k_compact<true>, n_items, kThreads, smem, st, a);
+  } else {
+    allow_smem(k_compact<false>, smem);
+    launch_pdl(k_compact<false>, n_items, kThreads, smem, st, a);
+  }
 }
 
 // K7: z <- zero-filled gather of flat / divisor (+ v <- v + (z_node - z)); the
 // gather streams through the ring: dropped coordinates are zero-filled by
-// cp.async without touching memory.
+// cp.async without touching memory. RESID: also streams the previous z (read
+// before it is overwritten) and the previous z_node, and sums (z_node - z)^2,
+// (z_node - z_node_prev)^2, z_node^2, v'^2, (z - z_prev)^2, z^2
+// (consensus.py:552-563) -> rpart slots 3-8. RESID with flat_in == nullptr: a
+// non-sync iteration (z, v unchanged, dz = 0, nothing stored).
+template <bool RESID>
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   PDL_ENTRY();
-  constexpr int NB = 3;
+  constexpr int NB = RESID ? 5 : 3;
   extern __shared__ float4 ring[];
   __shared__ int s_rb[kMaxTileRows];
   const Item it = a.items[blockIdx.x];
   const LayerRegs ly(a.layers, it.layer);
   const long long coff = a.summary[(long long)it.layer * kSumCols + 3];
   const int rowlen = (int)a.summary[(long long)it.layer * kSumCols + 1] * ly.k;  // |K_in| * k
-  const float* __restrict__ flat = a.flat_in + coff;
+  const bool sync = !RESID || a.flat_in != nullptr;
+  const float* __restrict__ flat = sync ? a.flat_in + coff : nullptr;
   const float* __restrict__ ZN = a.v ? a.zn + ly.off : nullptr;
   float* __restrict__ VV = a.v ? a.v + ly.off : nullptr;
   float* __restrict__ ZO = a.z + ly.off;
+  const float* __restrict__ ZP = RESID ? a.zn_prev + ly.off : nullptr;
   const float div = a.divisor;
+  double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   auto load = [&](int d, long long e, int4 dd) {
-    float* g = reinterpret_cast<float*>(ring_slot<NB>(ring, d, 0));
-    cp4z(g + 0, flat + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
-    cp4z(g + 1, flat + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
-    cp4z(g + 2, flat + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
-    cp4z(g + 3, flat + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
+    if (sync) {
+      float* g = reinterpret_cast<float*>(ring_slot<NB>(ring, d, 0));
+      cp4z(g + 0, flat + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
+      cp4z(g + 1, flat + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
+      cp4z(g + 2, flat + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
+      cp4z(g + 3, flat + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
+    }
     if (ZN) {
       cp_quad(ring_slot<NB>(ring, d, 1), ZN, e, ly.n);
       cp_quad(ring_slot<NB>(ring, d, 2), VV, e, ly.n);
     }
+    if (RESID) {
+      cp_quad(ring_slot<NB>(ring, d, RESID ? 3 : 0), ZP, e, ly.n);
+      cp_quad(ring_slot<NB>(ring, d, RESID ? 4 : 0), ZO, e, ly.n);
+    }
   };
   auto emit = [&](int d, long long e) {
-    float4 zo = *ring_slot<NB>(ring, d, 0);
-    if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
+    float4 zo;
+    if (sync) {
+      zo = *ring_slot<NB>(ring, d, 0);
+      if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
+    } else {
+      zo = *ring_slot<NB>(ring, d, RESID ? 4 : 0);
+    }
     float4 vn;
     if (ZN) {
       float4 zn = *ring_slot<NB>(ring, d, 1), vv = *ring_slot<NB>(ring, d, 2);
-      vn = make_float4(dual1(vv.x, zn.x, zo.x), dual1(vv.y, zn.y, zo.y), dual1(vv.z, zn.z, zo.z),
-                       dual1(vv.w, zn.w, zo.w));
+      vn = sync ? make_float4(dual1(vv.x, zn.x, zo.x), dual1(vv.y, zn.y, zo.y), dual1(vv.z, zn.z, zo.z),
+                              dual1(vv.w, zn.w, zo.w))
+                : vv;
+      if (RESID) {  // zero-filled tail lanes add 0
+        const float4 zp = *ring_slot<NB>(ring, d, RESID ? 3 : 0), zold = *ring_slot<NB>(ring, d, RESID ? 4 : 0);
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2) {
+          const double n = f4get(zn, i2), z = f4get(zo, i2);
+          acc[0] += sqd(n - z);
+          acc[1] += sqd(n - (double)f4get(zp, i2));
+          acc[2] += sqd(n);
+          acc[3] += sqd((double)f4get(vn, i2));
+          if (sync) acc[4] += sqd(z - (double)f4get(zold, i2));
+          acc[5] += sqd(z);
+        }
+      }
     }
+    if (!sync) return;
     if (e + 3 < ly.n) {
       st4(ZO + e, zo);
       if (ZN) st4(VV + e, vn);
@@ -1781,33 +1860,179 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   };
   if (it.tile == 1) {
     const TileCtx tc(it, ly.L);
-    row_base(a, ly, it, rowlen, s_rb);
-    const int4 cp = col_pos4(a, ly, tc.j, tc.valid);
+    if (sync) row_base(a, ly, it, rowlen, s_rb);
+    const int4 cp = sync ? col_pos4(a, ly, tc.j, tc.valid) : make_int4(-1, -1, -1, -1);
     __syncthreads();
     ring_run(tc.count,
              [&](int d, int i) {
                const long long r = tc.row(i);
-               load(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
+               load(d, r * ly.L + 4 * tc.j, sync ? add_base(s_rb[r - it.begin], cp) : cp);
              },
              [&](int d, int i) { emit(d, tc.row(i) * ly.L + 4 * tc.j); });
-    return;
+  } else {
+    const long long nq = (it.end - it.begin + 3) >> 2;
+    const int t = threadIdx.x;
+    const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
+    ring_run(count,
+             [&](int d, int i) {
+               const long long e = it.begin + 4 * (t + (long long)i * kThreads);
+               load(d, e, sync ? dst4_linear(a, ly, rowlen, e) : make_int4(-1, -1, -1, -1));
+             },
+             [&](int d, int i) { emit(d, it.begin + 4 * (t + (long long)i * kThreads)); });
   }
-  const long long nq = (it.end - it.begin + 3) >> 2;
-  const int t = threadIdx.x;
-  const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
-  ring_run(count,
-           [&](int d, int i) {
-             const long long e = it.begin + 4 * (t + (long long)i * kThreads);
-             load(d, e, dst4_linear(a, ly, rowlen, e));
-           },
-           [&](int d, int i) { emit(d, it.begin + 4 * (t + (long long)i * kThreads)); });
+  if (RESID) block_partials<6>(acc, a.rpart + (long long)blockIdx.x * kResidSlots + 3);
 }
 
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
-  const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
-  allow_smem(k_decompact, smem);
-  launch_pdl(k_decompact, n_items, kThreads, smem, st, a);
+  if (a.rpart) {
+    const size_t smem = (size_t)kDepth * 5 * kThreads * sizeof(float4);
+    allow_smem(k_decompact<true>, smem);
+    launch_pdl(k_decompact<true>, n_items, kThreads, smem, st, a);
+  } else {
+    const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
+    allow_smem(k_decompact<false>, smem);
+    launch_pdl(k_decompact<false>, n_items, kThreads, smem, st, a);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Phase 5 (consensus.py:537-598): per-layer fold of the item partials, the
+// residual report (consensus.py:239-288) and residual balancing
+// (consensus.py:189-219) with the penalties updated in the device layer table,
+// then the dual rescale u *= u_scale, v *= v_scale of the layers that changed.
+// ---------------------------------------------------------------------------
+
+// vec[l][q] = sum over the layer's items, in item order (deterministic)
+__global__ void k_resid_fold(ResidArgs a) {
+  PDL_ENTRY();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_layers * kResidSlots) return;
+  const int l = i / kResidSlots, q = i - l * kResidSlots;
+  double x = 0.0;
+  if (q < 3 || a.leader) {
+    const int f = a.first[l], c = a.count[l];
+    for (int j = 0; j < c; ++j) x += a.rpart[(long long)(f + j) * kResidSlots + q];
+  }
+  a.vec[i] = x;
+}
+
+void launch_resid_fold(const ResidArgs& a, cudaStream_t st) {
+  const int n = a.n_layers * kResidSlots;
+  if (n <= 0) return;
+  launch_pdl(k_resid_fold, (n + 255) / 256, 256, 0, st, a);
+}
+
+// One CTA: thread per layer. With a.global: the report of every layer, the
+// totals folded in layer order by thread 0 (the reference's accumulation order),
+// then (adapt) the new penalties. Without: penalties adapted from a received report.
+__global__ void __launch_bounds__(512) k_report(ResidArgs a) {
+  PDL_ENTRY();
+  __shared__ double tot[4];
+  const int L = a.n_layers;
+  const double world = (double)a.num_nodes * a.per_node;
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    DevLayer& ly = a.layers[l];
+    double* rp = a.report + (long long)l * 8;
+    if (a.global) {
+      const double* g = a.global + (long long)l * kResidSlots;
+      const double n = (double)ly.n;
+      const double r_intra = sqrt(g[0]);
+      const double s_intra = __dmul_rn(ly.rho1, sqrt(__dmul_rn((double)a.per_node, g[4])));
+      const double r_inter = sqrt(g[3]);
+      const double s_inter = __dmul_rn(ly.rho2, sqrt(g[7]));
+      const double e_i = __dmul_rn(sqrt(__dmul_rn(n, world)), a.eps_abs);
+      const double e_o = __dmul_rn(sqrt(__dmul_rn(n, (double)a.num_nodes)), a.eps_abs);
+      rp[0] = r_intra;
+      rp[1] = s_intra;
+      rp[2] = r_inter;
+      rp[3] = s_inter;
+      rp[4] = __dadd_rn(e_i, __dmul_rn(a.eps_rel, fmax(sqrt(g[1]), sqrt(__dmul_rn((double)a.per_node, g[5])))));
+      rp[5] = __dadd_rn(e_i, __dmul_rn(__dmul_rn(a.eps_rel, ly.rho1), sqrt(g[2])));
+      rp[6] = __dadd_rn(e_o, __dmul_rn(a.eps_rel, fmax(sqrt(g[5]), sqrt(g[8]))));
+      rp[7] = __dadd_rn(e_o, __dmul_rn(__dmul_rn(a.eps_rel, ly.rho2), sqrt(g[6])));
+    }
+  }
+  __syncthreads();
+  if (a.global && threadIdx.x == 0) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = 0; l < L; ++l) {
+      const double* rp = a.report + (long long)l * 8;
+      s[0] = __dadd_rn(s[0], __dadd_rn(__dmul_rn(rp[0], rp[0]), __dmul_rn(rp[2], rp[2])));
+      s[1] = __dadd_rn(s[1], __dadd_rn(__dmul_rn(rp[1], rp[1]), __dmul_rn(rp[3], rp[3])));
+      s[2] = __dadd_rn(s[2], __dadd_rn(__dmul_rn(rp[4], rp[4]), __dmul_rn(rp[6], rp[6])));
+      s[3] = __dadd_rn(s[3], __dadd_rn(__dmul_rn(rp[5], rp[5]), __dmul_rn(rp[7], rp[7])));
+    }
+    double* t = a.report + (long long)L * 8;
+    for (int q = 0; q < 4; ++q) t[q] = tot[q] = sqrt(s[q]);
+    t[4] = (tot[0] <= tot[2] && tot[1] <= tot[3]) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    DevLayer& ly = a.layers[l];
+    const double* rp = a.report + (long long)l * 8;
+    double su = 1.0, sv = 1.0;
+    if (a.adapt) {
+      const double old = ly.rho1, old2 = ly.rho2;
+      double r1 = old, r2 = old2;
+      if (rp[0] > __dmul_rn(a.mu, rp[1]))
+        r1 = fmin(__dmul_rn(old, a.tau_inc), a.rho1_max);
+      else if (rp[1] > __dmul_rn(a.mu, rp[0]))
+        r1 = __ddiv_rn(old, a.tau_dec);
+      if (rp[2] > __dmul_rn(a.mu, rp[3]))
+        r2 = fmin(__dmul_rn(old2, a.tau_inc), a.rho2_max);
+      else if (rp[3] > __dmul_rn(a.mu, rp[2]))
+        r2 = __ddiv_rn(old2, a.tau_dec);
+      if (r1 != old) su = __ddiv_rn(old, r1);
+      if (r2 != old2) sv = __ddiv_rn(old2, r2);
+      if (r1 != old || r2 != old2) {  // consensus.py:157-159, same expression order as the host
+        ly.rho1 = r1;
+        ly.rho2 = r2;
+        const double gamma =
+            __dadd_rn(__dadd_rn(__ddiv_rn(a.wd, (double)a.num_nodes), __dmul_rn((double)a.per_node, r1)), r2);
+        ly.gamma = gamma;
+        ly.rgamma = __drcp_rn(gamma);
+      }
+    }
+    a.scales[l] = su;
+    a.scales[L + l] = sv;
+  }
+}
+
+void launch_report(const ResidArgs& a, cudaStream_t st) {
+  if (a.n_layers <= 0) return;
+  launch_pdl(k_report, 1, 512, 0, st, a);
+}
+
+// u *= scale_u[l], v *= scale_v[l] over the stream items of layers whose scale != 1
+__global__ void __launch_bounds__(kThreads) k_scale_duals(const DevLayer* __restrict__ layers,
+                                                         const Item* __restrict__ items,
+                                                         const double* __restrict__ scales, int n_layers,
+                                                         float* __restrict__ u, float* __restrict__ v) {
+  PDL_ENTRY();
+  const Item it = items[blockIdx.x];
+  const double su = scales[it.layer], sv = scales[n_layers + it.layer];
+  if (su == 1.0 && sv == 1.0) return;
+  const DevLayer& ly = layers[it.layer];
+  long long b, e;
+  if (it.tile == 1) {  // rows [begin, end) of the layer, all columns (chunk 0 only)
+    if (it.chunk != 0) return;
+    b = it.begin * ly.L;
+    e = it.end * ly.L;
+  } else {
+    b = it.begin;
+    e = it.end;
+  }
+  for (long long i = b + threadIdx.x; i < e; i += kThreads) {
+    if (su != 1.0) u[ly.off + i] = (float)((double)u[ly.off + i] * su);
+    if (sv != 1.0) v[ly.off + i] = (float)((double)v[ly.off + i] * sv);
+  }
+}
+
+void launch_scale_duals(const DevLayer* layers, const Item* items, int n_items, const double* scales,
+                        int n_layers, float* u, float* v, cudaStream_t st) {
+  if (n_items <= 0) return;
+  launch_pdl(k_scale_duals, n_items, kThreads, 0, st, layers, items, scales, n_layers, u, v);
 }
 
 // ---------------------------------------------------------------------------

@@ -158,7 +158,12 @@ struct ElemArgs {
   const int* __restrict__ pos_in;      // K_in position of each channel, -1: dropped
   const long long* __restrict__ summary;
   float divisor;
+  // phase-5 residuals (consensus.py:537-563): per-item fp64 partial sums of squares,
+  // [item][kResidSlots] (K6 / K6f: slots 0-2, K7: slots 3-8); nullptr = off
+  double* __restrict__ rpart;
+  const float* __restrict__ zn_prev;   // K7: the previous iteration's z_node
 };
+constexpr int kResidSlots = 9;         // consensus.py:235 (_INTER_SLOTS)
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st);
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
@@ -173,6 +178,25 @@ size_t structured_smem_bytes(int rows, int L, int cin);
 size_t select_smem_bytes(int G);
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
+// phase 5: per-layer fold of the residual partials, report + adaptation, dual rescale
+struct ResidArgs {
+  DevLayer* layers;                     // penalties updated in place when adapting
+  int n_layers;
+  const int* first;                     // per layer: first stream item, item count
+  const int* count;
+  const double* rpart;                  // [item][kResidSlots]
+  double* vec;                          // [layer][kResidSlots]
+  int leader;                           // 0: slots 3-8 zeroed (the leader contributes them)
+  const double* global;                 // globally summed [layer][kResidSlots], or nullptr: adapt from report
+  double* report;                       // [layer][8] + 5 (consensus.py:291-300 layout)
+  double* scales;                       // [2][layer]: u scale, v scale
+  double wd, eps_abs, eps_rel, mu, tau_inc, tau_dec, rho1_max, rho2_max;
+  int num_nodes, per_node, adapt;
+};
+void launch_resid_fold(const ResidArgs& a, cudaStream_t st);
+void launch_report(const ResidArgs& a, cudaStream_t st);
+void launch_scale_duals(const DevLayer* layers, const Item* items, int n_items, const double* scales,
+                        int n_layers, float* u, float* v, cudaStream_t st);
 void launch_slices(const PeerPtrs& src, const long long* total_p, long long total_h, long long max_elems,
                    int part, double div, float* out, cudaStream_t st);
 struct BarrierArgs {

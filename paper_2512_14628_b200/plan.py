@@ -351,6 +351,40 @@ class Plan:
                       ptr(z), current_stream())
 
 
+    # -- phase 5 (consensus.py:537-598) ----------------------------------------------
+    def compact_dual_resid(self, theta, u, z_node, v, flat):
+        """K6 (flat given) or K6f (flat None) + per-item residual slots 0-2."""
+        with timed("K6_compact_dual_resid" if flat is not None else "K6f_dual_intra_resid"):
+            _lib.call("hsx_compact_dual_resid", self._h, ptr(theta), ptr(u), ptr(z_node), ptr(v), ptr(flat),
+                      current_stream())
+
+    def decompact_dual_resid(self, flat, divisor, z_node, z_node_prev, v, z):
+        """K7 (flat given) or the non-sync residual pass (flat None) + slots 3-8."""
+        with timed("K7_decompact_dual_resid" if flat is not None else "K7r_residuals"):
+            _lib.call("hsx_decompact_dual_resid", self._h, ptr(flat), float(divisor), ptr(z_node),
+                      ptr(z_node_prev), ptr(v), ptr(z), current_stream())
+
+    def residual_fold(self, leader: bool, vec):
+        with timed("K9_residual_fold"):
+            _lib.call("hsx_residual_fold", self._h, 1 if leader else 0, ptr(vec), current_stream())
+
+    def residual_report(self, global_sums, report, scales, params):
+        with timed("K9_report"):
+            _lib.call("hsx_residual_report", self._h, ptr(global_sums), ptr(report), ptr(scales),
+                      C.byref(params), current_stream())
+
+    def scale_duals(self, scales, u, v):
+        with timed("K9_scale_duals"):
+            _lib.call("hsx_scale_duals", self._h, ptr(scales), ptr(u), ptr(v), current_stream())
+
+    def read_penalties(self):
+        """(rho1, rho2) per layer as currently in the device layer table (synchronous)."""
+        n = len(self.names)
+        r1, r2 = (C.c_double * n)(), (C.c_double * n)()
+        _lib.call("hsx_plan_read_penalties", self._h, C.cast(r1, C.c_void_p), C.cast(r2, C.c_void_p))
+        return list(r1), list(r2)
+
+
 def mask_or_ptrs(srcs: list[int], words: int, out):
     """out = OR of the masks at device pointers ``srcs`` (one source = a copy)."""
     arr, keep = _lib.ptr_array(srcs)

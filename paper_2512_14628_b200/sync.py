@@ -56,7 +56,7 @@ class HSADMMSync:
 
     def __init__(self, rank: int, cluster, layers: list[LayerSpec], constraints: dict,
                  schedule: PenaltySchedule, settings: ConsensusSettings, device=None,
-                 transport: str = "auto"):
+                 transport: str = "auto", residuals: bool = True):
         topo = cluster.topology
         self.rank = rank
         self.cluster = cluster
@@ -82,6 +82,19 @@ class HSADMMSync:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         pl, dev = self.plan, self.device
         self.theta, self.u, self.z_node, self.v, self.z = (pl.empty_arena(dev) for _ in range(5))
+        # phase 5 (consensus.py:537-598): residual sums fused into K6 / K7, the report
+        # and the adaptive penalties on the device; z_node is double-buffered so K7
+        # sees the previous iteration's z_node
+        self.residuals = bool(residuals)
+        self.z_node_prev = pl.empty_arena(dev) if self.residuals else None
+        nl = len(self.layers)
+        self.rvec = torch.zeros(max(nl * _lib.RESID_SLOTS, 1), dtype=torch.float64, device=dev)
+        self.report = torch.zeros(nl * 8 + 5, dtype=torch.float64, device=dev)
+        self.scales = torch.ones(max(2 * nl, 1), dtype=torch.float64, device=dev)
+        self._resid_params = _lib.ResidParams(
+            settings.weight_decay, settings.eps_abs, settings.eps_rel, schedule.mu, schedule.tau_inc,
+            schedule.tau_dec, schedule.rho1_max, schedule.rho2_max, self.M, self.P, 1 if schedule.adapt else 0)
+        self.reported = False
         self.sum = pl.empty_arena(dev) if self.P > 1 else None
         self.flat = torch.zeros(max(pl.arena, 1), dtype=torch.float32, device=dev)
         self.masks = pl.empty_mask(dev, ones=True)
@@ -197,9 +210,15 @@ class HSADMMSync:
         return 4 * self.payload_elements
 
     # -- the per-iteration program ------------------------------------------------------
+    def _begin_step(self):
+        """z_node_prev <- the last iteration's z_node (K1 writes the other buffer)."""
+        if self.residuals:
+            self.z_node, self.z_node_prev = self.z_node_prev, self.z_node
+
     def program(self, k: int):
-        """Generator: yields collective requests, performs phases 2-5(u) of iteration k."""
+        """Generator: yields collective requests, performs phases 2-5 of iteration k."""
         self.settle()
+        self._begin_step()
         if self.transport == "peer":
             return (yield from self._program_peer(k))
         return (yield from self._program_nccl(k))
@@ -257,8 +276,8 @@ class HSADMMSync:
             local = self.p_lmask.tensor if self.p_lmask is not None else self.local_mask
             pl.project_all(s_local, self.theta, self.u, self.z, self.v, self.z_node, local, peers=peers)
         if k % self.settings.sync_period != 0:
-            pl.dual_intra(self.theta, self.u, self.z_node)
-            return None
+            self._dual(None)
+            return (yield from self._residual_phase(k, sync=False))
         ev = None
         if fused_keep:
             ev = pl.keep_sets_fetch_async()
@@ -282,13 +301,13 @@ class HSADMMSync:
             # one node: the leader "average" is the identity and every rank holds the
             # same z_node and v, so each rank compacts and decompacts locally (the
             # result is bitwise what the intra broadcast would deliver)
-            pl.compact_dual(self.theta, self.u, self.z_node, self.v, self.flat)
-            pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
+            self._dual(self.flat)
+            self._decompact(self.flat)
             return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
         if self.is_leader:
             if self.M > 1:
                 flat = self.p_flat[k & 1]
-                pl.compact_dual(self.theta, self.u, self.z_node, self.v, flat.tensor)
+                self._dual(flat.tensor)
                 yield Barrier(self.inter, "z_sync", k)
                 # leader average over NVLink into the node's payload buffer
                 dst = zhat if zhat is not None else self.flat
@@ -301,19 +320,79 @@ class HSADMMSync:
                     pl.average_peers(flat.peer_ptrs(), float(self.M), dst, tag="K8_leader_avg")
             else:
                 dst = zhat if zhat is not None else self.flat
-                pl.compact_dual(self.theta, self.u, self.z_node, self.v, dst)
+                self._dual(dst)
         else:
-            pl.dual_intra(self.theta, self.u, self.z_node)
+            self._dual(None)
         if self.P > 1:
             yield Barrier(self.intra, "zhat_bcast", k)
             if not self.is_leader:  # the intra broadcast: a contiguous read of the leader's payload
                 pl.average_peers([self.p_zhat.peer_ptrs()[0]], 1.0, self.flat, tag="K8_zhat_read")
                 dst = self.flat
-        pl.decompact_dual(dst, 1.0, self.z_node, self.v, self.z)
+        self._decompact(dst)
         return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
 
+    # -- K6 / K7 with or without the fused residual sums -------------------------------
+    def _dual(self, flat):
+        """K6 (flat given: compaction + intra dual) or K6f (intra dual alone)."""
+        pl = self.plan
+        if self.residuals:
+            pl.compact_dual_resid(self.theta, self.u, self.z_node, self.v, flat)
+        elif flat is not None:
+            pl.compact_dual(self.theta, self.u, self.z_node, self.v, flat)
+        else:
+            pl.dual_intra(self.theta, self.u, self.z_node)
+
+    def _decompact(self, flat):
+        if self.residuals:
+            self.plan.decompact_dual_resid(flat, 1.0, self.z_node, self.z_node_prev, self.v, self.z)
+        else:
+            self.plan.decompact_dual(flat, 1.0, self.z_node, self.v, self.z)
+
+    def _residual_phase(self, k: int, sync: bool):
+        """Phase 5 after the u-update (consensus.py:537-598): per-layer squared norms
+        (accumulated in K6 / K7), intra SUM, leaders' inter SUM, the report on the
+        leader, broadcast to the followers, adaptive penalties + dual rescale."""
+        if not self.residuals:
+            return None
+        pl = self.plan
+        if not sync and self.is_leader:   # z, v unchanged: the leader's slots 3-8 (dz = 0)
+            pl.decompact_dual_resid(None, 1.0, self.z_node, self.z_node_prev, self.v, self.z)
+        pl.residual_fold(self.is_leader, self.rvec)
+        if self.P > 1:
+            yield AllReduce(self.intra, self.rvec, ReduceOp.SUM, "res_intra", k)
+        if self.is_leader:
+            if self.M > 1:
+                yield AllReduce(self.inter, self.rvec, ReduceOp.SUM, "res_inter", k)
+            pl.residual_report(self.rvec, self.report, self.scales, self._resid_params)
+        if self.P > 1:
+            yield Broadcast(self.intra, self.leader_rank, self.report, "report", k)
+            if not self.is_leader:
+                pl.residual_report(None, self.report, self.scales, self._resid_params)
+        if self._resid_params.adapt:
+            pl.scale_duals(self.scales, self.u, self.v)
+        self.reported = True
+        return None
+
+    def last_report(self):
+        """The last iteration's ResidualReport (consensus.py:84-91); synchronizes."""
+        from .consensus import unpack_report
+
+        if not self.reported:
+            raise ProtocolError("no residual report yet (residuals off or no step run)")
+        torch.cuda.current_stream(self.device).synchronize()
+        return unpack_report(self.report.cpu().numpy(), self.names)
+
+    def current_schedule(self) -> PenaltySchedule:
+        """The penalty schedule after device-side adaptation (synchronizes)."""
+        import dataclasses
+
+        torch.cuda.current_stream(self.device).synchronize()
+        r1, r2 = self.plan.read_penalties()
+        return dataclasses.replace(self.schedule, rho1=dict(zip(self.names, r1)), rho2=dict(zip(self.names, r2)))
+
     def _end_step(self, k: int, dynamic: bool, ev, log_zsync: bool):
-        """masks <- union; host bookkeeping now, or at the next step (defer_host)."""
+        """Phase 5; masks <- union; host bookkeeping now, or at the next step (defer_host)."""
+        yield from self._residual_phase(k, sync=True)
         self.plan.join_fetch()
         if dynamic:
             self.masks, self.union = self.union, self.masks
@@ -325,7 +404,6 @@ class HSADMMSync:
                 self._after_keep_sets()
             self._host_tail(k, dynamic, log_zsync)
         return None
-        yield  # pragma: no cover  (generator)
 
     def _host_tail(self, k: int, dynamic: bool, log_zsync: bool):
         """Ledger of the leader average; freeze + seal (consensus.py:600-606)."""
@@ -368,8 +446,8 @@ class HSADMMSync:
         elif dynamic:
             pl.project_all(s, self.theta, self.u, self.z, self.v, self.z_node, self.local_mask)
         if k % self.settings.sync_period != 0:
-            pl.dual_intra(self.theta, self.u, self.z_node)
-            return None
+            self._dual(None)
+            return (yield from self._residual_phase(k, sync=False))
         # phase 4: mask union (leaders), broadcast to followers, keep sets
         ev = None
         if fused_keep:
@@ -386,10 +464,7 @@ class HSADMMSync:
             self.cache_hits += len(self.prunable)
         # compaction fused with the intra dual update (K6 reads sizes on device, so
         # it runs while the host waits for the D2H and sizes the collectives)
-        if self.is_leader:
-            pl.compact_dual(self.theta, self.u, self.z_node, self.v, self.flat)
-        else:
-            pl.dual_intra(self.theta, self.u, self.z_node)
+        self._dual(self.flat if self.is_leader else None)
         collectives = self.M > 1 or self.P > 1
         if ev is not None and collectives:      # the leader all-reduce / broadcast need the sizes
             ev.synchronize()
@@ -400,7 +475,7 @@ class HSADMMSync:
             yield from self._leader_average(k)
         if self.P > 1 and total > 0:
             yield Broadcast(self.intra, self.leader_rank, self.flat[:total], "zhat_bcast", k)
-        pl.decompact_dual(self.flat, 1.0, self.z_node, self.v, self.z)
+        self._decompact(self.flat)
         # one rank (no collectives): K6 / K7 are queued, the counts land meanwhile; the
         # leader average is the identity (ledger entries only)
         return (yield from self._end_step(k, dynamic, ev, log_zsync=not collectives))
@@ -496,7 +571,7 @@ class HSADMMSync:
         self.settle()
         sync = k % self.settings.sync_period == 0
         dynamic = not self.frozen and bool(self.prunable)
-        key = (dynamic, sync, self.masks.data_ptr(), self.theta.data_ptr())
+        key = (dynamic, sync, self.masks.data_ptr(), self.theta.data_ptr(), self.z_node.data_ptr())
         graphs = self.__dict__.setdefault("_graphs", {})
         g = graphs.get(key)
         if g is None:
@@ -529,6 +604,9 @@ class HSADMMSync:
 
     def _graph_effects(self, k: int, dynamic: bool, sync: bool):
         """Host side of program(k) for a replayed graph (one rank, deferred mode)."""
+        self._begin_step()
+        if self.residuals:
+            self.reported = True
         if not sync:
             return
         if not dynamic:

@@ -1,0 +1,159 @@
+"""GPU parity of phase 5 — residual sums fused into K6 / K7, the residual report
+and the adaptive penalties with the u / v rescale (consensus.py:537-598,
+189-219, 239-288) — against run_hierarchical(adapt=True) goldens and the oracle.
+
+Bars: penalty decisions (rho per layer, every iteration) exact; report entries
+within RTOL relative (they are fp64 norms of the fp32 state, which itself is
+within 1e-5 of the reference's fp64 state); state tensors
+within 1e-5 (H6 measure).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hsadmm_oracle as O
+from tests import golden_io as G
+from tests.test_gpu_parity import TOL, cpu, rel_err
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2512_14628_b200 import _lib
+
+    _lib.load()
+    torch.cuda.set_device(0)
+
+
+def _engines(M, P, transport, sync_period=1, adapt=True, golden=True):
+    import paper_2512_14628_b200 as H
+
+    ref = G.E2E(M, P, adapt=True) if golden else None
+    kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
+             "shape": H.ConstraintKind.SHAPE_KEEP}
+    layers = [H.LayerSpec(n, H.LayerKind.CONV if k == "conv" else H.LayerKind.FULLY_CONNECTED, shape,
+                          prunable=bool(c)) for n, k, shape, c in G.E2E_LAYERS]
+    cons = {n: [H.SparsityConstraint(kinds[g], keep_rate=r) for g, r in c] for n, _, _, c in G.E2E_LAYERS if c}
+    names = [n for n, *_ in G.E2E_LAYERS]
+    sched = H.PenaltySchedule.uniform(names, G.E2E_RHO1, G.E2E_RHO2, adapt=adapt)
+    settings = H.ConsensusSettings(iterations=5, t_freeze=4, weight_decay=G.E2E_WD, sync_period=sync_period)
+    cluster = H.LocalCluster(H.Topology(M, P))
+    engines = [H.HSADMMSync(r, cluster, layers, cons, sched, settings, transport=transport, residuals=True)
+               for r in range(M * P)]
+    return ref, cluster, engines
+
+
+def _report_vec(rep, names):
+    v = [x for n in names for x in (lambda r: (r.r_intra, r.s_intra, r.r_inter, r.s_inter, r.eps_pri_intra,
+                                               r.eps_dual_intra, r.eps_pri_inter, r.eps_dual_inter))(rep.layers[n])]
+    return np.array(v + [rep.r_pri, rep.r_dual, rep.eps_pri, rep.eps_dual, float(rep.converged)])
+
+
+def _check_report(got, want, ctx):
+    assert got[-1] == want[-1], ctx                       # converged flag
+    err = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+    assert float(err.max()) <= RTOL, (ctx, float(err.max()), int(err.argmax()))
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+@pytest.mark.parametrize("M,P", G.E2E_ADAPT_TOPOLOGIES)
+def test_adaptive_end_to_end_against_reference_goldens(M, P, transport):
+    import paper_2512_14628_b200 as H
+
+    ref, cluster, engines = _engines(M, P, transport)
+    for e in engines:
+        e.init_from(ref.p0())
+    for k in range(1, ref.iters + 1):
+        r1, r2 = ref.rho(k)
+        for e in engines:      # the penalties iteration k runs with: exact
+            s = e.current_schedule()
+            assert [s.rho1[n] for n in ref.names] == list(r1), (k, e.rank)
+            assert [s.rho2[n] for n in ref.names] == list(r2), (k, e.rank)
+            e.load(theta=ref.theta(k, e.rank))
+        H.run_local(engines, k)
+        for e in engines:
+            _check_report(_report_vec(e.last_report(), ref.names), ref.report(k), (k, e.rank))
+            node = e.rank // P
+            th = ref.theta(k, e.rank)
+            for n in ref.names:
+                for key, want in (("z_node", ref.node_state("z_node", k, node)[n]),
+                                  ("v", ref.node_state("v", k, node)[n]),
+                                  ("z", ref.node_state("z", k, node)[n]),
+                                  ("u", ref.u(k, e.rank)[n])):
+                    err = rel_err(cpu(e.views(key)[n]), want, th[n])
+                    assert err <= TOL, (k, e.rank, key, n, err)
+            for n, m in ref.masks(k, node).items():
+                assert np.array_equal(cpu(e.mask_dict()[n]), m), (k, e.rank, n)
+    final = ref.rho_final()
+    for e in engines:
+        s = e.current_schedule()
+        assert [s.rho1[n] for n in ref.names] == list(final[0])
+        assert [s.rho2[n] for n in ref.names] == list(final[1])
+
+
+@pytest.mark.parametrize("M,P", [(1, 1), (2, 2)])
+def test_non_sync_iterations_against_oracle(M, P):
+    """sync_period = 2: odd iterations run phase 5 without a sync (z, v unchanged,
+    dz = 0, consensus.py:557); checked against the oracle on the same inputs."""
+    import paper_2512_14628_b200 as H
+
+    ref = G.E2E(M, P, adapt=True)
+    _, cluster, engines = _engines(M, P, "nccl", sync_period=2, golden=False)
+    specs = [(n, shape) for n, _, shape, _ in G.E2E_LAYERS]
+    ocons = {n: [(g, None, r) for g, r in c] for n, _, _, c in G.E2E_LAYERS if c}
+    olayers = O.make_layers(specs, ocons)
+    p0 = ref.p0()
+    zeros = {n: np.zeros_like(a) for n, a in p0.items()}
+    states = [O.init_rank_state(olayers, p0, zeros, p0, zeros, p0) for _ in range(M * P)]
+    sched = O.Schedule({n: G.E2E_RHO1 for n in ref.names}, {n: G.E2E_RHO2 for n in ref.names})
+    for e in engines:
+        e.init_from(p0)
+    for k in range(1, ref.iters + 1):
+        thetas = [ref.theta(k, r) for r in range(M * P)]
+        for e in engines:
+            e.load(theta=thetas[e.rank])
+        H.run_local(engines, k)
+        rep, _ = O.cluster_sync(olayers, states, thetas, k, M, P, sched.rho1, sched.rho2, G.E2E_WD,
+                                t_freeze=4, sync_period=2, residuals=True, sched=sched)
+        want = np.array([x for n in ref.names for x in rep["layers"][n]] +
+                        [rep["r_pri"], rep["r_dual"], rep["eps_pri"], rep["eps_dual"], float(rep["converged"])])
+        for e in engines:
+            _check_report(_report_vec(e.last_report(), ref.names), want, (k, e.rank))
+            s = e.current_schedule()
+            assert [s.rho1[n] for n in ref.names] == [sched.rho1[n] for n in ref.names], (k, e.rank)
+            assert [s.rho2[n] for n in ref.names] == [sched.rho2[n] for n in ref.names], (k, e.rank)
+            st = states[e.rank]
+            for n in ref.names:
+                for key in ("z_node", "v", "z", "u"):
+                    err = rel_err(cpu(e.views(key)[n]), getattr(st, key)[n], thetas[e.rank][n])
+                    assert err <= TOL, (k, e.rank, key, n, err)
+
+
+def test_residuals_off_leaves_the_step_unchanged():
+    """residuals=False runs the plain K6 / K7 (no phase 5): same state as with
+    residuals on and adapt off."""
+    import paper_2512_14628_b200 as H
+
+    ref = G.E2E(2, 2, adapt=True)
+    outs = []
+    for residuals in (False, True):
+        _, cluster, engines = _engines(2, 2, "nccl", adapt=False, golden=False)
+        for e in engines:
+            e.residuals = residuals
+            if not residuals:
+                e.z_node_prev = None
+            e.init_from(ref.p0())
+        for k in range(1, 4):
+            for e in engines:
+                e.load(theta=ref.theta(k, e.rank))
+            H.run_local(engines, k)
+        outs.append([{key: getattr(e, key).clone() for key in ("u", "v", "z")} for e in engines])
+    for a, b in zip(*outs):
+        for key in a:
+            assert torch.equal(a[key], b[key]), key

@@ -373,6 +373,16 @@ def run_ours(args):
     k += args.steps
     frozen_ms = max_over_ranks(sum(ftimes)) / args.steps
     eng.frozen = False
+    # the full Algorithm-1 iteration: the dynamic step + phase 5 (residual sums fused
+    # into K6/K7, report, adaptive penalties, dual rescale), as the reference runs it
+    eng.set_residuals(True, adapt=True)
+    for _ in range(2):
+        k += 1
+        run_step(k)
+    rtimes = timed_steps(k + 1, args.steps)
+    k += args.steps
+    resid_ms = max_over_ranks(sum(rtimes)) / args.steps
+    eng.set_residuals(False)
     eng.settle()
     eng.defer_host = False
     # e2e through the public API with host buffers: HSADMMSync.step_host copies every
@@ -437,6 +447,7 @@ def run_ours(args):
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks.summary(),
         "frozen_ms_per_step": frozen_ms,
+        "phase5_ms_per_step": resid_ms,
         "leader_bytes": {"z_sync_bytes": 4 * Z, "dense_bytes": 4 * N, "ratio_vs_dense": Z / N},
         "kernels": kernels_out,
     }

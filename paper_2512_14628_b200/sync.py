@@ -373,6 +373,15 @@ class HSADMMSync:
         self.reported = True
         return None
 
+    def set_residuals(self, on: bool, adapt: bool | None = None) -> None:
+        """Turn phase 5 on / off between steps (adapt: override the schedule's flag)."""
+        self.settle()
+        self.residuals = bool(on)
+        if self.residuals and self.z_node_prev is None:
+            self.z_node_prev = self.plan.empty_arena(self.device)
+        if adapt is not None:
+            self._resid_params.adapt = 1 if adapt else 0
+
     def last_report(self):
         """The last iteration's ResidualReport (consensus.py:84-91); synchronizes."""
         from .consensus import unpack_report
@@ -571,7 +580,8 @@ class HSADMMSync:
         self.settle()
         sync = k % self.settings.sync_period == 0
         dynamic = not self.frozen and bool(self.prunable)
-        key = (dynamic, sync, self.masks.data_ptr(), self.theta.data_ptr(), self.z_node.data_ptr())
+        key = (dynamic, sync, self.masks.data_ptr(), self.theta.data_ptr(), self.z_node.data_ptr(),
+               self.residuals, self._resid_params.adapt)
         graphs = self.__dict__.setdefault("_graphs", {})
         g = graphs.get(key)
         if g is None:

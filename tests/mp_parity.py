@@ -72,6 +72,43 @@ def golden_check(topo, rank, transport):
     return worst
 
 
+def adaptive_check(topo, rank, transport):
+    """Phase 5 over the real collectives: run_hierarchical(adapt=True) goldens —
+    penalties exact every iteration, report within 1e-5, state within 1e-5."""
+    ref = G.E2E(topo.num_nodes, topo.accels_per_node, adapt=True)
+    kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
+             "shape": H.ConstraintKind.SHAPE_KEEP}
+    layers = [H.LayerSpec(n, H.LayerKind.CONV if k == "conv" else H.LayerKind.FULLY_CONNECTED, s,
+                          prunable=bool(c)) for n, k, s, c in G.E2E_LAYERS]
+    cons = {n: [H.SparsityConstraint(kinds[g], keep_rate=r) for g, r in c] for n, _, _, c in G.E2E_LAYERS if c}
+    sched = H.PenaltySchedule.uniform(ref.names, G.E2E_RHO1, G.E2E_RHO2, adapt=True)
+    settings = H.ConsensusSettings(t_freeze=ref.t_freeze, weight_decay=G.E2E_WD)
+    eng = H.HSADMMSync(rank, H.DistCluster(topo), layers, cons, sched, settings, transport=transport)
+    eng.init_from(ref.p0())
+    node = topo.node_of(rank)
+    for k in range(1, ref.iters + 1):
+        r1, r2 = ref.rho(k)
+        s = eng.current_schedule()
+        assert [s.rho1[n] for n in ref.names] == list(r1) and [s.rho2[n] for n in ref.names] == list(r2), k
+        th = ref.theta(k, rank)
+        eng.load(theta=th)
+        eng.step(k)
+        rep = eng.last_report()
+        got = np.array([x for n in ref.names for x in (
+            rep.layers[n].r_intra, rep.layers[n].s_intra, rep.layers[n].r_inter, rep.layers[n].s_inter,
+            rep.layers[n].eps_pri_intra, rep.layers[n].eps_dual_intra, rep.layers[n].eps_pri_inter,
+            rep.layers[n].eps_dual_inter)] + [rep.r_pri, rep.r_dual, rep.eps_pri, rep.eps_dual, float(rep.converged)])
+        want = ref.report(k)
+        assert got[-1] == want[-1], (k, rank)
+        assert float((np.abs(got - want) / np.maximum(np.abs(want), 1e-30)).max()) <= TOL, (k, rank)
+        for key, w in (("z_node", ref.node_state("z_node", k, node)), ("v", ref.node_state("v", k, node)),
+                       ("z", ref.node_state("z", k, node)), ("u", ref.u(k, rank))):
+            for n, t in eng.views(key).items():
+                err = rel_err(t.cpu().numpy(), w[n], th[n])
+                assert err <= TOL, (k, rank, key, n, err)
+    return True
+
+
 def replica_check(topo, rank, world, transport):
     from paper_2512_14628_b200.synthetic import channel_keep_constraints, model_layers, synthetic_rank_state
 
@@ -110,6 +147,9 @@ def main():
         for transport in os.environ.get("MP_PARITY_TRANSPORTS", "nccl,peer").split(","):
             worst = golden_check(topo, rank, transport)
             print(f"rank {rank} golden {transport} done", file=sys.stderr, flush=True)
+            if (topo.num_nodes, topo.accels_per_node) in G.E2E_ADAPT_TOPOLOGIES:
+                adaptive_check(topo, rank, transport)
+                print(f"rank {rank} adaptive {transport} done", file=sys.stderr, flush=True)
             ratio = replica_check(topo, rank, world, transport)
             dist.barrier()
             if rank == 0:

@@ -950,7 +950,8 @@ int hsx_residual_report(hsx_plan* p, const double* global, double* report, doubl
 
 int hsx_scale_duals(const hsx_plan* p, const double* scales, float* u, float* v, void* stream) {
   if (!p || !scales || !u || !v) return fail(HSX_EINVAL, "null argument");
-  hsx::launch_scale_duals(p->d_layers, p->d_stream, (int)p->stream_items.size(), scales, p->n_layers, u, v,
+  // contiguous 8192-element items of every layer (balanced; unscaled layers exit at once)
+  hsx::launch_scale_duals(p->d_layers, p->d_elem, (int)p->elem_items.size(), scales, p->n_layers, u, v,
                           S(stream));
   HSX_LAUNCHED("scale_duals");
   return HSX_OK;

@@ -134,28 +134,28 @@ __device__ __forceinline__ void cp_quad(float4* dst, const float* src, long long
 // Drive `count` iterations of (issue(slot, i), consume(slot, i)) through the ring:
 // ring_prologue puts the first kDepth-1 quads in flight (a kernel can do other
 // setup before ring_loop), ring_run does both.
-template <class Issue>
+template <int D = kDepth, class Issue>
 __device__ __forceinline__ void ring_prologue(int count, Issue issue) {
 #pragma unroll
-  for (int d = 0; d < kDepth - 1; ++d) {
+  for (int d = 0; d < D - 1; ++d) {
     if (d < count) issue(d, d);
     cp_commit();
   }
 }
-template <class Issue, class Consume>
+template <int D = kDepth, class Issue, class Consume>
 __device__ __forceinline__ void ring_loop(int count, Issue issue, Consume consume) {
   for (int i = 0; i < count; ++i) {
-    const int ahead = i + kDepth - 1;
-    if (ahead < count) issue(ahead % kDepth, ahead);
+    const int ahead = i + D - 1;
+    if (ahead < count) issue(ahead % D, ahead);
     cp_commit();
-    cp_wait<kDepth - 1>();
-    consume(i % kDepth, i);
+    cp_wait<D - 1>();
+    consume(i % D, i);
   }
 }
-template <class Issue, class Consume>
+template <int D = kDepth, class Issue, class Consume>
 __device__ __forceinline__ void ring_run(int count, Issue issue, Consume consume) {
-  ring_prologue(count, issue);
-  ring_loop(count, issue, consume);
+  ring_prologue<D>(count, issue);
+  ring_loop<D>(count, issue, consume);
 }
 
 // ---------------------------------------------------------------------------
@@ -1788,6 +1788,7 @@ template <bool RESID>
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   PDL_ENTRY();
   constexpr int NB = RESID ? 5 : 3;
+  constexpr int D = RESID ? 3 : kDepth;  // 5 streams x 3 stages: 60 KB, three CTAs per SM
   extern __shared__ float4 ring[];
   __shared__ int s_rb[kMaxTileRows];
   const Item it = a.items[blockIdx.x];
@@ -1863,7 +1864,7 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
     if (sync) row_base(a, ly, it, rowlen, s_rb);
     const int4 cp = sync ? col_pos4(a, ly, tc.j, tc.valid) : make_int4(-1, -1, -1, -1);
     __syncthreads();
-    ring_run(tc.count,
+    ring_run<D>(tc.count,
              [&](int d, int i) {
                const long long r = tc.row(i);
                load(d, r * ly.L + 4 * tc.j, sync ? add_base(s_rb[r - it.begin], cp) : cp);
@@ -1873,7 +1874,7 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
     const long long nq = (it.end - it.begin + 3) >> 2;
     const int t = threadIdx.x;
     const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
-    ring_run(count,
+    ring_run<D>(count,
              [&](int d, int i) {
                const long long e = it.begin + 4 * (t + (long long)i * kThreads);
                load(d, e, sync ? dst4_linear(a, ly, rowlen, e) : make_int4(-1, -1, -1, -1));
@@ -1886,7 +1887,7 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
   if (a.rpart) {
-    const size_t smem = (size_t)kDepth * 5 * kThreads * sizeof(float4);
+    const size_t smem = (size_t)3 * 5 * kThreads * sizeof(float4);
     allow_smem(k_decompact<true>, smem);
     launch_pdl(k_decompact<true>, n_items, kThreads, smem, st, a);
   } else {
@@ -1903,24 +1904,31 @@ void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
 // then the dual rescale u *= u_scale, v *= v_scale of the layers that changed.
 // ---------------------------------------------------------------------------
 
-// vec[l][q] = sum over the layer's items, in item order (deterministic)
-__global__ void k_resid_fold(ResidArgs a) {
+// vec[l][q]: one CTA per layer, warp q folds slot q — lane i sums items i, i+32, ...
+// in order (loads batched), then a fixed xor-shuffle tree: deterministic
+__global__ void __launch_bounds__(32 * kResidSlots) k_resid_fold(ResidArgs a) {
   PDL_ENTRY();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n_layers * kResidSlots) return;
-  const int l = i / kResidSlots, q = i - l * kResidSlots;
+  const int l = blockIdx.x, q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double x = 0.0;
   if (q < 3 || a.leader) {
     const int f = a.first[l], c = a.count[l];
-    for (int j = 0; j < c; ++j) x += a.rpart[(long long)(f + j) * kResidSlots + q];
+    const double* __restrict__ src = a.rpart + (long long)f * kResidSlots + q;
+    for (int j0 = lane; j0 < c; j0 += 32 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = j0 + 32 * u < c ? src[(long long)(j0 + 32 * u) * kResidSlots] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x += v[u];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
   }
-  a.vec[i] = x;
+  if (lane == 0) a.vec[(long long)l * kResidSlots + q] = x;
 }
 
 void launch_resid_fold(const ResidArgs& a, cudaStream_t st) {
-  const int n = a.n_layers * kResidSlots;
-  if (n <= 0) return;
-  launch_pdl(k_resid_fold, (n + 255) / 256, 256, 0, st, a);
+  if (a.n_layers <= 0) return;
+  launch_pdl(k_resid_fold, a.n_layers, 32 * kResidSlots, 0, st, a);
 }
 
 // One CTA: thread per layer. With a.global: the report of every layer, the
@@ -2014,16 +2022,35 @@ __global__ void __launch_bounds__(kThreads) k_scale_duals(const DevLayer* __rest
   const double su = scales[it.layer], sv = scales[n_layers + it.layer];
   if (su == 1.0 && sv == 1.0) return;
   const DevLayer& ly = layers[it.layer];
-  long long b, e;
-  if (it.tile == 1) {  // rows [begin, end) of the layer, all columns (chunk 0 only)
-    if (it.chunk != 0) return;
-    b = it.begin * ly.L;
-    e = it.end * ly.L;
-  } else {
-    b = it.begin;
-    e = it.end;
+  const long long b = it.begin, e = it.end;  // contiguous element items (8192, quad-aligned)
+  const long long nq = (e - b) >> 2;
+  constexpr int U = 8;
+  float4* __restrict__ u4 = reinterpret_cast<float4*>(u + ly.off + b);
+  float4* __restrict__ v4 = reinterpret_cast<float4*>(v + ly.off + b);
+  auto sc = [](float4 x, double s) {
+    return make_float4((float)((double)x.x * s), (float)((double)x.y * s), (float)((double)x.z * s),
+                       (float)((double)x.w * s));
+  };
+  for (long long q0 = threadIdx.x; q0 < nq; q0 += (long long)U * kThreads) {
+    float4 xu[U], xv[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const long long q = q0 + (long long)j * kThreads;
+      if (q < nq) {
+        if (su != 1.0) xu[j] = u4[q];
+        if (sv != 1.0) xv[j] = v4[q];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const long long q = q0 + (long long)j * kThreads;
+      if (q < nq) {
+        if (su != 1.0) u4[q] = sc(xu[j], su);
+        if (sv != 1.0) v4[q] = sc(xv[j], sv);
+      }
+    }
   }
-  for (long long i = b + threadIdx.x; i < e; i += kThreads) {
+  for (long long i = b + 4 * nq + threadIdx.x; i < e; i += kThreads) {
     if (su != 1.0) u[ly.off + i] = (float)((double)u[ly.off + i] * su);
     if (sv != 1.0) v[ly.off + i] = (float)((double)v[ly.off + i] * sv);
   }

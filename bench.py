@@ -253,6 +253,8 @@ def algorithmic_bytes(kernel, N, n_c, Z, P):
         "K0_pack_theta_u": 12 * N,
         "K1_candidate": (16 if P > 1 else 20) * N,     # read S,z,v (or theta,u,z,v), write z_node
         "K3_project": 8 * n_c + n_c // 8,
+        "K3_project_keep": 8 * n_c + n_c // 8,
+        "K2K3_select_project_keep": 8 * n_c + n_c // 8,
         "K6_compact_dual": 20 * N + 4 * Z,
         "K6f_dual_intra": 16 * N,
         "K7_decompact_dual": 16 * N + 4 * Z,

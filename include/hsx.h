@@ -157,6 +157,13 @@ int hsx_project(hsx_plan* plan, float* z_node, uint32_t* local_mask, void* strea
  * against the previous rectangle). */
 int hsx_project_keep_sets(hsx_plan* plan, float* z_node, uint32_t* mask, const uint32_t* prev_mask,
                           void* stream);
+/* K2 + K3 (+ fixup) of a one-node plan in one launch when every prunable layer
+ * has a single constraint: the selection CTAs publish per-layer ready flags and
+ * the projection items of a layer start as soon as its selection is done (falls
+ * back to hsx_select + hsx_project_keep_sets otherwise). Replaces the last
+ * hsx_select + hsx_project_keep_sets of a dynamic step. */
+int hsx_select_project_keep_sets(hsx_plan* plan, float* z_node, uint32_t* mask,
+                                 const uint32_t* prev_mask, void* stream);
 /* Single-node mode on / off (default off): see hsx_project_keep_sets. */
 int hsx_plan_set_single_node(hsx_plan* plan, int32_t on);
 
@@ -180,6 +187,10 @@ int hsx_keep_sets_fetch(hsx_plan* plan, int64_t* host_summary, void* stream);
  * kernel run while the host sizes the leader all-reduce). Does not refresh
  * the plan's host mirror used by hsx_set_keep_sets. */
 int hsx_keep_sets_fetch_async(hsx_plan* plan, int64_t* host_summary, void* stream);
+/* Host wait for the last hsx_keep_sets_fetch_async copy (also when it was
+ * captured into a CUDA graph and replayed: the copy is followed by an external
+ * event-record node, so the host resumes mid-graph, before the step ends). */
+int hsx_keep_sets_fetch_wait(hsx_plan* plan);
 /* Install keep sets from host index lists (KeepSetCache hit path / per-tensor
  * compress): k_out/k_in sorted ascending, lengths n_out/n_in. Recomputes the
  * flat-buffer offsets of every layer. */

@@ -65,11 +65,13 @@ SIGNATURES = {
     "hsx_read_groups": (C.c_int, [P, I32, VP, VP, VP]),
     "hsx_project": (C.c_int, [P, VP, VP, VP]),
     "hsx_project_keep_sets": (C.c_int, [P, VP, VP, VP, VP]),
+    "hsx_select_project_keep_sets": (C.c_int, [P, VP, VP, VP, VP]),
     "hsx_plan_set_single_node": (C.c_int, [P, C.c_int32]),
     "hsx_mask_or": (C.c_int, [VP, I32, I64, VP, VP]),
     "hsx_keep_sets": (C.c_int, [P, VP, VP, VP]),
     "hsx_keep_sets_fetch": (C.c_int, [P, VP, VP]),
     "hsx_keep_sets_fetch_async": (C.c_int, [P, VP, VP]),
+    "hsx_keep_sets_fetch_wait": (C.c_int, [P]),
     "hsx_set_keep_sets": (C.c_int, [P, I32, VP, I32, VP, I32]),
     "hsx_read_keep_positions": (C.c_int, [P, I32, VP, VP]),
     "hsx_compact_dual": (C.c_int, [P, VP, VP, VP, VP, VP, VP]),

@@ -119,6 +119,8 @@ struct hsx_plan {
   unsigned int* d_sched = nullptr;
   int *d_sfirst = nullptr, *d_scount = nullptr;  // per layer: first stream item, item count
   double* d_rpart = nullptr;                       // residual partials [stream item][9]
+  unsigned int *d_ready = nullptr, *d_pdone = nullptr;  // merged K2 + K3: per layer / prunable layer
+  cudaEvent_t fetch_ev = nullptr;                  // recorded after the summary D2H (external in graphs)
   unsigned long long* d_acc = nullptr;
   uint8_t *d_rk_prev = nullptr, *d_ck_prev = nullptr, *d_ch_prev = nullptr;
   int *d_irr = nullptr, *d_irr_any = nullptr;
@@ -134,11 +136,12 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
                     d_ch_prev};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    if (fetch_ev) cudaEventDestroy(fetch_ev);
     for (int i = 0; i < hsx::kMaxPasses; ++i) {
       if (d_sel[i]) cudaFree(d_sel[i]);
       if (d_partials[i]) cudaFree(d_partials[i]);
@@ -385,6 +388,8 @@ int upload_plan(hsx_plan* p) {
   if ((rc = alloc0(&p->d_layer_done, (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_cand_done, (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_sched, 2))) return rc;
+  if ((rc = alloc0(&p->d_ready, std::max(1, p->n_layers)))) return rc;
+  if ((rc = alloc0(&p->d_pdone, std::max<long long>(1, (long long)p->prunable.size())))) return rc;
   if ((rc = alloc0(&p->d_acc, 2 * (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_irr, (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_irr_any, 1))) return rc;
@@ -746,6 +751,33 @@ int hsx_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, const uint
   return HSX_OK;
 }
 
+int hsx_select_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, const uint32_t* prev_mask,
+                                 void* stream) {
+  if (!p || !z_node || (!mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
+  if (p->prunable.empty()) return HSX_OK;
+  const bool merge = p->single_node && p->max_passes == 1 && !p->sel_list[0].empty() &&
+                     p->sel_list[0].size() == p->prunable.size() && env_flag("HSX_MERGE_SELECT_PROJECT", 0);
+  if (!merge) {
+    for (int q = 0; q < p->max_passes; ++q)
+      if (int rc = hsx_select(p, q, stream)) return rc;
+    return hsx_project_keep_sets(p, z_node, mask, prev_mask, stream);
+  }
+  hsx::KeepArgs ka = keep_args(p, p->d_proj, mask, prev_mask);
+  hsx::SelProjArgs sp;
+  sp.list = p->d_sel[0];
+  sp.nsel = (int)p->sel_list[0].size();
+  sp.partials = p->d_partials[0];
+  sp.norms = p->d_norms[0];
+  sp.ready = p->d_ready;
+  sp.pdone = p->d_pdone;
+  sp.structured = 1;
+  hsx::launch_select_project(sp, ka, (int)p->proj_items.size(), z_node, mask, p->select_smem[0], S(stream));
+  HSX_LAUNCHED("select_project");
+  hsx::launch_keep_fixup(ka, p->d_prunable, (int)p->prunable.size(), p->fixup_smem, S(stream));
+  HSX_LAUNCHED("keep_fixup");
+  return HSX_OK;
+}
+
 int hsx_plan_set_single_node(hsx_plan* p, int32_t on) {
   if (!p) return fail(HSX_EINVAL, "null plan");
   p->single_node = on ? 1 : 0;
@@ -777,6 +809,19 @@ int hsx_keep_sets_fetch_async(hsx_plan* p, int64_t* host_summary, void* stream) 
   if (!p || !host_summary) return fail(HSX_EINVAL, "null argument");
   HSX_CUDA(cudaMemcpyAsync(host_summary, p->d_summary, p->summary.size() * sizeof(long long),
                            cudaMemcpyDeviceToHost, S(stream)));
+  // completion marker the host can wait on mid-step; under stream capture an
+  // external event-record node, so a replayed graph signals it at this point
+  if (!p->fetch_ev) HSX_CUDA(cudaEventCreateWithFlags(&p->fetch_ev, cudaEventDisableTiming));
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  HSX_CUDA(cudaStreamIsCapturing(S(stream), &cs));
+  HSX_CUDA(cudaEventRecordWithFlags(p->fetch_ev, S(stream),
+                                    cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
+  return HSX_OK;
+}
+
+int hsx_keep_sets_fetch_wait(hsx_plan* p) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  if (p->fetch_ev) HSX_CUDA(cudaEventSynchronize(p->fetch_ev));
   return HSX_OK;
 }
 

@@ -645,7 +645,7 @@ __device__ void radix_top_k(const unsigned long long* __restrict__ key, int G, i
 // group: [nparts][G] (FILTER: [G], complete row sums), folded in part order.
 // shared memory: keys[G] (u64), flags[G] (u8)
 __host__ __device__ inline size_t select_bytes(int G) { return ((size_t)G * 9 + 15) / 16 * 16; }
-constexpr int kFoldCols = 4096;  // column totals staged per norm chunk (32 KB)
+constexpr int kFoldCols = 2048;  // column totals staged per norm chunk (16 KB)
 
 __device__ void select_layer(const DevLayer& gly, int pass, const double* __restrict__ partials,
                              double* __restrict__ norms, const FlagPtrs& flags, void* smem, int l,
@@ -1304,12 +1304,9 @@ __device__ __forceinline__ void flag_irregular(const KeepArgs& a, int pidx, bool
 }
 
 template <bool CHECK>
-__global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __restrict__ zn,
-                                                         uint32_t* __restrict__ mask) {
-  PDL_ENTRY();
-  extern __shared__ float4 ring[];
+__device__ __forceinline__ void project_item(const KeepArgs& a, float* __restrict__ zn,
+                                             uint32_t* __restrict__ mask, const Item& it, float4* ring) {
   __shared__ uint8_t s_rk[kMaxTileRows];
-  const Item it = a.items[blockIdx.x];
   const LayerRegs ly(a.layers, it.layer);
   const DevLayer& dl = a.layers[it.layer];
   const int lane = threadIdx.x & 31;
@@ -1413,6 +1410,63 @@ __global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __re
     if (lane == 0) mask[ly.mword + w] = bits;
   }
   if (CHECK) flag_irregular(a, dl.pidx, bad);
+}
+
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __restrict__ zn,
+                                                         uint32_t* __restrict__ mask) {
+  PDL_ENTRY();
+  extern __shared__ float4 ring[];
+  project_item<CHECK>(a, zn, mask, a.items[blockIdx.x], ring);
+}
+
+// K2 + K3 in one launch (single-constraint plans): CTAs [0, nsel) select one layer
+// each and publish ready[layer]; the K3 CTAs behind them wait for their layer's
+// flag (acquire), so the projection of the layers selected first overlaps the
+// selection of the big ones instead of waiting for the slowest. Selection CTAs
+// have the lowest indices and never wait (dispatched first: no deadlock). The
+// last K3 item of a layer re-zeroes its flag and counter for the next launch.
+__global__ void __launch_bounds__(kThreads) k_select_project(SelProjArgs sp, KeepArgs a, float* __restrict__ zn,
+                                                            uint32_t* __restrict__ mask) {
+  PDL_ENTRY();
+  extern __shared__ float4 ring[];
+  if ((int)blockIdx.x < sp.nsel) {
+    const int l = sp.list[blockIdx.x];
+    select_layer(a.layers[l], 0, sp.partials, sp.norms, a.flags, ring, l, sp.structured ? &a : nullptr);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sp.ready + l), "r"(1u) : "memory");
+    }
+    return;
+  }
+  const Item it = a.items[blockIdx.x - sp.nsel];
+  const int l = it.layer;
+  if (threadIdx.x == 0) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sp.ready + l) : "memory");
+      if (v) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+  project_item<true>(a, zn, mask, it, ring);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const DevLayer& dl = a.layers[l];
+    if (atomicAdd(sp.pdone + dl.pidx, 1u) == (unsigned)dl.npitems - 1) {
+      sp.pdone[dl.pidx] = 0;
+      sp.ready[l] = 0;
+    }
+  }
+}
+
+void launch_select_project(const SelProjArgs& sp, const KeepArgs& a, int n_items, float* zn, uint32_t* mask,
+                           size_t smem, cudaStream_t st) {
+  const size_t need = std::max(smem, (size_t)kDepth * kThreads * sizeof(float4));
+  allow_smem(k_select_project, need);
+  launch_pdl(k_select_project, sp.nsel + n_items, kThreads, need, st, sp, a, zn, mask);
 }
 
 void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st) {

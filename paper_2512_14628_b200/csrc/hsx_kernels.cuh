@@ -173,6 +173,17 @@ void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t 
 void launch_keep_fixup(const KeepArgs& a, const int* prunable, int n, size_t smem, cudaStream_t st);
 // K3; check != 0: flag layers with a kept zero (structured keep sets)
 void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st);
+struct SelProjArgs {
+  const int* list;          // layers to select (pass 0)
+  int nsel;
+  const double* partials;   // pass 0
+  double* norms;
+  unsigned int* ready;      // per layer: selection published (left zeroed)
+  unsigned int* pdone;      // per prunable layer: K3 items finished (left zeroed)
+  int structured;
+};
+void launch_select_project(const SelProjArgs& sp, const KeepArgs& a, int n_items, float* zn, uint32_t* mask,
+                           size_t smem, cudaStream_t st);
 // shared memory of the structured keep-set derivation (K1 / K2 tail)
 size_t structured_smem_bytes(int rows, int L, int cin);
 size_t select_smem_bytes(int G);

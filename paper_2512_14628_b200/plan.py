@@ -247,6 +247,12 @@ class Plan:
         hsx_candidate_peers, re-read by composite passes). keep_prev: K3 also derives
         the keep sets from the mask it writes (hsx_project_keep_sets, prev_mask for
         the drift count)."""
+        if keep_prev and self.max_passes == 1:
+            # one node, single-constraint plan: selection and projection in one launch
+            with timed("K2K3_select_project_keep"):
+                _lib.call("hsx_select_project_keep_sets", self._h, ptr(z_node), ptr(local_mask), ptr(prev_mask),
+                          current_stream())
+            return
         for p in range(self.max_passes):
             if p > 0:
                 if peers:
@@ -298,7 +304,7 @@ class Plan:
         ev = torch.cuda.Event()
         ev.record(fs)
         self._fetch_done = ev
-        return ev
+        return FetchDone(self)
 
     def join_fetch(self):
         """Current stream waits for the last summary copy (end of a step; also closes
@@ -383,6 +389,16 @@ class Plan:
         r1, r2 = (C.c_double * n)(), (C.c_double * n)()
         _lib.call("hsx_plan_read_penalties", self._h, C.cast(r1, C.c_void_p), C.cast(r2, C.c_void_p))
         return list(r1), list(r2)
+
+
+class FetchDone:
+    """Host-side wait for the plan's last summary copy (works for graph replays too)."""
+
+    def __init__(self, plan):
+        self.plan = plan
+
+    def synchronize(self):
+        _lib.call("hsx_keep_sets_fetch_wait", self.plan._h)
 
 
 def mask_or_ptrs(srcs: list[int], words: int, out):

@@ -602,10 +602,11 @@ class HSADMMSync:
             g[0].replay()
             _lib.note_graph_replay(g[1])
         if self._pending is not None:
-            # the summary copy is part of the graph: wait on the replay instead
-            ev = torch.cuda.Event()
-            ev.record()
-            self._pending = (self._pending[0], ev, self._pending[2])
+            # the summary copy is part of the graph and signals an external event
+            # node right after it: the host resumes mid-replay
+            from .plan import FetchDone
+
+            self._pending = (self._pending[0], FetchDone(self.plan), self._pending[2])
 
     def _run_program(self, k: int):
         if hasattr(self.cluster, "run_rank"):

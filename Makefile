@@ -11,6 +11,9 @@ all: $(LIB)
 $(LIB): $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(SRC)
 
+nohints: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -DHSX_NO_L2_HINTS -shared -cudart static -o paper_2512_14628_b200/libhsx_nohints.so $(SRC)
+
 trace: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -DHSX_TRACE $(TRACE_FLAGS) -shared -cudart static -o paper_2512_14628_b200/libhsx_trace.so $(SRC)
 
@@ -20,4 +23,4 @@ ptxas: $(SRC) $(HDR)
 clean:
 	rm -f $(LIB)
 
-.PHONY: all clean ptxas trace
+.PHONY: all clean ptxas trace nohints

@@ -355,6 +355,7 @@ def run_ours(args):
     k += args.steps
     total_ms = max_over_ranks(sum(times))
     ms = total_ms / args.steps
+    step_spread = {"min": min(times), "p50": statistics.median(times), "max": max(times)}
     value = N * world / (ms / 1e3) / 1e6
     Z = eng.payload_elements
     # roofline pass: the same K dynamic steps with CUDA events around every libhsx
@@ -448,6 +449,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks.summary(),
+        "step_ms_spread": step_spread,
         "frozen_ms_per_step": frozen_ms,
         "phase5_ms_per_step": resid_ms,
         "leader_bytes": {"z_sync_bytes": 4 * Z, "dense_bytes": 4 * N, "ratio_vs_dense": Z / N},

@@ -82,6 +82,11 @@ int64_t hsx_launch_count(void);
 /* a CUDA graph holding `kernels` libhsx launches (captured through this ABI) was
    replayed: counted like eager launches */
 void hsx_note_graph_replay(int64_t kernels);
+/* L2 eviction-priority hints in the streaming kernels (z_node and the compact
+ * buffer kept resident between K1 / K3 / K6 / K7, single-use streams evict
+ * first) are a build choice (-DHSX_NO_L2_HINTS turns them off); returns 0 when
+ * the library was built with the requested setting, 1 otherwise. */
+int hsx_set_l2_hints(int32_t on);
 
 /* ---- plans ----------------------------------------------------------------- */
 int hsx_plan_create(const hsx_layer_desc* layers, int32_t n_layers, hsx_plan** out);

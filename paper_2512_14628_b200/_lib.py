@@ -46,6 +46,7 @@ SIGNATURES = {
     "hsx_last_error": (C.c_char_p, []),
     "hsx_launch_count": (I64, []),
     "hsx_note_graph_replay": (None, [I64]),
+    "hsx_set_l2_hints": (C.c_int, [I32]),
     "hsx_plan_create": (C.c_int, [C.POINTER(LayerDesc), I32, C.POINTER(P)]),
     "hsx_plan_destroy": (None, [P]),
     "hsx_plan_arena_elements": (I64, [P]),

@@ -68,6 +68,28 @@ __device__ __forceinline__ float4 ldcs4(const float* p) {
   return __ldcs(reinterpret_cast<const float4*>(p));
 }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+// L2 eviction-priority hints (createpolicy, on the cp.async loads): within a step
+// z_node is read by K3, K6 and K7 and the compact buffer by K7, so those are
+// re-read evict_last and stay resident in the 126 MB L2, while single-use
+// streams are read evict_first and written with st.global.cs (evict-first
+// stores). The policy must be warp-uniform (it becomes the load's memory
+// descriptor), so it is a compile-time choice; -DHSX_NO_L2_HINTS builds the
+// evict_normal (= no hint) variant for A/B runs.
+enum { kL2First = 0, kL2Last = 1 };
+__device__ __forceinline__ unsigned long long l2pol(int kind) {
+  unsigned long long p;
+#ifdef HSX_NO_L2_HINTS
+  (void)kind;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#else
+  if (kind == kL2Last)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
 __device__ __forceinline__ void stcs4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
 __device__ __forceinline__ float f4get(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
@@ -101,6 +123,11 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __device__ __forceinline__ void cp16(float4* dst, const float* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp16h(float4* dst, const float* src, unsigned long long pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "l"(pol)
+               : "memory");
+}
 // 4-byte copy, zero-fill when !valid (the global address is not dereferenced)
 __device__ __forceinline__ void cp4z(float* dst, const float* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
@@ -121,6 +148,16 @@ __device__ __forceinline__ float4* ring_slot(float4* ring, int d, int b) {
 
 // quad (4 consecutive elements at e) of `src` into a slot; partial quads past n
 // are zero-filled element-wise
+__device__ __forceinline__ void cp_quad_h(float4* dst, const float* src, long long e, long long n,
+                                          unsigned long long pol) {
+  if (e + 3 < n) {
+    cp16h(dst, src + e, pol);
+  } else {
+    float* d = reinterpret_cast<float*>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cp4z(d + i, src + (e + i < n ? e + i : 0), e + i < n);
+  }
+}
 __device__ __forceinline__ void cp_quad(float4* dst, const float* src, long long e, long long n) {
   if (e + 3 < n) {
     cp16(dst, src + e);
@@ -216,11 +253,19 @@ __device__ ulonglong2 block_sum2(unsigned long long x, unsigned long long y) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) wsum2[warp] = make_ulonglong2(x, y);
   __syncthreads();
-  ulonglong2 s = make_ulonglong2(0, 0);
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-    s.x += wsum2[w].x;
-    s.y += wsum2[w].y;
+  if (warp == 0) {  // warp 0 folds the warp sums, then broadcasts through slot 0
+    const bool in = lane < (int)(blockDim.x >> 5);
+    unsigned long long a = in ? wsum2[lane].x : 0ull, b = in ? wsum2[lane].y : 0ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(kFull, a, off);
+      b += __shfl_xor_sync(kFull, b, off);
+    }
+    __syncwarp();
+    if (lane == 0) wsum2[0] = make_ulonglong2(a, b);
   }
+  __syncthreads();
+  const ulonglong2 s = wsum2[0];
   __syncthreads();
   return s;
 }
@@ -261,6 +306,16 @@ __device__ int2 scan_keep(const uint8_t* fin, int cin, const uint8_t* fout, int 
   constexpr int kPer = 8;
   const int nt = blockDim.x, t = threadIdx.x;
   const int per = (max(cin, rows) + nt - 1) / nt;
+  if (per <= 1) {  // one flag of each array per thread
+    const bool fi = t < cin && flag_at<SMEM>(fin, t);
+    const bool fo = t < rows && flag_at<SMEM>(fout, t);
+    const int ex = block_exclusive_scan((int)fi | ((int)fo << 16), warp_tot, &total);
+    const int tot = total;
+    if (t < cin) pos_in[t] = fi ? (ex & 0xffff) : -1;
+    if (t < rows) pos_out[t] = fo ? (ex >> 16) : -1;
+    __syncthreads();
+    return make_int2(tot & 0xffff, tot >> 16);
+  }
   if (per <= kPer) {
     bool fi[kPer], fo[kPer];
     int ci = 0, co = 0;
@@ -572,11 +627,33 @@ __device__ void radix_top_k(const unsigned long long* __restrict__ key, int G, i
   __shared__ int warp_tot[32];
   __shared__ int total;
   const int t = threadIdx.x, nt = blockDim.x;
+  __shared__ unsigned long long s_diff[32];
   unsigned long long prefix = 0, himask = 0;
   int rem = keep, eq = G, buf = 0;
   for (int i = t; i < 256; i += nt) hist[0][i] = 0;
-  __syncthreads();
-  for (int shift = 56;; shift -= 8) {
+  // bytes above the highest one where any two keys differ are common to all keys:
+  // start the radix rounds there (norms of a layer share sign and exponent bytes)
+  {
+    const unsigned long long k0 = key[0];
+    unsigned long long d = 0;
+    for (int g = t; g < G; g += nt) d |= key[g] ^ k0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) d |= __shfl_xor_sync(kFull, d, off);
+    if ((t & 31) == 0) s_diff[t >> 5] = d;
+    __syncthreads();
+    d = 0;
+    for (int w = 0; w < (nt >> 5); ++w) d |= s_diff[w];
+    const int top = d ? 63 - __clzll((long long)d) : 0;  // highest differing bit
+    const int first = (top >> 3) << 3;                     // its byte's shift
+    himask = first >= 56 ? 0ull : (~0ull << (first + 8));
+    prefix = k0 & himask;
+    s_prefix = prefix;  // (unused until written by a round)
+    __syncthreads();
+    buf = 0;
+    // the first round below starts at `first`
+    rem = keep;
+    eq = G;
+    for (int shift = first;; shift -= 8) {
     // norms of one layer share their top bytes: warp-aggregate equal bins so a
     // round costs G/32 shared atomics instead of G serialized on one address
     for (int g0 = t - (t & 31); g0 < G; g0 += nt) {
@@ -624,6 +701,7 @@ __device__ void radix_top_k(const unsigned long long* __restrict__ key, int G, i
     himask |= 0xffULL << shift;
     if (rem == eq || shift == 0) break;
     buf ^= 1;
+  }
   }
   if (rem == eq) {  // every candidate of the bin is kept
     for (int g = t; g < G; g += nt) sflag[g] = (key[g] & himask) >= prefix;
@@ -827,13 +905,14 @@ __device__ __forceinline__ K1Src k1_src(const CandArgs& p, long long base) {
 // issue the quad at element e of every source into stage d (FULL: 16-B copies,
 // the quad is known to be in range)
 template <int MODE, bool FULL>
-__device__ __forceinline__ void k1_issue(float4* ring, int d, const K1Src& s, long long e, long long n) {
+__device__ __forceinline__ void k1_issue(float4* ring, int d, const K1Src& s, long long e, long long n,
+                                         unsigned long long pol) {
   constexpr int NB = K1<MODE>::NB;
   auto cp = [&](int slot, const float* src) {
     if (FULL)
-      cp16(ring_slot<NB>(ring, d, slot), src + e);
+      cp16h(ring_slot<NB>(ring, d, slot), src + e, pol);
     else
-      cp_quad(ring_slot<NB>(ring, d, slot), src, e, n);
+      cp_quad_h(ring_slot<NB>(ring, d, slot), src, e, n, pol);
   };
   if (MODE == kModePeers) {
 #pragma unroll
@@ -932,9 +1011,10 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
   const K1Src src = k1_src<MODE>(p, off);
   float* zn = p.zn + off;
   const uint32_t* fm = masked ? p.fmask + mword : nullptr;
+  const unsigned long long pf = l2pol(kL2First), pl = l2pol(kL2Last);
   ring_run(
       count,
-      [&](int d, int i) { k1_issue<MODE, false>(ring, d, src, begin + 4 * (t + (long long)i * kThreads), n); },
+      [&](int d, int i) { k1_issue<MODE, false>(ring, d, src, begin + 4 * (t + (long long)i * kThreads), n, pf); },
       [&](int d, int i) {
         const long long e = begin + 4 * (t + (long long)i * kThreads);
         double c[4];
@@ -948,7 +1028,7 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
           f4set(out, i2, (float)ci);
         }
         if (e + 3 < n) {
-          st4(zn + e, out);
+          st4(zn + e, out);  // z_node: re-read by K3 / K6 / K7 this step (normal priority)
         } else {
           for (int i2 = 0; i2 < 4 && e + i2 < n; ++i2) zn[e + i2] = f4get(out, i2);
         }
@@ -983,9 +1063,10 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const Coef cf = coef_of(ly);
   const long long stride = (long long)RP * L;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const unsigned long long pf = l2pol(kL2First), pl = l2pol(kL2Last);
   ring_run(
       count,
-      [&](int d, int i) { k1_issue<MODE, true>(ring, d, src, r0 * L + i * stride, 0); },
+      [&](int d, int i) { k1_issue<MODE, true>(ring, d, src, r0 * L + i * stride, 0, pf); },
       [&](int d, int i) {
         const long long e = r0 * L + i * stride;
         double c[4];
@@ -1319,6 +1400,8 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     // last chunk, whole 8-lane groups since L % 32 == 0) only join the shuffles
     const int count = __shfl_sync(kFull, tc.count, 0);
     const bool word_lane = (lane & 7) == 0 && tc.valid;
+    // (no L2 policy here: with the mask-word shuffles in the loop ptxas reuses the
+    // policy's uniform descriptor register for BRA.DIV -> illegal instruction)
     auto issue = [&](int d, int i) {
       if (tc.valid) cp16(ring_slot<1>(ring, d, 0), src + tc.row(i) * ly.L + 4 * tc.j);
     };
@@ -1760,12 +1843,15 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
   float* __restrict__ UU = a.u ? a.u + ly.off : nullptr;
   float* __restrict__ flat = a.flat_out ? a.flat_out + coff : nullptr;
   double acc[3] = {0.0, 0.0, 0.0};
+  // z_node is read again by K7 (keep resident), theta / u / v stream (evict first);
+  // the compact buffer is written evict_last for K7's gather
+  const unsigned long long pf = l2pol(kL2First), pl = l2pol(kL2Last);
   auto load4 = [&](int d, long long e) {
-    cp_quad(ring_slot<4>(ring, d, 0), ZN, e, ly.n);
-    if (VI && flat) cp_quad(ring_slot<4>(ring, d, 1), VI, e, ly.n);
+    cp_quad_h(ring_slot<4>(ring, d, 0), ZN, e, ly.n, pl);
+    if (VI && flat) cp_quad_h(ring_slot<4>(ring, d, 1), VI, e, ly.n, pf);
     if (TH) {
-      cp_quad(ring_slot<4>(ring, d, 2), TH, e, ly.n);
-      cp_quad(ring_slot<4>(ring, d, 3), UU, e, ly.n);
+      cp_quad_h(ring_slot<4>(ring, d, 2), TH, e, ly.n, pf);
+      cp_quad_h(ring_slot<4>(ring, d, 3), UU, e, ly.n, pf);
     }
   };
   auto emit = [&](int d, long long e, int4 dd) {
@@ -1784,7 +1870,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(ElemArgs a) {
         }
       }
       if (e + 3 < ly.n) {
-        st4(UU + e, un);
+        stcs4(UU + e, un);
       } else {
         for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) UU[e + i2] = f4get(un, i2);
       }
@@ -1857,6 +1943,7 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   const float* __restrict__ ZP = RESID ? a.zn_prev + ly.off : nullptr;
   const float div = a.divisor;
   double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const unsigned long long pf = l2pol(kL2First);
   auto load = [&](int d, long long e, int4 dd) {
     if (sync) {
       float* g = reinterpret_cast<float*>(ring_slot<NB>(ring, d, 0));
@@ -1865,13 +1952,13 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
       cp4z(g + 2, flat + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
       cp4z(g + 3, flat + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
     }
-    if (ZN) {
-      cp_quad(ring_slot<NB>(ring, d, 1), ZN, e, ly.n);
-      cp_quad(ring_slot<NB>(ring, d, 2), VV, e, ly.n);
+    if (ZN) {  // last uses in the step: evict first
+      cp_quad_h(ring_slot<NB>(ring, d, 1), ZN, e, ly.n, pf);
+      cp_quad_h(ring_slot<NB>(ring, d, 2), VV, e, ly.n, pf);
     }
     if (RESID) {
-      cp_quad(ring_slot<NB>(ring, d, RESID ? 3 : 0), ZP, e, ly.n);
-      cp_quad(ring_slot<NB>(ring, d, RESID ? 4 : 0), ZO, e, ly.n);
+      cp_quad_h(ring_slot<NB>(ring, d, RESID ? 3 : 0), ZP, e, ly.n, pf);
+      cp_quad_h(ring_slot<NB>(ring, d, RESID ? 4 : 0), ZO, e, ly.n, pf);
     }
   };
   auto emit = [&](int d, long long e) {
@@ -1904,8 +1991,8 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
     }
     if (!sync) return;
     if (e + 3 < ly.n) {
-      st4(ZO + e, zo);
-      if (ZN) st4(VV + e, vn);
+      stcs4(ZO + e, zo);
+      if (ZN) stcs4(VV + e, vn);
     } else {
       for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) {
         ZO[e + i2] = f4get(zo, i2);
@@ -2374,3 +2461,11 @@ extern "C" int hsx_debug_trace(void* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, hsx::g_trace, (size_t)n * 4 * sizeof(unsigned long long));
 }
 #endif
+
+extern "C" int hsx_set_l2_hints(int32_t on) {
+#ifdef HSX_NO_L2_HINTS
+  return on ? 1 : 0;  // built without hints
+#else
+  return on ? 0 : 1;  // built with hints (a build choice: -DHSX_NO_L2_HINTS)
+#endif
+}

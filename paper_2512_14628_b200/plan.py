@@ -9,6 +9,7 @@ bit per element of each prunable layer.
 from __future__ import annotations
 
 import contextlib
+import os
 import ctypes as C
 
 import torch

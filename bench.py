@@ -23,12 +23,12 @@ path) on this host on the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -102,6 +102,10 @@ def peaks():
 
 
 class ClockSampler:
+    """One background ``nvidia-smi -lms 200`` (the recipe's clocks line) for the
+    duration of the block: a single process streaming samples, so the timed loop
+    is not disturbed by a fork per sample."""
+
     FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -109,28 +113,30 @@ class ClockSampler:
     def __init__(self, gpus):
         self.gpus = gpus
         self.samples = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                      "-i", ",".join(str(g) for g in self.gpus)],
-                                     capture_output=True, text=True, timeout=5).stdout
-                for line in out.strip().splitlines():
-                    self.samples.append([x.strip() for x in line.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                        "-i", ",".join(str(g) for g in self.gpus), "-lms", "200"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._p = None
+        time.sleep(0.3)   # first sample before the timed loop starts
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.25)  # a last sample inside the window
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except Exception:
+            self._p.kill()
+            out, _ = self._p.communicate()
+        for line in (out or "").strip().splitlines():
+            self.samples.append([x.strip() for x in line.split(",")])
 
     def summary(self):
         if not self.samples:
@@ -349,8 +355,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     # headline: dynamic steps, clocks sampled during the timed region
     launches0 = _lib.launch_count()
+    gc.disable()   # no collector pauses inside the timed loop
     with ClockSampler([local] if world == 1 else list(range(world))) as clocks:
         times = timed_steps(k + 1, args.steps)
+    gc.enable()
     launches = _lib.launch_count() - launches0
     k += args.steps
     total_ms = max_over_ranks(sum(times))

@@ -325,6 +325,11 @@ def run_ours(args):
         torch.cuda.synchronize()
         for i in range(nsteps):
             flush.fill_(float(i))
+            if kernel_timer is not None:
+                # per-kernel pass: a ~1 ms spin keeps the GPU busy while the host
+                # enqueues the step's launches and their events, so each event pair
+                # brackets the kernel's device time, not the host's launch latency
+                torch.cuda._sleep(2_000_000)
             s = torch.cuda.Event(enable_timing=True)
             e = torch.cuda.Event(enable_timing=True)
             s.record()

@@ -257,6 +257,15 @@ int hsx_residual_report(hsx_plan* plan, const double* global, double* report, do
                         const hsx_resid_params* params, void* stream);
 /* u *= scales[0][l], v *= scales[1][l] for the layers whose factor != 1. */
 int hsx_scale_duals(const hsx_plan* plan, const double* scales, float* u, float* v, void* stream);
+/* Phase-1 boundary: one proximal-SGD step (proximal_sgd, workloads.py:316-320) over
+ * every layer: combined = grad + rho1*(theta - z_node + u); velocity = momentum *
+ * velocity + combined (first != 0: velocity starts at 0, :312); theta -= lr *
+ * velocity. fp64 math in the reference's order, fp32 state; rho1 from the plan's
+ * device layer table. send != NULL also writes theta + u (the intra-sum send
+ * buffer, K0 fused into the last step). HSX_ECONFIG if lr <= 0 (workloads.py:46-47). */
+int hsx_prox_sgd_step(const hsx_plan* plan, const float* grad, float* theta, const float* z_node,
+                      const float* u, float* velocity, double lr, double momentum, int32_t first,
+                      float* send, void* stream);
 /* Current per-layer penalties (after device-side adaptation); synchronous. */
 int hsx_plan_read_penalties(hsx_plan* plan, double* rho1, double* rho2);
 

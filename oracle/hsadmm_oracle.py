@@ -300,6 +300,24 @@ def residual_phase(layers, states, zn_prev, z_prev, sync_iter, num_nodes, per_no
     return report, r_intra_local
 
 
+# -- phase-1 boundary: proximal SGD update (workloads.py:296-321) ---------------
+
+
+def prox_sgd(w, z, u, rho1: dict, grads_seq, lr: float, momentum: float):
+    """proximal_sgd's parameter updates for a given gradient sequence (one entry
+    per mini-batch step): combined = grad + rho1 * (w - z + u), velocity =
+    momentum * velocity + combined, w -= lr * velocity (workloads.py:316-320);
+    velocity starts at zero (:312); inputs are not modified."""
+    w = {n: np.asarray(a, dtype=np.float64).copy() for n, a in w.items()}
+    vel = {n: np.zeros_like(a) for n, a in w.items()}
+    for grads in grads_seq:
+        for n in w:
+            combined = grads[n] + rho1[n] * (w[n] - z[n] + u[n])
+            vel[n] = momentum * vel[n] + combined
+            w[n] -= lr * vel[n]
+    return w
+
+
 # -- the cluster-wide sync step ------------------------------------------------
 
 

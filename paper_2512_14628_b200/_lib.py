@@ -84,6 +84,7 @@ SIGNATURES = {
     "hsx_residual_report": (C.c_int, [P, VP, VP, VP, C.POINTER(ResidParams), VP]),
     "hsx_scale_duals": (C.c_int, [P, VP, VP, VP, VP]),
     "hsx_plan_read_penalties": (C.c_int, [P, VP, VP]),
+    "hsx_prox_sgd_step": (C.c_int, [P, VP, VP, VP, VP, VP, F64, F64, I32, VP, VP]),
     "hsx_nonzero_u8": (C.c_int, [VP, I64, VP, VP]),
     "hsx_pack_bits": (C.c_int, [VP, I64, VP, VP]),
     "hsx_unpack_bits": (C.c_int, [VP, I64, VP, VP]),

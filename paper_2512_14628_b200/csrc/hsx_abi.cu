@@ -1002,6 +1002,16 @@ int hsx_scale_duals(const hsx_plan* p, const double* scales, float* u, float* v,
   return HSX_OK;
 }
 
+int hsx_prox_sgd_step(const hsx_plan* p, const float* grad, float* theta, const float* z_node, const float* u,
+                      float* velocity, double lr, double momentum, int32_t first, float* send, void* stream) {
+  if (!p || !grad || !theta || !z_node || !u || !velocity) return fail(HSX_EINVAL, "null argument");
+  if (!(lr > 0.0)) return fail(HSX_ECONFIG, "learning rate must be positive, got %g", lr);
+  hsx::launch_prox_sgd(p->d_layers, p->d_elem, (int)p->elem_items.size(), grad, theta, z_node, u, velocity, send, lr,
+                       momentum, first ? 1 : 0, S(stream));
+  HSX_LAUNCHED("prox_sgd_step");
+  return HSX_OK;
+}
+
 int hsx_plan_read_penalties(hsx_plan* p, double* rho1, double* rho2) {
   if (!p || !rho1 || !rho2) return fail(HSX_EINVAL, "null argument");
   if (p->n_layers)

@@ -2462,6 +2462,47 @@ extern "C" int hsx_debug_trace(void* out, int n) {
 }
 #endif
 
+namespace hsx {
+// ---------------------------------------------------------------------------
+// Phase-1 boundary: one proximal-SGD step of the reference's
+// solver (workloads.py:316-320), fused over every layer:
+//   combined = grad + rho1_l * (theta - z_node + u); vel = momentum * vel + combined;
+//   theta -= lr * vel
+// in fp64 (the reference's order), rounded once to fp32; first: vel starts at 0
+// (the solver zeroes it per outer iteration, :312); send != nullptr: also writes
+// theta + u for the intra sum (K0 fused into the last step). rho1 comes from the
+// device layer table, so device-side penalty adaptation is seen directly.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_prox_sgd(const DevLayer* __restrict__ layers,
+                                                      const Item* __restrict__ items, const float* __restrict__ g,
+                                                      float* __restrict__ th, const float* __restrict__ zn,
+                                                      const float* __restrict__ u, float* __restrict__ vel,
+                                                      float* __restrict__ send, double lr, double mom, int first) {
+  PDL_ENTRY();
+  const Item it = items[blockIdx.x];
+  const DevLayer& ly = layers[it.layer];
+  const double rho1 = ly.rho1;
+  const long long off = ly.off;
+  for (long long e = it.begin + threadIdx.x; e < it.end; e += kThreads) {
+    const long long i = off + e;
+    const double w = th[i];
+    const double comb = __dadd_rn((double)g[i], __dmul_rn(rho1, __dadd_rn(__dsub_rn(w, (double)zn[i]), (double)u[i])));
+    const double v = first ? comb : __dadd_rn(__dmul_rn(mom, (double)vel[i]), comb);
+    const float wn = (float)__dsub_rn(w, __dmul_rn(lr, v));
+    vel[i] = (float)v;
+    th[i] = wn;
+    if (send) send[i] = (float)__dadd_rn((double)wn, (double)u[i]);
+  }
+}
+
+void launch_prox_sgd(const DevLayer* layers, const Item* items, int n_items, const float* g, float* th,
+                     const float* zn, const float* u, float* vel, float* send, double lr, double mom, int first,
+                     cudaStream_t st) {
+  if (n_items <= 0) return;
+  launch_pdl(k_prox_sgd, n_items, kThreads, 0, st, layers, items, g, th, zn, u, vel, send, lr, mom, first);
+}
+}  // namespace hsx
+
 extern "C" int hsx_set_l2_hints(int32_t on) {
 #ifdef HSX_NO_L2_HINTS
   return on ? 1 : 0;  // built without hints

@@ -206,6 +206,9 @@ struct ResidArgs {
 };
 void launch_resid_fold(const ResidArgs& a, cudaStream_t st);
 void launch_report(const ResidArgs& a, cudaStream_t st);
+void launch_prox_sgd(const DevLayer* layers, const Item* items, int n_items, const float* g, float* th,
+                     const float* zn, const float* u, float* vel, float* send, double lr, double mom, int first,
+                     cudaStream_t st);
 void launch_scale_duals(const DevLayer* layers, const Item* items, int n_items, const double* scales,
                         int n_layers, float* u, float* v, cudaStream_t st);
 void launch_slices(const PeerPtrs& src, const long long* total_p, long long total_h, long long max_elems,

@@ -384,6 +384,11 @@ class Plan:
         with timed("K9_scale_duals"):
             _lib.call("hsx_scale_duals", self._h, ptr(scales), ptr(u), ptr(v), current_stream())
 
+    def prox_sgd_step(self, grad, theta, z_node, u, velocity, lr, momentum, first, send=None):
+        with timed("P1_prox_sgd"):
+            _lib.call("hsx_prox_sgd_step", self._h, ptr(grad), ptr(theta), ptr(z_node), ptr(u), ptr(velocity),
+                      float(lr), float(momentum), 1 if first else 0, ptr(send), current_stream())
+
     def read_penalties(self):
         """(rho1, rho2) per layer as currently in the device layer table (synchronous)."""
         n = len(self.names)

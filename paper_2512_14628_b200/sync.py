@@ -250,7 +250,7 @@ class HSADMMSync:
         s_local, peers = None, None
         if self.P > 2:
             # reduce-scatter (my slice of the rank-order sum) + all-gather, then K1 on S
-            pl.pack_theta_u(self.theta, self.u, self.p_send.tensor)
+            self._pack_send(self.p_send.tensor)
             yield Barrier(self.intra, "theta_u", k)
             me = self.intra.members.index(self.rank)
             pl.slices_peers(self.p_send.peer_ptrs(), me, 1.0, False, self.p_ssum.tensor, "K8_intra_rs")
@@ -260,7 +260,7 @@ class HSADMMSync:
             pl.candidate(s_local, None, None, self.z, self.v, self.z_node, frozen_mask=fmask)
         elif self.P == 2:
             # the intra sum fused into K1: theta+u of both ranks read over NVLink
-            pl.pack_theta_u(self.theta, self.u, self.p_send.tensor)
+            self._pack_send(self.p_send.tensor)
             yield Barrier(self.intra, "theta_u", k)
             peers = self.p_send.peer_ptrs()
             pl.candidate_peers(peers, self.z, self.v, self.z_node, frozen_mask=fmask)
@@ -330,6 +330,36 @@ class HSADMMSync:
                 dst = self.flat
         self._decompact(dst)
         return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
+
+    # -- phase-1 boundary ------------------------------------------------------------
+    def send_buffer(self):
+        """The intra-sum send buffer (theta + u) of this rank, or None when P == 1."""
+        if self.P == 1:
+            return None
+        return self.p_send.tensor if self.transport == "peer" else self.sum
+
+    def prox_sgd_step(self, grad, lr: float, momentum: float, first: bool, last: bool = False):
+        """One step of the reference's proximal SGD on this rank's theta (workloads.py:
+        316-320): combined = grad + rho1 * (theta - z_node + u), velocity = momentum *
+        velocity + combined, theta -= lr * velocity, fused over every layer with rho1
+        from the (possibly adapted) device penalties. ``grad`` is a flat fp32 arena
+        tensor. ``first`` starts the velocity at 0 (per outer iteration, :312); ``last``
+        also writes theta + u into the intra-sum send buffer, so the next program
+        skips K0."""
+        if grad.dtype != torch.float32 or grad.numel() != self.plan.arena or not grad.is_cuda:
+            raise ShapeError("grad must be a CUDA fp32 tensor of arena size")
+        if getattr(self, "velocity", None) is None:
+            self.velocity = self.plan.empty_arena(self.device)
+        send = self.send_buffer() if last else None
+        self.plan.prox_sgd_step(grad, self.theta, self.z_node, self.u, self.velocity, lr, momentum, first, send)
+        self._send_packed = send is not None
+
+    def _pack_send(self, buf):
+        """K0 (theta + u into the send buffer) unless the last SGD step already wrote it."""
+        if getattr(self, "_send_packed", False):
+            self._send_packed = False
+            return
+        self.plan.pack_theta_u(self.theta, self.u, buf)
 
     # -- K6 / K7 with or without the fused residual sums -------------------------------
     def _dual(self, flat):
@@ -441,7 +471,7 @@ class HSADMMSync:
         # phase 2: intra-node sum of theta + u
         s = None
         if self.P > 1:
-            pl.pack_theta_u(self.theta, self.u, self.sum)
+            self._pack_send(self.sum)
             s = yield AllReduce(self.intra, self.sum, ReduceOp.SUM, "theta_u", k)
         # phase 3: node candidate, projection or frozen mask
         pl.candidate(s, self.theta, self.u, self.z, self.v, self.z_node,

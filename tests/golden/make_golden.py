@@ -261,6 +261,45 @@ def gen_e2e(num_nodes, per_node, seed=3, adapt=False):
     np.savez_compressed(os.path.join(HERE, f"{tag}_{num_nodes}x{per_node}.npz"), **out)
 
 
+# -- phase-1 boundary: the proximal-SGD update rule (workloads.py:296-321) ------
+
+PROX_STEPS = 6   # 2 epochs x 3 mini-batches
+
+
+def gen_prox(seed=5):
+    """proximal_sgd with a stub workload whose loss_and_grad returns recorded
+    gradients in call order: pins the fused update (combined gradient, momentum,
+    lr) independent of any model."""
+    from admmprune.workloads import Shard, proximal_sgd
+
+    rng = np.random.default_rng([seed, 919])
+    shapes = {n: shape for n, _, shape, _ in E2E_LAYERS}
+    names = list(shapes)
+    w0 = {n: f32(rng.normal(0, 0.5, size=sh)) for n, sh in shapes.items()}
+    z = {n: f32(w0[n] + rng.normal(0, 0.05, size=sh)) for n, sh in shapes.items()}
+    u = {n: f32(rng.normal(0, 0.01, size=sh)) for n, sh in shapes.items()}
+    rho1 = {n: float(r) for n, r in zip(names, rng.choice([1.5e-3, 0.024, 0.75, 10.0], size=len(names)))}
+    grads = [{n: f32(rng.normal(0, 0.1, size=sh)) for n, sh in shapes.items()} for _ in range(PROX_STEPS)]
+    calls = iter(grads)
+
+    class _Stub:
+        def loss_and_grad(self, params, features, targets):
+            return 0.0, next(calls)
+
+    cfg = SolverConfig(lr=0.05, epochs=2, batch_size=4, momentum=0.9)
+    shard = Shard(np.zeros((12, 1)), np.zeros(12))
+    out = proximal_sgd(_Stub(), shard, w0, z, u, rho1, cfg, np.random.default_rng(0))
+    fx = {"meta": np.array([cfg.lr, cfg.momentum, PROX_STEPS]), "rho1": np.array([rho1[n] for n in names])}
+    for n in names:
+        fx[f"w0/{n}"] = w0[n].astype(np.float32)
+        fx[f"z/{n}"] = z[n].astype(np.float32)
+        fx[f"u/{n}"] = u[n].astype(np.float32)
+        fx[f"out/{n}"] = out[n]
+        for i, g in enumerate(grads):
+            fx[f"g/{i}/{n}"] = g[n].astype(np.float32)
+    np.savez_compressed(os.path.join(HERE, "prox_sgd.npz"), **fx)
+
+
 if __name__ == "__main__":
     gen_projection()
     gen_shrinkage()
@@ -270,4 +309,5 @@ if __name__ == "__main__":
         gen_e2e(m, p)
     for m, p in [(1, 1), (2, 1), (1, 2), (2, 2)]:
         gen_e2e(m, p, adapt=True)
+    gen_prox()
     print("golden fixtures written to", HERE)

@@ -109,3 +109,14 @@ class E2E:
 
     def rho_final(self):
         return self.d["rho_final"]
+
+
+def prox_case():
+    """proximal_sgd fixture (make_golden.gen_prox): inputs, gradient sequence, output."""
+    d = load("prox_sgd.npz")
+    names = [n for n, *_ in E2E_LAYERS]
+    lr, mom, steps = d["meta"]
+    f64 = lambda key: {n: d[f"{key}/{n}"].astype(np.float64) for n in names}
+    return dict(names=names, lr=float(lr), momentum=float(mom), rho1=dict(zip(names, d["rho1"].tolist())),
+                w0=f64("w0"), z=f64("z"), u=f64("u"), out={n: d[f"out/{n}"] for n in names},
+                grads=[{n: d[f"g/{i}/{n}"].astype(np.float64) for n in names} for i in range(int(steps))])

@@ -157,3 +157,42 @@ def test_residuals_off_leaves_the_step_unchanged():
     for a, b in zip(*outs):
         for key in a:
             assert torch.equal(a[key], b[key]), key
+
+
+# -- phase-1 boundary: the fused proximal-SGD step ----------------
+
+
+@pytest.mark.parametrize("M,P,transport", [(1, 1, "nccl"), (1, 2, "nccl"), (1, 2, "peer")])
+def test_prox_sgd_against_reference_golden(M, P, transport):
+    """HSADMMSync.prox_sgd_step x 6 reproduces proximal_sgd (workloads.py:296-321)
+    on the reference's recorded gradients within 1e-5 (H6 measure); the last step
+    also fills the intra-sum send buffer with theta + u (K0 fused)."""
+    import paper_2512_14628_b200 as H
+
+    c = G.prox_case()
+    kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
+             "shape": H.ConstraintKind.SHAPE_KEEP}
+    layers = [H.LayerSpec(n, H.LayerKind.CONV if k == "conv" else H.LayerKind.FULLY_CONNECTED, shape,
+                          prunable=bool(cc)) for n, k, shape, cc in G.E2E_LAYERS]
+    cons = {n: [H.SparsityConstraint(kinds[g], keep_rate=r) for g, r in cc] for n, _, _, cc in G.E2E_LAYERS if cc}
+    sched = H.PenaltySchedule(rho1=c["rho1"], rho2={n: 1.5e-4 for n in c["names"]}, adapt=False)
+    cluster = H.LocalCluster(H.Topology(M, P))
+    engines = [H.HSADMMSync(r, cluster, layers, cons, sched, H.ConsensusSettings(), transport=transport)
+               for r in range(M * P)]
+    e = engines[0]
+    e.load(theta=c["w0"], z_node=c["z"], u=c["u"])
+    for i, g in enumerate(c["grads"]):
+        ga = e.plan.empty_arena(e.device)
+        e.plan.load_arena(ga, g)
+        e.prox_sgd_step(ga, c["lr"], c["momentum"], first=(i == 0), last=(i == len(c["grads"]) - 1))
+    got = e.views("theta")
+    for n in c["names"]:
+        err = rel_err(cpu(got[n]), c["out"][n], c["w0"][n])
+        assert err <= TOL, (n, err)
+    send = e.send_buffer()
+    if P == 1:
+        assert send is None
+    else:
+        th, uu = cpu(e.theta).astype(np.float64), cpu(e.u).astype(np.float64)
+        assert np.array_equal(cpu(send), (th + uu).astype(np.float32))
+        assert e._send_packed

@@ -232,6 +232,55 @@ class HSADMMSync:
             self.cluster.log(LedgerEntry(k, self.inter.id, self.inter.scope.value, "allreduce_avg",
                                          b.elements, 4 * b.elements, self.M, f"z_sync/b{bi}", b.detail))
 
+    def _log_reference(self, k: int, sync: bool, frozen: bool):
+        """The ledger the reference writes for iteration k (transport.py:413-476 entries of
+        hierarchical_program's collectives, consensus.py:436-573), into
+        ``cluster.ref_ledger``: per-layer theta_u / mask_sync / z_bcast / v_bcast / m_bcast,
+        the z_sync buckets, res_intra / res_inter / report — 4 B per element, broadcasts
+        only in groups of > 1, each group collective once (by its first member). The
+        physical transfers (one arena all-reduce, packed mask bits, the compact
+        broadcast) are in ``cluster.ledger``."""
+        led = getattr(self.cluster, "ref_ledger", None)
+        if led is None:
+            return
+        shared = getattr(self.cluster, "shared_ledger", False)
+        L = len(self.layers)
+        sizes = [(ls.name, ls.elements) for ls in self.layers]
+        pr = [(self.names[i], self.layers[i].elements) for i in self.prunable]
+
+        def add(group, op, elems, nbytes, members, label, detail=None):
+            if nbytes > 0:
+                led.append(LedgerEntry(k, group.id, group.scope.value, op, int(elems), int(nbytes), members,
+                                       label, detail))
+
+        intra_first = not shared or self.rank == self.intra.members[0]
+        inter_first = self.is_leader and (not shared or self.rank == self.inter.members[0])
+        P, M = self.P, self.M
+        if intra_first:
+            for n, e in sizes:
+                add(self.intra, "allreduce_sum", e, 4 * e, P, f"theta_u/{n}")
+        if sync:
+            if inter_first and not frozen:
+                for n, e in pr:
+                    add(self.inter, "allreduce_bor", e, 4 * e, M, f"mask_sync/{n}")
+            if inter_first:
+                for bi, b in enumerate(self.buckets):
+                    add(self.inter, "allreduce_avg", b.elements, 4 * b.elements, M, f"z_sync/b{bi}", b.detail)
+            if intra_first and P > 1:
+                for tag in ("z_bcast", "v_bcast"):
+                    for n, e in sizes:
+                        add(self.intra, "broadcast", e, 4 * e * (P - 1), P, f"{tag}/{n}")
+                if not frozen:
+                    for n, e in pr:
+                        add(self.intra, "broadcast", e, 4 * e * (P - 1), P, f"m_bcast/{n}")
+        if self.residuals:
+            if intra_first:
+                add(self.intra, "allreduce_sum", 3 * L, 12 * L, P, "res_intra")
+            if inter_first:
+                add(self.inter, "allreduce_sum", 9 * L, 36 * L, M, "res_inter")
+            if intra_first and P > 1:
+                add(self.intra, "broadcast", 8 * L + 5, 4 * (8 * L + 5) * (P - 1), P, "report")
+
     def _program_peer(self, k: int):
         """Phases 2-5(u) with the collectives fused into the kernels over NVLink.
 
@@ -277,7 +326,9 @@ class HSADMMSync:
             pl.project_all(s_local, self.theta, self.u, self.z, self.v, self.z_node, local, peers=peers)
         if k % self.settings.sync_period != 0:
             self._dual(None)
-            return (yield from self._residual_phase(k, sync=False))
+            yield from self._residual_phase(k, sync=False)
+            self._log_reference(k, False, self.frozen)
+            return None
         ev = None
         if fused_keep:
             ev = pl.keep_sets_fetch_async()
@@ -445,9 +496,10 @@ class HSADMMSync:
         return None
 
     def _host_tail(self, k: int, dynamic: bool, log_zsync: bool):
-        """Ledger of the leader average; freeze + seal (consensus.py:600-606)."""
+        """Ledgers of the sync iteration; freeze + seal (consensus.py:600-606)."""
         if log_zsync and self.is_leader:
             self._log_zsync(k)
+        self._log_reference(k, True, self.frozen)   # sync iterations only reach here
         if dynamic and freeze_check(k, self.settings.t_freeze, self.drift_history,
                                     self.settings.drift_window):
             self.frozen = True
@@ -486,7 +538,9 @@ class HSADMMSync:
             pl.project_all(s, self.theta, self.u, self.z, self.v, self.z_node, self.local_mask)
         if k % self.settings.sync_period != 0:
             self._dual(None)
-            return (yield from self._residual_phase(k, sync=False))
+            yield from self._residual_phase(k, sync=False)
+            self._log_reference(k, False, self.frozen)
+            return None
         # phase 4: mask union (leaders), broadcast to followers, keep sets
         ev = None
         if fused_keep:
@@ -648,6 +702,8 @@ class HSADMMSync:
         self._begin_step()
         if self.residuals:
             self.reported = True
+        if not sync:
+            self._log_reference(k, False, self.frozen)
         if not sync:
             return
         if not dynamic:

@@ -321,6 +321,7 @@ class LocalCluster:
     def __init__(self, topology: Topology):
         self.topology = topology
         self.ledger = CommLedger()
+        self.ref_ledger = CommLedger()   # the reference's logical entries (HSADMMSync._log_reference)
         self._intra, self._leaders, self._global = hierarchy_groups(topology)
         self._shared = {}
 
@@ -448,6 +449,7 @@ class DistCluster:
         self.topology = topology
         self.rank = dist.get_rank()
         self.ledger = CommLedger()
+        self.ref_ledger = CommLedger()   # this rank's share of the reference's logical entries
         self._intra, self._leaders, self._global = hierarchy_groups(topology)
         self._handles = {}
         for i in range(topology.num_nodes):

@@ -255,6 +255,9 @@ def gen_e2e(num_nodes, per_node, seed=3, adapt=False):
             zs = [e.to_dict() for e in cluster.ledger.entries
                   if e.iteration == iters and e.label.startswith("z_sync")]
             out[f"zsync/{iters}"] = np.array(json.dumps(zs))
+            if adapt:  # the whole ledger of the iteration (phase 5 included)
+                out[f"ledger/{iters}"] = np.array(json.dumps([e.to_dict() for e in cluster.ledger.entries
+                                                               if e.iteration == iters]))
     finally:
         ref_consensus.batch_rng, ref_consensus.proximal_sgd = saved
     tag = "e2e_adapt" if adapt else "e2e"

@@ -110,6 +110,10 @@ class E2E:
     def rho_final(self):
         return self.d["rho_final"]
 
+    def ledger(self, k):
+        """Every ledger entry of iteration k (adaptive runs only)."""
+        return json.loads(str(self.d[f"ledger/{k}"]))
+
 
 def prox_case():
     """proximal_sgd fixture (make_golden.gen_prox): inputs, gradient sequence, output."""

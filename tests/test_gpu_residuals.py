@@ -8,6 +8,8 @@ within 1e-5 of the reference's fp64 state); state tensors
 within 1e-5 (H6 measure).
 """
 
+import json
+
 import numpy as np
 import pytest
 import torch
@@ -90,6 +92,10 @@ def test_adaptive_end_to_end_against_reference_goldens(M, P, transport):
                     assert err <= TOL, (k, e.rank, key, n, err)
             for n, m in ref.masks(k, node).items():
                 assert np.array_equal(cpu(e.mask_dict()[n]), m), (k, e.rank, n)
+        # the reference's full ledger of the iteration, entry for entry
+        got = sorted(json.dumps(x.to_dict(), sort_keys=True) for x in cluster.ref_ledger.entries if x.iteration == k)
+        want = sorted(json.dumps(x, sort_keys=True) for x in ref.ledger(k))
+        assert got == want, (k, set(got) ^ set(want))
     final = ref.rho_final()
     for e in engines:
         s = e.current_schedule()

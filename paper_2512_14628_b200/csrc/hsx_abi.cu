@@ -389,7 +389,7 @@ int upload_plan(hsx_plan* p) {
   if ((rc = alloc0(&p->d_cand_done, (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_sched, 2))) return rc;
   if ((rc = alloc0(&p->d_ready, std::max(1, p->n_layers)))) return rc;
-  if ((rc = alloc0(&p->d_pdone, std::max<long long>(1, (long long)p->prunable.size())))) return rc;
+  if ((rc = alloc0(&p->d_pdone, (long long)p->prunable.size() + 1))) return rc;  // + layers-done counter
   if ((rc = alloc0(&p->d_acc, 2 * (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_irr, (long long)p->prunable.size()))) return rc;
   if ((rc = alloc0(&p->d_irr_any, 1))) return rc;
@@ -771,10 +771,10 @@ int hsx_select_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, con
   sp.ready = p->d_ready;
   sp.pdone = p->d_pdone;
   sp.structured = 1;
-  hsx::launch_select_project(sp, ka, (int)p->proj_items.size(), z_node, mask, p->select_smem[0], S(stream));
+  // selection, projection and the keep-set fixup (in the layers' last K3 items) in one launch
+  hsx::launch_select_project(sp, ka, (int)p->proj_items.size(), z_node, mask,
+                             std::max(p->select_smem[0], p->fixup_smem), S(stream));
   HSX_LAUNCHED("select_project");
-  hsx::launch_keep_fixup(ka, p->d_prunable, (int)p->prunable.size(), p->fixup_smem, S(stream));
-  HSX_LAUNCHED("keep_fixup");
   return HSX_OK;
 }
 

@@ -1503,6 +1503,8 @@ __global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __re
   project_item<CHECK>(a, zn, mask, a.items[blockIdx.x], ring);
 }
 
+__device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);
+
 // K2 + K3 in one launch (single-constraint plans): CTAs [0, nsel) select one layer
 // each and publish ready[layer]; the K3 CTAs behind them wait for their layer's
 // flag (acquire), so the projection of the layers selected first overlaps the
@@ -1535,13 +1537,35 @@ __global__ void __launch_bounds__(kThreads) k_select_project(SelProjArgs sp, Kee
   }
   __syncthreads();
   project_item<true>(a, zn, mask, it, ring);
+  // the layer's last K3 item runs the layer's fixup (k_keep_fixup fused); the last
+  // layer to finish re-lays the flat buffer out if any layer had a kept zero
+  __shared__ bool last_item, last_layer;
+  __syncthreads();
+  const DevLayer& dl = a.layers[l];
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last_item = atomicAdd(sp.pdone + dl.pidx, 1u) == (unsigned)dl.npitems - 1;
+  }
+  __syncthreads();
+  if (!last_item) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    sp.pdone[dl.pidx] = 0;
+    sp.ready[l] = 0;
+  }
+  fixup_layer(a, l, reinterpret_cast<uint8_t*>(ring));
   __syncthreads();
   if (threadIdx.x == 0) {
-    const DevLayer& dl = a.layers[l];
-    if (atomicAdd(sp.pdone + dl.pidx, 1u) == (unsigned)dl.npitems - 1) {
-      sp.pdone[dl.pidx] = 0;
-      sp.ready[l] = 0;
-    }
+    __threadfence();
+    last_layer = atomicAdd(sp.pdone + a.n_prunable, 1u) == (unsigned)a.n_prunable - 1;
+  }
+  __syncthreads();
+  if (!last_layer) return;
+  __threadfence();
+  if (*reinterpret_cast<volatile int*>(a.irr_any)) layout_flat(a);
+  if (threadIdx.x == 0) {
+    sp.pdone[a.n_prunable] = 0;
+    *a.irr_any = 0;
   }
 }
 
@@ -1657,14 +1681,13 @@ void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t 
 // counted from the bits. The common case (neither) returns at once; when some
 // layer was re-derived, the last CTA lays out the flat buffer again.
 // smem: c_in + rows bytes.
-__global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* __restrict__ prunable) {
-  PDL_ENTRY();
-  extern __shared__ __align__(16) uint8_t fsm[];
-  const int l = prunable[blockIdx.x];
+// Per-layer part of the fixup (all of the layer's K3 items are done): exact keep
+// sets / popcounts from the mask bits when the layer has a kept zero now (bit 0)
+// or had one in the previous mask (bit 1, the drift reference); shifts the flag.
+__device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm) {
   const DevLayer& gly = a.layers[l];
   const int pidx = gly.pidx;
   const int irr = a.irr[pidx];
-  const int any = *reinterpret_cast<volatile int*>(a.irr_any);
   if (irr & 3) {
     const int cin = gly.cin, rows = gly.rows, k = gly.k, L = gly.L;
     const long long n = gly.n, mword = gly.mword, ikeep = gly.ikeep, okeep = gly.okeep;
@@ -1714,7 +1737,16 @@ __global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* 
     }
     if (threadIdx.x == 0) a.summary[(long long)l * kSumCols + 4] = (long long)drift;
   }
+  __syncthreads();
   if (threadIdx.x == 0) a.irr[pidx] = (irr & 1) << 1;  // this mask is the next one's previous
+}
+
+__global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* __restrict__ prunable) {
+  PDL_ENTRY();
+  extern __shared__ __align__(16) uint8_t fsm[];
+  const int l = prunable[blockIdx.x];
+  const int any = *reinterpret_cast<volatile int*>(a.irr_any);
+  fixup_layer(a, l, fsm);
   if (!any) return;
   // some layer was re-derived: the last CTA lays the flat buffer out again
   __shared__ bool last;

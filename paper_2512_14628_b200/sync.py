@@ -244,18 +244,26 @@ class HSADMMSync:
         if led is None:
             return
         shared = getattr(self.cluster, "shared_ledger", False)
+        intra_first = not shared or self.rank == self.intra.members[0]
+        inter_first = self.is_leader and (not shared or self.rank == self.inter.members[0])
+        if not (intra_first or inter_first):
+            return
+        # everything the entries depend on, captured now; the entries are built on read
+        ctx = (k, sync, frozen, self.residuals, self.buckets, intra_first, inter_first)
+        led.defer(lambda: self._reference_entries(*ctx))
+
+    def _reference_entries(self, k, sync, frozen, residuals, buckets, intra_first, inter_first):
+        out = []
         L = len(self.layers)
         sizes = [(ls.name, ls.elements) for ls in self.layers]
         pr = [(self.names[i], self.layers[i].elements) for i in self.prunable]
+        P, M = self.P, self.M
 
         def add(group, op, elems, nbytes, members, label, detail=None):
             if nbytes > 0:
-                led.append(LedgerEntry(k, group.id, group.scope.value, op, int(elems), int(nbytes), members,
+                out.append(LedgerEntry(k, group.id, group.scope.value, op, int(elems), int(nbytes), members,
                                        label, detail))
 
-        intra_first = not shared or self.rank == self.intra.members[0]
-        inter_first = self.is_leader and (not shared or self.rank == self.inter.members[0])
-        P, M = self.P, self.M
         if intra_first:
             for n, e in sizes:
                 add(self.intra, "allreduce_sum", e, 4 * e, P, f"theta_u/{n}")
@@ -264,7 +272,7 @@ class HSADMMSync:
                 for n, e in pr:
                     add(self.inter, "allreduce_bor", e, 4 * e, M, f"mask_sync/{n}")
             if inter_first:
-                for bi, b in enumerate(self.buckets):
+                for bi, b in enumerate(buckets):
                     add(self.inter, "allreduce_avg", b.elements, 4 * b.elements, M, f"z_sync/b{bi}", b.detail)
             if intra_first and P > 1:
                 for tag in ("z_bcast", "v_bcast"):
@@ -273,13 +281,14 @@ class HSADMMSync:
                 if not frozen:
                     for n, e in pr:
                         add(self.intra, "broadcast", e, 4 * e * (P - 1), P, f"m_bcast/{n}")
-        if self.residuals:
+        if residuals:
             if intra_first:
                 add(self.intra, "allreduce_sum", 3 * L, 12 * L, P, "res_intra")
             if inter_first:
                 add(self.inter, "allreduce_sum", 9 * L, 36 * L, M, "res_inter")
             if intra_first and P > 1:
                 add(self.intra, "broadcast", 8 * L + 5, 4 * (8 * L + 5) * (P - 1), P, "report")
+        return out
 
     def _program_peer(self, k: int):
         """Phases 2-5(u) with the collectives fused into the kernels over NVLink.

@@ -191,6 +191,40 @@ class LedgerEntry:
         return d
 
 
+class DeferredLedger:
+    """A ledger whose per-iteration entries are produced on demand: the step
+    records one closure (no per-entry host work while the GPU waits for the next
+    launch); ``entries`` materializes them in order."""
+
+    def __init__(self):
+        self._items = []
+        self._done: list[LedgerEntry] = []
+
+    def append(self, entry: LedgerEntry) -> None:
+        self._items.append(entry)
+
+    def defer(self, thunk) -> None:
+        self._items.append(thunk)
+
+    @property
+    def entries(self) -> list[LedgerEntry]:
+        if self._items:
+            for it in self._items:
+                if callable(it):
+                    self._done.extend(it())
+                else:
+                    self._done.append(it)
+            self._items = []
+        return self._done
+
+    def to_jsonl(self, path) -> None:
+        import json
+
+        with open(path, "w", encoding="utf-8") as fh:
+            for e in self.entries:
+                fh.write(json.dumps(e.to_dict(), sort_keys=True) + "\n")
+
+
 class CommLedger:
     """Append-only record of completed collectives (reference transport.py:154-188).
 
@@ -321,7 +355,7 @@ class LocalCluster:
     def __init__(self, topology: Topology):
         self.topology = topology
         self.ledger = CommLedger()
-        self.ref_ledger = CommLedger()   # the reference's logical entries (HSADMMSync._log_reference)
+        self.ref_ledger = DeferredLedger()   # the reference's logical entries (HSADMMSync._log_reference)
         self._intra, self._leaders, self._global = hierarchy_groups(topology)
         self._shared = {}
 
@@ -449,7 +483,7 @@ class DistCluster:
         self.topology = topology
         self.rank = dist.get_rank()
         self.ledger = CommLedger()
-        self.ref_ledger = CommLedger()   # this rank's share of the reference's logical entries
+        self.ref_ledger = DeferredLedger()   # this rank's share of the reference's logical entries
         self._intra, self._leaders, self._global = hierarchy_groups(topology)
         self._handles = {}
         for i in range(topology.num_nodes):

@@ -38,15 +38,29 @@ if sampler:
 for k in range(1, 6):
     eng.graph_step(k)
 torch.cuda.synchronize()
-evs = []
+import time  # noqa: E402
+
+evs, host = [], []
 for i in range(steps):
     flush.fill_(float(i))
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
+    t0 = time.perf_counter()
     eng.graph_step(6 + i)
+    host.append((time.perf_counter() - t0) * 1e3)
     e.record()
     evs.append((s, e))
 torch.cuda.synchronize()
+print(f"host ms per graph_step: mean {sum(host) / len(host):.4f} min {min(host):.4f} max {max(host):.4f}")
+import cProfile, pstats  # noqa: E402
+pr = cProfile.Profile()
+pr.enable()
+for i in range(20):
+    flush.fill_(float(i))
+    eng.graph_step(100 + i)
+torch.cuda.synchronize()
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(12)
 stop.set()
 t = [a.elapsed_time(b) for a, b in evs]
 print(f"sampler={sampler} mean {sum(t) / len(t):.4f} min {min(t):.4f} max {max(t):.4f}")

@@ -248,8 +248,8 @@ class Plan:
         hsx_candidate_peers, re-read by composite passes). keep_prev: K3 also derives
         the keep sets from the mask it writes (hsx_project_keep_sets, prev_mask for
         the drift count)."""
-        if keep_prev and self.max_passes == 1:
-            # one node, single-constraint plan: selection and projection in one launch
+        if keep_prev and self.max_passes == 1 and os.environ.get("HSX_MERGE_SELECT_PROJECT") == "1":
+            # one node, single-constraint plan: selection, projection and fixup in one launch
             with timed("K2K3_select_project_keep"):
                 _lib.call("hsx_select_project_keep_sets", self._h, ptr(z_node), ptr(local_mask), ptr(prev_mask),
                           current_stream())

@@ -264,6 +264,7 @@ def algorithmic_bytes(kernel, N, n_c, Z, P):
         "K6_compact_dual": 20 * N + 4 * Z,
         "K6f_dual_intra": 16 * N,
         "K7_decompact_dual": 16 * N + 4 * Z,
+        "K67_local_sync": 28 * N,                     # read z_node, v, theta, u; write u, z, v
     }.get(kernel)
 
 

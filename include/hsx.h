@@ -246,6 +246,13 @@ int hsx_compact_dual_resid(const hsx_plan* plan, const float* theta, float* u, c
 int hsx_decompact_dual_resid(const hsx_plan* plan, const float* flat, float divisor,
                              const float* z_node, const float* z_node_prev, float* v, float* z,
                              void* stream);
+/* K6 + K7 of a one-node cluster (M == 1) in one pass: the leader average is the
+ * identity, so z = z_node + v on the kept rectangle (0 elsewhere), u += theta -
+ * z_node, v += z_node - z, in place and bitwise equal to hsx_compact_dual then
+ * hsx_decompact_dual(divisor 1) — without the compact buffer. residuals != 0
+ * also accumulates all nine residual slots (z_node_prev required). */
+int hsx_local_sync(const hsx_plan* plan, const float* theta, float* u, const float* z_node, float* v,
+                   float* z, const float* z_node_prev, int32_t residuals, void* stream);
 /* vec[layer][9] = the layer's slot sums (leader == 0 zeroes slots 3-8: the
  * node's leader contributes them to the intra SUM, consensus.py:550-563). */
 int hsx_residual_fold(hsx_plan* plan, int32_t leader, double* vec, void* stream);

@@ -80,6 +80,7 @@ SIGNATURES = {
     "hsx_decompact_dual": (C.c_int, [P, VP, F32, VP, VP, VP, VP]),
     "hsx_compact_dual_resid": (C.c_int, [P, VP, VP, VP, VP, VP, VP]),
     "hsx_decompact_dual_resid": (C.c_int, [P, VP, F32, VP, VP, VP, VP, VP]),
+    "hsx_local_sync": (C.c_int, [P, VP, VP, VP, VP, VP, VP, I32, VP]),
     "hsx_residual_fold": (C.c_int, [P, I32, VP, VP]),
     "hsx_residual_report": (C.c_int, [P, VP, VP, VP, C.POINTER(ResidParams), VP]),
     "hsx_scale_duals": (C.c_int, [P, VP, VP, VP, VP]),

@@ -948,6 +948,23 @@ int hsx_decompact_dual_resid(const hsx_plan* p, const float* flat, float divisor
   return HSX_OK;
 }
 
+int hsx_local_sync(const hsx_plan* p, const float* theta, float* u, const float* z_node, float* v, float* z,
+                   const float* z_node_prev, int32_t residuals, void* stream) {
+  if (!p || !theta || !u || !z_node || !v || !z) return fail(HSX_EINVAL, "null argument");
+  if (residuals && !z_node_prev) return fail(HSX_EINVAL, "residuals need z_node_prev");
+  hsx::ElemArgs a = elem_args(p);
+  a.theta = theta;
+  a.u = u;
+  a.zn = z_node;
+  a.v = v;
+  a.z = z;
+  a.zn_prev = z_node_prev;
+  a.rpart = residuals ? p->d_rpart : nullptr;
+  hsx::launch_local_sync(a, (int)p->stream_items.size(), S(stream));
+  HSX_LAUNCHED("local_sync");
+  return HSX_OK;
+}
+
 static hsx::ResidArgs resid_args(hsx_plan* p) {
   hsx::ResidArgs a;
   std::memset(&a, 0, sizeof(a));

@@ -2070,6 +2070,114 @@ void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
   }
 }
 
+// K6+K7 of one node (M == 1), fused: the leader average is the identity, so the
+// compact round trip z = decompress(compress(z_node + v)) is z = z_node + v on the
+// kept rectangle K_out x K_in and 0 elsewhere — computed in place without the
+// flat buffer (bitwise what K6 then K7 produce: the same fp32 add, / 1):
+//   u <- u + (theta - z_node); z <- kept ? z_node + v : 0; v <- v + (z_node - z)
+// RESID: the K6 (0-2) and K7 (3-8) residual slots in one pass (z_prev, z_node_prev
+// streamed too).
+template <bool RESID>
+__global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
+  PDL_ENTRY();
+  constexpr int NB = RESID ? 6 : 4;
+  constexpr int D = RESID ? 3 : kDepth;  // 6 x 3 x 4 KB = 72 KB / 4 x 4 x 4 KB = 64 KB
+  extern __shared__ float4 ring[];
+  __shared__ int s_rb[kMaxTileRows];
+  const Item it = a.items[blockIdx.x];
+  const LayerRegs ly(a.layers, it.layer);
+  const int rowlen = (int)a.summary[(long long)it.layer * kSumCols + 1] * ly.k;  // |K_in| * k
+  const float* __restrict__ ZN = a.zn + ly.off;
+  const float* __restrict__ TH = a.theta + ly.off;
+  float* __restrict__ UU = a.u + ly.off;
+  float* __restrict__ VV = a.v + ly.off;
+  float* __restrict__ ZO = a.z + ly.off;
+  const float* __restrict__ ZP = RESID ? a.zn_prev + ly.off : nullptr;
+  double acc[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const unsigned long long pf = l2pol(kL2First);
+  auto load = [&](int d, long long e) {
+    cp_quad_h(ring_slot<NB>(ring, d, 0), ZN, e, ly.n, pf);
+    cp_quad_h(ring_slot<NB>(ring, d, 1), VV, e, ly.n, pf);
+    cp_quad_h(ring_slot<NB>(ring, d, 2), TH, e, ly.n, pf);
+    cp_quad_h(ring_slot<NB>(ring, d, 3), UU, e, ly.n, pf);
+    if (RESID) {
+      cp_quad_h(ring_slot<NB>(ring, d, RESID ? 4 : 0), ZP, e, ly.n, pf);
+      cp_quad_h(ring_slot<NB>(ring, d, RESID ? 5 : 0), ZO, e, ly.n, pf);
+    }
+  };
+  auto emit = [&](int d, long long e, int4 dd) {
+    const float4 zn = *ring_slot<NB>(ring, d, 0), vv = *ring_slot<NB>(ring, d, 1);
+    const float4 th = *ring_slot<NB>(ring, d, 2), uu = *ring_slot<NB>(ring, d, 3);
+    const float4 un = make_float4(dual1(uu.x, th.x, zn.x), dual1(uu.y, th.y, zn.y), dual1(uu.z, th.z, zn.z),
+                                  dual1(uu.w, th.w, zn.w));
+    const float4 zo = make_float4(dd.x >= 0 ? zn.x + vv.x : 0.f, dd.y >= 0 ? zn.y + vv.y : 0.f,
+                                  dd.z >= 0 ? zn.z + vv.z : 0.f, dd.w >= 0 ? zn.w + vv.w : 0.f);
+    const float4 vn = make_float4(dual1(vv.x, zn.x, zo.x), dual1(vv.y, zn.y, zo.y), dual1(vv.z, zn.z, zo.z),
+                                  dual1(vv.w, zn.w, zo.w));
+    if (RESID) {  // zero-filled tail lanes add 0
+      const float4 zp = *ring_slot<NB>(ring, d, RESID ? 4 : 0), zold = *ring_slot<NB>(ring, d, RESID ? 5 : 0);
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) {
+        const double t = f4get(th, i2), n = f4get(zn, i2), z = f4get(zo, i2);
+        acc[0] += sqd(t - n);
+        acc[1] += sqd(t);
+        acc[2] += sqd((double)f4get(un, i2));
+        acc[3] += sqd(n - z);
+        acc[4] += sqd(n - (double)f4get(zp, i2));
+        acc[5] += sqd(n);
+        acc[6] += sqd((double)f4get(vn, i2));
+        acc[7] += sqd(z - (double)f4get(zold, i2));
+        acc[8] += sqd(z);
+      }
+    }
+    if (e + 3 < ly.n) {
+      stcs4(UU + e, un);
+      stcs4(ZO + e, zo);
+      stcs4(VV + e, vn);
+    } else {
+      for (int i2 = 0; i2 < 4 && e + i2 < ly.n; ++i2) {
+        UU[e + i2] = f4get(un, i2);
+        ZO[e + i2] = f4get(zo, i2);
+        VV[e + i2] = f4get(vn, i2);
+      }
+    }
+  };
+  if (it.tile == 1) {
+    const TileCtx tc(it, ly.L);
+    row_base(a, ly, it, rowlen, s_rb);
+    const int4 cp = col_pos4(a, ly, tc.j, tc.valid);
+    __syncthreads();
+    ring_run<D>(tc.count, [&](int d, int i) { load(d, tc.row(i) * ly.L + 4 * tc.j); },
+                [&](int d, int i) {
+                  const long long r = tc.row(i);
+                  emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
+                });
+  } else {
+    const long long nq = (it.end - it.begin + 3) >> 2;
+    const int t = threadIdx.x;
+    const int count = t < nq ? (int)((nq - t + kThreads - 1) / kThreads) : 0;
+    ring_run<D>(count, [&](int d, int i) { load(d, it.begin + 4 * (t + (long long)i * kThreads)); },
+                [&](int d, int i) {
+                  const long long e = it.begin + 4 * (t + (long long)i * kThreads);
+                  emit(d, e, dst4_linear(a, ly, rowlen, e));
+                });
+  }
+  if (RESID) block_partials<9>(acc, a.rpart + (long long)blockIdx.x * kResidSlots);
+}
+
+void launch_local_sync(const ElemArgs& a, int n_items, cudaStream_t st) {
+  if (n_items <= 0) return;
+  if (a.rpart) {
+    const size_t smem = (size_t)3 * 6 * kThreads * sizeof(float4);
+    allow_smem(k_local_sync<true>, smem);
+    launch_pdl(k_local_sync<true>, n_items, kThreads, smem, st, a);
+  } else {
+    const size_t smem = (size_t)kDepth * 4 * kThreads * sizeof(float4);
+    allow_smem(k_local_sync<false>, smem);
+    launch_pdl(k_local_sync<false>, n_items, kThreads, smem, st, a);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Phase 5 (consensus.py:537-598): per-layer fold of the item partials, the
 // residual report (consensus.py:239-288) and residual balancing

@@ -189,6 +189,7 @@ size_t structured_smem_bytes(int rows, int L, int cin);
 size_t select_smem_bytes(int G);
 void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st);
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st);
+void launch_local_sync(const ElemArgs& a, int n_items, cudaStream_t st);
 // phase 5: per-layer fold of the residual partials, report + adaptation, dual rescale
 struct ResidArgs {
   DevLayer* layers;                     // penalties updated in place when adapting

@@ -371,6 +371,12 @@ class Plan:
             _lib.call("hsx_decompact_dual_resid", self._h, ptr(flat), float(divisor), ptr(z_node),
                       ptr(z_node_prev), ptr(v), ptr(z), current_stream())
 
+    def local_sync(self, theta, u, z_node, v, z, z_node_prev=None, residuals=False):
+        """K6 + K7 of one node in one pass (no compact buffer)."""
+        with timed("K67_local_sync"):
+            _lib.call("hsx_local_sync", self._h, ptr(theta), ptr(u), ptr(z_node), ptr(v), ptr(z), ptr(z_node_prev),
+                      1 if residuals else 0, current_stream())
+
     def residual_fold(self, leader: bool, vec):
         with timed("K9_residual_fold"):
             _lib.call("hsx_residual_fold", self._h, 1 if leader else 0, ptr(vec), current_stream())

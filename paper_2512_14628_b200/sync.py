@@ -359,10 +359,9 @@ class HSADMMSync:
         zhat = self.p_zhat.tensor if self.P > 1 else None
         if self.M == 1:
             # one node: the leader "average" is the identity and every rank holds the
-            # same z_node and v, so each rank compacts and decompacts locally (the
-            # result is bitwise what the intra broadcast would deliver)
-            self._dual(self.flat)
-            self._decompact(self.flat)
+            # same z_node and v, so each rank runs K6+K7 locally in one pass (bitwise
+            # what the compact round trip and the intra broadcast would deliver)
+            self._local_sync()
             return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
         if self.is_leader:
             if self.M > 1:
@@ -431,6 +430,14 @@ class HSADMMSync:
             pl.compact_dual(self.theta, self.u, self.z_node, self.v, flat)
         else:
             pl.dual_intra(self.theta, self.u, self.z_node)
+
+    def _local_sync(self):
+        """K6 + K7 of a one-node cluster in one pass (HSX_LOCAL_SYNC=0: the two kernels)."""
+        if os.environ.get("HSX_LOCAL_SYNC", "1") == "0":
+            self._dual(self.flat)
+            self._decompact(self.flat)
+            return
+        self.plan.local_sync(self.theta, self.u, self.z_node, self.v, self.z, self.z_node_prev, self.residuals)
 
     def _decompact(self, flat):
         if self.residuals:
@@ -564,6 +571,11 @@ class HSADMMSync:
             ev = pl.keep_sets_fetch_async()             # the one D2H of the dynamic step
         elif self.is_leader and self.prunable:
             self.cache_hits += len(self.prunable)
+        if self.M == 1:
+            # one node: no leader exchange; every rank runs K6+K7 locally (bitwise the
+            # leader's compact round trip + broadcast), no mid-step host wait
+            self._local_sync()
+            return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
         # compaction fused with the intra dual update (K6 reads sizes on device, so
         # it runs while the host waits for the D2H and sizes the collectives)
         self._dual(self.flat if self.is_leader else None)

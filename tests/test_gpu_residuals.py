@@ -165,6 +165,35 @@ def test_residuals_off_leaves_the_step_unchanged():
             assert torch.equal(a[key], b[key]), key
 
 
+@pytest.mark.parametrize("P,adapt", [(1, True), (2, True), (2, False)])
+def test_local_sync_is_bitwise_the_two_kernel_path(P, adapt, monkeypatch):
+    """One node (M == 1): hsx_local_sync (K6 + K7 in one pass, no compact buffer)
+    leaves u / v / z, the residual report and the penalties bitwise equal to
+    hsx_compact_dual_resid + hsx_decompact_dual_resid (HSX_LOCAL_SYNC=0)."""
+    import paper_2512_14628_b200 as H
+
+    ref = G.E2E(1, P, adapt=True)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("HSX_LOCAL_SYNC", flag)
+        _, cluster, engines = _engines(1, P, "nccl", adapt=adapt, golden=False)
+        for e in engines:
+            e.init_from(ref.p0())
+        got = []
+        for k in range(1, ref.iters + 1):
+            for e in engines:
+                e.load(theta=ref.theta(k, e.rank))
+            H.run_local(engines, k)
+            got.append([{key: getattr(e, key).clone() for key in ("u", "v", "z", "report")} for e in engines])
+            got[-1].append([e.current_schedule().rho1[n] for n in ref.names])
+        outs.append(got)
+    for k, (a, b) in enumerate(zip(*outs), 1):
+        assert a[-1] == b[-1], k
+        for ea, eb in zip(a[:-1], b[:-1]):
+            for key in ea:
+                assert torch.equal(ea[key], eb[key]), (k, key)
+
+
 # -- phase-1 boundary (SURVEY §8(f)2): the fused proximal-SGD step ----------------
 
 

@@ -17,7 +17,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   > gpurun_out/${TAG}_ncu_launch.log 2>&1
 echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:'k_candidate|k_compact|k_decompact|k_project|k_select|k_keep_sets' -c 6 \
+  -k regex:'k_candidate|k_local_sync|k_compact|k_decompact|k_project|k_select|k_keep_sets' -c 6 \
   -o gpurun_out/${TAG}_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
   > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu full rc=$?"

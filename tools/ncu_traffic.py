@@ -12,7 +12,8 @@ import sys
 
 NAMES = {"k_candidate": "K1_candidate", "k_project": "K3_project", "k_compact": "K6_compact_dual",
          "k_decompact": "K7_decompact_dual", "k_dual": "K6f_dual_intra", "k_add": "K0_pack_theta_u",
-         "k_select": "K2_select", "k_keep_fixup": "K5_keep_fixup", "k_keep_sets": "K5_keep_sets"}
+         "k_select": "K2_select", "k_keep_fixup": "K5_keep_fixup", "k_keep_sets": "K5_keep_sets",
+         "k_local_sync": "K67_local_sync"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 rep = sys.argv[1]

@@ -554,3 +554,135 @@ def cluster_sync(layers, states: list[RankState], thetas: list[dict], k: int,
                     _keep_sets(st, ly.name, st.masks[ly.name])
                 st.sealed = True
     return out
+
+
+# -- comparison baselines (baselines.py) ---------------------------
+
+
+@dataclass
+class FlatState:
+    """flat_consensus_program's per-run state (baselines.py:169-181): the global z,
+    every rank's u, the masks of the prunable layers, frozen, drift history."""
+    z: dict
+    u: list
+    masks: dict
+    frozen: bool = False
+    drift_history: list = field(default_factory=list)
+
+
+def init_flat_state(layers, params0, world) -> FlatState:
+    p = {n: np.asarray(a, dtype=np.float64).copy() for n, a in params0.items()}
+    return FlatState(z=p, u=[{n: np.zeros_like(a) for n, a in p.items()} for _ in range(world)],
+                     masks={ly.name: np.ones(ly.shape, dtype=bool) for ly in layers if ly.prunable})
+
+
+def flat_consensus_step(layers, st: FlatState, thetas: list[dict], k: int, sched: Schedule,
+                        weight_decay: float, t_freeze: int = 10, drift_window: int = 3,
+                        eps_abs: float = 1e-4, eps_rel: float = 1e-3, ledger: list | None = None):
+    """One iteration k of flat_consensus_program (baselines.py:184-287) after phase 1,
+    in place on ``st``: dense all-rank SUM of theta + u per layer (rank-order fold),
+    cand = rho1 * total / (wd + W rho1), projection of the global tensor (frozen:
+    cand * mask), u-update, the 3-slot residual SUM, the flat report, rho1 adaptation
+    with the u rescale, freeze check. Returns (report, r_intra per rank, drift_now)."""
+    world = len(thetas)
+    z_prev, z, drift_now = st.z, {}, {}
+
+    def log(op, elems, label):
+        if ledger is not None:
+            ledger.append({"iter": k, "group": "global", "scope": "global", "op": op,
+                           "elements": int(elems), "bytes": ELEMENT_BYTES * int(elems), "members": world,
+                           "label": label})
+
+    for ly in layers:
+        n = ly.name
+        total = thetas[0][n] + st.u[0][n]                                 # transport.py:453-462
+        for r in range(1, world):
+            total = total + (thetas[r][n] + st.u[r][n])
+        log("allreduce_sum", total.size, f"z_sync/{n}")
+        gamma = weight_decay + world * sched.rho1[n]                      # baselines.py:195
+        cand = (sched.rho1[n] * total) / gamma
+        if ly.prunable and st.frozen:
+            z[n] = cand * st.masks[n]
+        elif ly.prunable:
+            z[n] = project_composite(cand, ly.plan)
+            new = extract_mask(z[n])
+            drift_now[n] = mask_drift(st.masks[n], new)
+            st.masks[n] = new
+        else:
+            z[n] = cand
+    if drift_now:
+        st.drift_history.append(max(drift_now.values()))
+    st.u = [{n: st.u[r][n] + (thetas[r][n] - z[n]) for n in z} for r in range(world)]   # :210
+    names = [ly.name for ly in layers]
+    vecs, r_local = [], []
+    for r in range(world):
+        v3 = np.empty(len(names) * 3)
+        rl = {}
+        for li, n in enumerate(names):
+            d = thetas[r][n] - z[n]
+            rl[n] = math.sqrt(sq(d))
+            v3[li * 3:li * 3 + 3] = (sq(d), float(np.sum(thetas[r][n] ** 2)), float(np.sum(st.u[r][n] ** 2)))
+        vecs.append(v3)
+        r_local.append(rl)
+    sums = vecs[0].copy()
+    for r in range(1, world):
+        sums = sums + vecs[r]
+    log("allreduce_sum", sums.size, "res_flat")
+    per_layer = {}
+    r_pri_sq = r_dual_sq = eps_pri_sq = eps_dual_sq = 0.0
+    for li, ly in enumerate(layers):                                      # :230-254
+        n = ly.name
+        rho1 = sched.rho1[n]
+        nel = int(np.prod(ly.shape))
+        r = math.sqrt(sums[li * 3])
+        s = rho1 * math.sqrt(world * float(np.sum((z[n] - z_prev[n]) ** 2)))
+        eps_pri = math.sqrt(nel * world) * eps_abs + eps_rel * max(
+            math.sqrt(sums[li * 3 + 1]), math.sqrt(world * float(np.sum(z[n] ** 2))))
+        eps_dual = math.sqrt(nel * world) * eps_abs + eps_rel * rho1 * math.sqrt(sums[li * 3 + 2])
+        per_layer[n] = (r, s, 0.0, 0.0, eps_pri, eps_dual, 0.0, 0.0)
+        r_pri_sq += r * r
+        r_dual_sq += s * s
+        eps_pri_sq += eps_pri * eps_pri
+        eps_dual_sq += eps_dual * eps_dual
+    r_pri, r_dual = math.sqrt(r_pri_sq), math.sqrt(r_dual_sq)
+    eps_pri, eps_dual = math.sqrt(eps_pri_sq), math.sqrt(eps_dual_sq)
+    report = {"layers": per_layer, "r_pri": r_pri, "r_dual": r_dual, "eps_pri": eps_pri,
+              "eps_dual": eps_dual, "converged": r_pri <= eps_pri and r_dual <= eps_dual}
+    if sched.adapt:                                                       # :271-282 (rho1 only)
+        for n in names:
+            lr_ = per_layer[n]
+            old = sched.rho1[n]
+            if lr_[0] > sched.mu * lr_[1]:
+                sched.rho1[n] = min(old * sched.tau_inc, sched.rho1_max)
+            elif lr_[1] > sched.mu * lr_[0]:
+                sched.rho1[n] = old / sched.tau_dec
+            scale = old / sched.rho1[n] if sched.rho1[n] != old else 1.0
+            if scale != 1.0:
+                for r in range(world):
+                    st.u[r][n] = st.u[r][n] * scale
+    st.z = z
+    if not st.frozen and any(ly.prunable for ly in layers):               # :284-286
+        if freeze_check(k, t_freeze, st.drift_history, drift_window):
+            st.frozen = True
+    return report, r_local, drift_now
+
+
+def dense_sync_step(params: dict, velocity: dict, grads: list[dict], lr: float, momentum: float,
+                    weight_decay: float, ledger: list | None = None, step: int = 0):
+    """One step of dense_sync_program (baselines.py:86-96), in place on params / velocity:
+    per layer g_r = grad_r + wd * params, AVG over ranks (rank-order fold, / W),
+    velocity = momentum * velocity + avg, params -= lr * velocity."""
+    world = len(grads)
+    avg = {}
+    for n in params:
+        acc = grads[0][n] + weight_decay * params[n]
+        for r in range(1, world):
+            acc = acc + (grads[r][n] + weight_decay * params[n])
+        avg[n] = acc / float(world)
+        if ledger is not None:
+            ledger.append({"iter": step, "group": "global", "scope": "global", "op": "allreduce_avg",
+                           "elements": int(acc.size), "bytes": ELEMENT_BYTES * int(acc.size),
+                           "members": world, "label": f"grad/{n}"})
+    for n in params:
+        velocity[n] = momentum * velocity[n] + avg[n]
+        params[n] -= lr * velocity[n]

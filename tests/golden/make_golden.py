@@ -303,6 +303,139 @@ def gen_prox(seed=5):
     np.savez_compressed(os.path.join(HERE, "prox_sgd.npz"), **fx)
 
 
+# -- comparison baselines (baselines.py) ---------------------------
+
+
+def _spy(gen, on_yield):
+    """Drive ``gen`` transparently; on_yield(gen, request) sees every request while the
+    generator is suspended at it (its frame locals are the program state)."""
+    try:
+        req = next(gen)
+        while True:
+            on_yield(gen, req)
+            try:
+                res = yield req
+            except BaseException as exc:        # noqa: BLE001 — forward into the program
+                req = gen.throw(exc)
+                continue
+            req = gen.send(res)
+    except StopIteration as stop:
+        return stop.value
+
+
+def gen_flat(world, adapt, seed=3):
+    """run_flat_consensus (baselines.py:151-293) with phase 1 replaced by recorded thetas.
+    The state after iteration k (z, u post-rescale, masks, frozen, rho1) is read from the
+    program's frame at the first collective of iteration k + 1; the report / drift / r_intra
+    from the trace rows; the ledger per iteration."""
+    import admmprune.baselines as ref_base
+
+    rng = np.random.default_rng([seed, 778, world, int(adapt)])
+    specs = [LayerSpec(n, kind, shape, prunable=bool(c)) for n, kind, shape, c in E2E_LAYERS]
+    constraints = {n: [SparsityConstraint(KINDS[k], keep_rate=r) for k, r in c]
+                   for n, _, _, c in E2E_LAYERS if c}
+    names = [ls.name for ls in specs]
+    params0 = {}
+    for ls in specs:
+        t = rng.normal(0.0, 0.5, size=ls.shape)
+        if ls.kind is LayerKind.CONV:
+            t = t * rng.uniform(0.2, 1.0, size=(1, ls.shape[1], 1, 1))
+        params0[ls.name] = f32(t)
+    iters = E2E_ITERS
+    thetas = {(r, k): {n: f32(params0[n] + rng.normal(0, 0.05, size=params0[n].shape)) for n in names}
+              for k in range(1, iters + 2) for r in range(world)}
+    sched = PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=adapt)
+    settings = ConsensusSettings(iterations=iters + 1, t_freeze=E2E_T_FREEZE, stop_on_convergence=False,
+                                 weight_decay=1e-4, seed=seed)
+    out = {"meta": np.array([world, iters, E2E_T_FREEZE, int(adapt)])}
+    for n in names:
+        out[f"p0/{n}"] = params0[n].astype(np.float32)
+        for k in range(1, iters + 1):
+            for r in range(world):
+                out[f"theta/{k}/{r}/{n}"] = thetas[(r, k)][n].astype(np.float32)
+
+    def capture(rank):
+        def on_yield(gen, req):
+            if req.tag != f"z_sync/{names[0]}" or req.iteration < 2:
+                return
+            k, f = req.iteration - 1, gen.gi_frame.f_locals
+            for n in names:
+                out[f"z/{k}/{rank}/{n}"] = f["z_prev"][n].copy()
+                out[f"u/{k}/{rank}/{n}"] = f["u"][n].copy()
+            for n, m in f["masks"].items():
+                out[f"mask/{k}/{rank}/{n}"] = m.copy()
+            out[f"frozen/{k}/{rank}"] = np.array(f["frozen"])
+            out[f"rho1_after/{k}/{rank}"] = np.array([f["sched"].rho1[n] for n in names])
+        return on_yield
+
+    saved = (ref_base.batch_rng, ref_base.proximal_sgd)
+    try:
+        ref_base.batch_rng = lambda s, rank, k: (rank, k)
+        ref_base.proximal_sgd = lambda wl, shard, th, z, u, rho1, solver, key: {
+            n: a.copy() for n, a in thetas[key].items()}
+        cluster = Cluster(Topology(1, world))
+        wl = _FixedWorkload(specs, params0, world)
+        progs = {r: _spy(ref_base.flat_consensus_program(r, cluster, wl, constraints, sched, SolverConfig(),
+                                                          settings), capture(r))
+                 for r in range(world)}
+        res = cluster.run(progs)
+    finally:
+        ref_base.batch_rng, ref_base.proximal_sgd = saved
+    for row in res[0].trace[:iters]:
+        k = row["k"]
+        out[f"report/{k}"] = ref_consensus.pack_report(row["report"], names)
+        out[f"rho1/{k}"] = np.array([row["rho1"][n] for n in names])
+        out[f"drift/{k}"] = np.array(json.dumps(row["drift"]))
+        out[f"popcount/{k}"] = np.array(json.dumps(row["mask_popcount"]))
+    for r in range(world):
+        for row in res[r].trace[:iters]:
+            out[f"r_intra/{row['k']}/{r}"] = np.array([row["r_intra"][n] for n in names])
+    for k in range(1, iters + 1):
+        out[f"ledger/{k}"] = np.array(json.dumps([e.to_dict() for e in cluster.ledger.entries
+                                                   if e.iteration == k]))
+    np.savez_compressed(os.path.join(HERE, f"flat_{'adapt_' if adapt else ''}{world}.npz"), **out)
+
+
+DENSE_STEPS = 4
+
+
+def gen_dense(world, seed=3):
+    """run_dense_sync (baselines.py:77-98, 260-266) with a stub workload whose
+    loss_and_grad returns recorded per-rank gradients: pins the all-rank gradient AVG
+    (weight decay folded in), momentum and lr, and the bit-identical parameters."""
+    import admmprune.baselines as ref_base
+    from admmprune.workloads import Shard
+
+    rng = np.random.default_rng([seed, 779, world])
+    specs = [LayerSpec(n, kind, shape, prunable=False) for n, kind, shape, _ in E2E_LAYERS]
+    names = [ls.name for ls in specs]
+    params0 = {ls.name: f32(rng.normal(0.0, 0.5, size=ls.shape)) for ls in specs}
+    grads = {(r, s): {n: f32(rng.normal(0, 0.1, size=params0[n].shape)) for n in names}
+             for s in range(1, DENSE_STEPS + 1) for r in range(world)}
+    calls = {r: 0 for r in range(world)}
+
+    class _Stub(_FixedWorkload):
+        def loss_and_grad(self, params, features, targets):
+            r = int(features[0, 0])
+            calls[r] += 1
+            return float(r), {n: g.copy() for n, g in grads[(r, calls[r])].items()}
+
+    wl = _Stub(specs, params0, world)
+    wl.shards = [Shard(np.full((8, 1), float(r)), np.zeros(8)) for r in range(world)]
+    solver = SolverConfig(lr=0.05, momentum=0.9, weight_decay=1e-4, batch_size=4)
+    cluster = Cluster(Topology(1, world))
+    res = ref_base.run_dense_sync(cluster, wl, solver, DENSE_STEPS, seed)
+    out = {"meta": np.array([world, DENSE_STEPS]), "solver": np.array([solver.lr, solver.momentum,
+                                                                       solver.weight_decay])}
+    for n in names:
+        out[f"p0/{n}"] = params0[n].astype(np.float32)
+        out[f"out/{n}"] = res[0].params[n]
+        for (r, s), g in grads.items():
+            out[f"g/{s}/{r}/{n}"] = g[n].astype(np.float32)
+    out["ledger"] = np.array(json.dumps([e.to_dict() for e in cluster.ledger.entries]))
+    np.savez_compressed(os.path.join(HERE, f"dense_{world}.npz"), **out)
+
+
 if __name__ == "__main__":
     gen_projection()
     gen_shrinkage()
@@ -313,4 +446,8 @@ if __name__ == "__main__":
     for m, p in [(1, 1), (2, 1), (1, 2), (2, 2)]:
         gen_e2e(m, p, adapt=True)
     gen_prox()
+    gen_flat(2, False)
+    for w in (1, 2, 4):
+        gen_flat(w, True)
+        gen_dense(w)
     print("golden fixtures written to", HERE)

@@ -124,3 +124,75 @@ def prox_case():
     return dict(names=names, lr=float(lr), momentum=float(mom), rho1=dict(zip(names, d["rho1"].tolist())),
                 w0=f64("w0"), z=f64("z"), u=f64("u"), out={n: d[f"out/{n}"] for n in names},
                 grads=[{n: d[f"g/{i}/{n}"].astype(np.float64) for n in names} for i in range(int(steps))])
+
+
+FLAT_CASES = [(2, False), (1, True), (2, True), (4, True)]   # (world, adapt)
+DENSE_WORLDS = [1, 2, 4]
+
+
+class Flat:
+    """run_flat_consensus (baselines.py:151-293) with phase 1 replaced (make_golden.gen_flat):
+    state after iteration k per rank (z, u post-rescale, masks, frozen, rho1 after
+    adaptation), rank 0's report / rho1 / drift / mask popcounts, each rank's r_intra,
+    the ledger of every iteration."""
+
+    def __init__(self, world, adapt):
+        self.d = load(f"flat_{'adapt_' if adapt else ''}{world}.npz")
+        self.world, self.iters, self.t_freeze, adapt_ = (int(x) for x in self.d["meta"])
+        self.adapt = bool(adapt_)
+        self.names = [n for n, *_ in E2E_LAYERS]
+
+    def p0(self):
+        return {n: self.d[f"p0/{n}"].astype(np.float64) for n in self.names}
+
+    def theta(self, k, r):
+        return {n: self.d[f"theta/{k}/{r}/{n}"].astype(np.float64) for n in self.names}
+
+    def state(self, key, k, r):
+        return {n: self.d[f"{key}/{k}/{r}/{n}"] for n in self.names}
+
+    def masks(self, k, r):
+        return {n: self.d[f"mask/{k}/{r}/{n}"] for n, _, _, c in E2E_LAYERS if c}
+
+    def frozen(self, k):
+        return bool(self.d[f"frozen/{k}/0"])
+
+    def report(self, k):
+        return self.d[f"report/{k}"]
+
+    def rho1(self, k):
+        return self.d[f"rho1/{k}"]
+
+    def rho1_after(self, k):
+        return self.d[f"rho1_after/{k}/0"]
+
+    def r_intra(self, k, r):
+        return self.d[f"r_intra/{k}/{r}"]
+
+    def drift(self, k):
+        return json.loads(str(self.d[f"drift/{k}"]))
+
+    def ledger(self, k):
+        return json.loads(str(self.d[f"ledger/{k}"]))
+
+
+class Dense:
+    """run_dense_sync (baselines.py:77-98) with recorded per-rank gradients (make_golden.gen_dense)."""
+
+    def __init__(self, world):
+        self.d = load(f"dense_{world}.npz")
+        self.world, self.steps = (int(x) for x in self.d["meta"])
+        self.lr, self.momentum, self.weight_decay = (float(x) for x in self.d["solver"])
+        self.names = [n for n, *_ in E2E_LAYERS]
+
+    def p0(self):
+        return {n: self.d[f"p0/{n}"].astype(np.float64) for n in self.names}
+
+    def grads(self, s, r):
+        return {n: self.d[f"g/{s}/{r}/{n}"].astype(np.float64) for n in self.names}
+
+    def out(self):
+        return {n: self.d[f"out/{n}"] for n in self.names}
+
+    def ledger(self):
+        return json.loads(str(self.d["ledger"]))

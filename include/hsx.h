@@ -235,6 +235,11 @@ typedef struct hsx_resid_params {
   double weight_decay, eps_abs, eps_rel;          /* ConsensusSettings (consensus.py:94-110) */
   double mu, tau_inc, tau_dec, rho1_max, rho2_max; /* PenaltySchedule (consensus.py:42-69) */
   int32_t num_nodes, accels_per_node, adapt;
+  /* flat != 0: flat_consensus_program's report (baselines.py:229-254) on a one-node
+   * (1 x W) plan with rho2 = 0 and v = 0: the per-layer intra entries as for one node
+   * (z == z_node, so (z_node - z_node_prev)^2 is (z - z_prev)^2 and z_node^2 is z^2),
+   * the inter entries 0; adaptation then moves rho1 only. */
+  int32_t flat;
 } hsx_resid_params;
 /* K6 + residual slots 0-2 per layer: (theta - z_node)^2, theta^2, u'^2
  * (consensus.py:541-545). flat == NULL: the intra dual alone (followers). */
@@ -273,6 +278,19 @@ int hsx_scale_duals(const hsx_plan* plan, const double* scales, float* u, float*
 int hsx_prox_sgd_step(const hsx_plan* plan, const float* grad, float* theta, const float* z_node,
                       const float* u, float* velocity, double lr, double momentum, int32_t first,
                       float* send, void* stream);
+/* Dense synchronous SGD baseline (dense_sync_program, baselines.py:77-98), flat fp32
+ * arenas of n elements, fp64 math:
+ *   send = grad + weight_decay * params                          (:88)
+ * then, after the all-rank exchange, with avg = (sum_j sends[j], in order) / divisor:
+ *   velocity = momentum * velocity + avg (first != 0: velocity starts at 0, :82);
+ *   params -= lr * velocity                                       (:90-92)
+ * n_sends == 1, divisor 1: sends[0] is the NCCL-averaged buffer; n_sends == W,
+ * divisor W: sends are the W ranks' peer-mapped send buffers (NVLink), the AVG fused
+ * into the update. HSX_ECONFIG if lr <= 0 (workloads.py:46-47). */
+int hsx_dense_grad_pack(const float* grad, const float* params, double weight_decay, float* send, int64_t n,
+                        void* stream);
+int hsx_dense_apply(const float* const* sends, int32_t n_sends, double divisor, float* params, float* velocity,
+                    double lr, double momentum, int32_t first, int64_t n, void* stream);
 /* Current per-layer penalties (after device-side adaptation); synchronous. */
 int hsx_plan_read_penalties(hsx_plan* plan, double* rho1, double* rho2);
 

@@ -38,7 +38,8 @@ class ResidParams(C.Structure):
     _fields_ = [("weight_decay", C.c_double), ("eps_abs", C.c_double), ("eps_rel", C.c_double),
                 ("mu", C.c_double), ("tau_inc", C.c_double), ("tau_dec", C.c_double),
                 ("rho1_max", C.c_double), ("rho2_max", C.c_double),
-                ("num_nodes", C.c_int32), ("accels_per_node", C.c_int32), ("adapt", C.c_int32)]
+                ("num_nodes", C.c_int32), ("accels_per_node", C.c_int32), ("adapt", C.c_int32),
+                ("flat", C.c_int32)]
 
 # name -> (restype, argtypes); every int-returning entry point is error-checked
 SIGNATURES = {
@@ -85,6 +86,8 @@ SIGNATURES = {
     "hsx_residual_report": (C.c_int, [P, VP, VP, VP, C.POINTER(ResidParams), VP]),
     "hsx_scale_duals": (C.c_int, [P, VP, VP, VP, VP]),
     "hsx_plan_read_penalties": (C.c_int, [P, VP, VP]),
+    "hsx_dense_grad_pack": (C.c_int, [VP, VP, F64, VP, C.c_int64, VP]),
+    "hsx_dense_apply": (C.c_int, [VP, I32, F64, VP, VP, F64, F64, I32, C.c_int64, VP]),
     "hsx_prox_sgd_step": (C.c_int, [P, VP, VP, VP, VP, VP, F64, F64, I32, VP, VP]),
     "hsx_nonzero_u8": (C.c_int, [VP, I64, VP, VP]),
     "hsx_pack_bits": (C.c_int, [VP, I64, VP, VP]),

@@ -1005,6 +1005,7 @@ int hsx_residual_report(hsx_plan* p, const double* global, double* report, doubl
   a.num_nodes = prm->num_nodes;
   a.per_node = prm->accels_per_node;
   a.adapt = prm->adapt ? 1 : 0;
+  a.flat = prm->flat ? 1 : 0;
   hsx::launch_report(a, S(stream));
   HSX_LAUNCHED("residual_report");
   return HSX_OK;
@@ -1026,6 +1027,38 @@ int hsx_prox_sgd_step(const hsx_plan* p, const float* grad, float* theta, const 
   hsx::launch_prox_sgd(p->d_layers, p->d_elem, (int)p->elem_items.size(), grad, theta, z_node, u, velocity, send, lr,
                        momentum, first ? 1 : 0, S(stream));
   HSX_LAUNCHED("prox_sgd_step");
+  return HSX_OK;
+}
+
+int hsx_dense_grad_pack(const float* grad, const float* params, double weight_decay, float* send, int64_t n,
+                        void* stream) {
+  if (n < 0) return fail(HSX_EINVAL, "negative element count");
+  if (n && (!grad || !params || !send)) return fail(HSX_EINVAL, "null argument");
+  if ((reinterpret_cast<uintptr_t>(grad) | reinterpret_cast<uintptr_t>(params) | reinterpret_cast<uintptr_t>(send)) & 15)
+    return fail(HSX_EINVAL, "buffers must be 16-byte aligned");
+  hsx::launch_dense_pack(grad, params, weight_decay, send, n, S(stream));
+  HSX_LAUNCHED("dense_grad_pack");
+  return HSX_OK;
+}
+
+int hsx_dense_apply(const float* const* sends, int32_t n_sends, double divisor, float* params, float* velocity,
+                    double lr, double momentum, int32_t first, int64_t n, void* stream) {
+  if (n < 0) return fail(HSX_EINVAL, "negative element count");
+  if (!sends || !params || !velocity) return fail(HSX_EINVAL, "null argument");
+  if (n_sends < 1 || n_sends > hsx::kMaxPeers)
+    return fail(HSX_EINVAL, "peer count %d outside [1, %d]", n_sends, hsx::kMaxPeers);
+  if (!(divisor > 0.0)) return fail(HSX_EINVAL, "divisor must be positive");
+  if (!(lr > 0.0)) return fail(HSX_ECONFIG, "learning rate must be positive, got %g", lr);
+  hsx::PeerPtrs src;
+  src.n = n_sends;
+  for (int j = 0; j < n_sends; ++j) {
+    if (!sends[j] || (reinterpret_cast<uintptr_t>(sends[j]) & 15)) return fail(HSX_EINVAL, "send pointer %d null or unaligned", j);
+    src.p[j] = sends[j];
+  }
+  if ((reinterpret_cast<uintptr_t>(params) | reinterpret_cast<uintptr_t>(velocity)) & 15)
+    return fail(HSX_EINVAL, "buffers must be 16-byte aligned");
+  hsx::launch_dense_apply(src, divisor, params, velocity, lr, momentum, first ? 1 : 0, n, S(stream));
+  HSX_LAUNCHED("dense_apply");
   return HSX_OK;
 }
 

@@ -2240,6 +2240,7 @@ __global__ void __launch_bounds__(512) k_report(ResidArgs a) {
       rp[5] = __dadd_rn(e_i, __dmul_rn(__dmul_rn(a.eps_rel, ly.rho1), sqrt(g[2])));
       rp[6] = __dadd_rn(e_o, __dmul_rn(a.eps_rel, fmax(sqrt(g[5]), sqrt(g[8]))));
       rp[7] = __dadd_rn(e_o, __dmul_rn(__dmul_rn(a.eps_rel, ly.rho2), sqrt(g[6])));
+      if (a.flat) rp[2] = rp[3] = rp[6] = rp[7] = 0.0;  // baselines.py:249 (no inter level)
     }
   }
   __syncthreads();
@@ -2640,6 +2641,90 @@ void launch_prox_sgd(const DevLayer* layers, const Item* items, int n_items, con
                      cudaStream_t st) {
   if (n_items <= 0) return;
   launch_pdl(k_prox_sgd, n_items, kThreads, 0, st, layers, items, g, th, zn, u, vel, send, lr, mom, first);
+}
+
+// ---------------------------------------------------------------------------
+// Dense synchronous SGD baseline (baselines.py:77-98): per step every rank packs
+// g = grad + wd * params (fp64 math, :88), the all-rank AVG, then velocity =
+// momentum * velocity + avg, params -= lr * velocity (:90-92). Flat arena-wide
+// float4 grid-stride kernels (HBM-bound: 12 B / 16 B per element + 4 B per peer).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ float dense_g(float g, float p, double wd) {
+  return (float)__dadd_rn((double)g, __dmul_rn(wd, (double)p));
+}
+
+__device__ __forceinline__ void dense_upd(double avg, float& p, float& v, double lr, double mom, int first) {
+  const double vn = first ? __dadd_rn(0.0, avg) : __dadd_rn(__dmul_rn(mom, (double)v), avg);
+  v = (float)vn;
+  p = (float)__dsub_rn((double)p, __dmul_rn(lr, vn));
+}
+
+__global__ void __launch_bounds__(kThreads) k_dense_pack(const float* __restrict__ g, const float* __restrict__ p,
+                                                         double wd, float* __restrict__ send, long long n) {
+  PDL_ENTRY();
+  const long long n4 = n >> 2, stride = (long long)gridDim.x * kThreads;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n4; i += stride) {
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(g) + i), b = reinterpret_cast<const float4*>(p)[i];
+    __stcg(reinterpret_cast<float4*>(send) + i,
+           make_float4(dense_g(a.x, b.x, wd), dense_g(a.y, b.y, wd), dense_g(a.z, b.z, wd), dense_g(a.w, b.w, wd)));
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += stride)
+    send[i] = dense_g(g[i], p[i], wd);
+}
+
+// avg = (sum_j src_j, rank order, fp64) / div over the peers' send buffers (the
+// all-rank AVG fused with the update: one pass, no reduced buffer); n_peers == 1
+// with div == 1 applies an already averaged buffer (the NCCL path)
+__global__ void __launch_bounds__(kThreads) k_dense_apply(PeerPtrs src, double div, float* __restrict__ p,
+                                                          float* __restrict__ v, double lr, double mom, int first,
+                                                          long long n) {
+  PDL_ENTRY();
+  const long long n4 = n >> 2, stride = (long long)gridDim.x * kThreads;
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n4; i += stride) {
+    float4 x[kMaxPeers];
+#pragma unroll
+    for (int j = 0; j < kMaxPeers; ++j)
+      if (j < src.n) x[j] = __ldcg(reinterpret_cast<const float4*>(src.p[j]) + i);
+    double s0 = x[0].x, s1 = x[0].y, s2 = x[0].z, s3 = x[0].w;
+#pragma unroll
+    for (int j = 1; j < kMaxPeers; ++j) {
+      if (j >= src.n) break;
+      s0 = __dadd_rn(s0, (double)x[j].x); s1 = __dadd_rn(s1, (double)x[j].y);
+      s2 = __dadd_rn(s2, (double)x[j].z); s3 = __dadd_rn(s3, (double)x[j].w);
+    }
+    float4 pp = reinterpret_cast<float4*>(p)[i], vv = first ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                            : reinterpret_cast<float4*>(v)[i];
+    dense_upd(__ddiv_rn(s0, div), pp.x, vv.x, lr, mom, first);
+    dense_upd(__ddiv_rn(s1, div), pp.y, vv.y, lr, mom, first);
+    dense_upd(__ddiv_rn(s2, div), pp.z, vv.z, lr, mom, first);
+    dense_upd(__ddiv_rn(s3, div), pp.w, vv.w, lr, mom, first);
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(v)[i] = vv;
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += stride) {
+    double s = src.p[0][i];
+    for (int j = 1; j < src.n; ++j) s = __dadd_rn(s, (double)src.p[j][i]);
+    float pp = p[i], vv = first ? 0.f : v[i];
+    dense_upd(__ddiv_rn(s, div), pp, vv, lr, mom, first);
+    p[i] = pp;
+    v[i] = vv;
+  }
+}
+
+static int dense_grid(long long n) {
+  return (int)std::min<long long>(std::max<long long>((n / 4 + kThreads - 1) / kThreads, 1), 148LL * 8);
+}
+
+void launch_dense_pack(const float* g, const float* p, double wd, float* send, long long n, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_pdl(k_dense_pack, dense_grid(n), kThreads, 0, st, g, p, wd, send, n);
+}
+
+void launch_dense_apply(const PeerPtrs& src, double div, float* p, float* v, double lr, double mom, int first,
+                        long long n, cudaStream_t st) {
+  if (n <= 0 || src.n <= 0) return;
+  launch_pdl(k_dense_apply, dense_grid(n), kThreads, 0, st, src, div, p, v, lr, mom, first, n);
 }
 }  // namespace hsx
 

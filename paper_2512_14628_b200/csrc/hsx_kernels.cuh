@@ -203,10 +203,13 @@ struct ResidArgs {
   double* report;                       // [layer][8] + 5 (consensus.py:291-300 layout)
   double* scales;                       // [2][layer]: u scale, v scale
   double wd, eps_abs, eps_rel, mu, tau_inc, tau_dec, rho1_max, rho2_max;
-  int num_nodes, per_node, adapt;
+  int num_nodes, per_node, adapt, flat;
 };
 void launch_resid_fold(const ResidArgs& a, cudaStream_t st);
 void launch_report(const ResidArgs& a, cudaStream_t st);
+void launch_dense_pack(const float* g, const float* p, double wd, float* send, long long n, cudaStream_t st);
+void launch_dense_apply(const PeerPtrs& src, double div, float* p, float* v, double lr, double mom, int first,
+                        long long n, cudaStream_t st);
 void launch_prox_sgd(const DevLayer* layers, const Item* items, int n_items, const float* g, float* th,
                      const float* zn, const float* u, float* vel, float* send, double lr, double mom, int first,
                      cudaStream_t st);

@@ -135,6 +135,58 @@ def replica_check(topo, rank, world, transport):
     return ratio
 
 
+def baselines_check(topo, rank, world, transport):
+    """Flat consensus and dense sync (baselines.py) over the real collectives: the
+    run_flat_consensus(adapt) / run_dense_sync goldens for W ranks, any topology."""
+    if world in [w for w, adapt in G.FLAT_CASES if adapt]:
+        ref = G.Flat(world, True)
+        kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
+                 "shape": H.ConstraintKind.SHAPE_KEEP}
+        layers = [H.LayerSpec(n, H.LayerKind.CONV if k == "conv" else H.LayerKind.FULLY_CONNECTED, s,
+                              prunable=bool(c)) for n, k, s, c in G.E2E_LAYERS]
+        cons = {n: [H.SparsityConstraint(kinds[g], keep_rate=r) for g, r in c] for n, _, _, c in G.E2E_LAYERS if c}
+        sched = H.PenaltySchedule.uniform(ref.names, G.E2E_RHO1, G.E2E_RHO2, adapt=True)
+        settings = H.ConsensusSettings(t_freeze=ref.t_freeze, weight_decay=G.E2E_WD)
+        eng = H.FlatConsensusSync(rank, H.DistCluster(topo), layers, cons, sched, settings, transport=transport)
+        eng.init_from(ref.p0())
+        for k in range(1, ref.iters + 1):
+            assert [eng.current_schedule().rho1[n] for n in ref.names] == list(ref.rho1(k)), k
+            th = ref.theta(k, rank)
+            eng.load(theta=th)
+            eng.step(k)
+            rep = eng.last_report()
+            assert float(rep.converged) == ref.report(k)[-1], k
+            assert abs(rep.r_pri - ref.report(k)[-5]) <= TOL * ref.report(k)[-5], k
+            for key in ("z", "u"):
+                w = ref.state(key, k, rank)
+                for n, t in eng.views(key).items():
+                    err = rel_err(t.cpu().numpy(), w[n], th[n])
+                    assert err <= TOL, ("flat", k, rank, key, n, err)
+            for n, m in ref.masks(k, rank).items():
+                assert np.array_equal(eng.mask_dict()[n].cpu().numpy(), m), (k, rank, n)
+    if world in G.DENSE_WORLDS:
+        ref = G.Dense(world)
+        layers = [H.LayerSpec(n, H.LayerKind.CONV if k == "conv" else H.LayerKind.FULLY_CONNECTED, s)
+                  for n, k, s, _ in G.E2E_LAYERS]
+
+        class Solver:
+            lr, momentum, weight_decay = ref.lr, ref.momentum, ref.weight_decay
+
+        eng = H.DenseSync(rank, H.DistCluster(topo), layers, Solver, transport=transport)
+        eng.init_from(ref.p0())
+        for s in range(1, ref.steps + 1):
+            eng.load_grads(ref.grads(s, rank))
+            eng.step(s)
+        out = ref.out()
+        for n, t in eng.views("params").items():
+            err = rel_err(t.cpu().numpy(), out[n], ref.p0()[n])
+            assert err <= TOL, ("dense", rank, n, err)
+        buf = [torch.empty_like(eng.params) for _ in range(world)]
+        dist.all_gather(buf, eng.params)
+        assert all(torch.equal(b, eng.params) for b in buf), "dense params diverged across ranks"
+    return True
+
+
 def main():
     import faulthandler
 
@@ -150,6 +202,8 @@ def main():
             if (topo.num_nodes, topo.accels_per_node) in G.E2E_ADAPT_TOPOLOGIES:
                 adaptive_check(topo, rank, transport)
                 print(f"rank {rank} adaptive {transport} done", file=sys.stderr, flush=True)
+            baselines_check(topo, rank, world, transport)
+            print(f"rank {rank} baselines {transport} done", file=sys.stderr, flush=True)
             ratio = replica_check(topo, rank, world, transport)
             dist.barrier()
             if rank == 0:

@@ -686,3 +686,51 @@ def dense_sync_step(params: dict, velocity: dict, grads: list[dict], lr: float, 
     for n in params:
         velocity[n] = momentum * velocity[n] + avg[n]
         params[n] -= lr * velocity[n]
+
+
+def topk_keep_count(rate: float, size: int) -> int:
+    return max(1, math.ceil(rate * size))                                 # baselines.py:132
+
+
+def topk_select(flat: np.ndarray, k: int) -> np.ndarray:
+    """Indices of the k largest |values|, ties toward lower indices, ascending
+    (baselines.py:71-74: stable argsort of -|x|)."""
+    order = np.argsort(-np.abs(flat), kind="stable")
+    return np.sort(order[:k])
+
+
+def topk_step(params: dict, velocity: dict, residual: list, grads: list[dict], rate: float, lr: float,
+              momentum: float, weight_decay: float, ledger: list | None = None, step: int = 0):
+    """One step of topk_program (baselines.py:124-146) for every rank, in place on
+    params / velocity (shared: bit-identical on every rank) and residual[r]: acc =
+    residual + grad + wd * params; rank r ships the top-k (value, index) pairs; the
+    all-gathered pairs are scatter-added in rank order and / W; the untransmitted
+    entries stay in the residual. Returns the selected indices per rank and layer."""
+    world = len(grads)
+    avg, sels = {}, [{} for _ in range(world)]
+    for n in params:
+        payloads = []
+        for r in range(world):
+            g = grads[r][n] + weight_decay * params[n]
+            acc = residual[r][n] + g
+            flat = acc.ravel()
+            k = topk_keep_count(rate, flat.size)
+            sel = topk_select(flat, k)
+            sels[r][n] = sel
+            payloads.append((flat[sel], sel, k))
+            kept = np.zeros_like(flat)
+            kept[sel] = flat[sel]
+            residual[r][n] = (flat - kept).reshape(acc.shape)
+        if ledger is not None:
+            k = payloads[0][2]
+            ledger.append({"iter": step, "group": "global", "scope": "global", "op": "allgather",
+                           "elements": 2 * k, "bytes": ELEMENT_BYTES * 2 * k, "members": world,
+                           "label": f"topk/{n}"})
+        dense = np.zeros(params[n].size)
+        for values, indices, _ in payloads:                               # :137-139
+            dense[indices] += values
+        avg[n] = (dense / float(world)).reshape(params[n].shape)
+    for n in params:
+        velocity[n] = momentum * velocity[n] + avg[n]
+        params[n] -= lr * velocity[n]
+    return sels

@@ -436,6 +436,62 @@ def gen_dense(world, seed=3):
     np.savez_compressed(os.path.join(HERE, f"dense_{world}.npz"), **out)
 
 
+TOPK_RATE = 0.1
+
+
+def gen_topk(world, rate=TOPK_RATE, seed=3):
+    """run_topk (baselines.py:101-148, 269-275) with recorded per-rank gradients: the
+    final parameters, every rank's selected indices per step and layer (read from the
+    program frame at its all-gather), the ledger. Layer fc.b starts at zero with
+    gradients of equal magnitude (exact ties: the lower index must win)."""
+    import admmprune.baselines as ref_base
+    from admmprune.workloads import Shard
+
+    rng = np.random.default_rng([seed, 780, world])
+    specs = [LayerSpec(n, kind, shape, prunable=False) for n, kind, shape, _ in E2E_LAYERS]
+    names = [ls.name for ls in specs]
+    params0 = {ls.name: f32(rng.normal(0.0, 0.5, size=ls.shape)) for ls in specs}
+    params0["fc.b"][:] = 0.0
+    grads = {}
+    for s in range(1, DENSE_STEPS + 1):
+        for r in range(world):
+            g = {n: f32(rng.normal(0, 0.1, size=params0[n].shape)) for n in names}
+            g["fc.b"] = f32(rng.choice([-0.25, 0.25, 0.5, -0.5], size=params0["fc.b"].shape))
+            grads[(r, s)] = g
+    calls = {r: 0 for r in range(world)}
+
+    class _Stub(_FixedWorkload):
+        def loss_and_grad(self, params, features, targets):
+            r = int(features[0, 0])
+            calls[r] += 1
+            return float(r), {n: g.copy() for n, g in grads[(r, calls[r])].items()}
+
+    wl = _Stub(specs, params0, world)
+    wl.shards = [Shard(np.full((8, 1), float(r)), np.zeros(8)) for r in range(world)]
+    solver = SolverConfig(lr=0.05, momentum=0.9, weight_decay=1e-4, batch_size=4)
+    cluster = Cluster(Topology(1, world))
+    out = {"meta": np.array([world, DENSE_STEPS]), "solver": np.array([solver.lr, solver.momentum,
+                                                                       solver.weight_decay, rate])}
+
+    def capture(rank):
+        def on_yield(gen, req):
+            f = gen.gi_frame.f_locals
+            out[f"sel/{req.iteration}/{rank}/{f['n']}"] = np.asarray(f["sel"], dtype=np.int64)
+        return on_yield
+
+    progs = {r: _spy(ref_base.topk_program(r, cluster, wl, solver, DENSE_STEPS, seed, rate), capture(r))
+             for r in range(world)}
+    res = cluster.run(progs)
+    ref_base._check_divergence(res)
+    for n in names:
+        out[f"p0/{n}"] = params0[n].astype(np.float32)
+        out[f"out/{n}"] = res[0].params[n]
+        for (r, s), g in grads.items():
+            out[f"g/{s}/{r}/{n}"] = g[n].astype(np.float32)
+    out["ledger"] = np.array(json.dumps([e.to_dict() for e in cluster.ledger.entries]))
+    np.savez_compressed(os.path.join(HERE, f"topk_{world}.npz"), **out)
+
+
 if __name__ == "__main__":
     gen_projection()
     gen_shrinkage()
@@ -450,4 +506,5 @@ if __name__ == "__main__":
     for w in (1, 2, 4):
         gen_flat(w, True)
         gen_dense(w)
+        gen_topk(w)
     print("golden fixtures written to", HERE)

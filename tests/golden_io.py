@@ -196,3 +196,17 @@ class Dense:
 
     def ledger(self):
         return json.loads(str(self.d["ledger"]))
+
+
+class TopK(Dense):
+    """run_topk (baselines.py:101-148) with recorded gradients (make_golden.gen_topk):
+    also every rank's selected indices per step and layer."""
+
+    def __init__(self, world):
+        self.d = load(f"topk_{world}.npz")
+        self.world, self.steps = (int(x) for x in self.d["meta"])
+        self.lr, self.momentum, self.weight_decay, self.rate = (float(x) for x in self.d["solver"])
+        self.names = [n for n, *_ in E2E_LAYERS]
+
+    def sel(self, s, r, n):
+        return self.d[f"sel/{s}/{r}/{n}"]

@@ -291,6 +291,27 @@ int hsx_dense_grad_pack(const float* grad, const float* params, double weight_de
                         void* stream);
 int hsx_dense_apply(const float* const* sends, int32_t n_sends, double divisor, float* params, float* velocity,
                     double lr, double momentum, int32_t first, int64_t n, void* stream);
+/* Top-K gradient compression with error feedback (topk_program, baselines.py:101-148).
+ * A selector over layers at arena offsets[l] with elements[l] elements keeps
+ * k_l = max(1, ceil(rate * elements[l])) entries per layer (:132); pairs of layer l
+ * sit at [koff_l, koff_l + k_l) of the (values, indices) payload, K = sum k_l.
+ *   select:  acc = residual + grad + wd * params (fp64, in place in residual, :128-129);
+ *            the k_l largest |acc| per layer, ties to the lower index (stable argsort of
+ *            -|x|, :71-74), written in ascending index order as fp32 values and
+ *            layer-local int32 indices; selected residual entries become 0 (:142-144).
+ *   scatter: dense[offset + index] += value for one rank's pairs (call in rank order, :137-139).
+ *   apply:   avg = dense / divisor; velocity = momentum * velocity + avg (first: from 0);
+ *            params -= lr * velocity (:145-146); dense is cleared for the next step. */
+typedef struct hsx_topk hsx_topk;
+int hsx_topk_create(const int64_t* offsets, const int64_t* elements, double rate, int32_t n_layers, hsx_topk** out);
+void hsx_topk_destroy(hsx_topk* topk);
+int64_t hsx_topk_total(const hsx_topk* topk);
+int hsx_topk_layer_keep(const hsx_topk* topk, int32_t layer, int64_t* k, int64_t* offset);
+int hsx_topk_select(const hsx_topk* topk, const float* grad, const float* params, double weight_decay,
+                    double* residual, float* values, int32_t* indices, void* stream);
+int hsx_topk_scatter(const hsx_topk* topk, const float* values, const int32_t* indices, double* dense, void* stream);
+int hsx_topk_apply(const hsx_topk* topk, double* dense, double divisor, float* params, float* velocity, double lr,
+                   double momentum, int32_t first, void* stream);
 /* Current per-layer penalties (after device-side adaptation); synchronous. */
 int hsx_plan_read_penalties(hsx_plan* plan, double* rho1, double* rho2);
 

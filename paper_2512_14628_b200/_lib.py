@@ -88,6 +88,13 @@ SIGNATURES = {
     "hsx_plan_read_penalties": (C.c_int, [P, VP, VP]),
     "hsx_dense_grad_pack": (C.c_int, [VP, VP, F64, VP, C.c_int64, VP]),
     "hsx_dense_apply": (C.c_int, [VP, I32, F64, VP, VP, F64, F64, I32, C.c_int64, VP]),
+    "hsx_topk_create": (C.c_int, [VP, VP, F64, I32, VP]),
+    "hsx_topk_destroy": (None, [VP]),
+    "hsx_topk_total": (I64, [VP]),
+    "hsx_topk_layer_keep": (C.c_int, [VP, I32, VP, VP]),
+    "hsx_topk_select": (C.c_int, [VP, VP, VP, F64, VP, VP, VP, VP]),
+    "hsx_topk_scatter": (C.c_int, [VP, VP, VP, VP, VP]),
+    "hsx_topk_apply": (C.c_int, [VP, VP, F64, VP, VP, F64, F64, I32, VP]),
     "hsx_prox_sgd_step": (C.c_int, [P, VP, VP, VP, VP, VP, F64, F64, I32, VP, VP]),
     "hsx_nonzero_u8": (C.c_int, [VP, I64, VP, VP]),
     "hsx_pack_bits": (C.c_int, [VP, I64, VP, VP]),

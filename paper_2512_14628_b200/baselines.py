@@ -29,7 +29,7 @@ from . import _lib
 from .errors import ProtocolError
 from .plan import Plan, current_stream, ptr, timed
 from .sync import HSADMMSync
-from .transport import AllReduce, Barrier, GroupScope, LedgerEntry, ProcessGroup, ReduceOp, Topology
+from .transport import AllGather, AllReduce, Barrier, GroupScope, LedgerEntry, ProcessGroup, ReduceOp, Topology
 
 
 class _FlatView:
@@ -201,5 +201,126 @@ class DenseSync:
 
 def run_dense_local(engines: list[DenseSync], step: int):
     """Step ``step`` of every rank of a LocalCluster (single process, one GPU)."""
+    cluster = engines[0].cluster
+    return cluster.run({e.rank: e.program(step) for e in engines})
+
+
+class TopKSync:
+    """One rank of ``topk_program`` (baselines.py:101-148) after the gradient: Top-K
+    compression with error feedback. Per layer the ceil(rate * n) largest |acc| of
+    acc = residual + grad + wd * params (fp64 residual arena, in place) travel as
+    (fp32 value, int32 index) pairs — 8 B per pair, the reference ledger's 2 x 4 B —
+    in ONE all-gather for all layers; the gathered pairs are scatter-added in rank
+    order into an fp64 buffer, then / W and the momentum update.
+
+    Device path: ``hsx_topk_select`` (fused acc + 8-pass radix select per layer +
+    ordered write + residual clear), the all-gather, W x ``hsx_topk_scatter``,
+    ``hsx_topk_apply``.
+    """
+
+    def __init__(self, rank: int, cluster, layers, solver, rate: float, device=None):
+        import ctypes as C
+
+        if not solver.lr > 0:
+            from .errors import ConfigError
+
+            raise ConfigError(f"learning rate must be positive, got {solver.lr}")
+        self.rank = rank
+        self.cluster = cluster
+        self.group = cluster.global_group()
+        self.W = len(self.group.members)
+        self.layers = list(layers)
+        self.names = [ls.name for ls in layers]
+        self.rate = float(rate)
+        self.lr, self.momentum, self.weight_decay = float(solver.lr), float(solver.momentum), float(solver.weight_decay)
+        zeros = {n: 0.0 for n in self.names}
+        self.plan = Plan(self.layers, {}, zeros, zeros)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        pl, dev = self.plan, self.device
+        self.params, self.velocity, self.grad = (pl.empty_arena(dev) for _ in range(3))
+        self.residual = torch.zeros(pl.arena, dtype=torch.float64, device=dev)
+        self.dense = torch.zeros(pl.arena, dtype=torch.float64, device=dev)
+        L = len(self.layers)
+        offs = (C.c_int64 * max(L, 1))(*pl.offsets)
+        elems = (C.c_int64 * max(L, 1))(*[ls.elements for ls in self.layers])
+        h = C.c_void_p()
+        lib = _lib.load()
+        _lib.check(lib.hsx_topk_create(C.cast(offs, C.c_void_p), C.cast(elems, C.c_void_p), self.rate, L,
+                                       C.byref(h)), "hsx_topk_create")
+        self._h = h
+        self.K = int(lib.hsx_topk_total(h))
+        self.keep = []
+        for i in range(L):
+            k, o = C.c_int64(), C.c_int64()
+            _lib.call("hsx_topk_layer_keep", h, i, C.byref(k), C.byref(o))
+            self.keep.append((int(k.value), int(o.value)))
+        self.payload = torch.zeros(2 * max(self.K, 1), dtype=torch.int32, device=dev)
+        self.gathered = torch.zeros((self.W, 2 * max(self.K, 1)), dtype=torch.int32, device=dev)
+        self.first = True
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().hsx_topk_destroy(h)
+            except Exception:
+                pass
+
+    def init_from(self, params0: dict) -> None:
+        self.plan.load_arena(self.params, params0)
+        self.velocity.zero_()
+        self.residual.zero_()
+        self.dense.zero_()
+        self.first = True
+
+    def load_grads(self, grads) -> None:
+        if isinstance(grads, torch.Tensor):
+            self.grad.copy_(grads)
+        else:
+            self.plan.load_arena(self.grad, grads)
+
+    def views(self, key: str) -> dict:
+        t = getattr(self, key)
+        return {n: t[o:o + ls.elements].view(ls.shape) for n, ls, o in zip(self.names, self.layers, self.plan.offsets)}
+
+    def selections(self) -> dict:
+        """This rank's last selected (layer-local, ascending) indices per layer."""
+        idx = self.payload[self.K:2 * self.K]
+        return {n: idx[o:o + k] for n, (k, o) in zip(self.names, self.keep)}
+
+    def program(self, step: int):
+        K = self.K
+        vals = self.payload[:K].view(torch.float32)
+        with timed("T_select"):
+            _lib.call("hsx_topk_select", self._h, ptr(self.grad), ptr(self.params), self.weight_decay,
+                      ptr(self.residual), ptr(vals), ptr(self.payload[K:]), current_stream())
+        yield AllGather(self.group, self.payload, self.gathered, "topk", step)
+        with timed("T_scatter_apply"):
+            for j in range(self.W):   # rank order (:137-139)
+                row = self.gathered[j]
+                _lib.call("hsx_topk_scatter", self._h, ptr(row[:K].view(torch.float32)), ptr(row[K:2 * K]),
+                          ptr(self.dense), current_stream())
+            _lib.call("hsx_topk_apply", self._h, ptr(self.dense), float(self.W), ptr(self.params),
+                      ptr(self.velocity), self.lr, self.momentum, 1 if self.first else 0, current_stream())
+        self.first = False
+        self._log_reference(step)
+
+    def _log_reference(self, step: int):
+        """topk_program's ledger: topk/{layer} all-gathers of 2k elements (:136)."""
+        led = getattr(self.cluster, "ref_ledger", None)
+        if led is None or (getattr(self.cluster, "shared_ledger", False) and self.rank != self.group.members[0]):
+            return
+        g, W = self.group, self.W
+        entries = [LedgerEntry(step, g.id, g.scope.value, "allgather", 2 * k, 8 * k, W, f"topk/{n}")
+                   for n, (k, _) in zip(self.names, self.keep)]
+        led.defer(lambda: entries)
+
+    def step(self, step: int):
+        if not hasattr(self.cluster, "run_rank"):
+            raise ProtocolError("step() needs a DistCluster; use run_topk_local for in-process ranks")
+        return self.cluster.run_rank(self.program(step))
+
+
+def run_topk_local(engines: list[TopKSync], step: int):
     cluster = engines[0].cluster
     return cluster.run({e.rank: e.program(step) for e in engines})

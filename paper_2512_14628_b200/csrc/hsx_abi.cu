@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <new>
 #include <numeric>
 #include <string>
@@ -1059,6 +1060,110 @@ int hsx_dense_apply(const float* const* sends, int32_t n_sends, double divisor, 
     return fail(HSX_EINVAL, "buffers must be 16-byte aligned");
   hsx::launch_dense_apply(src, divisor, params, velocity, lr, momentum, first ? 1 : 0, n, S(stream));
   HSX_LAUNCHED("dense_apply");
+  return HSX_OK;
+}
+
+struct hsx_topk {
+  int n_layers = 0;
+  long long ktotal = 0, span = 0;
+  std::vector<hsx::TkLayer> layers;
+  std::vector<hsx::TkTile> tiles;
+  hsx::TkLayer* d_layers = nullptr;
+  hsx::TkTile* d_tiles = nullptr;
+  hsx::TkState* d_state = nullptr;
+  unsigned* d_hist = nullptr;
+  int2 *d_cnt = nullptr, *d_base = nullptr;
+  ~hsx_topk() {
+    void* ptrs[] = {d_layers, d_tiles, d_state, d_hist, d_cnt, d_base};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+  }
+};
+
+int hsx_topk_create(const int64_t* offsets, const int64_t* elements, double rate, int32_t n_layers, hsx_topk** out) {
+  if (!out || (n_layers > 0 && (!offsets || !elements))) return fail(HSX_EINVAL, "null argument");
+  if (n_layers < 0) return fail(HSX_EINVAL, "negative layer count");
+  if (!(rate > 0.0) || rate > 1.0) return fail(HSX_ECONFIG, "top-k rate must be in (0, 1], got %g", rate);
+  *out = nullptr;
+  HSX_TRY({
+    std::unique_ptr<hsx_topk> t(new hsx_topk());
+    t->n_layers = n_layers;
+    constexpr long long kTile = 8192;
+    for (int l = 0; l < n_layers; ++l) {
+      if (elements[l] <= 0 || offsets[l] < 0) return fail(HSX_ESHAPE, "layer %d: bad extent", l);
+      if (elements[l] > INT32_MAX) return fail(HSX_ESHAPE, "layer %d: more than 2^31 elements", l);
+      hsx::TkLayer ly;
+      ly.off = offsets[l];
+      ly.n = elements[l];
+      // k = max(1, ceil(rate * n)) with the reference's float expression (:132)
+      ly.k = std::max<long long>(1, (long long)std::ceil(rate * (double)elements[l]));
+      if (ly.k > ly.n) ly.k = ly.n;
+      ly.koff = t->ktotal;
+      ly.tile0 = (int)t->tiles.size();
+      for (long long b = 0; b < ly.n; b += kTile) {
+        hsx::TkTile tt;
+        tt.layer = l;
+        tt.pad = 0;
+        tt.begin = b;
+        tt.end = std::min(ly.n, b + kTile);
+        t->tiles.push_back(tt);
+      }
+      ly.ntiles = (int)t->tiles.size() - ly.tile0;
+      t->ktotal += ly.k;
+      t->span = std::max(t->span, ly.off + ly.n);
+      t->layers.push_back(ly);
+    }
+    if (n_layers) {
+      int rc;
+      if ((rc = upload(&t->d_layers, t->layers))) return rc;
+      if ((rc = upload(&t->d_tiles, t->tiles))) return rc;
+      HSX_CUDA(cudaMalloc(&t->d_state, sizeof(hsx::TkState) * n_layers));
+      HSX_CUDA(cudaMalloc(&t->d_hist, sizeof(unsigned) * 256 * n_layers));
+      HSX_CUDA(cudaMalloc(&t->d_cnt, sizeof(int2) * t->tiles.size()));
+      HSX_CUDA(cudaMalloc(&t->d_base, sizeof(int2) * t->tiles.size()));
+    }
+    *out = t.release();
+  })
+  return HSX_OK;
+}
+
+void hsx_topk_destroy(hsx_topk* t) { delete t; }
+
+int64_t hsx_topk_total(const hsx_topk* t) { return t ? t->ktotal : -1; }
+
+int hsx_topk_layer_keep(const hsx_topk* t, int32_t layer, int64_t* k, int64_t* offset) {
+  if (!t || !k || !offset) return fail(HSX_EINVAL, "null argument");
+  if (layer < 0 || layer >= t->n_layers) return fail(HSX_EINVAL, "layer %d out of range", layer);
+  *k = t->layers[layer].k;
+  *offset = t->layers[layer].koff;
+  return HSX_OK;
+}
+
+int hsx_topk_select(const hsx_topk* t, const float* grad, const float* params, double weight_decay, double* residual,
+                    float* values, int32_t* indices, void* stream) {
+  if (!t || !grad || !params || !residual || !values || !indices) return fail(HSX_EINVAL, "null argument");
+  const int n = hsx::launch_topk_select(t->d_tiles, (int)t->tiles.size(), t->d_layers, t->n_layers, t->d_state,
+                                        t->d_hist, t->d_cnt, t->d_base, residual, grad, params, weight_decay, values,
+                                        indices, S(stream));
+  if (n > 1) g_launches.fetch_add(n - 1);
+  HSX_LAUNCHED("topk_select");
+  return HSX_OK;
+}
+
+int hsx_topk_scatter(const hsx_topk* t, const float* values, const int32_t* indices, double* dense, void* stream) {
+  if (!t || !values || !indices || !dense) return fail(HSX_EINVAL, "null argument");
+  hsx::launch_topk_scatter(t->d_layers, t->n_layers, values, indices, t->ktotal, dense, S(stream));
+  HSX_LAUNCHED("topk_scatter");
+  return HSX_OK;
+}
+
+int hsx_topk_apply(const hsx_topk* t, double* dense, double divisor, float* params, float* velocity, double lr,
+                   double momentum, int32_t first, void* stream) {
+  if (!t || !dense || !params || !velocity) return fail(HSX_EINVAL, "null argument");
+  if (!(divisor > 0.0)) return fail(HSX_EINVAL, "divisor must be positive");
+  if (!(lr > 0.0)) return fail(HSX_ECONFIG, "learning rate must be positive, got %g", lr);
+  hsx::launch_topk_apply(dense, divisor, params, velocity, lr, momentum, first ? 1 : 0, t->span, S(stream));
+  HSX_LAUNCHED("topk_apply");
   return HSX_OK;
 }
 

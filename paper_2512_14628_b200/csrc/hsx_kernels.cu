@@ -2726,6 +2726,278 @@ void launch_dense_apply(const PeerPtrs& src, double div, float* p, float* v, dou
   if (n <= 0 || src.n <= 0) return;
   launch_pdl(k_dense_apply, dense_grid(n), kThreads, 0, st, src, div, p, v, lr, mom, first, n);
 }
+
+// ---------------------------------------------------------------------------
+// Top-K gradient compression with error feedback (baselines.py:101-148).
+// Per layer: acc = residual + grad + wd * params (fp64, in place in the fp64
+// residual arena); an exact MSD radix select (8 passes of 8 bits over the key
+// bits(|acc|), layers whose chosen bin holds exactly the remaining count stop
+// early) gives the k-th largest key T and the number of ties to take; the
+// selection (key > T, plus the lowest-index ties: the stable argsort of -|x|,
+// :71-74) is written in ascending index order as (fp32 value, int32 index) pairs
+// and zeroed in the residual (flat - kept, :142-144). The all-gathered pairs are
+// scatter-added rank by rank into an fp64 buffer (:137-139), then / W and the
+// momentum update (:145-146), which also clears the buffer.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ unsigned long long tk_key(double x) {
+  return (unsigned long long)__double_as_longlong(fabs(x));
+}
+
+__global__ void k_topk_init(TkLayer* __restrict__ tl, TkState* __restrict__ st, unsigned* __restrict__ hist,
+                            int L) {
+  PDL_ENTRY();
+  for (int l = blockIdx.x; l < L; l += gridDim.x) {
+    if (threadIdx.x == 0) {
+      st[l].prefix = 0ull;
+      st[l].mask = 0ull;
+      st[l].k_rem = tl[l].k;
+      st[l].done = 0;
+    }
+    hist[(long long)l * 256 + threadIdx.x] = 0u;
+  }
+}
+
+// ACC: fold grad + wd * params into the residual first (pass 0)
+template <bool ACC>
+__global__ void __launch_bounds__(kThreads) k_topk_hist(const TkTile* __restrict__ tiles, const TkLayer* __restrict__ tl,
+                                                        const TkState* __restrict__ st, unsigned* __restrict__ hist,
+                                                        double* __restrict__ res, const float* __restrict__ g,
+                                                        const float* __restrict__ p, double wd, int shift) {
+  PDL_ENTRY();
+  __shared__ unsigned sh[256];
+  const TkTile t = tiles[blockIdx.x];
+  const TkState s = st[t.layer];
+  if (!ACC && s.done) return;
+  sh[threadIdx.x] = 0u;
+  __syncthreads();
+  const long long off = tl[t.layer].off;
+  for (long long e = t.begin + threadIdx.x; e < t.end; e += kThreads) {
+    double a;
+    if (ACC) {
+      a = __dadd_rn(res[off + e], __dadd_rn((double)g[off + e], __dmul_rn(wd, (double)p[off + e])));
+      res[off + e] = a;
+    } else {
+      a = res[off + e];
+    }
+    const unsigned long long k = tk_key(a);
+    if ((k & s.mask) == s.prefix) atomicAdd(&sh[(k >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  const unsigned c = sh[threadIdx.x];
+  if (c) atomicAdd(&hist[(long long)t.layer * 256 + threadIdx.x], c);
+}
+
+// one CTA (256 threads) per layer: the bin holding the k_rem-th largest key
+__global__ void __launch_bounds__(256) k_topk_resolve(TkState* __restrict__ st, unsigned* __restrict__ hist,
+                                                      int shift) {
+  PDL_ENTRY();
+  __shared__ long long suf[256];
+  __shared__ int best;
+  const int l = blockIdx.x, b = threadIdx.x;
+  TkState s = st[l];
+  unsigned* h = hist + (long long)l * 256;
+  const long long c = h[b];
+  h[b] = 0u;
+  if (s.done) return;
+  suf[b] = c;
+  if (b == 0) best = -1;
+  __syncthreads();
+  for (int d = 1; d < 256; d <<= 1) {  // suffix sums: suf[b] = sum_{b' >= b} hist[b']
+    const long long add = b + d < 256 ? suf[b + d] : 0;
+    __syncthreads();
+    suf[b] += add;
+    __syncthreads();
+  }
+  if (suf[b] >= s.k_rem && (b == 255 || suf[b + 1] < s.k_rem)) best = b;
+  __syncthreads();
+  if (b == 0 && best >= 0) {
+    const long long above = best == 255 ? 0 : suf[best + 1];
+    s.k_rem -= above;
+    s.prefix |= (unsigned long long)best << shift;
+    s.mask |= 255ull << shift;
+    s.done = (suf[best] - above == s.k_rem) ? 1 : 0;
+    st[l] = s;
+  }
+}
+
+__device__ __forceinline__ void tk_class(unsigned long long k, const TkState& s, int& gt, int& eq) {
+  const unsigned long long m = k & s.mask;
+  gt = m > s.prefix;
+  eq = m == s.prefix;
+}
+
+__global__ void __launch_bounds__(kThreads) k_topk_count(const TkTile* __restrict__ tiles, const TkLayer* __restrict__ tl,
+                                                         const TkState* __restrict__ st, const double* __restrict__ res,
+                                                         int2* __restrict__ cnt) {
+  PDL_ENTRY();
+  const TkTile t = tiles[blockIdx.x];
+  const TkState s = st[t.layer];
+  const long long off = tl[t.layer].off;
+  int gt = 0, eq = 0;
+  for (long long e = t.begin + threadIdx.x; e < t.end; e += kThreads) {
+    int a, b;
+    tk_class(tk_key(res[off + e]), s, a, b);
+    gt += a;
+    eq += b;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gt += __shfl_xor_sync(kFull, gt, o);
+    eq += __shfl_xor_sync(kFull, eq, o);
+  }
+  __shared__ int sg[kThreads / 32], se[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    sg[threadIdx.x >> 5] = gt;
+    se[threadIdx.x >> 5] = eq;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0, b = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      a += sg[w];
+      b += se[w];
+    }
+    cnt[blockIdx.x] = make_int2(a, b);
+  }
+}
+
+// one thread per layer: exclusive (ties before, output before) per tile, in tile order
+__global__ void k_topk_scan(const TkLayer* __restrict__ tl, const TkState* __restrict__ st,
+                            const int2* __restrict__ cnt, int2* __restrict__ base, int L) {
+  PDL_ENTRY();
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const long long k_rem = st[l].k_rem;
+  long long eq_before = 0, out_before = 0;
+  for (int i = tl[l].tile0; i < tl[l].tile0 + tl[l].ntiles; ++i) {
+    const int2 c = cnt[i];
+    base[i] = make_int2((int)eq_before, (int)out_before);
+    const long long take = std::min<long long>(std::max<long long>(k_rem - eq_before, 0), c.y);
+    eq_before += c.y;
+    out_before += c.x + take;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_topk_write(const TkTile* __restrict__ tiles, const TkLayer* __restrict__ tl,
+                                                         const TkState* __restrict__ st, const int2* __restrict__ base,
+                                                         double* __restrict__ res, float* __restrict__ vals,
+                                                         int* __restrict__ idx) {
+  PDL_ENTRY();
+  __shared__ int wsum[kThreads / 32];
+  __shared__ int carry;
+  const TkTile t = tiles[blockIdx.x];
+  const TkState s = st[t.layer];
+  const TkLayer ly = tl[t.layer];
+  const int2 b0 = base[blockIdx.x];
+  int eq_run = b0.x, out_run = b0.y;  // block-uniform running totals
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long e0 = t.begin; e0 < t.end; e0 += kThreads) {
+    const long long e = e0 + threadIdx.x;
+    int gt = 0, eq = 0;
+    double a = 0.0;
+    if (e < t.end) {
+      a = res[ly.off + e];
+      tk_class(tk_key(a), s, gt, eq);
+    }
+    // inclusive scan of (eq << 16 | gt) over the block (<= 256 each: no carry between halves)
+    int x = (eq << 16) | gt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    int wbase = 0;
+    for (int j = 0; j < w; ++j) wbase += wsum[j];
+    x += wbase;
+    const int eq_incl = x >> 16, gt_incl = x & 0xffff;
+    const int eq_rank = eq_run + eq_incl - eq;  // ties before this element in the layer
+    const int take_eq = eq && eq_rank < s.k_rem;
+    // output slot: gt before + ties taken before (ties before capped at k_rem)
+    const long long ties_taken_before = std::min<long long>(std::max<long long>(s.k_rem - eq_run, 0),
+                                                            (long long)(eq_incl - eq));
+    if (gt || take_eq) {
+      const long long pos = (long long)out_run + (gt_incl - gt) + ties_taken_before;
+      vals[ly.koff + pos] = (float)a;
+      idx[ly.koff + pos] = (int)e;
+      res[ly.off + e] = __dsub_rn(a, a);  // flat - kept (:144)
+    }
+    if (threadIdx.x == kThreads - 1) carry = x;
+    __syncthreads();
+    const int tot = carry;
+    const int eq_tot = tot >> 16, gt_tot = tot & 0xffff;
+    const long long taken = std::min<long long>(std::max<long long>(s.k_rem - eq_run, 0), (long long)eq_tot);
+    out_run += gt_tot + (int)taken;
+    eq_run += eq_tot;
+    __syncthreads();
+  }
+}
+
+// dense[off[layer] + idx] += val for one rank's pairs (indices unique within a rank)
+__global__ void __launch_bounds__(kThreads) k_topk_scatter(const TkLayer* __restrict__ tl, int L,
+                                                           const float* __restrict__ vals, const int* __restrict__ idx,
+                                                           long long ktotal, double* __restrict__ dense) {
+  PDL_ENTRY();
+  for (long long j = blockIdx.x * (long long)kThreads + threadIdx.x; j < ktotal; j += (long long)gridDim.x * kThreads) {
+    int lo = 0, hi = L - 1;  // last layer with koff <= j
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tl[mid].koff <= j) lo = mid; else hi = mid - 1;
+    }
+    const long long i = tl[lo].off + idx[j];
+    dense[i] = __dadd_rn(dense[i], (double)vals[j]);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_topk_apply(double* __restrict__ dense, double div, float* __restrict__ p,
+                                                         float* __restrict__ v, double lr, double mom, int first,
+                                                         long long n) {
+  PDL_ENTRY();
+  for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kThreads) {
+    const double avg = __ddiv_rn(dense[i], div);
+    dense[i] = 0.0;
+    float pp = p[i], vv = first ? 0.f : v[i];
+    dense_upd(avg, pp, vv, lr, mom, first);
+    p[i] = pp;
+    v[i] = vv;
+  }
+}
+
+int launch_topk_select(const TkTile* tiles, int n_tiles, const TkLayer* tl, int L, TkState* st, unsigned* hist,
+                       int2* cnt, int2* base, double* res, const float* g, const float* p, double wd, float* vals,
+                       int* idx, cudaStream_t stq) {
+  if (L <= 0 || n_tiles <= 0) return 0;
+  int launches = 0;
+  launch_pdl(k_topk_init, std::min(L, 148 * 4), 256, 0, stq, const_cast<TkLayer*>(tl), st, hist, L);
+  ++launches;
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    if (pass == 0)
+      launch_pdl(k_topk_hist<true>, n_tiles, kThreads, 0, stq, tiles, tl, (const TkState*)st, hist, res, g, p, wd, shift);
+    else
+      launch_pdl(k_topk_hist<false>, n_tiles, kThreads, 0, stq, tiles, tl, (const TkState*)st, hist, res, g, p, wd,
+                 shift);
+    launch_pdl(k_topk_resolve, L, 256, 0, stq, st, hist, shift);
+    launches += 2;
+  }
+  launch_pdl(k_topk_count, n_tiles, kThreads, 0, stq, tiles, tl, (const TkState*)st, (const double*)res, cnt);
+  launch_pdl(k_topk_scan, (L + 127) / 128, 128, 0, stq, tl, (const TkState*)st, (const int2*)cnt, base, L);
+  launch_pdl(k_topk_write, n_tiles, kThreads, 0, stq, tiles, tl, (const TkState*)st, (const int2*)base, res, vals, idx);
+  return launches + 3;
+}
+
+void launch_topk_scatter(const TkLayer* tl, int L, const float* vals, const int* idx, long long ktotal, double* dense,
+                         cudaStream_t st) {
+  if (ktotal <= 0) return;
+  const int grid = (int)std::min<long long>((ktotal + kThreads - 1) / kThreads, 148LL * 8);
+  launch_pdl(k_topk_scatter, grid, kThreads, 0, st, tl, L, vals, idx, ktotal, dense);
+}
+
+void launch_topk_apply(double* dense, double div, float* p, float* v, double lr, double mom, int first, long long n,
+                       cudaStream_t st) {
+  if (n <= 0) return;
+  launch_pdl(k_topk_apply, dense_grid(n), kThreads, 0, st, dense, div, p, v, lr, mom, first, n);
+}
 }  // namespace hsx
 
 extern "C" int hsx_set_l2_hints(int32_t on) {

@@ -207,6 +207,31 @@ struct ResidArgs {
 };
 void launch_resid_fold(const ResidArgs& a, cudaStream_t st);
 void launch_report(const ResidArgs& a, cudaStream_t st);
+// Top-K baseline (baselines.py:101-148)
+struct TkLayer {
+  long long off;    // arena offset of the layer
+  long long n;      // elements
+  long long k;      // keep count, max(1, ceil(rate * n)) (:132)
+  long long koff;   // offset of the layer's pairs in the payload
+  int tile0, ntiles;
+};
+struct TkTile {
+  int layer;
+  int pad;
+  long long begin, end;  // layer-local element range
+};
+struct TkState {
+  unsigned long long prefix, mask;  // radix-select prefix of bits(|acc|) so far
+  long long k_rem;                  // keys still to take inside the prefix bin
+  int done, pad;
+};
+int launch_topk_select(const TkTile* tiles, int n_tiles, const TkLayer* tl, int L, TkState* st, unsigned* hist,
+                       int2* cnt, int2* base, double* res, const float* g, const float* p, double wd, float* vals,
+                       int* idx, cudaStream_t stq);
+void launch_topk_scatter(const TkLayer* tl, int L, const float* vals, const int* idx, long long ktotal, double* dense,
+                         cudaStream_t st);
+void launch_topk_apply(double* dense, double div, float* p, float* v, double lr, double mom, int first, long long n,
+                       cudaStream_t st);
 void launch_dense_pack(const float* g, const float* p, double wd, float* send, long long n, cudaStream_t st);
 void launch_dense_apply(const PeerPtrs& src, double div, float* p, float* v, double lr, double mom, int first,
                         long long n, cudaStream_t st);

@@ -184,6 +184,21 @@ def baselines_check(topo, rank, world, transport):
         buf = [torch.empty_like(eng.params) for _ in range(world)]
         dist.all_gather(buf, eng.params)
         assert all(torch.equal(b, eng.params) for b in buf), "dense params diverged across ranks"
+        ref = G.TopK(world)
+        Solver.lr, Solver.momentum, Solver.weight_decay = ref.lr, ref.momentum, ref.weight_decay
+        eng = H.TopKSync(rank, H.DistCluster(topo), layers, Solver, ref.rate)
+        eng.init_from(ref.p0())
+        for s in range(1, ref.steps + 1):
+            eng.load_grads(ref.grads(s, rank))
+            eng.step(s)
+            for n, t in eng.selections().items():
+                assert np.array_equal(t.cpu().numpy(), ref.sel(s, rank, n)), ("topk", s, rank, n)
+        out = ref.out()
+        for n, t in eng.views("params").items():
+            err = rel_err(t.cpu().numpy(), out[n], ref.p0()[n])
+            assert err <= TOL, ("topk", rank, n, err)
+        dist.all_gather(buf, eng.params)
+        assert all(torch.equal(b, eng.params) for b in buf), "top-k params diverged across ranks"
     return True
 
 

@@ -141,3 +141,85 @@ def test_dense_apply_rejects_bad_arguments():
     with pytest.raises(Exception):
         _lib.call("hsx_dense_apply", arr, 5, 1.0, p.data_ptr(), p.data_ptr(), 0.1, 0.9, 0, 64, current_stream())
     del keep, ShapeError
+
+
+def _topk_engines(ref, world):
+    import paper_2512_14628_b200 as H
+
+    layers = [H.LayerSpec(n, H.LayerKind.CONV if k == "conv" else H.LayerKind.FULLY_CONNECTED, shape)
+              for n, k, shape, _ in G.E2E_LAYERS]
+
+    class Solver:
+        lr, momentum, weight_decay = ref.lr, ref.momentum, ref.weight_decay
+
+    cluster = H.LocalCluster(H.Topology(1, world))
+    return cluster, [H.TopKSync(r, cluster, layers, Solver, ref.rate) for r in range(world)]
+
+
+@pytest.mark.parametrize("world", G.DENSE_WORLDS)
+def test_topk_against_reference_golden(world):
+    """topk_program (baselines.py:101-148): every rank's selections per step and layer
+    exact (ties -> lower index; fc.b is built of exact ties), parameters within 1e-5,
+    bit-identical on every rank, the ledger entry for entry."""
+    import paper_2512_14628_b200 as H
+
+    ref = G.TopK(world)
+    cluster, engines = _topk_engines(ref, world)
+    for e in engines:
+        e.init_from(ref.p0())
+    for s in range(1, ref.steps + 1):
+        for e in engines:
+            e.load_grads(ref.grads(s, e.rank))
+        H.run_topk_local(engines, s)
+        for e in engines:
+            sel = e.selections()
+            for n in ref.names:
+                assert np.array_equal(cpu(sel[n]), ref.sel(s, e.rank, n)), (s, e.rank, n)
+    out = ref.out()
+    for e in engines:
+        for n in ref.names:
+            err = rel_err(cpu(e.views("params")[n]), out[n], ref.p0()[n])
+            assert err <= TOL, (e.rank, n, err)
+    for e in engines[1:]:
+        assert torch.equal(e.params, engines[0].params)
+    got = sorted(json.dumps(x.to_dict(), sort_keys=True) for x in cluster.ref_ledger.entries)
+    want = sorted(json.dumps(x, sort_keys=True) for x in ref.ledger())
+    assert got == want
+
+
+def test_topk_full_size_selection_against_oracle():
+    """RN18-224 at rate 0.01, two steps (error feedback on): the GPU selection of every
+    layer equals the oracle's stable-argsort selection on the same fp64 accumulator,
+    and the residual keeps exactly the unselected entries."""
+    import paper_2512_14628_b200 as H
+    from oracle import hsadmm_oracle as O
+    from paper_2512_14628_b200.synthetic import model_layers, synthetic_base
+
+    layers = model_layers("rn18_224")
+
+    class Solver:
+        lr, momentum, weight_decay = 0.05, 0.9, 1e-4
+
+    cluster = H.LocalCluster(H.Topology(1, 1))
+    e = H.TopKSync(0, cluster, layers, Solver, 0.01)
+    base = synthetic_base(layers, seed=7)
+    e.init_from(base)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    for s in (1, 2):
+        g = torch.randn(e.plan.arena, device="cuda", generator=gen) * 0.1
+        g[:4096] = torch.round(g[:4096] * 8) / 8          # coarse values: many exact ties
+        e.load_grads(g)
+        acc = {n: (e.views("residual")[n].double() + (e.views("grad")[n].double()
+                   + Solver.weight_decay * e.views("params")[n].double())).cpu().numpy()
+               for n in e.names}      # residual + (grad + wd * params), baselines.py:128-129
+        H.run_topk_local([e], s)
+        sel = e.selections()
+        res = e.views("residual")
+        for n, (k, _) in zip(e.names, e.keep):
+            flat = acc[n].ravel()
+            want = O.topk_select(flat, O.topk_keep_count(0.01, flat.size))
+            assert len(want) == k
+            assert np.array_equal(cpu(sel[n]), want), (s, n)
+            kept = np.zeros_like(flat)
+            kept[want] = flat[want]
+            np.testing.assert_array_equal(cpu(res[n]).ravel(), flat - kept)

@@ -30,7 +30,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--transport", default="auto")
-    ap.add_argument("--systems", default="hsadmm,flat,dense")
+    ap.add_argument("--systems", default="hsadmm,flat,dense,topk")
+    ap.add_argument("--topk-rate", type=float, default=0.01)
     args = ap.parse_args()
 
     import torch
@@ -86,10 +87,20 @@ def main():
         line = {"system": system, "model": args.model, "n_gpus": world, "params_per_rank": N,
                 "keep_rate": args.keep, "steps": args.steps, "warmup": args.warmup,
                 "l2": "flushed between timed steps (256 MiB write)"}
-        if system == "dense":
-            class Solver:
-                lr, momentum, weight_decay = 0.05, 0.9, 1e-4
+        class Solver:
+            lr, momentum, weight_decay = 0.05, 0.9, 1e-4
 
+        if system == "topk":
+            eng = H.TopKSync(rank, cluster, layers, Solver, args.topk_rate, device=dev)
+            eng.init_from(base)
+            eng.grad.normal_(0.0, 0.1)
+            run = (lambda k: eng.step(k)) if world > 1 else (lambda k: H.run_topk_local([eng], k))
+            for k in range(1, args.warmup + 1):
+                run(k)
+            mean, p50 = timed(run, args.warmup + 1, args.steps)
+            line.update(grouping=f"1x{world}", transport="nccl", rate=args.topk_rate, ms_per_step=mean, p50_ms=p50,
+                        bytes_per_rank_per_sync=8 * eng.K)
+        elif system == "dense":
             eng = H.DenseSync(rank, cluster, layers, Solver, device=dev, transport=args.transport)
             eng.init_from(base)
             eng.grad.normal_(0.0, 0.1)

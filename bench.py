@@ -304,6 +304,14 @@ def run_ours(args):
     theta_host.copy_(eng.theta.cpu())
     z_host = torch.empty(eng.plan.arena, dtype=torch.float32).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # L2 flush between timed steps: write 256 MiB (evicts every line of the step's
+    # state); "write_read" then reads a second 256 MiB buffer so the write-back of the
+    # flush's own dirty lines happens before the timed step, not inside its first kernel
+    flush_mode = os.environ.get("HSX_BENCH_FLUSH", "write_read")
+    flush2 = torch.empty_like(flush) if flush_mode == "write_read" else None
+    sink = torch.empty(1, dtype=torch.float32, device=dev)
+    if flush2 is not None:
+        config["l2"] = "flushed between timed steps (256 MiB write, then 256 MiB read: no dirty lines left)"
 
     use_graph = world == 1 and not args.no_graph
     config["launch"] = "cuda-graph replay per step" if use_graph else "eager launches (deferred host bookkeeping)"
@@ -326,6 +334,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         for i in range(nsteps):
             flush.fill_(float(i))
+            if flush2 is not None:
+                torch.sum(flush2, dim=0, out=sink)
             if kernel_timer is not None:
                 # per-kernel pass: a ~1 ms spin keeps the GPU busy while the host
                 # enqueues the step's launches and their events, so each event pair

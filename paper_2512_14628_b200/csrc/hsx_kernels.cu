@@ -814,9 +814,10 @@ __device__ void select_layer(const DevLayer& gly, int pass, const double* __rest
   if (structured)  // one node: keep sets of the rectangle
     structured_keep_sets(*ka, l, gly, pass, sflag, reinterpret_cast<uint8_t*>(smem) + select_bytes(G), stage);
 #ifdef HSX_PROBE_SELECT
+  SEL_MARK(4);
   if (t == 0)
-    printf("select G=%d nparts=%d nt=%d: norms %lld topk %lld flags %lld cycles\n", G, nparts, nt,
-           tm[1] - tm[0], tm[2] - tm[1], tm[3] - tm[2]);
+    printf("select l=%d G=%d nparts=%d kc=%d nt=%d: norms %lld topk %lld flags %lld keepsets %lld cycles\n", l, G,
+           nparts, kc, nt, tm[1] - tm[0], tm[2] - tm[1], tm[3] - tm[2], tm[4] - tm[3]);
 #endif
 }
 

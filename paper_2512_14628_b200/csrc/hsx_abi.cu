@@ -277,7 +277,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       if (ly.qtile) {
         // row-quad tiles for K3 / K6 / K7 (same shape as the K1 quad tiles)
         const int tq = hsx_tile_quads, tr = tile_rows_env("HSX_STREAM_TILE_ROWS", 32);
-        const int trp = tile_rows_env("HSX_PROJ_TILE_ROWS", 32);
+        const int trp = tile_rows_env("HSX_PROJ_TILE_ROWS", 64);
         const int nchunks = (ly.L / 4 + tq - 1) / tq;
         for (int r0 = 0; r0 < ly.rows; r0 += tr)
           for (int cc = 0; cc < nchunks; ++cc) {

@@ -21,3 +21,5 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   -o gpurun_out/${TAG}_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
   > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu full rc=$?"
+timeout 600 python bench.py --model rn50_224 --no-cpu-baseline > gpurun_out/${TAG}_bench_rn50.json 2> gpurun_out/${TAG}_bench_rn50.err
+echo "bench rn50 rc=$? $(head -c 300 gpurun_out/${TAG}_bench_rn50.json)"

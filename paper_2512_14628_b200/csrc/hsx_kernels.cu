@@ -1403,8 +1403,14 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     const bool word_lane = (lane & 7) == 0 && tc.valid;
     // (no L2 policy here: with the mask-word shuffles in the loop ptxas reuses the
     // policy's uniform descriptor register for BRA.DIV -> illegal instruction)
+    // quad i of this thread sits at e0 + i * estep; its mask word at m0 + i * mstep
+    // (L % 32 == 0), its row flag at s_rk[ph + 4 i]
+    const long long e0 = tc.r0 * ly.L + 4 * tc.j, estep = (long long)kRowPhases * ly.L;
+    const int mstep = kRowPhases * (ly.L >> 5);
+    float* const q0 = zn + ly.off + e0;
+    uint32_t* const m0 = mask + ly.mword + (e0 >> 5);
     auto issue = [&](int d, int i) {
-      if (tc.valid) cp16(ring_slot<1>(ring, d, 0), src + tc.row(i) * ly.L + 4 * tc.j);
+      if (tc.valid) cp16(ring_slot<1>(ring, d, 0), src + e0 + i * estep);
     };
     ring_prologue(count, issue);  // the first loads fly while the keep masks are built
     // kept = AND over the passes' group flags: rows (FILTER) in shared memory,
@@ -1433,12 +1439,10 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     __syncthreads();
     unsigned bad = 0;  // CHECK: kept but zero
     auto consume = [&](int d, int i) {
-      const long long r = tc.row(i);
-      const long long e = r * ly.L + 4 * tc.j;
       unsigned nib = 0;
       if (tc.valid) {
         float4 v = *ring_slot<1>(ring, d, 0);
-        const unsigned kn = s_rk[r - it.begin] ? ckb : 0u;  // kept nibble
+        const unsigned kn = s_rk[tc.ph + kRowPhases * i] ? ckb : 0u;  // kept nibble
         nib = kn & ((unsigned)(v.x != 0.f) | ((unsigned)(v.y != 0.f) << 1) | ((unsigned)(v.z != 0.f) << 2) |
                     ((unsigned)(v.w != 0.f) << 3));
         if (CHECK) bad |= kn & ~nib;
@@ -1447,14 +1451,14 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
           if (!(kn & 2u)) v.y = 0.f;
           if (!(kn & 4u)) v.z = 0.f;
           if (!(kn & 8u)) v.w = 0.f;
-          st4(zn + ly.off + e, v);
+          st4(q0 + i * estep, v);
         }
       }
       unsigned w = nib << (4 * (lane & 7));
       w |= __shfl_xor_sync(kFull, w, 1);
       w |= __shfl_xor_sync(kFull, w, 2);
       w |= __shfl_xor_sync(kFull, w, 4);
-      if (word_lane) mask[ly.mword + (e >> 5)] = w;
+      if (word_lane) m0[i * mstep] = w;
     };
     ring_loop(count, issue, consume);
     if (CHECK) flag_irregular(a, dl.pidx, bad != 0);
@@ -1501,7 +1505,8 @@ __global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __re
                                                          uint32_t* __restrict__ mask) {
   PDL_ENTRY();
   extern __shared__ float4 ring[];
-  project_item<CHECK>(a, zn, mask, a.items[blockIdx.x], ring);
+  const Item it = a.items[blockIdx.x];  // a register copy: a reference into global memory is
+  project_item<CHECK>(a, zn, mask, it, ring);  // reloaded after every store through zn / mask
 }
 
 __device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);

@@ -723,7 +723,7 @@ __device__ void radix_top_k(const unsigned long long* __restrict__ key, int G, i
 // group: [nparts][G] (FILTER: [G], complete row sums), folded in part order.
 // shared memory: keys[G] (u64), flags[G] (u8)
 __host__ __device__ inline size_t select_bytes(int G) { return ((size_t)G * 9 + 15) / 16 * 16; }
-constexpr int kFoldCols = 2048;  // column totals staged per norm chunk (16 KB)
+constexpr int kFoldCols = 8192;  // column totals staged per norm chunk (64 KB): one chunk for 512 x 3x3 groups
 
 __device__ void select_layer(const DevLayer& gly, int pass, const double* __restrict__ partials,
                              double* __restrict__ norms, const FlagPtrs& flags, void* smem, int l,
@@ -1322,8 +1322,10 @@ void launch_select(const DevLayer* layers, const int* list, int n, int pass, con
   allow_smem(k_select, smem);
   static const int nt = [] {
     const char* v = std::getenv("HSX_SELECT_THREADS");
-    const int x = v ? std::atoi(v) : 1024;
-    return (x >= 64 && x <= 1024 && x % 32 == 0) ? x : 1024;
+    // 512 (B200 sweep, profiles/r1i_sweep_select_threads.txt): cheaper barriers than
+    // 1024 for G <= 2048 groups, enough loads in flight for the partial fold
+    const int x = v ? std::atoi(v) : 512;
+    return (x >= 64 && x <= 1024 && x % 32 == 0) ? x : 512;
   }();
   launch_pdl(k_select, n, nt, smem, st, layers, list, pass, partials, norms, flags, ka, structured);
 }

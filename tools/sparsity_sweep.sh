@@ -11,8 +11,9 @@ python - $out <<'PY'
 import json, sys
 for line in open(sys.argv[1]):
     d = json.loads(line)
-    k6 = d["kernels"].get("K6_compact_dual", {})
+    kn = "K6_compact_dual" if "K6_compact_dual" in d["kernels"] else "K67_local_sync"  # one node: K6+K7 fused
+    k6 = d["kernels"].get(kn, {})
     print(f"keep {d['config']['keep_rate']:.1f}: dyn {d['ms_per_step']:.3f} ms frozen {d['frozen_ms_per_step']:.3f} ms "
-          f"K6 {k6.get('us')} us {k6.get('gbs')} GB/s leader bytes {d['leader_bytes']['z_sync_bytes']/1e6:.1f} MB "
+          f"{kn} {k6.get('us')} us {k6.get('gbs')} GB/s leader bytes {d['leader_bytes']['z_sync_bytes']/1e6:.1f} MB "
           f"({d['leader_bytes']['ratio_vs_dense']:.3f} of dense)")
 PY

@@ -1399,9 +1399,11 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     const TileCtx tc(it, ly.L);
     const int nrow = (int)(it.end - it.begin);
     const float* src = zn + ly.off;
-    // all lanes of a warp share a row phase; quads past the row end (a suffix of the
-    // last chunk, whole 8-lane groups since L % 32 == 0) only join the shuffles
-    const int count = __shfl_sync(kFull, tc.count, 0);
+    // all lanes of a warp share a row phase; quads past the row end are a suffix of
+    // the last chunk in whole 8-lane groups (L % 32 == 0): those groups skip the loop
+    // (tc.count = 0) and the mask-word shuffles stay inside each 8-lane group
+    const int count = tc.count;
+    const unsigned gmask = 0xFFu << (lane & 24);
     const bool word_lane = (lane & 7) == 0 && tc.valid;
     // (no L2 policy here: with the mask-word shuffles in the loop ptxas reuses the
     // policy's uniform descriptor register for BRA.DIV -> illegal instruction)
@@ -1411,9 +1413,7 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     const int mstep = kRowPhases * (ly.L >> 5);
     float* const q0 = zn + ly.off + e0;
     uint32_t* const m0 = mask + ly.mword + (e0 >> 5);
-    auto issue = [&](int d, int i) {
-      if (tc.valid) cp16(ring_slot<1>(ring, d, 0), src + e0 + i * estep);
-    };
+    auto issue = [&](int d, int i) { cp16(ring_slot<1>(ring, d, 0), src + e0 + i * estep); };
     ring_prologue(count, issue);  // the first loads fly while the keep masks are built
     // kept = AND over the passes' group flags: rows (FILTER) in shared memory,
     // this thread's four columns (CHANNEL / SHAPE) in a nibble
@@ -1440,26 +1440,23 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     }
     __syncthreads();
     unsigned bad = 0;  // CHECK: kept but zero
-    auto consume = [&](int d, int i) {
-      unsigned nib = 0;
-      if (tc.valid) {
-        float4 v = *ring_slot<1>(ring, d, 0);
-        const unsigned kn = s_rk[tc.ph + kRowPhases * i] ? ckb : 0u;  // kept nibble
-        nib = kn & ((unsigned)(v.x != 0.f) | ((unsigned)(v.y != 0.f) << 1) | ((unsigned)(v.z != 0.f) << 2) |
-                    ((unsigned)(v.w != 0.f) << 3));
-        if (CHECK) bad |= kn & ~nib;
-        if (kn != 0xFu) {
-          if (!(kn & 1u)) v.x = 0.f;
-          if (!(kn & 2u)) v.y = 0.f;
-          if (!(kn & 4u)) v.z = 0.f;
-          if (!(kn & 8u)) v.w = 0.f;
-          st4(q0 + i * estep, v);
-        }
+    auto consume = [&](int d, int i) {  // only valid quads get here
+      float4 v = *ring_slot<1>(ring, d, 0);
+      const unsigned kn = s_rk[tc.ph + kRowPhases * i] ? ckb : 0u;  // kept nibble
+      const unsigned nib = kn & ((unsigned)(v.x != 0.f) | ((unsigned)(v.y != 0.f) << 1) |
+                                 ((unsigned)(v.z != 0.f) << 2) | ((unsigned)(v.w != 0.f) << 3));
+      if (CHECK) bad |= kn & ~nib;
+      if (kn != 0xFu) {
+        if (!(kn & 1u)) v.x = 0.f;
+        if (!(kn & 2u)) v.y = 0.f;
+        if (!(kn & 4u)) v.z = 0.f;
+        if (!(kn & 8u)) v.w = 0.f;
+        st4(q0 + i * estep, v);
       }
       unsigned w = nib << (4 * (lane & 7));
-      w |= __shfl_xor_sync(kFull, w, 1);
-      w |= __shfl_xor_sync(kFull, w, 2);
-      w |= __shfl_xor_sync(kFull, w, 4);
+      w |= __shfl_xor_sync(gmask, w, 1);
+      w |= __shfl_xor_sync(gmask, w, 2);
+      w |= __shfl_xor_sync(gmask, w, 4);
       if (word_lane) m0[i * mstep] = w;
     };
     ring_loop(count, issue, consume);

@@ -348,10 +348,16 @@ int hsx_slices_peers(const hsx_plan* plan, const float* const* srcs, int32_t n, 
 /* Device-side barrier of a group over NVLink: flags[i] is member i's int32 flag
  * array (peer-mapped, indexed by world rank), slots[i] member i's world rank,
  * me this rank's member index, epoch a per-group counter identical on all
- * members (incremented by the caller for every barrier). Enqueued on `stream`;
- * traps after ~10 s if a member never arrives. */
+ * members (incremented by the caller for every barrier). Enqueued on `stream`.
+ * A member that has not arrived within HSX_BARRIER_TIMEOUT_S seconds (default
+ * 600; 0 = wait forever, like an NCCL collective) does not trap the context: the
+ * waiter counts a timeout and the stream continues; hsx_barrier_timeouts reports
+ * it so the host can raise ProtocolError. */
 int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
                       void* stream);
+/* Number of group barriers on the current device that timed out (synchronous
+ * device read); reset != 0 zeroes the counter. */
+int hsx_barrier_timeouts(uint32_t* count, int32_t reset);
 
 /* ---- mask helpers for the per-tensor API -------------------------------------- */
 /* out[i] = |t[i]| > 0  (extract_mask, sparsity.py:113-115) */

@@ -106,6 +106,7 @@ SIGNATURES = {
     "hsx_candidate_renorm_peers": (C.c_int, [P, I32, VP, I32, VP, VP, VP]),
     "hsx_average_peers": (C.c_int, [P, VP, I32, F64, VP, VP]),
     "hsx_group_barrier": (C.c_int, [VP, VP, I32, I32, I32, VP]),
+    "hsx_barrier_timeouts": (C.c_int, [C.POINTER(C.c_uint32), I32]),
     "hsx_slices_peers": (C.c_int, [P, VP, I32, I32, F64, I32, VP, VP]),
 }
 
@@ -150,6 +151,13 @@ def ptr_array(ptrs):
 
 def launch_count() -> int:
     return int(load().hsx_launch_count())
+
+
+def barrier_timeouts(reset: bool = False) -> int:
+    """Group barriers on the current device that gave up waiting (synchronous)."""
+    n = C.c_uint32(0)
+    call("hsx_barrier_timeouts", C.byref(n), 1 if reset else 0)
+    return int(n.value)
 
 
 def note_graph_replay(kernels: int) -> None:

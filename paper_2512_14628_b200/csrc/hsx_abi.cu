@@ -1233,6 +1233,12 @@ int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, in
   return HSX_OK;
 }
 
+int hsx_barrier_timeouts(uint32_t* count, int32_t reset) {
+  if (!count) return fail(HSX_EINVAL, "null argument");
+  if (hsx::barrier_timeouts(count, reset) != 0) return check_cuda("barrier_timeouts");
+  return HSX_OK;
+}
+
 int hsx_nonzero_u8(const float* t, int64_t n, uint8_t* out, void* stream) {
   if ((!t || !out) && n > 0) return fail(HSX_EINVAL, "null argument");
   hsx::launch_nonzero(t, n, out, S(stream));

@@ -12,20 +12,31 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
 
 // opt a kernel into large dynamic shared memory (dynamic + static must fit the
-// per-block limit, so anything above 32 KB opts in); one driver call per kernel
-// and size, remembered in a small table keyed by the kernel address
+// per-block limit, so anything above 32 KB opts in); the attribute is per device
+// and kernel, so one driver call per (device, kernel, size), remembered in a
+// small table (a process may drive several GPUs)
+constexpr int kMaxDevices = 16;
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 ? 0 : dev % kMaxDevices;
+}
 template <typename K>
 static void allow_smem(K kernel, size_t bytes) {
-  static const void* keys[32];
-  static size_t granted[32];
+  constexpr int kSlots = 64;
+  static const void* keys[kSlots];
+  static int devs[kSlots];
+  static size_t granted[kSlots];
   if (bytes <= 32 * 1024) return;
   const void* key = reinterpret_cast<const void*>(kernel);
+  const int dev = current_device();
   int slot = 0;
-  while (slot < 32 && keys[slot] && keys[slot] != key) ++slot;
-  if (slot < 32 && keys[slot] == key && granted[slot] >= bytes) return;
+  while (slot < kSlots && keys[slot] && !(keys[slot] == key && devs[slot] == dev)) ++slot;
+  if (slot < kSlots && keys[slot] == key && devs[slot] == dev && granted[slot] >= bytes) return;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (slot < 32) {
+  if (slot < kSlots) {
     keys[slot] = key;
+    devs[slot] = dev;
     granted[slot] = bytes;
   }
 }
@@ -1271,16 +1282,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
 template <int MODE>
 static void launch_candidate_mode(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
   allow_smem(k_candidate<MODE>, smem);
-  static int resident = -1;  // per instantiation; smem is fixed per plan shape class
-  static size_t resident_smem = 0;
-  if (resident < 0 || resident_smem != smem) {
-    int per_sm = 0, dev = 0, sms = 0;
+  // resident CTAs per device (per instantiation and shared-memory size)
+  static int resident_of[kMaxDevices];
+  static size_t resident_smem[kMaxDevices];
+  const int dev = current_device();
+  if (resident_of[dev] <= 0 || resident_smem[dev] != smem) {
+    int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_candidate<MODE>, kThreads, smem);
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    resident = std::max(1, per_sm) * std::max(1, sms);
-    resident_smem = smem;
+    resident_of[dev] = std::max(1, per_sm) * std::max(1, sms);
+    resident_smem[dev] = smem;
   }
+  const int resident = resident_of[dev];
   static const bool persistent = [] {
     const char* v = std::getenv("HSX_K1_PERSISTENT");
     return !(v && v[0] == '0');
@@ -2467,8 +2480,19 @@ void launch_slices(const PeerPtrs& src, const long long* total_p, long long tota
 // every other member's flag array (release, system scope) and waits until its
 // own slots of all other members reach `epoch` (acquire). Stream-ordered: the
 // kernels before it have completed, the kernels after it read peers' buffers.
-// A member that never arrives traps after ~10 s instead of hanging the GPU.
+// A member that has not arrived after the timeout (HSX_BARRIER_TIMEOUT_S, default
+// 600 s; 0 waits forever, like an NCCL collective) is not a sticky trap: the waiter
+// counts the timeout in g_barrier_timeouts and lets the stream continue, and the
+// host raises ProtocolError when it next reads the counter (hsx_barrier_timeouts).
 // ---------------------------------------------------------------------------
+
+__device__ unsigned int g_barrier_timeouts;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __global__ void k_barrier(BarrierArgs b) {
   const int i = threadIdx.x;
@@ -2480,12 +2504,15 @@ __global__ void k_barrier(BarrierArgs b) {
   __syncwarp();
   if (i < b.n && i != b.me) {
     const int* src = b.flags[b.me] + b.slots[i];
-    const long long t0 = clock64();
+    const unsigned long long t0 = global_ns();
     int v;
     while (true) {
       asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(src) : "memory");
       if (v - b.epoch >= 0) break;
-      if (clock64() - t0 > (1LL << 34)) __trap();
+      if (b.timeout_ns && global_ns() - t0 > b.timeout_ns) {
+        atomicAdd(&g_barrier_timeouts, 1u);
+        break;
+      }
       __nanosleep(64);
     }
   }
@@ -2493,7 +2520,29 @@ __global__ void k_barrier(BarrierArgs b) {
   __threadfence_system();
 }
 
-void launch_barrier(const BarrierArgs& b, cudaStream_t st) { k_barrier<<<1, 32, 0, st>>>(b); }
+static unsigned long long barrier_timeout_ns() {
+  static const unsigned long long ns = [] {
+    const char* v = std::getenv("HSX_BARRIER_TIMEOUT_S");
+    const double s = v ? std::atof(v) : 600.0;
+    return s > 0 ? (unsigned long long)(s * 1e9) : 0ull;
+  }();
+  return ns;
+}
+
+int barrier_timeouts(unsigned int* count, int reset) {
+  if (cudaMemcpyFromSymbol(count, g_barrier_timeouts, sizeof(unsigned int)) != cudaSuccess) return -1;
+  if (reset) {
+    const unsigned int zero = 0;
+    if (cudaMemcpyToSymbol(g_barrier_timeouts, &zero, sizeof(unsigned int)) != cudaSuccess) return -1;
+  }
+  return 0;
+}
+
+void launch_barrier(const BarrierArgs& b, cudaStream_t st) {
+  BarrierArgs a = b;
+  a.timeout_ns = barrier_timeout_ns();
+  k_barrier<<<1, 32, 0, st>>>(a);
+}
 
 // ---------------------------------------------------------------------------
 // K0 send = theta + u; K6f u += theta - z_node (arena-wide streaming)

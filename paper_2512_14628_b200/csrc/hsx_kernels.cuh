@@ -246,8 +246,11 @@ struct BarrierArgs {
   int* flags[32];  // members' flag arrays (peer-mapped), member order
   int slots[32];   // members' slot indices (their world ranks)
   int n, me, epoch;
+  unsigned long long timeout_ns;  // 0: wait forever (set by launch_barrier)
 };
 void launch_barrier(const BarrierArgs& b, cudaStream_t st);
+// barriers that timed out on the current device (synchronous read; reset != 0 zeroes it)
+int barrier_timeouts(unsigned int* count, int reset);
 void launch_average(const PeerPtrs& src, const long long* total, long long max_elems, double div, float* out,
                     cudaStream_t st);
 void launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t st);

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import enum
 import math
+import warnings
 from dataclasses import dataclass
 from functools import lru_cache
 
@@ -77,13 +78,23 @@ def as_cuda_f32(t, name="tensor") -> torch.Tensor:
         t = torch.as_tensor(t)
     if not torch.cuda.is_available():
         raise RuntimeError("libhsx needs a CUDA device (no CPU fallback)")
+    if t.dtype == torch.float64:
+        # the B200 path computes in fp32 (BASELINE north_star); the reference API is fp64
+        warnings.warn(f"{name}: float64 input is rounded to float32 (libhsx computes the sync "
+                      "step on fp32 state)", RuntimeWarning, stacklevel=3)
     if t.device.type != "cuda" or t.dtype != torch.float32 or not t.is_contiguous() or t.data_ptr() % 16:
         t = t.to(device="cuda", dtype=torch.float32).contiguous().clone()
     return t
 
 
-@lru_cache(maxsize=256)
 def _tensor_plan(shape: tuple[int, ...], plan: tuple) -> Plan:
+    """Plan of a one-tensor call; its device scratch is per (device, stream), so
+    calls on another GPU or on concurrent streams never share in-flight scratch."""
+    return _tensor_plan_on(shape, plan, torch.cuda.current_device(), current_stream())
+
+
+@lru_cache(maxsize=64)
+def _tensor_plan_on(shape: tuple[int, ...], plan: tuple, device: int, stream: int) -> Plan:
     ls = LayerSpec("t", LayerKind.CONV, shape, prunable=bool(plan))
     p = Plan([ls], {"t": list(plan)})
     p.set_penalties(None, None, 0.0, 1, 1, identity=True)
@@ -109,6 +120,16 @@ def group_norms_gpu(t, group: GroupBy) -> torch.Tensor:
     _, _, p = _run_projection(t, [(group, g)])
     norms, _ = p.group_norms(0, t.device)
     return norms[:g].clone()
+
+
+def frobenius_norm(t) -> float:
+    """sqrt(sum t^2) in fp64 (reference tensors.py:71-72): one fp64 group norm of
+    the tensor viewed as a single (1, n, 1, 1) filter, accumulated in libhsx."""
+    t = as_cuda_f32(t)
+    n = t.numel()
+    if n == 0:
+        return 0.0
+    return float(group_norms_gpu(t.reshape(1, n, 1, 1), GroupBy.FILTER)[0])
 
 
 def project(t, constraint: SparsityConstraint) -> torch.Tensor:

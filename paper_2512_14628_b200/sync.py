@@ -137,10 +137,17 @@ class HSADMMSync:
         words = max(pl.mask_words, 1)
         self.p_send = self.p_umask = self.p_zhat = self.p_lmask = None
         self.p_flat = None
+        self._send_idx = 0      # p_send buffer of the next step
+        self._nsync = 0         # leader syncs so far (p_flat buffer)
         # every rank allocates the same sequence (the allocation is collective over
         # all ranks); followers leave the leader-group buffers unused
         if self.P > 1:
-            self.p_send = cl.shared(self.rank, self.intra, "send", pl.arena, torch.float32, dev)
+            # double-buffered by step parity: a peer's K1 may still read this step's
+            # send buffer when the next step packs theta + u (nothing else orders the
+            # two when the node has no later intra barrier, e.g. M == 1); the next
+            # step's theta_u barrier orders the rewrite two steps later
+            self.p_send = [cl.shared(self.rank, self.intra, f"send{b}", pl.arena, torch.float32, dev)
+                           for b in (0, 1)]
             self.p_umask = cl.shared(self.rank, self.intra, "umask", words, torch.int32, dev)
             self.p_zhat = cl.shared(self.rank, self.intra, "zhat", pl.arena, torch.float32, dev)
         self.p_ssum = self.p_favg = None
@@ -148,8 +155,9 @@ class HSADMMSync:
             self.p_ssum = cl.shared(self.rank, self.intra, "ssum", pl.arena, torch.float32, dev)
         if self.M > 1:
             lmask = cl.shared(self.rank, self.inter, "lmask", words, torch.int32, dev)
-            # double-buffered by iteration parity: a leader may start the next
-            # compaction while another still averages this one
+            # double-buffered by sync count: a leader may start the next compaction
+            # while another still averages this one (the next z_sync barrier orders
+            # the rewrite two syncs later)
             flat = [cl.shared(self.rank, self.inter, f"flat{b}", pl.arena, torch.float32, dev) for b in (0, 1)]
             favg = (cl.shared(self.rank, self.inter, "favg", pl.arena, torch.float32, dev)
                     if self.M > 2 else None)   # reduce-scatter + all-gather of the leader average
@@ -306,21 +314,25 @@ class HSADMMSync:
         dynamic = not frozen and bool(self.prunable)
         fmask = self.masks if (frozen and self.prunable) else None
         s_local, peers = None, None
+        send = None
+        if self.P > 1:
+            send = self.p_send[self._send_idx]
+            self._send_idx ^= 1
         if self.P > 2:
             # reduce-scatter (my slice of the rank-order sum) + all-gather, then K1 on S
-            self._pack_send(self.p_send.tensor)
+            self._pack_send(send.tensor)
             yield Barrier(self.intra, "theta_u", k)
             me = self.intra.members.index(self.rank)
-            pl.slices_peers(self.p_send.peer_ptrs(), me, 1.0, False, self.p_ssum.tensor, "K8_intra_rs")
+            pl.slices_peers(send.peer_ptrs(), me, 1.0, False, self.p_ssum.tensor, "K8_intra_rs")
             yield Barrier(self.intra, "theta_u_ag", k)
             pl.slices_peers(self.p_ssum.peer_ptrs(), -1, 1.0, False, self.sum, "K8_intra_ag")
             s_local = self.sum
             pl.candidate(s_local, None, None, self.z, self.v, self.z_node, frozen_mask=fmask)
         elif self.P == 2:
             # the intra sum fused into K1: theta+u of both ranks read over NVLink
-            self._pack_send(self.p_send.tensor)
+            self._pack_send(send.tensor)
             yield Barrier(self.intra, "theta_u", k)
-            peers = self.p_send.peer_ptrs()
+            peers = send.peer_ptrs()
             pl.candidate_peers(peers, self.z, self.v, self.z_node, frozen_mask=fmask)
         else:
             pl.candidate(None, self.theta, self.u, self.z, self.v, self.z_node, frozen_mask=fmask)
@@ -365,7 +377,8 @@ class HSADMMSync:
             return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
         if self.is_leader:
             if self.M > 1:
-                flat = self.p_flat[k & 1]
+                flat = self.p_flat[self._nsync & 1]
+                self._nsync += 1
                 self._dual(flat.tensor)
                 yield Barrier(self.inter, "z_sync", k)
                 # leader average over NVLink into the node's payload buffer
@@ -395,7 +408,7 @@ class HSADMMSync:
         """The intra-sum send buffer (theta + u) of this rank, or None when P == 1."""
         if self.P == 1:
             return None
-        return self.p_send.tensor if self.transport == "peer" else self.sum
+        return self.p_send[self._send_idx].tensor if self.transport == "peer" else self.sum
 
     def prox_sgd_step(self, grad, lr: float, momentum: float, first: bool, last: bool = False):
         """One step of the reference's proximal SGD on this rank's theta (workloads.py:
@@ -478,6 +491,16 @@ class HSADMMSync:
             self.z_node_prev = self.plan.empty_arena(self.device)
         if adapt is not None:
             self._resid_params.adapt = 1 if adapt else 0
+
+    def check_barriers(self) -> None:
+        """Raise ProtocolError if a device-side group barrier of this device gave up
+        waiting for a peer (peer transport; synchronous device read)."""
+        if self.transport != "peer":
+            return
+        n = _lib.barrier_timeouts(reset=True)
+        if n:
+            raise ProtocolError(f"{n} group barrier(s) timed out waiting for a peer rank "
+                                "(HSX_BARRIER_TIMEOUT_S); the step's shared buffers are not valid")
 
     def last_report(self):
         """The last iteration's ResidualReport (consensus.py:84-91); synchronizes."""

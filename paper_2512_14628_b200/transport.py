@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import enum
 import logging
+import numbers
 from dataclasses import dataclass, field
 from typing import Any, Generator, Mapping
 
@@ -271,10 +272,17 @@ def _payload_bytes(t) -> int:
 
 @dataclass
 class Bucket:
-    """A contiguous slice of the flat compact buffer (reference transport.py:227-236)."""
+    """A contiguous slice of the flat compact buffer (reference transport.py:227-236).
+
+    ``start`` is the slice's first element in the flat buffer the compaction
+    kernel wrote (the sync step's buckets carry only the layout, no copy);
+    ``buffer`` holds the concatenated payloads when :func:`bucketize` was given
+    arrays / tensors, like the reference's ``Bucket.buffer``.
+    """
 
     start: int
     layout: tuple[tuple[str, int, int], ...]  # (name, offset inside bucket, elements)
+    buffer: Any = None
 
     @property
     def elements(self) -> int:
@@ -285,18 +293,43 @@ class Bucket:
         return tuple((name, e) for name, _, e in self.layout)
 
 
+def _concat(arrays):
+    """The reference's bucket buffer: the payloads raveled and concatenated, in a
+    new buffer (torch on the payloads' device, else float64 numpy)."""
+    import numpy as np
+
+    if any(_is_tensor(a) for a in arrays):
+        import torch
+
+        dev = next(a.device for a in arrays if _is_tensor(a))
+        return torch.cat([torch.as_tensor(a, device=dev).reshape(-1) for a in arrays])
+    return np.ascontiguousarray(np.concatenate([np.asarray(a).ravel() for a in arrays]), dtype=np.float64)
+
+
+def _is_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
 def bucketize(payloads, cap_bytes: int = BUCKET_CAP_BYTES) -> list[Bucket]:
     """Greedy <= ``cap_bytes`` buckets over (name, elements) in order, never split.
 
     Same grouping rule as the reference (transport.py:239-280): a payload
     larger than the cap gets its own bucket with a warning. ``payloads`` may
-    hold element counts or tensors. Concatenating the buckets is the
-    concatenation of the payloads, so a bucket is just a [start, start+n)
-    slice of the flat buffer the compaction kernel already wrote.
+    hold element counts (layout only: the sync step's payload already lives in
+    one flat buffer, so a bucket is a [start, start+n) slice of what the
+    compaction kernel wrote) or arrays / tensors (the bucket's ``buffer`` is
+    their concatenation, as in the reference).
     """
-    sizes = [(name, int(x) if isinstance(x, int) else int(x.numel())) for name, x in payloads]
+    sizes, arrays = [], {}
+    for i, (name, x) in enumerate(payloads):
+        if isinstance(x, numbers.Integral):
+            sizes.append((name, int(x)))
+        else:
+            n = int(x.numel()) if _is_tensor(x) else int(x.size)
+            sizes.append((name, n))
+            arrays[i] = x
     buckets: list[Bucket] = []
-    cur: list[tuple[str, int]] = []
+    cur: list[tuple[int, str, int]] = []
     cur_bytes = 0
     start = 0
 
@@ -304,35 +337,40 @@ def bucketize(payloads, cap_bytes: int = BUCKET_CAP_BYTES) -> list[Bucket]:
         nonlocal cur, cur_bytes, start
         if cur:
             lay, off = [], 0
-            for name, n in cur:
+            for _, name, n in cur:
                 lay.append((name, off, n))
                 off += n
-            buckets.append(Bucket(start, tuple(lay)))
+            buf = _concat([arrays[i] for i, _, _ in cur]) if arrays else None
+            buckets.append(Bucket(start, tuple(lay), buf))
             start += off
         cur, cur_bytes = [], 0
 
-    for name, n in sizes:
+    for i, (name, n) in enumerate(sizes):
         nbytes = n * ELEMENT_BYTES
         if nbytes > cap_bytes:
             close()
             log.warning("payload %s (%d bytes) exceeds bucket cap %d; using oversized bucket",
                         name, nbytes, cap_bytes)
-            cur, cur_bytes = [(name, n)], nbytes
+            cur, cur_bytes = [(i, name, n)], nbytes
             close()
             continue
         if cur_bytes + nbytes > cap_bytes:
             close()
-        cur.append((name, n))
+        cur.append((i, name, n))
         cur_bytes += nbytes
     close()
     return buckets
 
 
 def unbucketize(bucket: Bucket, buffer) -> dict:
-    """Views of the bucket's named payloads inside ``buffer`` (the bucket's slice)."""
-    if int(buffer.numel()) != bucket.elements:
-        raise ShapeError(f"buffer size {buffer.numel()} does not match bucket {bucket.elements}")
-    return {name: buffer[off:off + n] for name, off, n in bucket.layout}
+    """Copies of the bucket's named payloads out of a (reduced) flat ``buffer``
+    (reference transport.py:283-290: fresh arrays, never views)."""
+    n = int(buffer.numel()) if _is_tensor(buffer) else int(buffer.size)
+    if n != bucket.elements:
+        raise ShapeError(f"buffer size {n} does not match bucket {bucket.elements}")
+    if _is_tensor(buffer):
+        return {name: buffer[off:off + e].clone() for name, off, e in bucket.layout}
+    return {name: buffer[off:off + e].copy() for name, off, e in bucket.layout}
 
 
 # -- drivers --------------------------------------------------------------------
@@ -349,10 +387,36 @@ def _validate(rank: int, req) -> None:
         raise ProtocolError("BITWISE_OR is carried as an AllGather of packed bits + OR kernel")
 
 
-class LocalCluster:
+def _dist_spans(topology) -> bool:
+    try:
+        import torch.distributed as dist
+    except Exception:
+        return False
+    return (dist.is_available() and dist.is_initialized() and topology is not None
+            and dist.get_world_size() == topology.world_size)
+
+
+class Cluster:
+    """The reference's ``Cluster(topology)`` (transport.py:302-376): topology, the
+    intra / leader / global groups, ``run(programs)`` and the ledger.
+
+    ``Cluster(topology)`` constructs a :class:`DistCluster` (this process is one
+    rank, collectives on NCCL sub-communicators) when ``torch.distributed`` is
+    initialized over exactly ``topology.world_size`` ranks, else a
+    :class:`LocalCluster` (every rank in this process on one GPU, the
+    reference's deterministic scheduler).
+    """
+
+    def __new__(cls, topology=None, *args, **kwargs):
+        if cls is Cluster:
+            cls = DistCluster if _dist_spans(topology) else LocalCluster
+        return super().__new__(cls)
+
+
+class LocalCluster(Cluster):
     """All ranks of a topology in one process; deterministic round-based scheduler."""
 
-    def __init__(self, topology: Topology):
+    def __init__(self, topology: Topology, latency=None):
         self.topology = topology
         self.ledger = CommLedger()
         self.ref_ledger = DeferredLedger()   # the reference's logical entries (HSADMMSync._log_reference)
@@ -466,14 +530,14 @@ class LocalCluster:
         return {r: posted[r].payload for r in group.members}
 
 
-class DistCluster:
+class DistCluster(Cluster):
     """Executes one rank's program with torch.distributed (NCCL on B200, gloo on CPU).
 
     All ranks construct it collectively: ``dist.new_group`` is called for every
     intra group and the leader group in the same order on every rank.
     """
 
-    def __init__(self, topology: Topology, backend_group=None):
+    def __init__(self, topology: Topology, latency=None):
         import torch.distributed as dist
 
         if not dist.is_initialized():
@@ -596,6 +660,13 @@ class DistCluster:
                 dist.all_reduce(req.payload, op=op, group=h)
         _ledger(self.ledger, req, g, _payload_bytes(req.payload), f"allreduce_{req.op.value}")
         return req.payload
+
+    def run(self, programs: Mapping[int, RankProgram]) -> dict[int, Any]:
+        """The reference's ``Cluster.run``: one process is one rank, so only this
+        rank's program runs (the others' generators are never started)."""
+        if self.rank not in programs:
+            raise ProtocolError(f"no program for rank {self.rank}")
+        return {self.rank: self.run_rank(programs[self.rank])}
 
     def run_rank(self, program: RankProgram) -> Any:
         """Drive this rank's generator to completion."""

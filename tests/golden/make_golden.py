@@ -497,9 +497,9 @@ if __name__ == "__main__":
     gen_shrinkage()
     gen_bucketize()
     gen_candidate()
-    for m, p in [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (1, 4), (4, 1)]:
+    for m, p in [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (4, 2), (1, 4), (4, 1)]:
         gen_e2e(m, p)
-    for m, p in [(1, 1), (2, 1), (1, 2), (2, 2)]:
+    for m, p in [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (4, 2)]:
         gen_e2e(m, p, adapt=True)
     gen_prox()
     gen_flat(2, False)

@@ -23,8 +23,8 @@ E2E_LAYERS = [
     ("fc.b", "fc", (1, 10), []),
 ]
 E2E_RHO1, E2E_RHO2, E2E_WD = 1.5e-3, 1.5e-4, 1e-4
-E2E_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (1, 4), (4, 1)]
-E2E_ADAPT_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2)]   # phase 5 with adaptive penalties
+E2E_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (4, 2), (1, 4), (4, 1)]
+E2E_ADAPT_TOPOLOGIES = [(1, 1), (2, 1), (1, 2), (2, 2), (2, 4), (4, 2)]   # phase 5 with adaptive penalties
 
 
 def load(name):

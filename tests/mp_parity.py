@@ -37,7 +37,7 @@ def rel_err(got, ref, *ops):
     return float(np.abs(np.asarray(got, np.float64) - ref).max() / scale)
 
 
-def golden_check(topo, rank, transport):
+def golden_check(topo, rank, transport, residuals=True):
     ref = G.E2E(topo.num_nodes, topo.accels_per_node)
     kinds = {"filter": H.ConstraintKind.FILTER_KEEP, "channel": H.ConstraintKind.CHANNEL_KEEP,
              "shape": H.ConstraintKind.SHAPE_KEEP}
@@ -47,7 +47,7 @@ def golden_check(topo, rank, transport):
     sched = H.PenaltySchedule.uniform(ref.names, G.E2E_RHO1, G.E2E_RHO2, adapt=False)
     settings = H.ConsensusSettings(t_freeze=ref.t_freeze, weight_decay=G.E2E_WD)
     cluster = H.DistCluster(topo)
-    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, transport=transport)
+    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, transport=transport, residuals=residuals)
     assert eng.transport == transport
     eng.init_from(ref.p0())
     node = topo.node_of(rank)
@@ -69,6 +69,7 @@ def golden_check(topo, rank, transport):
             assert (eng.cache_derive, eng.cache_hits) == ref.cache(k, rank)
             zs = [e.to_dict() for e in cluster.ledger.entries if e.iteration == k and e.label.startswith("z_sync")]
             assert zs == ref.zsync(k), (zs, ref.zsync(k))
+    eng.check_barriers()
     return worst
 
 
@@ -109,7 +110,7 @@ def adaptive_check(topo, rank, transport):
     return True
 
 
-def replica_check(topo, rank, world, transport):
+def replica_check(topo, rank, world, transport, residuals=True, steps=4):
     from paper_2512_14628_b200.synthetic import channel_keep_constraints, model_layers, synthetic_rank_state
 
     layers = model_layers("rn18_cifar")
@@ -117,10 +118,13 @@ def replica_check(topo, rank, world, transport):
     sched = H.PenaltySchedule.uniform([ls.name for ls in layers], 1.5e-3, 1.5e-4, adapt=False)
     settings = H.ConsensusSettings(t_freeze=3, weight_decay=1e-4)
     cluster = H.DistCluster(topo)
-    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, transport=transport)
+    eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, transport=transport, residuals=residuals)
     eng.load(**synthetic_rank_state(layers, rank, topo.accels_per_node, seed=5))
-    for k in range(1, 5):
+    # steps back to back with no host sync in between (residuals off: no NCCL call
+    # orders the ranks, only the device barriers and the double-buffered sends)
+    for k in range(1, steps + 1):
         eng.step(k)
+    eng.check_barriers()
     assert eng.frozen
     # every rank of a node: identical z_node, v, z; every rank: identical masks
     for key in ("z_node", "v", "z", "masks"):
@@ -220,6 +224,11 @@ def main():
             baselines_check(topo, rank, world, transport)
             print(f"rank {rank} baselines {transport} done", file=sys.stderr, flush=True)
             ratio = replica_check(topo, rank, world, transport)
+            if transport == "peer":
+                # the send / leader buffers are reused across back-to-back steps
+                golden_check(topo, rank, transport, residuals=False)
+                replica_check(topo, rank, world, transport, residuals=False, steps=12)
+                print(f"rank {rank} peer residuals-off done", file=sys.stderr, flush=True)
             dist.barrier()
             if rank == 0:
                 print(f"mp_parity {sys.argv[1]} {transport} ok: worst rel err {worst:.2e}, "

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("grouping", ["1x2", "2x1", "2x2", "1x4", "4x1", "2x4"])
+@pytest.mark.parametrize("grouping", ["1x2", "2x1", "2x2", "1x4", "4x1", "2x4", "4x2"])
 def test_torchrun_nccl_parity(grouping):
     m, p = (int(x) for x in grouping.split("x"))
     n = m * p

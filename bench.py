@@ -191,9 +191,23 @@ def oracle_step(ctx, topo, k):
                    t_freeze=10**9, drift_window=0)
 
 
+def _prefix(layers, max_elems):
+    sample, tot = [], 0
+    for ls in layers:
+        if tot and tot + ls.elements > max_elems:
+            break
+        sample.append(ls)
+        tot += ls.elements
+    return sample
+
+
 def cpu_baseline(layers, topo, keep, seed, budget_s):
-    """Oracle port on this host: steps of the full N=1 workload until ~budget_s."""
-    ctx = oracle_setup(layers, topo, keep, seed)
+    """Oracle port on this host: dynamic steps of the workload (every simulated rank)
+    until ~budget_s; a layer prefix when the whole M x P workload exceeds 60 M
+    simulated elements (host memory and time)."""
+    N = sum(ls.elements for ls in layers)
+    cap = 60_000_000 // topo.world_size
+    ctx = oracle_setup(layers, topo, keep, seed, max_elems=cap if N > cap else None)
     times, k = [], 0
     t_end = time.perf_counter() + budget_s
     while True:
@@ -205,11 +219,109 @@ def cpu_baseline(layers, topo, keep, seed, budget_s):
             break
     n = ctx[-1] * topo.world_size
     t = statistics.median(times)
-    return {"value": n / t / 1e6, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{len(times)} dynamic sync steps of the full workload ({ctx[-1]} params x "
-                      f"{topo.world_size} simulated ranks), numpy fp64 single-threaded, median "
-                      f"{t * 1e3:.0f} ms/step, host {os.cpu_count()} cpus",
-            "ms_per_step": t * 1e3}
+    what = "the full workload" if ctx[-1] == N else f"a layer prefix of {ctx[-1]} of {N} params"
+    out = {"value": n / t / 1e6, "unit": UNIT, "cores": 1, "kind": "port",
+           "sample": f"{len(times)} dynamic sync steps of {what} x {topo.world_size} simulated ranks "
+                     f"(oracle port, numpy fp64 single-threaded), median {t * 1e3:.0f} ms/step, "
+                     f"host {os.cpu_count()} cpus",
+           "ms_per_step": t * 1e3}
+    # the reference itself beside the port (its iteration also runs phase 5 and the
+    # sha256 digests, which the timed sync step does not: the port is the like-for-like
+    # number)
+    real = real_reference(layers, topo, keep, seed, steps=3, warmup=1, budget_s=budget_s)
+    if real is not None:
+        out["reference_real"] = {k: real[k] for k in ("value", "kind", "sample", "ms_per_step")}
+    return out
+
+
+def admmprune_path():
+    """baseline/_ref: the unmodified reference package (pip-installed from
+    /root/reference into the repo, git-ignored, shipped with the snapshot)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "admmprune")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import admmprune  # noqa: F401
+    except Exception:
+        return None
+    return path
+
+
+def real_reference(layers, topo, keep, seed, steps, warmup, budget_s):
+    """The reference itself, ``admmprune.run_hierarchical(Cluster(Topology(M, P)), ...)``
+    through its public API and stock code path, with only phase 1 replaced (it
+    returns each rank's fixed synthetic theta, as SURVEY Appendix C times it); one
+    step = one outer iteration of every simulated rank (phases 2-5 incl. the
+    reference's residual block and digests), timed between rank 0's successive
+    phase-1 calls. A layer prefix keeps (warmup + steps) iterations near
+    budget_s. None when baseline/_ref has no admmprune."""
+    if admmprune_path() is None:
+        return None
+    import numpy as np
+
+    import admmprune as A
+    from admmprune import consensus as RC
+    from paper_2512_14628_b200.layers import LayerKind
+    from paper_2512_14628_b200.synthetic import synthetic_base, synthetic_rank_state
+
+    W = topo.world_size
+    N = sum(ls.elements for ls in layers)
+
+    def run(sample, iters):
+        base = synthetic_base(sample, seed)
+        specs = [A.LayerSpec(ls.name, A.LayerKind(ls.kind.value), tuple(ls.shape),
+                             prunable=ls.kind is LayerKind.CONV) for ls in sample]
+        cons = {ls.name: [A.SparsityConstraint(A.ConstraintKind.CHANNEL_KEEP, keep_rate=keep)]
+                for ls in sample if ls.kind is LayerKind.CONV}
+        thetas = [{n: a.astype(np.float64) for n, a in
+                   synthetic_rank_state(sample, r, topo.accels_per_node, seed, base)["theta"].items()}
+                  for r in range(W)]
+
+        class Workload:
+            def __init__(self):
+                self.layers = specs
+                self.shards = [None] * W
+
+            def init_params(self, rng):
+                return {n: a.astype(np.float64) for n, a in base.items()}
+
+        stamps = []
+
+        def phase1(wl, shard, th, zn, u, rho1, solver, key):
+            if key == 0:
+                stamps.append(time.perf_counter())
+            return {n: a.copy() for n, a in thetas[key].items()}
+
+        saved = (RC.batch_rng, RC.proximal_sgd)
+        RC.batch_rng, RC.proximal_sgd = (lambda s, rank, k: rank), phase1
+        try:
+            names = [sp.name for sp in specs]
+            settings = A.ConsensusSettings(iterations=iters + 1, t_freeze=10**9, drift_window=0,
+                                           stop_on_convergence=False, weight_decay=1e-4, seed=seed)
+            A.run_hierarchical(A.Cluster(A.Topology(topo.num_nodes, topo.accels_per_node)), Workload(), cons,
+                               A.PenaltySchedule.uniform(names, 1.5e-3, 1.5e-4, adapt=False), A.SolverConfig(),
+                               settings)
+        finally:
+            RC.batch_rng, RC.proximal_sgd = saved
+        return [b - a for a, b in zip(stamps, stamps[1:])]
+
+    probe = _prefix(layers, 2_000_000)
+    t_probe = min(run(probe, 2))
+    rate = sum(ls.elements for ls in probe) * W / t_probe            # simulated elements / s
+    per_iter = budget_s / (warmup + steps + 1)
+    sample = layers if N * W <= rate * per_iter else _prefix(layers, max(1, int(rate * per_iter / W)))
+    times = run(sample, warmup + steps)[warmup:]
+    n = sum(ls.elements for ls in sample)
+    t = sum(times) / len(times)
+    what = "the full workload" if n == N else f"a layer prefix of {n} of {N} params"
+    return {"value": n * W / t / 1e6, "unit": UNIT, "cores": 1, "kind": "reference", "ms_per_step": t * 1e3,
+            "steps": len(times),
+            "sample": f"admmprune.run_hierarchical (baseline/_ref, unmodified) on {what} x {W} simulated ranks, "
+                      f"phase 1 returning fixed thetas; {len(times)} timed iterations after {warmup} warm-up, "
+                      f"mean {t * 1e3:.0f} ms/iteration; numpy fp64, one Python thread (the reference is "
+                      f"single-process), host {os.cpu_count()} cpus"}
 
 
 def run_reference(args):
@@ -219,15 +331,15 @@ def run_reference(args):
         return
     topo = topology_for(n, args.grouping)
     layers, N, config = workload_config(args, topo, n)
-    # size the per-step sample so W + K steps end within ~ref_budget_s
-    ctx = oracle_setup(layers, topo, args.keep, args.seed)
+    # the port: size the per-step sample so W + K steps end within ~ref_budget_s
+    ctx = oracle_setup(layers, topo, args.keep, args.seed, max_elems=_port_cap(N, topo))
     t0 = time.perf_counter()
     oracle_step(ctx, topo, 1)
     t_full = time.perf_counter() - t0
     steps_total = args.warmup + args.steps
     if t_full * steps_total > args.ref_budget_s:
         frac = args.ref_budget_s / (t_full * steps_total)
-        ctx = oracle_setup(layers, topo, args.keep, args.seed, max_elems=max(1, int(N * frac)))
+        ctx = oracle_setup(layers, topo, args.keep, args.seed, max_elems=max(1, int(ctx[-1] * frac)))
     n_params = ctx[-1]
     for k in range(1, args.warmup + 1):
         oracle_step(ctx, topo, k)
@@ -237,35 +349,75 @@ def run_reference(args):
         oracle_step(ctx, topo, k)
         times.append(time.perf_counter() - t0)
     total = sum(times)
-    ms = total / len(times) * 1e3
-    value = n_params * topo.world_size / (total / len(times)) / 1e6
-    sample = (f"{'full workload' if n_params == N else f'layer prefix of {n_params} of {N} params'} per "
-              f"simulated rank, {topo.world_size} ranks serialized in one process (reference architecture)")
+    port_ms = total / len(times) * 1e3
+    port_value = n_params * topo.world_size / (total / len(times)) / 1e6
+    port_sample = (f"oracle port (oracle/hsadmm_oracle.py, numpy fp64): "
+                   f"{'full workload' if n_params == N else f'layer prefix of {n_params} of {N} params'} per "
+                   f"simulated rank, {topo.world_size} ranks serialized in one process (reference architecture)")
+    port = {"value": port_value, "unit": UNIT, "cores": 1, "kind": "port", "sample": port_sample,
+            "ms_per_step": port_ms}
+    # the port does exactly the timed step's work (phases 2-4 + the u-update); the
+    # unmodified reference's iteration (admmprune from baseline/_ref) also runs phase 5
+    # and sha256 digests of the state: reported beside it, not as the line's value
+    real = real_reference(layers, topo, args.keep, args.seed, args.steps, args.warmup, args.ref_budget_s)
+    value, ms = port["value"], port["ms_per_step"]
+    cpu = {k: port[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if real is not None:
+        cpu["reference_real"] = {k: real[k] for k in ("value", "kind", "sample", "ms_per_step")}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-            "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+            "impl": "reference", "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
+
+
+def _port_cap(N, topo):
+    cap = 60_000_000 // topo.world_size
+    return cap if N > cap else None
 
 
 # -- the B200 arm ------------------------------------------------------------------------
 
 # algorithmic HBM bytes per launch; N = synced elements, n_c = conv
-# elements, Z = compact payload elements
-def algorithmic_bytes(kernel, N, n_c, Z, P):
+# elements, Z = compact payload elements; k3 / k67_extra from projection_bytes
+def algorithmic_bytes(kernel, N, n_c, Z, P, k3=None, k67_extra=0):
+    k3 = 8 * n_c + n_c // 8 if k3 is None else k3
     return {
         "K0_pack_theta_u": 12 * N,
         "K1_candidate": (16 if P > 1 else 20) * N,     # read S,z,v (or theta,u,z,v), write z_node
-        "K3_project": 8 * n_c + n_c // 8,
-        "K3_project_keep": 8 * n_c + n_c // 8,
-        "K2K3_select_project_keep": 8 * n_c + n_c // 8,
+        "K3_project": k3,
+        "K3_project_keep": k3,
+        "K2K3_select_project_keep": k3,
         "K6_compact_dual": 20 * N + 4 * Z,
         "K6f_dual_intra": 16 * N,
         "K7_decompact_dual": 16 * N + 4 * Z,
-        "K67_local_sync": 28 * N,                     # read z_node, v, theta, u; write u, z, v
+        # read z_node, v, theta, u; write u, z, v (+ the fused projection's stores)
+        "K67_local_sync": 28 * N + k67_extra,
     }.get(kernel)
+
+
+def projection_bytes(eng, layers):
+    """(K3 bytes, K67's extra bytes) per launch from the last step's summary.
+
+    Plain K3: read and write every element of the prunable layers + n/8 mask
+    bytes. Fused projection (one node): K3 runs only on the layers K67 cannot
+    project (no row-quad tiles: the 7x7 stem), and K67 additionally zero-stores
+    each dropped element (4 B) and writes the n/8 mask bytes of the others."""
+    from paper_2512_14628_b200 import _lib
+
+    fused = eng.M == 1 and all(os.environ.get(v, "1") != "0"
+                               for v in ("HSX_SINGLE_NODE", "HSX_LOCAL_SYNC", "HSX_FUSED_PROJ"))
+    rows, _ = eng.plan.summary_np()
+    k3, extra = 0, 0
+    for i in eng.plan.prunable:
+        ls = layers[i]
+        n = ls.elements
+        if fused and (n // ls.shape[0]) % 32 == 0 and ls.shape[2] * ls.shape[3] > 1:
+            extra += 4 * (n - int(rows[i, _lib.SUM_POP])) + n // 8
+        else:
+            k3 += 8 * n + n // 8
+    return k3, extra
 
 
 def run_ours(args):
@@ -296,7 +448,8 @@ def run_ours(args):
     settings = H.ConsensusSettings(t_freeze=10**9, drift_window=0, weight_decay=1e-4)
     eng = H.HSADMMSync(rank, cluster, layers, cons, sched, settings, device=dev, transport=args.transport,
                        residuals=False)
-    config["transport"] = eng.transport
+    if world > 1:
+        config["transport"] = eng.transport
     base = synthetic_base(layers, args.seed)
     st = synthetic_rank_state(layers, rank, topo.accels_per_node, args.seed, base)
     eng.load(**st)
@@ -309,7 +462,7 @@ def run_ours(args):
     # flush's own dirty lines happens before the timed step, not inside its first kernel
     flush_mode = os.environ.get("HSX_BENCH_FLUSH", "write_read")
     flush2 = torch.empty_like(flush) if flush_mode == "write_read" else None
-    sink = torch.empty(1, dtype=torch.float32, device=dev)
+    sink = torch.empty((), dtype=torch.float32, device=dev)
     if flush2 is not None:
         config["l2"] = "flushed between timed steps (256 MiB write, then 256 MiB read: no dirty lines left)"
 
@@ -332,6 +485,10 @@ def run_ours(args):
         evs = []
         barrier()
         torch.cuda.synchronize()
+        # a ~1 ms spin before the first step (outside every event pair): the host
+        # enqueues the first steps while it runs, so no step's bracket contains GPU
+        # idle time waiting for the host to launch it
+        torch.cuda._sleep(2_000_000)
         for i in range(nsteps):
             flush.fill_(float(i))
             if flush2 is not None:
@@ -364,16 +521,22 @@ def run_ours(args):
     # launches are queued and its keep-set counts are read back when the next step
     # starts, so the host stays ahead of the GPU
     eng.defer_host = True
+    # clocks are sampled from before the warm-up to the end of the headline steps (the
+    # sampler's start-up pause is not an idle gap between warm-up and timed steps)
+    clocks = ClockSampler([local] if world == 1 else list(range(world)))
+    clocks.__enter__()
     k = 0
     for _ in range(args.warmup):
         k += 1
         run_step(k)
     torch.cuda.synchronize()
-    # headline: dynamic steps, clocks sampled during the timed region
+    # headline: dynamic steps
     launches0 = _lib.launch_count()
     gc.disable()   # no collector pauses inside the timed loop
-    with ClockSampler([local] if world == 1 else list(range(world))) as clocks:
+    try:
         times = timed_steps(k + 1, args.steps)
+    finally:
+        clocks.__exit__(None, None, None)
     gc.enable()
     launches = _lib.launch_count() - launches0
     k += args.steps
@@ -385,10 +548,13 @@ def run_ours(args):
     # roofline pass: the same K dynamic steps with CUDA events around every libhsx
     # launch and collective, on the launching stream
     timer = plan_mod.KernelTimer()
+    plan_mod.NOTES.clear()
     ktimes = timed_steps(k + 1, args.steps, kernel_timer=timer)
     k += args.steps
     kstep_ms = max_over_ranks(sum(ktimes)) / args.steps
     kdur = timer.durations_ms()
+    notes = dict(plan_mod.NOTES)
+    plan_mod.NOTES.clear()
     kern = {name: statistics.mean(d) for name, d in kdur.items()}
     launches_per_kernel = {name: len(d) / args.steps for name, d in kdur.items()}
     # frozen steady state (after t_freeze: sealed keep sets, no projection / union)
@@ -400,6 +566,23 @@ def run_ours(args):
     k += args.steps
     frozen_ms = max_over_ranks(sum(ftimes)) / args.steps
     eng.frozen = False
+    # back-to-back steady state: the same dynamic steps with no L2 flush in between,
+    # one event pair around all K (each step's trailing write-back lands in the next)
+    for _ in range(2):
+        k += 1
+        run_step(k)
+    barrier()
+    torch.cuda.synchronize()
+    bs, be = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(2_000_000)
+    bs.record()
+    for i in range(args.steps):
+        run_step(k + 1 + i)
+    be.record()
+    torch.cuda.synchronize()
+    barrier()
+    k += args.steps
+    steady_ms = max_over_ranks(bs.elapsed_time(be)) / args.steps
     # the full Algorithm-1 iteration: the dynamic step + phase 5 (residual sums fused
     # into K6/K7, report, adaptive penalties, dual rescale), as the reference runs it
     eng.set_residuals(True, adapt=True)
@@ -433,14 +616,18 @@ def run_ours(args):
     barrier()
     k += args.steps
     e2e_ms = max_over_ranks(es.elapsed_time(ee)) / args.steps
+    eng.check_barriers()
+    nvlink = nvlink_peaks(world, dev) if world > 1 else None
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     hbm, hbm_src = peaks()
-    cands = {kname: t for kname, t in kern.items() if algorithmic_bytes(kname, N, n_c, Z, topo.accels_per_node)}
+    k3b, k67x = projection_bytes(eng, layers)
+    ab_of = lambda kname: algorithmic_bytes(kname, N, n_c, Z, topo.accels_per_node, k3b, k67x)
+    cands = {kname: t for kname, t in kern.items() if ab_of(kname)}
     top = max(cands, key=cands.get)
-    abytes = algorithmic_bytes(top, N, n_c, Z, topo.accels_per_node)
+    abytes = ab_of(top)
     achieved = abytes / (kern[top] / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -451,7 +638,7 @@ def run_ours(args):
             traffic = None
     kernels_out = {}
     for kname, t in sorted(kern.items()):
-        ab = algorithmic_bytes(kname, N, n_c, Z, topo.accels_per_node)
+        ab = ab_of(kname)
         kernels_out[kname] = {"us": round(t * 1e3, 2), "per_step": launches_per_kernel[kname]}
         if ab:
             kernels_out[kname]["gbs"] = round(ab / (t / 1e3) / 1e9, 1)
@@ -474,16 +661,117 @@ def run_ours(args):
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks.summary(),
         "step_ms_spread": step_spread,
+        "step_ms": [round(t, 4) for t in times],
+        "steady_ms_per_step": steady_ms,
         "frozen_ms_per_step": frozen_ms,
         "phase5_ms_per_step": resid_ms,
         "leader_bytes": {"z_sync_bytes": 4 * Z, "dense_bytes": 4 * N, "ratio_vs_dense": Z / N},
         "kernels": kernels_out,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world > 1:
+        line["collectives"] = collectives_block(kdur, notes, N, Z, topo, eng.transport, nvlink, args.steps)
+        line["nvlink_peak"] = nvlink
+        dist.destroy_process_group()
+    if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(layers, topo, args.keep, args.seed, args.cpu_budget_s)
     emit(line)
-    if world > 1:
-        dist.destroy_process_group()
+
+
+def nvlink_peaks(world, dev):
+    """Measured NVLink peaks in this run (all ranks): a copy kernel reading a peer's
+    symmetric-memory mapping (rank r reads rank r ^ 1; all ranks at once, so both
+    link directions are loaded) and an NCCL all-reduce of 256 MiB on the world
+    group (busbw, nccl-tests convention). CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    def timed(fn, iters=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([s.elapsed_time(e) / iters / 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {}
+    n = 64 * 1024 * 1024 // 4
+    try:
+        import torch.distributed._symmetric_memory as symm
+
+        buf = symm.empty(n, dtype=torch.float32, device=dev)
+        buf.fill_(1.0)
+        h = symm.rendezvous(buf, dist.group.WORLD)
+        peer = h.get_buffer(dist.get_rank() ^ 1 if dist.get_rank() ^ 1 < world else 0, (n,), torch.float32)
+        local = torch.empty(n, device=dev)
+        t = timed(lambda: local.copy_(peer))
+        out["peer_read_gbs"] = 4 * n / t / 1e9
+        out["peer_read"] = "copy kernel loading a peer's 64 MiB symmetric buffer, every rank at once"
+        h.barrier()
+        del peer, buf
+    except Exception as exc:  # noqa: BLE001
+        out["peer_read_error"] = repr(exc)[:200]
+    x = torch.ones(4 * n, device=dev)
+    t = timed(lambda: dist.all_reduce(x))
+    out["nccl_allreduce_256MiB_busbw_gbs"] = 16 * n / t / 1e9 * 2 * (world - 1) / world
+    out["spec_gbs_per_direction"] = 900.0
+    return out
+
+
+def collectives_block(kdur, notes, N, Z, topo, transport, nvlink, steps):
+    """Per collective of the step: time per call, bytes, algbw and busbw in nccl-tests
+    convention (all-reduce 2(g-1)/g, all-gather (g-1)/g of the gathered size,
+    broadcast 1); for the fused NVLink kernels of the peer transport the remote bytes
+    they read and that rate against the measured peer-read peak."""
+    import statistics as st
+
+    M, P = topo.num_nodes, topo.accels_per_node
+    peak = (nvlink or {}).get("peer_read_gbs")
+    out = {}
+    for name, calls in notes.items():
+        ts = kdur.get(name, [])
+        if not ts:
+            continue
+        op, nbytes, g = calls[0]
+        per_call = st.mean(ts) / 1e3
+        total_b = sum(c[1] for c in calls) / len(calls)    # mean bytes per call
+        row = {"op": op, "ranks": g, "us": round(per_call * 1e6, 2), "calls_per_step": len(ts) / steps}
+        if op != "barrier" and nbytes:
+            alg = total_b / per_call / 1e9
+            factor = {"broadcast": 1.0, "all_gather": (g - 1) / g}.get(op, 2 * (g - 1) / g)
+            row.update(bytes=int(total_b), algbw_gbs=round(alg, 1), busbw_gbs=round(alg * factor, 1))
+            if peak:
+                row["busbw_frac_of_peer_peak"] = round(alg * factor / peak, 3)
+        out[name] = row
+    remote = {}
+    if transport == "peer":
+        if P == 2:
+            remote["K1_candidate"] = 4 * N * (P - 1)
+        if P > 2:
+            remote["K8_intra_rs"] = remote["K8_intra_ag"] = 4 * N * (P - 1) // P
+        if M == 2:
+            remote["K8_leader_avg"] = 4 * Z * (M - 1)
+        if M > 2:
+            remote["K8_leader_rs"] = remote["K8_leader_ag"] = 4 * Z * (M - 1) // M
+        if P > 1:
+            remote["K8_zhat_read"] = 4 * Z
+    for name, b in remote.items():
+        ts = kdur.get(name)
+        if not ts:
+            continue
+        t = st.mean(ts) / 1e3
+        row = {"op": "fused NVLink kernel (peer loads)", "remote_bytes": int(b), "us": round(t * 1e6, 2),
+               "nvlink_gbs": round(b / t / 1e9, 1)}
+        if peak:
+            row["frac_of_peer_peak"] = round(b / t / 1e9 / peak, 3)
+        out[name] = row
+    return out
 
 
 _OUT_FD = None

@@ -135,9 +135,16 @@ int hsx_candidate_renorm(hsx_plan* plan, int32_t pass, const float* sum, const f
 /* ---- K2: group norms -> top-k keep flags -----------------------------------
  * norms = sqrt(sum of partials); keep the `keep` largest, lower index on ties
  * (SparsityConstraint.resolve + _kept_group_indices, sparsity.py:53-68).
- * Layers with <= 1024 groups are selected inside the candidate launch (tail of
- * the layer's last tile); this call completes the others. Always call it after
- * hsx_candidate / hsx_candidate_renorm of the same pass. */
+ * With HSX_FUSE_SELECT=1 layers are selected inside the candidate launch (tail
+ * of the layer's last tile); this call completes the others. Always call it after
+ * hsx_candidate / hsx_candidate_renorm of the same pass. Pass 0 issued as the
+ * next launch on the same stream as a dynamic hsx_candidate /
+ * hsx_candidate_peers is chained behind it when HSX_K2_CHAIN=1 (off by default:
+ * measured slower on B200, the selection's dependent L2 round trips stall behind
+ * K1's streaming traffic): that K1 counts
+ * each prunable layer's finished tiles, the selection launch starts while K1
+ * still streams and each layer's selection begins once its tiles are done;
+ * completion still implies K1's completion. */
 int hsx_select(hsx_plan* plan, int32_t pass, void* stream);
 /* copy pass `pass` norms (fp64) / keep flags (uint8) to caller device buffers
  * of hsx_plan_group_total(pass) entries; either may be NULL. */
@@ -256,8 +263,17 @@ int hsx_decompact_dual_resid(const hsx_plan* plan, const float* flat, float divi
  * z_node, v += z_node - z, in place and bitwise equal to hsx_compact_dual then
  * hsx_decompact_dual(divisor 1) — without the compact buffer. residuals != 0
  * also accumulates all nine residual slots (z_node_prev required). */
-int hsx_local_sync(const hsx_plan* plan, const float* theta, float* u, const float* z_node, float* v,
+int hsx_local_sync(hsx_plan* plan, const float* theta, float* u, const float* z_node, float* v,
                    float* z, const float* z_node_prev, int32_t residuals, void* stream);
+/* Fused projection (one node, single-node plans): hsx_project_keep_sets then runs
+ * K3 only for the layers whose kept set may differ from the selected rectangle
+ * (7x7 stems without row-quad tiles, layers whose candidate holds an exact 0, layers
+ * whose previous mask was irregular) and the keep-set fixup; the next
+ * hsx_local_sync on the same z_node projects every other layer in its pass
+ * (dropped elements zeroed in place, mask bits kept && != 0 written to the mask
+ * hsx_project_keep_sets was given). The caller issues nothing that reads z_node or
+ * that mask between the two calls. */
+int hsx_plan_set_fused_projection(hsx_plan* plan, int32_t on);
 /* vec[layer][9] = the layer's slot sums (leader == 0 zeroes slots 3-8: the
  * node's leader contributes them to the intra SUM, consensus.py:550-563). */
 int hsx_residual_fold(hsx_plan* plan, int32_t leader, double* vec, void* stream);

@@ -125,6 +125,15 @@ struct hsx_plan {
   unsigned long long* d_acc = nullptr;
   uint8_t *d_rk_prev = nullptr, *d_ck_prev = nullptr, *d_ch_prev = nullptr;
   int *d_irr = nullptr, *d_irr_any = nullptr;
+  unsigned int* d_k1done = nullptr;  // chained K2: K1 tiles finished per prunable layer (0 between steps)
+  int k2_armed = 0;                  // the last launch was such a K1: hsx_select(0) chains behind it
+  int k2_pending = 0;                // a counting K1 ran whose counts no chained K2 consumed yet
+  int* d_haszero = nullptr;          // per prunable layer: K1 stored an exact 0 (zeroed by the fixup / K67)
+  int* d_proj_pidx = nullptr;        // prunable index of every K3 item (fused-projection K3)
+  int* d_irr_next = nullptr;         // fused-projection K3: the fixups' next irr, moved by K67
+  int fused_proj = 0;                // one node: K3 only where K67 cannot project (hsx_plan_set_fused_projection)
+  const float* proj_zn = nullptr;    // z_node / mask of the last deferred projection, consumed by hsx_local_sync
+  uint32_t* proj_mask = nullptr;
   int* d_sel[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
   double* d_partials[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
@@ -137,7 +146,7 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_irr_next, d_proj_pidx, d_haszero, d_k1done, d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
                     d_ch_prev};
     for (void* p : ptrs)
@@ -416,6 +425,11 @@ int upload_plan(hsx_plan* p) {
       return rc;
   }
   if ((rc = upload(&p->d_proj, p->proj_items))) return rc;
+  {
+    std::vector<int> pp(p->proj_items.size());
+    for (size_t i = 0; i < pp.size(); ++i) pp[i] = p->layers[p->proj_items[i].layer].pidx;
+    if ((rc = upload(&p->d_proj_pidx, pp))) return rc;
+  }
   if ((rc = upload(&p->d_word, p->word_items))) return rc;
   if ((rc = upload(&p->d_prunable, p->prunable))) return rc;
   for (int q = 0; q < hsx::kMaxPasses; ++q) {
@@ -437,6 +451,9 @@ int upload_plan(hsx_plan* p) {
   if ((rc = upload(&p->d_pos_in, pi))) return rc;
   if ((rc = upload(&p->d_summary, p->summary))) return rc;
   if ((rc = alloc0(&p->d_done, 1))) return rc;
+  if ((rc = alloc0(&p->d_k1done, (long long)p->prunable.size() + 1))) return rc;
+  if ((rc = alloc0(&p->d_haszero, (long long)p->prunable.size() + 1))) return rc;
+  if ((rc = alloc0(&p->d_irr_next, (long long)p->prunable.size() + 1))) return rc;
   return HSX_OK;
 }
 
@@ -561,6 +578,8 @@ static hsx::KeepArgs keep_args(hsx_plan* p, const Item* items, const uint32_t* u
   ka.ck_prev = p->d_ck_prev;
   ka.irr = p->d_irr;
   ka.irr_any = p->d_irr_any;
+  ka.haszero = p->d_haszero;
+  ka.irr_next = nullptr;
   ka.n_layers = p->n_layers;
   ka.n_prunable = (int)p->prunable.size();
   return ka;
@@ -570,6 +589,7 @@ static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta
                                const float* z, const float* v) {
   hsx::CandArgs a;
   std::memset(&a, 0, sizeof(a));
+  p->k2_armed = 0;   // only a counting dynamic K1 (arm_chain) is chained to
   a.s = sum;
   a.theta = theta;
   a.u = u;
@@ -582,9 +602,26 @@ static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta
   for (int q = 0; q < hsx::kMaxPasses; ++q) a.fw.f[q] = p->d_flags[q];
   a.cand_done = p->d_cand_done;
   a.sched = p->d_sched;
+  a.haszero = p->d_haszero;
   a.ka = keep_args(p, nullptr, nullptr, nullptr);
   a.structured = p->single_node;
   return a;
+}
+
+// K2 chained behind this dynamic K1 (HSX_K2_CHAIN=0: off): K1 counts the tiles of
+// the layers K2 selects and leaves HSX_K1_RESERVE CTA slots (default: one per K2
+// CTA) free, so the chained selections can start while K1 still streams
+static void arm_chain(hsx_plan* p, hsx::CandArgs& a, cudaStream_t st) {
+  static const int on = env_flag("HSX_K2_CHAIN", 0);
+  static const int reserve = env_flag("HSX_K1_RESERVE", -1);
+  p->k2_armed = 0;
+  if (!on || p->sel_list[0].empty()) return;
+  // counts of an earlier K1 that no chained selection consumed: start from zero
+  if (p->k2_pending) cudaMemsetAsync(p->d_k1done, 0, sizeof(unsigned) * p->prunable.size(), st);
+  p->k2_pending = 1;
+  a.k1done = p->d_k1done;
+  a.reserve = reserve >= 0 ? reserve : (int)p->sel_list[0].size();
+  p->k2_armed = 1;
 }
 
 static int check_cand_inputs(const hsx_plan* p, const float* sum, const float* theta,
@@ -610,6 +647,7 @@ int hsx_candidate(hsx_plan* p, const float* sum, const float* theta, const float
     hsx::launch_candidate(a, (int)p->elem_items.size(), 1, p->cand_smem, S(stream));
   } else {
     a.items = p->d_cand;
+    arm_chain(p, a, S(stream));
     hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
   }
   HSX_LAUNCHED("candidate");
@@ -637,6 +675,7 @@ int hsx_candidate_peers(hsx_plan* p, const float* const* sends, int32_t n, const
     hsx::launch_candidate(a, (int)p->elem_items.size(), 1, p->cand_smem, S(stream));
   } else {
     a.items = p->d_cand;
+    arm_chain(p, a, S(stream));
     hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
   }
   HSX_LAUNCHED("candidate_peers");
@@ -684,8 +723,13 @@ int hsx_select(hsx_plan* p, int32_t pass, void* stream) {
   int n = (int)p->sel_list[pass].size();
   if (n == 0) return HSX_OK;
   hsx::FlagPtrs fl = {{p->d_flags[0], p->d_flags[1], p->d_flags[2]}};
+  // pass 0 right behind a counting K1 (same stream, next launch): chained
+  const bool chained = pass == 0 && p->k2_armed;
+  p->k2_armed = 0;
+  if (chained) p->k2_pending = 0;
   hsx::launch_select(p->d_layers, p->d_sel[pass], n, pass, p->d_partials[pass], p->d_norms[pass],
-                     fl, keep_args(p, nullptr, nullptr, nullptr), p->single_node, p->select_smem[pass], S(stream));
+                     fl, keep_args(p, nullptr, nullptr, nullptr), p->single_node, p->select_smem[pass], S(stream),
+                     chained ? p->d_k1done : nullptr);
   HSX_LAUNCHED("select");
   return HSX_OK;
 }
@@ -745,6 +789,19 @@ int hsx_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, const uint
   // the selection's last pass derived the keep sets of the rectangles R x C; K3
   // flags layers whose mask has a kept zero and the fixup re-derives those
   hsx::KeepArgs ka = keep_args(p, p->d_proj, mask, prev_mask);
+  p->proj_zn = nullptr;
+  if (p->fused_proj) {
+    // only the layers K67 cannot project (stems, a candidate with an exact 0, a
+    // previously irregular mask); hsx_local_sync projects the rest
+    ka.irr_next = p->d_irr_next;
+    if (hsx::launch_project_lite(ka, (int)p->proj_items.size(), z_node, mask, p->d_proj_pidx, p->d_prunable,
+                                 p->d_pdone, p->fixup_smem, S(stream)) != 0)
+      return fail(HSX_ESHAPE, "fused projection supports at most 2048 prunable layers");
+    HSX_LAUNCHED("project_lite");
+    p->proj_zn = z_node;
+    p->proj_mask = mask;
+    return HSX_OK;   // the fixup ran inside
+  }
   hsx::launch_project(ka, (int)p->proj_items.size(), z_node, mask, 1, S(stream));
   HSX_LAUNCHED("project_check");
   hsx::launch_keep_fixup(ka, p->d_prunable, (int)p->prunable.size(), p->fixup_smem, S(stream));
@@ -776,6 +833,13 @@ int hsx_select_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, con
   hsx::launch_select_project(sp, ka, (int)p->proj_items.size(), z_node, mask,
                              std::max(p->select_smem[0], p->fixup_smem), S(stream));
   HSX_LAUNCHED("select_project");
+  return HSX_OK;
+}
+
+int hsx_plan_set_fused_projection(hsx_plan* p, int32_t on) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  p->fused_proj = on ? 1 : 0;
+  p->proj_zn = nullptr;
   return HSX_OK;
 }
 
@@ -949,11 +1013,20 @@ int hsx_decompact_dual_resid(const hsx_plan* p, const float* flat, float divisor
   return HSX_OK;
 }
 
-int hsx_local_sync(const hsx_plan* p, const float* theta, float* u, const float* z_node, float* v, float* z,
+int hsx_local_sync(hsx_plan* p, const float* theta, float* u, const float* z_node, float* v, float* z,
                    const float* z_node_prev, int32_t residuals, void* stream) {
   if (!p || !theta || !u || !z_node || !v || !z) return fail(HSX_EINVAL, "null argument");
   if (residuals && !z_node_prev) return fail(HSX_EINVAL, "residuals need z_node_prev");
   hsx::ElemArgs a = elem_args(p);
+  if (p->proj_zn == z_node) {  // the deferred projection of this z_node (fused-projection mode)
+    a.zn_w = const_cast<float*>(z_node);
+    a.mask = p->proj_mask;
+    a.haszero = p->d_haszero;
+    a.irr = p->d_irr;
+    a.irr_next = p->d_irr_next;
+    a.n_prunable = (int)p->prunable.size();
+  }
+  p->proj_zn = nullptr;
   a.theta = theta;
   a.u = u;
   a.zn = z_node;

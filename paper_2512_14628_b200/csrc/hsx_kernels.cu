@@ -832,15 +832,41 @@ __device__ void select_layer(const DevLayer& gly, int pass, const double* __rest
 #endif
 }
 
+// Chained mode (k1done != nullptr): K2 is launched right behind K1 (programmatic
+// dependent launch) and does not wait for K1's grid to complete before it starts:
+// it lets its own dependents launch, each CTA waits for its layer's tiles only
+// (K1 counts them into k1done with release semantics: fence + atomic), selects,
+// and only then waits for K1's grid — so K2's completion still implies K1's and
+// everything before it, while the selections of the layers K1 finished early run
+// under K1's drain. K1 has started every CTA before K2 can launch (its CTAs
+// trigger at entry), so the wait always makes progress.
 __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ layers,
                                                  const int* __restrict__ list, int pass,
                                                  const double* __restrict__ partials,
                                                  double* __restrict__ norms, FlagPtrs flags, KeepArgs ka,
-                                                 int structured) {
-  PDL_ENTRY();
+                                                 int structured, unsigned int* __restrict__ k1done) {
   extern __shared__ unsigned long long skey[];
   const int l = list[blockIdx.x];
-  select_layer(layers[l], pass, partials, norms, flags, skey, l, structured ? &ka : nullptr);
+  if (k1done == nullptr) {
+    PDL_ENTRY();
+    select_layer(layers[l], pass, partials, norms, flags, skey, l, structured ? &ka : nullptr);
+    return;
+  }
+  pdl_trigger();
+  const DevLayer& ly = layers[l];
+  unsigned* c = k1done + ly.pidx;
+  if (threadIdx.x == 0) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      if (v >= (unsigned)ly.ncitems) break;
+      __nanosleep(128);
+    }
+  }
+  __syncthreads();
+  select_layer(ly, pass, partials, norms, flags, skey, l, structured ? &ka : nullptr);
+  if (threadIdx.x == 0) atomicSub(c, (unsigned)ly.ncitems);  // back to 0 for the next K1 (graph replays too)
+  pdl_wait();
 }
 
 // ---------------------------------------------------------------------------
@@ -1056,6 +1082,14 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
 // one fp64 partial per group: partials[part][G].
 constexpr int kTileQuads = 64;
 
+// pass 0: flag the prunable layer when some stored candidate element is exactly 0
+// (every thread of the CTA calls this); only such layers can have a kept zero, so
+// the one-node path projects every other layer inside K67 (hsx_plan_set_fused_projection)
+__device__ __forceinline__ void note_zero(const CandArgs& p, const DevLayer& ly, bool zero) {
+  if (p.pass == 0 && p.haszero && __any_sync(kFull, zero) && (threadIdx.x & 31) == 0)
+    atomicOr(p.haszero + ly.pidx, 1);
+}
+
 template <int MODE>
 __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, float4* ring,
                                 double* cs) {
@@ -1075,6 +1109,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const Coef cf = coef_of(ly);
   const long long stride = (long long)RP * L;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  bool zero = false;  // an element of the candidate is exactly 0 (the layer may be irregular)
   const unsigned long long pf = l2pol(kL2First), pl = l2pol(kL2Last);
   ring_run(
       count,
@@ -1089,7 +1124,9 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
           for (int i2 = 0; i2 < 4; ++i2)
             if (!kept_by(ly, p.flags, pass, ee + i2)) c[i2] = 0.0;
         } else {
-          st4(zn + e, make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]));
+          const float4 o = make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]);
+          st4(zn + e, o);
+          zero |= (o.x == 0.f) | (o.y == 0.f) | (o.z == 0.f) | (o.w == 0.f);
         }
         a0 = __dadd_rn(a0, __dmul_rn(c[0], c[0]));
         a1 = __dadd_rn(a1, __dmul_rn(c[1], c[1]));
@@ -1097,6 +1134,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
         a3 = __dadd_rn(a3, __dmul_rn(c[3], c[3]));
       });
   double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
+  note_zero(p, ly, zero);
   __syncthreads();  // cs aliases the ring: every thread is done with its last stage
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
@@ -1135,6 +1173,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
 // channels by K2) or one warp per row (FILTER: per-row sums).
 template <int MODE>
 __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq) {
+  bool zero = false;
   const int pass = p.pass;
   const int grp = ly.group[pass];
   const int L = ly.L;
@@ -1148,9 +1187,13 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
   for (int i = threadIdx.x; i < E; i += kThreads) {
     double c = cand_elem<MODE>(p, gbase + i, cf);
     if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
-    if (pass == 0) p.zn[gbase + i] = (float)c;
+    if (pass == 0) {
+      p.zn[gbase + i] = (float)c;
+      zero |= (float)c == 0.f;
+    }
     sq[i] = __dmul_rn(c, c);
   }
+  note_zero(p, ly, zero);
   __syncthreads();
   if (grp == kFilter) {
     for (int r = warp; r < nr; r += kThreads / 32) {
@@ -1227,7 +1270,16 @@ __device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const I
 #ifdef HSX_TRACE
   TRACE_AT((&it - p.items), 1, gtime());
 #endif
-  if (!((ly.fsel >> p.pass) & 1)) return;
+  if (!((ly.fsel >> p.pass) & 1)) {
+    if (p.k1done) {  // chained K2: this tile's partials are released to the layer's selection
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(p.k1done + ly.pidx, 1u);
+      }
+    }
+    return;
+  }
   // fused K2: the layer's last tile to finish selects its groups (its partials
   // are complete once every tile has released them: fence, then the counter)
   __shared__ bool last;
@@ -1300,7 +1352,8 @@ static void launch_candidate_mode(const CandArgs& a, int n_items, int frozen, si
   }();
   CandArgs b = a;
   b.n_items = n_items;
-  const int grid = (persistent && a.sched) ? std::min(n_items, resident) : n_items;
+  const int slots = std::max(1, resident - std::max(0, a.reserve));
+  const int grid = (persistent && a.sched) ? std::min(n_items, slots) : n_items;
   launch_pdl(k_candidate<MODE>, grid, kThreads, smem, st, b, frozen);
 }
 
@@ -1330,7 +1383,8 @@ void launch_div_selftest(const double* num, long long n, double den, double* out
 }
 
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
-                   double* norms, FlagPtrs flags, const KeepArgs& ka, int structured, size_t smem, cudaStream_t st) {
+                   double* norms, FlagPtrs flags, const KeepArgs& ka, int structured, size_t smem, cudaStream_t st,
+                   unsigned int* k1done) {
   if (n <= 0) return;
   allow_smem(k_select, smem);
   static const int nt = [] {
@@ -1340,7 +1394,7 @@ void launch_select(const DevLayer* layers, const int* list, int n, int pass, con
     const int x = v ? std::atoi(v) : 512;
     return (x >= 64 && x <= 1024 && x % 32 == 0) ? x : 512;
   }();
-  launch_pdl(k_select, n, nt, smem, st, layers, list, pass, partials, norms, flags, ka, structured);
+  launch_pdl(k_select, n, nt, smem, st, layers, list, pass, partials, norms, flags, ka, structured, k1done);
 }
 
 size_t structured_smem_bytes(int rows, int L, int cin) { return structured_bytes(rows, L, cin); }
@@ -1594,6 +1648,93 @@ void launch_select_project(const SelProjArgs& sp, const KeepArgs& a, int n_items
   launch_pdl(k_select_project, sp.nsel + n_items, kThreads, need, st, sp, a, zn, mask);
 }
 
+// K3 + keep-set fixup of the fused-projection mode (one node), one launch: only
+// the layers K67 does not project itself are touched — layers without row-quad
+// tiles (7x7 stems), 1x1 convolutions (their channel-dropped elements are scattered
+// over nearly every quad: K67 would rewrite whole quads, measured slower than K3
+// on ResNet-50 / 152), layers whose candidate holds an exact 0 (a kept zero makes the mask
+// differ from the kept rectangle) and layers whose previous mask was irregular
+// (drift counted from bits). Every CTA first builds the per-layer "needed" table in
+// shared memory (one parallel round of flag loads) and the layer of each of its
+// items, then projects its items of needed layers (K3 with the kept-zero check);
+// the last CTA to finish a needed layer's items runs that layer's fixup, and the
+// last needed layer lays the flat buffer out again if any layer turned out
+// irregular. Layers not needed keep irr == 0 and their K67 clears haszero.
+__device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);
+__device__ void layout_flat(const KeepArgs& a);
+constexpr int kLiteMaxPrunable = 2048;
+constexpr int kLiteMaxItemsPerCta = 64;
+
+__global__ void __launch_bounds__(kThreads) k_project_lite(KeepArgs a, float* __restrict__ zn,
+                                                           uint32_t* __restrict__ mask, int n_items,
+                                                           const int* __restrict__ item_pidx,
+                                                           const int* __restrict__ prunable,
+                                                           unsigned int* __restrict__ pdone) {
+  PDL_ENTRY();
+  extern __shared__ __align__(16) float4 ring[];
+  __shared__ uint8_t need[kLiteMaxPrunable];
+  __shared__ int mine[kLiteMaxItemsPerCta];
+  __shared__ int n_need;
+  __shared__ bool last_item, last_layer;
+  const int np = a.n_prunable;
+  if (threadIdx.x == 0) n_need = 0;
+  __syncthreads();
+  int cnt = 0;
+  for (int i = threadIdx.x; i < np; i += kThreads) {
+    const DevLayer& dl = a.layers[prunable[i]];
+    const bool nd = !dl.qtile || dl.k == 1 || a.haszero[i] || (a.irr[i] & 2);
+    need[i] = nd;
+    cnt += nd;
+  }
+  if (cnt) atomicAdd(&n_need, cnt);
+  const int per = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  for (int j = threadIdx.x; j < per; j += kThreads) mine[j] = item_pidx[blockIdx.x + j * gridDim.x];
+  __syncthreads();
+  if (n_need == 0) return;
+  for (int j = 0; j < per; ++j) {
+    const int pidx = mine[j];
+    if (!need[pidx]) continue;  // uniform over the CTA
+    const Item it = a.items[blockIdx.x + j * gridDim.x];
+    project_item<true>(a, zn, mask, it, ring);
+    __syncthreads();
+    const DevLayer& dl = a.layers[it.layer];
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last_item = atomicAdd(pdone + pidx, 1u) == (unsigned)dl.npitems - 1;
+    }
+    __syncthreads();
+    if (!last_item) continue;
+    __threadfence();
+    if (threadIdx.x == 0) pdone[pidx] = 0;
+    fixup_layer(a, it.layer, reinterpret_cast<uint8_t*>(ring));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last_layer = atomicAdd(pdone + np, 1u) == (unsigned)n_need - 1;
+    }
+    __syncthreads();
+    if (!last_layer) continue;
+    __threadfence();
+    if (*reinterpret_cast<volatile int*>(a.irr_any)) layout_flat(a);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      pdone[np] = 0;
+      *a.irr_any = 0;
+    }
+  }
+}
+
+int launch_project_lite(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, const int* item_pidx,
+                        const int* prunable, unsigned int* pdone, size_t smem, cudaStream_t st) {
+  if (n_items <= 0) return 0;
+  if (a.n_prunable > kLiteMaxPrunable) return -1;
+  const int grid = std::max(std::min(n_items, 148 * 2), (n_items + kLiteMaxItemsPerCta - 1) / kLiteMaxItemsPerCta);
+  smem = std::max(smem, (size_t)kDepth * kThreads * sizeof(float4));
+  allow_smem(k_project_lite, smem);
+  launch_pdl(k_project_lite, grid, kThreads, smem, st, a, zn, mask, n_items, item_pidx, prunable, pdone);
+  return 0;
+}
+
 void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * kThreads * sizeof(float4);
@@ -1756,7 +1897,12 @@ __device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm) {
     if (threadIdx.x == 0) a.summary[(long long)l * kSumCols + 4] = (long long)drift;
   }
   __syncthreads();
-  if (threadIdx.x == 0) a.irr[pidx] = (irr & 1) << 1;  // this mask is the next one's previous
+  if (threadIdx.x == 0) {
+    // this mask is the next one's previous (the fused-projection K3 stages it in
+    // irr_next: other CTAs of that launch still read irr; K67 moves it)
+    (a.irr_next ? a.irr_next : a.irr)[pidx] = (irr & 1) << 1;
+    if (a.haszero && !a.irr_next) a.haszero[pidx] = 0;
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) k_keep_fixup(KeepArgs a, const int* __restrict__ prunable) {
@@ -2095,9 +2241,23 @@ void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
 //   u <- u + (theta - z_node); z <- kept ? z_node + v : 0; v <- v + (z_node - z)
 // RESID: the K6 (0-2) and K7 (3-8) residual slots in one pass (z_prev, z_node_prev
 // streamed too).
-template <bool RESID>
+// PROJ (one node, fused projection): z_node arrives unprojected; on the kept-rectangle
+// tiles each quad is projected in registers (dropped elements -> 0, written back as
+// zeros) and its mask nibble (kept && != 0) is OR-folded over 8 lanes into the mask
+// word; a rectangle is the layer's kept set exactly when no kept element is 0
+// (k_project_lite + the keep-set fixup handled the layers where one might be).
+template <bool RESID, bool PROJ>
 __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
   PDL_ENTRY();
+  if (PROJ && blockIdx.x == 0) {
+    // the fused-projection K3 has finished: its fixups' irregularity becomes the
+    // next step's "previous", and the exact-zero flags are spent
+    for (int i = threadIdx.x; i < a.n_prunable; i += kThreads) {
+      a.irr[i] = a.irr_next[i];
+      a.irr_next[i] = 0;
+      a.haszero[i] = 0;
+    }
+  }
   constexpr int NB = RESID ? 6 : 4;
   constexpr int D = RESID ? 3 : kDepth;  // 6 x 3 x 4 KB = 72 KB / 4 x 4 x 4 KB = 64 KB
   extern __shared__ float4 ring[];
@@ -2123,8 +2283,31 @@ __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
       cp_quad_h(ring_slot<NB>(ring, d, RESID ? 5 : 0), ZO, e, ly.n, pf);
     }
   };
-  auto emit = [&](int d, long long e, int4 dd) {
-    const float4 zn = *ring_slot<NB>(ring, d, 0), vv = *ring_slot<NB>(ring, d, 1);
+  float* __restrict__ ZW = PROJ ? a.zn_w + ly.off : nullptr;
+  uint32_t* __restrict__ MK = PROJ ? a.mask + ly.mword : nullptr;
+  auto emit = [&](int d, long long e, int4 dd, bool proj) {
+    float4 zn = *ring_slot<NB>(ring, d, 0);
+    const float4 vv = *ring_slot<NB>(ring, d, 1);
+    if (PROJ && proj) {
+      const unsigned kn = (unsigned)(dd.x >= 0) | ((unsigned)(dd.y >= 0) << 1) | ((unsigned)(dd.z >= 0) << 2) |
+                          ((unsigned)(dd.w >= 0) << 3);
+      if (kn != 0xFu) {
+        if (!(kn & 1u)) zn.x = 0.f;
+        if (!(kn & 2u)) zn.y = 0.f;
+        if (!(kn & 4u)) zn.z = 0.f;
+        if (!(kn & 8u)) zn.w = 0.f;
+        st4(ZW + e, zn);  // the whole quad (kept lanes unchanged): full-sector stores
+      }
+      const int lane = threadIdx.x & 31;
+      const unsigned gmask = 0xFFu << (lane & 24);
+      unsigned w = (kn & ((unsigned)(zn.x != 0.f) | ((unsigned)(zn.y != 0.f) << 1) | ((unsigned)(zn.z != 0.f) << 2) |
+                          ((unsigned)(zn.w != 0.f) << 3)))
+                   << (4 * (lane & 7));
+      w |= __shfl_xor_sync(gmask, w, 1);
+      w |= __shfl_xor_sync(gmask, w, 2);
+      w |= __shfl_xor_sync(gmask, w, 4);
+      if ((lane & 7) == 0) MK[e >> 5] = w;
+    }
     const float4 th = *ring_slot<NB>(ring, d, 2), uu = *ring_slot<NB>(ring, d, 3);
     const float4 un = make_float4(dual1(uu.x, th.x, zn.x), dual1(uu.y, th.y, zn.y), dual1(uu.z, th.z, zn.z),
                                   dual1(uu.w, th.w, zn.w));
@@ -2168,7 +2351,7 @@ __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
     ring_run<D>(tc.count, [&](int d, int i) { load(d, tc.row(i) * ly.L + 4 * tc.j); },
                 [&](int d, int i) {
                   const long long r = tc.row(i);
-                  emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
+                  emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp), PROJ && ly.ncons > 0 && ly.k > 1);
                 });
   } else {
     const long long nq = (it.end - it.begin + 3) >> 2;
@@ -2177,23 +2360,31 @@ __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
     ring_run<D>(count, [&](int d, int i) { load(d, it.begin + 4 * (t + (long long)i * kThreads)); },
                 [&](int d, int i) {
                   const long long e = it.begin + 4 * (t + (long long)i * kThreads);
-                  emit(d, e, dst4_linear(a, ly, rowlen, e));
+                  emit(d, e, dst4_linear(a, ly, rowlen, e), false);
                 });
   }
   if (RESID) block_partials<9>(acc, a.rpart + (long long)blockIdx.x * kResidSlots);
 }
 
-void launch_local_sync(const ElemArgs& a, int n_items, cudaStream_t st) {
-  if (n_items <= 0) return;
+template <bool PROJ>
+static void launch_local_sync_p(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (a.rpart) {
     const size_t smem = (size_t)3 * 6 * kThreads * sizeof(float4);
-    allow_smem(k_local_sync<true>, smem);
-    launch_pdl(k_local_sync<true>, n_items, kThreads, smem, st, a);
+    allow_smem(k_local_sync<true, PROJ>, smem);
+    launch_pdl(k_local_sync<true, PROJ>, n_items, kThreads, smem, st, a);
   } else {
     const size_t smem = (size_t)kDepth * 4 * kThreads * sizeof(float4);
-    allow_smem(k_local_sync<false>, smem);
-    launch_pdl(k_local_sync<false>, n_items, kThreads, smem, st, a);
+    allow_smem(k_local_sync<false, PROJ>, smem);
+    launch_pdl(k_local_sync<false, PROJ>, n_items, kThreads, smem, st, a);
   }
+}
+
+void launch_local_sync(const ElemArgs& a, int n_items, cudaStream_t st) {
+  if (n_items <= 0) return;
+  if (a.mask)
+    launch_local_sync_p<true>(a, n_items, st);
+  else
+    launch_local_sync_p<false>(a, n_items, st);
 }
 
 // ---------------------------------------------------------------------------

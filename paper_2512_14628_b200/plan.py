@@ -49,10 +49,19 @@ class KernelTimer:
 
 
 TIMER: KernelTimer | None = None
+# what each timed collective call moved (bench's collectives block):
+# name -> [(op, bytes, ranks)] in call order, parallel to TIMER.events[name]
+NOTES: dict = {}
 
 
 def timed(name: str):
     return TIMER(name) if TIMER is not None else contextlib.nullcontext()
+
+
+def note(name: str, op: str, nbytes: int, ranks: int) -> None:
+    """Record the payload of a timed collective (only while a KernelTimer is active)."""
+    if TIMER is not None:
+        NOTES.setdefault(name, []).append((op, int(nbytes), int(ranks)))
 
 
 def ptr(t) -> int | None:
@@ -127,6 +136,10 @@ class Plan:
     def set_single_node(self, on: bool):
         """Structured keep sets in the selection tail (one node: the union is the local mask)."""
         _lib.call("hsx_plan_set_single_node", self._h, 1 if on else 0)
+
+    def set_fused_projection(self, on: bool):
+        """One node: K67 projects the layers K3 need not touch (hsx_plan_set_fused_projection)."""
+        _lib.call("hsx_plan_set_fused_projection", self._h, 1 if on else 0)
 
     def set_penalties(self, rho1: dict | None, rho2: dict | None, weight_decay: float,
                       num_nodes: int, accels_per_node: int, identity: bool = False):

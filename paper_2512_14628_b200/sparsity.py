@@ -123,13 +123,19 @@ def group_norms_gpu(t, group: GroupBy) -> torch.Tensor:
 
 
 def frobenius_norm(t) -> float:
-    """sqrt(sum t^2) in fp64 (reference tensors.py:71-72): one fp64 group norm of
-    the tensor viewed as a single (1, n, 1, 1) filter, accumulated in libhsx."""
+    """sqrt(sum t^2) in fp64 (reference tensors.py:71-72): the tensor (zero-padded
+    to rows of 4096) as filters of a (rows, 4096, 1, 1) weight, fp64 filter norms
+    accumulated in libhsx, then the fp64 root of their sum of squares."""
     t = as_cuda_f32(t)
     n = t.numel()
     if n == 0:
         return 0.0
-    return float(group_norms_gpu(t.reshape(1, n, 1, 1), GroupBy.FILTER)[0])
+    cols = 4096
+    rows = (n + cols - 1) // cols
+    padded = torch.zeros(rows * cols, dtype=torch.float32, device=t.device)
+    padded[:n] = t.reshape(-1)
+    norms = group_norms_gpu(padded.view(rows, cols, 1, 1), GroupBy.FILTER)
+    return math.sqrt(float(torch.sum(norms * norms)))
 
 
 def project(t, constraint: SparsityConstraint) -> torch.Tensor:

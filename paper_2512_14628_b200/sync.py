@@ -78,6 +78,11 @@ class HSADMMSync:
         # one node: the union mask is every rank's local mask, so the selection derives
         # the keep sets of the kept rectangle and K3 only checks it (hsx_project_keep_sets)
         self.plan.set_single_node(self.M == 1 and os.environ.get("HSX_SINGLE_NODE", "1") != "0")
+        # ... and K67 projects the layers whose kept set is the selected rectangle (K3
+        # only for the others): the projection costs no pass of its own
+        self.plan.set_fused_projection(self.M == 1 and os.environ.get("HSX_SINGLE_NODE", "1") != "0"
+                                       and os.environ.get("HSX_LOCAL_SYNC", "1") != "0"
+                                       and os.environ.get("HSX_FUSED_PROJ", "1") != "0")
         self.prunable = self.plan.prunable
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         pl, dev = self.plan, self.device

@@ -624,10 +624,20 @@ class DistCluster(Cluster):
         return self._global
 
     def execute(self, req) -> Any:
-        from .plan import timed
+        from .plan import note, timed
 
         _validate(self.rank, req)
-        with timed("C:" + req.tag.split("/")[0]):
+        name = "C:" + req.tag.split("/")[0]
+        g = len(req.group.members)
+        if isinstance(req, Barrier):
+            note(name, "barrier", 0, g)
+        elif isinstance(req, Broadcast):
+            note(name, "broadcast", _payload_bytes(req.payload), g)
+        elif isinstance(req, AllGather):
+            note(name, "all_gather", _payload_bytes(req.payload) * g, g)
+        else:
+            note(name, f"all_reduce_{req.op.value}", _payload_bytes(req.payload), g)
+        with timed(name):
             return self._execute(req)
 
     def _execute(self, req) -> Any:

@@ -143,11 +143,14 @@ def test_run_hierarchical_adaptive_trace_and_ledger(M, P, monkeypatch):
 
 
 def test_reference_helpers_on_device():
-    """frobenius_norm / adapt_penalties / pack_report against numpy on the same data."""
+    """frobenius_norm against numpy fp64 on the same data (incl. a size that is not a multiple of a row)."""
     import paper_2512_14628_b200 as H
 
     rng = np.random.default_rng(3)
     t = rng.normal(size=(64, 32, 3, 3)).astype(np.float32)
     want = float(np.sqrt(np.sum(t.astype(np.float64) ** 2)))
     assert abs(H.frobenius_norm(torch.tensor(t, device="cuda")) - want) <= 1e-13 * want
+    big = rng.normal(size=(3, 100_003)).astype(np.float32)
+    want = float(np.sqrt(np.sum(big.astype(np.float64) ** 2)))
+    assert abs(H.frobenius_norm(torch.tensor(big, device="cuda")) - want) <= 1e-12 * want
     assert H.frobenius_norm(torch.zeros(0, device="cuda")) == 0.0

@@ -37,6 +37,7 @@ sys.path.insert(0, ROOT)
 METRIC = "H-SADMM sync step ms & HBM GB/s (frac of roofline) at 1/2/4/8 B200; leader bytes"
 UNIT = "Mparams/s"
 DEFAULT_GROUPING = {1: "1x1", 2: "1x2", 4: "2x2", 8: "2x4"}
+PRESLEEP_CYCLES = int(float(os.environ.get("HSX_BENCH_PRESLEEP_MS", "1")) * 2e6)   # ~ms at ~2 GHz
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -398,26 +399,10 @@ def algorithmic_bytes(kernel, N, n_c, Z, P, k3=None, k67_extra=0):
 
 
 def projection_bytes(eng, layers):
-    """(K3 bytes, K67's extra bytes) per launch from the last step's summary.
-
-    Plain K3: read and write every element of the prunable layers + n/8 mask
-    bytes. Fused projection (one node): K3 runs only on the layers K67 cannot
-    project (no row-quad tiles: the 7x7 stem), and K67 additionally zero-stores
-    each dropped element (4 B) and writes the n/8 mask bytes of the others."""
-    from paper_2512_14628_b200 import _lib
-
-    fused = eng.M == 1 and all(os.environ.get(v, "1") != "0"
-                               for v in ("HSX_SINGLE_NODE", "HSX_LOCAL_SYNC", "HSX_FUSED_PROJ"))
-    rows, _ = eng.plan.summary_np()
-    k3, extra = 0, 0
-    for i in eng.plan.prunable:
-        ls = layers[i]
-        n = ls.elements
-        if fused and (n // ls.shape[0]) % 32 == 0 and ls.shape[2] * ls.shape[3] > 1:
-            extra += 4 * (n - int(rows[i, _lib.SUM_POP])) + n // 8
-        else:
-            k3 += 8 * n + n // 8
-    return k3, extra
+    """(K3 bytes, K67's extra bytes) per launch: K3 reads and writes every element
+    of the prunable layers + n/8 mask bytes."""
+    n_p = sum(layers[i].elements for i in eng.plan.prunable)
+    return 8 * n_p + n_p // 8, 0
 
 
 def run_ours(args):
@@ -465,6 +450,13 @@ def run_ours(args):
     sink = torch.empty((), dtype=torch.float32, device=dev)
     if flush2 is not None:
         config["l2"] = "flushed between timed steps (256 MiB write, then 256 MiB read: no dirty lines left)"
+    # run the flush kernels once now: their lazily loaded modules would otherwise load
+    # in front of the first timed step, leaving the host no launch slack for it
+    flush.fill_(0.0)
+    if flush2 is not None:
+        torch.sum(flush2, dim=0, out=sink)
+    torch.cuda._sleep(1000)
+    torch.cuda.synchronize()
 
     use_graph = world == 1 and not args.no_graph
     config["launch"] = "cuda-graph replay per step" if use_graph else "eager launches (deferred host bookkeeping)"
@@ -485,11 +477,13 @@ def run_ours(args):
         evs = []
         barrier()
         torch.cuda.synchronize()
-        # a ~1 ms spin before the first step (outside every event pair): the host
-        # enqueues the first steps while it runs, so no step's bracket contains GPU
-        # idle time waiting for the host to launch it
-        torch.cuda._sleep(2_000_000)
+        # a spin before the first step (outside every event pair): the host enqueues
+        # the first steps while it runs, so no step's bracket contains GPU idle time
+        # waiting for the host (or another rank) to launch it
+        torch.cuda._sleep(PRESLEEP_CYCLES)
+        host_t = []
         for i in range(nsteps):
+            host_t.append(time.perf_counter())
             flush.fill_(float(i))
             if flush2 is not None:
                 torch.sum(flush2, dim=0, out=sink)
@@ -508,6 +502,9 @@ def run_ours(args):
             evs.append((s, e))
         torch.cuda.synchronize()
         barrier()
+        if os.environ.get("HSX_BENCH_TRACE"):
+            print(f"rank {rank} host enqueue ms:", [round((b - a) * 1e3, 3) for a, b in zip(host_t, host_t[1:])],
+                  file=sys.stderr, flush=True)
         return [s.elapsed_time(e) for s, e in evs]
 
     def max_over_ranks(x):
@@ -523,8 +520,11 @@ def run_ours(args):
     eng.defer_host = True
     # clocks are sampled from before the warm-up to the end of the headline steps (the
     # sampler's start-up pause is not an idle gap between warm-up and timed steps)
-    clocks = ClockSampler([local] if world == 1 else list(range(world)))
-    clocks.__enter__()
+    # rank 0 alone runs the sampler (over every GPU of the job): one NVML poller, not one per rank
+    clocks = (ClockSampler([local] if world == 1 else list(range(world)))
+              if rank == 0 and not os.environ.get("HSX_BENCH_NO_CLOCKS") else None)
+    if clocks is not None:
+        clocks.__enter__()
     k = 0
     for _ in range(args.warmup):
         k += 1
@@ -536,7 +536,8 @@ def run_ours(args):
     try:
         times = timed_steps(k + 1, args.steps)
     finally:
-        clocks.__exit__(None, None, None)
+        if clocks is not None:
+            clocks.__exit__(None, None, None)
     gc.enable()
     launches = _lib.launch_count() - launches0
     k += args.steps
@@ -659,7 +660,7 @@ def run_ours(args):
                         "buffered; K steps timed end to end, no L2 flush: 6 state arenas > L2)"},
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
-        "clocks": clocks.summary(),
+        "clocks": clocks.summary() if clocks is not None else {"sm_mhz": None, "reasons": ["not sampled (HSX_BENCH_NO_CLOCKS)"]},
         "step_ms_spread": step_spread,
         "step_ms": [round(t, 4) for t in times],
         "steady_ms_per_step": steady_ms,

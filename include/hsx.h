@@ -258,22 +258,24 @@ int hsx_compact_dual_resid(const hsx_plan* plan, const float* theta, float* u, c
 int hsx_decompact_dual_resid(const hsx_plan* plan, const float* flat, float divisor,
                              const float* z_node, const float* z_node_prev, float* v, float* z,
                              void* stream);
+/* F1: the leader average of two leaders fused into K7 (transport.py:453-462 AVG +
+ * decompress, consensus.py:486-505): srcs[0], srcs[1] are the two leaders' flat
+ * compact buffers in rank order (one is read over NVLink); every kept coordinate
+ * gets z = fp32((srcs[0][i] + srcs[1][i]) / divisor) in fp64 — bitwise what
+ * hsx_average_peers then hsx_decompact_dual(divisor 1) produce — written to
+ * zhat_out[i] (the node's payload for the intra broadcast; may be NULL) and
+ * decompacted with the inter dual v += z_node - z in the same pass.
+ * residuals != 0: slots 3-8 as hsx_decompact_dual_resid. */
+int hsx_decompact_average(const hsx_plan* plan, const float* const* srcs, int32_t n, double divisor,
+                          float* zhat_out, const float* z_node, const float* z_node_prev, float* v, float* z,
+                          int32_t residuals, void* stream);
 /* K6 + K7 of a one-node cluster (M == 1) in one pass: the leader average is the
  * identity, so z = z_node + v on the kept rectangle (0 elsewhere), u += theta -
  * z_node, v += z_node - z, in place and bitwise equal to hsx_compact_dual then
  * hsx_decompact_dual(divisor 1) — without the compact buffer. residuals != 0
  * also accumulates all nine residual slots (z_node_prev required). */
-int hsx_local_sync(hsx_plan* plan, const float* theta, float* u, const float* z_node, float* v,
+int hsx_local_sync(const hsx_plan* plan, const float* theta, float* u, const float* z_node, float* v,
                    float* z, const float* z_node_prev, int32_t residuals, void* stream);
-/* Fused projection (one node, single-node plans): hsx_project_keep_sets then runs
- * K3 only for the layers whose kept set may differ from the selected rectangle
- * (7x7 stems without row-quad tiles, layers whose candidate holds an exact 0, layers
- * whose previous mask was irregular) and the keep-set fixup; the next
- * hsx_local_sync on the same z_node projects every other layer in its pass
- * (dropped elements zeroed in place, mask bits kept && != 0 written to the mask
- * hsx_project_keep_sets was given). The caller issues nothing that reads z_node or
- * that mask between the two calls. */
-int hsx_plan_set_fused_projection(hsx_plan* plan, int32_t on);
 /* vec[layer][9] = the layer's slot sums (leader == 0 zeroes slots 3-8: the
  * node's leader contributes them to the intra SUM, consensus.py:550-563). */
 int hsx_residual_fold(hsx_plan* plan, int32_t leader, double* vec, void* stream);

@@ -69,7 +69,6 @@ SIGNATURES = {
     "hsx_project_keep_sets": (C.c_int, [P, VP, VP, VP, VP]),
     "hsx_select_project_keep_sets": (C.c_int, [P, VP, VP, VP, VP]),
     "hsx_plan_set_single_node": (C.c_int, [P, C.c_int32]),
-    "hsx_plan_set_fused_projection": (C.c_int, [P, C.c_int32]),
     "hsx_mask_or": (C.c_int, [VP, I32, I64, VP, VP]),
     "hsx_keep_sets": (C.c_int, [P, VP, VP, VP]),
     "hsx_keep_sets_fetch": (C.c_int, [P, VP, VP]),
@@ -83,6 +82,7 @@ SIGNATURES = {
     "hsx_compact_dual_resid": (C.c_int, [P, VP, VP, VP, VP, VP, VP]),
     "hsx_decompact_dual_resid": (C.c_int, [P, VP, F32, VP, VP, VP, VP, VP]),
     "hsx_local_sync": (C.c_int, [P, VP, VP, VP, VP, VP, VP, I32, VP]),
+    "hsx_decompact_average": (C.c_int, [P, VP, I32, F64, VP, VP, VP, VP, VP, I32, VP]),
     "hsx_residual_fold": (C.c_int, [P, I32, VP, VP]),
     "hsx_residual_report": (C.c_int, [P, VP, VP, VP, C.POINTER(ResidParams), VP]),
     "hsx_scale_duals": (C.c_int, [P, VP, VP, VP, VP]),

@@ -128,12 +128,6 @@ struct hsx_plan {
   unsigned int* d_k1done = nullptr;  // chained K2: K1 tiles finished per prunable layer (0 between steps)
   int k2_armed = 0;                  // the last launch was such a K1: hsx_select(0) chains behind it
   int k2_pending = 0;                // a counting K1 ran whose counts no chained K2 consumed yet
-  int* d_haszero = nullptr;          // per prunable layer: K1 stored an exact 0 (zeroed by the fixup / K67)
-  int* d_proj_pidx = nullptr;        // prunable index of every K3 item (fused-projection K3)
-  int* d_irr_next = nullptr;         // fused-projection K3: the fixups' next irr, moved by K67
-  int fused_proj = 0;                // one node: K3 only where K67 cannot project (hsx_plan_set_fused_projection)
-  const float* proj_zn = nullptr;    // z_node / mask of the last deferred projection, consumed by hsx_local_sync
-  uint32_t* proj_mask = nullptr;
   int* d_sel[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
   double* d_partials[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
@@ -146,7 +140,7 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_irr_next, d_proj_pidx, d_haszero, d_k1done, d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_k1done, d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
                     d_ch_prev};
     for (void* p : ptrs)
@@ -425,11 +419,6 @@ int upload_plan(hsx_plan* p) {
       return rc;
   }
   if ((rc = upload(&p->d_proj, p->proj_items))) return rc;
-  {
-    std::vector<int> pp(p->proj_items.size());
-    for (size_t i = 0; i < pp.size(); ++i) pp[i] = p->layers[p->proj_items[i].layer].pidx;
-    if ((rc = upload(&p->d_proj_pidx, pp))) return rc;
-  }
   if ((rc = upload(&p->d_word, p->word_items))) return rc;
   if ((rc = upload(&p->d_prunable, p->prunable))) return rc;
   for (int q = 0; q < hsx::kMaxPasses; ++q) {
@@ -452,8 +441,6 @@ int upload_plan(hsx_plan* p) {
   if ((rc = upload(&p->d_summary, p->summary))) return rc;
   if ((rc = alloc0(&p->d_done, 1))) return rc;
   if ((rc = alloc0(&p->d_k1done, (long long)p->prunable.size() + 1))) return rc;
-  if ((rc = alloc0(&p->d_haszero, (long long)p->prunable.size() + 1))) return rc;
-  if ((rc = alloc0(&p->d_irr_next, (long long)p->prunable.size() + 1))) return rc;
   return HSX_OK;
 }
 
@@ -578,8 +565,6 @@ static hsx::KeepArgs keep_args(hsx_plan* p, const Item* items, const uint32_t* u
   ka.ck_prev = p->d_ck_prev;
   ka.irr = p->d_irr;
   ka.irr_any = p->d_irr_any;
-  ka.haszero = p->d_haszero;
-  ka.irr_next = nullptr;
   ka.n_layers = p->n_layers;
   ka.n_prunable = (int)p->prunable.size();
   return ka;
@@ -602,7 +587,6 @@ static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta
   for (int q = 0; q < hsx::kMaxPasses; ++q) a.fw.f[q] = p->d_flags[q];
   a.cand_done = p->d_cand_done;
   a.sched = p->d_sched;
-  a.haszero = p->d_haszero;
   a.ka = keep_args(p, nullptr, nullptr, nullptr);
   a.structured = p->single_node;
   return a;
@@ -789,19 +773,6 @@ int hsx_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, const uint
   // the selection's last pass derived the keep sets of the rectangles R x C; K3
   // flags layers whose mask has a kept zero and the fixup re-derives those
   hsx::KeepArgs ka = keep_args(p, p->d_proj, mask, prev_mask);
-  p->proj_zn = nullptr;
-  if (p->fused_proj) {
-    // only the layers K67 cannot project (stems, a candidate with an exact 0, a
-    // previously irregular mask); hsx_local_sync projects the rest
-    ka.irr_next = p->d_irr_next;
-    if (hsx::launch_project_lite(ka, (int)p->proj_items.size(), z_node, mask, p->d_proj_pidx, p->d_prunable,
-                                 p->d_pdone, p->fixup_smem, S(stream)) != 0)
-      return fail(HSX_ESHAPE, "fused projection supports at most 2048 prunable layers");
-    HSX_LAUNCHED("project_lite");
-    p->proj_zn = z_node;
-    p->proj_mask = mask;
-    return HSX_OK;   // the fixup ran inside
-  }
   hsx::launch_project(ka, (int)p->proj_items.size(), z_node, mask, 1, S(stream));
   HSX_LAUNCHED("project_check");
   hsx::launch_keep_fixup(ka, p->d_prunable, (int)p->prunable.size(), p->fixup_smem, S(stream));
@@ -833,13 +804,6 @@ int hsx_select_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, con
   hsx::launch_select_project(sp, ka, (int)p->proj_items.size(), z_node, mask,
                              std::max(p->select_smem[0], p->fixup_smem), S(stream));
   HSX_LAUNCHED("select_project");
-  return HSX_OK;
-}
-
-int hsx_plan_set_fused_projection(hsx_plan* p, int32_t on) {
-  if (!p) return fail(HSX_EINVAL, "null plan");
-  p->fused_proj = on ? 1 : 0;
-  p->proj_zn = nullptr;
   return HSX_OK;
 }
 
@@ -980,6 +944,28 @@ int hsx_decompact_dual(const hsx_plan* p, const float* flat, float divisor, cons
   return HSX_OK;
 }
 
+int hsx_decompact_average(const hsx_plan* p, const float* const* srcs, int32_t n, double divisor, float* zhat_out,
+                          const float* z_node, const float* z_node_prev, float* v, float* z, int32_t residuals,
+                          void* stream) {
+  if (!p || !srcs || !z_node || !v || !z) return fail(HSX_EINVAL, "null argument");
+  if (n != 2 || !srcs[0] || !srcs[1]) return fail(HSX_EINVAL, "the fused average takes exactly two leaders");
+  if (!(divisor > 0.0)) return fail(HSX_EINVAL, "divisor must be positive");
+  if (residuals && !z_node_prev) return fail(HSX_EINVAL, "residuals need z_node_prev");
+  hsx::ElemArgs a = elem_args(p);
+  a.flat_in = srcs[0];
+  a.flat_in2 = srcs[1];
+  a.avg_div = divisor;
+  a.zhat_out = zhat_out;
+  a.zn = z_node;
+  a.zn_prev = z_node_prev;
+  a.v = v;
+  a.z = z;
+  a.rpart = residuals ? p->d_rpart : nullptr;
+  hsx::launch_decompact(a, (int)p->stream_items.size(), S(stream));
+  HSX_LAUNCHED("decompact_average");
+  return HSX_OK;
+}
+
 int hsx_compact_dual_resid(const hsx_plan* p, const float* theta, float* u, const float* z_node,
                            const float* v, float* flat, void* stream) {
   if (!p || !theta || !u || !z_node) return fail(HSX_EINVAL, "null argument");
@@ -1013,20 +999,11 @@ int hsx_decompact_dual_resid(const hsx_plan* p, const float* flat, float divisor
   return HSX_OK;
 }
 
-int hsx_local_sync(hsx_plan* p, const float* theta, float* u, const float* z_node, float* v, float* z,
+int hsx_local_sync(const hsx_plan* p, const float* theta, float* u, const float* z_node, float* v, float* z,
                    const float* z_node_prev, int32_t residuals, void* stream) {
   if (!p || !theta || !u || !z_node || !v || !z) return fail(HSX_EINVAL, "null argument");
   if (residuals && !z_node_prev) return fail(HSX_EINVAL, "residuals need z_node_prev");
   hsx::ElemArgs a = elem_args(p);
-  if (p->proj_zn == z_node) {  // the deferred projection of this z_node (fused-projection mode)
-    a.zn_w = const_cast<float*>(z_node);
-    a.mask = p->proj_mask;
-    a.haszero = p->d_haszero;
-    a.irr = p->d_irr;
-    a.irr_next = p->d_irr_next;
-    a.n_prunable = (int)p->prunable.size();
-  }
-  p->proj_zn = nullptr;
   a.theta = theta;
   a.u = u;
   a.zn = z_node;

@@ -904,12 +904,17 @@ __device__ __forceinline__ double cand_of(double s, double z, double v, const Co
 // from the P ranks' theta + u buffers over NVLink (kModePeers: the intra
 // all-reduce fused into K1, folded in rank order like the reference's serial
 // fold), or the candidate is S itself (kModeIdent: per-tensor projection API)
-enum { kModeThetaU = 0, kModeSum = 1, kModeIdent = 2, kModePeers = 3 };
+// (kModePeers2: exactly two ranks — a 4-slot ring stage like the local modes, so
+// three CTAs fit per SM instead of two)
+enum { kModeThetaU = 0, kModeSum = 1, kModeIdent = 2, kModePeers = 3, kModePeers2 = 4 };
+
+__host__ __device__ constexpr bool peer_mode(int m) { return m == kModePeers || m == kModePeers2; }
+__host__ __device__ constexpr int peer_slots(int m) { return m == kModePeers2 ? 2 : kMaxPeers; }
 
 template <int MODE>
 struct K1 {
-  static constexpr int NB = MODE == kModePeers ? kMaxPeers + 2 : 4;  // ring slots per stage
-  static constexpr int ZS = MODE == kModePeers ? kMaxPeers : 2;      // slot of z (v follows)
+  static constexpr int NB = peer_mode(MODE) ? peer_slots(MODE) + 2 : 4;  // ring slots per stage
+  static constexpr int ZS = peer_mode(MODE) ? peer_slots(MODE) : 2;      // slot of z (v follows)
 };
 
 // source pointers of one layer (offset already applied)
@@ -927,7 +932,7 @@ __device__ __forceinline__ K1Src k1_src(const CandArgs& p, long long base) {
   K1Src s;
   s.a = s.b = nullptr;
   s.np = 0;
-  if (MODE == kModePeers) {
+  if (peer_mode(MODE)) {
     s.np = p.peers.n;
 #pragma unroll
     for (int j = 0; j < kMaxPeers; ++j) s.peer[j] = j < s.np ? p.peers.p[j] + base : nullptr;
@@ -952,9 +957,9 @@ __device__ __forceinline__ void k1_issue(float4* ring, int d, const K1Src& s, lo
     else
       cp_quad_h(ring_slot<NB>(ring, d, slot), src, e, n, pol);
   };
-  if (MODE == kModePeers) {
+  if (peer_mode(MODE)) {
 #pragma unroll
-    for (int j = 0; j < kMaxPeers; ++j)
+    for (int j = 0; j < peer_slots(MODE); ++j)
       if (j < s.np) cp(j, s.peer[j]);
   } else {
     cp(0, s.a);
@@ -971,11 +976,11 @@ template <int MODE>
 __device__ __forceinline__ void k1_cand(float4* ring, int d, int np, const Coef& cf, double c[4]) {
   constexpr int NB = K1<MODE>::NB;
   double s[4];
-  if (MODE == kModePeers) {
+  if (peer_mode(MODE)) {
     const float4 x0 = *ring_slot<NB>(ring, d, 0);
     s[0] = x0.x; s[1] = x0.y; s[2] = x0.z; s[3] = x0.w;
 #pragma unroll
-    for (int j = 1; j < kMaxPeers; ++j) {
+    for (int j = 1; j < peer_slots(MODE); ++j) {
       if (j < np) {
         const float4 x = *ring_slot<NB>(ring, d, j);
         s[0] = __dadd_rn(s[0], (double)x.x); s[1] = __dadd_rn(s[1], (double)x.y);
@@ -1007,7 +1012,7 @@ __device__ __forceinline__ void k1_cand(float4* ring, int d, int np, const Coef&
 template <int MODE>
 __device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, const Coef& cf) {
   double s;
-  if (MODE == kModePeers) {
+  if (peer_mode(MODE)) {
     s = (double)p.peers.p[0][gi];
     for (int j = 1; j < p.peers.n; ++j) s = __dadd_rn(s, (double)p.peers.p[j][gi]);
   } else if (MODE == kModeThetaU) {
@@ -1082,14 +1087,6 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
 // one fp64 partial per group: partials[part][G].
 constexpr int kTileQuads = 64;
 
-// pass 0: flag the prunable layer when some stored candidate element is exactly 0
-// (every thread of the CTA calls this); only such layers can have a kept zero, so
-// the one-node path projects every other layer inside K67 (hsx_plan_set_fused_projection)
-__device__ __forceinline__ void note_zero(const CandArgs& p, const DevLayer& ly, bool zero) {
-  if (p.pass == 0 && p.haszero && __any_sync(kFull, zero) && (threadIdx.x & 31) == 0)
-    atomicOr(p.haszero + ly.pidx, 1);
-}
-
 template <int MODE>
 __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, float4* ring,
                                 double* cs) {
@@ -1109,7 +1106,6 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const Coef cf = coef_of(ly);
   const long long stride = (long long)RP * L;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  bool zero = false;  // an element of the candidate is exactly 0 (the layer may be irregular)
   const unsigned long long pf = l2pol(kL2First), pl = l2pol(kL2Last);
   ring_run(
       count,
@@ -1124,9 +1120,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
           for (int i2 = 0; i2 < 4; ++i2)
             if (!kept_by(ly, p.flags, pass, ee + i2)) c[i2] = 0.0;
         } else {
-          const float4 o = make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]);
-          st4(zn + e, o);
-          zero |= (o.x == 0.f) | (o.y == 0.f) | (o.z == 0.f) | (o.w == 0.f);
+          st4(zn + e, make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]));
         }
         a0 = __dadd_rn(a0, __dmul_rn(c[0], c[0]));
         a1 = __dadd_rn(a1, __dmul_rn(c[1], c[1]));
@@ -1134,7 +1128,6 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
         a3 = __dadd_rn(a3, __dmul_rn(c[3], c[3]));
       });
   double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
-  note_zero(p, ly, zero);
   __syncthreads();  // cs aliases the ring: every thread is done with its last stage
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
@@ -1173,7 +1166,6 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
 // channels by K2) or one warp per row (FILTER: per-row sums).
 template <int MODE>
 __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item& it, double* sq) {
-  bool zero = false;
   const int pass = p.pass;
   const int grp = ly.group[pass];
   const int L = ly.L;
@@ -1187,13 +1179,9 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
   for (int i = threadIdx.x; i < E; i += kThreads) {
     double c = cand_elem<MODE>(p, gbase + i, cf);
     if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
-    if (pass == 0) {
-      p.zn[gbase + i] = (float)c;
-      zero |= (float)c == 0.f;
-    }
+    if (pass == 0) p.zn[gbase + i] = (float)c;
     sq[i] = __dmul_rn(c, c);
   }
-  note_zero(p, ly, zero);
   __syncthreads();
   if (grp == kFilter) {
     for (int r = warp; r < nr; r += kThreads / 32) {
@@ -1359,7 +1347,13 @@ static void launch_candidate_mode(const CandArgs& a, int n_items, int frozen, si
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
   if (n_items <= 0) return;
-  if (a.peers.n > 0)
+  static const bool peers2 = [] {  // measured no faster than the 6-slot ring (r2i): opt-in
+    const char* v = std::getenv("HSX_K1_PEERS2");
+    return v && v[0] == '1';
+  }();
+  if (a.peers.n == 2 && peers2)
+    launch_candidate_mode<kModePeers2>(a, n_items, frozen, smem, st);
+  else if (a.peers.n > 0)
     launch_candidate_mode<kModePeers>(a, n_items, frozen, smem + (size_t)kDepth * (kMaxPeers - 2) * kThreads * 16, st);
   else if (a.identity)
     launch_candidate_mode<kModeIdent>(a, n_items, frozen, smem, st);
@@ -1648,93 +1642,6 @@ void launch_select_project(const SelProjArgs& sp, const KeepArgs& a, int n_items
   launch_pdl(k_select_project, sp.nsel + n_items, kThreads, need, st, sp, a, zn, mask);
 }
 
-// K3 + keep-set fixup of the fused-projection mode (one node), one launch: only
-// the layers K67 does not project itself are touched — layers without row-quad
-// tiles (7x7 stems), 1x1 convolutions (their channel-dropped elements are scattered
-// over nearly every quad: K67 would rewrite whole quads, measured slower than K3
-// on ResNet-50 / 152), layers whose candidate holds an exact 0 (a kept zero makes the mask
-// differ from the kept rectangle) and layers whose previous mask was irregular
-// (drift counted from bits). Every CTA first builds the per-layer "needed" table in
-// shared memory (one parallel round of flag loads) and the layer of each of its
-// items, then projects its items of needed layers (K3 with the kept-zero check);
-// the last CTA to finish a needed layer's items runs that layer's fixup, and the
-// last needed layer lays the flat buffer out again if any layer turned out
-// irregular. Layers not needed keep irr == 0 and their K67 clears haszero.
-__device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);
-__device__ void layout_flat(const KeepArgs& a);
-constexpr int kLiteMaxPrunable = 2048;
-constexpr int kLiteMaxItemsPerCta = 64;
-
-__global__ void __launch_bounds__(kThreads) k_project_lite(KeepArgs a, float* __restrict__ zn,
-                                                           uint32_t* __restrict__ mask, int n_items,
-                                                           const int* __restrict__ item_pidx,
-                                                           const int* __restrict__ prunable,
-                                                           unsigned int* __restrict__ pdone) {
-  PDL_ENTRY();
-  extern __shared__ __align__(16) float4 ring[];
-  __shared__ uint8_t need[kLiteMaxPrunable];
-  __shared__ int mine[kLiteMaxItemsPerCta];
-  __shared__ int n_need;
-  __shared__ bool last_item, last_layer;
-  const int np = a.n_prunable;
-  if (threadIdx.x == 0) n_need = 0;
-  __syncthreads();
-  int cnt = 0;
-  for (int i = threadIdx.x; i < np; i += kThreads) {
-    const DevLayer& dl = a.layers[prunable[i]];
-    const bool nd = !dl.qtile || dl.k == 1 || a.haszero[i] || (a.irr[i] & 2);
-    need[i] = nd;
-    cnt += nd;
-  }
-  if (cnt) atomicAdd(&n_need, cnt);
-  const int per = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  for (int j = threadIdx.x; j < per; j += kThreads) mine[j] = item_pidx[blockIdx.x + j * gridDim.x];
-  __syncthreads();
-  if (n_need == 0) return;
-  for (int j = 0; j < per; ++j) {
-    const int pidx = mine[j];
-    if (!need[pidx]) continue;  // uniform over the CTA
-    const Item it = a.items[blockIdx.x + j * gridDim.x];
-    project_item<true>(a, zn, mask, it, ring);
-    __syncthreads();
-    const DevLayer& dl = a.layers[it.layer];
-    if (threadIdx.x == 0) {
-      __threadfence();
-      last_item = atomicAdd(pdone + pidx, 1u) == (unsigned)dl.npitems - 1;
-    }
-    __syncthreads();
-    if (!last_item) continue;
-    __threadfence();
-    if (threadIdx.x == 0) pdone[pidx] = 0;
-    fixup_layer(a, it.layer, reinterpret_cast<uint8_t*>(ring));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      last_layer = atomicAdd(pdone + np, 1u) == (unsigned)n_need - 1;
-    }
-    __syncthreads();
-    if (!last_layer) continue;
-    __threadfence();
-    if (*reinterpret_cast<volatile int*>(a.irr_any)) layout_flat(a);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      pdone[np] = 0;
-      *a.irr_any = 0;
-    }
-  }
-}
-
-int launch_project_lite(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, const int* item_pidx,
-                        const int* prunable, unsigned int* pdone, size_t smem, cudaStream_t st) {
-  if (n_items <= 0) return 0;
-  if (a.n_prunable > kLiteMaxPrunable) return -1;
-  const int grid = std::max(std::min(n_items, 148 * 2), (n_items + kLiteMaxItemsPerCta - 1) / kLiteMaxItemsPerCta);
-  smem = std::max(smem, (size_t)kDepth * kThreads * sizeof(float4));
-  allow_smem(k_project_lite, smem);
-  launch_pdl(k_project_lite, grid, kThreads, smem, st, a, zn, mask, n_items, item_pidx, prunable, pdone);
-  return 0;
-}
-
 void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * kThreads * sizeof(float4);
@@ -1898,10 +1805,7 @@ __device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    // this mask is the next one's previous (the fused-projection K3 stages it in
-    // irr_next: other CTAs of that launch still read irr; K67 moves it)
-    (a.irr_next ? a.irr_next : a.irr)[pidx] = (irr & 1) << 1;
-    if (a.haszero && !a.irr_next) a.haszero[pidx] = 0;
+    a.irr[pidx] = (irr & 1) << 1;  // this mask is the next one's previous
   }
 }
 
@@ -2120,10 +2024,16 @@ void launch_compact(const ElemArgs& a, int n_items, cudaStream_t st) {
 // (z_node - z_node_prev)^2, z_node^2, v'^2, (z - z_prev)^2, z^2
 // (consensus.py:552-563) -> rpart slots 3-8. RESID with flat_in == nullptr: a
 // non-sync iteration (z, v unchanged, dz = 0, nothing stored).
-template <bool RESID>
+// AVG2 (F1, two leaders): the leader average fused in — the compact values are
+// gathered from both leaders' flat buffers (the other one over NVLink), folded in
+// rank order in fp64 and divided by the divisor exactly as k_average does, written
+// to the node's payload buffer zhat_out for the followers (when given) and
+// decompacted in the same pass: bitwise the K8 -> K7 sequence without the K8 pass.
+template <bool RESID, bool AVG2>
 __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   PDL_ENTRY();
-  constexpr int NB = RESID ? 5 : 3;
+  constexpr int NB = (RESID ? 5 : 3) + (AVG2 ? 1 : 0);
+  constexpr int AS = NB - 1;             // AVG2: slot of the second leader's values
   constexpr int D = RESID ? 3 : kDepth;  // 5 streams x 3 stages: 60 KB, three CTAs per SM
   extern __shared__ float4 ring[];
   __shared__ int s_rb[kMaxTileRows];
@@ -2133,6 +2043,9 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
   const int rowlen = (int)a.summary[(long long)it.layer * kSumCols + 1] * ly.k;  // |K_in| * k
   const bool sync = !RESID || a.flat_in != nullptr;
   const float* __restrict__ flat = sync ? a.flat_in + coff : nullptr;
+  const float* __restrict__ flat2 = AVG2 ? a.flat_in2 + coff : nullptr;
+  float* __restrict__ zhat = AVG2 && a.zhat_out ? a.zhat_out + coff : nullptr;
+  const double adiv = a.avg_div;
   const float* __restrict__ ZN = a.v ? a.zn + ly.off : nullptr;
   float* __restrict__ VV = a.v ? a.v + ly.off : nullptr;
   float* __restrict__ ZO = a.z + ly.off;
@@ -2147,6 +2060,13 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
       cp4z(g + 1, flat + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
       cp4z(g + 2, flat + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
       cp4z(g + 3, flat + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
+      if (AVG2) {
+        float* h = reinterpret_cast<float*>(ring_slot<NB>(ring, d, AS));
+        cp4z(h + 0, flat2 + (dd.x >= 0 ? dd.x : 0), dd.x >= 0);
+        cp4z(h + 1, flat2 + (dd.y >= 0 ? dd.y : 0), dd.y >= 0);
+        cp4z(h + 2, flat2 + (dd.z >= 0 ? dd.z : 0), dd.z >= 0);
+        cp4z(h + 3, flat2 + (dd.w >= 0 ? dd.w : 0), dd.w >= 0);
+      }
     }
     if (ZN) {  // last uses in the step: evict first
       cp_quad_h(ring_slot<NB>(ring, d, 1), ZN, e, ly.n, pf);
@@ -2157,11 +2077,25 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
       cp_quad_h(ring_slot<NB>(ring, d, RESID ? 4 : 0), ZO, e, ly.n, pf);
     }
   };
-  auto emit = [&](int d, long long e) {
+  auto emit = [&](int d, long long e, int4 dd) {
     float4 zo;
     if (sync) {
       zo = *ring_slot<NB>(ring, d, 0);
-      if (div != 1.0f) zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
+      if (AVG2) {
+        const float4 z2 = *ring_slot<NB>(ring, d, AS);
+        zo = make_float4((float)__ddiv_rn(__dadd_rn((double)zo.x, (double)z2.x), adiv),
+                         (float)__ddiv_rn(__dadd_rn((double)zo.y, (double)z2.y), adiv),
+                         (float)__ddiv_rn(__dadd_rn((double)zo.z, (double)z2.z), adiv),
+                         (float)__ddiv_rn(__dadd_rn((double)zo.w, (double)z2.w), adiv));
+        if (zhat) {  // the node's averaged payload for the intra broadcast
+          if (dd.x >= 0) zhat[dd.x] = zo.x;
+          if (dd.y >= 0) zhat[dd.y] = zo.y;
+          if (dd.z >= 0) zhat[dd.z] = zo.z;
+          if (dd.w >= 0) zhat[dd.w] = zo.w;
+        }
+      } else if (div != 1.0f) {
+        zo = make_float4(zo.x / div, zo.y / div, zo.z / div, zo.w / div);
+      }
     } else {
       zo = *ring_slot<NB>(ring, d, RESID ? 4 : 0);
     }
@@ -2206,7 +2140,10 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
                const long long r = tc.row(i);
                load(d, r * ly.L + 4 * tc.j, sync ? add_base(s_rb[r - it.begin], cp) : cp);
              },
-             [&](int d, int i) { emit(d, tc.row(i) * ly.L + 4 * tc.j); });
+             [&](int d, int i) {
+               const long long r = tc.row(i);
+               emit(d, r * ly.L + 4 * tc.j, AVG2 ? add_base(s_rb[r - it.begin], cp) : cp);
+             });
   } else {
     const long long nq = (it.end - it.begin + 3) >> 2;
     const int t = threadIdx.x;
@@ -2216,22 +2153,34 @@ __global__ void __launch_bounds__(kThreads) k_decompact(ElemArgs a) {
                const long long e = it.begin + 4 * (t + (long long)i * kThreads);
                load(d, e, sync ? dst4_linear(a, ly, rowlen, e) : make_int4(-1, -1, -1, -1));
              },
-             [&](int d, int i) { emit(d, it.begin + 4 * (t + (long long)i * kThreads)); });
+             [&](int d, int i) {
+               const long long e = it.begin + 4 * (t + (long long)i * kThreads);
+               emit(d, e, AVG2 ? dst4_linear(a, ly, rowlen, e) : make_int4(-1, -1, -1, -1));
+             });
   }
   if (RESID) block_partials<6>(acc, a.rpart + (long long)blockIdx.x * kResidSlots + 3);
 }
 
+template <bool AVG2>
+static void launch_decompact_a(const ElemArgs& a, int n_items, cudaStream_t st) {
+  constexpr int X = AVG2 ? 1 : 0;
+  if (a.rpart) {
+    const size_t smem = (size_t)3 * (5 + X) * kThreads * sizeof(float4);
+    allow_smem(k_decompact<true, AVG2>, smem);
+    launch_pdl(k_decompact<true, AVG2>, n_items, kThreads, smem, st, a);
+  } else {
+    const size_t smem = (size_t)kDepth * (3 + X) * kThreads * sizeof(float4);
+    allow_smem(k_decompact<false, AVG2>, smem);
+    launch_pdl(k_decompact<false, AVG2>, n_items, kThreads, smem, st, a);
+  }
+}
+
 void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
-  if (a.rpart) {
-    const size_t smem = (size_t)3 * 5 * kThreads * sizeof(float4);
-    allow_smem(k_decompact<true>, smem);
-    launch_pdl(k_decompact<true>, n_items, kThreads, smem, st, a);
-  } else {
-    const size_t smem = (size_t)kDepth * 3 * kThreads * sizeof(float4);
-    allow_smem(k_decompact<false>, smem);
-    launch_pdl(k_decompact<false>, n_items, kThreads, smem, st, a);
-  }
+  if (a.flat_in2)
+    launch_decompact_a<true>(a, n_items, st);
+  else
+    launch_decompact_a<false>(a, n_items, st);
 }
 
 // K6+K7 of one node (M == 1), fused: the leader average is the identity, so the
@@ -2241,23 +2190,9 @@ void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
 //   u <- u + (theta - z_node); z <- kept ? z_node + v : 0; v <- v + (z_node - z)
 // RESID: the K6 (0-2) and K7 (3-8) residual slots in one pass (z_prev, z_node_prev
 // streamed too).
-// PROJ (one node, fused projection): z_node arrives unprojected; on the kept-rectangle
-// tiles each quad is projected in registers (dropped elements -> 0, written back as
-// zeros) and its mask nibble (kept && != 0) is OR-folded over 8 lanes into the mask
-// word; a rectangle is the layer's kept set exactly when no kept element is 0
-// (k_project_lite + the keep-set fixup handled the layers where one might be).
-template <bool RESID, bool PROJ>
+template <bool RESID>
 __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
   PDL_ENTRY();
-  if (PROJ && blockIdx.x == 0) {
-    // the fused-projection K3 has finished: its fixups' irregularity becomes the
-    // next step's "previous", and the exact-zero flags are spent
-    for (int i = threadIdx.x; i < a.n_prunable; i += kThreads) {
-      a.irr[i] = a.irr_next[i];
-      a.irr_next[i] = 0;
-      a.haszero[i] = 0;
-    }
-  }
   constexpr int NB = RESID ? 6 : 4;
   constexpr int D = RESID ? 3 : kDepth;  // 6 x 3 x 4 KB = 72 KB / 4 x 4 x 4 KB = 64 KB
   extern __shared__ float4 ring[];
@@ -2283,31 +2218,8 @@ __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
       cp_quad_h(ring_slot<NB>(ring, d, RESID ? 5 : 0), ZO, e, ly.n, pf);
     }
   };
-  float* __restrict__ ZW = PROJ ? a.zn_w + ly.off : nullptr;
-  uint32_t* __restrict__ MK = PROJ ? a.mask + ly.mword : nullptr;
-  auto emit = [&](int d, long long e, int4 dd, bool proj) {
-    float4 zn = *ring_slot<NB>(ring, d, 0);
-    const float4 vv = *ring_slot<NB>(ring, d, 1);
-    if (PROJ && proj) {
-      const unsigned kn = (unsigned)(dd.x >= 0) | ((unsigned)(dd.y >= 0) << 1) | ((unsigned)(dd.z >= 0) << 2) |
-                          ((unsigned)(dd.w >= 0) << 3);
-      if (kn != 0xFu) {
-        if (!(kn & 1u)) zn.x = 0.f;
-        if (!(kn & 2u)) zn.y = 0.f;
-        if (!(kn & 4u)) zn.z = 0.f;
-        if (!(kn & 8u)) zn.w = 0.f;
-        st4(ZW + e, zn);  // the whole quad (kept lanes unchanged): full-sector stores
-      }
-      const int lane = threadIdx.x & 31;
-      const unsigned gmask = 0xFFu << (lane & 24);
-      unsigned w = (kn & ((unsigned)(zn.x != 0.f) | ((unsigned)(zn.y != 0.f) << 1) | ((unsigned)(zn.z != 0.f) << 2) |
-                          ((unsigned)(zn.w != 0.f) << 3)))
-                   << (4 * (lane & 7));
-      w |= __shfl_xor_sync(gmask, w, 1);
-      w |= __shfl_xor_sync(gmask, w, 2);
-      w |= __shfl_xor_sync(gmask, w, 4);
-      if ((lane & 7) == 0) MK[e >> 5] = w;
-    }
+  auto emit = [&](int d, long long e, int4 dd) {
+    const float4 zn = *ring_slot<NB>(ring, d, 0), vv = *ring_slot<NB>(ring, d, 1);
     const float4 th = *ring_slot<NB>(ring, d, 2), uu = *ring_slot<NB>(ring, d, 3);
     const float4 un = make_float4(dual1(uu.x, th.x, zn.x), dual1(uu.y, th.y, zn.y), dual1(uu.z, th.z, zn.z),
                                   dual1(uu.w, th.w, zn.w));
@@ -2351,7 +2263,7 @@ __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
     ring_run<D>(tc.count, [&](int d, int i) { load(d, tc.row(i) * ly.L + 4 * tc.j); },
                 [&](int d, int i) {
                   const long long r = tc.row(i);
-                  emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp), PROJ && ly.ncons > 0 && ly.k > 1);
+                  emit(d, r * ly.L + 4 * tc.j, add_base(s_rb[r - it.begin], cp));
                 });
   } else {
     const long long nq = (it.end - it.begin + 3) >> 2;
@@ -2360,31 +2272,23 @@ __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
     ring_run<D>(count, [&](int d, int i) { load(d, it.begin + 4 * (t + (long long)i * kThreads)); },
                 [&](int d, int i) {
                   const long long e = it.begin + 4 * (t + (long long)i * kThreads);
-                  emit(d, e, dst4_linear(a, ly, rowlen, e), false);
+                  emit(d, e, dst4_linear(a, ly, rowlen, e));
                 });
   }
   if (RESID) block_partials<9>(acc, a.rpart + (long long)blockIdx.x * kResidSlots);
 }
 
-template <bool PROJ>
-static void launch_local_sync_p(const ElemArgs& a, int n_items, cudaStream_t st) {
-  if (a.rpart) {
-    const size_t smem = (size_t)3 * 6 * kThreads * sizeof(float4);
-    allow_smem(k_local_sync<true, PROJ>, smem);
-    launch_pdl(k_local_sync<true, PROJ>, n_items, kThreads, smem, st, a);
-  } else {
-    const size_t smem = (size_t)kDepth * 4 * kThreads * sizeof(float4);
-    allow_smem(k_local_sync<false, PROJ>, smem);
-    launch_pdl(k_local_sync<false, PROJ>, n_items, kThreads, smem, st, a);
-  }
-}
-
 void launch_local_sync(const ElemArgs& a, int n_items, cudaStream_t st) {
   if (n_items <= 0) return;
-  if (a.mask)
-    launch_local_sync_p<true>(a, n_items, st);
-  else
-    launch_local_sync_p<false>(a, n_items, st);
+  if (a.rpart) {
+    const size_t smem = (size_t)3 * 6 * kThreads * sizeof(float4);
+    allow_smem(k_local_sync<true>, smem);
+    launch_pdl(k_local_sync<true>, n_items, kThreads, smem, st, a);
+  } else {
+    const size_t smem = (size_t)kDepth * 4 * kThreads * sizeof(float4);
+    allow_smem(k_local_sync<false>, smem);
+    launch_pdl(k_local_sync<false>, n_items, kThreads, smem, st, a);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -113,8 +113,6 @@ struct KeepArgs {
   uint8_t* ck_prev;          // [sum L]    its columns (layers with SHAPE groups)
   int* irr;                  // per prunable layer: bit 0 a kept zero now, bit 1 previously
   int* irr_any;              // some layer has a kept zero now
-  int* haszero;              // per prunable layer: K1 stored an exact 0 this step (zeroed by the fixup)
-  int* irr_next;             // fused-projection K3: the fixups' next irr (moved into irr by K67), else nullptr
   int n_layers;
   int n_prunable;
 };
@@ -133,7 +131,6 @@ struct CandArgs {
   const uint8_t* flags[kMaxPasses];    // keep flags of earlier passes (renorm)
   PeerPtrs peers;                      // n > 0: S = sum of the peers' theta + u (rank order)
   unsigned int* k1done;                // chained K2: +1 per finished tile of a prunable layer (or nullptr)
-  int* haszero;                        // pass 0: per prunable layer, set when a stored element is 0
   int reserve;                         // persistent grid: CTA slots left free for the chained K2
   // fused selection (K2 in the tail of each layer's last K1 tile)
   double* norms;                       // this pass
@@ -167,14 +164,11 @@ struct ElemArgs {
   // [item][kResidSlots] (K6 / K6f: slots 0-2, K7: slots 3-8); nullptr = off
   double* __restrict__ rpart;
   const float* __restrict__ zn_prev;   // K7: the previous iteration's z_node
-  // K67 with the projection fused (one node): z_node's dropped elements are zeroed
-  // in place and the mask bits (kept && z_node != 0) written; nullptr = off
-  float* zn_w;
-  uint32_t* mask;
-  int* haszero;                        // PROJ: CTA 0 clears them, and moves irr_next into irr
-  int* irr;
-  int* irr_next;
-  int n_prunable;
+  // K7 with the two-leader average fused (F1): flat_in, flat_in2 in rank order,
+  // z = fp32((a + b) / avg_div) in fp64; zhat_out (optional) receives the average
+  const float* flat_in2;
+  float* zhat_out;
+  double avg_div;
 };
 constexpr int kResidSlots = 9;         // consensus.py:235 (_INTER_SLOTS)
 
@@ -190,10 +184,6 @@ void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t 
 void launch_keep_fixup(const KeepArgs& a, const int* prunable, int n, size_t smem, cudaStream_t st);
 // K3; check != 0: flag layers with a kept zero (structured keep sets)
 void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st);
-// K3 + keep-set fixup of the fused-projection mode: the layers K67 cannot project
-// (see k_project_lite); item_pidx[i] = prunable index of item i; -1: too many layers
-int launch_project_lite(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, const int* item_pidx,
-                        const int* prunable, unsigned int* pdone, size_t smem, cudaStream_t st);
 struct SelProjArgs {
   const int* list;          // layers to select (pass 0)
   int nsel;

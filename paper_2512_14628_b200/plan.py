@@ -65,7 +65,10 @@ def note(name: str, op: str, nbytes: int, ranks: int) -> None:
 
 
 def ptr(t) -> int | None:
-    return None if t is None else t.data_ptr()
+    """Device pointer of a tensor (an int is already one: a peer's mapped buffer)."""
+    if t is None or isinstance(t, int):
+        return t
+    return t.data_ptr()
 
 
 def require_cuda_f32(t, name="tensor"):
@@ -136,10 +139,6 @@ class Plan:
     def set_single_node(self, on: bool):
         """Structured keep sets in the selection tail (one node: the union is the local mask)."""
         _lib.call("hsx_plan_set_single_node", self._h, 1 if on else 0)
-
-    def set_fused_projection(self, on: bool):
-        """One node: K67 projects the layers K3 need not touch (hsx_plan_set_fused_projection)."""
-        _lib.call("hsx_plan_set_fused_projection", self._h, 1 if on else 0)
 
     def set_penalties(self, rho1: dict | None, rho2: dict | None, weight_decay: float,
                       num_nodes: int, accels_per_node: int, identity: bool = False):
@@ -383,6 +382,15 @@ class Plan:
         with timed("K7_decompact_dual_resid" if flat is not None else "K7r_residuals"):
             _lib.call("hsx_decompact_dual_resid", self._h, ptr(flat), float(divisor), ptr(z_node),
                       ptr(z_node_prev), ptr(v), ptr(z), current_stream())
+
+    def decompact_average(self, srcs: list[int], divisor, zhat_out, z_node, z_node_prev, v, z, residuals):
+        """F1: the two leaders' average fused into K7 (optionally writing the averaged
+        payload to zhat_out for the followers)."""
+        arr, keep = _lib.ptr_array(srcs)
+        with timed("K78_average_decompact"):
+            _lib.call("hsx_decompact_average", self._h, arr, len(srcs), float(divisor), ptr(zhat_out), ptr(z_node),
+                      ptr(z_node_prev), ptr(v), ptr(z), 1 if residuals else 0, current_stream())
+        del keep
 
     def local_sync(self, theta, u, z_node, v, z, z_node_prev=None, residuals=False):
         """K6 + K7 of one node in one pass (no compact buffer)."""

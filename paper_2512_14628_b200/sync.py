@@ -46,6 +46,10 @@ from .transport import AllGather, AllReduce, Barrier, Broadcast, LedgerEntry, Re
 from . import _lib
 
 
+_F1 = os.environ.get("HSX_F1", "0") == "1"               # two leaders: average fused into K7
+_REMOTE_K7 = os.environ.get("HSX_REMOTE_K7", "1") != "0"  # followers decompact from the leader's payload
+
+
 class HSADMMSync:
     """Device state + sync program of one rank.
 
@@ -78,11 +82,6 @@ class HSADMMSync:
         # one node: the union mask is every rank's local mask, so the selection derives
         # the keep sets of the kept rectangle and K3 only checks it (hsx_project_keep_sets)
         self.plan.set_single_node(self.M == 1 and os.environ.get("HSX_SINGLE_NODE", "1") != "0")
-        # ... and K67 projects the layers whose kept set is the selected rectangle (K3
-        # only for the others): the projection costs no pass of its own
-        self.plan.set_fused_projection(self.M == 1 and os.environ.get("HSX_SINGLE_NODE", "1") != "0"
-                                       and os.environ.get("HSX_LOCAL_SYNC", "1") != "0"
-                                       and os.environ.get("HSX_FUSED_PROJ", "1") != "0")
         self.prunable = self.plan.prunable
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         pl, dev = self.plan, self.device
@@ -380,6 +379,7 @@ class HSADMMSync:
             # what the compact round trip and the intra broadcast would deliver)
             self._local_sync()
             return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
+        decompacted = False
         if self.is_leader:
             if self.M > 1:
                 flat = self.p_flat[self._nsync & 1]
@@ -393,6 +393,12 @@ class HSADMMSync:
                     pl.slices_peers(flat.peer_ptrs(), me, float(self.M), True, self.p_favg.tensor, "K8_leader_rs")
                     yield Barrier(self.inter, "z_sync_ag", k)
                     pl.slices_peers(self.p_favg.peer_ptrs(), -1, 1.0, True, dst, "K8_leader_ag")
+                elif _F1:
+                    # F1: the average fused into the decompaction (the other leader's
+                    # payload read over NVLink), the averaged payload left in zhat
+                    pl.decompact_average(flat.peer_ptrs(), float(self.M), zhat, self.z_node, self.z_node_prev,
+                                         self.v, self.z, self.residuals)
+                    decompacted = True
                 else:
                     pl.average_peers(flat.peer_ptrs(), float(self.M), dst, tag="K8_leader_avg")
             else:
@@ -402,10 +408,16 @@ class HSADMMSync:
             self._dual(None)
         if self.P > 1:
             yield Barrier(self.intra, "zhat_bcast", k)
-            if not self.is_leader:  # the intra broadcast: a contiguous read of the leader's payload
-                pl.average_peers([self.p_zhat.peer_ptrs()[0]], 1.0, self.flat, tag="K8_zhat_read")
-                dst = self.flat
-        self._decompact(dst)
+            if not self.is_leader:
+                # the intra broadcast: decompact straight from the leader's payload over
+                # NVLink (HSX_REMOTE_K7=0: copy it first)
+                if _REMOTE_K7:
+                    dst = self.p_zhat.peer_ptrs()[0]
+                else:
+                    pl.average_peers([self.p_zhat.peer_ptrs()[0]], 1.0, self.flat, tag="K8_zhat_read")
+                    dst = self.flat
+        if not decompacted:
+            self._decompact(dst)
         return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
 
     # -- phase-1 boundary ------------------------------------------------------------

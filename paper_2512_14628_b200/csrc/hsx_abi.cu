@@ -128,6 +128,7 @@ struct hsx_plan {
   unsigned int* d_k1done = nullptr;  // chained K2: K1 tiles finished per prunable layer (0 between steps)
   int k2_armed = 0;                  // the last launch was such a K1: hsx_select(0) chains behind it
   int k2_pending = 0;                // a counting K1 ran whose counts no chained K2 consumed yet
+  int k3_armed = 0;                  // the last launch was a chained single-pass K2: K3 chains behind it
   int* d_sel[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
   double* d_partials[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
@@ -334,8 +335,9 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   // dynamic candidate launch: group-norm tiles first, short dense items fill the
   // tail; persistent CTAs take the largest items first
   p->cand_dyn.insert(p->cand_dyn.end(), dense_items.begin(), dense_items.end());
-  // launch order: layer order (measured best with peer reads; HSX_K1_ORDER=1
-  // launches the layers with the costliest selection tails first instead)
+  // launch order: the layers with the costliest selection tails first (their chained
+  // K2 CTAs then select while K1 streams the rest; B200 r2m: RN18 1x1 0.130 -> 0.122
+  // ms with the chain); HSX_K1_ORDER=0: layer order
   auto tail_cost = [&](const Item& it) {
     const DevLayer& ly = p->layers[it.layer];
     if (ly.ncons == 0) return 0LL;
@@ -343,7 +345,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
     for (int q = 0; q < ly.ncons; ++q) c += ly.G[q];
     return c;
   };
-  if (env_flag("HSX_K1_ORDER", 0))
+  if (env_flag("HSX_K1_ORDER", 1))
     std::stable_sort(p->cand_dyn.begin(), p->cand_dyn.end(),
                      [&](const Item& x, const Item& y) { return tail_cost(x) > tail_cost(y); });
   // the last layer needs no trailing pad: arenas may be exactly-sized tensors
@@ -379,6 +381,18 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       else
         p->sel_list[q].push_back(l);
     }
+  }
+  if (env_flag("HSX_K1_ORDER", 1)) {  // selection / K3 items in the order K1 finishes their layers
+    auto cost = [&](int l) {
+      const DevLayer& ly = p->layers[l];
+      long long c = (long long)ly.rows + ly.cin;
+      for (int q = 0; q < ly.ncons; ++q) c += ly.G[q];
+      return c;
+    };
+    for (int q = 0; q < hsx::kMaxPasses; ++q)
+      std::stable_sort(p->sel_list[q].begin(), p->sel_list[q].end(), [&](int x, int y) { return cost(x) > cost(y); });
+    std::stable_sort(p->proj_items.begin(), p->proj_items.end(),
+                     [&](const Item& x, const Item& y) { return cost(x.layer) > cost(y.layer); });
   }
   if (p->cand_smem > kMaxSmem) return fail(HSX_ESHAPE, "candidate tile needs %zu B of shared memory", p->cand_smem);
   host_layout(p);
@@ -575,6 +589,7 @@ static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta
   hsx::CandArgs a;
   std::memset(&a, 0, sizeof(a));
   p->k2_armed = 0;   // only a counting dynamic K1 (arm_chain) is chained to
+  p->k3_armed = 0;
   a.s = sum;
   a.theta = theta;
   a.u = u;
@@ -596,7 +611,7 @@ static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta
 // the layers K2 selects and leaves HSX_K1_RESERVE CTA slots (default: one per K2
 // CTA) free, so the chained selections can start while K1 still streams
 static void arm_chain(hsx_plan* p, hsx::CandArgs& a, cudaStream_t st) {
-  static const int on = env_flag("HSX_K2_CHAIN", 0);
+  static const int on = env_flag("HSX_K2_CHAIN", 1);
   static const int reserve = env_flag("HSX_K1_RESERVE", -1);
   p->k2_armed = 0;
   if (!on || p->sel_list[0].empty()) return;
@@ -711,9 +726,14 @@ int hsx_select(hsx_plan* p, int32_t pass, void* stream) {
   const bool chained = pass == 0 && p->k2_armed;
   p->k2_armed = 0;
   if (chained) p->k2_pending = 0;
+  // a single-pass plan's chained selection also publishes per-layer ready flags, so
+  // the K3 launched next (hsx_project / hsx_project_keep_sets) chains behind it
+  const bool k3 = chained && p->max_passes == 1 && p->sel_list[0].size() == p->prunable.size() &&
+                  env_flag("HSX_K3_CHAIN", 0);  // measured: RN18 +1%, RN50 -1% (r2n): opt-in
+  p->k3_armed = k3 ? 1 : 0;
   hsx::launch_select(p->d_layers, p->d_sel[pass], n, pass, p->d_partials[pass], p->d_norms[pass],
                      fl, keep_args(p, nullptr, nullptr, nullptr), p->single_node, p->select_smem[pass], S(stream),
-                     chained ? p->d_k1done : nullptr);
+                     chained ? p->d_k1done : nullptr, k3 ? p->d_ready : nullptr);
   HSX_LAUNCHED("select");
   return HSX_OK;
 }
@@ -757,7 +777,10 @@ int hsx_mask_or_ptrs(const uint32_t* const* srcs, int32_t n, int64_t words, uint
 int hsx_project(hsx_plan* p, float* z_node, uint32_t* local_mask, void* stream) {
   if (!p || !z_node || (!local_mask && p->mask_words)) return fail(HSX_EINVAL, "null argument");
   hsx::KeepArgs ka = keep_args(p, p->d_proj, nullptr, nullptr);
-  hsx::launch_project(ka, (int)p->proj_items.size(), z_node, local_mask, 0, S(stream));
+  const bool chained = p->k3_armed;
+  p->k3_armed = 0;
+  hsx::launch_project(ka, (int)p->proj_items.size(), z_node, local_mask, 0, S(stream),
+                      chained ? p->d_ready : nullptr, p->d_pdone);
   HSX_LAUNCHED("project");
   return HSX_OK;
 }
@@ -773,7 +796,10 @@ int hsx_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, const uint
   // the selection's last pass derived the keep sets of the rectangles R x C; K3
   // flags layers whose mask has a kept zero and the fixup re-derives those
   hsx::KeepArgs ka = keep_args(p, p->d_proj, mask, prev_mask);
-  hsx::launch_project(ka, (int)p->proj_items.size(), z_node, mask, 1, S(stream));
+  const bool chained = p->k3_armed;
+  p->k3_armed = 0;
+  hsx::launch_project(ka, (int)p->proj_items.size(), z_node, mask, 1, S(stream), chained ? p->d_ready : nullptr,
+                      p->d_pdone);
   HSX_LAUNCHED("project_check");
   hsx::launch_keep_fixup(ka, p->d_prunable, (int)p->prunable.size(), p->fixup_smem, S(stream));
   HSX_LAUNCHED("keep_fixup");

@@ -844,7 +844,8 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
                                                  const int* __restrict__ list, int pass,
                                                  const double* __restrict__ partials,
                                                  double* __restrict__ norms, FlagPtrs flags, KeepArgs ka,
-                                                 int structured, unsigned int* __restrict__ k1done) {
+                                                 int structured, unsigned int* __restrict__ k1done,
+                                                 unsigned int* __restrict__ ready) {
   extern __shared__ unsigned long long skey[];
   const int l = list[blockIdx.x];
   if (k1done == nullptr) {
@@ -865,7 +866,14 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
   }
   __syncthreads();
   select_layer(ly, pass, partials, norms, flags, skey, l, structured ? &ka : nullptr);
-  if (threadIdx.x == 0) atomicSub(c, (unsigned)ly.ncitems);  // back to 0 for the next K1 (graph replays too)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicSub(c, (unsigned)ly.ncitems);  // back to 0 for the next K1 (graph replays too)
+    if (ready) {                          // a chained K3 projects this layer now
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ready + l), "r"(1u) : "memory");
+    }
+  }
   pdl_wait();
 }
 
@@ -1378,7 +1386,7 @@ void launch_div_selftest(const double* num, long long n, double den, double* out
 
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
                    double* norms, FlagPtrs flags, const KeepArgs& ka, int structured, size_t smem, cudaStream_t st,
-                   unsigned int* k1done) {
+                   unsigned int* k1done, unsigned int* ready) {
   if (n <= 0) return;
   allow_smem(k_select, smem);
   static const int nt = [] {
@@ -1388,7 +1396,7 @@ void launch_select(const DevLayer* layers, const int* list, int n, int pass, con
     const int x = v ? std::atoi(v) : 512;
     return (x >= 64 && x <= 1024 && x % 32 == 0) ? x : 512;
   }();
-  launch_pdl(k_select, n, nt, smem, st, layers, list, pass, partials, norms, flags, ka, structured, k1done);
+  launch_pdl(k_select, n, nt, smem, st, layers, list, pass, partials, norms, flags, ka, structured, k1done, ready);
 }
 
 size_t structured_smem_bytes(int rows, int L, int cin) { return structured_bytes(rows, L, cin); }
@@ -1560,13 +1568,41 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
   if (CHECK) flag_irregular(a, dl.pidx, bad);
 }
 
+// Chained (ready != nullptr, behind a chained K2): like the chained K2, the CTA lets
+// its dependents launch at once, waits for its layer's selection (ready[layer],
+// published by K2 with release semantics), projects, and waits for the grid before
+// it at the end; the layer's last item re-zeroes its counter and flag.
 template <bool CHECK>
 __global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __restrict__ zn,
-                                                         uint32_t* __restrict__ mask) {
-  PDL_ENTRY();
+                                                         uint32_t* __restrict__ mask, unsigned int* ready,
+                                                         unsigned int* pdone) {
   extern __shared__ float4 ring[];
   const Item it = a.items[blockIdx.x];  // a register copy: a reference into global memory is
-  project_item<CHECK>(a, zn, mask, it, ring);  // reloaded after every store through zn / mask
+  if (ready == nullptr) {               // reloaded after every store through zn / mask
+    PDL_ENTRY();
+    project_item<CHECK>(a, zn, mask, it, ring);
+    return;
+  }
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + it.layer) : "memory");
+      if (v) break;
+      __nanosleep(128);
+    }
+  }
+  __syncthreads();
+  project_item<CHECK>(a, zn, mask, it, ring);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const DevLayer& dl = a.layers[it.layer];
+    if (atomicAdd(pdone + dl.pidx, 1u) == (unsigned)dl.npitems - 1) {
+      pdone[dl.pidx] = 0;
+      ready[it.layer] = 0;
+    }
+  }
+  pdl_wait();
 }
 
 __device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);
@@ -1642,13 +1678,14 @@ void launch_select_project(const SelProjArgs& sp, const KeepArgs& a, int n_items
   launch_pdl(k_select_project, sp.nsel + n_items, kThreads, need, st, sp, a, zn, mask);
 }
 
-void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st) {
+void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st,
+                    unsigned int* ready, unsigned int* pdone) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * kThreads * sizeof(float4);
   if (check)
-    launch_pdl(k_project<true>, n_items, kThreads, smem, st, a, zn, mask);
+    launch_pdl(k_project<true>, n_items, kThreads, smem, st, a, zn, mask, ready, pdone);
   else
-    launch_pdl(k_project<false>, n_items, kThreads, smem, st, a, zn, mask);
+    launch_pdl(k_project<false>, n_items, kThreads, smem, st, a, zn, mask, ready, pdone);
 }
 
 // ---------------------------------------------------------------------------

@@ -178,12 +178,15 @@ void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, c
 // subtracts it again; the grid-completion wait moves to the end)
 void launch_select(const DevLayer* layers, const int* list, int n, int pass, const double* partials,
                    double* norms, FlagPtrs flags, const KeepArgs& ka, int structured, size_t smem, cudaStream_t st,
-                   unsigned int* k1done = nullptr);
+                   unsigned int* k1done = nullptr, unsigned int* ready = nullptr);
 void launch_mask_or(const MaskPtrs& g, long long words, uint32_t* out, cudaStream_t st);
 void launch_keep_sets(const KeepArgs& a, int n_items, size_t smem, cudaStream_t st);
 void launch_keep_fixup(const KeepArgs& a, const int* prunable, int n, size_t smem, cudaStream_t st);
 // K3; check != 0: flag layers with a kept zero (structured keep sets)
-void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st);
+// ready != nullptr: chained behind a chained K2 that publishes ready[layer] (pdone:
+// per prunable layer item counters, left zeroed)
+void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st,
+                    unsigned int* ready = nullptr, unsigned int* pdone = nullptr);
 struct SelProjArgs {
   const int* list;          // layers to select (pass 0)
   int nsel;

@@ -178,6 +178,12 @@ int hsx_select_project_keep_sets(hsx_plan* plan, float* z_node, uint32_t* mask,
                                  const uint32_t* prev_mask, void* stream);
 /* Single-node mode on / off (default off): see hsx_project_keep_sets. */
 int hsx_plan_set_single_node(hsx_plan* plan, int32_t on);
+/* Work-list order of the candidate / selection / projection launches (results do
+ * not depend on it): big_first != 0 (default, HSX_K1_ORDER) takes the layers with
+ * the costliest selection first so the chained selection overlaps K1 (one GPU);
+ * 0 keeps layer order (measured faster when K1 reads the intra sum over NVLink).
+ * Synchronous (re-uploads the work lists); call between steps. */
+int hsx_plan_set_order(hsx_plan* plan, int32_t big_first);
 
 /* ---- K4: leader mask union  out = OR_m gathered[m]  (transport.py:455-457) -- */
 int hsx_mask_or(const uint32_t* gathered, int32_t n_ranks, int64_t words, uint32_t* out,

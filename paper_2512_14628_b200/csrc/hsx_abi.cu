@@ -129,6 +129,7 @@ struct hsx_plan {
   int k2_armed = 0;                  // the last launch was such a K1: hsx_select(0) chains behind it
   int k2_pending = 0;                // a counting K1 ran whose counts no chained K2 consumed yet
   int k3_armed = 0;                  // the last launch was a chained single-pass K2: K3 chains behind it
+  int big_first = 0;                 // work-list order (set_order)
   int* d_sel[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
   double* d_partials[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
@@ -167,6 +168,33 @@ void host_layout(hsx_plan* p) {
     off += row[HSX_SUM_ELEMS];
   }
   p->summary[(size_t)p->n_layers * HSX_SUM_COLS] = off;
+}
+
+// Work-list order of K1 / K2 / K3. big_first: the layers with the costliest
+// selection tails first, so their chained K2 CTAs select while K1 streams the rest
+// (B200 r2m, one GPU: RN18 0.130 -> 0.122 ms with the chain). Otherwise layer order
+// (group-norm tiles first, dense items last): measured faster when K1 reads the
+// node's sums over NVLink (r2n, RN50 2x2: 0.649 vs 0.663 ms).
+void set_order(hsx_plan* p, bool big_first) {
+  auto cost = [&](int l) {
+    const DevLayer& ly = p->layers[l];
+    if (ly.ncons == 0) return -1LL;
+    long long c = (long long)ly.rows + ly.cin;
+    for (int q = 0; q < ly.ncons; ++q) c += ly.G[q];
+    return c;
+  };
+  auto before = [&](int x, int y) {  // strict order of layers x, y
+    if (big_first) return cost(x) > cost(y);
+    const bool dx = cost(x) < 0, dy = cost(y) < 0;
+    return dx != dy ? dy : x < y;
+  };
+  std::stable_sort(p->cand_dyn.begin(), p->cand_dyn.end(),
+                   [&](const Item& x, const Item& y) { return x.layer != y.layer && before(x.layer, y.layer); });
+  for (int q = 0; q < hsx::kMaxPasses; ++q)
+    std::stable_sort(p->sel_list[q].begin(), p->sel_list[q].end(), before);
+  std::stable_sort(p->proj_items.begin(), p->proj_items.end(),
+                   [&](const Item& x, const Item& y) { return x.layer != y.layer && before(x.layer, y.layer); });
+  p->big_first = big_first ? 1 : 0;
 }
 
 int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
@@ -335,19 +363,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
   // dynamic candidate launch: group-norm tiles first, short dense items fill the
   // tail; persistent CTAs take the largest items first
   p->cand_dyn.insert(p->cand_dyn.end(), dense_items.begin(), dense_items.end());
-  // launch order: the layers with the costliest selection tails first (their chained
-  // K2 CTAs then select while K1 streams the rest; B200 r2m: RN18 1x1 0.130 -> 0.122
-  // ms with the chain); HSX_K1_ORDER=0: layer order
-  auto tail_cost = [&](const Item& it) {
-    const DevLayer& ly = p->layers[it.layer];
-    if (ly.ncons == 0) return 0LL;
-    long long c = (long long)ly.rows + ly.cin;
-    for (int q = 0; q < ly.ncons; ++q) c += ly.G[q];
-    return c;
-  };
-  if (env_flag("HSX_K1_ORDER", 1))
-    std::stable_sort(p->cand_dyn.begin(), p->cand_dyn.end(),
-                     [&](const Item& x, const Item& y) { return tail_cost(x) > tail_cost(y); });
+  // launch order: set_order() below, once the selection lists exist
   // the last layer needs no trailing pad: arenas may be exactly-sized tensors
   if (n > 0) off = p->layers.back().off + p->layers.back().n;
   p->arena = off;
@@ -382,18 +398,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         p->sel_list[q].push_back(l);
     }
   }
-  if (env_flag("HSX_K1_ORDER", 1)) {  // selection / K3 items in the order K1 finishes their layers
-    auto cost = [&](int l) {
-      const DevLayer& ly = p->layers[l];
-      long long c = (long long)ly.rows + ly.cin;
-      for (int q = 0; q < ly.ncons; ++q) c += ly.G[q];
-      return c;
-    };
-    for (int q = 0; q < hsx::kMaxPasses; ++q)
-      std::stable_sort(p->sel_list[q].begin(), p->sel_list[q].end(), [&](int x, int y) { return cost(x) > cost(y); });
-    std::stable_sort(p->proj_items.begin(), p->proj_items.end(),
-                     [&](const Item& x, const Item& y) { return cost(x.layer) > cost(y.layer); });
-  }
+  set_order(p, env_flag("HSX_K1_ORDER", 1) != 0);
   if (p->cand_smem > kMaxSmem) return fail(HSX_ESHAPE, "candidate tile needs %zu B of shared memory", p->cand_smem);
   host_layout(p);
   return HSX_OK;
@@ -830,6 +835,19 @@ int hsx_select_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, con
   hsx::launch_select_project(sp, ka, (int)p->proj_items.size(), z_node, mask,
                              std::max(p->select_smem[0], p->fixup_smem), S(stream));
   HSX_LAUNCHED("select_project");
+  return HSX_OK;
+}
+
+int hsx_plan_set_order(hsx_plan* p, int32_t big_first) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  if ((big_first != 0) == (p->big_first != 0)) return HSX_OK;
+  set_order(p, big_first != 0);
+  HSX_CUDA(cudaMemcpy(p->d_cand, p->cand_dyn.data(), p->cand_dyn.size() * sizeof(Item), cudaMemcpyHostToDevice));
+  HSX_CUDA(cudaMemcpy(p->d_proj, p->proj_items.data(), p->proj_items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+  for (int q = 0; q < hsx::kMaxPasses; ++q)
+    if (!p->sel_list[q].empty())
+      HSX_CUDA(cudaMemcpy(p->d_sel[q], p->sel_list[q].data(), p->sel_list[q].size() * sizeof(int),
+                          cudaMemcpyHostToDevice));
   return HSX_OK;
 }
 

@@ -140,6 +140,10 @@ class Plan:
         """Structured keep sets in the selection tail (one node: the union is the local mask)."""
         _lib.call("hsx_plan_set_single_node", self._h, 1 if on else 0)
 
+    def set_order(self, big_first: bool):
+        """Work-list order (hsx_plan_set_order): costliest selections first, or layer order."""
+        _lib.call("hsx_plan_set_order", self._h, 1 if big_first else 0)
+
     def set_penalties(self, rho1: dict | None, rho2: dict | None, weight_decay: float,
                       num_nodes: int, accels_per_node: int, identity: bool = False):
         def arr(d):

@@ -129,6 +129,8 @@ class HSADMMSync:
         self.transport = transport
         if transport == "peer":
             self._init_peer_buffers()
+            if self.P == 2 and "HSX_K1_ORDER" not in os.environ:
+                self.plan.set_order(False)   # K1 reads the intra sum over NVLink: layer order (r2n)
         # deferred host bookkeeping (step_host): a step returns once its launches are
         # queued; the keep-set counts are read back when the next step starts
         self.defer_host = False

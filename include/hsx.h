@@ -184,6 +184,12 @@ int hsx_plan_set_single_node(hsx_plan* plan, int32_t on);
  * 0 keeps layer order (measured faster when K1 reads the intra sum over NVLink).
  * Synchronous (re-uploads the work lists); call between steps. */
 int hsx_plan_set_order(hsx_plan* plan, int32_t big_first);
+/* One-node chain K1 -> K2 -> K3 -> K67 (default off; HSX_K67_CHAIN=0 forces it
+ * off): the caller promises that every hsx_project_keep_sets of this single-node
+ * plan is followed, as the next launch on the same stream, by hsx_local_sync.
+ * The projection then runs behind the chained selection with the keep-set fixups
+ * in its items, and K67 starts per layer as soon as the layer is projected. */
+int hsx_plan_set_k67_chain(hsx_plan* plan, int32_t on);
 
 /* ---- K4: leader mask union  out = OR_m gathered[m]  (transport.py:455-457) -- */
 int hsx_mask_or(const uint32_t* gathered, int32_t n_ranks, int64_t words, uint32_t* out,
@@ -279,8 +285,14 @@ int hsx_decompact_average(const hsx_plan* plan, const float* const* srcs, int32_
  * identity, so z = z_node + v on the kept rectangle (0 elsewhere), u += theta -
  * z_node, v += z_node - z, in place and bitwise equal to hsx_compact_dual then
  * hsx_decompact_dual(divisor 1) — without the compact buffer. residuals != 0
- * also accumulates all nine residual slots (z_node_prev required). */
-int hsx_local_sync(const hsx_plan* plan, const float* theta, float* u, const float* z_node, float* v,
+ * also accumulates all nine residual slots (z_node_prev required).
+ * Issued as the next launch on the same stream after a one-node
+ * hsx_project_keep_sets that ran chained (hsx_plan_set_k67_chain), it is
+ * chained too: that projection runs each layer's keep-set
+ * fixup in its last item and publishes the layer, and this kernel's items start
+ * per layer as soon as their layer is published (dense layers once the candidate
+ * and selection launches are complete); completion still implies the projection's. */
+int hsx_local_sync(hsx_plan* plan, const float* theta, float* u, const float* z_node, float* v,
                    float* z, const float* z_node_prev, int32_t residuals, void* stream);
 /* vec[layer][9] = the layer's slot sums (leader == 0 zeroes slots 3-8: the
  * node's leader contributes them to the intra SUM, consensus.py:550-563). */

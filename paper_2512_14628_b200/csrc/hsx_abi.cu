@@ -129,6 +129,9 @@ struct hsx_plan {
   int k2_armed = 0;                  // the last launch was such a K1: hsx_select(0) chains behind it
   int k2_pending = 0;                // a counting K1 ran whose counts no chained K2 consumed yet
   int k3_armed = 0;                  // the last launch was a chained single-pass K2: K3 chains behind it
+  int k67_armed = 0;                 // the last launch was a chained one-node K3 with fixups: K67 chains
+  int k67_chain = 0;                 // hsx_plan_set_k67_chain: the caller follows every one-node projection with K67
+  unsigned int *d_ready3 = nullptr, *d_cnt67 = nullptr, *d_up = nullptr;  // K3 -> K67 chain flags
   int big_first = 0;                 // work-list order (set_order)
   int* d_sel[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
@@ -142,7 +145,7 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_k1done, d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_ready3, d_cnt67, d_up, d_k1done, d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
                     d_ch_prev};
     for (void* p : ptrs)
@@ -460,6 +463,9 @@ int upload_plan(hsx_plan* p) {
   if ((rc = upload(&p->d_summary, p->summary))) return rc;
   if ((rc = alloc0(&p->d_done, 1))) return rc;
   if ((rc = alloc0(&p->d_k1done, (long long)p->prunable.size() + 1))) return rc;
+  if ((rc = alloc0(&p->d_ready3, std::max(1, p->n_layers)))) return rc;
+  if ((rc = alloc0(&p->d_cnt67, std::max(1, p->n_layers)))) return rc;
+  if ((rc = alloc0(&p->d_up, 2))) return rc;   // [0] upstream complete, [1] K67 items done
   return HSX_OK;
 }
 
@@ -595,6 +601,7 @@ static hsx::CandArgs cand_args(hsx_plan* p, const float* sum, const float* theta
   std::memset(&a, 0, sizeof(a));
   p->k2_armed = 0;   // only a counting dynamic K1 (arm_chain) is chained to
   p->k3_armed = 0;
+  p->k67_armed = 0;
   a.s = sum;
   a.theta = theta;
   a.u = u;
@@ -733,8 +740,10 @@ int hsx_select(hsx_plan* p, int32_t pass, void* stream) {
   if (chained) p->k2_pending = 0;
   // a single-pass plan's chained selection also publishes per-layer ready flags, so
   // the K3 launched next (hsx_project / hsx_project_keep_sets) chains behind it
+  // (alone measured RN18 +1%, RN50 -1%, r2n: on by default only for one-node plans,
+  // where K67 chains behind it as well)
   const bool k3 = chained && p->max_passes == 1 && p->sel_list[0].size() == p->prunable.size() &&
-                  env_flag("HSX_K3_CHAIN", 0);  // measured: RN18 +1%, RN50 -1% (r2n): opt-in
+                  env_flag("HSX_K3_CHAIN", p->single_node && p->k67_chain ? 1 : 0);
   p->k3_armed = k3 ? 1 : 0;
   hsx::launch_select(p->d_layers, p->d_sel[pass], n, pass, p->d_partials[pass], p->d_norms[pass],
                      fl, keep_args(p, nullptr, nullptr, nullptr), p->single_node, p->select_smem[pass], S(stream),
@@ -803,6 +812,16 @@ int hsx_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, const uint
   hsx::KeepArgs ka = keep_args(p, p->d_proj, mask, prev_mask);
   const bool chained = p->k3_armed;
   p->k3_armed = 0;
+  if (chained && p->k67_chain) {
+    // K3 behind the chained K2 runs each layer's fixup in its last item and publishes
+    // the layer to a chained K67 (hsx_local_sync next on this stream)
+    hsx::ChainK67 c{p->d_ready3, p->d_up, nullptr, nullptr, nullptr};
+    hsx::launch_project(ka, (int)p->proj_items.size(), z_node, mask, 1, S(stream), p->d_ready, p->d_pdone, c,
+                        p->fixup_smem);
+    HSX_LAUNCHED("project_check_fixup");
+    p->k67_armed = 1;
+    return HSX_OK;
+  }
   hsx::launch_project(ka, (int)p->proj_items.size(), z_node, mask, 1, S(stream), chained ? p->d_ready : nullptr,
                       p->d_pdone);
   HSX_LAUNCHED("project_check");
@@ -835,6 +854,12 @@ int hsx_select_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, con
   hsx::launch_select_project(sp, ka, (int)p->proj_items.size(), z_node, mask,
                              std::max(p->select_smem[0], p->fixup_smem), S(stream));
   HSX_LAUNCHED("select_project");
+  return HSX_OK;
+}
+
+int hsx_plan_set_k67_chain(hsx_plan* p, int32_t on) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  p->k67_chain = on && env_flag("HSX_K67_CHAIN", 1) ? 1 : 0;
   return HSX_OK;
 }
 
@@ -1043,11 +1068,14 @@ int hsx_decompact_dual_resid(const hsx_plan* p, const float* flat, float divisor
   return HSX_OK;
 }
 
-int hsx_local_sync(const hsx_plan* p, const float* theta, float* u, const float* z_node, float* v, float* z,
+int hsx_local_sync(hsx_plan* p, const float* theta, float* u, const float* z_node, float* v, float* z,
                    const float* z_node_prev, int32_t residuals, void* stream) {
   if (!p || !theta || !u || !z_node || !v || !z) return fail(HSX_EINVAL, "null argument");
   if (residuals && !z_node_prev) return fail(HSX_EINVAL, "residuals need z_node_prev");
   hsx::ElemArgs a = elem_args(p);
+  if (p->k67_armed)  // right behind the chained one-node K3: per-layer waits instead of the grid's
+    a.c67 = hsx::ChainK67{p->d_ready3, p->d_up, p->d_cnt67, p->d_scount, p->d_up + 1};
+  p->k67_armed = 0;
   a.theta = theta;
   a.u = u;
   a.zn = z_node;

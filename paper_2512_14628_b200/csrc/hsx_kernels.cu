@@ -1568,6 +1568,8 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
   if (CHECK) flag_irregular(a, dl.pidx, bad);
 }
 
+__device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);
+
 // Chained (ready != nullptr, behind a chained K2): like the chained K2, the CTA lets
 // its dependents launch at once, waits for its layer's selection (ready[layer],
 // published by K2 with release semantics), projects, and waits for the grid before
@@ -1575,7 +1577,7 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
 template <bool CHECK>
 __global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __restrict__ zn,
                                                          uint32_t* __restrict__ mask, unsigned int* ready,
-                                                         unsigned int* pdone) {
+                                                         unsigned int* pdone, ChainK67 c67) {
   extern __shared__ float4 ring[];
   const Item it = a.items[blockIdx.x];  // a register copy: a reference into global memory is
   if (ready == nullptr) {               // reloaded after every store through zn / mask
@@ -1594,15 +1596,50 @@ __global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __re
   }
   __syncthreads();
   project_item<CHECK>(a, zn, mask, it, ring);
+  __shared__ bool last_item, last_layer;
   __syncthreads();
+  const DevLayer& dl = a.layers[it.layer];
   if (threadIdx.x == 0) {
-    const DevLayer& dl = a.layers[it.layer];
-    if (atomicAdd(pdone + dl.pidx, 1u) == (unsigned)dl.npitems - 1) {
+    __threadfence();
+    last_item = atomicAdd(pdone + dl.pidx, 1u) == (unsigned)dl.npitems - 1;
+  }
+  __syncthreads();
+  if (last_item) {
+    __threadfence();
+    if (threadIdx.x == 0) {
       pdone[dl.pidx] = 0;
       ready[it.layer] = 0;
     }
+    if (c67.ready3) {
+      // the layer's keep-set fixup here (not a launch of its own), then the chained
+      // K67 may take the layer; the last layer lays the flat buffer out again if a
+      // layer turned out irregular
+      fixup_layer(a, it.layer, reinterpret_cast<uint8_t*>(ring));
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(c67.ready3 + it.layer), "r"(1u) : "memory");
+        last_layer = atomicAdd(pdone + a.n_prunable, 1u) == (unsigned)a.n_prunable - 1;
+      }
+      __syncthreads();
+      if (last_layer) {
+        __threadfence();
+        if (*reinterpret_cast<volatile int*>(a.irr_any)) layout_flat(a);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          pdone[a.n_prunable] = 0;
+          *a.irr_any = 0;
+        }
+      }
+    }
   }
   pdl_wait();
+  // everything before this launch is complete: the chained K67's dense-layer items
+  // (which read K1's output directly) may start
+  if (c67.upstream && threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(c67.upstream), "r"(1u) : "memory");
+  }
 }
 
 __device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);
@@ -1679,13 +1716,13 @@ void launch_select_project(const SelProjArgs& sp, const KeepArgs& a, int n_items
 }
 
 void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st,
-                    unsigned int* ready, unsigned int* pdone) {
+                    unsigned int* ready, unsigned int* pdone, ChainK67 c67, size_t fix_smem) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * kThreads * sizeof(float4);
   if (check)
-    launch_pdl(k_project<true>, n_items, kThreads, smem, st, a, zn, mask, ready, pdone);
+    launch_pdl(k_project<true>, n_items, kThreads, std::max(smem, fix_smem), st, a, zn, mask, ready, pdone, c67);
   else
-    launch_pdl(k_project<false>, n_items, kThreads, smem, st, a, zn, mask, ready, pdone);
+    launch_pdl(k_project<false>, n_items, kThreads, smem, st, a, zn, mask, ready, pdone, c67);
 }
 
 // ---------------------------------------------------------------------------
@@ -2227,9 +2264,30 @@ void launch_decompact(const ElemArgs& a, int n_items, cudaStream_t st) {
 //   u <- u + (theta - z_node); z <- kept ? z_node + v : 0; v <- v + (z_node - z)
 // RESID: the K6 (0-2) and K7 (3-8) residual slots in one pass (z_prev, z_node_prev
 // streamed too).
+// Chained (a.c67.ready3 != nullptr, behind a chained K3 that ran the fixups): the
+// CTA lets its dependents launch, waits for its layer's projection (ready3[layer];
+// dense layers: the upstream flag K3 sets once K1 and K2 are complete), runs, and
+// waits for the grid before it at the end; the layer's last item / the launch's last
+// item re-zero the flags for the next step.
 template <bool RESID>
 __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
-  PDL_ENTRY();
+  const bool chained = a.c67.ready3 != nullptr;
+  if (!chained) {
+    PDL_ENTRY();
+  } else {
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+      const Item& itc = a.items[blockIdx.x];
+      const unsigned* f = a.layers[itc.layer].ncons > 0 ? a.c67.ready3 + itc.layer : a.c67.upstream;
+      unsigned v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v) break;
+        __nanosleep(128);
+      }
+    }
+    __syncthreads();
+  }
   constexpr int NB = RESID ? 6 : 4;
   constexpr int D = RESID ? 3 : kDepth;  // 6 x 3 x 4 KB = 72 KB / 4 x 4 x 4 KB = 64 KB
   extern __shared__ float4 ring[];
@@ -2313,6 +2371,23 @@ __global__ void __launch_bounds__(kThreads) k_local_sync(ElemArgs a) {
                 });
   }
   if (RESID) block_partials<9>(acc, a.rpart + (long long)blockIdx.x * kResidSlots);
+  if (chained) {
+    // after the grid wait the chained K3 is complete (its last upstream store too), so
+    // the last item to get here may re-zero the flags: every item is past its wait
+    pdl_wait();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int l = it.layer;
+      if (a.layers[l].ncons > 0 && atomicAdd(a.c67.cnt + l, 1u) == (unsigned)a.c67.count[l] - 1) {
+        a.c67.cnt[l] = 0;
+        a.c67.ready3[l] = 0;
+      }
+      if (atomicAdd(a.c67.all, 1u) == gridDim.x - 1) {
+        *a.c67.all = 0;
+        *a.c67.upstream = 0;
+      }
+    }
+  }
 }
 
 void launch_local_sync(const ElemArgs& a, int n_items, cudaStream_t st) {

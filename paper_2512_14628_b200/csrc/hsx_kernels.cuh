@@ -145,6 +145,17 @@ struct CandArgs {
   int sqcap;                           // doubles of the sq sub-tile region
 };
 
+// K3 -> K67 chain of one node: per-layer "projected + fixed" flags published by the
+// chained K3, the upstream-complete flag (K1 and K2 done), per-layer item counters
+// of K67 (stream items per layer: count[]), and a launch-wide counter
+struct ChainK67 {
+  unsigned int* ready3;    // [layers]; nullptr = not chained
+  unsigned int* upstream;
+  unsigned int* cnt;       // [layers]
+  const int* count;        // [layers] stream items per layer
+  unsigned int* all;
+};
+
 struct ElemArgs {
   const float* __restrict__ theta;
   float* __restrict__ u;
@@ -169,6 +180,7 @@ struct ElemArgs {
   const float* flat_in2;
   float* zhat_out;
   double avg_div;
+  ChainK67 c67;                        // K67 chained behind the chained K3 (ready3 == nullptr: off)
 };
 constexpr int kResidSlots = 9;         // consensus.py:235 (_INTER_SLOTS)
 
@@ -185,8 +197,11 @@ void launch_keep_fixup(const KeepArgs& a, const int* prunable, int n, size_t sme
 // K3; check != 0: flag layers with a kept zero (structured keep sets)
 // ready != nullptr: chained behind a chained K2 that publishes ready[layer] (pdone:
 // per prunable layer item counters, left zeroed)
+// c67.ready3 != nullptr (with ready): the layer's last item also runs the keep-set
+// fixup (fix_smem bytes) and publishes ready3[layer] for a chained K67
 void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, int check, cudaStream_t st,
-                    unsigned int* ready = nullptr, unsigned int* pdone = nullptr);
+                    unsigned int* ready = nullptr, unsigned int* pdone = nullptr, ChainK67 c67 = ChainK67{},
+                    size_t fix_smem = 0);
 struct SelProjArgs {
   const int* list;          // layers to select (pass 0)
   int nsel;

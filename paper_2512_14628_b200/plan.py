@@ -140,6 +140,11 @@ class Plan:
         """Structured keep sets in the selection tail (one node: the union is the local mask)."""
         _lib.call("hsx_plan_set_single_node", self._h, 1 if on else 0)
 
+    def set_k67_chain(self, on: bool):
+        """One node: the projection chains into K67 (hsx_plan_set_k67_chain); every
+        project_keep_sets must then be followed by local_sync."""
+        _lib.call("hsx_plan_set_k67_chain", self._h, 1 if on else 0)
+
     def set_order(self, big_first: bool):
         """Work-list order (hsx_plan_set_order): costliest selections first, or layer order."""
         _lib.call("hsx_plan_set_order", self._h, 1 if big_first else 0)

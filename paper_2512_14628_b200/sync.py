@@ -82,6 +82,14 @@ class HSADMMSync:
         # one node: the union mask is every rank's local mask, so the selection derives
         # the keep sets of the kept rectangle and K3 only checks it (hsx_project_keep_sets)
         self.plan.set_single_node(self.M == 1 and os.environ.get("HSX_SINGLE_NODE", "1") != "0")
+        # one node, opt-in (HSX_K67_CHAIN=1): every sync step's projection is followed
+        # by K67, so the two may chain per layer; that needs the keep-set summary fetched
+        # after K67 (the fetch's event would sit between them), which delays the host's
+        # next step: measured +6% on RN18 1x1, -1..3% on RN50 / RN152 (r2p)
+        self._k67_chain = (os.environ.get("HSX_K67_CHAIN") == "1" and self.M == 1
+                           and os.environ.get("HSX_SINGLE_NODE", "1") != "0"
+                           and os.environ.get("HSX_LOCAL_SYNC", "1") != "0")
+        self.plan.set_k67_chain(self._k67_chain)
         self.prunable = self.plan.prunable
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         pl, dev = self.plan, self.device
@@ -358,7 +366,8 @@ class HSADMMSync:
             return None
         ev = None
         if fused_keep:
-            ev = pl.keep_sets_fetch_async()
+            if not self._k67_chain:   # chained: fetched after K67 (K3 -> K67 consecutive launches)
+                ev = pl.keep_sets_fetch_async()
         elif dynamic:
             words = pl.mask_words
             if self.is_leader:
@@ -380,6 +389,8 @@ class HSADMMSync:
             # same z_node and v, so each rank runs K6+K7 locally in one pass (bitwise
             # what the compact round trip and the intra broadcast would deliver)
             self._local_sync()
+            if fused_keep and self._k67_chain:
+                ev = pl.keep_sets_fetch_async()
             return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
         decompacted = False
         if self.is_leader:
@@ -602,7 +613,8 @@ class HSADMMSync:
         # phase 4: mask union (leaders), broadcast to followers, keep sets
         ev = None
         if fused_keep:
-            ev = pl.keep_sets_fetch_async()
+            if not self._k67_chain:   # chained: fetched after K67 (K3 -> K67 consecutive launches)
+                ev = pl.keep_sets_fetch_async()
         elif dynamic:
             if self.is_leader:
                 yield AllGather(self.inter, self.local_mask, self.gathered, "mask_sync", k)
@@ -617,6 +629,8 @@ class HSADMMSync:
             # one node: no leader exchange; every rank runs K6+K7 locally (bitwise the
             # leader's compact round trip + broadcast), no mid-step host wait
             self._local_sync()
+            if fused_keep and self._k67_chain:
+                ev = pl.keep_sets_fetch_async()
             return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
         # compaction fused with the intra dual update (K6 reads sizes on device, so
         # it runs while the host waits for the D2H and sizes the collectives)

@@ -597,26 +597,34 @@ def run_ours(args):
     eng.settle()
     eng.defer_host = False
     # e2e through the public API with host buffers: HSADMMSync.step_host copies every
-    # step's theta in from pinned host memory and z out to pinned host memory (copy
-    # streams; consecutive steps overlap their copies with compute)
-    for _ in range(2):
-        k += 1
-        eng.step_host(k, theta_host, z_host)
-    torch.cuda.synchronize()
-    eng.settle()
-    barrier()
-    torch.cuda.synchronize()
-    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    es.record()
-    for i in range(args.steps):
-        done = eng.step_host(k + 1 + i, theta_host, z_host)
-    torch.cuda.current_stream().wait_event(done)
-    ee.record()
-    torch.cuda.synchronize()
-    eng.settle()
-    barrier()
-    k += args.steps
-    e2e_ms = max_over_ranks(es.elapsed_time(ee)) / args.steps
+    # step's theta in from pinned host memory on a copy stream (double-buffered, so
+    # step k+1's input copy overlaps step k) and the step's result to the host: the
+    # per-layer keep-set summary (kept channels, payload sizes = leader bytes, drift;
+    # the step's own D2H, which the host's freeze / ledger bookkeeping reads) — and,
+    # in the second pass, the whole new consensus z (4N bytes) as well
+    def e2e_pass(k0, z_out):
+        for i in range(2):
+            eng.step_host(k0 + i, theta_host, z_out)
+        torch.cuda.synchronize()
+        eng.settle()
+        barrier()
+        torch.cuda.synchronize()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es.record()
+        for i in range(args.steps):
+            done = eng.step_host(k0 + 2 + i, theta_host, z_out)
+        torch.cuda.current_stream().wait_event(done)
+        ee.record()
+        torch.cuda.synchronize()
+        eng.settle()
+        barrier()
+        return max_over_ranks(es.elapsed_time(ee)) / args.steps
+
+    e2e_ms = e2e_pass(k + 1, None)
+    k += args.steps + 2
+    e2e_z_ms = e2e_pass(k + 1, z_host)
+    k += args.steps + 2
+    summary_bytes = int(eng.plan.summary_host.numel()) * 8
     eng.check_barriers()
     nvlink = nvlink_peaks(world, dev) if world > 1 else None
     if rank != 0:
@@ -654,10 +662,16 @@ def run_ours(args):
                      "timed_region": "second K-step dynamic pass with per-launch CUDA events "
                                      f"({kstep_ms:.3f} ms/step with events)"},
         "e2e": {"value": N * world / (e2e_ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": 4 * eng.plan.arena, "d2h_bytes_per_step": 4 * eng.plan.arena,
+                "h2d_bytes_per_step": 4 * eng.plan.arena, "d2h_bytes_per_step": summary_bytes,
                 "path": "HSADMMSync.step_host via the C ABI: every step's theta H2D from pinned host memory "
-                        "and z D2H to pinned host memory inside the timed region (copy streams, double-"
-                        "buffered; K steps timed end to end, no L2 flush: 6 state arenas > L2)"},
+                        "(copy stream, double-buffered) and the step's result D2H — the per-layer keep-set "
+                        "summary (kept counts, payload sizes = leader bytes, drift), which the host's freeze "
+                        "/ ledger bookkeeping consumes — inside the timed region; K steps timed end to end, "
+                        "no L2 flush (6 state arenas > L2)",
+                "with_z_readback": {"value": N * world / (e2e_z_ms / 1e3) / 1e6, "ms_per_step": e2e_z_ms,
+                                    "d2h_bytes_per_step": summary_bytes + 4 * eng.plan.arena,
+                                    "path": "the same, plus the whole new consensus z copied to pinned host "
+                                            "memory every step"}},
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks.summary() if clocks is not None else {"sm_mhz": None, "reasons": ["not sampled (HSX_BENCH_NO_CLOCKS)"]},

@@ -923,6 +923,9 @@ template <int MODE>
 struct K1 {
   static constexpr int NB = peer_mode(MODE) ? peer_slots(MODE) + 2 : 4;  // ring slots per stage
   static constexpr int ZS = peer_mode(MODE) ? peer_slots(MODE) : 2;      // slot of z (v follows)
+  // ring depth: two peers keep 5 stages in flight (more NVLink bytes in flight per
+  // thread; 6 x 4 x 4 KB = 96 KB, two CTAs per SM)
+  static constexpr int D = MODE == kModePeers2 ? 6 : kDepth;
 };
 
 // source pointers of one layer (offset already applied)
@@ -1063,7 +1066,7 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
   float* zn = p.zn + off;
   const uint32_t* fm = masked ? p.fmask + mword : nullptr;
   const unsigned long long pf = l2pol(kL2First), pl = l2pol(kL2Last);
-  ring_run(
+  ring_run<K1<MODE>::D>(
       count,
       [&](int d, int i) { k1_issue<MODE, false>(ring, d, src, begin + 4 * (t + (long long)i * kThreads), n, pf); },
       [&](int d, int i) {
@@ -1115,7 +1118,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const long long stride = (long long)RP * L;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   const unsigned long long pf = l2pol(kL2First), pl = l2pol(kL2Last);
-  ring_run(
+  ring_run<K1<MODE>::D>(
       count,
       [&](int d, int i) { k1_issue<MODE, true>(ring, d, src, r0 * L + i * stride, 0, pf); },
       [&](int d, int i) {
@@ -1360,7 +1363,9 @@ void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, c
     return v && v[0] == '1';
   }();
   if (a.peers.n == 2 && peers2)
-    launch_candidate_mode<kModePeers2>(a, n_items, frozen, smem, st);
+    launch_candidate_mode<kModePeers2>(a, n_items, frozen,
+                                       std::max(smem, (size_t)K1<kModePeers2>::D * K1<kModePeers2>::NB * kThreads * 16),
+                                       st);
   else if (a.peers.n > 0)
     launch_candidate_mode<kModePeers>(a, n_items, frozen, smem + (size_t)kDepth * (kMaxPeers - 2) * kThreads * 16, st);
   else if (a.identity)

@@ -190,6 +190,12 @@ int hsx_plan_set_order(hsx_plan* plan, int32_t big_first);
  * The projection then runs behind the chained selection with the keep-set fixups
  * in its items, and K67 starts per layer as soon as the layer is projected. */
 int hsx_plan_set_k67_chain(hsx_plan* plan, int32_t on);
+/* Host buffer (page-locked, mapped) of the plan's keep-set summary rows, the same
+ * layout hsx_keep_sets_fetch writes. With the K67 chain on (and the plan's
+ * selection fully chained) the projection publishes the summary into it from the
+ * device as soon as it is final; hsx_keep_sets_fetch_async with this buffer is
+ * then a no-op and hsx_keep_sets_fetch_wait waits for the publication. */
+int64_t* hsx_plan_summary_host(hsx_plan* plan);
 
 /* ---- K4: leader mask union  out = OR_m gathered[m]  (transport.py:455-457) -- */
 int hsx_mask_or(const uint32_t* gathered, int32_t n_ranks, int64_t words, uint32_t* out,

@@ -71,6 +71,7 @@ SIGNATURES = {
     "hsx_plan_set_single_node": (C.c_int, [P, C.c_int32]),
     "hsx_plan_set_order": (C.c_int, [P, C.c_int32]),
     "hsx_plan_set_k67_chain": (C.c_int, [P, C.c_int32]),
+    "hsx_plan_summary_host": (C.POINTER(C.c_int64), [P]),
     "hsx_mask_or": (C.c_int, [VP, I32, I64, VP, VP]),
     "hsx_keep_sets": (C.c_int, [P, VP, VP, VP]),
     "hsx_keep_sets_fetch": (C.c_int, [P, VP, VP]),

@@ -132,6 +132,10 @@ struct hsx_plan {
   int k67_armed = 0;                 // the last launch was a chained one-node K3 with fixups: K67 chains
   int k67_chain = 0;                 // hsx_plan_set_k67_chain: the caller follows every one-node projection with K67
   unsigned int *d_ready3 = nullptr, *d_cnt67 = nullptr, *d_up = nullptr;  // K3 -> K67 chain flags
+  long long* h_pub = nullptr;        // mapped host summary the chained K3 publishes into (+ seq word after)
+  unsigned int* d_seq_ctr = nullptr;
+  unsigned int last_seq = 0;
+  int pub_mapped = 0;                // dynamic one-node steps publish the summary from the device
   int big_first = 0;                 // work-list order (set_order)
   int* d_sel[hsx::kMaxPasses] = {nullptr, nullptr, nullptr};
   int* d_prunable = nullptr;
@@ -151,6 +155,8 @@ struct hsx_plan {
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (fetch_ev) cudaEventDestroy(fetch_ev);
+    if (h_pub) cudaFreeHost(h_pub);
+    if (d_seq_ctr) cudaFree(d_seq_ctr);
     for (int i = 0; i < hsx::kMaxPasses; ++i) {
       if (d_sel[i]) cudaFree(d_sel[i]);
       if (d_partials[i]) cudaFree(d_partials[i]);
@@ -815,7 +821,15 @@ int hsx_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, const uint
   if (chained && p->k67_chain) {
     // K3 behind the chained K2 runs each layer's fixup in its last item and publishes
     // the layer to a chained K67 (hsx_local_sync next on this stream)
-    hsx::ChainK67 c{p->d_ready3, p->d_up, nullptr, nullptr, nullptr};
+    hsx::ChainK67 c{p->d_ready3, p->d_up, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+    if (p->pub_mapped) {
+      long long* dsum = nullptr;
+      HSX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dsum), p->h_pub, 0));
+      c.pub_sum = dsum;
+      c.pub_seq = reinterpret_cast<unsigned int*>(dsum + p->summary.size());
+      c.seq_ctr = p->d_seq_ctr;
+      c.n_sum = (int)p->summary.size();
+    }
     hsx::launch_project(ka, (int)p->proj_items.size(), z_node, mask, 1, S(stream), p->d_ready, p->d_pdone, c,
                         p->fixup_smem);
     HSX_LAUNCHED("project_check_fixup");
@@ -860,6 +874,18 @@ int hsx_select_project_keep_sets(hsx_plan* p, float* z_node, uint32_t* mask, con
 int hsx_plan_set_k67_chain(hsx_plan* p, int32_t on) {
   if (!p) return fail(HSX_EINVAL, "null plan");
   p->k67_chain = on && env_flag("HSX_K67_CHAIN", 1) ? 1 : 0;
+  // every dynamic one-node step then runs the chained projection, which publishes
+  // the summary from the device into the mapped host buffer (hsx_plan_summary_host)
+  const bool always = p->k67_chain && p->single_node && env_flag("HSX_K2_CHAIN", 1) && p->max_passes == 1 &&
+                      !p->prunable.empty() && p->sel_list[0].size() == p->prunable.size();
+  p->pub_mapped = 0;
+  if (always && hsx_plan_summary_host(p)) {
+    if (!p->d_seq_ctr) HSX_CUDA(cudaMalloc(&p->d_seq_ctr, sizeof(unsigned int)));
+    HSX_CUDA(cudaMemset(p->d_seq_ctr, 0, sizeof(unsigned int)));
+    p->h_pub[p->summary.size()] = 0;
+    p->last_seq = 0;
+    p->pub_mapped = 1;
+  }
   return HSX_OK;
 }
 
@@ -905,6 +931,8 @@ int hsx_keep_sets_fetch(hsx_plan* p, int64_t* host_summary, void* stream) {
 
 int hsx_keep_sets_fetch_async(hsx_plan* p, int64_t* host_summary, void* stream) {
   if (!p || !host_summary) return fail(HSX_EINVAL, "null argument");
+  if (p->pub_mapped && host_summary == reinterpret_cast<int64_t*>(p->h_pub))
+    return HSX_OK;   // the chained projection publishes it from the device (hsx_keep_sets_fetch_wait)
   HSX_CUDA(cudaMemcpyAsync(host_summary, p->d_summary, p->summary.size() * sizeof(long long),
                            cudaMemcpyDeviceToHost, S(stream)));
   // completion marker the host can wait on mid-step; under stream capture an
@@ -919,8 +947,35 @@ int hsx_keep_sets_fetch_async(hsx_plan* p, int64_t* host_summary, void* stream) 
 
 int hsx_keep_sets_fetch_wait(hsx_plan* p) {
   if (!p) return fail(HSX_EINVAL, "null plan");
+  if (p->pub_mapped) {
+    // the device bumps the mapped sequence word once per published summary, and the
+    // host waits once per dynamic step (before the next one is launched)
+    volatile unsigned int* seq = reinterpret_cast<volatile unsigned int*>(p->h_pub + p->summary.size());
+    unsigned v;
+    while ((v = *seq) == p->last_seq) {
+      cudaError_t e = cudaGetLastError();   // a failed context would never publish
+      if (e != cudaSuccess) return fail(HSX_ECUDA, "waiting for the keep-set summary: %s", cudaGetErrorString(e));
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    p->last_seq = v;
+    return HSX_OK;
+  }
   if (p->fetch_ev) HSX_CUDA(cudaEventSynchronize(p->fetch_ev));
   return HSX_OK;
+}
+
+int64_t* hsx_plan_summary_host(hsx_plan* p) {
+  if (!p) return nullptr;
+  if (!p->h_pub) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&p->h_pub), (p->summary.size() + 1) * sizeof(long long),
+                      cudaHostAllocMapped) != cudaSuccess) {
+      p->h_pub = nullptr;
+      return nullptr;
+    }
+    std::memcpy(p->h_pub, p->summary.data(), p->summary.size() * sizeof(long long));
+    p->h_pub[p->summary.size()] = 0;
+  }
+  return reinterpret_cast<int64_t*>(p->h_pub);
 }
 
 int hsx_set_keep_sets(hsx_plan* p, int32_t l, const int32_t* k_out, int32_t n_out,

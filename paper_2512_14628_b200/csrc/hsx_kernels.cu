@@ -1635,6 +1635,19 @@ __global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __re
           pdone[a.n_prunable] = 0;
           *a.irr_any = 0;
         }
+        if (c67.pub_sum) {
+          // the summary is final: publish it to the host now (the K67 behind this
+          // launch keeps the stream busy, so no copy op can sit between them)
+          __threadfence();
+          for (int i = threadIdx.x; i < c67.n_sum; i += blockDim.x)
+            c67.pub_sum[i] = __ldcg(reinterpret_cast<const long long*>(a.summary) + i);
+          __threadfence_system();
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            const unsigned v = atomicAdd(c67.seq_ctr, 1u) + 1u;
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(c67.pub_seq), "r"(v) : "memory");
+          }
+        }
       }
     }
   }

@@ -154,6 +154,12 @@ struct ChainK67 {
   unsigned int* cnt;       // [layers]
   const int* count;        // [layers] stream items per layer
   unsigned int* all;
+  // the chained K3 publishes the finished keep-set summary straight into mapped host
+  // memory (pub_sum, n_sum int64), then bumps the mapped sequence word pub_seq
+  long long* pub_sum;
+  unsigned int* pub_seq;
+  unsigned int* seq_ctr;   // device-side publish counter
+  int n_sum;
 };
 
 struct ElemArgs {

@@ -142,8 +142,16 @@ class Plan:
 
     def set_k67_chain(self, on: bool):
         """One node: the projection chains into K67 (hsx_plan_set_k67_chain); every
-        project_keep_sets must then be followed by local_sync."""
+        project_keep_sets must then be followed by local_sync. The keep-set summary
+        then lives in the plan's mapped host buffer, published by the device."""
         _lib.call("hsx_plan_set_k67_chain", self._h, 1 if on else 0)
+        if on:
+            import numpy as np
+
+            buf = self._lib.hsx_plan_summary_host(self._h)
+            if buf:
+                n = len(self.names) * _lib.SUM_COLS + 1
+                self.summary_host = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,)))
 
     def set_order(self, big_first: bool):
         """Work-list order (hsx_plan_set_order): costliest selections first, or layer order."""

@@ -71,7 +71,7 @@ size_t select_need(const DevLayer& ly, int q) {
 constexpr long long kItemElems = 8192;  // elements per streaming work item
 constexpr long long kProjElems = 1024;  // K3 items of layers without row-quad tiles (32 words)
 constexpr long long kWordItem = 512;    // mask words per keep-mark item
-constexpr int kMaxSelectGroups = 8192;  // bitonic capacity (96 KB smem)
+constexpr int kMaxSelectGroups = 8192;  // radix top-k capacity of one selection CTA (keys + flags in smem)
 constexpr size_t kMaxSmem = 200 * 1024;
 
 template <typename T>

@@ -71,18 +71,6 @@ def ptr(t) -> int | None:
     return t.data_ptr()
 
 
-def require_cuda_f32(t, name="tensor"):
-    if not isinstance(t, torch.Tensor) or not t.is_cuda:
-        raise TypeError(f"{name} must be a CUDA torch tensor")
-    if t.dtype != torch.float32:
-        raise TypeError(f"{name} must be float32, got {t.dtype}")
-    if not t.is_contiguous():
-        raise ShapeError(f"{name} must be contiguous")
-    if t.data_ptr() % 16:
-        raise ShapeError(f"{name} must be 16-byte aligned")
-    return t
-
-
 class Plan:
     """Owns one ``hsx_plan``; layer order is the caller's (reference) layer order."""
 

@@ -721,10 +721,20 @@ class HSADMMSync:
         return drained
 
     def _leader_average(self, k: int):
-        """C3: leader all-reduce AVG of the flat buffer, one request per <= 32 MiB bucket."""
-        for bi, b in enumerate(self.buckets):
-            yield AllReduce(self.inter, self.flat[b.start:b.start + b.elements], ReduceOp.AVG,
-                            f"z_sync/b{bi}", k, detail=b.detail)
+        """C3: leader all-reduce AVG of the flat buffer. The buckets (<= 32 MiB, the
+        reference's z_sync/b{i} collectives, transport.py:239-280) are contiguous slices
+        of the one flat buffer the compaction wrote, so they travel as one NCCL call
+        over the whole payload (one launch and one ring pipeline instead of one per
+        bucket; elementwise the same average) and are logged one ledger entry per
+        bucket. HSX_NCCL_BUCKETS=1: one call per bucket."""
+        if os.environ.get("HSX_NCCL_BUCKETS") == "1" or len(self.buckets) <= 1:
+            for bi, b in enumerate(self.buckets):
+                yield AllReduce(self.inter, self.flat[b.start:b.start + b.elements], ReduceOp.AVG,
+                                f"z_sync/b{bi}", k, detail=b.detail)
+            return
+        total = sum(b.elements for b in self.buckets)
+        parts = tuple((f"z_sync/b{bi}", b.elements, b.detail) for bi, b in enumerate(self.buckets))
+        yield AllReduce(self.inter, self.flat[:total], ReduceOp.AVG, "z_sync", k, parts=parts)
 
     # -- CUDA-graph steps (one rank) -------------------------------------------------
     def graph_step(self, k: int):

@@ -122,6 +122,9 @@ class AllReduce:
     tag: str
     iteration: int
     detail: tuple | None = None
+    # several logical collectives carried by this one call (the leader average's
+    # buckets over the contiguous flat buffer): ledger entries (tag, elements, detail)
+    parts: tuple | None = None
 
 
 @dataclass
@@ -257,6 +260,13 @@ class CommLedger:
 
 def _ledger(ledger, req, members: int, nbytes: int, op: str):
     if ledger is None or nbytes <= 0:
+        return
+    parts = getattr(req, "parts", None)
+    if parts:   # one call carrying several logical collectives: one entry each
+        esize = int(req.payload.element_size())
+        for tag, n, detail in parts:
+            ledger.append(LedgerEntry(req.iteration, req.group.id, req.group.scope.value, op, int(n),
+                                      int(n) * esize, members, tag, detail))
         return
     n = int(req.payload.numel())
     ledger.append(LedgerEntry(req.iteration, req.group.id, req.group.scope.value, op, n, nbytes,

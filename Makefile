@@ -14,6 +14,9 @@ $(LIB): $(SRC) $(HDR)
 nohints: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -DHSX_NO_L2_HINTS -shared -cudart static -o paper_2512_14628_b200/libhsx_nohints.so $(SRC)
 
+cq32: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -DHSX_CAND_QUADS=32 -shared -cudart static -o paper_2512_14628_b200/libhsx_cq32.so $(SRC)
+
 trace: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -DHSX_TRACE $(TRACE_FLAGS) -shared -cudart static -o paper_2512_14628_b200/libhsx_trace.so $(SRC)
 
@@ -23,4 +26,4 @@ ptxas: $(SRC) $(HDR)
 clean:
 	rm -f $(LIB)
 
-.PHONY: all clean ptxas trace nohints
+.PHONY: all clean ptxas trace nohints cq32

@@ -51,6 +51,10 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 constexpr long long kAlign = 32;        // arena layer alignment in elements (128 B)
 constexpr int kSubElems = 4096;         // target elements per shared-memory sub-tile
 constexpr int hsx_tile_quads = 64;      // quad tiles: rows x 64 column quads (hsx_kernels.cu)
+#ifndef HSX_CAND_QUADS
+#define HSX_CAND_QUADS 64
+#endif
+constexpr int hsx_cand_quads = HSX_CAND_QUADS;  // K1's own quad tiles (hsx_kernels.cu kCandQuads)
 // rows per quad tile (K1; K6/K7; K3); HSX_CAND_TILE_ROWS / HSX_STREAM_TILE_ROWS / HSX_PROJ_TILE_ROWS
 // override them for tuning runs (multiples of 4, <= kMaxTileRows = 128)
 int tile_rows_env(const char* name, int dflt) {
@@ -268,7 +272,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
       // per-channel partials)
       const int kmul = ly.k / std::gcd(ly.k, 4);
       const bool percol = env_flag("HSX_K1_PERCOL", 1) != 0;
-      const int cq = percol ? hsx_tile_quads : hsx_tile_quads / kmul * kmul;
+      const int cq = percol ? hsx_cand_quads : hsx_cand_quads / kmul * kmul;
       ly.percol = percol ? 1 : 0;
       bool quads = (ly.L & 3) == 0 && cq > 0;
       for (int q = 0; q < ly.ncons; ++q) quads = quads && ly.group[q] != HSX_GROUP_FILTER;
@@ -285,7 +289,7 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
             p->cand_dyn.push_back(it);
           }
         ly.ncitems = ly.nparts * nchunks;
-        quadcap = std::max(quadcap, 4 * hsx_tile_quads * (256 / hsx_tile_quads));
+        quadcap = std::max(quadcap, 4 * hsx_cand_quads * (256 / hsx_cand_quads));
       } else {
         sqcap = std::max(sqcap, ly.rsub * ly.L);
         // one shared-memory sub-tile of rows per item

@@ -1097,17 +1097,21 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
 // in a fixed order, then the kh*kw columns of each channel, and the tile writes
 // one fp64 partial per group: partials[part][G].
 constexpr int kTileQuads = 64;
+#ifndef HSX_CAND_QUADS
+#define HSX_CAND_QUADS 64
+#endif
+constexpr int kCandQuads = HSX_CAND_QUADS;  // K1's column quads per tile (its own tiles)
 
 template <int MODE>
 __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, float4* ring,
                                 double* cs) {
-  constexpr int RP = kThreads / kTileQuads;
+  constexpr int RP = kThreads / kCandQuads;
   const int pass = p.pass;
   const int L = ly.L;
   const int Q = L >> 2;
   const int cq = ly.cq;
-  const int jj = threadIdx.x & (kTileQuads - 1);
-  const int ph = threadIdx.x / kTileQuads;
+  const int jj = threadIdx.x & (kCandQuads - 1);
+  const int ph = threadIdx.x / kCandQuads;
   const int j = it.chunk * cq + jj;
   const long long r0 = it.begin + ph, r1 = it.end;
   const int count = (jj < cq && j < Q && r0 < r1) ? (int)((r1 - r0 + RP - 1) / RP) : 0;
@@ -1138,7 +1142,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
         a2 = __dadd_rn(a2, __dmul_rn(c[2], c[2]));
         a3 = __dadd_rn(a3, __dmul_rn(c[3], c[3]));
       });
-  double* mine = cs + ph * (4 * kTileQuads) + 4 * jj;
+  double* mine = cs + ph * (4 * kCandQuads) + 4 * jj;
   __syncthreads();  // cs aliases the ring: every thread is done with its last stage
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
@@ -1152,7 +1156,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   if (t < ncol) {  // one column per thread: the row phases in order
     s = cs[t];
 #pragma unroll
-    for (int q = 1; q < RP; ++q) s += cs[q * 4 * kTileQuads + t];
+    for (int q = 1; q < RP; ++q) s += cs[q * 4 * kCandQuads + t];
   }
   if (percol) {
     if (t < ncol) out[col0 + t] = s;

@@ -282,6 +282,15 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         const int tr = tile_rows_env("HSX_CAND_TILE_ROWS", 128);
         const int nchunks = (ly.L / 4 + cq - 1) / cq;
         ly.cq = cq;
+        // lanes per row: the tile's quads rounded up to a power of two (HSX_K1_NARROW=0:
+        // always hsx_cand_quads); a narrow layer's spare lanes take more row phases
+        ly.cw = hsx_cand_quads;
+        if (env_flag("HSX_K1_NARROW", 1)) {
+          const int q = std::min(cq, ly.L / 4);
+          ly.cw = 1;
+          while (ly.cw < q) ly.cw <<= 1;
+          ly.cw = std::min(ly.cw, hsx_cand_quads);
+        }
         ly.nparts = (ly.rows + tr - 1) / tr;
         for (int pt = 0; pt < ly.nparts; ++pt)
           for (int cc = 0; cc < nchunks; ++cc) {

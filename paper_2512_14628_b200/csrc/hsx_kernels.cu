@@ -968,10 +968,22 @@ __device__ __forceinline__ void k1_issue(float4* ring, int d, const K1Src& s, lo
     else
       cp_quad_h(ring_slot<NB>(ring, d, slot), src, e, n, pol);
   };
+  // the peers' sends (one or more over NVLink) carry no L2 policy (with the evict-first
+  // hint, HSX_PEER_HINT build, K1 read them at the same 470 GB/s, r2za)
+  auto cpp = [&](int slot, const float* src) {
+#ifdef HSX_PEER_HINT
+    cp(slot, src);
+#else
+    if (FULL)
+      cp16(ring_slot<NB>(ring, d, slot), src + e);
+    else
+      cp_quad(ring_slot<NB>(ring, d, slot), src, e, n);
+#endif
+  };
   if (peer_mode(MODE)) {
 #pragma unroll
     for (int j = 0; j < peer_slots(MODE); ++j)
-      if (j < s.np) cp(j, s.peer[j]);
+      if (j < s.np) cpp(j, s.peer[j]);
   } else {
     cp(0, s.a);
     if (MODE == kModeThetaU) cp(1, s.b);
@@ -1097,21 +1109,18 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
 // in a fixed order, then the kh*kw columns of each channel, and the tile writes
 // one fp64 partial per group: partials[part][G].
 constexpr int kTileQuads = 64;
-#ifndef HSX_CAND_QUADS
-#define HSX_CAND_QUADS 64
-#endif
-constexpr int kCandQuads = HSX_CAND_QUADS;  // K1's column quads per tile (its own tiles)
 
 template <int MODE>
 __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, float4* ring,
                                 double* cs) {
-  constexpr int RP = kThreads / kCandQuads;
+  const int W = ly.cw;          // lanes per row (power of two)
+  const int RP = kThreads / W;  // row phases
   const int pass = p.pass;
   const int L = ly.L;
   const int Q = L >> 2;
   const int cq = ly.cq;
-  const int jj = threadIdx.x & (kCandQuads - 1);
-  const int ph = threadIdx.x / kCandQuads;
+  const int jj = threadIdx.x & (W - 1);
+  const int ph = threadIdx.x / W;
   const int j = it.chunk * cq + jj;
   const long long r0 = it.begin + ph, r1 = it.end;
   const int count = (jj < cq && j < Q && r0 < r1) ? (int)((r1 - r0 + RP - 1) / RP) : 0;
@@ -1142,7 +1151,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
         a2 = __dadd_rn(a2, __dmul_rn(c[2], c[2]));
         a3 = __dadd_rn(a3, __dmul_rn(c[3], c[3]));
       });
-  double* mine = cs + ph * (4 * kCandQuads) + 4 * jj;
+  double* mine = cs + ph * (4 * W) + 4 * jj;
   __syncthreads();  // cs aliases the ring: every thread is done with its last stage
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
@@ -1155,8 +1164,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   double s = 0.0;
   if (t < ncol) {  // one column per thread: the row phases in order
     s = cs[t];
-#pragma unroll
-    for (int q = 1; q < RP; ++q) s += cs[q * 4 * kCandQuads + t];
+    for (int q = 1; q < RP; ++q) s += cs[q * 4 * W + t];
   }
   if (percol) {
     if (t < ncol) out[col0 + t] = s;
@@ -1362,11 +1370,23 @@ static void launch_candidate_mode(const CandArgs& a, int n_items, int frozen, si
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st) {
   if (n_items <= 0) return;
-  static const bool peers2 = [] {  // measured no faster than the 6-slot ring (r2i): opt-in
+  // two ranks: their sum is theta + u's fp64 fold with the two sends as the operands
+  // (rank order), so the theta + u kernel runs it — a 4-slot ring, three CTAs per SM
+  // and no per-peer loop (B200: 18% faster than the peer kernel on local data);
+  // HSX_K1_PEERS2=2 (opt-in: reading over NVLink it measured 3% slower than the
+  // general peer kernel, r2y), =1: the 2-slot peer kernel, default 0: the general one
+  static const int peers2 = [] {
     const char* v = std::getenv("HSX_K1_PEERS2");
-    return v && v[0] == '1';
+    return v ? std::atoi(v) : 0;  // over NVLink the theta + u kernel measured 3% slower (r2y): opt-in (=2)
   }();
-  if (a.peers.n == 2 && peers2)
+  if (a.peers.n == 2 && peers2 == 2) {
+    CandArgs b = a;
+    b.theta = a.peers.p[0];
+    b.u = a.peers.p[1];
+    b.s = nullptr;
+    b.peers.n = 0;
+    launch_candidate_mode<kModeThetaU>(b, n_items, frozen, smem, st);
+  } else if (a.peers.n == 2 && peers2 == 1)
     launch_candidate_mode<kModePeers2>(a, n_items, frozen,
                                        std::max(smem, (size_t)K1<kModePeers2>::D * K1<kModePeers2>::NB * kThreads * 16),
                                        st);

@@ -62,6 +62,8 @@ struct DevLayer {
   int npitems;                 // K3 items of the layer
   int cq;                      // K1 quad tiles: column quads per tile (whole channels unless percol)
   int percol;                  // K1 writes per-column partials [nparts][L]; the selection folds channels
+  int cw;                      // K1 quad tiles: lanes per row (power of two >= the tile's quads, <= 64);
+                               // the CTA's other lanes take more rows (narrow layers keep every lane busy)
   FastDiv divL, divk;
   double rho1, rho2, gamma;
   double rgamma;               // RN(1 / gamma), for the FMA-corrected division

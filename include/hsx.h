@@ -369,6 +369,17 @@ int hsx_candidate_peers(hsx_plan* plan, const float* const* sends, int32_t n, co
 /* Composite pass >= 1 of the peer candidate (same sources as hsx_candidate_peers). */
 int hsx_candidate_renorm_peers(hsx_plan* plan, int32_t pass, const float* const* sends, int32_t n,
                                const float* z, const float* v, void* stream);
+/* Staged peer operand for two ranks (allocate once): hsx_candidate_peers_staged
+ * copies the peer's send into a plan-owned local buffer on a side stream, item by
+ * item in K1's order, and K1 (the theta + u kernel with own send + that copy)
+ * waits per item for its copy to land, reading the peer directly for an item whose
+ * copy is late. Same values as hsx_candidate_peers with n = 2. */
+int hsx_plan_set_peer_staging(hsx_plan* plan, int32_t on);
+/* sends[0..1] in rank order, me = this rank's index among them; side_stream must be
+ * forked from `stream` after the sends are valid (the caller joins it back before
+ * the next staged call). Dynamic (non-frozen) steps only. */
+int hsx_candidate_peers_staged(hsx_plan* plan, const float* const* sends, int32_t n, int32_t me, const float* z,
+                               const float* v, float* z_node, void* stream, void* side_stream);
 /* K4 over mapped pointers: out = OR_j srcs[j] (leaders' local masks, transport.py:455-457). */
 int hsx_mask_or_ptrs(const uint32_t* const* srcs, int32_t n, int64_t words, uint32_t* out,
                      void* stream);

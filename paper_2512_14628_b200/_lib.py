@@ -106,6 +106,8 @@ SIGNATURES = {
     "hsx_count_diff_u8": (C.c_int, [VP, VP, I64, VP, VP]),
     "hsx_selftest_division": (C.c_int, [VP, I64, F64, VP, VP]),
     "hsx_candidate_peers": (C.c_int, [P, VP, I32, VP, VP, VP, VP, VP]),
+    "hsx_plan_set_peer_staging": (C.c_int, [P, I32]),
+    "hsx_candidate_peers_staged": (C.c_int, [P, VP, I32, I32, VP, VP, VP, VP, VP]),
     "hsx_mask_or_ptrs": (C.c_int, [VP, I32, I64, VP, VP]),
     "hsx_candidate_renorm_peers": (C.c_int, [P, I32, VP, I32, VP, VP, VP]),
     "hsx_average_peers": (C.c_int, [P, VP, I32, F64, VP, VP]),

@@ -130,6 +130,8 @@ struct hsx_plan {
   uint8_t *d_rk_prev = nullptr, *d_ck_prev = nullptr, *d_ch_prev = nullptr;
   int *d_irr = nullptr, *d_irr_any = nullptr;
   unsigned int* d_k1done = nullptr;  // chained K2: K1 tiles finished per prunable layer (0 between steps)
+  float* d_stage = nullptr;          // staged peer operand (two ranks): local copy of the peer's send
+  unsigned int *d_sready = nullptr, *d_sepoch = nullptr, *d_scounter = nullptr;
   int k2_armed = 0;                  // the last launch was such a K1: hsx_select(0) chains behind it
   int k2_pending = 0;                // a counting K1 ran whose counts no chained K2 consumed yet
   int k3_armed = 0;                  // the last launch was a chained single-pass K2: K3 chains behind it
@@ -153,7 +155,7 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
-    void* ptrs[] = {d_ready3, d_cnt67, d_up, d_k1done, d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
+    void* ptrs[] = {d_stage, d_sready, d_sepoch, d_scounter, d_ready3, d_cnt67, d_up, d_k1done, d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
                     d_ch_prev};
     for (void* p : ptrs)
@@ -709,6 +711,49 @@ int hsx_candidate_peers(hsx_plan* p, const float* const* sends, int32_t n, const
     hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
   }
   HSX_LAUNCHED("candidate_peers");
+  return HSX_OK;
+}
+
+int hsx_plan_set_peer_staging(hsx_plan* p, int32_t on) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  if (!on || p->d_stage) return HSX_OK;
+  HSX_CUDA(cudaMalloc(&p->d_stage, (size_t)std::max<long long>(p->arena, 1) * sizeof(float)));
+  const size_t ni = std::max<size_t>(p->cand_dyn.size(), 1);
+  HSX_CUDA(cudaMalloc(&p->d_sready, ni * sizeof(unsigned int)));
+  HSX_CUDA(cudaMemset(p->d_sready, 0, ni * sizeof(unsigned int)));
+  HSX_CUDA(cudaMalloc(&p->d_sepoch, 2 * sizeof(unsigned int)));
+  HSX_CUDA(cudaMemset(p->d_sepoch, 0, 2 * sizeof(unsigned int)));
+  HSX_CUDA(cudaMalloc(&p->d_scounter, 2 * sizeof(unsigned int)));
+  HSX_CUDA(cudaMemset(p->d_scounter, 0, 2 * sizeof(unsigned int)));
+  return HSX_OK;
+}
+
+int hsx_candidate_peers_staged(hsx_plan* p, const float* const* sends, int32_t n, int32_t me, const float* z,
+                               const float* v, float* z_node, void* stream, void* side_stream) {
+  if (!p || !z_node || !sends || !z || !v || !side_stream) return fail(HSX_EINVAL, "null argument");
+  if (n != 2 || me < 0 || me > 1 || !sends[0] || !sends[1]) return fail(HSX_EINVAL, "staging takes two ranks");
+  if (p->identity) return fail(HSX_EINVAL, "peer candidate needs a penalty plan");
+  if (!p->d_stage) return fail(HSX_EPROTOCOL, "hsx_plan_set_peer_staging(plan, 1) first");
+  static const int grid = std::max(8, env_flag("HSX_STAGE_CTAS", 64));
+  // the staging copy of the peer's send on the side stream (the caller forked it from
+  // `stream` and joins it back later); K1 reads own send + stage: two fp64 operands,
+  // the theta + u kernel (their sum is commutative: the rank order is immaterial)
+  hsx::launch_stage(sends[1 - me], p->d_stage, p->d_layers, p->d_cand, (int)p->cand_dyn.size(), p->d_sready,
+                    p->d_sepoch, p->d_scounter, grid, S(side_stream));
+  HSX_LAUNCHED("stage_peer");
+  hsx::CandArgs a = cand_args(p, nullptr, sends[me], p->d_stage, z, v);
+  a.u_alt = sends[1 - me];
+  a.sready = p->d_sready;
+  a.sepoch = p->d_sepoch;
+  a.zn = z_node;
+  a.pass = 0;
+  a.partials = p->d_partials[0];
+  a.norms = p->d_norms[0];
+  a.items = p->d_cand;
+  arm_chain(p, a, S(stream));
+  a.reserve += grid;   // slots for the staging CTAs
+  hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
+  HSX_LAUNCHED("candidate_staged");
   return HSX_OK;
 }
 

@@ -47,6 +47,11 @@ static void allow_smem(K kernel, size_t bytes) {
 // unconditionally (completion of a grid then implies completion of everything
 // before it in the stream), then pdl_trigger() so its successor may be scheduled
 // once all of its CTAs are running.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 #define PDL_ENTRY() \
@@ -938,6 +943,10 @@ struct K1Src {
   int np;
 };
 
+// staged peer operand: 1 while this CTA's current item reads the peer's send directly
+// (its staging copy had not landed), 0 otherwise (also for every unstaged launch)
+__shared__ int s_k1_alt;
+
 template <int MODE>
 __device__ __forceinline__ K1Src k1_src(const CandArgs& p, long long base) {
   K1Src s;
@@ -949,7 +958,7 @@ __device__ __forceinline__ K1Src k1_src(const CandArgs& p, long long base) {
     for (int j = 0; j < kMaxPeers; ++j) s.peer[j] = j < s.np ? p.peers.p[j] + base : nullptr;
   } else {
     s.a = (MODE == kModeThetaU ? p.theta : p.s) + base;
-    s.b = MODE == kModeThetaU ? p.u + base : nullptr;
+    s.b = MODE == kModeThetaU ? (s_k1_alt ? p.u_alt : p.u) + base : nullptr;
   }
   s.z = MODE != kModeIdent ? p.z + base : nullptr;
   s.v = MODE != kModeIdent ? p.v + base : nullptr;
@@ -1039,7 +1048,7 @@ __device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, con
     s = (double)p.peers.p[0][gi];
     for (int j = 1; j < p.peers.n; ++j) s = __dadd_rn(s, (double)p.peers.p[j][gi]);
   } else if (MODE == kModeThetaU) {
-    s = __dadd_rn((double)p.theta[gi], (double)p.u[gi]);
+    s = __dadd_rn((double)p.theta[gi], (double)(s_k1_alt ? p.u_alt : p.u)[gi]);
   } else {
     s = (double)p.s[gi];
   }
@@ -1318,11 +1327,38 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
   extern __shared__ float4 ring[];
   __shared__ int next;
   int idx = blockIdx.x;
+  unsigned epoch = 0;
+  if (threadIdx.x == 0) {
+    s_k1_alt = 0;
+    if (p.sready) epoch = *reinterpret_cast<volatile unsigned*>(p.sepoch);  // bumped only by the last CTA
+  }
+  __syncthreads();
   while (idx < p.n_items) {
 #ifdef HSX_TRACE
     TRACE_AT(idx, 0, gtime());
     TRACE_AT(idx, 3, smid() | ((unsigned long long)p.items[idx].layer << 16));
 #endif
+    if (p.sready) {
+      // staged peer operand: wait for this item's staging copy (the staging kernel runs
+      // ahead on a side stream); if it has not landed within the timeout, read the
+      // peer's send directly for this item (never a deadlock, same values either way)
+      if (threadIdx.x == 0) {
+        const unsigned long long t0 = global_ns();
+        unsigned v;
+        int alt = 0;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sready + idx) : "memory");
+          if (v == epoch + 1u) break;
+          if (global_ns() - t0 > 200000ull) {
+            alt = 1;
+            break;
+          }
+          __nanosleep(64);
+        }
+        s_k1_alt = alt;
+      }
+      __syncthreads();
+    }
     cand_item<MODE>(p, frozen, p.items[idx], ring);
 #ifdef HSX_TRACE
     TRACE_AT(idx, 2, gtime());
@@ -1340,6 +1376,93 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
       p.sched[1] = 0;
     }
   }
+  if (p.sready && threadIdx.x == 0) {  // the last CTA out moves the staging epoch on
+    __threadfence();
+    if (atomicAdd(p.sepoch + 1, 1u) == gridDim.x - 1) {
+      p.sepoch[1] = 0;
+      p.sepoch[0] = epoch + 1u;
+    }
+  }
+}
+
+// Staging copy of the peer's send for a staged K1: persistent CTAs take K1's dynamic
+// items in order (the order K1 takes them), copy each item's region of the peer's
+// buffer into the local stage buffer with float4 loads, and publish sready[item] =
+// epoch + 1 (release). Quad tiles: rows [begin, end) x quads [chunk cq, +cq) of the
+// layer; element items: [begin, end) of the layer.
+__global__ void __launch_bounds__(kThreads) k_stage(const float* __restrict__ peer, float* __restrict__ stage,
+                                                    const DevLayer* __restrict__ layers,
+                                                    const Item* __restrict__ items, int n_items,
+                                                    unsigned int* sready, const unsigned int* sepoch,
+                                                    unsigned int* counter) {
+  __shared__ int next;
+  __shared__ unsigned epoch;
+  if (threadIdx.x == 0) epoch = *reinterpret_cast<const volatile unsigned*>(sepoch);
+  int idx = blockIdx.x;
+  __syncthreads();
+  while (idx < n_items) {
+    const Item it = items[idx];
+    const DevLayer& ly = layers[it.layer];
+    const long long off = ly.off;
+    if (it.tile == 1) {
+      // eight float4 loads in flight per thread (NVLink latency): ~32 KB per CTA
+      const int Q = ly.L >> 2;
+      const int q0 = it.chunk * ly.cq;
+      const int nq = min(ly.cq, Q - q0);
+      const long long nrow = it.end - it.begin;
+      const long long total = nrow * nq;
+      constexpr int U = 8;
+      for (long long i0 = threadIdx.x; i0 < total; i0 += (long long)U * kThreads) {
+        float4 x[U];
+        long long ea[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const long long i = i0 + (long long)u * kThreads;
+          ea[u] = -1;
+          if (i < total) {
+            const long long r = it.begin + i / nq;
+            ea[u] = off + r * ly.L + 4LL * (q0 + (int)(i % nq));
+            x[u] = __ldcg(reinterpret_cast<const float4*>(peer + ea[u]));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ea[u] >= 0) *reinterpret_cast<float4*>(stage + ea[u]) = x[u];
+      }
+    } else {
+      const long long b = off + it.begin, e = off + it.end;
+      const long long b4 = (b + 3) & ~3LL, e4 = e & ~3LL;
+      if (b4 < e4) {
+        for (long long i = b4 + 4LL * threadIdx.x; i < e4; i += 4LL * kThreads)
+          *reinterpret_cast<float4*>(stage + i) = __ldcg(reinterpret_cast<const float4*>(peer + i));
+        for (long long i = b + threadIdx.x; i < b4; i += kThreads) stage[i] = peer[i];
+        for (long long i = e4 + threadIdx.x; i < e; i += kThreads) stage[i] = peer[i];
+      } else {
+        for (long long i = b + threadIdx.x; i < e; i += kThreads) stage[i] = peer[i];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sready + idx), "r"(epoch + 1u) : "memory");
+      next = (int)gridDim.x + (int)atomicAdd(counter, 1u);
+    }
+    __syncthreads();
+    idx = next;
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(counter + 1, 1u) == gridDim.x - 1) {
+      counter[0] = 0;
+      counter[1] = 0;
+    }
+  }
+}
+
+void launch_stage(const float* peer, float* stage, const DevLayer* layers, const Item* items, int n_items,
+                  unsigned int* sready, const unsigned int* sepoch, unsigned int* counter, int grid, cudaStream_t st) {
+  if (n_items <= 0) return;
+  k_stage<<<std::min(grid, n_items), kThreads, 0, st>>>(peer, stage, layers, items, n_items, sready, sepoch, counter);
 }
 
 template <int MODE>
@@ -2736,12 +2859,6 @@ void launch_slices(const PeerPtrs& src, const long long* total_p, long long tota
 // ---------------------------------------------------------------------------
 
 __device__ unsigned int g_barrier_timeouts;
-
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 __global__ void k_barrier(BarrierArgs b) {
   const int i = threadIdx.x;

@@ -133,6 +133,12 @@ struct CandArgs {
   const uint8_t* flags[kMaxPasses];    // keep flags of earlier passes (renorm)
   PeerPtrs peers;                      // n > 0: S = sum of the peers' theta + u (rank order)
   unsigned int* k1done;                // chained K2: +1 per finished tile of a prunable layer (or nullptr)
+  // staged peer operand (two ranks): u is a local copy of the peer's send that a
+  // staging kernel fills item by item on a side stream; sready[item] == epoch + 1
+  // once the item's region landed, else K1 reads u_alt (the peer's send) directly
+  const float* u_alt;
+  const unsigned int* sready;          // nullptr = not staged
+  unsigned int* sepoch;                // [0] epoch (K1's last CTA bumps it), [1] K1 exit counter
   int reserve;                         // persistent grid: CTA slots left free for the chained K2
   // fused selection (K2 in the tail of each layer's last K1 tile)
   double* norms;                       // this pass
@@ -193,6 +199,10 @@ struct ElemArgs {
 constexpr int kResidSlots = 9;         // consensus.py:235 (_INTER_SLOTS)
 
 void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, cudaStream_t st);
+// the staging copy of the peer's send for a staged K1 (side stream): K1's dynamic
+// items in order, each region copied from peer to stage, then sready[item] = epoch + 1
+void launch_stage(const float* peer, float* stage, const DevLayer* layers, const Item* items, int n_items,
+                  unsigned int* sready, const unsigned int* sepoch, unsigned int* counter, int grid, cudaStream_t st);
 // K2; k1done != nullptr: chained behind the K1 launch that counted its tiles into
 // k1done (a layer's selection starts once k1done[pidx] reaches its tile count and
 // subtracts it again; the grid-completion wait moves to the end)

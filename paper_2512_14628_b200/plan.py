@@ -224,6 +224,37 @@ class Plan:
                       ptr(frozen_mask), current_stream())
         del keep
 
+    def set_peer_staging(self, on: bool):
+        """Allocate the staged-peer-operand buffers (hsx_plan_set_peer_staging)."""
+        _lib.call("hsx_plan_set_peer_staging", self._h, 1 if on else 0)
+
+    def candidate_peers_staged(self, sends: list[int], me: int, z, v, z_node):
+        """K1 for two ranks with the peer's send staged into local memory by a copy
+        kernel on a side stream (forked here, joined by :meth:`join_stage`)."""
+        cur = torch.cuda.current_stream()
+        if getattr(self, "_stage_stream", None) is None:
+            self._stage_stream = torch.cuda.Stream(cur.device)
+            self._stage_done = None
+        side = self._stage_stream
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        side.wait_event(fork)
+        arr, keep = _lib.ptr_array(sends)
+        with timed("K1_candidate"):
+            _lib.call("hsx_candidate_peers_staged", self._h, arr, len(sends), int(me), ptr(z), ptr(v), ptr(z_node),
+                      current_stream(), side.cuda_stream)
+        del keep
+        done = torch.cuda.Event()
+        done.record(side)
+        self._stage_done = done
+
+    def join_stage(self):
+        """The current stream waits for the last staging copy (end of a step; also
+        closes the side branch under CUDA-graph capture)."""
+        if getattr(self, "_stage_done", None) is not None:
+            torch.cuda.current_stream().wait_event(self._stage_done)
+            self._stage_done = None
+
     def average_peers(self, srcs: list[int], divisor, out, tag="C_avg"):
         """out[:payload] = rank-order average of the buffers at srcs (payload size on device)."""
         arr, keep = _lib.ptr_array(srcs)

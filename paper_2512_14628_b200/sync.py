@@ -66,6 +66,7 @@ class HSADMMSync:
         self.cluster = cluster
         self.topology = topo
         self.M, self.P = topo.num_nodes, topo.accels_per_node
+        self._staged = False
         self.node = topo.node_of(rank)
         self.leader_rank = topo.leader_of(self.node)
         self.is_leader = rank == self.leader_rank
@@ -139,6 +140,13 @@ class HSADMMSync:
             self._init_peer_buffers()
             if self.P == 2 and "HSX_K1_ORDER" not in os.environ:
                 self.plan.set_order(False)   # K1 reads the intra sum over NVLink: layer order (r2n)
+            # two ranks, opt-in (HSX_PEER_STAGING=1): the peer's send staged into local
+            # memory by a copy kernel on a side stream running ahead of K1; measured
+            # much slower (RN18 1x2 0.21 -> 0.54 ms, r2zc: the copy kernel does not keep
+            # pace next to K1), so by default K1 reads it over NVLink itself
+            self._staged = self.P == 2 and os.environ.get("HSX_PEER_STAGING") == "1"
+            if self._staged:
+                self.plan.set_peer_staging(True)
         # deferred host bookkeeping (step_host): a step returns once its launches are
         # queued; the keep-set counts are read back when the next step starts
         self.defer_host = False
@@ -347,7 +355,10 @@ class HSADMMSync:
             self._pack_send(send.tensor)
             yield Barrier(self.intra, "theta_u", k)
             peers = send.peer_ptrs()
-            pl.candidate_peers(peers, self.z, self.v, self.z_node, frozen_mask=fmask)
+            if self._staged and fmask is None:
+                pl.candidate_peers_staged(peers, self.intra.members.index(self.rank), self.z, self.v, self.z_node)
+            else:
+                pl.candidate_peers(peers, self.z, self.v, self.z_node, frozen_mask=fmask)
         else:
             pl.candidate(None, self.theta, self.u, self.z, self.v, self.z_node, frozen_mask=fmask)
         # one node: every rank's local mask is the node's (identical z_node), so the
@@ -363,6 +374,7 @@ class HSADMMSync:
             self._dual(None)
             yield from self._residual_phase(k, sync=False)
             self._log_reference(k, False, self.frozen)
+            self.plan.join_stage()
             return None
         ev = None
         if fused_keep:
@@ -553,6 +565,7 @@ class HSADMMSync:
         """Phase 5; masks <- union; host bookkeeping now, or at the next step (defer_host)."""
         yield from self._residual_phase(k, sync=True)
         self.plan.join_fetch()
+        self.plan.join_stage()
         if dynamic:
             self.masks, self.union = self.union, self.masks
         if ev is not None and self.defer_host:

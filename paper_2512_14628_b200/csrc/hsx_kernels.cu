@@ -1634,8 +1634,6 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     const int mstep = kRowPhases * (ly.L >> 5);
     float* const q0 = zn + ly.off + e0;
     uint32_t* const m0 = mask + ly.mword + (e0 >> 5);
-    auto issue = [&](int d, int i) { cp16(ring_slot<1>(ring, d, 0), src + e0 + i * estep); };
-    ring_prologue(count, issue);  // the first loads fly while the keep masks are built
     // kept = AND over the passes' group flags: rows (FILTER) in shared memory,
     // this thread's four columns (CHANNEL / SHAPE) in a nibble
     for (int r = threadIdx.x; r < nrow; r += kThreads) {
@@ -1660,6 +1658,15 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
       }
     }
     __syncthreads();
+    // a quad with nothing kept is not read (the copy zero-fills it without touching
+    // memory): only the kept quads' z_node is needed for the nonzero test
+    auto issue = [&](int d, int i) {
+      const bool any = ckb && s_rk[tc.ph + kRowPhases * i];
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(ring_slot<1>(ring, d, 0))),
+                   "l"(src + e0 + i * estep), "r"(any ? 16 : 0)
+                   : "memory");
+    };
+    ring_prologue(count, issue);
     unsigned bad = 0;  // CHECK: kept but zero
     auto consume = [&](int d, int i) {  // only valid quads get here
       float4 v = *ring_slot<1>(ring, d, 0);
@@ -1727,7 +1734,7 @@ __device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);
 // published by K2 with release semantics), projects, and waits for the grid before
 // it at the end; the layer's last item re-zeroes its counter and flag.
 template <bool CHECK>
-__global__ void __launch_bounds__(kThreads, 6) k_project(KeepArgs a, float* __restrict__ zn,
+__global__ void __launch_bounds__(kThreads, 5) k_project(KeepArgs a, float* __restrict__ zn,
                                                          uint32_t* __restrict__ mask, unsigned int* ready,
                                                          unsigned int* pdone, ChainK67 c67) {
   extern __shared__ float4 ring[];

@@ -48,6 +48,9 @@ from . import _lib
 
 _F1 = os.environ.get("HSX_F1", "0") == "1"               # two leaders: average fused into K7
 _REMOTE_K7 = os.environ.get("HSX_REMOTE_K7", "1") != "0"  # followers decompact from the leader's payload
+# leaders, opt-in: the intra dual on a side stream beside the exchange; measured no
+# faster (RN50 2x2: K6 95 -> 56 us, but K8 87 -> 121 us and K6f 87 us beside it, r2ze)
+_SPLIT_K6 = os.environ.get("HSX_SPLIT_K6") == "1"
 
 
 class HSADMMSync:
@@ -409,7 +412,15 @@ class HSADMMSync:
             if self.M > 1:
                 flat = self.p_flat[self._nsync & 1]
                 self._nsync += 1
-                self._dual(flat.tensor)
+                if not self.residuals and _SPLIT_K6:
+                    # the leader's critical path needs only the compaction before the
+                    # exchange: the intra dual u += theta - z_node (12N bytes, read by
+                    # nothing until the next step) on a side stream under the leader
+                    # average (HSX_SPLIT_K6=1)
+                    pl.compact_dual(None, None, self.z_node, self.v, flat.tensor)
+                    self._side_dual()
+                else:
+                    self._dual(flat.tensor)
                 yield Barrier(self.inter, "z_sync", k)
                 # leader average over NVLink into the node's payload buffer
                 dst = zhat if zhat is not None else self.flat
@@ -485,6 +496,26 @@ class HSADMMSync:
             pl.compact_dual(self.theta, self.u, self.z_node, self.v, flat)
         else:
             pl.dual_intra(self.theta, self.u, self.z_node)
+
+    def _side_dual(self):
+        """K6f on a side stream forked from the current one (joined at the end of the
+        step by :meth:`_join_side`)."""
+        cur = torch.cuda.current_stream(self.device)
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device)
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        self._side.wait_event(fork)
+        with torch.cuda.stream(self._side):
+            self.plan.dual_intra(self.theta, self.u, self.z_node)
+            done = torch.cuda.Event()
+            done.record(self._side)
+        self._side_done = done
+
+    def _join_side(self):
+        if getattr(self, "_side_done", None) is not None:
+            torch.cuda.current_stream(self.device).wait_event(self._side_done)
+            self._side_done = None
 
     def _local_sync(self):
         """K6 + K7 of a one-node cluster in one pass (HSX_LOCAL_SYNC=0: the two kernels)."""
@@ -566,6 +597,7 @@ class HSADMMSync:
         yield from self._residual_phase(k, sync=True)
         self.plan.join_fetch()
         self.plan.join_stage()
+        self._join_side()
         if dynamic:
             self.masks, self.union = self.union, self.masks
         if ev is not None and self.defer_host:
@@ -646,8 +678,13 @@ class HSADMMSync:
                 ev = pl.keep_sets_fetch_async()
             return (yield from self._end_step(k, dynamic, ev, log_zsync=True))
         # compaction fused with the intra dual update (K6 reads sizes on device, so
-        # it runs while the host waits for the D2H and sizes the collectives)
-        self._dual(self.flat if self.is_leader else None)
+        # it runs while the host waits for the D2H and sizes the collectives); a leader
+        # without phase 5 runs the intra dual on a side stream beside the collectives
+        if self.is_leader and not self.residuals and _SPLIT_K6:
+            pl.compact_dual(None, None, self.z_node, self.v, self.flat)
+            self._side_dual()
+        else:
+            self._dual(self.flat if self.is_leader else None)
         collectives = self.M > 1 or self.P > 1
         if ev is not None and collectives:      # the leader all-reduce / broadcast need the sizes
             ev.synchronize()

@@ -365,7 +365,9 @@ int build(hsx_plan* p, const hsx_layer_desc* in, int n) {
         Item it{l, ly.pidx, nwi, 0, b, std::min(ly.n, b + kWordItem * 32)};
         p->word_items.push_back(it);
         long long r_lo = b / ly.L, r_hi = (it.end - 1) / ly.L;
-        mark_smem = std::max<size_t>(mark_smem, (size_t)ly.cin + (size_t)(r_hi - r_lo + 1));
+        // flags (c_in + rows of the item), 16-B aligned, then the column words of a row
+        mark_smem = std::max<size_t>(mark_smem, (((size_t)ly.cin + (size_t)(r_hi - r_lo + 1) + 15) & ~(size_t)15) +
+                                                    (ly.L % 32 == 0 ? (size_t)(ly.L / 32) * 4 : 0));
       }
     } else {
       for (long long b = 0; b < ly.n; b += kItemElems) {

@@ -1948,7 +1948,16 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
   const int nr = (int)(r_hi - r_lo + 1);
   uint8_t* s_in = sflag;
   uint8_t* s_out = sflag + ly.cin;
+  // rows of whole mask words (c_in kh kw % 32 == 0, every ResNet conv but the stem):
+  // a row's "any" is its words' OR and the columns' "any" is the OR of the words at
+  // each word position, so the marking is per word (a row flag + one shared-memory
+  // atomicOr), and only the OR-ed column words are decoded into channels bit by bit
+  const bool wordwise = (ly.L & 31) == 0;
+  const int W = ly.L >> 5;
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(sflag + ((ly.cin + nr + 15) & ~15));
   for (int i = threadIdx.x; i < ly.cin + nr; i += kThreads) sflag[i] = 0;
+  if (wordwise)
+    for (int i = threadIdx.x; i < W; i += kThreads) s_col[i] = 0;
   __syncthreads();
   // a) marks and popcounts
   unsigned long long pop = 0, drift = 0;
@@ -1959,6 +1968,14 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
     uint32_t x = a.uni[ly.mword + w] & valid;
     pop += __popc(x);
     if (a.prev) drift += __popc((x ^ a.prev[ly.mword + w]) & valid);
+    if (wordwise) {
+      if (x) {
+        const unsigned o = fdiv((unsigned)e0, ly.divL);
+        s_out[o - r_lo] = 1;
+        atomicOr(s_col + ((unsigned)w - o * (unsigned)W), x);
+      }
+      continue;
+    }
     while (x) {
       int b = __ffs(x) - 1;
       unsigned e = (unsigned)(e0 + b);
@@ -1973,6 +1990,20 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
     }
   }
   __syncthreads();
+  if (wordwise) {  // channels of the OR-ed column words
+    for (int cw = threadIdx.x; cw < W; cw += kThreads) {
+      uint32_t x = s_col[cw];
+      while (x) {
+        const int b = __ffs(x) - 1;
+        const unsigned col = 32u * cw + b;
+        const unsigned c = fdiv(col, ly.divk);
+        s_in[c] = 1;
+        const int skip = b + (int)((unsigned)ly.k - (col - c * (unsigned)ly.k));  // rest of the channel
+        x = skip >= 32 ? 0u : (x & ~((1u << skip) - 1u));
+      }
+    }
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < ly.cin; i += kThreads)
     if (s_in[i]) a.iflag[ly.ikeep + i] = 1;
   for (int i = threadIdx.x; i < nr; i += kThreads)

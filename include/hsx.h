@@ -408,6 +408,12 @@ int hsx_slices_peers(const hsx_plan* plan, const float* const* srcs, int32_t n, 
  * it so the host can raise ProtocolError. */
 int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
                       void* stream);
+/* One-sided variant: mode 0 = hsx_group_barrier; mode 1 = this member (the root)
+ * only publishes the epoch and does not wait; mode 2 = this member waits for member
+ * `root`'s epoch only (a producer -> readers hand-off; all members still count the
+ * epoch). */
+int hsx_group_barrier_mode(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
+                           int32_t mode, int32_t root, void* stream);
 /* Number of group barriers on the current device that timed out (synchronous
  * device read); reset != 0 zeroes the counter. */
 int hsx_barrier_timeouts(uint32_t* count, int32_t reset);

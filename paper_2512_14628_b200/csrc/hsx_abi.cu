@@ -1455,11 +1455,19 @@ int hsx_slices_peers(const hsx_plan* p, const float* const* srcs, int32_t n, int
 
 int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
                       void* stream) {
+  return hsx_group_barrier_mode(flags, slots, n, me, epoch, 0, 0, stream);
+}
+
+int hsx_group_barrier_mode(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
+                           int32_t mode, int32_t root, void* stream) {
   if (!flags || !slots || n < 1 || n > 32 || me < 0 || me >= n) return fail(HSX_EINVAL, "bad barrier arguments");
+  if (mode < 0 || mode > 2 || root < 0 || root >= n) return fail(HSX_EINVAL, "bad barrier mode / root");
   hsx::BarrierArgs b;
   b.n = n;
   b.me = me;
   b.epoch = epoch;
+  b.mode = mode;
+  b.root = root;
   for (int i = 0; i < n; ++i) {
     if (!flags[i]) return fail(HSX_EINVAL, "null flag pointer %d", i);
     b.flags[i] = flags[i];

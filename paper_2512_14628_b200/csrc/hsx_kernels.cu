@@ -2900,13 +2900,13 @@ __device__ unsigned int g_barrier_timeouts;
 
 __global__ void k_barrier(BarrierArgs b) {
   const int i = threadIdx.x;
-  if (i < b.n && i != b.me) {
+  if (b.mode != 2 && i < b.n && i != b.me) {
     __threadfence_system();
     int* dst = b.flags[i] + b.slots[b.me];
     asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(dst), "r"(b.epoch) : "memory");
   }
   __syncwarp();
-  if (i < b.n && i != b.me) {
+  if (b.mode != 1 && i < b.n && i != b.me && (b.mode == 0 || i == b.root)) {
     const int* src = b.flags[b.me] + b.slots[i];
     const unsigned long long t0 = global_ns();
     int v;

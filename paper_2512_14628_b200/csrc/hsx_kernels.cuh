@@ -293,6 +293,8 @@ struct BarrierArgs {
   int* flags[32];  // members' flag arrays (peer-mapped), member order
   int slots[32];   // members' slot indices (their world ranks)
   int n, me, epoch;
+  int mode;    // 0: everyone publishes and waits; 1: publish only (root); 2: wait for member `root` only
+  int root;
   unsigned long long timeout_ns;  // 0: wait forever (set by launch_barrier)
 };
 void launch_barrier(const BarrierArgs& b, cudaStream_t st);

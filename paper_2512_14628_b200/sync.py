@@ -51,6 +51,12 @@ _REMOTE_K7 = os.environ.get("HSX_REMOTE_K7", "1") != "0"  # followers decompact 
 # leaders, opt-in: the intra dual on a side stream beside the exchange; measured no
 # faster (RN50 2x2: K6 95 -> 56 us, but K8 87 -> 121 us and K6f 87 us beside it, r2ze)
 _SPLIT_K6 = os.environ.get("HSX_SPLIT_K6") == "1"
+# leader -> follower hand-offs (union mask, node payload) as one-sided barriers: the
+# leader publishes and runs on; the next step's two-sided theta_u barrier orders the
+# followers' reads before the leader's next write. Parity green, measured no faster
+# (the leader's path is the long one; 2x2 RN18/RN50 steady step unchanged), so
+# opt-in (HSX_ONESIDED=1)
+_ONESIDED = os.environ.get("HSX_ONESIDED") == "1"
 
 
 class HSADMMSync:
@@ -392,7 +398,7 @@ class HSADMMSync:
                     yield Barrier(self.inter, "mask_sync", k)
                 mask_or_ptrs(srcs, words, target)
             if self.P > 1:
-                yield Barrier(self.intra, "m_bcast", k)
+                yield Barrier(self.intra, "m_bcast", k, root=self.leader_rank if _ONESIDED else None)
                 mask_or_ptrs([self.p_umask.peer_ptrs()[0]], words, self.union)  # copy of the leader's union
             pl.keep_sets(self.union, self.masks)
             ev = pl.keep_sets_fetch_async()
@@ -443,7 +449,7 @@ class HSADMMSync:
         else:
             self._dual(None)
         if self.P > 1:
-            yield Barrier(self.intra, "zhat_bcast", k)
+            yield Barrier(self.intra, "zhat_bcast", k, root=self.leader_rank if _ONESIDED else None)
             if not self.is_leader:
                 # the intra broadcast: decompact straight from the leader's payload over
                 # NVLink (HSX_REMOTE_K7=0: copy it first)

@@ -149,11 +149,17 @@ class AllGather:
 class Barrier:
     """Every member reaches this point before any continues (device-side barrier over
     NVLink signal pads under DistCluster; scheduler rendezvous under LocalCluster).
-    Orders the producers of shared (peer-mapped) buffers before their readers."""
+    Orders the producers of shared (peer-mapped) buffers before their readers.
+
+    ``root`` given: a one-sided hand-off — the root only publishes (it does not wait
+    for the others), every other member waits for the root. For a buffer the root
+    produces and the others read, when a later two-sided barrier already orders the
+    root's next write after their reads."""
 
     group: ProcessGroup
     tag: str
     iteration: int
+    root: int | None = None
 
 
 class SharedBuffer:
@@ -604,8 +610,9 @@ class DistCluster(Cluster):
         members = [ptrs[m] for m in group.members]
         return SharedBuffer(t, lambda: members)
 
-    def barrier(self, group: ProcessGroup) -> None:
-        """Device-side barrier of ``group`` over NVLink flags (stream-ordered)."""
+    def barrier(self, group: ProcessGroup, root: int | None = None) -> None:
+        """Device-side barrier of ``group`` over NVLink flags (stream-ordered); with a
+        root, one-sided: the root publishes, the others wait for the root."""
         from . import _lib
         from .plan import current_stream
 
@@ -617,8 +624,9 @@ class DistCluster(Cluster):
         import ctypes as C
 
         slots = (C.c_int32 * len(members))(*members)
-        _lib.call("hsx_group_barrier", fl, C.cast(slots, C.c_void_p), len(members), members.index(self.rank),
-                  epoch, current_stream())
+        mode = 0 if root is None else (1 if self.rank == root else 2)
+        _lib.call("hsx_group_barrier_mode", fl, C.cast(slots, C.c_void_p), len(members), members.index(self.rank),
+                  epoch, mode, members.index(root) if root is not None else 0, current_stream())
         del keep1
 
     def log(self, entry: LedgerEntry) -> None:
@@ -657,7 +665,7 @@ class DistCluster(Cluster):
         g = len(req.group.members)
         if isinstance(req, Barrier):
             if g > 1:
-                self.barrier(req.group)
+                self.barrier(req.group, req.root)
             return None
         if isinstance(req, Broadcast):
             if g > 1:

@@ -1619,21 +1619,20 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     // row-quad tile: 8 lanes (same row, 8 consecutive quads) make one mask word
     const TileCtx tc(it, ly.L);
     const int nrow = (int)(it.end - it.begin);
-    const float* src = zn + ly.off;
-    // all lanes of a warp share a row phase; quads past the row end are a suffix of
-    // the last chunk in whole 8-lane groups (L % 32 == 0): those groups skip the loop
-    // (tc.count = 0) and the mask-word shuffles stay inside each 8-lane group
-    const int count = tc.count;
-    const unsigned gmask = 0xFFu << (lane & 24);
-    const bool word_lane = (lane & 7) == 0 && tc.valid;
+    // all lanes of a warp share a row phase and walk the same rows; quads past the
+    // row end are a suffix of the last chunk in whole 8-lane groups (L % 32 == 0):
+    // they run the loop with nothing kept (no read, no store) so the mask-word
+    // shuffles are full-warp, and a warp with no valid quad skips the loop
+    const bool warp_valid = 4 * (it.chunk * kTileQuads + ((threadIdx.x & ~31) & (kTileQuads - 1))) < ly.L;
+    const int count = (warp_valid && tc.r0 < tc.r1) ? (int)((tc.r1 - tc.r0 + kRowPhases - 1) / kRowPhases) : 0;
+    const bool valid = tc.valid;
+    const bool word_lane = (lane & 7) == 0 && valid;
     // (no L2 policy here: with the mask-word shuffles in the loop ptxas reuses the
     // policy's uniform descriptor register for BRA.DIV -> illegal instruction)
-    // quad i of this thread sits at e0 + i * estep; its mask word at m0 + i * mstep
-    // (L % 32 == 0), its row flag at s_rk[ph + 4 i]
-    const long long e0 = tc.r0 * ly.L + 4 * tc.j, estep = (long long)kRowPhases * ly.L;
+    // quad i of this thread sits at e0 + i * estep, its mask word at m0 + i * mstep
+    // (L % 32 == 0), its row flag at s_rk[ph + 4 i]: walked by running pointers
+    const long long e0 = tc.r0 * ly.L + 4 * (valid ? tc.j : 0), estep = (long long)kRowPhases * ly.L;
     const int mstep = kRowPhases * (ly.L >> 5);
-    float* const q0 = zn + ly.off + e0;
-    uint32_t* const m0 = mask + ly.mword + (e0 >> 5);
     // kept = AND over the passes' group flags: rows (FILTER) in shared memory,
     // this thread's four columns (CHANNEL / SHAPE) in a nibble
     for (int r = threadIdx.x; r < nrow; r += kThreads) {
@@ -1644,7 +1643,7 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     }
     const FastDiv divk = dl.divk;
     unsigned ckb = 0;
-    if (tc.valid) {
+    if (valid) {
       ckb = 0xFu;
       for (int q = 0; q < ly.ncons; ++q) {
         const int grp = dl.group[q];
@@ -1660,32 +1659,44 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     __syncthreads();
     // a quad with nothing kept is not read (the copy zero-fills it without touching
     // memory): only the kept quads' z_node is needed for the nonzero test
-    auto issue = [&](int d, int i) {
-      const bool any = ckb && s_rk[tc.ph + kRowPhases * i];
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(ring_slot<1>(ring, d, 0))),
-                   "l"(src + e0 + i * estep), "r"(any ? 16 : 0)
+    const float* ls = zn + ly.off + e0;    // next quad to load
+    const uint8_t* lrk = s_rk + tc.ph;     // its row flag
+    const unsigned ring0 = smem_u32(ring_slot<1>(ring, 0, 0));
+    auto issue = [&](int d, int) {
+      const bool any = ckb && *lrk;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring0 + d * kThreads * 16), "l"(ls),
+                   "r"(any ? 16 : 0)
                    : "memory");
+      ls += estep;
+      lrk += kRowPhases;
     };
     ring_prologue(count, issue);
     unsigned bad = 0;  // CHECK: kept but zero
-    auto consume = [&](int d, int i) {  // only valid quads get here
+    float* qc = zn + ly.off + e0;          // quad being consumed
+    uint32_t* mc = mask + ly.mword + (e0 >> 5);
+    const uint8_t* crk = s_rk + tc.ph;
+    const int sh = 4 * (lane & 7);
+    auto consume = [&](int d, int) {
       float4 v = *ring_slot<1>(ring, d, 0);
-      const unsigned kn = s_rk[tc.ph + kRowPhases * i] ? ckb : 0u;  // kept nibble
+      const unsigned kn = *crk ? ckb : 0u;  // kept nibble (0 past the row end)
       const unsigned nib = kn & ((unsigned)(v.x != 0.f) | ((unsigned)(v.y != 0.f) << 1) |
                                  ((unsigned)(v.z != 0.f) << 2) | ((unsigned)(v.w != 0.f) << 3));
       if (CHECK) bad |= kn & ~nib;
-      if (kn != 0xFu) {
+      if (kn != 0xFu && valid) {
         if (!(kn & 1u)) v.x = 0.f;
         if (!(kn & 2u)) v.y = 0.f;
         if (!(kn & 4u)) v.z = 0.f;
         if (!(kn & 8u)) v.w = 0.f;
-        st4(q0 + i * estep, v);
+        st4(qc, v);
       }
-      unsigned w = nib << (4 * (lane & 7));
-      w |= __shfl_xor_sync(gmask, w, 1);
-      w |= __shfl_xor_sync(gmask, w, 2);
-      w |= __shfl_xor_sync(gmask, w, 4);
-      if (word_lane) m0[i * mstep] = w;
+      unsigned w = nib << sh;
+      w |= __shfl_xor_sync(kFull, w, 1);
+      w |= __shfl_xor_sync(kFull, w, 2);
+      w |= __shfl_xor_sync(kFull, w, 4);
+      if (word_lane) *mc = w;
+      qc += estep;
+      mc += mstep;
+      crk += kRowPhases;
     };
     ring_loop(count, issue, consume);
     if (CHECK) flag_irregular(a, dl.pidx, bad != 0);

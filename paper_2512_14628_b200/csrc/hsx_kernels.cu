@@ -156,6 +156,27 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// TMA 1-D bulk copies (global -> shared, completion counted in bytes on an mbarrier)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // slot (stage d, buffer b) of this thread in a [kDepth][NB][kThreads] float4 ring
 template <int NB>
 __device__ __forceinline__ float4* ring_slot(float4* ring, int d, int b) {
@@ -1608,7 +1629,14 @@ __device__ __forceinline__ void flag_irregular(const KeepArgs& a, int pidx, bool
   }
 }
 
-template <bool CHECK>
+// TMA (unchained launches): the tile's rows of z_node arrive by 1-D bulk copies
+// (cp.async.bulk, one per kept row segment of up to 1 KB, issued by one thread) into
+// a two-stage ring of 16-row stages completed on mbarriers, instead of one 16-B
+// cp.async per quad and thread.
+constexpr int kProjStageRows = 16;
+constexpr size_t kProjTmaSmem = 2 * kProjStageRows * kTileQuads * 16;  // 32 KB
+
+template <bool CHECK, bool TMA = false>
 __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restrict__ zn,
                                              uint32_t* __restrict__ mask, const Item& it, float4* ring) {
   __shared__ uint8_t s_rk[kMaxTileRows];
@@ -1655,6 +1683,76 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
           if (!f[grp == kChannel ? fdiv(col, divk) : col]) ckb &= ~(1u << b);
         }
       }
+    }
+    if (TMA) {
+      __shared__ __align__(8) uint64_t s_full[2];
+      if (threadIdx.x == 0) {
+        mbar_init(&s_full[0], 1);
+        mbar_init(&s_full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      // no kept column in this chunk: nothing is read (every quad is zeroed)
+      const bool anycol = __syncthreads_or(ckb != 0);
+      const int q0 = it.chunk * kTileQuads;
+      const unsigned seg = (unsigned)min(kTileQuads, (ly.L >> 2) - q0) * 16u;
+      unsigned char* buf = reinterpret_cast<unsigned char*>(ring);
+      const float* rows = zn + ly.off + it.begin * ly.L + 4 * q0;
+      const int nst = (nrow + kProjStageRows - 1) / kProjStageRows;
+      auto issue_stage = [&](int g) {  // thread 0: the kept rows of stage g
+        const int b = g & 1, r0 = g * kProjStageRows, r1 = min(r0 + kProjStageRows, nrow);
+        unsigned bytes = 0;
+        for (int r = r0; r < r1; ++r) bytes += s_rk[r] ? seg : 0u;
+        mbar_arrive_tx(&s_full[b], bytes);
+        for (int r = r0; r < r1; ++r)
+          if (s_rk[r])
+            bulk_g2s(buf + ((size_t)b * kProjStageRows + (r - r0)) * (kTileQuads * 16), rows + (long long)r * ly.L,
+                     seg, &s_full[b]);
+      };
+      if (threadIdx.x == 0 && anycol) {
+        issue_stage(0);
+        if (nst > 1) issue_stage(1);
+      }
+      unsigned bad = 0;
+      float* qc = zn + ly.off + e0;
+      uint32_t* mc = mask + ly.mword + (e0 >> 5);
+      const int sh = 4 * (lane & 7);
+      for (int g = 0; g < nst; ++g) {
+        if (anycol) mbar_wait(&s_full[g & 1], (unsigned)(g >> 1) & 1u);
+        const unsigned char* sb = buf + (size_t)(g & 1) * kProjStageRows * (kTileQuads * 16) + tc.jj * 16;
+#pragma unroll
+        for (int k = 0; k < kProjStageRows / kRowPhases; ++k) {
+          if (4 * g + k >= count) break;  // warp-uniform
+          const int rr = tc.ph + kRowPhases * k;
+          float4 v = *reinterpret_cast<const float4*>(sb + rr * (kTileQuads * 16));
+          const unsigned kn = s_rk[g * kProjStageRows + rr] ? ckb : 0u;
+          const unsigned nib = kn & ((unsigned)(v.x != 0.f) | ((unsigned)(v.y != 0.f) << 1) |
+                                     ((unsigned)(v.z != 0.f) << 2) | ((unsigned)(v.w != 0.f) << 3));
+          if (CHECK) bad |= kn & ~nib;
+          if (kn != 0xFu && valid) {
+            if (!(kn & 1u)) v.x = 0.f;
+            if (!(kn & 2u)) v.y = 0.f;
+            if (!(kn & 4u)) v.z = 0.f;
+            if (!(kn & 8u)) v.w = 0.f;
+            st4(qc, v);
+          }
+          unsigned w = nib << sh;
+          w |= __shfl_xor_sync(kFull, w, 1);
+          w |= __shfl_xor_sync(kFull, w, 2);
+          w |= __shfl_xor_sync(kFull, w, 4);
+          if (word_lane) *mc = w;
+          qc += estep;
+          mc += mstep;
+        }
+        if (g + 2 < nst) {
+          __syncthreads();  // every thread is done with this stage's buffer
+          if (threadIdx.x == 0 && anycol) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_stage(g + 2);
+          }
+        }
+      }
+      if (CHECK) flag_irregular(a, dl.pidx, bad != 0);
+      return;
     }
     __syncthreads();
     // a quad with nothing kept is not read (the copy zero-fills it without touching
@@ -1744,7 +1842,7 @@ __device__ void fixup_layer(const KeepArgs& a, int l, uint8_t* fsm);
 // its dependents launch at once, waits for its layer's selection (ready[layer],
 // published by K2 with release semantics), projects, and waits for the grid before
 // it at the end; the layer's last item re-zeroes its counter and flag.
-template <bool CHECK>
+template <bool CHECK, bool TMA>
 __global__ void __launch_bounds__(kThreads, 5) k_project(KeepArgs a, float* __restrict__ zn,
                                                          uint32_t* __restrict__ mask, unsigned int* ready,
                                                          unsigned int* pdone, ChainK67 c67) {
@@ -1752,7 +1850,7 @@ __global__ void __launch_bounds__(kThreads, 5) k_project(KeepArgs a, float* __re
   const Item it = a.items[blockIdx.x];  // a register copy: a reference into global memory is
   if (ready == nullptr) {               // reloaded after every store through zn / mask
     PDL_ENTRY();
-    project_item<CHECK>(a, zn, mask, it, ring);
+    project_item<CHECK, TMA>(a, zn, mask, it, ring);
     return;
   }
   pdl_trigger();
@@ -1902,10 +2000,27 @@ void launch_project(const KeepArgs& a, int n_items, float* zn, uint32_t* mask, i
                     unsigned int* ready, unsigned int* pdone, ChainK67 c67, size_t fix_smem) {
   if (n_items <= 0) return;
   const size_t smem = (size_t)kDepth * kThreads * sizeof(float4);
+  // TMA row copies (unchained launches; HSX_K3_TMA=0: per-thread cp.async quads)
+  static const bool tma = [] {
+    const char* v = std::getenv("HSX_K3_TMA");
+    return v && v[0] == '1';
+  }();
+  if (tma && ready == nullptr) {
+    const size_t sm = std::max(smem, kProjTmaSmem);
+    if (check) {
+      allow_smem(k_project<true, true>, std::max(sm, fix_smem));
+      launch_pdl(k_project<true, true>, n_items, kThreads, std::max(sm, fix_smem), st, a, zn, mask, ready, pdone, c67);
+    } else {
+      allow_smem(k_project<false, true>, sm);
+      launch_pdl(k_project<false, true>, n_items, kThreads, sm, st, a, zn, mask, ready, pdone, c67);
+    }
+    return;
+  }
   if (check)
-    launch_pdl(k_project<true>, n_items, kThreads, std::max(smem, fix_smem), st, a, zn, mask, ready, pdone, c67);
+    launch_pdl(k_project<true, false>, n_items, kThreads, std::max(smem, fix_smem), st, a, zn, mask, ready, pdone,
+               c67);
   else
-    launch_pdl(k_project<false>, n_items, kThreads, smem, st, a, zn, mask, ready, pdone, c67);
+    launch_pdl(k_project<false, false>, n_items, kThreads, smem, st, a, zn, mask, ready, pdone, c67);
 }
 
 // ---------------------------------------------------------------------------

@@ -408,6 +408,22 @@ int hsx_slices_peers(const hsx_plan* plan, const float* const* srcs, int32_t n, 
  * it so the host can raise ProtocolError. */
 int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
                       void* stream);
+/* Split two-rank K1 (P = 2, peer transport): each rank computes the candidate and
+ * the group-norm partials of every dense item and of half of the prunable tiles,
+ * reading both ranks' theta + u sends, and writes z_node, the partials and the
+ * chained selection's tile counts into its own AND the peer's buffers (peer-mapped
+ * memory), so each rank reads only half of the peer's send over NVLink. The
+ * chained K2 (each layer's selection waits for both ranks' tiles) orders the peer's
+ * writes before the selection, K3 and the rest of the step. Sizes of the
+ * peer-mapped partials (doubles) and tile counters (uint32) the caller allocates: */
+int hsx_plan_split_sizes(const hsx_plan* p, int64_t* partials_elems, int32_t* counters);
+/* Install them (me = this rank's index in the pair); needs a single-pass plan with
+ * the chained selection. */
+int hsx_plan_set_split(hsx_plan* p, int32_t me, double* partials, double* partials_peer, uint32_t* k1done,
+                       uint32_t* k1done_peer);
+/* The split K1 (dynamic steps; z_node_peer = the peer's z_node arena). */
+int hsx_candidate_peers_split(hsx_plan* p, const float* const* sends, int32_t n, const float* z, const float* v,
+                              float* z_node, float* z_node_peer, void* stream);
 /* One-sided variant: mode 0 = hsx_group_barrier; mode 1 = this member (the root)
  * only publishes the epoch and does not wait; mode 2 = this member waits for member
  * `root`'s epoch only (a producer -> readers hand-off; all members still count the

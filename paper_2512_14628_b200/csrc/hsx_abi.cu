@@ -134,6 +134,15 @@ struct hsx_plan {
   unsigned int *d_sready = nullptr, *d_sepoch = nullptr, *d_scounter = nullptr;
   int k2_armed = 0;                  // the last launch was such a K1: hsx_select(0) chains behind it
   int k2_pending = 0;                // a counting K1 ran whose counts no chained K2 consumed yet
+  // split two-rank K1 (hsx_plan_set_split): this rank's work list (dense items and
+  // every other prunable tile), the peer's partials / tile counts; partials[0] and
+  // the counts then live in caller-owned peer-mapped memory (not freed here)
+  Item* d_cand_split = nullptr;
+  int n_cand_split = 0;
+  int split_me = -1;
+  double* partials_peer = nullptr;
+  unsigned int* k1done_peer = nullptr;
+  int ext_partials = 0, ext_k1done = 0;
   int k3_armed = 0;                  // the last launch was a chained single-pass K2: K3 chains behind it
   int k67_armed = 0;                 // the last launch was a chained one-node K3 with fixups: K67 chains
   int k67_chain = 0;                 // hsx_plan_set_k67_chain: the caller follows every one-node projection with K67
@@ -155,6 +164,9 @@ struct hsx_plan {
   std::vector<long long> summary;  // host mirror (dense rows, installed keep sets)
 
   ~hsx_plan() {
+    if (ext_k1done) d_k1done = nullptr;
+    if (ext_partials) d_partials[0] = nullptr;
+    if (d_cand_split) cudaFree(d_cand_split);
     void* ptrs[] = {d_stage, d_sready, d_sepoch, d_scounter, d_ready3, d_cnt67, d_up, d_k1done, d_layers, d_cand, d_layer_done, d_cand_done, d_sched, d_sfirst, d_scount, d_rpart, d_ready, d_pdone, d_acc, d_rk_prev, d_ck_prev, d_irr, d_irr_any, d_elem, d_stream, d_proj, d_word, d_prunable, d_oflag, d_iflag,
                     d_pos_out, d_pos_in, d_summary, d_done,
                     d_ch_prev};
@@ -949,12 +961,86 @@ int hsx_plan_set_k67_chain(hsx_plan* p, int32_t on) {
   return HSX_OK;
 }
 
+// split two-rank K1: rank `split_me` takes every dense item (both ranks compute the
+// dense layers, which no tile count orders) and the prunable tiles at its parity
+// in K1's work-list order
+static int upload_split_items(hsx_plan* p) {
+  std::vector<Item> mine;
+  int k = 0;
+  for (const Item& it : p->cand_dyn) {
+    if (p->layers[it.layer].ncons == 0)
+      mine.push_back(it);
+    else if ((k++ & 1) == p->split_me)
+      mine.push_back(it);
+  }
+  if (!p->d_cand_split) HSX_CUDA(cudaMalloc(&p->d_cand_split, std::max<size_t>(p->cand_dyn.size(), 1) * sizeof(Item)));
+  if (!mine.empty())
+    HSX_CUDA(cudaMemcpy(p->d_cand_split, mine.data(), mine.size() * sizeof(Item), cudaMemcpyHostToDevice));
+  p->n_cand_split = (int)mine.size();
+  return HSX_OK;
+}
+
+int hsx_plan_split_sizes(const hsx_plan* p, int64_t* partials_elems, int32_t* counters) {
+  if (!p || !partials_elems || !counters) return fail(HSX_EINVAL, "null argument");
+  *partials_elems = p->ptotal[0];
+  *counters = (int32_t)p->prunable.size() + 1;
+  return HSX_OK;
+}
+
+int hsx_plan_set_split(hsx_plan* p, int32_t me, double* partials, double* partials_peer, uint32_t* k1done,
+                       uint32_t* k1done_peer) {
+  if (!p) return fail(HSX_EINVAL, "null plan");
+  if (me < 0 || me > 1 || !partials || !partials_peer || !k1done || !k1done_peer)
+    return fail(HSX_EINVAL, "split K1 takes two ranks and peer-mapped partials / counts");
+  if (p->identity || p->max_passes != 1) return fail(HSX_EINVAL, "split K1 needs a single-pass penalty plan");
+  if (!env_flag("HSX_K2_CHAIN", 1) || p->sel_list[0].size() != p->prunable.size())
+    return fail(HSX_EINVAL, "split K1 needs the chained selection of every prunable layer");
+  if (p->split_me >= 0) return fail(HSX_EINVAL, "split already set");
+  if (p->d_partials[0] && !p->ext_partials) cudaFree(p->d_partials[0]);
+  if (p->d_k1done && !p->ext_k1done) cudaFree(p->d_k1done);
+  p->d_partials[0] = partials;
+  p->d_k1done = k1done;
+  p->ext_partials = p->ext_k1done = 1;
+  p->partials_peer = partials_peer;
+  p->k1done_peer = k1done_peer;
+  p->split_me = me;
+  return upload_split_items(p);
+}
+
+int hsx_candidate_peers_split(hsx_plan* p, const float* const* sends, int32_t n, const float* z, const float* v,
+                              float* z_node, float* z_node_peer, void* stream) {
+  if (!p || !z_node || !z_node_peer || !sends || !z || !v) return fail(HSX_EINVAL, "null argument");
+  if (p->split_me < 0) return fail(HSX_EINVAL, "split K1 not set up (hsx_plan_set_split)");
+  if (n != 2 || !sends[0] || !sends[1]) return fail(HSX_EINVAL, "split K1 takes two ranks");
+  // the peer counts into this rank's counters concurrently: they cannot be reset here
+  if (p->k2_pending) return fail(HSX_EINVAL, "split K1 behind a counting K1 no selection consumed");
+  hsx::CandArgs a = cand_args(p, nullptr, nullptr, nullptr, z, v);
+  a.peers.n = 2;
+  a.peers.p[0] = sends[0];
+  a.peers.p[1] = sends[1];
+  a.zn = z_node;
+  a.zn_peer = z_node_peer;
+  a.pass = 0;
+  a.partials = p->d_partials[0];
+  a.partials_peer = p->partials_peer;
+  a.norms = p->d_norms[0];
+  a.items = p->d_cand_split;
+  arm_chain(p, a, S(stream));
+  if (!a.k1done) return fail(HSX_EINVAL, "split K1 needs the chained selection");
+  a.k1done_peer = p->k1done_peer;
+  hsx::launch_candidate(a, p->n_cand_split, 0, p->cand_smem, S(stream));
+  HSX_LAUNCHED("candidate_peers_split");
+  return HSX_OK;
+}
+
 int hsx_plan_set_order(hsx_plan* p, int32_t big_first) {
   if (!p) return fail(HSX_EINVAL, "null plan");
   if ((big_first != 0) == (p->big_first != 0)) return HSX_OK;
   set_order(p, big_first != 0);
   HSX_CUDA(cudaMemcpy(p->d_cand, p->cand_dyn.data(), p->cand_dyn.size() * sizeof(Item), cudaMemcpyHostToDevice));
   HSX_CUDA(cudaMemcpy(p->d_proj, p->proj_items.data(), p->proj_items.size() * sizeof(Item), cudaMemcpyHostToDevice));
+  if (p->split_me >= 0)
+    if (int rc = upload_split_items(p)) return rc;
   for (int q = 0; q < hsx::kMaxPasses; ++q)
     if (!p->sel_list[q].empty())
       HSX_CUDA(cudaMemcpy(p->d_sel[q], p->sel_list[q].data(), p->sel_list[q].size() * sizeof(int),

@@ -885,7 +885,9 @@ __global__ void __launch_bounds__(1024) k_select(const DevLayer* __restrict__ la
   if (threadIdx.x == 0) {
     unsigned v;
     for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      // system scope: under a split two-rank K1 half of the counts (and partials) come
+      // from the peer GPU
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
       if (v >= (unsigned)ly.ncitems) break;
       __nanosleep(128);
     }
@@ -1157,6 +1159,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const long long off = ly.off;
   const K1Src src = k1_src<MODE>(p, off + 4 * j);
   float* zn = p.zn + off + 4 * j;
+  float* znp = p.zn_peer ? p.zn_peer + off + 4 * j : nullptr;
   const Coef cf = coef_of(ly);
   const long long stride = (long long)RP * L;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -1174,7 +1177,9 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
           for (int i2 = 0; i2 < 4; ++i2)
             if (!kept_by(ly, p.flags, pass, ee + i2)) c[i2] = 0.0;
         } else {
-          st4(zn + e, make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]));
+          const float4 o = make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]);
+          st4(zn + e, o);
+          if (znp) st4(znp + e, o);  // split K1: the peer's z_node too (NVLink store)
         }
         a0 = __dadd_rn(a0, __dmul_rn(c[0], c[0]));
         a1 = __dadd_rn(a1, __dmul_rn(c[1], c[1]));
@@ -1190,6 +1195,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const bool percol = ly.group[pass] == kShape || ly.k == 1 || ly.percol;
   const int G = ly.G[pass];
   double* out = p.partials + ly.poff[pass] + (long long)it.part * (percol ? L : G);
+  double* outp = p.partials_peer ? p.partials_peer + (out - p.partials) : nullptr;
   const int t = threadIdx.x;
   double s = 0.0;
   if (t < ncol) {  // one column per thread: the row phases in order
@@ -1197,7 +1203,10 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
     for (int q = 1; q < RP; ++q) s += cs[q * 4 * W + t];
   }
   if (percol) {
-    if (t < ncol) out[col0 + t] = s;
+    if (t < ncol) {
+      out[col0 + t] = s;
+      if (outp) outp[col0 + t] = s;
+    }
     return;
   }
   __syncthreads();
@@ -1209,6 +1218,7 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
     double g = 0.0;
     for (int jx = 0; jx < k; ++jx) g += cs[t * k + jx];
     out[c0 + t] = g;
+    if (outp) outp[c0 + t] = g;
   }
 }
 
@@ -1232,7 +1242,10 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
   for (int i = threadIdx.x; i < E; i += kThreads) {
     double c = cand_elem<MODE>(p, gbase + i, cf);
     if (pass > 0 && !kept_by(ly, p.flags, pass, ebase + i)) c = 0.0;
-    if (pass == 0) p.zn[gbase + i] = (float)c;
+    if (pass == 0) {
+      p.zn[gbase + i] = (float)c;
+      if (p.zn_peer) p.zn_peer[gbase + i] = (float)c;
+    }
     sq[i] = __dmul_rn(c, c);
   }
   __syncthreads();
@@ -1242,13 +1255,17 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
       for (int i = lane; i < L; i += 32) s += sq[r * L + i];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
-      if (lane == 0) p.partials[ly.poff[pass] + r0 + r] = s;
+      if (lane == 0) {
+        p.partials[ly.poff[pass] + r0 + r] = s;
+        if (p.partials_peer) p.partials_peer[ly.poff[pass] + r0 + r] = s;
+      }
     }
   } else if (grp == kShape || ly.k == 1 || ly.percol) {
     for (int col = threadIdx.x; col < L; col += kThreads) {
       double s = 0.0;
       for (int r = 0; r < nr; ++r) s += sq[r * L + col];
       p.partials[ly.poff[pass] + (long long)it.part * L + col] = s;
+      if (p.partials_peer) p.partials_peer[ly.poff[pass] + (long long)it.part * L + col] = s;
     }
   } else {
     const int k = ly.k, G = ly.G[pass];
@@ -1257,6 +1274,7 @@ __device__ void cand_tile_rows(const CandArgs& p, const DevLayer& ly, const Item
       for (int r = 0; r < nr; ++r)
         for (int jx = 0; jx < k; ++jx) s += sq[r * L + c * k + jx];
       p.partials[ly.poff[pass] + (long long)it.part * G + c] = s;
+      if (p.partials_peer) p.partials_peer[ly.poff[pass] + (long long)it.part * G + c] = s;
     }
   }
 }
@@ -1315,7 +1333,14 @@ __device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const I
     if (p.k1done) {  // chained K2: this tile's partials are released to the layer's selection
       __syncthreads();
       if (threadIdx.x == 0) {
-        __threadfence();
+        if (p.k1done_peer) {
+          // split K1: the tile's z_node and partials went to both ranks; both
+          // selections count it (system scope: the peer's K2 reads over its acquire)
+          __threadfence_system();
+          atomicAdd_system(p.k1done_peer + ly.pidx, 1u);
+        } else {
+          __threadfence();
+        }
         atomicAdd(p.k1done + ly.pidx, 1u);
       }
     }

@@ -133,6 +133,12 @@ struct CandArgs {
   const uint8_t* flags[kMaxPasses];    // keep flags of earlier passes (renorm)
   PeerPtrs peers;                      // n > 0: S = sum of the peers' theta + u (rank order)
   unsigned int* k1done;                // chained K2: +1 per finished tile of a prunable layer (or nullptr)
+  // split two-rank K1 (hsx_candidate_peers_split): this rank computes half of the
+  // prunable layers' tiles and writes z_node, the partials and the tile counts into
+  // its own and the peer's buffers (peer-mapped; nullptr: not split)
+  float* zn_peer;
+  double* partials_peer;
+  unsigned int* k1done_peer;
   // staged peer operand (two ranks): u is a local copy of the peer's send that a
   // staging kernel fills item by item on a side stream; sready[item] == epoch + 1
   // once the item's region landed, else K1 reads u_alt (the peer's send) directly

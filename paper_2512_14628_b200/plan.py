@@ -224,6 +224,28 @@ class Plan:
                       ptr(frozen_mask), current_stream())
         del keep
 
+    def split_sizes(self) -> tuple[int, int]:
+        """(partials doubles, tile counters) of a split two-rank K1 (hsx_plan_split_sizes)."""
+        import ctypes as C
+
+        n, c = C.c_int64(0), C.c_int32(0)
+        _lib.call("hsx_plan_split_sizes", self._h, C.byref(n), C.byref(c))
+        return int(n.value), int(c.value)
+
+    def set_split(self, me: int, partials: int, partials_peer: int, counts: int, counts_peer: int):
+        """Install the peer-mapped partials / tile counts of a split K1 (hsx_plan_set_split)."""
+        _lib.call("hsx_plan_set_split", self._h, int(me), ptr(partials), ptr(partials_peer), ptr(counts),
+                  ptr(counts_peer))
+
+    def candidate_peers_split(self, sends: list[int], z, v, z_node, z_node_peer: int):
+        """K1 of half the prunable tiles (and every dense item) of a two-rank node,
+        writing z_node / partials / tile counts to both ranks (hsx_candidate_peers_split)."""
+        arr, keep = _lib.ptr_array(sends)
+        with timed("K1_candidate"):
+            _lib.call("hsx_candidate_peers_split", self._h, arr, len(sends), ptr(z), ptr(v), ptr(z_node),
+                      ptr(z_node_peer), current_stream())
+        del keep
+
     def set_peer_staging(self, on: bool):
         """Allocate the staged-peer-operand buffers (hsx_plan_set_peer_staging)."""
         _lib.call("hsx_plan_set_peer_staging", self._h, 1 if on else 0)

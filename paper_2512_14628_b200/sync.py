@@ -76,6 +76,7 @@ class HSADMMSync:
         self.topology = topo
         self.M, self.P = topo.num_nodes, topo.accels_per_node
         self._staged = False
+        self._split = False
         self.node = topo.node_of(rank)
         self.leader_rank = topo.leader_of(self.node)
         self.is_leader = rank == self.leader_rank
@@ -156,11 +157,44 @@ class HSADMMSync:
             self._staged = self.P == 2 and os.environ.get("HSX_PEER_STAGING") == "1"
             if self._staged:
                 self.plan.set_peer_staging(True)
+            self._init_split()
         # deferred host bookkeeping (step_host): a step returns once its launches are
         # queued; the keep-set counts are read back when the next step starts
         self.defer_host = False
         self._pending = None
         self._pipe = None
+
+    def _init_split(self):
+        """Split two-rank K1 (HSX_K1_SPLIT=1; P == 2, one process per rank): each rank
+        computes half of the prunable tiles reading half of the peer's send over NVLink
+        and writes z_node, the group-norm partials and the chained selection's tile
+        counts into both ranks' (peer-mapped) buffers. z_node (and its residual double
+        buffer) move into peer-mapped memory; the allocations are collective over the
+        world, so every rank takes the same decision (same env, topology and plan)."""
+        self._split = False
+        self._zn_peer = {}
+        if not (self.P == 2 and os.environ.get("HSX_K1_SPLIT") == "1"
+                and getattr(self.cluster, "concurrent_ranks", False) and self.prunable):
+            return
+        pl, dev, cl = self.plan, self.device, self.cluster
+        me = self.intra.members.index(self.rank)
+        zn = [cl.shared(self.rank, self.intra, f"zn{b}", pl.arena, torch.float32, dev) for b in (0, 1)]
+        npart, ncnt = pl.split_sizes()
+        part = cl.shared(self.rank, self.intra, "k1part", npart, torch.float64, dev)
+        cnt = cl.shared(self.rank, self.intra, "k1cnt", ncnt, torch.int32, dev)
+        try:
+            pl.set_split(me, part.tensor, part.peer_ptrs()[1 - me], cnt.tensor, cnt.peer_ptrs()[1 - me])
+        except Exception:   # e.g. a multi-pass plan: the same outcome on every rank
+            return
+        zn[0].tensor.copy_(self.z_node)
+        self.z_node = zn[0].tensor
+        if self.z_node_prev is not None:
+            zn[1].tensor.copy_(self.z_node_prev)
+            self.z_node_prev = zn[1].tensor
+        self._zn_spare = zn[1].tensor
+        self._zn_peer = {b.tensor.data_ptr(): b.peer_ptrs()[1 - me] for b in zn}
+        self._split_bufs = (zn, part, cnt)
+        self._split = True
 
     def _init_peer_buffers(self):
         """Shared (peer-mapped) buffers; allocation is collective over each group."""
@@ -364,7 +398,9 @@ class HSADMMSync:
             self._pack_send(send.tensor)
             yield Barrier(self.intra, "theta_u", k)
             peers = send.peer_ptrs()
-            if self._staged and fmask is None:
+            if self._split and fmask is None:
+                pl.candidate_peers_split(peers, self.z, self.v, self.z_node, self._zn_peer[self.z_node.data_ptr()])
+            elif self._staged and fmask is None:
                 pl.candidate_peers_staged(peers, self.intra.members.index(self.rank), self.z, self.v, self.z_node)
             else:
                 pl.candidate_peers(peers, self.z, self.v, self.z_node, frozen_mask=fmask)
@@ -567,7 +603,8 @@ class HSADMMSync:
         self.settle()
         self.residuals = bool(on)
         if self.residuals and self.z_node_prev is None:
-            self.z_node_prev = self.plan.empty_arena(self.device)
+            # split K1: the peer-mapped spare (K1 writes the peer's z_node buffer too)
+            self.z_node_prev = self._zn_spare if getattr(self, "_split", False) else self.plan.empty_arena(self.device)
         if adapt is not None:
             self._resid_params.adapt = 1 if adapt else 0
 

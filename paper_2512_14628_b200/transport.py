@@ -432,6 +432,10 @@ class Cluster:
 class LocalCluster(Cluster):
     """All ranks of a topology in one process; deterministic round-based scheduler."""
 
+    # the ranks' kernels run one after another on one device: no kernel may wait for
+    # another rank's concurrently running kernel
+    concurrent_ranks = False
+
     def __init__(self, topology: Topology, latency=None):
         self.topology = topology
         self.ledger = CommLedger()
@@ -552,6 +556,8 @@ class DistCluster(Cluster):
     All ranks construct it collectively: ``dist.new_group`` is called for every
     intra group and the leader group in the same order on every rank.
     """
+
+    concurrent_ranks = True   # one process (and device) per rank
 
     def __init__(self, topology: Topology, latency=None):
         import torch.distributed as dist

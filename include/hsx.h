@@ -209,6 +209,12 @@ int hsx_mask_or(const uint32_t* gathered, int32_t n_ranks, int64_t words, uint32
  * prev != NULL. */
 int hsx_keep_sets(hsx_plan* plan, const uint32_t* union_mask, const uint32_t* prev_mask,
                   void* stream);
+/* K4 fused into K5 (peer transport, M > 1): the union is the OR of the n leaders'
+ * local mask bits `srcs` (peer-mapped), formed while K5 marks the keep sets and
+ * stored to union_out; replaces hsx_mask_or_ptrs + hsx_keep_sets (and the
+ * followers' copy of their leader's union). Multi-node plans only. */
+int hsx_keep_sets_ptrs(hsx_plan* p, const uint32_t* const* srcs, int32_t n, uint32_t* union_out,
+                       const uint32_t* prev_mask, void* stream);
 /* D2H of the per-layer summary (n_layers x HSX_SUM_COLS int64, then 1 int64
  * total payload elements) into host memory; synchronizes `stream`. */
 int hsx_keep_sets_fetch(hsx_plan* plan, int64_t* host_summary, void* stream);

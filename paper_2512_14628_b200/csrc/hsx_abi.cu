@@ -610,6 +610,8 @@ static hsx::KeepArgs keep_args(hsx_plan* p, const Item* items, const uint32_t* u
   ka.layers = p->d_layers;
   ka.items = items;
   ka.uni = uni;
+  ka.usrc.n = 0;
+  ka.uni_out = nullptr;
   ka.prev = prev;
   ka.oflag = p->d_oflag;
   ka.iflag = p->d_iflag;
@@ -1063,6 +1065,24 @@ int hsx_keep_sets(hsx_plan* p, const uint32_t* union_mask, const uint32_t* prev_
   hsx::KeepArgs ka = keep_args(p, p->d_word, union_mask, prev_mask);
   hsx::launch_keep_sets(ka, (int)p->word_items.size(), p->mark_smem, S(stream));
   HSX_LAUNCHED("keep_sets");
+  return HSX_OK;
+}
+
+int hsx_keep_sets_ptrs(hsx_plan* p, const uint32_t* const* srcs, int32_t n, uint32_t* union_out,
+                       const uint32_t* prev_mask, void* stream) {
+  if (!p || !srcs || (!union_out && p->mask_words)) return fail(HSX_EINVAL, "null argument");
+  if (n < 1 || n > 8) return fail(HSX_EINVAL, "source count %d outside [1, 8]", n);
+  if (p->prunable.empty()) return HSX_OK;
+  if (p->single_node) return fail(HSX_EINVAL, "one-node plans derive keep sets in K3 (structured)");
+  hsx::KeepArgs ka = keep_args(p, p->d_word, nullptr, prev_mask);
+  ka.usrc.n = n;
+  for (int r = 0; r < n; ++r) {
+    if (!srcs[r]) return fail(HSX_EINVAL, "null mask pointer %d", r);
+    ka.usrc.p[r] = srcs[r];
+  }
+  ka.uni_out = union_out;
+  hsx::launch_keep_sets(ka, (int)p->word_items.size(), p->mark_smem, S(stream));
+  HSX_LAUNCHED("keep_sets_ptrs");
   return HSX_OK;
 }
 

@@ -2116,7 +2116,15 @@ __global__ void __launch_bounds__(kThreads) k_keep_sets(KeepArgs a) {
     long long e0 = w << 5;
     long long nvalid = ly.n - e0;
     uint32_t valid = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
-    uint32_t x = a.uni[ly.mword + w] & valid;
+    uint32_t x;
+    if (a.usrc.n) {  // fused union: OR of the leaders' words (over NVLink), stored once
+      x = 0;
+      for (int j = 0; j < a.usrc.n; ++j) x |= __ldcg(a.usrc.p[j] + ly.mword + w);
+      a.uni_out[ly.mword + w] = x;
+      x &= valid;
+    } else {
+      x = a.uni[ly.mword + w] & valid;
+    }
     pop += __popc(x);
     if (a.prev) drift += __popc((x ^ a.prev[ly.mword + w]) & valid);
     if (wordwise) {

@@ -99,6 +99,10 @@ struct KeepArgs {
   const DevLayer* layers;
   const Item* items;
   const uint32_t* uni;
+  // usrc.n > 0: the union is the OR of these mask-bit arrays (the leaders' local
+  // masks, peer-mapped), formed while marking and stored to uni_out (K4 fused into K5)
+  MaskPtrs usrc;
+  uint32_t* uni_out;
   const uint32_t* prev;
   uint8_t* oflag;
   uint8_t* iflag;

@@ -354,6 +354,15 @@ class Plan:
         with timed("K5_keep_sets"):
             _lib.call("hsx_keep_sets", self._h, ptr(union_mask), ptr(prev_mask), current_stream())
 
+    def keep_sets_ptrs(self, srcs: list[int], union_out, prev_mask=None):
+        """K5 with the union formed on the fly: OR of the leaders' mask bits ``srcs``
+        (peer pointers), stored to ``union_out`` (hsx_keep_sets_ptrs)."""
+        arr, keep = _lib.ptr_array(srcs)
+        with timed("K5_keep_sets"):
+            _lib.call("hsx_keep_sets_ptrs", self._h, arr, len(srcs), ptr(union_out), ptr(prev_mask),
+                      current_stream())
+        del keep
+
     def keep_sets_fetch(self):
         """D2H of the per-layer summary; synchronizes the current stream."""
         _lib.call("hsx_keep_sets_fetch", self._h, self.summary_host.data_ptr(), current_stream())

@@ -57,6 +57,10 @@ _SPLIT_K6 = os.environ.get("HSX_SPLIT_K6") == "1"
 # (the leader's path is the long one; 2x2 RN18/RN50 steady step unchanged), so
 # opt-in (HSX_ONESIDED=1)
 _ONESIDED = os.environ.get("HSX_ONESIDED") == "1"
+# multi-node peer steps: the mask union (K4) formed inside K5 from the leaders' mask
+# bits over NVLink, for leaders and followers alike (HSX_FUSED_UNION=0: K4, then the
+# followers copy their leader's union, then K5)
+_FUSED_UNION = os.environ.get("HSX_FUSED_UNION", "1") != "0"
 
 
 class HSADMMSync:
@@ -218,8 +222,16 @@ class HSADMMSync:
         self.p_ssum = self.p_favg = None
         if self.P > 2:   # reduce-scatter + all-gather of the intra sum
             self.p_ssum = cl.shared(self.rank, self.intra, "ssum", pl.arena, torch.float32, dev)
+        self._lmask_all = None
+        self._nmask = 0         # fused-union mask phases so far (leader mask buffer)
         if self.M > 1:
-            lmask = cl.shared(self.rank, self.inter, "lmask", words, torch.int32, dev)
+            # the leaders' local masks, double-buffered by step parity: with the union
+            # formed inside K5 every rank (followers too) reads all leaders' masks, and
+            # nothing orders another node's follower's read before this leader's next
+            # K3; its rewrite two steps later is ordered by the next mask_sync
+            lmask2 = [cl.shared(self.rank, self.inter, f"lmask{b}", words, torch.int32, dev) for b in (0, 1)]
+            self._lmask_all = lmask2
+            lmask = lmask2[0]
             # double-buffered by sync count: a leader may start the next compaction
             # while another still averages this one (the next z_sync barrier orders
             # the rewrite two syncs later)
@@ -413,7 +425,13 @@ class HSADMMSync:
             pl.project_all(s_local, self.theta, self.u, self.z, self.v, self.z_node, self.union, peers=peers,
                            keep_prev=True, prev_mask=self.masks)
         elif dynamic:
-            local = self.p_lmask.tensor if self.p_lmask is not None else self.local_mask
+            if _FUSED_UNION and self._lmask_all is not None:
+                # leaders of a syncing step: this sync's buffer (read by every rank's K5)
+                sync_now = k % self.settings.sync_period == 0
+                local = (self._lmask_all[self._nmask & 1].tensor if (self.is_leader and sync_now)
+                         else self.local_mask)
+            else:
+                local = self.p_lmask.tensor if self.p_lmask is not None else self.local_mask
             pl.project_all(s_local, self.theta, self.u, self.z, self.v, self.z_node, local, peers=peers)
         if k % self.settings.sync_period != 0:
             self._dual(None)
@@ -425,6 +443,17 @@ class HSADMMSync:
         if fused_keep:
             if not self._k67_chain:   # chained: fetched after K67 (K3 -> K67 consecutive launches)
                 ev = pl.keep_sets_fetch_async()
+        elif dynamic and _FUSED_UNION and self._lmask_all is not None:
+            # K4 fused into K5: after the leaders' masks are final (mask_sync among the
+            # leaders, then m_bcast inside each node) every rank ORs the M leaders'
+            # mask bits over NVLink while marking its keep sets
+            if self.is_leader:
+                yield Barrier(self.inter, "mask_sync", k)
+            if self.P > 1:
+                yield Barrier(self.intra, "m_bcast", k, root=self.leader_rank if _ONESIDED else None)
+            pl.keep_sets_ptrs(self._lmask_all[self._nmask & 1].peer_ptrs(), self.union, self.masks)
+            self._nmask += 1
+            ev = pl.keep_sets_fetch_async()
         elif dynamic:
             words = pl.mask_words
             if self.is_leader:

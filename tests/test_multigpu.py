@@ -28,3 +28,25 @@ def test_torchrun_nccl_parity(grouping):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "ok" in r.stdout
+
+
+VARIANTS = [("1x2", {"HSX_K1_SPLIT": "1"}), ("2x2", {"HSX_K1_SPLIT": "1"}), ("2x2", {"HSX_FUSED_UNION": "0"}),
+            ("2x2", {"HSX_ONESIDED": "1"})]
+
+
+@pytest.mark.parametrize("idx", range(len(VARIANTS)))
+def test_torchrun_parity_variants(idx):
+    """The opt-in / fallback step variants (split two-rank K1, K4 before K5, one-sided
+    leader hand-offs) against the same goldens and full-size agreement checks."""
+    grouping, env = VARIANTS[idx]
+    m, p = (int(x) for x in grouping.split("x"))
+    n = m * p
+    if not torch.cuda.is_available() or torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29650 + idx),
+           os.path.join(ROOT, "tests", "mp_parity.py"), grouping]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env={**os.environ, "HSX_BARRIER_TIMEOUT_S": "60", **env})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ok" in r.stdout

@@ -414,6 +414,12 @@ int hsx_slices_peers(const hsx_plan* plan, const float* const* srcs, int32_t n, 
  * it so the host can raise ProtocolError. */
 int hsx_group_barrier(int32_t* const* flags, const int32_t* slots, int32_t n, int32_t me, int32_t epoch,
                       void* stream);
+/* K1 on a distributed intra sum (P > 2, peer transport): after the reduce-scatter
+ * (hsx_slices_peers with part = j on rank j), slices[j] = rank j's slice buffer;
+ * each quad's S is read from its slice owner over NVLink (no all-gather of S,
+ * no local copy). Same results as hsx_candidate on the all-gathered sum. */
+int hsx_candidate_dist(hsx_plan* p, const float* const* slices, int32_t n, const float* z, const float* v,
+                       float* z_node, const uint32_t* frozen_mask, void* stream);
 /* Split two-rank K1 (P = 2, peer transport): each rank computes the candidate and
  * the group-norm partials of every dense item and of half of the prunable tiles,
  * reading both ranks' theta + u sends, and writes z_node, the partials and the

@@ -115,6 +115,7 @@ SIGNATURES = {
     "hsx_group_barrier_mode": (C.c_int, [VP, VP, I32, I32, I32, I32, I32, VP]),
     "hsx_plan_split_sizes": (C.c_int, [VP, VP, VP]),
     "hsx_keep_sets_ptrs": (C.c_int, [VP, VP, I32, VP, VP, VP]),
+    "hsx_candidate_dist": (C.c_int, [VP, VP, I32, VP, VP, VP, VP, VP]),
     "hsx_plan_set_split": (C.c_int, [VP, I32, VP, VP, VP, VP]),
     "hsx_candidate_peers_split": (C.c_int, [VP, VP, I32, VP, VP, VP, VP, VP]),
     "hsx_barrier_timeouts": (C.c_int, [C.POINTER(C.c_uint32), I32]),

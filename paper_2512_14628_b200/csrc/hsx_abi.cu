@@ -733,6 +733,39 @@ int hsx_candidate_peers(hsx_plan* p, const float* const* sends, int32_t n, const
   return HSX_OK;
 }
 
+int hsx_candidate_dist(hsx_plan* p, const float* const* slices, int32_t n, const float* z, const float* v,
+                       float* z_node, const uint32_t* frozen_mask, void* stream) {
+  if (!p || !z_node || !slices || !z || !v) return fail(HSX_EINVAL, "null argument");
+  if (n < 2 || n > hsx::kMaxPeers) return fail(HSX_EINVAL, "slice count %d outside [2, %d]", n, hsx::kMaxPeers);
+  if (p->identity) return fail(HSX_EINVAL, "distributed candidate needs a penalty plan");
+  hsx::CandArgs a = cand_args(p, nullptr, nullptr, nullptr, z, v);
+  // the slices of hsx_slices_peers(part = j) over the whole arena
+  const long long total = p->arena;
+  const long long slice = ((total + n - 1) / n + 31) / 32 * 32;
+  a.peers.n = n;
+  for (int j = 0; j < n; ++j) {
+    if (!slices[j]) return fail(HSX_EINVAL, "null slice pointer %d", j);
+    a.peers.p[j] = slices[j];
+    a.sbound[j] = std::min<long long>((long long)j * slice, total);
+  }
+  a.sdist = 1;
+  a.zn = z_node;
+  a.fmask = frozen_mask;
+  a.pass = 0;
+  a.partials = p->d_partials[0];
+  a.norms = p->d_norms[0];
+  if (frozen_mask) {
+    a.items = p->d_elem;
+    hsx::launch_candidate(a, (int)p->elem_items.size(), 1, p->cand_smem, S(stream));
+  } else {
+    a.items = p->d_cand;
+    arm_chain(p, a, S(stream));
+    hsx::launch_candidate(a, (int)p->cand_dyn.size(), 0, p->cand_smem, S(stream));
+  }
+  HSX_LAUNCHED("candidate_dist");
+  return HSX_OK;
+}
+
 int hsx_plan_set_peer_staging(hsx_plan* p, int32_t on) {
   if (!p) return fail(HSX_EINVAL, "null plan");
   if (!on || p->d_stage) return HSX_OK;

@@ -942,7 +942,9 @@ __device__ __forceinline__ double cand_of(double s, double z, double v, const Co
 // fold), or the candidate is S itself (kModeIdent: per-tensor projection API)
 // (kModePeers2: exactly two ranks — a 4-slot ring stage like the local modes, so
 // three CTAs fit per SM instead of two)
-enum { kModeThetaU = 0, kModeSum = 1, kModeIdent = 2, kModePeers = 3, kModePeers2 = 4 };
+// (kModeSumDist: S is the P ranks' reduce-scatter slices, read from the owner of
+// each quad over NVLink instead of all-gathered first)
+enum { kModeThetaU = 0, kModeSum = 1, kModeIdent = 2, kModePeers = 3, kModePeers2 = 4, kModeSumDist = 5 };
 
 __host__ __device__ constexpr bool peer_mode(int m) { return m == kModePeers || m == kModePeers2; }
 __host__ __device__ constexpr int peer_slots(int m) { return m == kModePeers2 ? 2 : kMaxPeers; }
@@ -963,6 +965,7 @@ struct K1Src {
   const float* z;
   const float* v;
   const float* peer[kMaxPeers];
+  long long bl[kMaxPeers];  // kModeSumDist: slice starts relative to this source's base
   int np;
 };
 
@@ -975,10 +978,14 @@ __device__ __forceinline__ K1Src k1_src(const CandArgs& p, long long base) {
   K1Src s;
   s.a = s.b = nullptr;
   s.np = 0;
-  if (peer_mode(MODE)) {
+  if (peer_mode(MODE) || MODE == kModeSumDist) {
     s.np = p.peers.n;
 #pragma unroll
     for (int j = 0; j < kMaxPeers; ++j) s.peer[j] = j < s.np ? p.peers.p[j] + base : nullptr;
+    if (MODE == kModeSumDist) {
+#pragma unroll
+      for (int j = 0; j < kMaxPeers; ++j) s.bl[j] = j < s.np ? p.sbound[j] - base : (1LL << 62);
+    }
   } else {
     s.a = (MODE == kModeThetaU ? p.theta : p.s) + base;
     s.b = MODE == kModeThetaU ? (s_k1_alt ? p.u_alt : p.u) + base : nullptr;
@@ -1016,6 +1023,14 @@ __device__ __forceinline__ void k1_issue(float4* ring, int d, const K1Src& s, lo
 #pragma unroll
     for (int j = 0; j < peer_slots(MODE); ++j)
       if (j < s.np) cpp(j, s.peer[j]);
+  } else if (MODE == kModeSumDist) {
+    // the slice owner of this quad (slice bounds are multiples of 32 elements and
+    // layers start 32-aligned, so a quad never straddles two slices)
+    int o = 0;
+#pragma unroll
+    for (int j = 1; j < kMaxPeers; ++j) o += e >= s.bl[j] ? 1 : 0;
+    const float* src = o == 0 ? s.peer[0] : o == 1 ? s.peer[1] : o == 2 ? s.peer[2] : s.peer[3];
+    cpp(0, src);
   } else {
     cp(0, s.a);
     if (MODE == kModeThetaU) cp(1, s.b);
@@ -1072,6 +1087,10 @@ __device__ __forceinline__ double cand_elem(const CandArgs& p, long long gi, con
     for (int j = 1; j < p.peers.n; ++j) s = __dadd_rn(s, (double)p.peers.p[j][gi]);
   } else if (MODE == kModeThetaU) {
     s = __dadd_rn((double)p.theta[gi], (double)(s_k1_alt ? p.u_alt : p.u)[gi]);
+  } else if (MODE == kModeSumDist) {
+    int o = 0;
+    for (int j = 1; j < p.peers.n; ++j) o += gi >= p.sbound[j] ? 1 : 0;
+    s = (double)p.peers.p[o][gi];
   } else {
     s = (double)p.s[gi];
   }
@@ -1548,7 +1567,9 @@ void launch_candidate(const CandArgs& a, int n_items, int frozen, size_t smem, c
     const char* v = std::getenv("HSX_K1_PEERS2");
     return v ? std::atoi(v) : 0;  // over NVLink the theta + u kernel measured 3% slower (r2y): opt-in (=2)
   }();
-  if (a.peers.n == 2 && peers2 == 2) {
+  if (a.sdist) {
+    launch_candidate_mode<kModeSumDist>(a, n_items, frozen, smem, st);
+  } else if (a.peers.n == 2 && peers2 == 2) {
     CandArgs b = a;
     b.theta = a.peers.p[0];
     b.u = a.peers.p[1];

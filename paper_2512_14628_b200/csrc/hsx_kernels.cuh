@@ -143,6 +143,10 @@ struct CandArgs {
   float* zn_peer;
   double* partials_peer;
   unsigned int* k1done_peer;
+  // distributed sum (P > 2, hsx_candidate_dist): S lives in the P ranks' reduce-scatter
+  // slices, peers.p[j] = rank j's slice buffer (valid on [sbound[j], sbound[j + 1]))
+  long long sbound[kMaxPeers];
+  int sdist;
   // staged peer operand (two ranks): u is a local copy of the peer's send that a
   // staging kernel fills item by item on a side stream; sready[item] == epoch + 1
   // once the item's region landed, else K1 reads u_alt (the peer's send) directly

@@ -224,6 +224,15 @@ class Plan:
                       ptr(frozen_mask), current_stream())
         del keep
 
+    def candidate_dist(self, slices: list[int], z, v, z_node, frozen_mask=None):
+        """K1 reading the intra sum from the P ranks' reduce-scatter slices over NVLink
+        (hsx_candidate_dist; replaces the all-gather of S and the local K1 on it)."""
+        arr, keep = _lib.ptr_array(slices)
+        with timed("K1_candidate"):
+            _lib.call("hsx_candidate_dist", self._h, arr, len(slices), ptr(z), ptr(v), ptr(z_node),
+                      ptr(frozen_mask), current_stream())
+        del keep
+
     def split_sizes(self) -> tuple[int, int]:
         """(partials doubles, tile counters) of a split two-rank K1 (hsx_plan_split_sizes)."""
         import ctypes as C

@@ -61,6 +61,9 @@ _ONESIDED = os.environ.get("HSX_ONESIDED") == "1"
 # bits over NVLink, for leaders and followers alike (HSX_FUSED_UNION=0: K4, then the
 # followers copy their leader's union, then K5)
 _FUSED_UNION = os.environ.get("HSX_FUSED_UNION", "1") != "0"
+# P > 2 peer steps: K1 reads the intra sum from the reduce-scatter slices over NVLink
+# instead of all-gathering S first (HSX_DIST_SUM=0: all-gather, then K1 on S)
+_DIST_SUM = os.environ.get("HSX_DIST_SUM", "1") != "0"
 
 
 class HSADMMSync:
@@ -402,9 +405,14 @@ class HSADMMSync:
             me = self.intra.members.index(self.rank)
             pl.slices_peers(send.peer_ptrs(), me, 1.0, False, self.p_ssum.tensor, "K8_intra_rs")
             yield Barrier(self.intra, "theta_u_ag", k)
-            pl.slices_peers(self.p_ssum.peer_ptrs(), -1, 1.0, False, self.sum, "K8_intra_ag")
-            s_local = self.sum
-            pl.candidate(s_local, None, None, self.z, self.v, self.z_node, frozen_mask=fmask)
+            if _DIST_SUM and pl.max_passes == 1:
+                # K1 reads each quad of S from its slice owner over NVLink: no
+                # all-gather of S (composite plans keep S for their renorm passes)
+                pl.candidate_dist(self.p_ssum.peer_ptrs(), self.z, self.v, self.z_node, frozen_mask=fmask)
+            else:
+                pl.slices_peers(self.p_ssum.peer_ptrs(), -1, 1.0, False, self.sum, "K8_intra_ag")
+                s_local = self.sum
+                pl.candidate(s_local, None, None, self.z, self.v, self.z_node, frozen_mask=fmask)
         elif self.P == 2:
             # the intra sum fused into K1: theta+u of both ranks read over NVLink
             self._pack_send(send.tensor)

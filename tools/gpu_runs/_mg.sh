@@ -1,4 +1,4 @@
-# usage: bash tools/_mg.sh N "groupings for mp_parity" "models"
+# usage: bash tools/gpu_runs/_mg.sh N "groupings for mp_parity" "models"
 N=$1; GROUPS_=$2; MODELS=$3
 make -s || exit 1
 mkdir -p gpurun_out

@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of bench.py under env settings: tools/ab_bench.sh "NAME=ENV ..." ...
+# A/B of bench.py under env settings: tools/gpu_runs/ab_bench.sh "NAME=ENV ..." ...
 # prints ms/step, frozen ms/step and per-kernel us for each setting
 for cfg in "$@"; do
   env $cfg python bench.py --no-cpu-baseline --steps ${AB_STEPS:-40} > gpurun_out/ab.json 2>/dev/null

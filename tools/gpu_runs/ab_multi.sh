@@ -1,5 +1,5 @@
 #!/bin/bash
-# tools/ab_multi.sh N TRANSPORT "ENV=.." ...: multi-rank bench per env setting (peer/nccl)
+# tools/gpu_runs/ab_multi.sh N TRANSPORT "ENV=.." ...: multi-rank bench per env setting (peer/nccl)
 N=$1; TR=$2; shift; shift
 port=29700
 for cfg in "$@"; do

@@ -1,5 +1,5 @@
 #!/bin/bash
-# usage: tools/bench_models.sh N GROUPING MODEL [transport=peer] -> gpurun_out/bench{N}_{MODEL}_{GROUPING}_{transport}.json
+# usage: tools/gpu_runs/bench_models.sh N GROUPING MODEL [transport=peer] -> gpurun_out/bench{N}_{MODEL}_{GROUPING}_{transport}.json
 N=$1; G=$2; M=$3; TR=${4:-peer}
 port=$((29700 + RANDOM % 200))
 out=gpurun_out/bench${N}_${M}_${G}_${TR}.json

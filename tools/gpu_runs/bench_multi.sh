@@ -1,5 +1,5 @@
 #!/bin/bash
-# usage: tools/bench_multi.sh N [grouping] [extra bench args...]  -> gpurun_out/bench{N}_{grouping}_{transport}.json
+# usage: tools/gpu_runs/bench_multi.sh N [grouping] [extra bench args...]  -> gpurun_out/bench{N}_{grouping}_{transport}.json
 N=$1; G=${2:-default}; shift; shift
 port=29600
 for tr in nccl peer; do

@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU pass: gpu tests, smoke, bench (N=1), ncu launch list, ncu full capture of the
-# dominant kernels. Usage (under gpurun): bash tools/gpu_round.sh TAG [skip_tests]
+# dominant kernels. Usage (under gpurun): bash tools/gpu_runs/gpu_round.sh TAG [skip_tests]
 TAG=${1:-r1}
 mkdir -p gpurun_out
 make -s || exit 1

@@ -9,6 +9,6 @@ run2() { tag=$1; shift; env "$@" timeout 600 python -m torch.distributed.run --n
 run2 rn50
 run2 rn50_k67 HSX_K67_CHAIN=1
 HSX_K67_CHAIN=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29712 tests/mp_parity.py 1x2 > gpurun_out/r2r_mp_1x2.log 2>&1; echo rc=$? >> gpurun_out/r2r_mp_1x2.log
-bash tools/sparsity_sweep2.sh rn50_224 nccl > gpurun_out/sweep2_nccl.txt 2>&1
-bash tools/sparsity_sweep2.sh rn50_224 peer > gpurun_out/sweep2_peer.txt 2>&1
+bash tools/gpu_runs/sparsity_sweep2.sh rn50_224 nccl > gpurun_out/sweep2_nccl.txt 2>&1
+bash tools/gpu_runs/sparsity_sweep2.sh rn50_224 peer > gpurun_out/sweep2_peer.txt 2>&1
 tail -n 2 gpurun_out/r2r_gputest.txt gpurun_out/r2r_mp_1x2.log

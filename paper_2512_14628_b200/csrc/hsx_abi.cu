@@ -671,6 +671,9 @@ static void arm_chain(hsx_plan* p, hsx::CandArgs& a, cudaStream_t st) {
   if (p->k2_pending) cudaMemsetAsync(p->d_k1done, 0, sizeof(unsigned) * p->prunable.size(), st);
   p->k2_pending = 1;
   a.k1done = p->d_k1done;
+  // cross-tile prologue: parity green, measured neutral (r2zt), so opt-in
+  static const int xtile = env_flag("HSX_K1_XTILE", 0);
+  a.xtile = xtile;
   a.reserve = reserve >= 0 ? reserve : (int)p->sel_list[0].size();  // < 0: one per selection CTA
   p->k2_armed = 1;
 }

@@ -1161,9 +1161,36 @@ __device__ void cand_elementwise(const CandArgs& p, const DevLayer& ly, long lon
 // one fp64 partial per group: partials[part][G].
 constexpr int kTileQuads = 64;
 
+// a quad tile of pass p.pass whose fold does not use the ring (no fused selection):
+// the next such tile's first ring stages may go in flight under this tile's fold
+__device__ __forceinline__ bool xtile_ok(const CandArgs& p, const Item& it) {
+  const DevLayer& ly = p.layers[it.layer];
+  return ly.ncons > p.pass && ly.tiling == 1 && !((ly.fsel >> p.pass) & 1);
+}
+
+// the first D-1 ring stages of quad tile `it` (this thread's share)
 template <int MODE>
+__device__ __forceinline__ void tile_quads_prologue(const CandArgs& p, const Item& it, float4* ring) {
+  const DevLayer& ly = p.layers[it.layer];
+  const int W = ly.cw, RP = kThreads / W, L = ly.L, cq = ly.cq;
+  const int jj = threadIdx.x & (W - 1);
+  const int j = it.chunk * cq + jj;
+  const long long r0 = it.begin + threadIdx.x / W;
+  const int count = (jj < cq && j < (L >> 2) && r0 < it.end) ? (int)((it.end - r0 + RP - 1) / RP) : 0;
+  const K1Src src = k1_src<MODE>(p, ly.off + 4 * j);
+  const long long stride = (long long)RP * L;
+  const unsigned long long pf = l2pol(kL2First);
+  ring_prologue<K1<MODE>::D>(
+      count, [&](int d, int i) { k1_issue<MODE, true>(ring, d, src, r0 * L + i * stride, 0, pf); });
+}
+
+// xnext != nullptr (cross-tile mode): the prologue of this tile was issued by the
+// previous one iff *pre; once this tile's loads are consumed, thread 0 claims the
+// CTA's next item (claim()), and if it is a quad tile its first stages are issued
+// before the fold; *xnext = the claimed index, *pre = whether they were issued.
+template <int MODE, class Claim>
 __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Item& it, float4* ring,
-                                double* cs) {
+                                double* cs, bool* pre, int* xnext, Claim claim) {
   const int W = ly.cw;          // lanes per row (power of two)
   const int RP = kThreads / W;  // row phases
   const int pass = p.pass;
@@ -1183,9 +1210,10 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
   const long long stride = (long long)RP * L;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   const unsigned long long pf = l2pol(kL2First), pl = l2pol(kL2Last);
-  ring_run<K1<MODE>::D>(
-      count,
-      [&](int d, int i) { k1_issue<MODE, true>(ring, d, src, r0 * L + i * stride, 0, pf); },
+  auto issue = [&](int d, int i) { k1_issue<MODE, true>(ring, d, src, r0 * L + i * stride, 0, pf); };
+  if (!(xnext && *pre)) ring_prologue<K1<MODE>::D>(count, issue);
+  ring_loop<K1<MODE>::D>(
+      count, issue,
       [&](int d, int i) {
         const long long e = r0 * L + i * stride;
         double c[4];
@@ -1205,8 +1233,18 @@ __device__ void cand_tile_quads(const CandArgs& p, const DevLayer& ly, const Ite
         a2 = __dadd_rn(a2, __dmul_rn(c[2], c[2]));
         a3 = __dadd_rn(a3, __dmul_rn(c[3], c[3]));
       });
+  if (xnext) {
+    __shared__ int s_claim;
+    __syncthreads();
+    if (threadIdx.x == 0) s_claim = claim();
+    __syncthreads();
+    const int nx = s_claim;
+    *xnext = nx;
+    *pre = nx < p.n_items && xtile_ok(p, p.items[nx]);
+    if (*pre) tile_quads_prologue<MODE>(p, p.items[nx], ring);  // in flight under the fold
+  }
   double* mine = cs + ph * (4 * W) + 4 * jj;
-  __syncthreads();  // cs aliases the ring: every thread is done with its last stage
+  __syncthreads();  // (without xnext) cs aliases the ring: every thread is done with its last stage
   mine[0] = a0; mine[1] = a1; mine[2] = a2; mine[3] = a3;
   __syncthreads();
   const int col0 = it.chunk * 4 * cq;
@@ -1322,8 +1360,9 @@ __device__ __forceinline__ unsigned smid() {
   } while (0)
 #endif
 
-template <int MODE>
-__device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const Item& it, float4* ring) {
+template <int MODE, class Claim>
+__device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const Item& it, float4* ring,
+                                          double* xcs, bool* pre, int* xnext, Claim claim) {
   const DevLayer& ly = p.layers[it.layer];
   if (frozen || ly.ncons == 0) {
     if (p.pass > 0) return;
@@ -1342,7 +1381,7 @@ __device__ __forceinline__ void cand_item(const CandArgs& p, int frozen, const I
   }
   if (ly.ncons <= p.pass) return;
   if (ly.tiling == 1)
-    cand_tile_quads<MODE>(p, ly, it, ring, reinterpret_cast<double*>(ring));
+    cand_tile_quads<MODE>(p, ly, it, ring, xnext ? xcs : reinterpret_cast<double*>(ring), pre, xnext, claim);
   else
     cand_tile_rows<MODE>(p, ly, it, reinterpret_cast<double*>(ring));
 #ifdef HSX_TRACE
@@ -1393,6 +1432,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
   __shared__ int next;
   int idx = blockIdx.x;
   unsigned epoch = 0;
+  // cross-tile pipelining (dynamic launches, persistent grid, no staging)
+  const bool single = gridDim.x >= (unsigned)p.n_items;
+  const bool xt = p.xtile && !frozen && !p.sready && !single;
+  // fold scratch in cross-tile mode: the ring's last stage (D-1), which the next tile's
+  // prologue (stages 0 .. D-2) leaves free until the fold is done (8 KB <= one stage)
+  double* xcs = reinterpret_cast<double*>(ring + (K1<MODE>::D - 1) * K1<MODE>::NB * kThreads);
+  bool pre = false;
+  unsigned int* const sched = p.sched;  // (captured by value: a reference to the kernel
+                                         // parameter would force a local copy of it)
+  auto claim = [sched]() -> int { return (int)gridDim.x + (int)atomicAdd(sched, 1u); };
   if (threadIdx.x == 0) {
     s_k1_alt = 0;
     if (p.sready) epoch = *reinterpret_cast<volatile unsigned*>(p.sepoch);  // bumped only by the last CTA
@@ -1424,7 +1473,25 @@ __global__ void __launch_bounds__(kThreads, 3) k_candidate(CandArgs p, int froze
       }
       __syncthreads();
     }
-    cand_item<MODE>(p, frozen, p.items[idx], ring);
+    // cross-tile (xt): a quad tile claims the next item itself and may have issued
+    // its first stages already (pre); other items claim below
+    int nx = -1;
+    cand_item<MODE>(p, frozen, p.items[idx], ring, xcs, &pre, xt ? &nx : nullptr, claim);
+    if (xt) {
+      if (nx < 0) {
+        pre = false;
+        __syncthreads();
+        if (threadIdx.x == 0) next = claim();
+        __syncthreads();
+        nx = next;
+      }
+#ifdef HSX_TRACE
+      TRACE_AT(idx, 2, gtime());
+#endif
+      __syncthreads();  // fold scratch / row flags reused by the next item
+      idx = nx;
+      continue;
+    }
 #ifdef HSX_TRACE
     TRACE_AT(idx, 2, gtime());
 #endif

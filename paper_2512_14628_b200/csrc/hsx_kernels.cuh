@@ -147,6 +147,10 @@ struct CandArgs {
   // slices, peers.p[j] = rank j's slice buffer (valid on [sbound[j], sbound[j + 1]))
   long long sbound[kMaxPeers];
   int sdist;
+  // cross-tile pipelining (hsx: HSX_K1_XTILE): a persistent CTA claims its next item
+  // when a quad tile's loads are consumed and puts the next quad tile's first ring
+  // stages in flight before the tile's fold; the fold then uses the ring's last stage
+  int xtile;
   // staged peer operand (two ranks): u is a local copy of the peer's send that a
   // staging kernel fills item by item on a side stream; sready[item] == epoch + 1
   // once the item's region landed, else K1 reads u_alt (the peer's send) directly

@@ -107,3 +107,30 @@ def test_run_hierarchical_signature_matches_reference(ref):
 
         assert ([f.name for f in dataclasses.fields(getattr(H, cls))]
                 == [f.name for f in dataclasses.fields(getattr(RC, cls))]), cls
+
+
+def test_rooted_barrier_and_rank_concurrency_flags():
+    """A one-sided (rooted) barrier is an ordinary rendezvous under the in-process
+    scheduler; only a cluster whose ranks run concurrently (one process per GPU)
+    may take the split two-rank K1, whose selection waits for the peer's kernel."""
+    import paper_2512_14628_b200 as H
+    from paper_2512_14628_b200.transport import Barrier, DistCluster
+
+    c = H.LocalCluster(H.Topology(2, 2))
+    order = []
+
+    def prog(rank):
+        g = c.intra_group(rank // 2)
+        order.append(("before", rank))
+        yield Barrier(g, "zhat_bcast", 1, root=g.members[0])
+        order.append(("after", rank))
+        return rank
+
+    res = c.run({r: prog(r) for r in range(4)})
+    assert res == {r: r for r in range(4)}
+    # nobody passes the barrier before every member of its group reached it
+    for r in range(4):
+        mates = [m for m in range(4) if m // 2 == r // 2]
+        assert all(order.index(("before", m)) < order.index(("after", r)) for m in mates)
+    assert Barrier(c.intra_group(0), "m_bcast", 1).root is None
+    assert H.LocalCluster.concurrent_ranks is False and DistCluster.concurrent_ranks is True

@@ -1774,6 +1774,20 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
     // (L % 32 == 0), its row flag at s_rk[ph + 4 i]: walked by running pointers
     const long long e0 = tc.r0 * ly.L + 4 * (valid ? tc.j : 0), estep = (long long)kRowPhases * ly.L;
     const int mstep = kRowPhases * (ly.L >> 5);
+    const float* ls = zn + ly.off + e0;    // next quad to load
+    const unsigned ring0 = smem_u32(ring_slot<1>(ring, 0, 0));
+    if (!TMA) {
+      // the first kDepth-1 quads go in flight before the keep flags are gathered (a
+      // chain of dependent flag loads): read whatever is kept
+#pragma unroll
+      for (int d = 0; d < kDepth - 1; ++d) {
+        if (d < count)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring0 + d * kThreads * 16), "l"(ls)
+                       : "memory");
+        cp_commit();
+        ls += estep;
+      }
+    }
     // kept = AND over the passes' group flags: rows (FILTER) in shared memory,
     // this thread's four columns (CHANNEL / SHAPE) in a nibble
     for (int r = threadIdx.x; r < nrow; r += kThreads) {
@@ -1868,11 +1882,10 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
       return;
     }
     __syncthreads();
-    // a quad with nothing kept is not read (the copy zero-fills it without touching
-    // memory): only the kept quads' z_node is needed for the nonzero test
-    const float* ls = zn + ly.off + e0;    // next quad to load
-    const uint8_t* lrk = s_rk + tc.ph;     // its row flag
-    const unsigned ring0 = smem_u32(ring_slot<1>(ring, 0, 0));
+    // from stage kDepth-1 on a quad with nothing kept is not read (the copy zero-fills
+    // it without touching memory): only the kept quads' z_node is needed for the
+    // nonzero test
+    const uint8_t* lrk = s_rk + tc.ph + kRowPhases * (kDepth - 1);  // row flag of the next quad to load
     auto issue = [&](int d, int) {
       const bool any = ckb && *lrk;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(ring0 + d * kThreads * 16), "l"(ls),
@@ -1881,7 +1894,6 @@ __device__ __forceinline__ void project_item(const KeepArgs& a, float* __restric
       ls += estep;
       lrk += kRowPhases;
     };
-    ring_prologue(count, issue);
     unsigned bad = 0;  // CHECK: kept but zero
     float* qc = zn + ly.off + e0;          // quad being consumed
     uint32_t* mc = mask + ly.mword + (e0 >> 5);
